@@ -1,0 +1,437 @@
+#!/usr/bin/env python3
+"""ERX hot-path benchmark (driver contract: one JSON line from rank 0).
+
+Workload (default): BASELINE.json configs[3] — 64 independent scan streams,
+P=640 pixels x B=108 bands, alpha=0.1, full covariance (D = B, no_srp),
+streams sharded evenly over the ranks (no data-path collective).  One step =
+one window of T lines of every local stream through the five-kernel
+pipeline (stats -> scan -> factor -> score -> normalize) on inputs already
+resident in HBM.  Lines come from the BASELINE generator and are replayed
+from a device pool at least 2x the L2 size, so no step reads inputs left in
+L2 by the previous one.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config 3] [--mode full|srp] [--window T]
+
+`--impl reference` times the fp64 CPU restatement of the reference path
+(oracle/, "port": the reference ships declarations only) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    0: dict(streams=1, pixels=384, bands=108, alpha=0.1, lines=2000),
+    1: dict(streams=1, pixels=640, bands=224, alpha=0.05, lines=10000),
+    2: dict(streams=1, pixels=1024, bands=10, alpha=0.1, lines=20000),
+    3: dict(streams=64, pixels=640, bands=108, alpha=0.1, lines=5000),
+    4: dict(streams=4, pixels=1280, bands=448, alpha=0.05, lines=3000),
+}
+L2_BYTES = 126 * 1024 * 1024
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.rows = []
+        if self.proc is None:
+            return False
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            out = ""
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+        return False
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def algorithmic(cfgd, D, srp_nnz=0):
+    """Per-line algorithmic work: bytes read/written and flops per kernel."""
+    P, B = cfgd["pixels"], cfgd["bands"]
+    tri = D * (D + 1)  # 2 * D(D+1)/2 (flops of a symmetric rank-1 update / a triangular matvec per pixel)
+    proj = 2 * P * srp_nnz
+    return {
+        "bytes_line": 4 * P * B + 8 * P,
+        "flops_line": 2 * P * D * D + D ** 3 / 3 + proj,
+        "stats": dict(flops=P * tri + proj, bytes=4 * P * B),
+        "score": dict(flops=P * tri + proj, bytes=4 * P * B + 4 * P),
+        "factor": dict(flops=2 * D ** 3 / 3, bytes=0),
+        "scan": dict(flops=0, bytes=0),
+        "normalize": dict(flops=0, bytes=8 * P),
+    }
+
+
+def build_pool(pkg, cid, streams, lines_per_stream, threads=0):
+    """[S][L][P][B] fp32 host pool from the BASELINE generator."""
+    out = []
+    for s in streams:
+        x, _ = pkg.gen_lines(pkg.gen_spec(cid, s), 0, lines_per_stream, threads=threads, want_mask=False)
+        out.append(x)
+    return np.stack(out)
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2408_14947_b200 as pkg
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    cid = args.config
+    cfgd = CONFIGS[cid]
+    S_tot = cfgd["streams"]
+    if S_tot % world:
+        raise SystemExit(f"{S_tot} streams do not shard over {world} ranks")
+    S = S_tot // world
+    my_streams = list(range(rank * S, (rank + 1) * S))
+    P, B = cfgd["pixels"], cfgd["bands"]
+    no_srp = args.mode == "full"
+    cfg = pkg.ErxConfig(no_srp=no_srp, alpha=cfgd["alpha"])
+    T = args.window
+    line_bytes = P * B * 4
+    n_win = max(2, math.ceil(2 * L2_BYTES / (S * T * line_bytes)))
+    pool_lines = n_win * T
+    t0 = time.time()
+    host = build_pool(pkg, cid, my_streams, pool_lines)
+    gen_s = time.time() - t0
+    dev = torch.from_numpy(host).to(f"cuda:{local}")
+    # windows laid out [win][S][T][P][B] so each step reads one contiguous block
+    dev = dev.view(S, n_win, T, P, B).permute(1, 0, 2, 3, 4).contiguous()
+    raw = torch.empty((S, T, P), dtype=torch.float32, device=f"cuda:{local}")
+    norm = torch.empty_like(raw)
+    eng = pkg.Engine(cfg, B, n_streams=S, window_lines=T, device=local)
+    D = eng.dims
+
+    def step(k):
+        w = k % n_win
+        eng.run_device(dev[w].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr(), first_index=k * T)
+
+    for k in range(args.warmup):
+        step(k)
+    eng.sync()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches0 = eng.launch_count()
+    with ClockSampler(local) as clk:
+        eng.event_record(0)
+        for k in range(args.steps):
+            step(args.warmup + k)
+        eng.event_record(1)
+        ms = eng.event_elapsed_ms(0, 1)
+    eng.sync()
+    launches = eng.launch_count() - launches0
+    torch.cuda.synchronize()
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    if dist:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    lines_total = S_tot * T * args.steps
+    value = lines_total / (ms_max / 1e3)
+
+    # per-kernel device time (CUDA events on the engine stream), separate pass
+    eng.set_profiling(True)
+    prof_steps = max(3, min(args.steps, 10))
+    for k in range(prof_steps):
+        step(k)
+    eng.sync()
+    kt = eng.kernel_times()
+    eng.set_profiling(False)
+    alg = algorithmic(cfgd, D)
+    total_k = sum(v[0] for v in kt.values()) or 1.0
+    kernels = {}
+    for name, (kms, cnt) in kt.items():
+        per = kms / max(cnt, 1)
+        lines_per_launch = S * T
+        a = alg[name]
+        kernels[name] = {"ms_per_launch": per, "share": kms / total_k, "launches": cnt,
+                         "tflops": a["flops"] * lines_per_launch / (per * 1e-3) / 1e12 if per > 0 else None,
+                         "gbs": a["bytes"] * lines_per_launch / (per * 1e-3) / 1e9 if per > 0 else None}
+    dom = max(kernels, key=lambda k: kernels[k]["share"])
+    fp32_peak = eng.probe_fp32_tflops()
+    pk = peaks()
+    dk = kernels[dom]
+    if alg[dom]["flops"] > 0 and dom in ("stats", "score") and no_srp:
+        roof = {"bound": "fp32", "kernel": dom, "achieved": dk["tflops"], "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": dk["tflops"] / fp32_peak, "traffic": None,
+                "peak_source": "measured FFMA probe (erx_probe_fp32_tflops) on this GPU in this run",
+                "algorithmic": f"{alg[dom]['flops']:.4g} flop/line x {S*T} lines/launch"}
+    elif alg[dom]["flops"] > 0 and dom == "factor":
+        roof = {"bound": "fp64", "kernel": dom, "achieved": dk["tflops"], "peak": fp32_peak / 2, "unit": "TFLOP/s",
+                "frac": dk["tflops"] / (fp32_peak / 2), "traffic": None,
+                "peak_source": "half the measured FFMA probe (B200 FP64:FP32 = 1:2)",
+                "algorithmic": f"{alg[dom]['flops']:.4g} flop/line x {S*T} lines/launch"}
+    else:
+        roof = {"bound": "hbm", "kernel": dom, "achieved": dk["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": dk["gbs"] / pk["hbm_gbs"] if dk["gbs"] else None, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "algorithmic": f"{alg[dom]['bytes']} B/line x {S*T} lines/launch"}
+    # whole-pipeline roofline per the north star: slower of flops@peak and bytes@HBM per line
+    t_flop = alg["flops_line"] / (fp32_peak * 1e12)
+    t_byte = alg["bytes_line"] / (pk["hbm_gbs"] * 1e9)
+    roof_lines = 1.0 / max(t_flop, t_byte)
+    roofline_line = {"lines_per_s_roofline_per_gpu": roof_lines, "bound": "fp32" if t_flop > t_byte else "hbm",
+                     "frac": (value / world) / roof_lines}
+
+    # end-to-end through the public C ABI with HOST buffers (pinned), H2D + D2H inside the timed region
+    e2e = None
+    try:
+        e2e_steps = max(2, min(args.steps, 8))
+        eng2 = pkg.Engine(cfg, B, n_streams=S, window_lines=T, device=local)
+        pin = torch.from_numpy(np.ascontiguousarray(host[:, :T])).pin_memory().numpy()
+        for k in range(2):
+            eng2.push(pin, k * T)
+            eng2.pop()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for k in range(e2e_steps):
+            eng2.push(pin, (k + 2) * T)
+            _, _, r_, n_ = eng2.pop()
+        el = time.perf_counter() - t0
+        el_t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{local}")
+        if dist:
+            dist.all_reduce(el_t, op=dist.ReduceOp.MAX)
+        e2e = {"value": S_tot * T * e2e_steps / float(el_t.item()), "unit": "lines/s",
+               "h2d_bytes_per_step": S * T * P * B * 4, "d2h_bytes_per_step": S * T * (P * 4 * 2 + 4),
+               "path": "erx_push_host (pinned) -> 5 kernels -> erx_pop (fp64 ScoredLine payload)"}
+        eng2.close()
+    except Exception as ex:  # report, never hide
+        e2e = {"error": repr(ex)}
+
+    extra = {}
+    if world == 1 and not args.quick:
+        extra = secondary_measurements(pkg, args)
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cid, no_srp, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": "lines/sec (batched independent streams, aggregate over GPUs)",
+            "value": value, "unit": "lines/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 (FFMA stats/whitening) + f64 (scan, Cholesky, inverse)",
+            "data": "synthetic: BASELINE.json configs[3] generator (include/erx_datagen.h), device pool >= 2x L2 replayed",
+            "config": {"workload": f"configs[{cid}]", "streams": S_tot, "streams_per_gpu": S, "pixels": P,
+                       "bands": B, "dims": D, "mode": "D=B (no_srp)" if no_srp else "d=5 SRP",
+                       "alpha": cfgd["alpha"], "window_lines": T, "pool_lines_per_stream": pool_lines,
+                       "l2": "inputs larger than L2: device pool >= 2x L2, one window per step"},
+            "pixel_bands_per_s": value * P * B,
+            "roofline": roof, "roofline_line": roofline_line, "kernels": kernels,
+            "e2e": e2e, "clocks": clk.summary(), "gpu_launches": int(launches),
+            "cpu_baseline": cpu, "gen_seconds": gen_s,
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def secondary_measurements(pkg, args):
+    """Single-stream numbers named by the metric (1 GPU): configs[1] throughput and
+    configs[0] lag-0 per-line latency (north-star target < 1 ms at 108 bands)."""
+    import torch
+
+    out = {}
+    try:
+        cfgd = CONFIGS[1]
+        P, B, T = cfgd["pixels"], cfgd["bands"], 64
+        for mode in ("full", "srp"):
+            n_win = max(2, math.ceil(2 * L2_BYTES / (T * P * B * 4)))
+            host = build_pool(pkg, 1, [0], n_win * T)
+            dev = torch.from_numpy(host[0]).cuda().view(n_win, T, P, B)
+            raw = torch.empty((T, P), dtype=torch.float32, device="cuda")
+            norm = torch.empty_like(raw)
+            eng = pkg.Engine(pkg.ErxConfig(no_srp=mode == "full", alpha=cfgd["alpha"]), B, 1, T)
+            for k in range(3):
+                eng.run_device(dev[k % n_win].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr())
+            eng.sync()
+            K = 20
+            eng.event_record(0)
+            for k in range(K):
+                eng.run_device(dev[k % n_win].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr())
+            eng.event_record(1)
+            ms = eng.event_elapsed_ms(0, 1)
+            eng.sync()
+            lps = K * T / (ms / 1e3)
+            out.setdefault("single_stream", {"workload": "configs[1]: 1 stream, 640 px x 224 bands, alpha=0.05",
+                                             "window_lines": T})[mode] = {
+                "lines_per_s": lps, "pixel_bands_per_s": lps * P * B}
+            eng.close()
+    except Exception as ex:
+        out["single_stream"] = {"error": repr(ex)}
+    try:
+        cfgd = CONFIGS[0]
+        P, B = cfgd["pixels"], cfgd["bands"]
+        host = build_pool(pkg, 0, [0], 64)
+        dev = torch.from_numpy(host[0]).cuda()
+        raw = torch.empty((1, P), dtype=torch.float32, device="cuda")
+        norm = torch.empty_like(raw)
+        lat = {}
+        for mode in ("full", "srp"):
+            eng = pkg.Engine(pkg.ErxConfig(no_srp=mode == "full"), B, 1, 1)
+            for k in range(5):
+                eng.run_device(dev[k].data_ptr(), 1, P, raw.data_ptr(), norm.data_ptr())
+            eng.sync()
+            K = 50
+            eng.event_record(0)
+            for k in range(K):
+                eng.run_device(dev[k % 64].data_ptr(), 1, P, raw.data_ptr(), norm.data_ptr())
+            eng.event_record(1)
+            ms = eng.event_elapsed_ms(0, 1)
+            eng.sync()
+            lat[mode] = {"ms_per_line": ms / K}
+            eng.close()
+        out["latency"] = {"workload": "configs[0]: 384 px x 108 bands, window=1 (no lag), device-resident", **lat}
+    except Exception as ex:
+        out["latency"] = {"error": repr(ex)}
+    return out
+
+
+def cpu_baseline(cid, no_srp, seconds=12.0, threads=None):
+    """fp64 oracle (port of the reference path) on a bounded sample of the same workload."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_ctypes as orc
+
+    import paper_2408_14947_b200 as pkg
+
+    cfgd = CONFIGS[cid]
+    cores = threads or os.cpu_count() or 1
+    S = min(cfgd["streams"], cores) if cfgd["streams"] > 1 else 1
+    use_threads = S
+    ocfg = orc.OracleConfig(no_srp=no_srp, alpha=cfgd["alpha"])
+    probe = build_pool(pkg, cid, [0], 3)
+    t0 = time.perf_counter()
+    orc.run_streams(ocfg, probe, threads=1, want_scores=False)
+    per_line = (time.perf_counter() - t0) / 3
+    n_lines = int(max(4, min(cfgd["lines"], seconds / max(per_line, 1e-6))))
+    pool = build_pool(pkg, cid, list(range(S)), n_lines)
+    t0 = time.perf_counter()
+    orc.run_streams(ocfg, pool, threads=use_threads, want_scores=False)
+    el = time.perf_counter() - t0
+    lps = S * n_lines / el
+    model = ""
+    try:
+        model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except Exception:
+        pass
+    return {"value": lps, "unit": "lines/s", "cores": use_threads, "kind": "port",
+            "sample": f"{S} stream(s) x {n_lines} lines of configs[{cid}] ({'D=B' if no_srp else 'd=5'}), "
+                      f"one stream per thread, {el:.1f} s wall", "cpu_model": model,
+            "pixel_bands_per_s": lps * cfgd["pixels"] * cfgd["bands"]}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cid = args.config
+    no_srp = args.mode == "full"
+    samples = []
+    cores = os.cpu_count() or 1
+    last = None
+    for k in range(args.warmup + args.steps):
+        r = cpu_baseline(cid, no_srp, seconds=args.cpu_seconds / max(1, args.steps + args.warmup) * 2, threads=cores)
+        if k >= args.warmup:
+            samples.append(r["value"])
+        last = r
+    value = float(np.mean(samples))
+    cfgd = CONFIGS[cid]
+    line = {
+        "impl": "reference", "metric": "lines/sec (batched independent streams, aggregate over GPUs)",
+        "value": value, "unit": "lines/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: BASELINE.json configs generator",
+        "config": {"workload": f"configs[{cid}]", "streams": cfgd["streams"], "pixels": cfgd["pixels"],
+                   "bands": cfgd["bands"], "mode": "D=B (no_srp)" if no_srp else "d=5 SRP"},
+        "cpu_baseline": {"value": value, "unit": "lines/s", "cores": last["cores"], "kind": "port",
+                         "sample": last["sample"]},
+        "e2e": {"value": value, "unit": "lines/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference ships headers only (no bodies, no Eigen); timed path is the fp64 C++ restatement "
+                "oracle/erx_oracle.cpp through its own C API",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3, choices=[0, 1, 2, 3, 4])
+    ap.add_argument("--mode", default="full", choices=["full", "srp"])
+    ap.add_argument("--window", type=int, default=8)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip the single-stream / latency side measurements")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,158 @@
+/*
+ * erx_b200.h — C ABI of the B200-native ERX engine (liberx_b200.so).
+ *
+ * This is the drop-in boundary for the reference's per-line detector
+ * (had::ErxDetector, proj/include/hadkit/erx.hpp:56-71, behind the
+ * had::LineDetector interface, detector.hpp:15-27).  Plain pointers and
+ * sizes only; no C++ or torch types cross it; no exception crosses it.
+ * Every entry point below names the reference declaration it replaces.
+ *
+ * Status codes are the reference's had::ErrorKind values (errors.hpp:12-18)
+ * so a wrapper can rethrow the same exception types:
+ *   ERX_OK 0, ERX_ERR_CONFIG 2 (ConfigError), ERX_ERR_DATA 3 (DataError),
+ *   ERX_ERR_NUMERIC 5 (FactorizationError, pivot via erx_last_pivot),
+ *   ERX_ERR_IO 6; plus ERX_ERR_DEVICE 16 for CUDA failures (no reference
+ *   analogue) and ERX_ERR_STATE 17 for calls on a failed engine.
+ *
+ * Threading (detector.hpp:11): one engine per consumer
+ * thread at a time; engines are independent and may run concurrently.
+ */
+#ifndef ERX_B200_H
+#define ERX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ERX_OK 0
+#define ERX_ERR_CONFIG 2
+#define ERX_ERR_DATA 3
+#define ERX_ERR_NUMERIC 5
+#define ERX_ERR_IO 6
+#define ERX_ERR_DEVICE 16
+#define ERX_ERR_STATE 17
+
+/* Mirrors had::ErxConfig (erx.hpp:14-24) field for field. */
+typedef struct {
+    int32_t dims;            /* projected dimensions d (default 5) */
+    double alpha;            /* EMA momentum in (0, 1] (default 0.1) */
+    uint32_t buffer_len;     /* lines flagged warmup (default 99) */
+    double epsilon;          /* Cholesky regularisation (default 1e-5) */
+    uint64_t seed;           /* SRP seed (default 0) */
+    int32_t no_srp;          /* identity projection, d = b */
+    int32_t use_incremental; /* equal-weight Welford statistics instead of EMAs */
+} erx_config;
+
+typedef struct erx_engine erx_engine;
+
+/* ErxConfig{} defaults (erx.hpp:15-21). */
+void erx_config_default(erx_config* cfg);
+
+/* ErxConfig::validate (erx.hpp:23) plus the d <= b rule. */
+int erx_config_validate(const erx_config* cfg, uint32_t bands, char* msg, size_t msg_len);
+
+/* generate_srp (projection.hpp:26): bands x dims, row-major, explicit zeros. */
+int erx_generate_srp(uint32_t bands, uint32_t dims, uint64_t seed, double* weights);
+
+/*
+ * Replaces ErxDetector::ErxDetector(cfg, bands) (erx.hpp:58).  n_streams > 1
+ * holds that many independent detector instances advanced in lock-step (the
+ * batched multi-stream path).  window_lines is the pipelining
+ * lag T permitted by detector.hpp:11-14: up to T lines per stream are scored
+ * in one device pass (T = 1: no lag).  device: CUDA ordinal.
+ */
+int erx_create(const erx_config* cfg, uint32_t bands, uint32_t n_streams, uint32_t window_lines, int device,
+               erx_engine** out, char* msg, size_t msg_len);
+void erx_destroy(erx_engine* e);
+
+/* Message / failing pivot of the last error (FactorizationError::pivot, errors.hpp:51-56). */
+const char* erx_last_error(const erx_engine* e);
+int erx_last_pivot(const erx_engine* e);
+
+int erx_dims(const erx_engine* e);
+uint32_t erx_streams(const erx_engine* e);
+uint32_t erx_window(const erx_engine* e);
+
+/*
+ * Replaces LineDetector::process (detector.hpp:19) for all streams at once:
+ * `lines` is HOST memory [n_streams][n_lines][pixels][bands] fp32 (the
+ * SpectralLine payload, cube.hpp:48-55), line i of every stream carrying the
+ * emission index first_index + i.  The data is copied before return.  Full
+ * windows are scored immediately; results queue for erx_pop.
+ */
+int erx_push_host(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t pixels, uint32_t bands,
+                  const float* lines);
+
+/* Replaces LineDetector::finish (detector.hpp:21): scores any partial window. */
+int erx_finish(erx_engine* e);
+
+/* Scored lines waiting per stream. */
+uint32_t erx_ready(const erx_engine* e);
+
+/*
+ * Pops up to max_lines scored lines of every stream, oldest first: the
+ * ScoredLine fields (cube.hpp:76-82).  index/warmup: [n]; raw/norm:
+ * [n_streams][n][pixels] fp64.  Any pointer may be NULL.  Returns the count
+ * popped (>= 0) or a negative status.
+ */
+int erx_pop(erx_engine* e, uint32_t max_lines, int64_t* index, uint8_t* warmup, double* raw, double* norm);
+
+/*
+ * Device-resident path (no host copies): scores n_lines (<= window) lines
+ * per stream already in HBM, d_lines [n_streams][n_lines][pixels][bands]
+ * fp32, writing d_raw / d_norm [n_streams][n_lines][pixels] fp32.
+ * Asynchronous on the engine's stream; numeric failures are latched on the
+ * device and reported by erx_sync.
+ */
+int erx_run_device(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t pixels, const float* d_lines,
+                   float* d_raw, float* d_norm);
+int erx_sync(erx_engine* e);
+void* erx_cuda_stream(erx_engine* e);
+
+/* ErxDetector::state() (erx.hpp:65, ErxState erx.hpp:27-34) for one stream. */
+int erx_get_state(erx_engine* e, uint32_t stream, double* mu, double* cov, int64_t* lines_seen,
+                  int64_t* welford_n, int* initialized);
+/* ErxState::weights (SrpMatrix, projection.hpp:15-24); bands x dims. */
+int erx_get_weights(const erx_engine* e, double* weights);
+/* Overwrites one stream's background (mu, cov row-major d x d, welford_n)
+ * and marks the engine initialised: the carry hand-off for a line-range split
+ * of one stream across devices. */
+int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double* cov, int64_t lines_seen,
+                  int64_t welford_n);
+
+/* ---- instrumentation (bench / profiling; not part of the reference API) ---- */
+#define ERX_KERNEL_STATS 0
+#define ERX_KERNEL_SCAN 1
+#define ERX_KERNEL_FACTOR 2
+#define ERX_KERNEL_SCORE 3
+#define ERX_KERNEL_NORMALIZE 4
+#define ERX_NUM_KERNELS 5
+uint64_t erx_launch_count(const erx_engine* e);
+/* When on, every kernel launch is bracketed by CUDA events on the engine stream. */
+int erx_set_profiling(erx_engine* e, int on);
+/* Per-kernel summed device ms and launch counts since profiling was enabled. */
+int erx_kernel_times(erx_engine* e, double* ms, uint64_t* launches);
+
+/* Measured FP32 FFMA throughput of the engine's device (TFLOP/s): the
+ * roofline denominator for the FFMA-bound kernels. */
+int erx_probe_fp32_tflops(erx_engine* e, double* tflops);
+
+/* CUDA events on the engine stream, for callers timing device work. */
+int erx_event_record(erx_engine* e, int slot);
+int erx_event_elapsed_ms(erx_engine* e, int slot_a, int slot_b, float* ms);
+
+/* Memory helpers so callers need no CUDA runtime of their own. */
+void* erx_host_alloc(size_t bytes);
+void erx_host_free(void* p);
+void* erx_device_alloc(int device, size_t bytes);
+void erx_device_free(void* p);
+int erx_copy(void* dst, const void* src, size_t bytes, int kind /* 1 h2d, 2 d2h, 3 d2d */, erx_engine* on_stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -263,7 +263,7 @@ int erx_process(Erx& e, int64_t index, uint32_t p, uint32_t b, const float* data
     if (first) {                                                         // erx.hpp:54-55
         e.mu = e.mhat;
         e.cov = e.khat;
-        e.welford_n = p;
+        if (e.cfg.use_incremental) e.welford_n = p;  // "incremental mode only" (erx.hpp:32)
         e.initialized = true;
     }
     // Cholesky of K + eps I with eps escalation x10 up to 1e-1 (§9.2).

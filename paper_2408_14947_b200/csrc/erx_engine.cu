@@ -1,0 +1,647 @@
+// erx_engine.cu — host runtime behind the C ABI (include/erx_b200.h).
+//
+// An engine owns S independent ERX streams (S = 1 is the drop-in
+// had::ErxDetector, erx.hpp:56-71) advanced in lock-step through windows of
+// up to T lines.  It owns one CUDA stream, the SRP weights, the device-side
+// background state (ping-pong buffers), the window workspaces and a pinned
+// host staging area for the drop-in (host pointer) path.  No CPU fallback:
+// every score is computed by the kernels in erx_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <string>
+#include <vector>
+
+#include "../../include/erx_b200.h"
+#include "erx_kernels.cuh"
+#include "host_rng.hpp"
+
+using erxk::Geometry;
+
+namespace {
+
+struct ScoredRow {
+    int64_t index;
+    uint8_t warmup;
+    std::vector<float> raw;   // [S][P]
+    std::vector<float> norm;  // [S][P]
+};
+
+struct Timing {
+    int kernel;
+    cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct erx_engine {
+    erx_config cfg{};
+    uint32_t B = 0, S = 1, T = 1;
+    int device = 0;
+    int D = 0, Dp = 0;
+    cudaStream_t stream = nullptr;
+
+    std::vector<double> W;  // B x D (SRP only)
+    int* d_srp_ptr = nullptr;
+    int* d_srp_band = nullptr;
+    float* d_srp_sign = nullptr;
+    double srp_scale = 1.0;
+
+    uint32_t P = 0;  // pixels (set by the first line)
+    Geometry geo{};
+    erxk::StatsLaunch sl{};
+
+    // device buffers, capacity S*T lines
+    float* d_lines = nullptr;
+    double* d_stats = nullptr;
+    double* d_prior = nullptr;
+    double* d_state[2] = {nullptr, nullptr};
+    int cur = 0;
+    double* d_work = nullptr;
+    float* d_white = nullptr;
+    float* d_raw = nullptr;
+    float* d_norm = nullptr;
+    int* d_status = nullptr;
+    int* d_latch = nullptr;
+
+    // pinned host staging (drop-in path)
+    float* h_lines = nullptr;
+    float* h_raw = nullptr;
+    float* h_norm = nullptr;
+    int* h_status = nullptr;
+
+    bool initialized = false;
+    int64_t lines_seen = 0;
+    int64_t welford_n = 0;
+    uint32_t fill = 0;
+    std::vector<int64_t> win_index;
+    std::deque<ScoredRow> queue;
+
+    std::string err;
+    int pivot = -1;
+    bool failed = false;
+
+    uint64_t launches = 0;
+    bool profiling = false;
+    std::vector<Timing> timings;
+    std::vector<cudaEvent_t> event_pool;
+    double kms[ERX_NUM_KERNELS] = {0, 0, 0, 0, 0};
+    uint64_t kcount[ERX_NUM_KERNELS] = {0, 0, 0, 0, 0};
+    cudaEvent_t user_ev[8] = {};
+};
+
+namespace {
+
+int fail(erx_engine* e, int code, const std::string& m) {
+    if (e) e->err = m;
+    return code;
+}
+
+#define CU(call)                                                                                 \
+    do {                                                                                         \
+        cudaError_t _r = (call);                                                                 \
+        if (_r != cudaSuccess)                                                                   \
+            return fail(e, ERX_ERR_DEVICE, std::string(#call) + ": " + cudaGetErrorString(_r)); \
+    } while (0)
+
+void put_msg(char* dst, size_t n, const std::string& s) {
+    if (dst && n) std::snprintf(dst, n, "%s", s.c_str());
+}
+
+int validate(const erx_config* c, uint32_t bands, std::string& m) {
+    // ErxConfig::validate (erx.hpp:23)
+    if (!(c->alpha > 0.0 && c->alpha <= 1.0)) { m = "alpha must be in (0, 1]"; return ERX_ERR_CONFIG; }
+    if (!(c->epsilon > 0.0)) { m = "epsilon must be > 0"; return ERX_ERR_CONFIG; }
+    if (bands < 1) { m = "bands must be >= 1"; return ERX_ERR_CONFIG; }
+    if (!c->no_srp) {
+        if (c->dims < 1) { m = "dims must be >= 1"; return ERX_ERR_CONFIG; }
+        if (uint32_t(c->dims) > bands) { m = "dims must be <= bands"; return ERX_ERR_CONFIG; }
+    }
+    const uint32_t d = c->no_srp ? bands : uint32_t(c->dims);
+    if (d > 512) { m = "projected dims > 512 are not supported"; return ERX_ERR_CONFIG; }
+    return ERX_OK;
+}
+
+cudaEvent_t take_event(erx_engine* e) {
+    if (!e->event_pool.empty()) {
+        cudaEvent_t ev = e->event_pool.back();
+        e->event_pool.pop_back();
+        return ev;
+    }
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    return ev;
+}
+
+template <typename F>
+void timed(erx_engine* e, int kernel, F&& launch) {
+    if (e->profiling) {
+        Timing t{kernel, take_event(e), take_event(e)};
+        cudaEventRecord(t.a, e->stream);
+        launch();
+        cudaEventRecord(t.b, e->stream);
+        e->timings.push_back(t);
+    } else {
+        launch();
+    }
+    e->launches += 1;
+}
+
+void collect_timings(erx_engine* e) {
+    for (auto& t : e->timings) {
+        cudaEventSynchronize(t.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t.a, t.b);
+        e->kms[t.kernel] += ms;
+        e->kcount[t.kernel] += 1;
+        e->event_pool.push_back(t.a);
+        e->event_pool.push_back(t.b);
+    }
+    e->timings.clear();
+}
+
+void free_window(erx_engine* e) {
+    cudaFree(e->d_lines);
+    cudaFree(e->d_stats);
+    cudaFree(e->d_prior);
+    cudaFree(e->d_work);
+    cudaFree(e->d_white);
+    cudaFree(e->d_raw);
+    cudaFree(e->d_norm);
+    cudaFree(e->d_status);
+    cudaFreeHost(e->h_lines);
+    cudaFreeHost(e->h_raw);
+    cudaFreeHost(e->h_norm);
+    cudaFreeHost(e->h_status);
+    e->d_lines = nullptr;
+    e->d_stats = e->d_prior = e->d_work = nullptr;
+    e->d_white = e->d_raw = e->d_norm = nullptr;
+    e->d_status = nullptr;
+    e->h_lines = e->h_raw = e->h_norm = nullptr;
+    e->h_status = nullptr;
+}
+
+// (Re)plan the geometry for P pixels and size the window buffers.
+int configure(erx_engine* e, uint32_t P) {
+    CU(cudaSetDevice(e->device));
+    if (P == e->P && e->d_stats) return ERX_OK;
+    CU(cudaStreamSynchronize(e->stream));
+    free_window(e);
+    e->P = P;
+    Geometry& g = e->geo;
+    g.P = int(P);
+    g.B = int(e->B);
+    g.D = e->D;
+    g.Dp = e->Dp;
+    g.nb = e->Dp / erxk::kBlk;
+    g.SE = e->D + e->D * (e->D + 1) / 2;
+    g.srp = e->cfg.no_srp ? 0 : 1;
+    g.srp_ptr = e->d_srp_ptr;
+    g.srp_band = e->d_srp_band;
+    g.srp_w = e->d_srp_sign;
+    g.srp_scale = e->srp_scale;
+    e->sl = erxk::plan_stats(g);
+    const size_t L = size_t(e->S) * e->T;
+    CU(cudaMalloc(&e->d_stats, L * g.SE * sizeof(double)));
+    CU(cudaMalloc(&e->d_prior, L * g.SE * sizeof(double)));
+    CU(cudaMalloc(&e->d_work, L * 2 * size_t(g.Dp) * g.Dp * sizeof(double)));
+    CU(cudaMalloc(&e->d_white, L * size_t(g.Dp) * g.Dp * sizeof(float)));
+    CU(cudaMalloc(&e->d_raw, L * P * sizeof(float)));
+    CU(cudaMalloc(&e->d_norm, L * P * sizeof(float)));
+    CU(cudaMalloc(&e->d_status, L * sizeof(int)));
+    return ERX_OK;
+}
+
+int ensure_host_staging(erx_engine* e) {
+    if (e->h_lines) return ERX_OK;
+    const size_t L = size_t(e->S) * e->T;
+    CU(cudaMalloc(&e->d_lines, L * e->P * e->B * sizeof(float)));
+    CU(cudaMallocHost(&e->h_lines, L * e->P * e->B * sizeof(float)));
+    CU(cudaMallocHost(&e->h_raw, L * e->P * sizeof(float)));
+    CU(cudaMallocHost(&e->h_norm, L * e->P * sizeof(float)));
+    CU(cudaMallocHost(&e->h_status, L * sizeof(int)));
+    return ERX_OK;
+}
+
+// Enqueue the five-kernel window pipeline for n lines per stream.
+int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride, float* raw, float* norm) {
+    const Geometry& g = e->geo;
+    const int L = int(e->S * n);
+    const int line_base = int(e->lines_seen * e->S);
+    timed(e, ERX_KERNEL_STATS, [&] { erxk::launch_stats(g, e->sl, x, int(n), int(in_stride), L, e->d_stats, e->stream); });
+    timed(e, ERX_KERNEL_SCAN, [&] {
+        erxk::launch_scan(g, e->d_stats, e->d_prior, e->d_state[e->cur], e->d_state[e->cur ^ 1], int(e->S), int(n),
+                          e->initialized ? 1 : 0, e->cfg.alpha, e->cfg.use_incremental, e->welford_n, e->stream);
+    });
+    timed(e, ERX_KERNEL_FACTOR, [&] {
+        erxk::launch_factor(g, e->d_prior, L, e->cfg.epsilon, e->d_work, e->d_white, e->d_status, e->d_latch,
+                            line_base, e->stream);
+    });
+    timed(e, ERX_KERNEL_SCORE, [&] {
+        erxk::launch_score(g, x, int(n), int(in_stride), e->d_prior, e->d_white, L, raw, e->stream);
+    });
+    timed(e, ERX_KERNEL_NORMALIZE, [&] { erxk::launch_normalize(g, raw, L, norm, e->stream); });
+    cudaError_t r = cudaGetLastError();
+    if (r != cudaSuccess) return fail(e, ERX_ERR_DEVICE, std::string("kernel launch: ") + cudaGetErrorString(r));
+    e->cur ^= 1;
+    if (e->cfg.use_incremental) e->welford_n += int64_t(n) * e->P;
+    e->initialized = true;
+    e->lines_seen += n;
+    return ERX_OK;
+}
+
+// Score the staged partial/full window of the drop-in path and queue results.
+int run_host_window(erx_engine* e, bool staged = true) {
+    if (e->fill == 0) return ERX_OK;
+    const uint32_t n = e->fill;
+    const size_t line_f = size_t(e->P) * e->B;
+    if (!staged) {
+        // already copied to d_lines by the caller
+    } else if (n == e->T) {
+        CU(cudaMemcpyAsync(e->d_lines, e->h_lines, size_t(e->S) * e->T * line_f * sizeof(float),
+                           cudaMemcpyHostToDevice, e->stream));
+    } else {
+        for (uint32_t s = 0; s < e->S; ++s)
+            CU(cudaMemcpyAsync(e->d_lines + size_t(s) * e->T * line_f, e->h_lines + size_t(s) * e->T * line_f,
+                               n * line_f * sizeof(float), cudaMemcpyHostToDevice, e->stream));
+    }
+    int st = enqueue_window(e, e->d_lines, n, e->T, e->d_raw, e->d_norm);
+    if (st) return st;
+    const size_t L = size_t(e->S) * n;
+    CU(cudaMemcpyAsync(e->h_raw, e->d_raw, L * e->P * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
+    CU(cudaMemcpyAsync(e->h_norm, e->d_norm, L * e->P * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
+    CU(cudaMemcpyAsync(e->h_status, e->d_status, L * sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+    CU(cudaStreamSynchronize(e->stream));
+    // first failing line in emission order (then stream order)
+    int bad_t = -1, bad_piv = -1;
+    for (uint32_t t = 0; t < n && bad_t < 0; ++t)
+        for (uint32_t s = 0; s < e->S; ++s)
+            if (e->h_status[s * n + t] >= 0) {
+                bad_t = int(t);
+                bad_piv = e->h_status[s * n + t];
+                break;
+            }
+    const uint32_t good = bad_t < 0 ? n : uint32_t(bad_t);
+    for (uint32_t t = 0; t < good; ++t) {
+        ScoredRow row;
+        row.index = e->win_index[t];
+        row.warmup = (row.index < int64_t(e->cfg.buffer_len)) ? 1 : 0;
+        row.raw.resize(size_t(e->S) * e->P);
+        row.norm.resize(size_t(e->S) * e->P);
+        for (uint32_t s = 0; s < e->S; ++s) {
+            std::memcpy(row.raw.data() + size_t(s) * e->P, e->h_raw + (size_t(s) * n + t) * e->P,
+                        e->P * sizeof(float));
+            std::memcpy(row.norm.data() + size_t(s) * e->P, e->h_norm + (size_t(s) * n + t) * e->P,
+                        e->P * sizeof(float));
+        }
+        e->queue.push_back(std::move(row));
+    }
+    e->fill = 0;
+    if (bad_t >= 0) {
+        e->failed = true;
+        e->pivot = bad_piv;
+        return fail(e, ERX_ERR_NUMERIC,
+                    "Cholesky of K + eps*I failed at pivot " + std::to_string(bad_piv) + " for line index " +
+                        std::to_string(e->win_index[bad_t]) + " after epsilon escalation to 1e-1");
+    }
+    return ERX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void erx_config_default(erx_config* c) {
+    c->dims = 5;
+    c->alpha = 0.1;
+    c->buffer_len = 99;
+    c->epsilon = 1e-5;
+    c->seed = 0;
+    c->no_srp = 0;
+    c->use_incremental = 0;
+}
+
+int erx_config_validate(const erx_config* cfg, uint32_t bands, char* msg, size_t msg_len) {
+    std::string m;
+    int st = validate(cfg, bands, m);
+    if (st) put_msg(msg, msg_len, m);
+    return st;
+}
+
+int erx_generate_srp(uint32_t bands, uint32_t dims, uint64_t seed, double* w) {
+    if (bands < 1 || dims < 1) return ERX_ERR_CONFIG;
+    erx_host::generate_srp(bands, dims, seed, w);
+    return ERX_OK;
+}
+
+int erx_create(const erx_config* cfg, uint32_t bands, uint32_t n_streams, uint32_t window_lines, int device,
+               erx_engine** out, char* msg, size_t msg_len) {
+    *out = nullptr;
+    std::string m;
+    int st = validate(cfg, bands, m);
+    if (!st && (n_streams < 1 || window_lines < 1)) {
+        m = "n_streams and window_lines must be >= 1";
+        st = ERX_ERR_CONFIG;
+    }
+    if (st) {
+        put_msg(msg, msg_len, m);
+        return st;
+    }
+    erx_engine* e = new erx_engine();
+    e->cfg = *cfg;
+    e->B = bands;
+    e->S = n_streams;
+    e->T = window_lines;
+    e->device = device;
+    e->D = cfg->no_srp ? int(bands) : cfg->dims;
+    e->Dp = (e->D + erxk::kBlk - 1) / erxk::kBlk * erxk::kBlk;
+    e->win_index.resize(window_lines);
+    auto bail = [&](const std::string& why) {
+        put_msg(msg, msg_len, why);
+        erx_destroy(e);
+        return ERX_ERR_DEVICE;
+    };
+    cudaError_t r = cudaSetDevice(device);
+    if (r != cudaSuccess) return bail(std::string("cudaSetDevice: ") + cudaGetErrorString(r));
+    r = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
+    if (r != cudaSuccess) return bail(std::string("cudaStreamCreate: ") + cudaGetErrorString(r));
+    // SRP weights (generate_srp, projection.hpp:26) -> CSC of signs per output dim
+    std::vector<int> ptr(e->D + 1, 0), band;
+    std::vector<float> sign;
+    if (!cfg->no_srp) {
+        e->W.resize(size_t(bands) * e->D);
+        erx_host::generate_srp(bands, uint32_t(e->D), cfg->seed, e->W.data());
+        const double s = std::sqrt(double(bands));
+        e->srp_scale = std::sqrt(s) / std::sqrt(double(e->D));
+        for (int j = 0; j < e->D; ++j) {
+            ptr[j] = int(band.size());
+            for (uint32_t k = 0; k < bands; ++k) {
+                double w = e->W[size_t(k) * e->D + j];
+                if (w != 0.0) {
+                    band.push_back(int(k));
+                    sign.push_back(w > 0 ? 1.f : -1.f);
+                }
+            }
+        }
+        ptr[e->D] = int(band.size());
+    }
+    const size_t nnz = std::max<size_t>(band.size(), 1);
+    if (cudaMalloc(&e->d_srp_ptr, ptr.size() * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&e->d_srp_band, nnz * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&e->d_srp_sign, nnz * sizeof(float)) != cudaSuccess)
+        return bail("cudaMalloc (srp)");
+    cudaMemcpy(e->d_srp_ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice);
+    if (!band.empty()) {
+        cudaMemcpy(e->d_srp_band, band.data(), band.size() * sizeof(int), cudaMemcpyHostToDevice);
+        cudaMemcpy(e->d_srp_sign, sign.data(), sign.size() * sizeof(float), cudaMemcpyHostToDevice);
+    }
+    const int SE = e->D + e->D * (e->D + 1) / 2;
+    for (int k = 0; k < 2; ++k) {
+        if (cudaMalloc(&e->d_state[k], size_t(n_streams) * SE * sizeof(double)) != cudaSuccess)
+            return bail("cudaMalloc (state)");
+        cudaMemset(e->d_state[k], 0, size_t(n_streams) * SE * sizeof(double));
+    }
+    if (cudaMalloc(&e->d_latch, 4 * sizeof(int)) != cudaSuccess) return bail("cudaMalloc (latch)");
+    cudaMemset(e->d_latch, 0, 4 * sizeof(int));
+    for (auto& ev : e->user_ev) cudaEventCreate(&ev);
+    *out = e;
+    return ERX_OK;
+}
+
+void erx_destroy(erx_engine* e) {
+    if (!e) return;
+    cudaSetDevice(e->device);
+    if (e->stream) cudaStreamSynchronize(e->stream);
+    free_window(e);
+    cudaFree(e->d_srp_ptr);
+    cudaFree(e->d_srp_band);
+    cudaFree(e->d_srp_sign);
+    cudaFree(e->d_state[0]);
+    cudaFree(e->d_state[1]);
+    cudaFree(e->d_latch);
+    for (auto& t : e->timings) {
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
+    }
+    for (auto ev : e->event_pool) cudaEventDestroy(ev);
+    for (auto ev : e->user_ev)
+        if (ev) cudaEventDestroy(ev);
+    if (e->stream) cudaStreamDestroy(e->stream);
+    delete e;
+}
+
+const char* erx_last_error(const erx_engine* e) { return e ? e->err.c_str() : "null engine"; }
+int erx_last_pivot(const erx_engine* e) { return e ? e->pivot : -1; }
+int erx_dims(const erx_engine* e) { return e->D; }
+uint32_t erx_streams(const erx_engine* e) { return e->S; }
+uint32_t erx_window(const erx_engine* e) { return e->T; }
+
+int erx_push_host(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t pixels, uint32_t bands,
+                  const float* lines) {
+    if (e->failed) return fail(e, ERX_ERR_STATE, "engine is in a failed state: " + e->err);
+    if (bands != e->B) return fail(e, ERX_ERR_CONFIG, "band count mismatch");  // projection.hpp:31-32
+    if (pixels < 2) return fail(e, ERX_ERR_DATA, "a line needs p >= 2 pixels (1/(p-1) covariance)");  // erx.hpp:39
+    if (n_lines == 0) return ERX_OK;
+    if (pixels != e->P || !e->d_stats) {
+        int st = run_host_window(e);
+        if (st) return st;
+        st = configure(e, pixels);
+        if (st) return st;
+    }
+    int st = ensure_host_staging(e);
+    if (st) return st;
+    const size_t line_f = size_t(pixels) * bands;
+    uint32_t i = 0;
+    while (i < n_lines) {
+        if (e->fill == 0 && n_lines - i >= e->T) {
+            // a whole window straight from the caller's buffer (pinned memory: DMA; pageable: staged by CUDA)
+            for (uint32_t s = 0; s < e->S; ++s)
+                CU(cudaMemcpyAsync(e->d_lines + size_t(s) * e->T * line_f, lines + (size_t(s) * n_lines + i) * line_f,
+                                   size_t(e->T) * line_f * sizeof(float), cudaMemcpyHostToDevice, e->stream));
+            for (uint32_t k = 0; k < e->T; ++k) e->win_index[k] = first_index + int64_t(i + k);
+            e->fill = e->T;
+            st = run_host_window(e, /*staged=*/false);
+            if (st) return st;
+            i += e->T;
+            continue;
+        }
+        for (uint32_t s = 0; s < e->S; ++s)
+            std::memcpy(e->h_lines + (size_t(s) * e->T + e->fill) * line_f,
+                        lines + (size_t(s) * n_lines + i) * line_f, line_f * sizeof(float));
+        e->win_index[e->fill] = first_index + int64_t(i);
+        e->fill += 1;
+        i += 1;
+        if (e->fill == e->T) {
+            st = run_host_window(e, true);
+            if (st) return st;
+        }
+    }
+    return ERX_OK;
+}
+
+int erx_finish(erx_engine* e) {
+    if (e->failed) return fail(e, ERX_ERR_STATE, "engine is in a failed state: " + e->err);
+    return run_host_window(e);
+}
+
+uint32_t erx_ready(const erx_engine* e) { return uint32_t(e->queue.size()); }
+
+int erx_pop(erx_engine* e, uint32_t max_lines, int64_t* index, uint8_t* warmup, double* raw, double* norm) {
+    const uint32_t n = std::min<uint32_t>(max_lines, uint32_t(e->queue.size()));
+    for (uint32_t k = 0; k < n; ++k) {
+        const ScoredRow& r = e->queue[k];
+        if (index) index[k] = r.index;
+        if (warmup) warmup[k] = r.warmup;
+        for (uint32_t s = 0; s < e->S; ++s)
+            for (uint32_t p = 0; p < e->P; ++p) {
+                if (raw) raw[(size_t(s) * n + k) * e->P + p] = double(r.raw[size_t(s) * e->P + p]);
+                if (norm) norm[(size_t(s) * n + k) * e->P + p] = double(r.norm[size_t(s) * e->P + p]);
+            }
+    }
+    for (uint32_t k = 0; k < n; ++k) e->queue.pop_front();
+    return int(n);
+}
+
+int erx_run_device(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t pixels, const float* d_lines,
+                   float* d_raw, float* d_norm) {
+    (void)first_index;
+    if (e->failed) return fail(e, ERX_ERR_STATE, "engine is in a failed state: " + e->err);
+    if (pixels < 2) return fail(e, ERX_ERR_DATA, "a line needs p >= 2 pixels (1/(p-1) covariance)");
+    if (n_lines == 0) return ERX_OK;
+    if (n_lines > e->T) return fail(e, ERX_ERR_CONFIG, "n_lines exceeds the engine window");
+    if (e->fill) return fail(e, ERX_ERR_STATE, "host lines pending; call erx_finish first");
+    int st = configure(e, pixels);
+    if (st) return st;
+    return enqueue_window(e, d_lines, n_lines, n_lines, d_raw, d_norm);
+}
+
+int erx_sync(erx_engine* e) {
+    CU(cudaStreamSynchronize(e->stream));
+    int latch[4];
+    CU(cudaMemcpy(latch, e->d_latch, sizeof(latch), cudaMemcpyDeviceToHost));
+    if (latch[0]) {
+        e->failed = true;
+        e->pivot = latch[2];
+        return fail(e, ERX_ERR_NUMERIC, "Cholesky of K + eps*I failed at pivot " + std::to_string(latch[2]) +
+                                            " (window line id " + std::to_string(latch[1]) + ")");
+    }
+    return ERX_OK;
+}
+
+void* erx_cuda_stream(erx_engine* e) { return reinterpret_cast<void*>(e->stream); }
+
+int erx_get_state(erx_engine* e, uint32_t stream, double* mu, double* cov, int64_t* lines_seen,
+                  int64_t* welford_n, int* initialized) {
+    if (stream >= e->S) return fail(e, ERX_ERR_CONFIG, "stream index out of range");
+    if (lines_seen) *lines_seen = e->lines_seen;
+    if (welford_n) *welford_n = e->welford_n;
+    if (initialized) *initialized = e->initialized ? 1 : 0;
+    if (!e->initialized || (!mu && !cov)) return ERX_OK;
+    const int D = e->D, SE = D + D * (D + 1) / 2;
+    std::vector<double> h(SE);
+    CU(cudaStreamSynchronize(e->stream));
+    CU(cudaMemcpy(h.data(), e->d_state[e->cur] + size_t(stream) * SE, SE * sizeof(double), cudaMemcpyDeviceToHost));
+    if (mu) std::memcpy(mu, h.data(), D * sizeof(double));
+    if (cov)
+        for (int i = 0; i < D; ++i)
+            for (int j = 0; j <= i; ++j) {
+                const double v = h[D + erxk::tri(i, j)];
+                cov[size_t(i) * D + j] = v;
+                cov[size_t(j) * D + i] = v;
+            }
+    return ERX_OK;
+}
+
+int erx_get_weights(const erx_engine* e, double* w) {
+    if (e->cfg.no_srp) return ERX_ERR_CONFIG;
+    std::memcpy(w, e->W.data(), e->W.size() * sizeof(double));
+    return ERX_OK;
+}
+
+int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double* cov, int64_t lines_seen,
+                  int64_t welford_n) {
+    if (stream >= e->S) return fail(e, ERX_ERR_CONFIG, "stream index out of range");
+    const int D = e->D, SE = D + D * (D + 1) / 2;
+    std::vector<double> h(SE);
+    std::memcpy(h.data(), mu, D * sizeof(double));
+    for (int i = 0; i < D; ++i)
+        for (int j = 0; j <= i; ++j) h[D + erxk::tri(i, j)] = cov[size_t(i) * D + j];
+    CU(cudaStreamSynchronize(e->stream));
+    CU(cudaMemcpy(e->d_state[e->cur] + size_t(stream) * SE, h.data(), SE * sizeof(double), cudaMemcpyHostToDevice));
+    e->initialized = true;
+    e->lines_seen = lines_seen;
+    e->welford_n = welford_n;
+    return ERX_OK;
+}
+
+uint64_t erx_launch_count(const erx_engine* e) { return e->launches; }
+
+int erx_set_profiling(erx_engine* e, int on) {
+    collect_timings(e);
+    e->profiling = on != 0;
+    for (int k = 0; k < ERX_NUM_KERNELS; ++k) {
+        e->kms[k] = 0;
+        e->kcount[k] = 0;
+    }
+    return ERX_OK;
+}
+
+int erx_kernel_times(erx_engine* e, double* ms, uint64_t* launches) {
+    collect_timings(e);
+    for (int k = 0; k < ERX_NUM_KERNELS; ++k) {
+        if (ms) ms[k] = e->kms[k];
+        if (launches) launches[k] = e->kcount[k];
+    }
+    return ERX_OK;
+}
+
+int erx_event_record(erx_engine* e, int slot) {
+    if (slot < 0 || slot >= 8) return ERX_ERR_CONFIG;
+    CU(cudaEventRecord(e->user_ev[slot], e->stream));
+    return ERX_OK;
+}
+
+int erx_event_elapsed_ms(erx_engine* e, int a, int b, float* ms) {
+    if (a < 0 || a >= 8 || b < 0 || b >= 8) return ERX_ERR_CONFIG;
+    CU(cudaEventSynchronize(e->user_ev[b]));
+    CU(cudaEventElapsedTime(ms, e->user_ev[a], e->user_ev[b]));
+    return ERX_OK;
+}
+
+int erx_probe_fp32_tflops(erx_engine* e, double* tflops) {
+    CU(cudaSetDevice(e->device));
+    *tflops = erxk::probe_ffma_tflops(e->stream);
+    CU(cudaGetLastError());
+    return ERX_OK;
+}
+
+void* erx_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) != cudaSuccess) return nullptr;
+    return p;
+}
+void erx_host_free(void* p) { cudaFreeHost(p); }
+void* erx_device_alloc(int device, size_t bytes) {
+    void* p = nullptr;
+    cudaSetDevice(device);
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    return p;
+}
+void erx_device_free(void* p) { cudaFree(p); }
+
+int erx_copy(void* dst, const void* src, size_t bytes, int kind, erx_engine* e) {
+    cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice : kind == 2 ? cudaMemcpyDeviceToHost
+                                                                     : cudaMemcpyDeviceToDevice;
+    if (e) {
+        CU(cudaMemcpyAsync(dst, src, bytes, k, e->stream));
+    } else {
+        CU(cudaMemcpy(dst, src, bytes, k));
+    }
+    return ERX_OK;
+}
+
+}  // extern "C"

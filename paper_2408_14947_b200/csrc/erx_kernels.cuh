@@ -1,0 +1,77 @@
+// erx_kernels.cuh — device-side pieces of the windowed ERX pipeline.
+//
+// One window = n lines of each of S independent streams, line id
+// l = s * n + t.  The five kernels map onto the reference per-line chain
+// (erx.hpp:51-71) re-associated across lines:
+//
+//   stats      project_line + line_stats       (projection.hpp:33, erx.hpp:40)
+//   scan       ema_update / welford_batch_update (erx.hpp:43, linalg.hpp:36)
+//   factor     cholesky_lower(K + eps I) with eps escalation, then L^{-1}
+//                                               (linalg.hpp:15)
+//   score      forward_substitute as a whitening multiply m = L^{-1}(z - mu),
+//              delta = ||m||                    (linalg.hpp:21)
+//   normalize  normalize_scores                 (detector.hpp:29-32)
+//
+// Only line_stats is state-free, so every line of the window gets its
+// statistics at once; the EMA is an exact element-wise scan (same rounding
+// order as the sequential recurrence); factor and score then run for every
+// line against its own pre-update background (score-then-update).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace erxk {
+
+constexpr int kBlk = 8;          // register-block edge (stats / score)
+constexpr int kNB = 32;          // panel width of the blocked factorisation
+constexpr int kScoreTile = 64;   // pixels per score CTA
+constexpr int kScoreStride = kScoreTile + 4;
+
+// Packed lower-triangular index (row-major, j <= i).
+__host__ __device__ inline int tri(int i, int j) { return i * (i + 1) / 2 + j; }
+
+struct Geometry {
+    int P;         // pixels per line
+    int B;         // bands
+    int D;         // projected dims (B when no_srp)
+    int Dp;        // D rounded up to a multiple of kBlk
+    int nb;        // Dp / kBlk
+    int SE;        // slot elements: D + D(D+1)/2 (mean followed by packed lower covariance)
+    int srp;       // 1: sparse random projection, 0: identity
+    const int* srp_ptr;    // [D+1] CSC starts per output dim
+    const int* srp_band;   // [nnz] band index
+    const float* srp_w;    // [nnz] sign of the weight (+1 / -1)
+    double srp_scale;      // |w| = sqrt(s)/sqrt(d); z_j = scale * sum_k sign_k x_k (fp64)
+};
+
+struct StatsLaunch {
+    int CH;          // pixels staged per chunk
+    int n_pairs;     // lower-triangular 8x8 block pairs
+    int npc;         // pairs per CTA
+    int G;           // pixel groups per pair (threads per pair)
+    int cpl;         // CTAs per line
+    size_t smem;     // dynamic shared memory bytes
+};
+
+StatsLaunch plan_stats(const Geometry& g);
+size_t score_smem(const Geometry& g);
+size_t factor_smem(const Geometry& g);
+
+// Host launchers (erx_kernels.cu).  All asynchronous on `st`.
+void launch_stats(const Geometry& g, const StatsLaunch& sl, const float* x, int n_per_stream, int in_stride,
+                  int n_lines_total, double* stats, cudaStream_t st);
+void launch_scan(const Geometry& g, const double* stats, double* prior, const double* state_in, double* state_out,
+                 int n_streams, int n_per_stream, int initialized, double alpha, int incremental, int64_t n_seen0,
+                 cudaStream_t st);
+// latch: {flag, line, pivot} of the first factorisation failure (sticky until the host clears it).
+void launch_factor(const Geometry& g, const double* prior, int n_lines_total, double eps0, double* work,
+                   float* whiten, int* status, int* latch, int line_base, cudaStream_t st);
+void launch_score(const Geometry& g, const float* x, int n_per_stream, int in_stride, const double* prior,
+                  const float* whiten, int n_lines_total, float* raw, cudaStream_t st);
+void launch_normalize(const Geometry& g, const float* raw, int n_lines_total, float* norm, cudaStream_t st);
+
+// Measured FP32 FFMA throughput of the current device (TFLOP/s, best of 5).
+double probe_ffma_tflops(cudaStream_t st);
+
+}  // namespace erxk

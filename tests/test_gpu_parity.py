@@ -1,0 +1,244 @@
+"""GPU parity: the sm_100a ERX path (through the C ABI) against the fp64 CPU
+oracle on identical seeded inputs.
+
+Gates (BASELINE.json north_star):
+  * raw delta: max relative error <= 1e-3, median <= 1e-5;
+  * norm: |gpu - oracle| <= 1e-3 * max(1, |oracle|);
+  * top-1% anomaly set over pooled non-warmup norm scores identical except
+    for oracle scores within the norm tolerance of the cut;
+  * AUC of the pooled non-warmup norm scores vs the injected labels equal
+    to 3 decimals.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+RAW_MAX, RAW_MED = 1e-3, 1e-5
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2408_14947_b200 as p
+
+    p.lib()
+    return p
+
+
+def run_gpu(pkg, cfg, lines, window=32):
+    det = pkg.ErxDetector(cfg, lines.shape[2], window_lines=window)
+    out = []
+    for t in range(lines.shape[0]):
+        det.process(pkg.SpectralLine(t, lines[t]), out)
+    det.finish(out)
+    assert [s.index for s in out] == list(range(lines.shape[0]))
+    raw = np.stack([s.raw for s in out])
+    norm = np.stack([s.norm for s in out])
+    warm = np.array([s.warmup for s in out])
+    return raw, norm, warm, det
+
+
+def ocfg(oracle, cfg):
+    return oracle.OracleConfig(dims=cfg.dims, alpha=cfg.alpha, buffer_len=cfg.buffer_len, epsilon=cfg.epsilon,
+                               seed=cfg.seed, no_srp=cfg.no_srp, use_incremental=cfg.use_incremental)
+
+
+def check_gates(oracle, raw_g, norm_g, raw_o, norm_o, mask=None, warm=None, label=""):
+    rel = np.abs(raw_g - raw_o) / np.maximum(np.abs(raw_o), 1e-30)
+    assert rel.max() <= RAW_MAX, f"{label} raw max rel {rel.max():.3e}"
+    assert np.median(rel) <= RAW_MED, f"{label} raw median rel {np.median(rel):.3e}"
+    nerr = np.abs(norm_g - norm_o) / np.maximum(1.0, np.abs(norm_o))
+    assert nerr.max() <= 1e-3, f"{label} norm err {nerr.max():.3e}"
+    if warm is not None:
+        sel = ~np.asarray(warm, bool)
+        ng, no = norm_g[sel].ravel(), norm_o[sel].ravel()
+        k = max(1, int(math.ceil(0.01 * ng.size)))
+        cut = np.partition(no, no.size - k)[no.size - k]
+        top_g = set(np.argpartition(-ng, k - 1)[:k].tolist())
+        top_o = set(np.argpartition(-no, k - 1)[:k].tolist())
+        diff = np.array(sorted(top_g ^ top_o), dtype=np.int64)
+        if diff.size:
+            band = 1e-3 * max(1.0, abs(cut))
+            assert np.all(np.abs(no[diff] - cut) <= band), f"{label} top-1% differs beyond ties"
+        if mask is not None:
+            y = np.asarray(mask)[sel].ravel()
+            if 0 < y.sum() < y.size:
+                ag, ao = oracle.roc_auc(ng, y), oracle.roc_auc(no, y)
+                assert round(ag, 3) == round(ao, 3) or abs(ag - ao) < 1e-6, f"{label} AUC {ag} vs {ao}"
+    return float(rel.max()), float(np.median(rel))
+
+
+# ---------------------------------------------------------------- small randomized streams
+@pytest.mark.parametrize("no_srp", [True, False])
+@pytest.mark.parametrize("incremental", [False, True])
+@pytest.mark.parametrize("window", [1, 5, 32])
+def test_small_random_streams(pkg, oracle, no_srp, incremental, window):  # SPEC.md:696 shapes
+    rng = np.random.default_rng(100 + 10 * no_srp + 2 * incremental + window)
+    for s in range(6):
+        p = int(rng.integers(9, 21))
+        b = int(rng.integers(2, 9))
+        alpha = float(rng.choice([1.0, 0.5, 0.1, 0.01]))
+        lines = (rng.uniform(size=(120, p, b)) + np.linspace(0, 1, 120)[:, None, None]).astype(np.float32)
+        cfg = pkg.ErxConfig(no_srp=no_srp, dims=max(1, b // 2), alpha=alpha, seed=s, use_incremental=incremental,
+                            buffer_len=10)
+        raw_g, norm_g, warm, _ = run_gpu(pkg, cfg, lines, window)
+        raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), lines)
+        check_gates(oracle, raw_g, norm_g, raw_o, norm_o, label=f"s{s} p{p} b{b}")
+        assert warm.tolist() == [t < 10 for t in range(120)]
+
+
+def test_window_size_is_bitwise_invariant(pkg):
+    spec = pkg.gen_spec(0)
+    lines, _ = pkg.gen_lines(spec, 0, 40)
+    cfg = pkg.ErxConfig(no_srp=True)
+    ref = run_gpu(pkg, cfg, lines, 1)[0]
+    for w in (3, 16, 64):
+        assert np.array_equal(run_gpu(pkg, cfg, lines, w)[0], ref)
+
+
+def test_batched_streams_equal_single_streams(pkg):
+    S, n = 3, 24
+    lines = np.stack([pkg.gen_lines(pkg.gen_spec(3, s), 0, n)[0] for s in range(S)])
+    cfg = pkg.ErxConfig(no_srp=True)
+    eng = pkg.Engine(cfg, 108, n_streams=S, window_lines=8)
+    eng.push(lines, 0)
+    eng.finish()
+    idx, wu, raw, norm = eng.pop()
+    assert idx.tolist() == list(range(n))
+    for s in range(S):
+        single = run_gpu(pkg, cfg, lines[s], 8)[0]
+        assert np.array_equal(raw[s], single)
+
+
+def test_device_path_equals_host_path(pkg):
+    import torch
+
+    S, n = 2, 16
+    lines = np.stack([pkg.gen_lines(pkg.gen_spec(3, s), 0, n)[0] for s in range(S)])
+    cfg = pkg.ErxConfig(no_srp=True)
+    host = pkg.Engine(cfg, 108, n_streams=S, window_lines=n)
+    host.push(lines, 0)
+    host.finish()
+    _, _, raw_h, norm_h = host.pop()
+    dev = pkg.Engine(cfg, 108, n_streams=S, window_lines=n)
+    x = torch.from_numpy(lines).cuda()
+    raw = torch.empty((S, n, 640), dtype=torch.float32, device="cuda")
+    norm = torch.empty_like(raw)
+    torch.cuda.synchronize()
+    dev.run_device(x.data_ptr(), n, 640, raw.data_ptr(), norm.data_ptr())
+    dev.sync()
+    assert np.array_equal(raw.cpu().numpy().astype(np.float64), raw_h)
+    assert np.array_equal(norm.cpu().numpy().astype(np.float64), norm_h)
+
+
+# ---------------------------------------------------------------- BASELINE configs
+def run_config(pkg, oracle, cid, n_lines, no_srp, streams=(0,), overrides=None, window=32):
+    specs = []
+    for s in streams:
+        spec = pkg.gen_spec(cid, s)
+        for k, v in (overrides or {}).items():
+            if k == "scene_change_line":
+                for i, c in enumerate(v):
+                    spec.scene_change_line[i] = c
+            else:
+                setattr(spec, k, v)
+        specs.append(spec)
+    data = [pkg.gen_lines(sp, 0, n_lines) for sp in specs]
+    lines = np.stack([d[0] for d in data])
+    mask = np.stack([d[1] for d in data])
+    alpha = {0: 0.1, 1: 0.05, 2: 0.1, 3: 0.1, 4: 0.05}[cid]
+    cfg = pkg.ErxConfig(no_srp=no_srp, alpha=alpha)
+    eng = pkg.Engine(cfg, specs[0].bands, n_streams=len(streams), window_lines=window)
+    eng.push(lines, 0)
+    eng.finish()
+    idx, wu, raw_g, norm_g = eng.pop()
+    raw_o, norm_o = oracle.run_streams(ocfg(oracle, cfg), lines, threads=len(streams))
+    warm = np.broadcast_to(wu[None, :, None], raw_g.shape)
+    return check_gates(oracle, raw_g, norm_g, raw_o, norm_o, mask=mask, warm=warm,
+                       label=f"c{cid} {'D=B' if no_srp else 'd=5'}")
+
+
+@pytest.mark.parametrize("no_srp", [True, False])
+def test_config0_full_stream(pkg, oracle, no_srp):
+    run_config(pkg, oracle, 0, 2000, no_srp, window=64)
+
+
+@pytest.mark.parametrize("no_srp", [True, False])
+def test_config2_full_stream(pkg, oracle, no_srp):
+    run_config(pkg, oracle, 2, 20000, no_srp, window=128)
+
+
+@pytest.mark.parametrize("no_srp", [True, False])
+def test_config1_scene_change_subset(pkg, oracle, no_srp):
+    # c1 shortened: the line-5000 scene change is moved to line 160 so the
+    # adaptivity transient is inside the oracle-affordable prefix.
+    run_config(pkg, oracle, 1, 320, no_srp, overrides={"lines": 10000, "scene_change_line": [160]})
+
+
+@pytest.mark.parametrize("no_srp", [True, False])
+def test_config3_stream_subset(pkg, oracle, no_srp):
+    run_config(pkg, oracle, 3, 220, no_srp, streams=(0, 31, 63))
+
+
+@pytest.mark.parametrize("no_srp", [True, False])
+def test_config4_subset(pkg, oracle, no_srp):
+    run_config(pkg, oracle, 4, 60 if no_srp else 300, no_srp, streams=(0, 1, 2, 3),
+               overrides={"scene_change_line": [20, 40]}, window=16)
+
+
+# ---------------------------------------------------------------- contract edges
+def test_state_matches_oracle(pkg, oracle):
+    spec = pkg.gen_spec(0)
+    lines, _ = pkg.gen_lines(spec, 0, 30)
+    for cfg in (pkg.ErxConfig(no_srp=True), pkg.ErxConfig(), pkg.ErxConfig(use_incremental=True)):
+        _, _, _, det = run_gpu(pkg, cfg, lines, 8)
+        _, _, odet = oracle.run_stream(ocfg(oracle, cfg), lines)
+        g, o = det.state(), odet.state()
+        assert g.initialized and g.lines_seen == o["lines_seen"] == 30 and g.welford_n == o["welford_n"]
+        np.testing.assert_allclose(g.mu, o["mu"], rtol=1e-7, atol=1e-12)
+        np.testing.assert_allclose(g.cov, o["cov"], rtol=1e-4, atol=1e-9 * np.abs(o["cov"]).max())
+        if not cfg.no_srp:
+            np.testing.assert_array_equal(g.weights, o["weights"])
+
+
+def test_constant_line_and_init(pkg):
+    cfg = pkg.ErxConfig(no_srp=True)
+    det = pkg.ErxDetector(cfg, 4, window_lines=1)
+    out = []
+    det.process(pkg.SpectralLine(0, np.full((6, 4), 0.25, np.float32)), out)
+    assert np.array_equal(out[0].norm, np.zeros(6)) and np.array_equal(out[0].raw, np.zeros(6))
+    st = det.state()
+    assert np.allclose(st.mu, 0.25) and np.abs(st.cov).max() == 0.0
+
+
+def test_pixel_count_change_mid_stream(pkg, oracle):
+    rng = np.random.default_rng(5)
+    cfg = pkg.ErxConfig(no_srp=True)
+    det = pkg.ErxDetector(cfg, 5, window_lines=4)
+    odet = oracle.OracleErx(ocfg(oracle, cfg), 5)
+    out = []
+    ref = []
+    for t in range(14):
+        x = rng.uniform(size=(12 if t < 7 else 17, 5)).astype(np.float32)
+        det.process(pkg.SpectralLine(t, x), out)
+        ref.append(odet.process(t, x)[0])
+    det.finish(out)
+    for s, r in zip(out, ref):
+        assert np.max(np.abs(s.raw - r) / r) < 1e-3
+
+
+def test_errors(pkg):
+    det = pkg.ErxDetector(pkg.ErxConfig(no_srp=True), 3, window_lines=1)
+    with pytest.raises(pkg.ConfigError):
+        det.process(pkg.SpectralLine(0, np.zeros((5, 4), np.float32)), [])
+    with pytest.raises(pkg.DataError):
+        det.process(pkg.SpectralLine(0, np.zeros((1, 3), np.float32)), [])
+    x = np.random.default_rng(0).normal(size=(8, 3)).astype(np.float32)
+    x[0, 1] = np.nan
+    with pytest.raises(pkg.FactorizationError) as e:
+        det.process(pkg.SpectralLine(0, x), [])
+    assert e.value.pivot >= 0 and e.value.exit_code() == 3
+    with pytest.raises(pkg.DeviceError):  # sticky failed state (ERX_ERR_STATE)
+        det.process(pkg.SpectralLine(1, np.ones((8, 3), np.float32)), [])
