@@ -89,8 +89,10 @@ int erx_push_host(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t
 /* Replaces LineDetector::finish (detector.hpp:21): scores any partial window. */
 int erx_finish(erx_engine* e);
 
-/* Scored lines waiting per stream. */
+/* Scored lines waiting per stream (the leading run that shares one pixel
+ * count) and that pixel count (0 when nothing is queued). */
 uint32_t erx_ready(const erx_engine* e);
+uint32_t erx_next_pixels(const erx_engine* e);
 
 /*
  * Pops up to max_lines scored lines of every stream, oldest first: the

@@ -74,6 +74,7 @@ SIGNATURES = {
     "erx_push_host": (C.c_int, [_vp, C.c_int64, C.c_uint32, C.c_uint32, C.c_uint32, _fp]),
     "erx_finish": (C.c_int, [_vp]),
     "erx_ready": (C.c_uint32, [_vp]),
+    "erx_next_pixels": (C.c_uint32, [_vp]),
     "erx_pop": (C.c_int, [_vp, C.c_uint32, _i64p, _u8p, _dp, _dp]),
     "erx_run_device": (C.c_int, [_vp, C.c_int64, C.c_uint32, C.c_uint32, _vp, _vp, _vp]),
     "erx_sync": (C.c_int, [_vp]),

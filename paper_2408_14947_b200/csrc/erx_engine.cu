@@ -27,6 +27,7 @@ namespace {
 struct ScoredRow {
     int64_t index;
     uint8_t warmup;
+    uint32_t P;               // pixels of this line
     std::vector<float> raw;   // [S][P]
     std::vector<float> norm;  // [S][P]
 };
@@ -290,6 +291,7 @@ int run_host_window(erx_engine* e, bool staged = true) {
         ScoredRow row;
         row.index = e->win_index[t];
         row.warmup = (row.index < int64_t(e->cfg.buffer_len)) ? 1 : 0;
+        row.P = e->P;
         row.raw.resize(size_t(e->S) * e->P);
         row.norm.resize(size_t(e->S) * e->P);
         for (uint32_t s = 0; s < e->S; ++s) {
@@ -488,18 +490,29 @@ int erx_finish(erx_engine* e) {
     return run_host_window(e);
 }
 
-uint32_t erx_ready(const erx_engine* e) { return uint32_t(e->queue.size()); }
+uint32_t erx_ready(const erx_engine* e) {
+    // the leading run of queued lines that share one pixel count
+    uint32_t n = 0;
+    for (const auto& r : e->queue) {
+        if (r.P != e->queue.front().P) break;
+        ++n;
+    }
+    return n;
+}
+
+uint32_t erx_next_pixels(const erx_engine* e) { return e->queue.empty() ? 0u : e->queue.front().P; }
 
 int erx_pop(erx_engine* e, uint32_t max_lines, int64_t* index, uint8_t* warmup, double* raw, double* norm) {
-    const uint32_t n = std::min<uint32_t>(max_lines, uint32_t(e->queue.size()));
+    const uint32_t n = std::min<uint32_t>(max_lines, erx_ready(e));
     for (uint32_t k = 0; k < n; ++k) {
         const ScoredRow& r = e->queue[k];
+        const size_t P = r.P;
         if (index) index[k] = r.index;
         if (warmup) warmup[k] = r.warmup;
         for (uint32_t s = 0; s < e->S; ++s)
-            for (uint32_t p = 0; p < e->P; ++p) {
-                if (raw) raw[(size_t(s) * n + k) * e->P + p] = double(r.raw[size_t(s) * e->P + p]);
-                if (norm) norm[(size_t(s) * n + k) * e->P + p] = double(r.norm[size_t(s) * e->P + p]);
+            for (size_t p = 0; p < P; ++p) {
+                if (raw) raw[(size_t(s) * n + k) * P + p] = double(r.raw[size_t(s) * P + p]);
+                if (norm) norm[(size_t(s) * n + k) * P + p] = double(r.norm[size_t(s) * P + p]);
             }
     }
     for (uint32_t k = 0; k < n; ++k) e->queue.pop_front();

@@ -200,7 +200,7 @@ class Engine:
 
     def pop(self, max_lines: Optional[int] = None):
         n = self.ready() if max_lines is None else min(max_lines, self.ready())
-        P = self.pixels or 0
+        P = int(self._lib.erx_next_pixels(self._h))
         idx = np.zeros(n, np.int64)
         wu = np.zeros(n, np.uint8)
         raw = np.zeros((self.n_streams, n, P))
@@ -300,7 +300,7 @@ class ErxDetector(LineDetector):
         self._eng = Engine(cfg, bands, 1, window_lines, device)
 
     def _drain(self, out: List[ScoredLine]):
-        if self._eng.ready():
+        while self._eng.ready():
             idx, wu, raw, norm = self._eng.pop()
             for k in range(idx.size):
                 out.append(ScoredLine(int(idx[k]), raw[0, k].copy(), norm[0, k].copy(), None, bool(wu[k])))

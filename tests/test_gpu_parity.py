@@ -149,7 +149,8 @@ def run_config(pkg, oracle, cid, n_lines, no_srp, streams=(0,), overrides=None, 
     lines = np.stack([d[0] for d in data])
     mask = np.stack([d[1] for d in data])
     alpha = {0: 0.1, 1: 0.05, 2: 0.1, 3: 0.1, 4: 0.05}[cid]
-    cfg = pkg.ErxConfig(no_srp=no_srp, alpha=alpha)
+    # subsets shorter than the 99-line warm-up keep a scored (non-warmup) tail for the set/AUC gates
+    cfg = pkg.ErxConfig(no_srp=no_srp, alpha=alpha, buffer_len=min(99, n_lines // 3))
     eng = pkg.Engine(cfg, specs[0].bands, n_streams=len(streams), window_lines=window)
     eng.push(lines, 0)
     eng.finish()
