@@ -159,6 +159,7 @@ def run_ours(args):
     raw = torch.empty((S, T, P), dtype=torch.float32, device=f"cuda:{local}")
     norm = torch.empty_like(raw)
     eng = pkg.Engine(cfg, B, n_streams=S, window_lines=T, device=local)
+    eng.set_factor_precision(args.factor)
     D = eng.dims
 
     def step(k):
@@ -237,6 +238,7 @@ def run_ours(args):
     try:
         e2e_steps = max(2, min(args.steps, 8))
         eng2 = pkg.Engine(cfg, B, n_streams=S, window_lines=T, device=local)
+        eng2.set_factor_precision(args.factor)
         pin = torch.from_numpy(np.ascontiguousarray(host[:, :T])).pin_memory().numpy()
         for k in range(2):
             eng2.push(pin, k * T)
@@ -275,6 +277,7 @@ def run_ours(args):
             "config": {"workload": f"configs[{cid}]", "streams": S_tot, "streams_per_gpu": S, "pixels": P,
                        "bands": B, "dims": D, "mode": "D=B (no_srp)" if no_srp else "d=5 SRP",
                        "alpha": cfgd["alpha"], "window_lines": T, "pool_lines_per_stream": pool_lines,
+                       "factor_precision": eng.factor_precision(),
                        "l2": "inputs larger than L2: device pool >= 2x L2, one window per step"},
             "pixel_bands_per_s": value * P * B,
             "roofline": roof, "roofline_line": roofline_line, "kernels": kernels,
@@ -423,6 +426,8 @@ def main():
     ap.add_argument("--config", type=int, default=3, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--mode", default="full", choices=["full", "srp"])
     ap.add_argument("--window", type=int, default=8)
+    ap.add_argument("--factor", type=int, default=0, choices=[0, 1, 32, 64],
+                    help="factor kernel precision (ERX_OPT_FACTOR_PRECISION)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip the single-stream / latency side measurements")

@@ -125,6 +125,15 @@ int erx_get_weights(const erx_engine* e, double* weights);
 int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double* cov, int64_t lines_seen,
                   int64_t welford_n);
 
+/* Engine options.  ERX_OPT_FACTOR_PRECISION: 0 auto (fp64 in shared memory
+ * while the D x D factor fits, else fp32 in shared memory, else blocked fp64
+ * over global memory), 64, 32, or 1 (force the blocked fp64 global-memory
+ * kernel).  erx_get_option reports the precision in
+ * use once the first line has fixed the geometry (0 = blocked fp64 path). */
+#define ERX_OPT_FACTOR_PRECISION 1
+int erx_set_option(erx_engine* e, int option, int64_t value);
+int64_t erx_get_option(const erx_engine* e, int option);
+
 /* ---- instrumentation (bench / profiling; not part of the reference API) ---- */
 #define ERX_KERNEL_STATS 0
 #define ERX_KERNEL_SCAN 1

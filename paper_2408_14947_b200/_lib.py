@@ -21,6 +21,7 @@ ERX_ERR_DEVICE = 16
 ERX_ERR_STATE = 17
 NUM_KERNELS = 5
 KERNEL_NAMES = ("stats", "scan", "factor", "score", "normalize")
+OPT_FACTOR_PRECISION = 1
 
 
 class ErxConfigC(C.Structure):
@@ -83,6 +84,8 @@ SIGNATURES = {
     "erx_get_weights": (C.c_int, [_vp, _dp]),
     "erx_set_state": (C.c_int, [_vp, C.c_uint32, _dp, _dp, C.c_int64, C.c_int64]),
     "erx_launch_count": (C.c_uint64, [_vp]),
+    "erx_set_option": (C.c_int, [_vp, C.c_int, C.c_int64]),
+    "erx_get_option": (C.c_int64, [_vp, C.c_int]),
     "erx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "erx_kernel_times": (C.c_int, [_vp, _dp, _u64p]),
     "erx_probe_fp32_tflops": (C.c_int, [_vp, _dp]),

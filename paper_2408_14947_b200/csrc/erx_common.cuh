@@ -1,0 +1,45 @@
+// erx_common.cuh — device helpers shared by the ERX kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "erx_kernels.cuh"
+
+namespace erxk {
+
+__host__ __device__ __forceinline__ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Line l = s * n + t of a window whose input buffer holds in_stride lines per stream.
+__device__ __forceinline__ const float* line_ptr(const float* x, int line, int n, int in_stride, const Geometry& g) {
+    const int s = line / n, t = line - s * n;
+    return x + (size_t(s) * in_stride + t) * size_t(g.P) * g.B;
+}
+
+// Sparse random projection of one pixel row onto output dim j (project_line,
+// projection.hpp:31-34): z_j = |w| * sum_k sign_k x[band_k], summed in fp64 —
+// an fp32 radiance times +-1 is exact and the sum keeps fp64 precision, so z
+// matches the reference's fp64 Z = X W to rounding.
+__device__ __forceinline__ double srp_z(const Geometry& g, const float* __restrict__ row, int j) {
+    double z = 0.0;
+    for (int k = g.srp_ptr[j]; k < g.srp_ptr[j + 1]; ++k) z += double(__ldg(row + g.srp_band[k])) * double(g.srp_w[k]);
+    return z * g.srp_scale;
+}
+
+// Projected value of dim j of a pixel row (identity or SRP), fp64.
+__device__ __forceinline__ double proj(const Geometry& g, const float* __restrict__ row, int j) {
+    return g.srp ? srp_z(g, row, j) : double(__ldg(row + j));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+}  // namespace erxk

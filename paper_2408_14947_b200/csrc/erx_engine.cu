@@ -55,6 +55,9 @@ struct erx_engine {
     uint32_t P = 0;  // pixels (set by the first line)
     Geometry geo{};
     erxk::StatsLaunch sl{};
+    erxk::ScoreLaunch sc{};
+    int factor_req = 0;   // requested factor precision (0 auto, 32, 64)
+    int factor_prec = 0;  // precision in use (0 = blocked fp64 global path)
 
     // device buffers, capacity S*T lines
     float* d_lines = nullptr;
@@ -206,10 +209,12 @@ int configure(erx_engine* e, uint32_t P) {
     g.srp_w = e->d_srp_sign;
     g.srp_scale = e->srp_scale;
     e->sl = erxk::plan_stats(g);
+    e->sc = erxk::plan_score(g);
+    e->factor_prec = erxk::factor_precision(g, e->factor_req);
     const size_t L = size_t(e->S) * e->T;
     CU(cudaMalloc(&e->d_stats, L * g.SE * sizeof(double)));
     CU(cudaMalloc(&e->d_prior, L * g.SE * sizeof(double)));
-    CU(cudaMalloc(&e->d_work, L * 2 * size_t(g.Dp) * g.Dp * sizeof(double)));
+    if (e->factor_prec == 0) CU(cudaMalloc(&e->d_work, L * 2 * size_t(g.Dp) * g.Dp * sizeof(double)));
     CU(cudaMalloc(&e->d_white, L * size_t(g.Dp) * g.Dp * sizeof(float)));
     CU(cudaMalloc(&e->d_raw, L * P * sizeof(float)));
     CU(cudaMalloc(&e->d_norm, L * P * sizeof(float)));
@@ -240,10 +245,10 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     });
     timed(e, ERX_KERNEL_FACTOR, [&] {
         erxk::launch_factor(g, e->d_prior, L, e->cfg.epsilon, e->d_work, e->d_white, e->d_status, e->d_latch,
-                            line_base, e->stream);
+                            line_base, e->factor_prec, e->stream);
     });
     timed(e, ERX_KERNEL_SCORE, [&] {
-        erxk::launch_score(g, x, int(n), int(in_stride), e->d_prior, e->d_white, L, raw, e->stream);
+        erxk::launch_score(g, e->sc, x, int(n), int(in_stride), e->d_prior, e->d_white, L, raw, e->stream);
     });
     timed(e, ERX_KERNEL_NORMALIZE, [&] { erxk::launch_normalize(g, raw, L, norm, e->stream); });
     cudaError_t r = cudaGetLastError();
@@ -592,6 +597,26 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
 }
 
 uint64_t erx_launch_count(const erx_engine* e) { return e->launches; }
+
+int erx_set_option(erx_engine* e, int option, int64_t value) {
+    if (option == ERX_OPT_FACTOR_PRECISION) {
+        if (value != 0 && value != 1 && value != 32 && value != 64)
+            return fail(e, ERX_ERR_CONFIG, "factor precision: 0, 1, 32 or 64");
+        e->factor_req = int(value);
+        if (e->d_stats) {
+            const uint32_t P = e->P;
+            e->P = 0;  // force a re-plan with the new precision
+            return configure(e, P);
+        }
+        return ERX_OK;
+    }
+    return fail(e, ERX_ERR_CONFIG, "unknown option");
+}
+
+int64_t erx_get_option(const erx_engine* e, int option) {
+    if (option == ERX_OPT_FACTOR_PRECISION) return e->d_stats ? e->factor_prec : e->factor_req;
+    return -1;
+}
 
 int erx_set_profiling(erx_engine* e, int on) {
     collect_timings(e);

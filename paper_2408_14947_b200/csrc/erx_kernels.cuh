@@ -25,8 +25,6 @@ namespace erxk {
 
 constexpr int kBlk = 8;          // register-block edge (stats / score)
 constexpr int kNB = 32;          // panel width of the blocked factorisation
-constexpr int kScoreTile = 64;   // pixels per score CTA
-constexpr int kScoreStride = kScoreTile + 4;
 
 // Packed lower-triangular index (row-major, j <= i).
 __host__ __device__ inline int tri(int i, int j) { return i * (i + 1) / 2 + j; }
@@ -54,9 +52,22 @@ struct StatsLaunch {
     size_t smem;     // dynamic shared memory bytes
 };
 
+struct ScoreLaunch {
+    int npairs;      // row-block pairs {s, nb-1-s}
+    int G;           // pixel lanes per pair
+    int PT;          // pixels per CTA (4 per lane)
+    int threads;     // CTA size
+    int Dpad;        // smem row stride (floats), = 4 mod 32
+    int tiles;       // CTAs per line
+    size_t smem;
+};
+
 StatsLaunch plan_stats(const Geometry& g);
-size_t score_smem(const Geometry& g);
-size_t factor_smem(const Geometry& g);
+ScoreLaunch plan_score(const Geometry& g);
+// Factor precision actually used for a request (0 auto, 32, 64): 64 / 32 select the
+// shared-memory kernel in that precision, 0 the blocked fp64 global-memory kernel.
+int factor_precision(const Geometry& g, int requested);
+size_t factor_smem(const Geometry& g, int precision);
 
 // Host launchers (erx_kernels.cu).  All asynchronous on `st`.
 void launch_stats(const Geometry& g, const StatsLaunch& sl, const float* x, int n_per_stream, int in_stride,
@@ -66,9 +77,9 @@ void launch_scan(const Geometry& g, const double* stats, double* prior, const do
                  cudaStream_t st);
 // latch: {flag, line, pivot} of the first factorisation failure (sticky until the host clears it).
 void launch_factor(const Geometry& g, const double* prior, int n_lines_total, double eps0, double* work,
-                   float* whiten, int* status, int* latch, int line_base, cudaStream_t st);
-void launch_score(const Geometry& g, const float* x, int n_per_stream, int in_stride, const double* prior,
-                  const float* whiten, int n_lines_total, float* raw, cudaStream_t st);
+                   float* whiten, int* status, int* latch, int line_base, int precision, cudaStream_t st);
+void launch_score(const Geometry& g, const ScoreLaunch& sc, const float* x, int n_per_stream, int in_stride,
+                  const double* prior, const float* whiten, int n_lines_total, float* raw, cudaStream_t st);
 void launch_normalize(const Geometry& g, const float* raw, int n_lines_total, float* norm, cudaStream_t st);
 
 // Measured FP32 FFMA throughput of the current device (TFLOP/s, best of 5).

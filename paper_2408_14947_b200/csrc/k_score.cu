@@ -1,0 +1,181 @@
+// k_score.cu — per-pixel Mahalanobis distance against the pre-update
+// background: delta_i = || W (z_i - mu_{t-1}) ||, W = L^{-1},
+// i.e. forward_substitute_inplace (linalg.hpp:21) done as a whitening
+// multiply; and normalize_scores (detector.hpp:29-32).
+//
+// score: one CTA per (line, pixel tile).  The tile's centred pixels sit in
+// shared memory as rows [pixel][Dpad] (Dpad = 4 mod 32: the 16 pixel lanes of
+// a warp read 16 consecutive rows conflict-free).  Thread (s, q) owns
+// row-block pair {s, nb-1-s} (equal total work, nb+1 block steps) and pixels
+// q + G*p, p < 4; 8x4 fp32 register accumulators; W rows come from L2 with
+// warp-broadcast 128-bit loads.  Partial sums of squares per row block are
+// reduced in a fixed order (bitwise deterministic).
+#include "erx_common.cuh"
+
+namespace erxk {
+namespace {
+
+struct ScoreArgs {
+    Geometry g;
+    ScoreLaunch sc;
+    const float* x;
+    int n;
+    int in_stride;
+    const double* prior;
+    const float* W;
+    float* raw;
+};
+
+__global__ void __launch_bounds__(512) score_kernel(ScoreArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Geometry& g = a.g;
+    const ScoreLaunch& sc = a.sc;
+    const int line = blockIdx.x / sc.tiles;
+    const int tile = blockIdx.x - line * sc.tiles;
+    const int p0 = tile * sc.PT;
+    const int np = min(sc.PT, g.P - p0);
+    const int tid = threadIdx.x, nt = blockDim.x;
+    float* vt = reinterpret_cast<float*>(smem);                    // [PT][Dpad]
+    float* red = vt + size_t(sc.PT) * sc.Dpad;                      // [nb][PT]
+    double* mu = reinterpret_cast<double*>(smem + align_up((size_t(sc.PT) * sc.Dpad + size_t(g.nb) * sc.PT) * 4, 16));
+    const double* pr = a.prior + size_t(line) * g.SE;
+    for (int j = tid; j < g.Dp; j += nt) mu[j] = (j < g.D) ? pr[j] : 0.0;
+    __syncthreads();
+    const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
+    // stage: v = z - mu_{t-1} rounded once to fp32; padding dims / pixels are zero
+    if (!g.srp) {
+        const float* src = xl + size_t(p0) * g.B;
+        for (int i = tid; i < np * g.B; i += nt) {
+            const int pp = i / g.B, b = i - pp * g.B;
+            vt[size_t(pp) * sc.Dpad + b] = float(double(__ldg(src + i)) - mu[b]);
+        }
+    } else {
+        for (int i = tid; i < np * g.D; i += nt) {
+            const int pp = i / g.D, j = i - pp * g.D;
+            vt[size_t(pp) * sc.Dpad + j] = float(srp_z(g, xl + size_t(p0 + pp) * g.B, j) - mu[j]);
+        }
+    }
+    for (int i = tid; i < sc.PT * (g.Dp - g.D); i += nt) {
+        const int pp = i / (g.Dp - g.D), d = g.D + i % (g.Dp - g.D);
+        vt[size_t(pp) * sc.Dpad + d] = 0.f;
+    }
+    for (int i = tid; i < (sc.PT - np) * g.D; i += nt) {
+        const int pp = np + i / g.D, d = i % g.D;
+        vt[size_t(pp) * sc.Dpad + d] = 0.f;
+    }
+    __syncthreads();
+
+    const int s = tid / sc.G;
+    const int q = tid - s * sc.G;
+    const float* Wl = a.W + size_t(line) * g.Dp * g.Dp;
+    if (s < sc.npairs) {
+        for (int h = 0; h < 2; ++h) {
+            const int I = h == 0 ? s : g.nb - 1 - s;
+            if (h == 1 && I == s) break;
+            float acc[kBlk][4];
+#pragma unroll
+            for (int r = 0; r < kBlk; ++r)
+#pragma unroll
+                for (int p = 0; p < 4; ++p) acc[r][p] = 0.f;
+            for (int J = 0; J <= I; ++J) {
+                float vb[kBlk][4];
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    const float* row = vt + size_t(q + sc.G * p) * sc.Dpad + J * kBlk;
+                    const float4 t0 = *reinterpret_cast<const float4*>(row);
+                    const float4 t1 = *reinterpret_cast<const float4*>(row + 4);
+                    vb[0][p] = t0.x;
+                    vb[1][p] = t0.y;
+                    vb[2][p] = t0.z;
+                    vb[3][p] = t0.w;
+                    vb[4][p] = t1.x;
+                    vb[5][p] = t1.y;
+                    vb[6][p] = t1.z;
+                    vb[7][p] = t1.w;
+                }
+#pragma unroll
+                for (int r = 0; r < kBlk; ++r) {
+                    const float4* wr = reinterpret_cast<const float4*>(Wl + size_t(I * kBlk + r) * g.Dp + J * kBlk);
+                    const float4 w0 = __ldg(wr), w1 = __ldg(wr + 1);
+                    const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+                    for (int c = 0; c < kBlk; ++c)
+#pragma unroll
+                        for (int p = 0; p < 4; ++p) acc[r][p] = fmaf(wv[c], vb[c][p], acc[r][p]);
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                float ssq = 0.f;
+#pragma unroll
+                for (int r = 0; r < kBlk; ++r) ssq = fmaf(acc[r][p], acc[r][p], ssq);
+                red[I * sc.PT + q + sc.G * p] = ssq;
+            }
+        }
+    }
+    __syncthreads();
+    for (int pp = tid; pp < np; pp += nt) {
+        float ssq = 0.f;
+        for (int I = 0; I < g.nb; ++I) ssq += red[I * sc.PT + pp];
+        a.raw[size_t(line) * g.P + p0 + pp] = sqrtf(ssq);
+    }
+}
+
+// normalize_scores: per-line z-score, population std, std < 1e-12 -> zeros
+// (detector.hpp:29-32).  One warp per line, fp64.
+__global__ void __launch_bounds__(128) normalize_kernel(int P, const float* __restrict__ raw, int n_lines,
+                                                        float* __restrict__ norm) {
+    const int line = blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (line >= n_lines) return;
+    const float* r = raw + size_t(line) * P;
+    double s = 0.0;
+    for (int i = lane; i < P; i += 32) s += double(r[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const double mean = s / double(P);
+    double v = 0.0;
+    for (int i = lane; i < P; i += 32) {
+        const double d = double(r[i]) - mean;
+        v += d * d;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const double sd = sqrt(v / double(P));
+    float* out = norm + size_t(line) * P;
+    for (int i = lane; i < P; i += 32) out[i] = (sd < 1e-12) ? 0.f : float((double(r[i]) - mean) / sd);
+}
+
+}  // namespace
+
+ScoreLaunch plan_score(const Geometry& g) {
+    ScoreLaunch sc{};
+    sc.npairs = (g.nb + 1) / 2;
+    int rep = 1;
+    while (sc.npairs * 16 * rep * 2 <= 256 && rep < 8) rep *= 2;
+    sc.G = 16 * rep;
+    sc.PT = 4 * sc.G;
+    sc.threads = sc.npairs * sc.G;
+    sc.threads = (sc.threads + 31) / 32 * 32;
+    sc.Dpad = g.Dp + ((4 - g.Dp) % 32 + 32) % 32;  // Dpad = 4 (mod 32)
+    sc.tiles = (g.P + sc.PT - 1) / sc.PT;
+    sc.smem = align_up((size_t(sc.PT) * sc.Dpad + size_t(g.nb) * sc.PT) * 4, 16) + size_t(g.Dp) * 8;
+    return sc;
+}
+
+void launch_score(const Geometry& g, const ScoreLaunch& sc, const float* x, int n_per_stream, int in_stride,
+                  const double* prior, const float* whiten, int n_lines_total, float* raw, cudaStream_t st) {
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        attr_done = true;
+    }
+    ScoreArgs a{g, sc, x, n_per_stream, in_stride, prior, whiten, raw};
+    score_kernel<<<n_lines_total * sc.tiles, sc.threads, sc.smem, st>>>(a);
+}
+
+void launch_normalize(const Geometry& g, const float* raw, int n_lines_total, float* norm, cudaStream_t st) {
+    normalize_kernel<<<(n_lines_total + 3) / 4, 128, 0, st>>>(g.P, raw, n_lines_total, norm);
+}
+
+}  // namespace erxk

@@ -1,0 +1,250 @@
+// k_stats.cu — line_stats (erx.hpp:38-40) for every line of
+// a window, fused with project_line (projection.hpp:31-34).
+//
+// Output slot per line: [mu_hat (D) | K_hat packed lower (D(D+1)/2)], fp64.
+//
+// Work decomposition: the lower triangle of the D x D second-moment matrix is
+// tiled into 8x8 blocks (I >= J); one thread owns one block for a subset of
+// pixels (G pixel groups per block when the triangle is small, several CTAs
+// per line when it is large).  Pixels stream through shared memory in chunks
+// of CH rows, double-buffered with cp.async so the next chunk's HBM read
+// overlaps this chunk's FFMA work.
+//
+// Precision (SURVEY.md §7 study, reproduced in DESIGN.md): v = z - c with c
+// the fp64 mean of the line's first min(32, P) pixels, rounded once to fp32;
+// products accumulate in fp32 within a chunk and the chunk sums in a second
+// fp32 level; the exact line mean is restored in fp64:
+//   mu_hat = c + sum(v)/P,  K_hat = (S - sum(v) sum(v)^T / P) / (P - 1).
+#include "erx_common.cuh"
+
+namespace erxk {
+namespace {
+
+struct StatsArgs {
+    Geometry g;
+    StatsLaunch sl;
+    const float* x;
+    int n;
+    int in_stride;
+    double* stats;
+};
+
+__global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Geometry& g = a.g;
+    const StatsLaunch& sl = a.sl;
+    const int line = blockIdx.x / sl.cpl;
+    const int cta = blockIdx.x - line * sl.cpl;
+    const int tid = threadIdx.x;
+    const int nt = blockDim.x;
+
+    const size_t buf_floats = size_t(sl.CH) * g.Dp;
+    float* vbuf0 = reinterpret_cast<float*>(smem);
+    size_t off = align_up(2 * buf_floats * 4, 16);
+    const size_t red_bytes = (sl.G > 1) ? size_t(128) * 64 * 8 : 0;
+    off = off > red_bytes ? off : red_bytes;
+    double* cen = reinterpret_cast<double*>(smem + off);
+    double* colsum = cen + g.Dp;
+    double* red = reinterpret_cast<double*>(smem);  // aliases the chunk buffers after the loop
+
+    const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
+
+    const int q_local = tid / sl.G;
+    const int grp = tid - q_local * sl.G;
+    const int q = cta * sl.npc + q_local;
+    const bool active = (q_local < sl.npc) && (q < sl.n_pairs);
+    int I = 0, J = 0;
+    if (active) {  // column-major enumeration of the lower triangle of blocks
+        int rem = q;
+        while (rem >= g.nb - J) {
+            rem -= g.nb - J;
+            ++J;
+        }
+        I = J + rem;
+    }
+
+    // padded dims [D, Dp) stay zero in both buffers
+    if (g.Dp > g.D)
+        for (int i = tid; i < 2 * sl.CH * (g.Dp - g.D); i += nt) {
+            const int r = i / (g.Dp - g.D), c = g.D + i % (g.Dp - g.D);
+            vbuf0[size_t(r) * g.Dp + c] = 0.f;
+        }
+    // centre c: fp64 mean of the first min(32, P) projected pixels
+    {
+        const int n0 = min(32, g.P);
+        for (int j = tid; j < g.D; j += nt) {
+            double s = 0.0;
+            for (int pp = 0; pp < n0; ++pp) s += proj(g, xl + size_t(pp) * g.B, j);
+            cen[j] = s / double(n0);
+        }
+    }
+
+    const bool use_async = !g.srp && (g.B % 4 == 0);
+    const int nchunks = (g.P + sl.CH - 1) / sl.CH;
+    auto issue = [&](int c) {
+        const int c0 = c * sl.CH, n = min(sl.CH, g.P - c0);
+        float* dst = vbuf0 + (c & 1) * buf_floats;
+        const int q4 = g.B / 4;
+        const float* src = xl + size_t(c0) * g.B;
+        for (int i = tid; i < n * q4; i += nt) {
+            const int pp = i / q4, k = i - pp * q4;
+            cp_async16(dst + size_t(pp) * g.Dp + 4 * k, src + size_t(pp) * g.B + 4 * k);
+        }
+        cp_async_commit();
+    };
+    if (use_async) issue(0);
+    __syncthreads();  // cen visible
+
+    float acc2[kBlk][kBlk];
+#pragma unroll
+    for (int r = 0; r < kBlk; ++r)
+#pragma unroll
+        for (int c = 0; c < kBlk; ++c) acc2[r][c] = 0.f;
+    double cs[4] = {0.0, 0.0, 0.0, 0.0};
+
+    for (int c = 0; c < nchunks; ++c) {
+        const int c0 = c * sl.CH, n = min(sl.CH, g.P - c0);
+        float* v = vbuf0 + (c & 1) * buf_floats;
+        if (use_async) {
+            if (c + 1 < nchunks) {
+                issue(c + 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+            // centre in place and take the column sums (one thread per dim; fp32 per chunk)
+            for (int k = 0; k < 4; ++k) {
+                const int j = tid + k * nt;
+                if (j < g.D) {
+                    const double cj = cen[j];
+                    float s = 0.f;
+                    for (int pp = 0; pp < n; ++pp) {
+                        const float val = float(double(v[size_t(pp) * g.Dp + j]) - cj);
+                        v[size_t(pp) * g.Dp + j] = val;
+                        s += val;
+                    }
+                    cs[k] += double(s);
+                }
+            }
+        } else {
+            for (int i = tid; i < n * g.D; i += nt) {
+                const int pp = i / g.D, j = i - pp * g.D;
+                v[size_t(pp) * g.Dp + j] = float(proj(g, xl + size_t(c0 + pp) * g.B, j) - cen[j]);
+            }
+            __syncthreads();
+            for (int k = 0; k < 4; ++k) {
+                const int j = tid + k * nt;
+                if (j < g.D) {
+                    float s = 0.f;
+                    for (int pp = 0; pp < n; ++pp) s += v[size_t(pp) * g.Dp + j];
+                    cs[k] += double(s);
+                }
+            }
+        }
+        __syncthreads();
+        if (active) {
+            float acc[kBlk][kBlk];
+#pragma unroll
+            for (int r = 0; r < kBlk; ++r)
+#pragma unroll
+                for (int cc = 0; cc < kBlk; ++cc) acc[r][cc] = 0.f;
+            const float* va = v + I * kBlk;
+            const float* vb = v + J * kBlk;
+#pragma unroll 2
+            for (int pp = grp; pp < n; pp += sl.G) {
+                const float4 a0 = *reinterpret_cast<const float4*>(va + size_t(pp) * g.Dp);
+                const float4 a1 = *reinterpret_cast<const float4*>(va + size_t(pp) * g.Dp + 4);
+                const float4 b0 = *reinterpret_cast<const float4*>(vb + size_t(pp) * g.Dp);
+                const float4 b1 = *reinterpret_cast<const float4*>(vb + size_t(pp) * g.Dp + 4);
+                const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+                for (int r = 0; r < kBlk; ++r)
+#pragma unroll
+                    for (int cc = 0; cc < kBlk; ++cc) acc[r][cc] = fmaf(av[r], bv[cc], acc[r][cc]);
+            }
+#pragma unroll
+            for (int r = 0; r < kBlk; ++r)
+#pragma unroll
+                for (int cc = 0; cc < kBlk; ++cc) acc2[r][cc] += acc[r][cc];
+        }
+        __syncthreads();  // buffer (c & 1) is reissued at iteration c + 1
+    }
+
+    for (int k = 0; k < 4; ++k) {
+        const int j = tid + k * nt;
+        if (j < g.D) colsum[j] = cs[k];
+    }
+    if (sl.G > 1) {
+#pragma unroll
+        for (int r = 0; r < kBlk; ++r)
+#pragma unroll
+            for (int cc = 0; cc < kBlk; ++cc) red[tid * 64 + r * 8 + cc] = double(acc2[r][cc]);
+    }
+    __syncthreads();
+
+    double* out = a.stats + size_t(line) * g.SE;
+    const double P = double(g.P);
+    if (cta == 0)
+        for (int j = tid; j < g.D; j += nt) out[j] = cen[j] + colsum[j] / P;
+    if (active && grp == 0) {
+#pragma unroll
+        for (int r = 0; r < kBlk; ++r) {
+            const int ai = I * kBlk + r;
+#pragma unroll
+            for (int cc = 0; cc < kBlk; ++cc) {
+                const int bj = J * kBlk + cc;
+                if (ai < g.D && bj <= ai) {
+                    double s;
+                    if (sl.G > 1) {
+                        s = 0.0;
+                        for (int gg = 0; gg < sl.G; ++gg) s += red[(q_local * sl.G + gg) * 64 + r * 8 + cc];
+                    } else {
+                        s = double(acc2[r][cc]);
+                    }
+                    out[g.D + tri(ai, bj)] = (s - colsum[ai] * colsum[bj] / P) / (P - 1.0);
+                }
+            }
+        }
+    }
+}
+
+}  // namespace
+
+StatsLaunch plan_stats(const Geometry& g) {
+    StatsLaunch sl{};
+    sl.n_pairs = g.nb * (g.nb + 1) / 2;
+    if (sl.n_pairs <= 64) {
+        sl.G = 128 / sl.n_pairs;
+        sl.npc = sl.n_pairs;
+        sl.cpl = 1;
+    } else {
+        sl.G = 1;
+        sl.npc = 128;
+        sl.cpl = (sl.n_pairs + 127) / 128;
+    }
+    const size_t per_px = size_t(g.Dp) * 4 * 2;  // double buffered
+    int ch = 64;
+    if (sl.G > 1) ch = 256;
+    while (ch > 16 && size_t(ch) * per_px > 120 * 1024) ch /= 2;
+    sl.CH = ch;
+    size_t off = align_up(size_t(ch) * per_px, 16);
+    const size_t red_bytes = (sl.G > 1) ? size_t(128) * 64 * 8 : 0;
+    off = off > red_bytes ? off : red_bytes;
+    sl.smem = off + 2 * size_t(g.Dp) * 8;
+    return sl;
+}
+
+void launch_stats(const Geometry& g, const StatsLaunch& sl, const float* x, int n_per_stream, int in_stride,
+                  int n_lines_total, double* stats, cudaStream_t st) {
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaFuncSetAttribute(stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_done = true;
+    }
+    StatsArgs a{g, sl, x, n_per_stream, in_stride, stats};
+    stats_kernel<<<n_lines_total * sl.cpl, 128, sl.smem, st>>>(a);
+}
+
+}  // namespace erxk

@@ -239,6 +239,13 @@ class Engine:
         self._check(self._lib.erx_set_state(self._h, stream, _p(mu, C.c_double), _p(cov, C.c_double), lines_seen,
                                             welford_n))
 
+    def set_factor_precision(self, bits: int):
+        """0 auto, 32 or 64 (see ERX_OPT_FACTOR_PRECISION in include/erx_b200.h)."""
+        self._check(self._lib.erx_set_option(self._h, L.OPT_FACTOR_PRECISION, bits))
+
+    def factor_precision(self) -> int:
+        return int(self._lib.erx_get_option(self._h, L.OPT_FACTOR_PRECISION))
+
     # instrumentation
     def launch_count(self) -> int:
         return int(self._lib.erx_launch_count(self._h))

@@ -189,6 +189,26 @@ def test_config4_subset(pkg, oracle, no_srp):
                overrides={"scene_change_line": [20, 40]}, window=16)
 
 
+@pytest.mark.parametrize("cid,n_lines", [(0, 240), (1, 120)])
+@pytest.mark.parametrize("prec", [64, 32, 1])
+def test_factor_kernel_variants(pkg, oracle, cid, n_lines, prec):
+    """Every factor path (fp64 / fp32 shared-memory, blocked fp64 global) meets the gates."""
+    spec = pkg.gen_spec(cid)
+    lines, mask = pkg.gen_lines(spec, 0, n_lines)
+    alpha = 0.1 if cid == 0 else 0.05
+    cfg = pkg.ErxConfig(no_srp=True, alpha=alpha, buffer_len=n_lines // 3)
+    eng = pkg.Engine(cfg, spec.bands, window_lines=32)
+    eng.set_factor_precision(prec)
+    eng.push(lines[None], 0)
+    eng.finish()
+    want = {64: 64 if cid == 0 else 0, 32: 32, 1: 0}[prec]  # fp64 D=224 does not fit smem -> blocked
+    assert eng.factor_precision() == want
+    _, wu, raw_g, norm_g = eng.pop()
+    raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), lines)
+    warm = np.broadcast_to(wu[:, None], raw_o.shape)
+    check_gates(oracle, raw_g[0], norm_g[0], raw_o, norm_o, mask=mask, warm=warm, label=f"c{cid} factor{prec}")
+
+
 # ---------------------------------------------------------------- contract edges
 def test_state_matches_oracle(pkg, oracle):
     spec = pkg.gen_spec(0)
