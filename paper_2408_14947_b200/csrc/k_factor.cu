@@ -283,6 +283,93 @@ __global__ void __launch_bounds__(256) factor_smem_kernel(Geometry g, const doub
     if (tid == 0) status[line] = -1;
 }
 
+// ---------------------------------------------------------------------------
+// one warp per line (D <= kWarpFactorMaxD): no block barriers at all.  Lanes
+// own whole rows, so every step is __syncwarp-ordered and the inner loops run
+// over independent elements (ILP); a row pair {r, 63-r} per lane and round
+// balances the shrinking triangle of the Cholesky update.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(32) factor_warp_kernel(Geometry g, const double* __restrict__ prior, double eps0,
+                                                         float* __restrict__ whiten, int* __restrict__ status,
+                                                         int* __restrict__ latch, int line_base) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    T* A = reinterpret_cast<T*>(smem);
+    const int D = g.D, LD = D + 1;
+    const int line = blockIdx.x, lane = threadIdx.x;
+    const double* K = prior + size_t(line) * g.SE + D;
+    double eps = eps0;
+    int fail;
+    while (true) {
+        for (int i = 0; i < D; ++i)
+            for (int j = lane; j <= i; j += 32) A[i * LD + j] = T(K[tri(i, j)] + (i == j ? eps : 0.0));
+        __syncwarp();
+        fail = -1;
+        for (int j = 0; j < D; ++j) {
+            const T djj = A[j * LD + j];
+            if (!(djj > T(0))) {
+                fail = j;
+                break;
+            }
+            const T s = sqrt(djj);
+            for (int i = j + 1 + lane; i < D; i += 32) A[i * LD + j] /= s;
+            __syncwarp();
+            if (lane == 0) A[j * LD + j] = s;
+            const T* colj = A + j;
+            const int n = D - j - 1;
+            for (int base = 0; base < n; base += 64) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int r = base + (h == 0 ? lane : 63 - lane);
+                    if (r >= n) continue;
+                    const int i = j + 1 + r;
+                    T* rowi = A + i * LD;
+                    const T lij = rowi[j];
+#pragma unroll 4
+                    for (int k = j + 1; k <= i; ++k) rowi[k] -= lij * colj[k * LD];
+                }
+            }
+            __syncwarp();
+        }
+        if (fail < 0) break;
+        const double next = eps * 10.0;
+        if (!(next <= 1e-1 * (1.0 + 1e-9))) break;
+        eps = next;
+        __syncwarp();
+    }
+    if (fail >= 0) {
+        if (lane == 0) {
+            status[line] = fail;
+            if (atomicCAS(latch, 0, 1) == 0) {
+                latch[1] = line_base + line;
+                latch[2] = fail;
+            }
+        }
+        return;
+    }
+    // in-place inverse, right-looking by rows (see factor_smem_kernel); lane = row
+    for (int k = 0; k < D; ++k) {
+        const T inv = T(1) / A[k * LD + k];
+        __syncwarp();
+        for (int c = lane; c < k; c += 32) A[k * LD + c] *= inv;
+        if (lane == 0) A[k * LD + k] = inv;
+        __syncwarp();
+        const T* rowk = A + k * LD;
+        for (int i = k + 1 + lane; i < D; i += 32) {
+            T* rowi = A + i * LD;
+            const T l = rowi[k];
+            rowi[k] = -l * inv;
+#pragma unroll 4
+            for (int c = 0; c < k; ++c) rowi[c] -= l * rowk[c];
+        }
+        __syncwarp();
+    }
+    float* W = whiten + size_t(line) * g.Dp * g.Dp;
+    for (int i = 0; i < g.Dp; ++i)
+        for (int j = lane; j < g.Dp; j += 32) W[size_t(i) * g.Dp + j] = (i < D && j <= i) ? float(A[i * LD + j]) : 0.f;
+    if (lane == 0) status[line] = -1;
+}
+
 }  // namespace
 
 size_t factor_smem(const Geometry& g, int precision) {
@@ -309,7 +396,17 @@ int factor_precision(const Geometry& g, int requested) {
 void launch_factor(const Geometry& g, const double* prior, int n_lines_total, double eps0, double* work,
                    float* whiten, int* status, int* latch, int line_base, int precision, cudaStream_t st) {
     const size_t sm = factor_smem(g, precision);
-    if (precision == 64) {
+    if ((precision == 64 || precision == 32) && g.D <= kWarpFactorMaxD) {
+        if (precision == 64) {
+            cudaFuncSetAttribute(factor_warp_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            factor_warp_kernel<double><<<n_lines_total, 32, sm, st>>>(g, prior, eps0, whiten, status, latch,
+                                                                       line_base);
+        } else {
+            cudaFuncSetAttribute(factor_warp_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            factor_warp_kernel<float><<<n_lines_total, 32, sm, st>>>(g, prior, eps0, whiten, status, latch,
+                                                                      line_base);
+        }
+    } else if (precision == 64) {
         cudaFuncSetAttribute(factor_smem_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         factor_smem_kernel<double><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base);
     } else if (precision == 32) {

@@ -20,6 +20,11 @@
 namespace erxk {
 namespace {
 
+// Position of dim d inside a staged pixel row: the 8-blocks' low halves first,
+// then their high halves, so the warps' 16-byte reads of distinct blocks hit
+// distinct banks.
+__device__ __forceinline__ int spos(int d, int nb) { return ((((d >> 2) & 1) * nb) + (d >> 3)) * 4 + (d & 3); }
+
 struct StatsArgs {
     Geometry g;
     StatsLaunch sl;
@@ -67,7 +72,7 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
     if (g.Dp > g.D)
         for (int i = tid; i < 2 * sl.CH * (g.Dp - g.D); i += nt) {
             const int r = i / (g.Dp - g.D), c = g.D + i % (g.Dp - g.D);
-            vbuf0[size_t(r) * g.Dp + c] = 0.f;
+            vbuf0[size_t(r) * g.Dp + spos(c, g.nb)] = 0.f;
         }
     // centre c: fp64 mean of the first min(32, P) projected pixels
     {
@@ -88,7 +93,7 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
         const float* src = xl + size_t(c0) * g.B;
         for (int i = tid; i < n * q4; i += nt) {
             const int pp = i / q4, k = i - pp * q4;
-            cp_async16(dst + size_t(pp) * g.Dp + 4 * k, src + size_t(pp) * g.B + 4 * k);
+            cp_async16(dst + size_t(pp) * g.Dp + ((k & 1) * g.nb + (k >> 1)) * 4, src + size_t(pp) * g.B + 4 * k);
         }
         cp_async_commit();
     };
@@ -118,10 +123,11 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
                 const int j = tid + k * nt;
                 if (j < g.D) {
                     const double cj = cen[j];
+                    const int pj = spos(j, g.nb);
                     float s = 0.f;
                     for (int pp = 0; pp < n; ++pp) {
-                        const float val = float(double(v[size_t(pp) * g.Dp + j]) - cj);
-                        v[size_t(pp) * g.Dp + j] = val;
+                        const float val = float(double(v[size_t(pp) * g.Dp + pj]) - cj);
+                        v[size_t(pp) * g.Dp + pj] = val;
                         s += val;
                     }
                     cs[k] += double(s);
@@ -130,14 +136,15 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
         } else {
             for (int i = tid; i < n * g.D; i += nt) {
                 const int pp = i / g.D, j = i - pp * g.D;
-                v[size_t(pp) * g.Dp + j] = float(proj(g, xl + size_t(c0 + pp) * g.B, j) - cen[j]);
+                v[size_t(pp) * g.Dp + spos(j, g.nb)] = float(proj(g, xl + size_t(c0 + pp) * g.B, j) - cen[j]);
             }
             __syncthreads();
             for (int k = 0; k < 4; ++k) {
                 const int j = tid + k * nt;
                 if (j < g.D) {
                     float s = 0.f;
-                    for (int pp = 0; pp < n; ++pp) s += v[size_t(pp) * g.Dp + j];
+                    const int pj = spos(j, g.nb);
+                    for (int pp = 0; pp < n; ++pp) s += v[size_t(pp) * g.Dp + pj];
                     cs[k] += double(s);
                 }
             }
@@ -149,14 +156,18 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
             for (int r = 0; r < kBlk; ++r)
 #pragma unroll
                 for (int cc = 0; cc < kBlk; ++cc) acc[r][cc] = 0.f;
-            const float* va = v + I * kBlk;
-            const float* vb = v + J * kBlk;
+            // swizzled rows: low halves of all 8-blocks, then high halves (conflict-free 128-bit reads)
+            const float* va0 = v + I * 4;
+            const float* va1 = v + (g.nb + I) * 4;
+            const float* vb0 = v + J * 4;
+            const float* vb1 = v + (g.nb + J) * 4;
 #pragma unroll 2
             for (int pp = grp; pp < n; pp += sl.G) {
-                const float4 a0 = *reinterpret_cast<const float4*>(va + size_t(pp) * g.Dp);
-                const float4 a1 = *reinterpret_cast<const float4*>(va + size_t(pp) * g.Dp + 4);
-                const float4 b0 = *reinterpret_cast<const float4*>(vb + size_t(pp) * g.Dp);
-                const float4 b1 = *reinterpret_cast<const float4*>(vb + size_t(pp) * g.Dp + 4);
+                const size_t o = size_t(pp) * g.Dp;
+                const float4 a0 = *reinterpret_cast<const float4*>(va0 + o);
+                const float4 a1 = *reinterpret_cast<const float4*>(va1 + o);
+                const float4 b0 = *reinterpret_cast<const float4*>(vb0 + o);
+                const float4 b1 = *reinterpret_cast<const float4*>(vb1 + o);
                 const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
                 const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
