@@ -138,11 +138,13 @@ def run_ours(args):
         dist.init_process_group("nccl")
     cid = args.config
     cfgd = CONFIGS[cid]
+    from paper_2408_14947_b200.sharding import max_over_ranks, shard_streams
+
     S_tot = cfgd["streams"]
     if S_tot % world:
-        raise SystemExit(f"{S_tot} streams do not shard over {world} ranks")
-    S = S_tot // world
-    my_streams = list(range(rank * S, (rank + 1) * S))
+        raise SystemExit(f"{S_tot} streams do not shard evenly over {world} ranks")
+    my_streams = list(shard_streams(S_tot, world, rank))
+    S = len(my_streams)
     P, B = cfgd["pixels"], cfgd["bands"]
     no_srp = args.mode == "full"
     cfg = pkg.ErxConfig(no_srp=no_srp, alpha=cfgd["alpha"])
@@ -182,10 +184,7 @@ def run_ours(args):
     eng.sync()
     launches = eng.launch_count() - launches0
     torch.cuda.synchronize()
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
-    if dist:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+    ms_max = max_over_ranks(ms, dist, device=f"cuda:{local}")
     lines_total = S_tot * T * args.steps
     value = lines_total / (ms_max / 1e3)
 

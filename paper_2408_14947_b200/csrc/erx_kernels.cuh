@@ -25,7 +25,6 @@ namespace erxk {
 
 constexpr int kBlk = 8;          // register-block edge (stats / score)
 constexpr int kNB = 32;          // panel width of the blocked factorisation
-constexpr int kWarpFactorMaxD = 128;  // one warp per line up to this D (else one CTA per line)
 
 // Packed lower-triangular index (row-major, j <= i).
 __host__ __device__ inline int tri(int i, int j) { return i * (i + 1) / 2 + j; }

@@ -4,13 +4,14 @@
 // the whitening multiply of the score kernel.  A failing pivot is reported
 // per line (status) and latched for the device-resident path (latch).
 //
-// Two kernels, one CTA per line, chosen by the matrix size:
-//   factor_smem_kernel<T>   the whole matrix in shared memory (T = double
-//                            while D(D+1)*8 fits, float up to D = 233):
-//                            right-looking Cholesky then an in-place
-//                            right-looking triangular inverse;
-//   factor_global_kernel     blocked (panel 32) fp64 over an L2-resident
-//                            global workspace for larger D.
+// Three kernels, one CTA per line (ERX_OPT_FACTOR_PRECISION picks):
+//   factor_blk_kernel (32, default while it fits: D <= 233)  fp32, whole
+//       matrix in shared memory, 8x8 register-tiled blocked Cholesky and
+//       in-place blocked inverse;
+//   factor_smem_kernel<double> (64, D <= 165)  fp64 scalar right-looking
+//       Cholesky + in-place inverse in shared memory;
+//   factor_global_kernel (1, and any D beyond the above)  blocked (panel 32)
+//       fp64 over an L2-resident global workspace.
 #include <algorithm>
 
 #include "erx_common.cuh"
@@ -284,61 +285,118 @@ __global__ void __launch_bounds__(256) factor_smem_kernel(Geometry g, const doub
 }
 
 // ---------------------------------------------------------------------------
-// one warp per line (D <= kWarpFactorMaxD): no block barriers at all.  Lanes
-// own whole rows, so every step is __syncwarp-ordered and the inner loops run
-// over independent elements (ILP); a row pair {r, 63-r} per lane and round
-// balances the shrinking triangle of the Cholesky update.
+// fp32 blocked factorisation in shared memory (default for D <= 233): the
+// same 8x8 block grid as the stats / score kernels.  Cholesky: per block
+// column k, one warp factors the 8x8 diagonal block, the panel below is
+// solved row-parallel, and the trailing update runs one 8x8 block pair per
+// thread with register tiles (0.4 shared-memory accesses per FMA instead of
+// 3).  The inverse is computed in place by block rows with the same tiles.
+// ~7 barriers per block step instead of 5 per scalar step.
 // ---------------------------------------------------------------------------
-template <typename T>
-__global__ void __launch_bounds__(32) factor_warp_kernel(Geometry g, const double* __restrict__ prior, double eps0,
+__device__ __forceinline__ void ld8(const float* p, float* v) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void st8(float* p, const float* v) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+__global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const double* __restrict__ prior, double eps0,
                                                          float* __restrict__ whiten, int* __restrict__ status,
                                                          int* __restrict__ latch, int line_base) {
     extern __shared__ __align__(16) unsigned char smem[];
-    T* A = reinterpret_cast<T*>(smem);
-    const int D = g.D, LD = D + 1;
-    const int line = blockIdx.x, lane = threadIdx.x;
+    __shared__ int s_fail;
+    const int D = g.D, Dp = g.Dp, nb = g.nb, LD = Dp + 4;
+    float* A = reinterpret_cast<float*>(smem);  // [Dp][LD]; padding dims carry an identity block
+    float* Lc = A + size_t(Dp) * LD;            // [nb][64]: copy of a block column (inverse)
+    float* Dinv = Lc + size_t(nb) * 64;         // [64]: inverse of a diagonal block
+    const int line = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
     const double* K = prior + size_t(line) * g.SE + D;
     double eps = eps0;
     int fail;
     while (true) {
-        for (int i = 0; i < D; ++i)
-            for (int j = lane; j <= i; j += 32) A[i * LD + j] = T(K[tri(i, j)] + (i == j ? eps : 0.0));
-        __syncwarp();
-        fail = -1;
-        for (int j = 0; j < D; ++j) {
-            const T djj = A[j * LD + j];
-            if (!(djj > T(0))) {
-                fail = j;
-                break;
-            }
-            const T s = sqrt(djj);
-            for (int i = j + 1 + lane; i < D; i += 32) A[i * LD + j] /= s;
-            __syncwarp();
-            if (lane == 0) A[j * LD + j] = s;
-            const T* colj = A + j;
-            const int n = D - j - 1;
-            for (int base = 0; base < n; base += 64) {
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int r = base + (h == 0 ? lane : 63 - lane);
-                    if (r >= n) continue;
-                    const int i = j + 1 + r;
-                    T* rowi = A + i * LD;
-                    const T lij = rowi[j];
-#pragma unroll 4
-                    for (int k = j + 1; k <= i; ++k) rowi[k] -= lij * colj[k * LD];
+        for (int i = warp; i < Dp; i += nw)
+            for (int j = lane; j <= i; j += 32)
+                A[i * LD + j] = (i < D) ? float(K[tri(i, j)] + (i == j ? eps : 0.0)) : (i == j ? 1.f : 0.f);
+        if (tid == 0) s_fail = -1;
+        __syncthreads();
+        for (int k = 0; k < nb; ++k) {
+            const int k0 = k * kBlk;
+            float* Bk = A + k0 * LD + k0;
+            if (warp == 0) {  // (a) diagonal block, lanes 0..7 own its rows
+                for (int j = 0; j < kBlk; ++j) {
+                    __syncwarp();
+                    const float djj = Bk[j * LD + j];
+                    if (!(djj > 0.f)) {
+                        if (lane == 0) s_fail = k0 + j;
+                        break;
+                    }
+                    const float s = sqrtf(djj);
+                    __syncwarp();
+                    if (lane > j && lane < kBlk) Bk[lane * LD + j] /= s;
+                    __syncwarp();
+                    if (lane == j) Bk[j * LD + j] = s;
+                    if (lane > j && lane < kBlk) {
+                        const float l = Bk[lane * LD + j];
+                        for (int c = j + 1; c <= lane; ++c) Bk[lane * LD + c] -= l * Bk[c * LD + j];
+                    }
                 }
             }
-            __syncwarp();
+            __syncthreads();
+            if (s_fail >= 0) break;
+            // (b) panel: L_Ik = A_Ik L_kk^{-T}, one row per thread
+            for (int i = k0 + kBlk + tid; i < Dp; i += nt) {
+                float* row = A + i * LD + k0;
+                float a[kBlk], x[kBlk];
+                ld8(row, a);
+#pragma unroll
+                for (int c = 0; c < kBlk; ++c) {
+                    float s = a[c];
+#pragma unroll
+                    for (int l = 0; l < c; ++l) s -= x[l] * Bk[c * LD + l];
+                    x[c] = s / Bk[c * LD + c];
+                }
+                st8(row, x);
+            }
+            __syncthreads();
+            // (c) trailing update A_IJ -= L_Ik L_Jk^T, k < J <= I < nb
+            const int m = nb - k - 1;
+            const int npairs = m * (m + 1) / 2;
+            for (int q = tid; q < npairs; q += nt) {
+                int Ir = int((sqrtf(8.f * q + 1.f) - 1.f) * 0.5f);
+                while (Ir * (Ir + 1) / 2 > q) --Ir;
+                while ((Ir + 1) * (Ir + 2) / 2 <= q) ++Ir;
+                const int I = k + 1 + Ir, J = k + 1 + (q - Ir * (Ir + 1) / 2);
+                float b[kBlk][kBlk];
+#pragma unroll
+                for (int c = 0; c < kBlk; ++c) ld8(A + (J * kBlk + c) * LD + k0, b[c]);
+#pragma unroll
+                for (int r = 0; r < kBlk; ++r) {
+                    float a[kBlk], acc[kBlk];
+                    ld8(A + (I * kBlk + r) * LD + k0, a);
+                    ld8(A + (I * kBlk + r) * LD + J * kBlk, acc);
+#pragma unroll
+                    for (int c = 0; c < kBlk; ++c)
+#pragma unroll
+                        for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], b[c][l], acc[c]);
+                    st8(A + (I * kBlk + r) * LD + J * kBlk, acc);
+                }
+            }
+            __syncthreads();
         }
+        fail = s_fail;
         if (fail < 0) break;
         const double next = eps * 10.0;
         if (!(next <= 1e-1 * (1.0 + 1e-9))) break;
         eps = next;
-        __syncwarp();
+        __syncthreads();
     }
     if (fail >= 0) {
-        if (lane == 0) {
+        if (tid == 0) {
             status[line] = fail;
             if (atomicCAS(latch, 0, 1) == 0) {
                 latch[1] = line_base + line;
@@ -347,34 +405,95 @@ __global__ void __launch_bounds__(32) factor_warp_kernel(Geometry g, const doubl
         }
         return;
     }
-    // in-place inverse, right-looking by rows (see factor_smem_kernel); lane = row
-    for (int k = 0; k < D; ++k) {
-        const T inv = T(1) / A[k * LD + k];
-        __syncwarp();
-        for (int c = lane; c < k; c += 32) A[k * LD + c] *= inv;
-        if (lane == 0) A[k * LD + k] = inv;
-        __syncwarp();
-        const T* rowk = A + k * LD;
-        for (int i = k + 1 + lane; i < D; i += 32) {
-            T* rowi = A + i * LD;
-            const T l = rowi[k];
-            rowi[k] = -l * inv;
-#pragma unroll 4
-            for (int c = 0; c < k; ++c) rowi[c] -= l * rowk[c];
+    // In-place inverse by block rows.  Before step k, block (I, J), I > k,
+    // J < k, holds T_IJ = -sum_{m<k} L_Im X_mJ; block (I, J >= k) still holds L.
+    for (int k = 0; k < nb; ++k) {
+        const int k0 = k * kBlk;
+        const float* Bk = A + k0 * LD + k0;
+        if (warp == 0 && lane < kBlk) {  // Dinv = L_kk^{-1}, lane = column
+            float x[kBlk];
+#pragma unroll
+            for (int r = 0; r < kBlk; ++r) {
+                float s = (r == lane) ? 1.f : 0.f;
+#pragma unroll
+                for (int l = 0; l < r; ++l) s -= Bk[r * LD + l] * x[l];
+                x[r] = (r < lane) ? 0.f : s / Bk[r * LD + r];
+            }
+#pragma unroll
+            for (int r = 0; r < kBlk; ++r) Dinv[r * kBlk + lane] = x[r];
         }
-        __syncwarp();
+        for (int idx = tid; idx < (nb - k - 1) * 64; idx += nt) {
+            const int I = k + 1 + idx / 64, rc = idx % 64;
+            Lc[I * 64 + rc] = A[(I * kBlk + rc / kBlk) * LD + k0 + rc % kBlk];
+        }
+        __syncthreads();
+        // finalise block row k: X_kJ = Dinv T_kJ (J < k), X_kk = Dinv
+        for (int J = tid; J <= k; J += nt) {
+            float t[kBlk][kBlk];
+            if (J == k) {
+#pragma unroll
+                for (int r = 0; r < kBlk; ++r) ld8(Dinv + r * kBlk, t[r]);
+            } else {
+                float s[kBlk][kBlk];
+#pragma unroll
+                for (int r = 0; r < kBlk; ++r) ld8(A + (k0 + r) * LD + J * kBlk, s[r]);
+#pragma unroll
+                for (int r = 0; r < kBlk; ++r)
+#pragma unroll
+                    for (int c = 0; c < kBlk; ++c) {
+                        float v = 0.f;
+#pragma unroll
+                        for (int l = 0; l <= r; ++l) v = fmaf(Dinv[r * kBlk + l], s[l][c], v);
+                        t[r][c] = v;
+                    }
+            }
+#pragma unroll
+            for (int r = 0; r < kBlk; ++r) st8(A + (k0 + r) * LD + J * kBlk, t[r]);
+        }
+        __syncthreads();
+        // update block rows I > k: T_IJ -= L_Ik X_kJ (J < k), T_Ik = -L_Ik X_kk
+        const int ntask = (nb - k - 1) * (k + 1);
+        for (int q = tid; q < ntask; q += nt) {
+            const int I = k + 1 + q / (k + 1), J = q % (k + 1);
+            float xk[kBlk][kBlk];
+#pragma unroll
+            for (int l = 0; l < kBlk; ++l) ld8(A + (k0 + l) * LD + J * kBlk, xk[l]);
+#pragma unroll
+            for (int r = 0; r < kBlk; ++r) {
+                float a[kBlk], acc[kBlk];
+                ld8(Lc + I * 64 + r * kBlk, a);
+                if (J == k) {
+#pragma unroll
+                    for (int c = 0; c < kBlk; ++c) acc[c] = 0.f;
+                } else {
+                    ld8(A + (I * kBlk + r) * LD + J * kBlk, acc);
+                }
+#pragma unroll
+                for (int c = 0; c < kBlk; ++c)
+#pragma unroll
+                    for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], xk[l][c], acc[c]);
+                st8(A + (I * kBlk + r) * LD + J * kBlk, acc);
+            }
+        }
+        __syncthreads();
     }
-    float* W = whiten + size_t(line) * g.Dp * g.Dp;
-    for (int i = 0; i < g.Dp; ++i)
-        for (int j = lane; j < g.Dp; j += 32) W[size_t(i) * g.Dp + j] = (i < D && j <= i) ? float(A[i * LD + j]) : 0.f;
-    if (lane == 0) status[line] = -1;
+    float* W = whiten + size_t(line) * Dp * Dp;
+    for (int idx = tid; idx < Dp * Dp; idx += nt) {
+        const int i = idx / Dp, j = idx - i * Dp;
+        W[idx] = (i < D && j <= i) ? A[i * LD + j] : 0.f;
+    }
+    if (tid == 0) status[line] = -1;
 }
 
 }  // namespace
 
+size_t factor_blk_smem(const Geometry& g) {
+    return size_t(g.Dp) * (g.Dp + 4) * 4 + size_t(g.nb) * 64 * 4 + 64 * 4;
+}
+
 size_t factor_smem(const Geometry& g, int precision) {
     if (precision == 64) return size_t(g.D) * (g.D + 1) * 8;
-    if (precision == 32) return size_t(g.D) * (g.D + 1) * 4;
+    if (precision == 32) return factor_blk_smem(g);
     // global path: panel + diagonal block, or the inverse's row block
     size_t chol = size_t(kNB) * (kNB + 1) * 8 + size_t(std::max(g.D, 1)) * (kNB + 1) * 8;
     size_t inv = size_t(kNB) * (g.D + 1) * 8;
@@ -383,35 +502,22 @@ size_t factor_smem(const Geometry& g, int precision) {
 
 int factor_precision(const Geometry& g, int requested) {
     const size_t cap = 220 * 1024;
-    if (requested == 1) return 0;  // force the blocked global-memory path
-    if (requested == 64 && size_t(g.D) * (g.D + 1) * 8 <= cap) return 64;
-    if (requested == 32 && size_t(g.D) * (g.D + 1) * 4 <= cap) return 32;
-    if (requested == 0) {
-        if (size_t(g.D) * (g.D + 1) * 8 <= cap) return 64;
-        if (size_t(g.D) * (g.D + 1) * 4 <= cap) return 32;
-    }
+    const bool blk_fits = factor_blk_smem(g) <= cap;
+    const bool f64_fits = size_t(g.D) * (g.D + 1) * 8 <= cap;
+    if (requested == 64 && f64_fits) return 64;
+    if ((requested == 32 || requested == 0) && blk_fits) return 32;
     return 0;  // blocked fp64 over global memory
 }
 
 void launch_factor(const Geometry& g, const double* prior, int n_lines_total, double eps0, double* work,
                    float* whiten, int* status, int* latch, int line_base, int precision, cudaStream_t st) {
     const size_t sm = factor_smem(g, precision);
-    if ((precision == 64 || precision == 32) && g.D <= kWarpFactorMaxD) {
-        if (precision == 64) {
-            cudaFuncSetAttribute(factor_warp_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-            factor_warp_kernel<double><<<n_lines_total, 32, sm, st>>>(g, prior, eps0, whiten, status, latch,
-                                                                       line_base);
-        } else {
-            cudaFuncSetAttribute(factor_warp_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-            factor_warp_kernel<float><<<n_lines_total, 32, sm, st>>>(g, prior, eps0, whiten, status, latch,
-                                                                      line_base);
-        }
+    if (precision == 32) {
+        cudaFuncSetAttribute(factor_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        factor_blk_kernel<<<n_lines_total, 128, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base);
     } else if (precision == 64) {
         cudaFuncSetAttribute(factor_smem_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         factor_smem_kernel<double><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base);
-    } else if (precision == 32) {
-        cudaFuncSetAttribute(factor_smem_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        factor_smem_kernel<float><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base);
     } else {
         cudaFuncSetAttribute(factor_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         factor_global_kernel<<<n_lines_total, 256, sm, st>>>(g, prior, eps0, work, whiten, status, latch,
