@@ -207,18 +207,22 @@ def run_ours(args):
                          "tflops": a["flops"] * lines_per_launch / (per * 1e-3) / 1e12 if per > 0 else None,
                          "gbs": a["bytes"] * lines_per_launch / (per * 1e-3) / 1e9 if per > 0 else None}
     dom = max(kernels, key=lambda k: kernels[k]["share"])
-    fp32_peak = eng.probe_fp32_tflops()
+    reg_peak, const_peak = eng.probe_fp32_tflops()
+    fp32_peak = max(reg_peak, const_peak)  # the larger (conservative) measured FFMA rate
+    fprec = eng.factor_precision()
     pk = peaks()
     dk = kernels[dom]
+    src = (f"measured FFMA probe on this GPU in this run (erx_probe_fp32_tflops: register-form "
+           f"{reg_peak:.1f}, constant-form {const_peak:.1f} TFLOP/s; the larger is the peak)")
     if alg[dom]["flops"] > 0 and dom in ("stats", "score") and no_srp:
         roof = {"bound": "fp32", "kernel": dom, "achieved": dk["tflops"], "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": dk["tflops"] / fp32_peak, "traffic": None,
-                "peak_source": "measured FFMA probe (erx_probe_fp32_tflops) on this GPU in this run",
+                "frac": dk["tflops"] / fp32_peak, "traffic": None, "peak_source": src,
                 "algorithmic": f"{alg[dom]['flops']:.4g} flop/line x {S*T} lines/launch"}
     elif alg[dom]["flops"] > 0 and dom == "factor":
-        roof = {"bound": "fp64", "kernel": dom, "achieved": dk["tflops"], "peak": fp32_peak / 2, "unit": "TFLOP/s",
-                "frac": dk["tflops"] / (fp32_peak / 2), "traffic": None,
-                "peak_source": "half the measured FFMA probe (B200 FP64:FP32 = 1:2)",
+        fpk = fp32_peak if fprec == 32 else fp32_peak / 2
+        roof = {"bound": "fp32" if fprec == 32 else "fp64", "kernel": dom, "achieved": dk["tflops"], "peak": fpk,
+                "unit": "TFLOP/s", "frac": dk["tflops"] / fpk, "traffic": None,
+                "peak_source": src + ("" if fprec == 32 else "; fp64 = half (B200 FP64:FP32 = 1:2)"),
                 "algorithmic": f"{alg[dom]['flops']:.4g} flop/line x {S*T} lines/launch"}
     else:
         roof = {"bound": "hbm", "kernel": dom, "achieved": dk["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",

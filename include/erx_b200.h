@@ -147,9 +147,11 @@ int erx_set_profiling(erx_engine* e, int on);
 /* Per-kernel summed device ms and launch counts since profiling was enabled. */
 int erx_kernel_times(erx_engine* e, double* ms, uint64_t* launches);
 
-/* Measured FP32 FFMA throughput of the engine's device (TFLOP/s): the
- * roofline denominator for the FFMA-bound kernels. */
-int erx_probe_fp32_tflops(erx_engine* e, double* tflops);
+/* Measured FP32 FFMA throughput of the engine's device (TFLOP/s), the
+ * roofline denominator for the FFMA-bound kernels: reg_form = register-tile
+ * outer products (the kernels' own instruction shape), const_form = FFMA
+ * with constant-bank operands (highest issue rate).  Either may be NULL. */
+int erx_probe_fp32_tflops(erx_engine* e, double* reg_form, double* const_form);
 
 /* CUDA events on the engine stream, for callers timing device work. */
 int erx_event_record(erx_engine* e, int slot);

@@ -212,7 +212,7 @@ int configure(erx_engine* e, uint32_t P) {
     e->sc = erxk::plan_score(g);
     e->factor_prec = erxk::factor_precision(g, e->factor_req);
     const size_t L = size_t(e->S) * e->T;
-    CU(cudaMalloc(&e->d_stats, L * g.SE * sizeof(double)));
+    CU(cudaMalloc(&e->d_stats, L * (g.SE + g.D) * sizeof(double)));  // [c | s | S] per line
     CU(cudaMalloc(&e->d_prior, L * g.SE * sizeof(double)));
     if (e->factor_prec == 0) CU(cudaMalloc(&e->d_work, L * 2 * size_t(g.Dp) * g.Dp * sizeof(double)));
     CU(cudaMalloc(&e->d_white, L * size_t(g.Dp) * g.Dp * sizeof(float)));
@@ -650,9 +650,12 @@ int erx_event_elapsed_ms(erx_engine* e, int a, int b, float* ms) {
     return ERX_OK;
 }
 
-int erx_probe_fp32_tflops(erx_engine* e, double* tflops) {
+int erx_probe_fp32_tflops(erx_engine* e, double* reg_form, double* const_form) {
     CU(cudaSetDevice(e->device));
-    *tflops = erxk::probe_ffma_tflops(e->stream);
+    double r = 0, c = 0;
+    erxk::probe_ffma_tflops(e->stream, &r, &c);
+    if (reg_form) *reg_form = r;
+    if (const_form) *const_form = c;
     CU(cudaGetLastError());
     return ERX_OK;
 }

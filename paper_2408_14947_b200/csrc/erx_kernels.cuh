@@ -83,6 +83,6 @@ void launch_score(const Geometry& g, const ScoreLaunch& sc, const float* x, int 
 void launch_normalize(const Geometry& g, const float* raw, int n_lines_total, float* norm, cudaStream_t st);
 
 // Measured FP32 FFMA throughput of the current device (TFLOP/s, best of 5).
-double probe_ffma_tflops(cudaStream_t st);
+void probe_ffma_tflops(cudaStream_t st, double* reg_form, double* const_form);
 
 }  // namespace erxk

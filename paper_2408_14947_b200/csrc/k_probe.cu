@@ -1,5 +1,9 @@
-// k_probe.cu — FP32 FFMA throughput probe (roofline denominator for the
-// FFMA-bound kernels; MEASURED_PEAKS.json carries HBM and bf16 peaks only).
+// k_probe.cu — FP32 FFMA throughput probes: the roofline denominator for the
+// FFMA-bound kernels (MEASURED_PEAKS.json carries HBM and bf16 peaks only).
+//   reg form:   4x4 register outer products, all three operands in registers
+//               (the shape of the stats / score inner loops);
+//   const form: acc = fma(acc, x, y) with x, y kernel parameters (constant
+//               bank operands — the FFMA form with the highest issue rate).
 #include <algorithm>
 
 #include "erx_common.cuh"
@@ -7,7 +11,7 @@
 namespace erxk {
 namespace {
 
-__global__ void __launch_bounds__(256) ffma_probe_kernel(int iters, float x, float y, float* sink) {
+__global__ void __launch_bounds__(256) ffma_const_probe(int iters, float x, float y, float* sink) {
     float a[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) a[k] = float(threadIdx.x + k);
@@ -21,33 +25,67 @@ __global__ void __launch_bounds__(256) ffma_probe_kernel(int iters, float x, flo
     if (s == 123.456f) sink[0] = s;
 }
 
+__global__ void __launch_bounds__(256) ffma_reg_probe(int iters, const float* __restrict__ in, float* sink) {
+    float a[4], b[4], acc[4][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        a[k] = in[(threadIdx.x + k) & 63];
+        b[k] = in[(threadIdx.x + 7 * k + 3) & 63];
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = 0.f;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
+        a[i & 3] += acc[0][i & 3] * 1e-30f;  // loop-carried, keeps the operands in registers
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) s += acc[r][c];
+    if (s == 123.456f) sink[0] = s;
+}
+
 }  // namespace
 
-double probe_ffma_tflops(cudaStream_t st) {
-    float* sink = nullptr;
-    cudaMalloc(&sink, sizeof(float));
+void probe_ffma_tflops(cudaStream_t st, double* reg_form, double* const_form) {
+    float* buf = nullptr;
+    cudaMalloc(&buf, 64 * sizeof(float) + sizeof(float));
+    cudaMemset(buf, 0, 65 * sizeof(float));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int blocks = sms * 8, threads = 256, iters = 8192;
+    const int blocks = sms * 8, threads = 256, iters = 4096;
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    float best = 1e30f;
-    for (int rep = 0; rep < 6; ++rep) {
-        cudaEventRecord(a, st);
-        ffma_probe_kernel<<<blocks, threads, 0, st>>>(iters, 0.999f, 1e-3f, sink);
-        cudaEventRecord(b, st);
-        cudaEventSynchronize(b);
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, a, b);
-        if (rep > 0) best = std::min(best, ms);
+    for (int form = 0; form < 2; ++form) {
+        float best = 1e30f;
+        for (int rep = 0; rep < 6; ++rep) {
+            cudaEventRecord(a, st);
+            if (form == 0)
+                ffma_reg_probe<<<blocks, threads, 0, st>>>(iters, buf, buf + 64);
+            else
+                ffma_const_probe<<<blocks, threads, 0, st>>>(2 * iters, 0.999f, 1e-3f, buf + 64);
+            cudaEventRecord(b, st);
+            cudaEventSynchronize(b);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, a, b);
+            if (rep > 0) best = std::min(best, ms);
+        }
+        const double fma_per_thread = form == 0 ? 16.0 * iters : 8.0 * 2 * iters;
+        const double tf = 2.0 * fma_per_thread * blocks * threads / (double(best) * 1e-3) / 1e12;
+        if (form == 0) *reg_form = tf;
+        else *const_form = tf;
     }
     cudaEventDestroy(a);
     cudaEventDestroy(b);
-    cudaFree(sink);
-    const double flops = 2.0 * 8.0 * double(iters) * blocks * threads;
-    return flops / (double(best) * 1e-3) / 1e12;
+    cudaFree(buf);
 }
 
 }  // namespace erxk

@@ -1,20 +1,24 @@
 // k_scan.cu — the background recurrence over a window: ema_update
 // (erx.hpp:42-44) or welford_batch_update (linalg.hpp:33-36), element-wise
-// over (mu, packed K), sequential over the window's lines in the reference's
-// own order and rounding.
+// over (mu, packed K) and sequential over the window's lines in the
+// reference's own order, fp64.  Writes, per line, the PRE-update background
+// (score-then-update).  The first line ever initialises the
+// background with its own statistics (erx.hpp:54-55).
+//
+// Input per line (k_stats.cu): [c | s | S]; line statistics are finished
+// here:  mu_hat = c + s/P,  K_hat = (S - s_a s_b / P) / (P - 1).
 #include "erx_common.cuh"
 
 namespace erxk {
 namespace {
 
-// ---------------------------------------------------------------------------
-// scan: the EMA (erx.hpp:42-44) or batched-Welford (linalg.hpp:33-36)
-// recurrence over the window's lines, element-wise over (mu, packed K).
-// Writes, per line, the PRE-update background (score-then-update,
-// SPEC.md:324).  The first line ever initialises the background with its own
-// statistics (erx.hpp:54-55).  Multiplications are rounded separately
-// (__dmul_rn) to reproduce the reference's (1-a)*K + a*K_hat rounding.
-// ---------------------------------------------------------------------------
+__device__ __forceinline__ void unpack_tri(int k, int& a, int& b) {
+    a = int((sqrt(8.0 * k + 1.0) - 1.0) * 0.5);
+    while (a * (a + 1) / 2 > k) --a;
+    while ((a + 1) * (a + 2) / 2 <= k) ++a;
+    b = k - a * (a + 1) / 2;
+}
+
 __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __restrict__ stats,
                                                    double* __restrict__ prior, const double* __restrict__ st_in,
                                                    double* __restrict__ st_out, int n, int initialized,
@@ -22,14 +26,22 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
     const int s = blockIdx.y;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= g.SE) return;
+    const int D = g.D, SS = g.SE + g.D;  // stats slot stride
+    const double P = double(g.P), invP = 1.0 / P, invP1 = 1.0 / (P - 1.0);
+    int a = e, b = e;
+    if (e >= D) unpack_tri(e - D, a, b);
     const double* in = st_in + size_t(s) * g.SE;
     const size_t l0 = size_t(s) * n;
+    // line statistics of line l, this element (and the two means it couples)
+    auto mu_hat = [&](const double* st, int j) { return st[j] + st[D + j] * invP; };
+    auto k_hat = [&](const double* st) { return (st[2 * D + (e - D)] - st[D + a] * st[D + b] * invP) * invP1; };
     if (!incremental) {
         const double om = 1.0 - alpha;
         double state = in[e];
         for (int t = 0; t < n; ++t) {
             const size_t l = l0 + t;
-            const double stat = stats[l * g.SE + e];
+            const double* st = stats + l * SS;
+            const double stat = (e < D) ? mu_hat(st, e) : k_hat(st);
             double pr;
             if (!initialized && t == 0) {
                 pr = stat;
@@ -42,38 +54,28 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
         }
         st_out[size_t(s) * g.SE + e] = state;
     } else {
-        int a, b;
-        if (e < g.D) {
-            a = b = e;
-        } else {
-            int k = e - g.D;
-            a = int((sqrt(8.0 * k + 1.0) - 1.0) * 0.5);
-            while (a * (a + 1) / 2 > k) --a;
-            while ((a + 1) * (a + 2) / 2 <= k) ++a;
-            b = k - a * (a + 1) / 2;
-        }
         double ma = in[a], mb = in[b];
-        double cov = (e >= g.D) ? in[e] : 0.0;
+        double cov = (e >= D) ? in[e] : 0.0;
         double nseen = double(n_seen0);
-        const double nb = double(g.P);
+        const double nb = P;
         for (int t = 0; t < n; ++t) {
             const size_t l = l0 + t;
-            const double* st = stats + l * g.SE;
-            const double mha = st[a], mhb = st[b];
+            const double* st = stats + l * SS;
+            const double mha = mu_hat(st, a), mhb = mu_hat(st, b);
             double pr;
             if (!initialized && t == 0) {
                 ma = mha;
                 mb = mhb;
-                if (e >= g.D) cov = st[e];
+                if (e >= D) cov = k_hat(st);
                 nseen = nb;
-                pr = (e < g.D) ? ma : cov;
+                pr = (e < D) ? ma : cov;
             } else {
-                pr = (e < g.D) ? ma : cov;
+                pr = (e < D) ? ma : cov;
                 const double na = nseen, nn = na + nb;
                 const double da = mha - ma, db = mhb - mb;
-                if (e >= g.D) {
+                if (e >= D) {
                     const double m2a = (na >= 2.0) ? cov * (na - 1.0) : 0.0;
-                    const double m2b = st[e] * (nb - 1.0);
+                    const double m2b = k_hat(st) * (nb - 1.0);
                     const double m2 = m2a + m2b + da * db * (na * nb / nn);
                     cov = (nn >= 2.0) ? m2 / (nn - 1.0) : 0.0;
                 }
@@ -83,7 +85,7 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
             }
             prior[l * g.SE + e] = pr;
         }
-        st_out[size_t(s) * g.SE + e] = (e < g.D) ? ma : cov;
+        st_out[size_t(s) * g.SE + e] = (e < D) ? ma : cov;
     }
 }
 

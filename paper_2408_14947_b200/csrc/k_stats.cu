@@ -1,28 +1,29 @@
 // k_stats.cu — line_stats (erx.hpp:38-40) for every line of
 // a window, fused with project_line (projection.hpp:31-34).
 //
-// Output slot per line: [mu_hat (D) | K_hat packed lower (D(D+1)/2)], fp64.
+// Output slot per line (fp64): [c (D) | s = sum(v) (D) | S = sum(v v^T) packed
+// lower (D(D+1)/2)] with v = z - c.  The scan kernel turns it into
+//   mu_hat = c + s/P,  K_hat = (S - s s^T / P) / (P - 1)
+// so no fp64 division runs here.
 //
 // Work decomposition: the lower triangle of the D x D second-moment matrix is
 // tiled into 8x8 blocks (I >= J); one thread owns one block for a subset of
 // pixels (G pixel groups per block when the triangle is small, several CTAs
 // per line when it is large).  Pixels stream through shared memory in chunks
 // of CH rows, double-buffered with cp.async so the next chunk's HBM read
-// overlaps this chunk's FFMA work.
+// overlaps this chunk's FFMA work.  Rows are stored swizzled (low halves of
+// all 8-blocks, then high halves) so 16-byte reads of distinct blocks hit
+// distinct banks.
 //
-// Precision (SURVEY.md §7 study, reproduced in DESIGN.md): v = z - c with c
-// the fp64 mean of the line's first min(32, P) pixels, rounded once to fp32;
-// products accumulate in fp32 within a chunk and the chunk sums in a second
-// fp32 level; the exact line mean is restored in fp64:
-//   mu_hat = c + sum(v)/P,  K_hat = (S - sum(v) sum(v)^T / P) / (P - 1).
+// Precision: c = the line's first min(32, P) pixels' mean,
+// rounded to fp32; v = fl32(x - c) is the correctly rounded difference (exact
+// whenever x is within a factor 2 of c); products accumulate in fp32 within
+// a chunk and chunk sums in a second fp32 level.
 #include "erx_common.cuh"
 
 namespace erxk {
 namespace {
 
-// Position of dim d inside a staged pixel row: the 8-blocks' low halves first,
-// then their high halves, so the warps' 16-byte reads of distinct blocks hit
-// distinct banks.
 __device__ __forceinline__ int spos(int d, int nb) { return ((((d >> 2) & 1) * nb) + (d >> 3)) * 4 + (d & 3); }
 
 struct StatsArgs {
@@ -48,9 +49,8 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
     size_t off = align_up(2 * buf_floats * 4, 16);
     const size_t red_bytes = (sl.G > 1) ? size_t(128) * 64 * 8 : 0;
     off = off > red_bytes ? off : red_bytes;
-    double* cen = reinterpret_cast<double*>(smem + off);
-    double* colsum = cen + g.Dp;
-    double* red = reinterpret_cast<double*>(smem);  // aliases the chunk buffers after the loop
+    float* cen = reinterpret_cast<float*>(smem + off);  // [Dp] fp32 centre
+    double* red = reinterpret_cast<double*>(smem);     // aliases the chunk buffers after the loop
 
     const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
 
@@ -68,19 +68,17 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
         I = J + rem;
     }
 
-    // padded dims [D, Dp) stay zero in both buffers
-    if (g.Dp > g.D)
+    if (g.Dp > g.D)  // padded dims stay zero in both buffers
         for (int i = tid; i < 2 * sl.CH * (g.Dp - g.D); i += nt) {
             const int r = i / (g.Dp - g.D), c = g.D + i % (g.Dp - g.D);
             vbuf0[size_t(r) * g.Dp + spos(c, g.nb)] = 0.f;
         }
-    // centre c: fp64 mean of the first min(32, P) projected pixels
     {
         const int n0 = min(32, g.P);
         for (int j = tid; j < g.D; j += nt) {
             double s = 0.0;
             for (int pp = 0; pp < n0; ++pp) s += proj(g, xl + size_t(pp) * g.B, j);
-            cen[j] = s / double(n0);
+            cen[j] = float(s / double(n0));
         }
     }
 
@@ -122,12 +120,13 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
             for (int k = 0; k < 4; ++k) {
                 const int j = tid + k * nt;
                 if (j < g.D) {
-                    const double cj = cen[j];
-                    const int pj = spos(j, g.nb);
+                    const float cj = cen[j];
+                    float* col = v + spos(j, g.nb);
                     float s = 0.f;
+#pragma unroll 4
                     for (int pp = 0; pp < n; ++pp) {
-                        const float val = float(double(v[size_t(pp) * g.Dp + pj]) - cj);
-                        v[size_t(pp) * g.Dp + pj] = val;
+                        const float val = col[size_t(pp) * g.Dp] - cj;
+                        col[size_t(pp) * g.Dp] = val;
                         s += val;
                     }
                     cs[k] += double(s);
@@ -136,15 +135,15 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
         } else {
             for (int i = tid; i < n * g.D; i += nt) {
                 const int pp = i / g.D, j = i - pp * g.D;
-                v[size_t(pp) * g.Dp + spos(j, g.nb)] = float(proj(g, xl + size_t(c0 + pp) * g.B, j) - cen[j]);
+                v[size_t(pp) * g.Dp + spos(j, g.nb)] = float(proj(g, xl + size_t(c0 + pp) * g.B, j) - double(cen[j]));
             }
             __syncthreads();
             for (int k = 0; k < 4; ++k) {
                 const int j = tid + k * nt;
                 if (j < g.D) {
+                    const float* col = v + spos(j, g.nb);
                     float s = 0.f;
-                    const int pj = spos(j, g.nb);
-                    for (int pp = 0; pp < n; ++pp) s += v[size_t(pp) * g.Dp + pj];
+                    for (int pp = 0; pp < n; ++pp) s += col[size_t(pp) * g.Dp];
                     cs[k] += double(s);
                 }
             }
@@ -156,7 +155,6 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
             for (int r = 0; r < kBlk; ++r)
 #pragma unroll
                 for (int cc = 0; cc < kBlk; ++cc) acc[r][cc] = 0.f;
-            // swizzled rows: low halves of all 8-blocks, then high halves (conflict-free 128-bit reads)
             const float* va0 = v + I * 4;
             const float* va1 = v + (g.nb + I) * 4;
             const float* vb0 = v + J * 4;
@@ -183,23 +181,25 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
         __syncthreads();  // buffer (c & 1) is reissued at iteration c + 1
     }
 
-    for (int k = 0; k < 4; ++k) {
-        const int j = tid + k * nt;
-        if (j < g.D) colsum[j] = cs[k];
+    double* out = a.stats + size_t(line) * (g.SE + g.D);
+    if (cta == 0) {
+        for (int k = 0; k < 4; ++k) {
+            const int j = tid + k * nt;
+            if (j < g.D) {
+                out[j] = double(cen[j]);
+                out[g.D + j] = cs[k];
+            }
+        }
     }
     if (sl.G > 1) {
 #pragma unroll
         for (int r = 0; r < kBlk; ++r)
 #pragma unroll
             for (int cc = 0; cc < kBlk; ++cc) red[tid * 64 + r * 8 + cc] = double(acc2[r][cc]);
+        __syncthreads();
     }
-    __syncthreads();
-
-    double* out = a.stats + size_t(line) * g.SE;
-    const double P = double(g.P);
-    if (cta == 0)
-        for (int j = tid; j < g.D; j += nt) out[j] = cen[j] + colsum[j] / P;
     if (active && grp == 0) {
+        double* S = out + 2 * g.D;
 #pragma unroll
         for (int r = 0; r < kBlk; ++r) {
             const int ai = I * kBlk + r;
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
                     } else {
                         s = double(acc2[r][cc]);
                     }
-                    out[g.D + tri(ai, bj)] = (s - colsum[ai] * colsum[bj] / P) / (P - 1.0);
+                    S[tri(ai, bj)] = s;
                 }
             }
         }
@@ -243,7 +243,7 @@ StatsLaunch plan_stats(const Geometry& g) {
     size_t off = align_up(size_t(ch) * per_px, 16);
     const size_t red_bytes = (sl.G > 1) ? size_t(128) * 64 * 8 : 0;
     off = off > red_bytes ? off : red_bytes;
-    sl.smem = off + 2 * size_t(g.Dp) * 8;
+    sl.smem = off + size_t(g.Dp) * 4;
     return sl;
 }
 

@@ -259,10 +259,11 @@ class Engine:
         self._lib.erx_kernel_times(self._h, _p(ms, C.c_double), _p(n, C.c_uint64))
         return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(L.KERNEL_NAMES)}
 
-    def probe_fp32_tflops(self) -> float:
-        v = C.c_double(0)
-        self._check(self._lib.erx_probe_fp32_tflops(self._h, C.byref(v)))
-        return float(v.value)
+    def probe_fp32_tflops(self):
+        """(register-form, constant-form) measured FFMA TFLOP/s of this device."""
+        r, c = C.c_double(0), C.c_double(0)
+        self._check(self._lib.erx_probe_fp32_tflops(self._h, C.byref(r), C.byref(c)))
+        return float(r.value), float(c.value)
 
     def event_record(self, slot: int):
         self._check(self._lib.erx_event_record(self._h, slot))
