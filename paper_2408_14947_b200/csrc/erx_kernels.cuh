@@ -59,6 +59,7 @@ struct ScoreLaunch {
     int threads;     // CTA size
     int Dpad;        // smem row stride (floats), = 4 mod 32
     int tiles;       // CTAs per line
+    int wsmem;       // 1: the line's W blocks are staged in shared memory
     size_t smem;
 };
 

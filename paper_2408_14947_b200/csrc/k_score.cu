@@ -37,7 +37,22 @@ __global__ void __launch_bounds__(512) score_kernel(ScoreArgs a) {
     const int tid = threadIdx.x, nt = blockDim.x;
     float* vt = reinterpret_cast<float*>(smem);                    // [PT][Dpad]
     float* red = vt + size_t(sc.PT) * sc.Dpad;                      // [nb][PT]
-    double* mu = reinterpret_cast<double*>(smem + align_up((size_t(sc.PT) * sc.Dpad + size_t(g.nb) * sc.PT) * 4, 16));
+    const size_t mu_off = align_up((size_t(sc.PT) * sc.Dpad + size_t(g.nb) * sc.PT) * 4, 16);
+    double* mu = reinterpret_cast<double*>(smem + mu_off);
+    float* Ws = reinterpret_cast<float*>(smem + mu_off + align_up(size_t(g.Dp) * 8, 16));  // [tri(I,J)][8][8]
+    const float* Wl = a.W + size_t(line) * g.Dp * g.Dp;
+    if (sc.wsmem) {  // the line's lower-triangular W blocks -> smem (overlaps the pixel staging)
+        const int nblk = g.nb * (g.nb + 1) / 2;
+        for (int i = tid; i < nblk * 16; i += nt) {
+            const int bq = i >> 4, r = (i >> 1) & 7, h = i & 1;
+            int I = int((sqrtf(8.f * bq + 1.f) - 1.f) * 0.5f);
+            while (I * (I + 1) / 2 > bq) --I;
+            while ((I + 1) * (I + 2) / 2 <= bq) ++I;
+            const int J = bq - I * (I + 1) / 2;
+            cp_async16(Ws + bq * 64 + r * 8 + h * 4, Wl + size_t(I * kBlk + r) * g.Dp + J * kBlk + h * 4);
+        }
+        cp_async_commit();
+    }
     const double* pr = a.prior + size_t(line) * g.SE;
     for (int j = tid; j < g.Dp; j += nt) mu[j] = (j < g.D) ? pr[j] : 0.0;
     __syncthreads();
@@ -63,11 +78,11 @@ __global__ void __launch_bounds__(512) score_kernel(ScoreArgs a) {
         const int pp = np + i / g.D, d = i % g.D;
         vt[size_t(pp) * sc.Dpad + d] = 0.f;
     }
+    if (sc.wsmem) cp_async_wait<0>();
     __syncthreads();
 
     const int s = tid / sc.G;
     const int q = tid - s * sc.G;
-    const float* Wl = a.W + size_t(line) * g.Dp * g.Dp;
     if (s < sc.npairs) {
         for (int h = 0; h < 2; ++h) {
             const int I = h == 0 ? s : g.nb - 1 - s;
@@ -93,10 +108,19 @@ __global__ void __launch_bounds__(512) score_kernel(ScoreArgs a) {
                     vb[6][p] = t1.z;
                     vb[7][p] = t1.w;
                 }
+                const float* wblk = sc.wsmem ? Ws + (I * (I + 1) / 2 + J) * 64 : nullptr;
 #pragma unroll
                 for (int r = 0; r < kBlk; ++r) {
-                    const float4* wr = reinterpret_cast<const float4*>(Wl + size_t(I * kBlk + r) * g.Dp + J * kBlk);
-                    const float4 w0 = __ldg(wr), w1 = __ldg(wr + 1);
+                    float4 w0, w1;
+                    if (sc.wsmem) {  // warp-uniform address: shared-memory broadcast
+                        w0 = *reinterpret_cast<const float4*>(wblk + r * 8);
+                        w1 = *reinterpret_cast<const float4*>(wblk + r * 8 + 4);
+                    } else {
+                        const float4* wr =
+                            reinterpret_cast<const float4*>(Wl + size_t(I * kBlk + r) * g.Dp + J * kBlk);
+                        w0 = __ldg(wr);
+                        w1 = __ldg(wr + 1);
+                    }
                     const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
                     for (int c = 0; c < kBlk; ++c)
@@ -159,7 +183,10 @@ ScoreLaunch plan_score(const Geometry& g) {
     sc.threads = (sc.threads + 31) / 32 * 32;
     sc.Dpad = g.Dp + ((4 - g.Dp) % 32 + 32) % 32;  // Dpad = 4 (mod 32)
     sc.tiles = (g.P + sc.PT - 1) / sc.PT;
-    sc.smem = align_up((size_t(sc.PT) * sc.Dpad + size_t(g.nb) * sc.PT) * 4, 16) + size_t(g.Dp) * 8;
+    sc.smem = align_up((size_t(sc.PT) * sc.Dpad + size_t(g.nb) * sc.PT) * 4, 16) + align_up(size_t(g.Dp) * 8, 16);
+    const size_t wbytes = size_t(g.nb) * (g.nb + 1) / 2 * 64 * 4;
+    sc.wsmem = (sc.smem + wbytes <= 200 * 1024) ? 1 : 0;  // stage W in smem when it fits (D <= ~240)
+    if (sc.wsmem) sc.smem += wbytes;
     return sc;
 }
 
