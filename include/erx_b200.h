@@ -152,6 +152,8 @@ int erx_kernel_times(erx_engine* e, double* ms, uint64_t* launches);
  * outer products (the kernels' own instruction shape), const_form = FFMA
  * with constant-bank operands (highest issue rate).  Either may be NULL. */
 int erx_probe_fp32_tflops(erx_engine* e, double* reg_form, double* const_form);
+/* Same for the paired fma.rn.f32x2 (FFMA2) instruction. */
+int erx_probe_ffma2_tflops(erx_engine* e, double* tflops);
 
 /* CUDA events on the engine stream, for callers timing device work. */
 int erx_event_record(erx_engine* e, int slot);

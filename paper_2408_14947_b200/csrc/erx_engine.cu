@@ -215,7 +215,7 @@ int configure(erx_engine* e, uint32_t P) {
     CU(cudaMalloc(&e->d_stats, L * (g.SE + g.D) * sizeof(double)));  // [c | s | S] per line
     CU(cudaMalloc(&e->d_prior, L * g.SE * sizeof(double)));
     if (e->factor_prec == 0) CU(cudaMalloc(&e->d_work, L * 2 * size_t(g.Dp) * g.Dp * sizeof(double)));
-    CU(cudaMalloc(&e->d_white, L * size_t(g.Dp) * g.Dp * sizeof(float)));
+    CU(cudaMalloc(&e->d_white, L * erxk::whiten_floats_per_line(g) * sizeof(float)));
     CU(cudaMalloc(&e->d_raw, L * P * sizeof(float)));
     CU(cudaMalloc(&e->d_norm, L * P * sizeof(float)));
     CU(cudaMalloc(&e->d_status, L * sizeof(int)));
@@ -656,6 +656,13 @@ int erx_probe_fp32_tflops(erx_engine* e, double* reg_form, double* const_form) {
     erxk::probe_ffma_tflops(e->stream, &r, &c);
     if (reg_form) *reg_form = r;
     if (const_form) *const_form = c;
+    CU(cudaGetLastError());
+    return ERX_OK;
+}
+
+int erx_probe_ffma2_tflops(erx_engine* e, double* tflops) {
+    CU(cudaSetDevice(e->device));
+    *tflops = erxk::probe_ffma2_tflops(e->stream);
     CU(cudaGetLastError());
     return ERX_OK;
 }

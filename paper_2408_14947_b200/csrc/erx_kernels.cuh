@@ -65,6 +65,8 @@ struct ScoreLaunch {
 
 StatsLaunch plan_stats(const Geometry& g);
 ScoreLaunch plan_score(const Geometry& g);
+// floats of packed lower 8x8 W blocks per line (k_factor.cu: write_wblocks)
+size_t whiten_floats_per_line(const Geometry& g);
 // Factor precision actually used for a request (0 auto, 32, 64): 64 / 32 select the
 // shared-memory kernel in that precision, 0 the blocked fp64 global-memory kernel.
 int factor_precision(const Geometry& g, int requested);
@@ -85,5 +87,7 @@ void launch_normalize(const Geometry& g, const float* raw, int n_lines_total, fl
 
 // Measured FP32 FFMA throughput of the current device (TFLOP/s, best of 5).
 void probe_ffma_tflops(cudaStream_t st, double* reg_form, double* const_form);
+// Measured paired-FFMA (fma.rn.f32x2) throughput, TFLOP/s counting 2 FMAs per lane.
+double probe_ffma2_tflops(cudaStream_t st);
 
 }  // namespace erxk

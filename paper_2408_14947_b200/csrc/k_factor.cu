@@ -19,6 +19,26 @@
 namespace erxk {
 namespace {
 
+// W = L^{-1} leaves the factor kernels as the lower-triangular 8x8 blocks of
+// one line, packed in row-major block order (block (I, J), J <= I, at
+// tri(I, J)), each block column-major (element (r, c) at c * 8 + r) so the
+// score kernel reads row pairs of a column as one float2.  Entries above the
+// diagonal or in the padding are zero.
+template <typename Get>
+__device__ __forceinline__ void write_wblocks(float* __restrict__ whiten, int line, const Geometry& g, Get get) {
+    const int nblk = g.nb * (g.nb + 1) / 2;
+    float* Wp = whiten + size_t(line) * nblk * 64;
+    for (int idx = threadIdx.x; idx < nblk * 64; idx += blockDim.x) {
+        const int bq = idx >> 6, e = idx & 63, c = e >> 3, r = e & 7;
+        int I = int((sqrtf(8.f * bq + 1.f) - 1.f) * 0.5f);
+        while (I * (I + 1) / 2 > bq) --I;
+        while ((I + 1) * (I + 2) / 2 <= bq) ++I;
+        const int J = bq - I * (I + 1) / 2;
+        const int i = I * kBlk + r, j = J * kBlk + c;
+        Wp[idx] = (i < g.D && j <= i) ? get(i, j) : 0.f;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // factor: L = chol(K_{t-1} + eps I) with eps escalation x10 up to 1e-1
 // (SPEC.md:306), then X = L^{-1}, written as fp32 W (Dp x Dp, zeros above the
@@ -195,11 +215,7 @@ __global__ void __launch_bounds__(256) factor_global_kernel(Geometry g, const do
         return;
     }
     tri_inverse_blocked(A, X, D, Dp, reinterpret_cast<double*>(smem));
-    float* W = whiten + size_t(line) * Dp * Dp;
-    for (int idx = tid; idx < Dp * Dp; idx += nt) {
-        int i = idx / Dp, j = idx - i * Dp;
-        W[idx] = (i < D && j <= i) ? float(X[size_t(i) * Dp + j]) : 0.f;
-    }
+    write_wblocks(whiten, line, g, [&](int i, int j) { return float(X[size_t(i) * Dp + j]); });
     if (tid == 0) status[line] = -1;
 }
 
@@ -276,11 +292,7 @@ __global__ void __launch_bounds__(256) factor_smem_kernel(Geometry g, const doub
         }
         __syncthreads();
     }
-    float* W = whiten + size_t(line) * g.Dp * g.Dp;
-    for (int idx = tid; idx < g.Dp * g.Dp; idx += nt) {
-        const int i = idx / g.Dp, j = idx - i * g.Dp;
-        W[idx] = (i < D && j <= i) ? float(A[i * LD + j]) : 0.f;
-    }
+    write_wblocks(whiten, line, g, [&](int i, int j) { return float(A[i * LD + j]); });
     if (tid == 0) status[line] = -1;
 }
 
@@ -477,11 +489,7 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
         }
         __syncthreads();
     }
-    float* W = whiten + size_t(line) * Dp * Dp;
-    for (int idx = tid; idx < Dp * Dp; idx += nt) {
-        const int i = idx / Dp, j = idx - i * Dp;
-        W[idx] = (i < D && j <= i) ? A[i * LD + j] : 0.f;
-    }
+    write_wblocks(whiten, line, g, [&](int i, int j) { return A[i * LD + j]; });
     if (tid == 0) status[line] = -1;
 }
 

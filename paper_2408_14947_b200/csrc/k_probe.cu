@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) ffma_reg_probe(int iters, const float* __
         for (int r = 0; r < 4; ++r)
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
-        a[i & 3] += acc[0][i & 3] * 1e-30f;  // loop-carried, keeps the operands in registers
+        a[0] += acc[0][0] * 1e-30f;  // loop-carried, keeps the operands in registers
     }
     float s = 0.f;
 #pragma unroll
@@ -51,7 +51,63 @@ __global__ void __launch_bounds__(256) ffma_reg_probe(int iters, const float* __
     if (s == 123.456f) sink[0] = s;
 }
 
+// Paired FFMA2 (fma.rn.f32x2, sm_100): 4x2 float2 accumulators.
+__global__ void __launch_bounds__(256) ffma2_reg_probe(int iters, const float* __restrict__ in, float* sink) {
+    float2 a[4], b[2], acc[4][2];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float t = in[(threadIdx.x + k) & 63];
+        a[k] = make_float2(t, t);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) b[k] = make_float2(in[(threadIdx.x + 5 * k + 1) & 63], in[(threadIdx.x + 3 * k + 7) & 63]);
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) acc[r][c] = make_float2(0.f, 0.f);
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) acc[r][c] = __ffma2_rn(a[r], b[c], acc[r][c]);
+        a[0].x += acc[0][0].x * 1e-30f;
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) s += acc[r][c].x + acc[r][c].y;
+    if (s == 123.456f) sink[0] = s;
+}
+
 }  // namespace
+
+double probe_ffma2_tflops(cudaStream_t st) {
+    float* buf = nullptr;
+    cudaMalloc(&buf, 65 * sizeof(float));
+    cudaMemset(buf, 0, 65 * sizeof(float));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float best = 1e30f;
+    for (int rep = 0; rep < 6; ++rep) {
+        cudaEventRecord(a, st);
+        ffma2_reg_probe<<<blocks, threads, 0, st>>>(iters, buf, buf + 64);
+        cudaEventRecord(b, st);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        if (rep > 0) best = std::min(best, ms);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(buf);
+    return 4.0 * 8.0 * iters * double(blocks) * threads / (double(best) * 1e-3) / 1e12;
+}
 
 void probe_ffma_tflops(cudaStream_t st, double* reg_form, double* const_form) {
     float* buf = nullptr;

@@ -4,12 +4,14 @@
 // multiply; and normalize_scores (detector.hpp:29-32).
 //
 // score: one CTA per (line, pixel tile).  The tile's centred pixels sit in
-// shared memory as rows [pixel][Dpad] (Dpad = 4 mod 32: the 16 pixel lanes of
-// a warp read 16 consecutive rows conflict-free).  Thread (s, q) owns
+// shared memory as rows [pixel][Dpad] (Dpad = 4 mod 32: consecutive pixel
+// rows hit distinct banks).  The line's W arrives as packed lower 8x8 blocks,
+// column-major inside a block (k_factor.cu: write_wblocks), staged into
+// shared memory with cp.async when it fits.  Thread (s, q) owns the
 // row-block pair {s, nb-1-s} (equal total work, nb+1 block steps) and pixels
-// q + G*p, p < 4; 8x4 fp32 register accumulators; W rows come from L2 with
-// warp-broadcast 128-bit loads.  Partial sums of squares per row block are
-// reduced in a fixed order (bitwise deterministic).
+// q + G*p, p < 4; per block column c it issues 16 paired FFMA2 (rows
+// 2k, 2k+1 of W times a broadcast pixel value).  Partial sums of squares per
+// row block are reduced in a fixed order (bitwise deterministic).
 #include "erx_common.cuh"
 
 namespace erxk {
@@ -35,22 +37,15 @@ __global__ void __launch_bounds__(512) score_kernel(ScoreArgs a) {
     const int p0 = tile * sc.PT;
     const int np = min(sc.PT, g.P - p0);
     const int tid = threadIdx.x, nt = blockDim.x;
+    const int nblk = g.nb * (g.nb + 1) / 2;
     float* vt = reinterpret_cast<float*>(smem);                    // [PT][Dpad]
     float* red = vt + size_t(sc.PT) * sc.Dpad;                      // [nb][PT]
     const size_t mu_off = align_up((size_t(sc.PT) * sc.Dpad + size_t(g.nb) * sc.PT) * 4, 16);
     double* mu = reinterpret_cast<double*>(smem + mu_off);
-    float* Ws = reinterpret_cast<float*>(smem + mu_off + align_up(size_t(g.Dp) * 8, 16));  // [tri(I,J)][8][8]
-    const float* Wl = a.W + size_t(line) * g.Dp * g.Dp;
-    if (sc.wsmem) {  // the line's lower-triangular W blocks -> smem (overlaps the pixel staging)
-        const int nblk = g.nb * (g.nb + 1) / 2;
-        for (int i = tid; i < nblk * 16; i += nt) {
-            const int bq = i >> 4, r = (i >> 1) & 7, h = i & 1;
-            int I = int((sqrtf(8.f * bq + 1.f) - 1.f) * 0.5f);
-            while (I * (I + 1) / 2 > bq) --I;
-            while ((I + 1) * (I + 2) / 2 <= bq) ++I;
-            const int J = bq - I * (I + 1) / 2;
-            cp_async16(Ws + bq * 64 + r * 8 + h * 4, Wl + size_t(I * kBlk + r) * g.Dp + J * kBlk + h * 4);
-        }
+    float* Ws = reinterpret_cast<float*>(smem + mu_off + align_up(size_t(g.Dp) * 8, 16));
+    const float* Wl = a.W + size_t(line) * nblk * 64;
+    if (sc.wsmem) {  // the line's packed W blocks -> smem, overlapping the pixel staging
+        for (int i = tid; i < nblk * 16; i += nt) cp_async16(Ws + 4 * i, Wl + 4 * i);
         cp_async_commit();
     }
     const double* pr = a.prior + size_t(line) * g.SE;
@@ -83,15 +78,17 @@ __global__ void __launch_bounds__(512) score_kernel(ScoreArgs a) {
 
     const int s = tid / sc.G;
     const int q = tid - s * sc.G;
+    const float* Wsrc = sc.wsmem ? Ws : Wl;
     if (s < sc.npairs) {
         for (int h = 0; h < 2; ++h) {
             const int I = h == 0 ? s : g.nb - 1 - s;
             if (h == 1 && I == s) break;
-            float acc[kBlk][4];
+            float2 acc[kBlk / 2][4];  // rows (2k, 2k+1) x pixel p
 #pragma unroll
-            for (int r = 0; r < kBlk; ++r)
+            for (int k = 0; k < kBlk / 2; ++k)
 #pragma unroll
-                for (int p = 0; p < 4; ++p) acc[r][p] = 0.f;
+                for (int p = 0; p < 4; ++p) acc[k][p] = make_float2(0.f, 0.f);
+            const float* wrow = Wsrc + size_t(I * (I + 1) / 2) * 64;
             for (int J = 0; J <= I; ++J) {
                 float vb[kBlk][4];
 #pragma unroll
@@ -108,31 +105,34 @@ __global__ void __launch_bounds__(512) score_kernel(ScoreArgs a) {
                     vb[6][p] = t1.z;
                     vb[7][p] = t1.w;
                 }
-                const float* wblk = sc.wsmem ? Ws + (I * (I + 1) / 2 + J) * 64 : nullptr;
+                const float* wb = wrow + J * 64;
 #pragma unroll
-                for (int r = 0; r < kBlk; ++r) {
-                    float4 w0, w1;
-                    if (sc.wsmem) {  // warp-uniform address: shared-memory broadcast
-                        w0 = *reinterpret_cast<const float4*>(wblk + r * 8);
-                        w1 = *reinterpret_cast<const float4*>(wblk + r * 8 + 4);
+                for (int c = 0; c < kBlk; ++c) {
+                    float4 w0, w1;  // column c, rows 0..3 and 4..7 (warp-uniform address: broadcast)
+                    if (sc.wsmem) {
+                        w0 = *reinterpret_cast<const float4*>(wb + c * 8);
+                        w1 = *reinterpret_cast<const float4*>(wb + c * 8 + 4);
                     } else {
-                        const float4* wr =
-                            reinterpret_cast<const float4*>(Wl + size_t(I * kBlk + r) * g.Dp + J * kBlk);
-                        w0 = __ldg(wr);
-                        w1 = __ldg(wr + 1);
+                        w0 = __ldg(reinterpret_cast<const float4*>(wb + c * 8));
+                        w1 = __ldg(reinterpret_cast<const float4*>(wb + c * 8 + 4));
                     }
-                    const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+                    const float2 wp[4] = {make_float2(w0.x, w0.y), make_float2(w0.z, w0.w), make_float2(w1.x, w1.y),
+                                          make_float2(w1.z, w1.w)};
 #pragma unroll
-                    for (int c = 0; c < kBlk; ++c)
+                    for (int k = 0; k < kBlk / 2; ++k)
 #pragma unroll
-                        for (int p = 0; p < 4; ++p) acc[r][p] = fmaf(wv[c], vb[c][p], acc[r][p]);
+                        for (int p = 0; p < 4; ++p)
+                            acc[k][p] = __ffma2_rn(wp[k], make_float2(vb[c][p], vb[c][p]), acc[k][p]);
                 }
             }
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
                 float ssq = 0.f;
 #pragma unroll
-                for (int r = 0; r < kBlk; ++r) ssq = fmaf(acc[r][p], acc[r][p], ssq);
+                for (int k = 0; k < kBlk / 2; ++k) {
+                    ssq = fmaf(acc[k][p].x, acc[k][p].x, ssq);
+                    ssq = fmaf(acc[k][p].y, acc[k][p].y, ssq);
+                }
                 red[I * sc.PT + q + sc.G * p] = ssq;
             }
         }
@@ -189,6 +189,8 @@ ScoreLaunch plan_score(const Geometry& g) {
     if (sc.wsmem) sc.smem += wbytes;
     return sc;
 }
+
+size_t whiten_floats_per_line(const Geometry& g) { return size_t(g.nb) * (g.nb + 1) / 2 * 64; }
 
 void launch_score(const Geometry& g, const ScoreLaunch& sc, const float* x, int n_per_stream, int in_stride,
                   const double* prior, const float* whiten, int n_lines_total, float* raw, cudaStream_t st) {

@@ -49,7 +49,8 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
     size_t off = align_up(2 * buf_floats * 4, 16);
     const size_t red_bytes = (sl.G > 1) ? size_t(128) * 64 * 8 : 0;
     off = off > red_bytes ? off : red_bytes;
-    float* cen = reinterpret_cast<float*>(smem + off);  // [Dp] fp32 centre
+    double* colsum = reinterpret_cast<double*>(smem + off);       // [Dp] fp64 column sums of v
+    float* cen = reinterpret_cast<float*>(smem + off + g.Dp * 8);  // [Dp] fp32 centre
     double* red = reinterpret_cast<double*>(smem);     // aliases the chunk buffers after the loop
 
     const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
             double s = 0.0;
             for (int pp = 0; pp < n0; ++pp) s += proj(g, xl + size_t(pp) * g.B, j);
             cen[j] = float(s / double(n0));
+            colsum[j] = 0.0;
         }
     }
 
@@ -103,7 +105,6 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
     for (int r = 0; r < kBlk; ++r)
 #pragma unroll
         for (int c = 0; c < kBlk; ++c) acc2[r][c] = 0.f;
-    double cs[4] = {0.0, 0.0, 0.0, 0.0};
 
     for (int c = 0; c < nchunks; ++c) {
         const int c0 = c * sl.CH, n = min(sl.CH, g.P - c0);
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
                         col[size_t(pp) * g.Dp] = val;
                         s += val;
                     }
-                    cs[k] += double(s);
+                    colsum[j] += double(s);
                 }
             }
         } else {
@@ -144,51 +145,73 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
                     const float* col = v + spos(j, g.nb);
                     float s = 0.f;
                     for (int pp = 0; pp < n; ++pp) s += col[size_t(pp) * g.Dp];
-                    cs[k] += double(s);
+                    colsum[j] += double(s);
                 }
             }
         }
         __syncthreads();
         if (active) {
-            float acc[kBlk][kBlk];
+            // 8x8 outer products as paired FFMA2 (one operand broadcast from a
+            // scalar register), next pixel's operands prefetched into registers
+            float2 acc[kBlk][kBlk / 2];
 #pragma unroll
             for (int r = 0; r < kBlk; ++r)
 #pragma unroll
-                for (int cc = 0; cc < kBlk; ++cc) acc[r][cc] = 0.f;
+                for (int cc = 0; cc < kBlk / 2; ++cc) acc[r][cc] = make_float2(0.f, 0.f);
             const float* va0 = v + I * 4;
             const float* va1 = v + (g.nb + I) * 4;
             const float* vb0 = v + J * 4;
             const float* vb1 = v + (g.nb + J) * 4;
-#pragma unroll 2
-            for (int pp = grp; pp < n; pp += sl.G) {
+            const int G = sl.G;
+            int pp = grp;
+            float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, b0 = a0, b1 = a0;
+            if (pp < n) {
                 const size_t o = size_t(pp) * g.Dp;
-                const float4 a0 = *reinterpret_cast<const float4*>(va0 + o);
-                const float4 a1 = *reinterpret_cast<const float4*>(va1 + o);
-                const float4 b0 = *reinterpret_cast<const float4*>(vb0 + o);
-                const float4 b1 = *reinterpret_cast<const float4*>(vb1 + o);
+                a0 = *reinterpret_cast<const float4*>(va0 + o);
+                a1 = *reinterpret_cast<const float4*>(va1 + o);
+                b0 = *reinterpret_cast<const float4*>(vb0 + o);
+                b1 = *reinterpret_cast<const float4*>(vb1 + o);
+            }
+            while (pp < n) {
+                const int pn = pp + G;
+                float4 na0 = a0, na1 = a1, nb0 = b0, nb1 = b1;
+                if (pn < n) {
+                    const size_t o = size_t(pn) * g.Dp;
+                    na0 = *reinterpret_cast<const float4*>(va0 + o);
+                    na1 = *reinterpret_cast<const float4*>(va1 + o);
+                    nb0 = *reinterpret_cast<const float4*>(vb0 + o);
+                    nb1 = *reinterpret_cast<const float4*>(vb1 + o);
+                }
                 const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                                      make_float2(b1.z, b1.w)};
 #pragma unroll
                 for (int r = 0; r < kBlk; ++r)
 #pragma unroll
-                    for (int cc = 0; cc < kBlk; ++cc) acc[r][cc] = fmaf(av[r], bv[cc], acc[r][cc]);
+                    for (int cc = 0; cc < kBlk / 2; ++cc)
+                        acc[r][cc] = __ffma2_rn(make_float2(av[r], av[r]), bv[cc], acc[r][cc]);
+                a0 = na0;
+                a1 = na1;
+                b0 = nb0;
+                b1 = nb1;
+                pp = pn;
             }
 #pragma unroll
             for (int r = 0; r < kBlk; ++r)
 #pragma unroll
-                for (int cc = 0; cc < kBlk; ++cc) acc2[r][cc] += acc[r][cc];
+                for (int cc = 0; cc < kBlk / 2; ++cc) {
+                    acc2[r][2 * cc] += acc[r][cc].x;
+                    acc2[r][2 * cc + 1] += acc[r][cc].y;
+                }
         }
         __syncthreads();  // buffer (c & 1) is reissued at iteration c + 1
     }
 
     double* out = a.stats + size_t(line) * (g.SE + g.D);
     if (cta == 0) {
-        for (int k = 0; k < 4; ++k) {
-            const int j = tid + k * nt;
-            if (j < g.D) {
-                out[j] = double(cen[j]);
-                out[g.D + j] = cs[k];
-            }
+        for (int j = tid; j < g.D; j += nt) {
+            out[j] = double(cen[j]);
+            out[g.D + j] = colsum[j];
         }
     }
     if (sl.G > 1) {
@@ -243,7 +266,7 @@ StatsLaunch plan_stats(const Geometry& g) {
     size_t off = align_up(size_t(ch) * per_px, 16);
     const size_t red_bytes = (sl.G > 1) ? size_t(128) * 64 * 8 : 0;
     off = off > red_bytes ? off : red_bytes;
-    sl.smem = off + size_t(g.Dp) * 4;
+    sl.smem = off + size_t(g.Dp) * 12;  // colsum (fp64) + centre (fp32)
     return sl;
 }
 
