@@ -154,6 +154,10 @@ int erx_kernel_times(erx_engine* e, double* ms, uint64_t* launches);
 int erx_probe_fp32_tflops(erx_engine* e, double* reg_form, double* const_form);
 /* Same for the paired fma.rn.f32x2 (FFMA2) instruction. */
 int erx_probe_ffma2_tflops(erx_engine* e, double* tflops);
+/* tcgen05 self-test on device buffers: D[128][128] = A[128][K] . B[128][K]^T
+ * from bf16 operands (split = 0) or the 3-way bf16 split with 6 products
+ * (split = 1, fp32-accurate).  K a multiple of 16, <= 256. */
+int erx_tc_selftest(erx_engine* e, const float* dA, const float* dB, int K, int split, float* dD);
 
 /* CUDA events on the engine stream, for callers timing device work. */
 int erx_event_record(erx_engine* e, int slot);

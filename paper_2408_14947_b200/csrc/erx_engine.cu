@@ -660,6 +660,14 @@ int erx_probe_fp32_tflops(erx_engine* e, double* reg_form, double* const_form) {
     return ERX_OK;
 }
 
+int erx_tc_selftest(erx_engine* e, const float* dA, const float* dB, int K, int split, float* dD) {
+    CU(cudaSetDevice(e->device));
+    if (K % 16 || K < 16 || K > 256) return fail(e, ERX_ERR_CONFIG, "K must be a multiple of 16 in [16, 256]");
+    CU(cudaError_t(erxk::tc_selftest(dA, dB, K, split, dD, e->stream)));
+    CU(cudaStreamSynchronize(e->stream));
+    return ERX_OK;
+}
+
 int erx_probe_ffma2_tflops(erx_engine* e, double* tflops) {
     CU(cudaSetDevice(e->device));
     *tflops = erxk::probe_ffma2_tflops(e->stream);

@@ -89,5 +89,7 @@ void launch_normalize(const Geometry& g, const float* raw, int n_lines_total, fl
 void probe_ffma_tflops(cudaStream_t st, double* reg_form, double* const_form);
 // Measured paired-FFMA (fma.rn.f32x2) throughput, TFLOP/s counting 2 FMAs per lane.
 double probe_ffma2_tflops(cudaStream_t st);
+// tcgen05 self-test: D[128][128] = A[128][K] B[128][K]^T (bf16, split = 1: 3-way split, 6 products).
+int tc_selftest(const float* dA, const float* dB, int K, int split, float* dD, cudaStream_t st);
 
 }  // namespace erxk

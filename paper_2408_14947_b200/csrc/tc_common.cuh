@@ -1,0 +1,122 @@
+// tc_common.cuh — hand-written tcgen05 / TMEM / mbarrier wrappers (sm_100a).
+//
+// Operands live in shared memory in the canonical K-major, no-swizzle UMMA
+// layout: a "core matrix" is 8 rows x 16 bytes (8 bf16) stored contiguously
+// (128 B); the two 16-byte K chunks of one K=16 MMA slice sit LBO = 128 B
+// apart and consecutive 8-row groups SBO = 256 B apart, so one
+// 128-row x 16-K bf16 slice is 4 KB and slices are stacked every 4 KB.
+// Element (row m, k) of slice s is at byte
+//   s * 4096 + (m / 8) * 256 + ((k % 16) / 8) * 128 + (m % 8) * 16 + (k % 8) * 2.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace erxk {
+namespace tc {
+
+constexpr uint32_t kSliceBytes = 4096;  // 128 rows x 16 bf16
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// byte offset of bf16 element (m, k) inside a stack of 128-row K-slices
+__device__ __forceinline__ uint32_t kmajor_off(int m, int k) {
+    return uint32_t(k >> 4) * kSliceBytes + uint32_t(m >> 3) * 256u + uint32_t((k >> 3) & 1) * 128u +
+           uint32_t(m & 7) * 16u + uint32_t(k & 7) * 2u;
+}
+
+// Shared-memory matrix descriptor (K-major, SWIZZLE_NONE, version 1).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFF);          // start address  [0,14)
+    d |= uint64_t((128u >> 4) & 0x3FFF) << 16;     // LBO            [16,30)
+    d |= uint64_t((256u >> 4) & 0x3FFF) << 32;     // SBO            [32,46)
+    d |= uint64_t(1) << 46;                        // version        [46,48)
+    // base_offset 0, lbo_mode 0, layout_type SWIZZLE_NONE (0) at [61,64)
+    return d;
+}
+
+// Instruction descriptor: kind::f16, A = B = BF16, D = F32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
+    return (1u << 4)                     // c_format F32
+           | (1u << 7)                   // a_format BF16
+           | (1u << 10)                  // b_format BF16
+           | (uint32_t(N >> 3) << 17)    // n_dim
+           | (uint32_t(M >> 4) << 24);   // m_dim
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// Completion of all previously issued tcgen05 ops of this thread -> one mbarrier arrival.
+__device__ __forceinline__ void mma_commit(uint64_t* mbar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+        smem_u32(mbar)));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mbar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
+        "r"(phase));
+}
+
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::); }
+
+// TMEM allocation by one full warp; the base address lands in *slot.
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(slot)),
+                 "n"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+}
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_free(uint32_t base) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(base), "n"(kCols));
+}
+
+// 32 lanes x 32b, 16 consecutive columns: thread t of the warp gets row (lane base + t).
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Split fp32 values into three bf16 planes (hi + mid + lo == v to ~2^-24
+// relative): the "bf16x3" operand of the 6-product fp32-accurate MMA.
+__device__ __forceinline__ void split3_bf16x2(float a, float b, uint32_t& h, uint32_t& m, uint32_t& l) {
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));
+    const float ha = __uint_as_float(h << 16), hb = __uint_as_float(h & 0xFFFF0000u);
+    const float ra = a - ha, rb = b - hb;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(m) : "f"(rb), "f"(ra));
+    const float ma = __uint_as_float(m << 16), mb = __uint_as_float(m & 0xFFFF0000u);
+    const float sa = ra - ma, sb = rb - mb;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(sb), "f"(sa));
+}
+
+}  // namespace tc
+}  // namespace erxk
