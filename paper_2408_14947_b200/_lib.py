@@ -22,6 +22,7 @@ ERX_ERR_STATE = 17
 NUM_KERNELS = 5
 KERNEL_NAMES = ("stats", "scan", "factor", "score", "normalize")
 OPT_FACTOR_PRECISION = 1
+OPT_STATS_TENSOR = 2
 
 
 class ErxConfigC(C.Structure):

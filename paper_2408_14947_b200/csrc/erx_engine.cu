@@ -57,6 +57,7 @@ struct erx_engine {
     erxk::StatsLaunch sl{};
     erxk::ScoreLaunch sc{};
     int factor_req = 0;   // requested factor precision (0 auto, 32, 64)
+    int stats_tensor = 1;  // 1: tcgen05 stats kernel where eligible, 0: FFMA kernel
     int factor_prec = 0;  // precision in use (0 = blocked fp64 global path)
 
     // device buffers, capacity S*T lines
@@ -238,7 +239,12 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     const Geometry& g = e->geo;
     const int L = int(e->S * n);
     const int line_base = int(e->lines_seen * e->S);
-    timed(e, ERX_KERNEL_STATS, [&] { erxk::launch_stats(g, e->sl, x, int(n), int(in_stride), L, e->d_stats, e->stream); });
+    timed(e, ERX_KERNEL_STATS, [&] {
+        if (e->stats_tensor && erxk::stats_tc_eligible(g))
+            erxk::launch_stats_tc(g, x, int(n), int(in_stride), L, e->d_stats, e->stream);
+        else
+            erxk::launch_stats(g, e->sl, x, int(n), int(in_stride), L, e->d_stats, e->stream);
+    });
     timed(e, ERX_KERNEL_SCAN, [&] {
         erxk::launch_scan(g, e->d_stats, e->d_prior, e->d_state[e->cur], e->d_state[e->cur ^ 1], int(e->S), int(n),
                           e->initialized ? 1 : 0, e->cfg.alpha, e->cfg.use_incremental, e->welford_n, e->stream);
@@ -599,6 +605,10 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
 uint64_t erx_launch_count(const erx_engine* e) { return e->launches; }
 
 int erx_set_option(erx_engine* e, int option, int64_t value) {
+    if (option == ERX_OPT_STATS_TENSOR) {
+        e->stats_tensor = value ? 1 : 0;
+        return ERX_OK;
+    }
     if (option == ERX_OPT_FACTOR_PRECISION) {
         if (value != 0 && value != 1 && value != 32 && value != 64)
             return fail(e, ERX_ERR_CONFIG, "factor precision: 0, 1, 32 or 64");
@@ -615,6 +625,7 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
 
 int64_t erx_get_option(const erx_engine* e, int option) {
     if (option == ERX_OPT_FACTOR_PRECISION) return e->d_stats ? e->factor_prec : e->factor_req;
+    if (option == ERX_OPT_STATS_TENSOR) return (e->stats_tensor && e->d_stats && erxk::stats_tc_eligible(e->geo)) ? 1 : 0;
     return -1;
 }
 

@@ -72,7 +72,12 @@ size_t whiten_floats_per_line(const Geometry& g);
 int factor_precision(const Geometry& g, int requested);
 size_t factor_smem(const Geometry& g, int precision);
 
-// Host launchers (erx_kernels.cu).  All asynchronous on `st`.
+// tcgen05 stats kernel (k_stats_tc.cu): no_srp, 32 < D <= 128, B % 4 == 0.
+bool stats_tc_eligible(const Geometry& g);
+void launch_stats_tc(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
+                     double* stats, cudaStream_t st);
+
+// Host launchers.  All asynchronous on `st`.
 void launch_stats(const Geometry& g, const StatsLaunch& sl, const float* x, int n_per_stream, int in_stride,
                   int n_lines_total, double* stats, cudaStream_t st);
 void launch_scan(const Geometry& g, const double* stats, double* prior, const double* state_in, double* state_out,

@@ -243,6 +243,13 @@ class Engine:
         """0 auto, 32 or 64 (see ERX_OPT_FACTOR_PRECISION in include/erx_b200.h)."""
         self._check(self._lib.erx_set_option(self._h, L.OPT_FACTOR_PRECISION, bits))
 
+    def set_stats_tensor(self, on: bool):
+        """Use the tcgen05 stats kernel where eligible (default) or force the FFMA kernel."""
+        self._check(self._lib.erx_set_option(self._h, L.OPT_STATS_TENSOR, int(on)))
+
+    def stats_tensor(self) -> bool:
+        return bool(self._lib.erx_get_option(self._h, L.OPT_STATS_TENSOR))
+
     def factor_precision(self) -> int:
         return int(self._lib.erx_get_option(self._h, L.OPT_FACTOR_PRECISION))
 

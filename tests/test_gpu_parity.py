@@ -209,6 +209,23 @@ def test_factor_kernel_variants(pkg, oracle, cid, n_lines, prec):
     check_gates(oracle, raw_g[0], norm_g[0], raw_o, norm_o, mask=mask, warm=warm, label=f"c{cid} factor{prec}")
 
 
+@pytest.mark.parametrize("tensor", [True, False])
+def test_stats_kernel_variants(pkg, oracle, tensor):
+    """tcgen05 (bf16x3 split, 6 products) and FFMA line statistics both meet the gates."""
+    spec = pkg.gen_spec(3, 5)
+    lines, mask = pkg.gen_lines(spec, 0, 200)
+    cfg = pkg.ErxConfig(no_srp=True, alpha=0.1, buffer_len=60)
+    eng = pkg.Engine(cfg, spec.bands, window_lines=32)
+    eng.set_stats_tensor(tensor)
+    eng.push(lines[None], 0)
+    eng.finish()
+    assert eng.stats_tensor() == tensor
+    _, wu, raw_g, norm_g = eng.pop()
+    raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), lines)
+    warm = np.broadcast_to(wu[:, None], raw_o.shape)
+    check_gates(oracle, raw_g[0], norm_g[0], raw_o, norm_o, mask=mask, warm=warm, label=f"stats tensor={tensor}")
+
+
 # ---------------------------------------------------------------- contract edges
 def test_state_matches_oracle(pkg, oracle):
     spec = pkg.gen_spec(0)
