@@ -131,9 +131,10 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
  * kernel).  erx_get_option reports the precision in
  * use once the first line has fixed the geometry (0 = blocked fp64 path). */
 #define ERX_OPT_FACTOR_PRECISION 1
-/* ERX_OPT_STATS_TENSOR: 1 (default) runs line_stats on the tcgen05 tensor
- * cores where eligible (full covariance, 32 < D <= 128), 0 forces the FFMA
- * kernel.  erx_get_option reports whether the tensor kernel is in use. */
+/* ERX_OPT_STATS_TENSOR: 1 runs line_stats on the tcgen05 tensor cores where
+ * eligible (full covariance, 32 < D <= 128; bf16x3 split, 6 products), 0
+ * (default) the FFMA kernel.  erx_get_option reports whether the tensor
+ * kernel is in use. */
 #define ERX_OPT_STATS_TENSOR 2
 int erx_set_option(erx_engine* e, int option, int64_t value);
 int64_t erx_get_option(const erx_engine* e, int option);

@@ -57,7 +57,10 @@ struct erx_engine {
     erxk::StatsLaunch sl{};
     erxk::ScoreLaunch sc{};
     int factor_req = 0;   // requested factor precision (0 auto, 32, 64)
-    int stats_tensor = 1;  // 1: tcgen05 stats kernel where eligible, 0: FFMA kernel
+    // 1: tcgen05 bf16x3 stats kernel where eligible.  Off by default: the tensor
+    // core's fp32 accumulation truncates (measured -1.8e-8 relative per MMA,
+    // tools/tc_bias.py), which biases K in the noise subspace past the 1e-5 gate.
+    int stats_tensor = 0;
     int factor_prec = 0;  // precision in use (0 = blocked fp64 global path)
 
     // device buffers, capacity S*T lines
