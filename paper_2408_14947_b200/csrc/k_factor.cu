@@ -330,37 +330,47 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
     const double* K = prior + size_t(line) * g.SE + D;
     double eps = eps0;
     int fail;
+    const int ntri = D * (D + 1) / 2;
     while (true) {
-        for (int i = warp; i < Dp; i += nw)
-            for (int j = lane; j <= i; j += 32)
-                A[i * LD + j] = (i < D) ? float(K[tri(i, j)] + (i == j ? eps : 0.0)) : (i == j ? 1.f : 0.f);
-        if (tid == 0) s_fail = -1;
+        // fill: coalesced reads of the packed fp64 K (many loads in flight), padding = identity
+        for (int idx = tid; idx < ntri; idx += nt) {
+            int i = int((sqrtf(8.f * idx + 1.f) - 1.f) * 0.5f);
+            while (i * (i + 1) / 2 > idx) --i;
+            while ((i + 1) * (i + 2) / 2 <= idx) ++i;
+            const int j = idx - i * (i + 1) / 2;
+            A[i * LD + j] = float(__ldg(K + idx) + (i == j ? eps : 0.0));
+        }
+        for (int i = D + tid; i < Dp; i += nt)
+            for (int j = 0; j <= i; ++j) A[i * LD + j] = (i == j) ? 1.f : 0.f;
         __syncthreads();
+        fail = -1;
         for (int k = 0; k < nb; ++k) {
             const int k0 = k * kBlk;
             float* Bk = A + k0 * LD + k0;
-            if (warp == 0) {  // (a) diagonal block, lanes 0..7 own its rows
-                for (int j = 0; j < kBlk; ++j) {
-                    __syncwarp();
-                    const float djj = Bk[j * LD + j];
-                    if (!(djj > 0.f)) {
-                        if (lane == 0) s_fail = k0 + j;
-                        break;
-                    }
-                    const float s = sqrtf(djj);
-                    __syncwarp();
-                    if (lane > j && lane < kBlk) Bk[lane * LD + j] /= s;
-                    __syncwarp();
-                    if (lane == j) Bk[j * LD + j] = s;
-                    if (lane > j && lane < kBlk) {
-                        const float l = Bk[lane * LD + j];
-                        for (int c = j + 1; c <= lane; ++c) Bk[lane * LD + c] -= l * Bk[c * LD + j];
-                    }
+            // (a) every thread factors the 8x8 diagonal block in registers (redundant, no barrier;
+            //     the pivot test is uniform across the CTA)
+            float L[kBlk][kBlk], rd[kBlk];
+#pragma unroll
+            for (int r = 0; r < kBlk; ++r) ld8(Bk + r * LD, L[r]);
+#pragma unroll
+            for (int j = 0; j < kBlk; ++j) {
+                float d = L[j][j];
+#pragma unroll
+                for (int l = 0; l < j; ++l) d -= L[j][l] * L[j][l];
+                if (!(d > 0.f) && fail < 0) fail = k0 + j;
+                const float s = sqrtf(d);
+                L[j][j] = s;
+                rd[j] = 1.f / s;
+#pragma unroll
+                for (int r = j + 1; r < kBlk; ++r) {
+                    float v = L[r][j];
+#pragma unroll
+                    for (int l = 0; l < j; ++l) v -= L[r][l] * L[j][l];
+                    L[r][j] = v * rd[j];
                 }
             }
-            __syncthreads();
-            if (s_fail >= 0) break;
-            // (b) panel: L_Ik = A_Ik L_kk^{-T}, one row per thread
+            if (fail >= 0) break;
+            // (b) panel: L_Ik = A_Ik L_kk^{-T}, one row per thread, L_kk from registers
             for (int i = k0 + kBlk + tid; i < Dp; i += nt) {
                 float* row = A + i * LD + k0;
                 float a[kBlk], x[kBlk];
@@ -369,10 +379,18 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
                 for (int c = 0; c < kBlk; ++c) {
                     float s = a[c];
 #pragma unroll
-                    for (int l = 0; l < c; ++l) s -= x[l] * Bk[c * LD + l];
-                    x[c] = s / Bk[c * LD + c];
+                    for (int l = 0; l < c; ++l) s -= x[l] * L[c][l];
+                    x[c] = s * rd[c];
                 }
                 st8(row, x);
+            }
+            if (warp == nw - 1) {  // the factored diagonal block (lower part) for the inverse phase
+#pragma unroll
+                for (int r = 0; r < kBlk; ++r)
+                    if (lane == r) {
+#pragma unroll
+                        for (int c = 0; c <= r; ++c) Bk[r * LD + c] = L[r][c];
+                    }
             }
             __syncthreads();
             // (c) trailing update A_IJ -= L_Ik L_Jk^T, k < J <= I < nb
@@ -400,7 +418,6 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
             }
             __syncthreads();
         }
-        fail = s_fail;
         if (fail < 0) break;
         const double next = eps * 10.0;
         if (!(next <= 1e-1 * (1.0 + 1e-9))) break;
@@ -422,54 +439,76 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
     for (int k = 0; k < nb; ++k) {
         const int k0 = k * kBlk;
         const float* Bk = A + k0 * LD + k0;
-        if (warp == 0 && lane < kBlk) {  // Dinv = L_kk^{-1}, lane = column
-            float x[kBlk];
-#pragma unroll
-            for (int r = 0; r < kBlk; ++r) {
-                float s = (r == lane) ? 1.f : 0.f;
-#pragma unroll
-                for (int l = 0; l < r; ++l) s -= Bk[r * LD + l] * x[l];
-                x[r] = (r < lane) ? 0.f : s / Bk[r * LD + r];
-            }
-#pragma unroll
-            for (int r = 0; r < kBlk; ++r) Dinv[r * kBlk + lane] = x[r];
-        }
+        // block column k below the diagonal is overwritten by this step's update: keep a copy
         for (int idx = tid; idx < (nb - k - 1) * 64; idx += nt) {
             const int I = k + 1 + idx / 64, rc = idx % 64;
             Lc[I * 64 + rc] = A[(I * kBlk + rc / kBlk) * LD + k0 + rc % kBlk];
         }
-        __syncthreads();
-        // finalise block row k: X_kJ = Dinv T_kJ (J < k), X_kk = Dinv
+        // finalise block row k: X_kJ = L_kk^{-1} T_kJ (J < k), X_kk = L_kk^{-1}; the 8x8 inverse
+        // is recomputed in registers by each finalising thread (no serial phase, no barrier)
         for (int J = tid; J <= k; J += nt) {
+            float Lr[kBlk][kBlk], Di[kBlk][kBlk], rl[kBlk];
+#pragma unroll
+            for (int r = 0; r < kBlk; ++r) {
+                ld8(Bk + r * LD, Lr[r]);
+                rl[r] = 1.f / Lr[r][r];
+            }
+#pragma unroll
+            for (int c = 0; c < kBlk; ++c) {
+                Di[c][c] = rl[c];
+#pragma unroll
+                for (int r = c + 1; r < kBlk; ++r) {
+                    float s = 0.f;
+#pragma unroll
+                    for (int l = c; l < r; ++l) s = fmaf(Lr[r][l], Di[l][c], s);
+                    Di[r][c] = -s * rl[r];
+                }
+#pragma unroll
+                for (int r = 0; r < c; ++r) Di[r][c] = 0.f;
+            }
             float t[kBlk][kBlk];
             if (J == k) {
 #pragma unroll
-                for (int r = 0; r < kBlk; ++r) ld8(Dinv + r * kBlk, t[r]);
-            } else {
-                float s[kBlk][kBlk];
+                for (int r = 0; r < kBlk; ++r)
 #pragma unroll
-                for (int r = 0; r < kBlk; ++r) ld8(A + (k0 + r) * LD + J * kBlk, s[r]);
+                    for (int c = 0; c < kBlk; ++c) t[r][c] = Di[r][c];
+            } else {
 #pragma unroll
                 for (int r = 0; r < kBlk; ++r)
 #pragma unroll
-                    for (int c = 0; c < kBlk; ++c) {
-                        float v = 0.f;
+                    for (int c = 0; c < kBlk; ++c) t[r][c] = 0.f;
 #pragma unroll
-                        for (int l = 0; l <= r; ++l) v = fmaf(Dinv[r * kBlk + l], s[l][c], v);
-                        t[r][c] = v;
-                    }
+                for (int l = 0; l < kBlk; ++l) {
+                    float srow[kBlk];
+                    ld8(A + (k0 + l) * LD + J * kBlk, srow);
+#pragma unroll
+                    for (int r = l; r < kBlk; ++r)
+#pragma unroll
+                        for (int c = 0; c < kBlk; ++c) t[r][c] = fmaf(Di[r][l], srow[c], t[r][c]);
+                }
             }
+            // X_kk goes to scratch: other finalising threads are still reading L_kk
+            float* dst = (J == k) ? Dinv : A + k0 * LD + J * kBlk;
+            const int ld = (J == k) ? kBlk : LD;
 #pragma unroll
-            for (int r = 0; r < kBlk; ++r) st8(A + (k0 + r) * LD + J * kBlk, t[r]);
+            for (int r = 0; r < kBlk; ++r) st8(dst + r * ld, t[r]);
         }
         __syncthreads();
+        if (tid == 0)
+            for (int r = 0; r < kBlk; ++r) {
+                float row[kBlk];
+                ld8(Dinv + r * kBlk, row);
+                st8(A + (k0 + r) * LD + k0, row);
+            }
         // update block rows I > k: T_IJ -= L_Ik X_kJ (J < k), T_Ik = -L_Ik X_kk
         const int ntask = (nb - k - 1) * (k + 1);
         for (int q = tid; q < ntask; q += nt) {
             const int I = k + 1 + q / (k + 1), J = q % (k + 1);
             float xk[kBlk][kBlk];
+            const float* xs = (J == k) ? Dinv : A + k0 * LD + J * kBlk;
+            const int xld = (J == k) ? kBlk : LD;
 #pragma unroll
-            for (int l = 0; l < kBlk; ++l) ld8(A + (k0 + l) * LD + J * kBlk, xk[l]);
+            for (int l = 0; l < kBlk; ++l) ld8(xs + l * xld, xk[l]);
 #pragma unroll
             for (int r = 0; r < kBlk; ++r) {
                 float a[kBlk], acc[kBlk];
