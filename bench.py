@@ -109,8 +109,10 @@ def algorithmic(cfgd, D, srp_nnz=0):
         "flops_line": 2 * P * D * D + D ** 3 / 3 + proj,
         "stats": dict(flops=P * tri + proj, bytes=4 * P * B),
         "score": dict(flops=P * tri + proj, bytes=4 * P * B + 4 * P),
-        "factor": dict(flops=2 * D ** 3 / 3, bytes=0),
-        "scan": dict(flops=0, bytes=0),
+        # factor: Cholesky + triangular inverse; reads the packed fp64 prior, writes packed fp32 W blocks
+        "factor": dict(flops=2 * D ** 3 / 3, bytes=8 * D * (D + 1) // 2 + 4 * 64 * ((D + 7) // 8) * ((D + 15) // 8) // 2),
+        # scan: reads [c | s | S] and writes the pre-update (mu, K) per line, fp64
+        "scan": dict(flops=0, bytes=8 * (2 * D + D * (D + 1) // 2) + 8 * (D + D * (D + 1) // 2)),
         "normalize": dict(flops=0, bytes=8 * P),
     }
 
@@ -302,7 +304,8 @@ def secondary_measurements(pkg, args):
     out = {}
     try:
         cfgd = CONFIGS[1]
-        P, B, T = cfgd["pixels"], cfgd["bands"], 64
+        # a single stream only parallelises across the lines of a window: use a deep lag
+        P, B, T = cfgd["pixels"], cfgd["bands"], 256
         for mode in ("full", "srp"):
             n_win = max(2, math.ceil(2 * L2_BYTES / (T * P * B * 4)))
             host = build_pool(pkg, 1, [0], n_win * T)

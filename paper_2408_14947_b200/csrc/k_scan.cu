@@ -38,19 +38,34 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
     if (!incremental) {
         const double om = 1.0 - alpha;
         double state = in[e];
-        for (int t = 0; t < n; ++t) {
-            const size_t l = l0 + t;
-            const double* st = stats + l * SS;
-            const double stat = (e < D) ? mu_hat(st, e) : k_hat(st);
-            double pr;
-            if (!initialized && t == 0) {
-                pr = stat;
-                state = stat;
-            } else {
-                pr = state;
-                state = __dadd_rn(__dmul_rn(om, state), __dmul_rn(alpha, stat));
+        // the line statistics do not depend on the recurrence: load them 8 lines at a time
+        // (independent loads in flight), then run the sequential EMA in registers
+        constexpr int kB = 8;
+        for (int t0 = 0; t0 < n; t0 += kB) {
+            double stat[kB];
+#pragma unroll
+            for (int u = 0; u < kB; ++u) {
+                const int t = t0 + u;
+                stat[u] = 0.0;
+                if (t < n) {
+                    const double* st = stats + (l0 + t) * SS;
+                    stat[u] = (e < D) ? mu_hat(st, e) : k_hat(st);
+                }
             }
-            prior[l * g.SE + e] = pr;
+#pragma unroll
+            for (int u = 0; u < kB; ++u) {
+                const int t = t0 + u;
+                if (t >= n) break;
+                double pr;
+                if (!initialized && t == 0) {
+                    pr = stat[u];
+                    state = stat[u];
+                } else {
+                    pr = state;
+                    state = __dadd_rn(__dmul_rn(om, state), __dmul_rn(alpha, stat[u]));
+                }
+                prior[(l0 + t) * g.SE + e] = pr;
+            }
         }
         st_out[size_t(s) * g.SE + e] = state;
     } else {
