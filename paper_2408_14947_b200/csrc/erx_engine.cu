@@ -56,6 +56,9 @@ struct erx_engine {
     Geometry geo{};
     erxk::StatsLaunch sl{};
     erxk::ScoreLaunch sc{};
+    erxk::SmallLaunch smp{};
+    bool small = false;       // D <= 16: stats_small / score_small path
+    float* d_vcache = nullptr;  // [S*T][D][P] centred projections (small path)
     int factor_req = 0;   // requested factor precision (0 auto, 32, 64)
     // 1: tcgen05 bf16x3 stats kernel where eligible.  Off by default: the tensor
     // core's fp32 accumulation truncates (measured -1.8e-8 relative per MMA,
@@ -181,6 +184,8 @@ void free_window(erx_engine* e) {
     cudaFree(e->d_raw);
     cudaFree(e->d_norm);
     cudaFree(e->d_status);
+    cudaFree(e->d_vcache);
+    e->d_vcache = nullptr;
     cudaFreeHost(e->h_lines);
     cudaFreeHost(e->h_raw);
     cudaFreeHost(e->h_norm);
@@ -214,6 +219,8 @@ int configure(erx_engine* e, uint32_t P) {
     g.srp_scale = e->srp_scale;
     e->sl = erxk::plan_stats(g);
     e->sc = erxk::plan_score(g);
+    e->small = erxk::small_path(g);
+    if (e->small) e->smp = erxk::plan_small(g);
     e->factor_prec = erxk::factor_precision(g, e->factor_req);
     const size_t L = size_t(e->S) * e->T;
     CU(cudaMalloc(&e->d_stats, L * (g.SE + g.D) * sizeof(double)));  // [c | s | S] per line
@@ -223,6 +230,7 @@ int configure(erx_engine* e, uint32_t P) {
     CU(cudaMalloc(&e->d_raw, L * P * sizeof(float)));
     CU(cudaMalloc(&e->d_norm, L * P * sizeof(float)));
     CU(cudaMalloc(&e->d_status, L * sizeof(int)));
+    if (e->small) CU(cudaMalloc(&e->d_vcache, L * size_t(g.D) * P * sizeof(float)));
     return ERX_OK;
 }
 
@@ -243,7 +251,9 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     const int L = int(e->S * n);
     const int line_base = int(e->lines_seen * e->S);
     timed(e, ERX_KERNEL_STATS, [&] {
-        if (e->stats_tensor && erxk::stats_tc_eligible(g))
+        if (e->small)
+            erxk::launch_stats_small(g, e->smp, x, int(n), int(in_stride), L, e->d_stats, e->d_vcache, e->stream);
+        else if (e->stats_tensor && erxk::stats_tc_eligible(g))
             erxk::launch_stats_tc(g, x, int(n), int(in_stride), L, e->d_stats, e->stream);
         else
             erxk::launch_stats(g, e->sl, x, int(n), int(in_stride), L, e->d_stats, e->stream);
@@ -256,10 +266,17 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
         erxk::launch_factor(g, e->d_prior, L, e->cfg.epsilon, e->d_work, e->d_white, e->d_status, e->d_latch,
                             line_base, e->factor_prec, e->stream);
     });
-    timed(e, ERX_KERNEL_SCORE, [&] {
-        erxk::launch_score(g, e->sc, x, int(n), int(in_stride), e->d_prior, e->d_white, L, raw, e->stream);
-    });
-    timed(e, ERX_KERNEL_NORMALIZE, [&] { erxk::launch_normalize(g, raw, L, norm, e->stream); });
+    if (e->small) {  // score + normalisation fused
+        timed(e, ERX_KERNEL_SCORE, [&] {
+            erxk::launch_score_small(g, e->smp, e->d_stats, e->d_prior, e->d_white, e->d_vcache, L, raw, norm,
+                                     e->stream);
+        });
+    } else {
+        timed(e, ERX_KERNEL_SCORE, [&] {
+            erxk::launch_score(g, e->sc, x, int(n), int(in_stride), e->d_prior, e->d_white, L, raw, e->stream);
+        });
+        timed(e, ERX_KERNEL_NORMALIZE, [&] { erxk::launch_normalize(g, raw, L, norm, e->stream); });
+    }
     cudaError_t r = cudaGetLastError();
     if (r != cudaSuccess) return fail(e, ERX_ERR_DEVICE, std::string("kernel launch: ") + cudaGetErrorString(r));
     e->cur ^= 1;

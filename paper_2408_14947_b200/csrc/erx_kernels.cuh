@@ -52,6 +52,21 @@ struct StatsLaunch {
     size_t smem;     // dynamic shared memory bytes
 };
 
+struct SmallLaunch {
+    int CH;             // pixels staged per chunk
+    size_t smem_stats;
+    size_t smem_score;
+};
+
+// small-D path (k_small.cu): D <= 16, one CTA per line, fused normalisation
+bool small_path(const Geometry& g);
+SmallLaunch plan_small(const Geometry& g);
+void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x, int n_per_stream, int in_stride,
+                        int n_lines_total, double* stats, float* vcache, cudaStream_t st);
+void launch_score_small(const Geometry& g, const SmallLaunch& sm, const double* stats, const double* prior,
+                        const float* whiten, const float* vcache, int n_lines_total, float* raw, float* norm,
+                        cudaStream_t st);
+
 struct ScoreLaunch {
     int npairs;      // row-block pairs {s, nb-1-s}
     int G;           // pixel lanes per pair

@@ -1,0 +1,290 @@
+// k_small.cu — the small-D path (D <= 16: the paper's default d = 5 sparse
+// random projection, and narrow multispectral lines such as configs[2]).
+// At these sizes the path is HBM-bound, so the design goal is
+// one read of each line:
+//
+//   stats_small  one CTA per line: cp.async-stages pixel rows, projects each
+//                pixel once (project_line, projection.hpp:31-34; fp64 sums),
+//                accumulates sum(v) and sum(v v^T) with v = z - c
+//                (line_stats, erx.hpp:38-40), and writes v (fp32, dim-major)
+//                to a small per-line cache — D floats per pixel instead of B;
+//   score_small  one CTA per line: reads the cache, whitens with W = L^{-1}
+//                (forward_substitute, linalg.hpp:21), and z-normalises the
+//                line in the same kernel (normalize_scores, detector.hpp:29-32).
+//
+// Stats slot contract as k_stats.cu: [c | s | S packed lower], fp64.
+#include "erx_common.cuh"
+
+namespace erxk {
+namespace {
+
+constexpr int kSmallThreads = 256;
+
+struct SmallArgs {
+    Geometry g;
+    SmallLaunch sm;
+    const float* x;
+    int n;
+    int in_stride;
+    double* stats;
+    float* vcache;  // [line][D][P]
+};
+
+template <int DM>
+__global__ void __launch_bounds__(kSmallThreads) stats_small_kernel(SmallArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Geometry& g = a.g;
+    const SmallLaunch& sm = a.sm;
+    const int line = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int D = g.D, B = g.B;
+    const int NT = D * (D + 1) / 2;
+    float* stage = reinterpret_cast<float*>(smem);                                  // [2][CH][B]
+    double* red = reinterpret_cast<double*>(smem + align_up(size_t(2) * sm.CH * B * 4, 16));  // [8 warps][D + NT]
+    __shared__ double cen_s[16];
+    const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
+    float* vc = a.vcache + size_t(line) * D * g.P;
+
+    // centre: fp64 mean of the first min(32, P) projected pixels
+    if (tid < D) {
+        const int n0 = min(32, g.P);
+        double s = 0.0;
+        for (int pp = 0; pp < n0; ++pp) s += proj(g, xl + size_t(pp) * B, tid);
+        cen_s[tid] = s / double(n0);
+    }
+    const bool use_async = (B % 4) == 0;
+    const int nchunks = (g.P + sm.CH - 1) / sm.CH;
+    auto issue = [&](int c) {
+        const int c0 = c * sm.CH, n = min(sm.CH, g.P - c0);
+        float* dst = stage + (c & 1) * sm.CH * B;
+        const float* src = xl + size_t(c0) * B;
+        if (use_async) {
+            for (int i = tid; i < n * B / 4; i += kSmallThreads) cp_async16(dst + 4 * i, src + 4 * i);
+        } else {
+            for (int i = tid; i < n * B; i += kSmallThreads) dst[i] = __ldg(src + i);
+        }
+        cp_async_commit();
+    };
+    issue(0);
+    __syncthreads();
+    constexpr int DT = DM * (DM + 1) / 2;
+    double cen[DM];
+#pragma unroll
+    for (int j = 0; j < DM; ++j) cen[j] = (j < D) ? cen_s[j] : 0.0;
+
+    // per-thread partial sums over its pixels (few per thread), fp32 -> fp64 at the end
+    float s1[DM], s2[DT];
+#pragma unroll
+    for (int j = 0; j < DM; ++j) s1[j] = 0.f;
+#pragma unroll
+    for (int j = 0; j < DT; ++j) s2[j] = 0.f;
+
+    for (int c = 0; c < nchunks; ++c) {
+        if (c + 1 < nchunks) {
+            issue(c + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const int c0 = c * sm.CH, n = min(sm.CH, g.P - c0);
+        const float* st = stage + (c & 1) * sm.CH * B;
+        for (int pp = tid; pp < n; pp += kSmallThreads) {
+            const float* row = st + pp * B;
+            float v[DM];
+#pragma unroll
+            for (int j = 0; j < DM; ++j) {
+                v[j] = 0.f;
+                if (j < D) {
+                    double z;
+                    if (g.srp) {
+                        z = 0.0;
+                        for (int k = g.srp_ptr[j]; k < g.srp_ptr[j + 1]; ++k)
+                            z += double(row[g.srp_band[k]]) * double(g.srp_w[k]);
+                        z *= g.srp_scale;
+                    } else {
+                        z = double(row[j]);
+                    }
+                    v[j] = float(z - cen[j]);
+                    vc[size_t(j) * g.P + c0 + pp] = v[j];
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < DM; ++i) {
+                s1[i] += v[i];
+#pragma unroll
+                for (int j = 0; j <= i; ++j) s2[i * (i + 1) / 2 + j] = fmaf(v[i], v[j], s2[i * (i + 1) / 2 + j]);
+            }
+        }
+        __syncthreads();  // stage (c & 1) is refilled at iteration c + 1
+    }
+    // block reduction in fp64: warp shuffles, then one partial per warp in smem (fixed order)
+    const int lane = tid & 31, warp = tid >> 5;
+    const int NV = D + NT;
+#pragma unroll
+    for (int i = 0; i < DM; ++i) {
+        if (i < D) {
+            double v = double(s1[i]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) red[warp * NV + i] = v;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < DM; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j)
+            if (i < D) {
+                double v = double(s2[i * (i + 1) / 2 + j]);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) red[warp * NV + D + i * (i + 1) / 2 + j] = v;
+            }
+    __syncthreads();
+    double* out = a.stats + size_t(line) * (g.SE + D);
+    for (int q = tid; q < NV; q += kSmallThreads) {
+        double v = 0.0;
+        for (int w = 0; w < kSmallThreads / 32; ++w) v += red[w * NV + q];
+        if (q < D) {
+            out[q] = cen_s[q];
+            out[D + q] = v;
+        } else {
+            out[2 * D + (q - D)] = v;
+        }
+    }
+}
+
+// score_small + normalize.  W: packed lower 8x8 blocks (column-major inside).
+template <int DM>
+__global__ void __launch_bounds__(kSmallThreads) score_small_kernel(Geometry g, const double* __restrict__ stats,
+                                                                    const double* __restrict__ prior,
+                                                                    const float* __restrict__ Wp,
+                                                                    const float* __restrict__ vcache,
+                                                                    float* __restrict__ raw, float* __restrict__ norm) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float* dl = reinterpret_cast<float*>(smem);  // raw scores of the line [P]
+    __shared__ float Wd[16][16];
+    __shared__ float off[16];
+    __shared__ double red[8];
+    __shared__ double mean_s, sd_s;
+    const int line = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int D = g.D;
+    const int nblk = g.nb * (g.nb + 1) / 2;
+    const float* W = Wp + size_t(line) * nblk * 64;
+    for (int i = tid; i < 256; i += kSmallThreads) {
+        const int r = i / 16, c = i % 16;
+        float w = 0.f;
+        if (r < D && c <= r) {
+            const int I = r / 8, J = c / 8;
+            w = W[(I * (I + 1) / 2 + J) * 64 + (c % 8) * 8 + (r % 8)];
+        }
+        Wd[r][c] = w;
+    }
+    if (tid < 16) {
+        // u = v - (mu_{t-1} - c_t): v is centred on this line's c_t
+        const double* st = stats + size_t(line) * (g.SE + D);
+        const double* pr = prior + size_t(line) * g.SE;
+        off[tid] = (tid < D) ? float(pr[tid] - st[tid]) : 0.f;
+    }
+    __syncthreads();
+    const float* vc = vcache + size_t(line) * D * g.P;
+    double ls = 0.0;
+    for (int p = tid; p < g.P; p += kSmallThreads) {
+        float u[DM];
+#pragma unroll
+        for (int j = 0; j < DM; ++j) u[j] = (j < D) ? vc[size_t(j) * g.P + p] - off[j] : 0.f;
+        float ssq = 0.f;
+#pragma unroll
+        for (int r = 0; r < DM; ++r) {
+            if (r < D) {
+                float m = 0.f;
+#pragma unroll
+                for (int c = 0; c <= r; ++c) m = fmaf(Wd[r][c], u[c], m);
+                ssq = fmaf(m, m, ssq);
+            }
+        }
+        const float d = sqrtf(ssq);
+        dl[p] = d;
+        raw[size_t(line) * g.P + p] = d;
+        ls += double(d);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
+    if (lane == 0) red[warp] = ls;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kSmallThreads / 32; ++w) s += red[w];
+        mean_s = s / double(g.P);
+    }
+    __syncthreads();
+    const double mean = mean_s;
+    double lv = 0.0;
+    for (int p = tid; p < g.P; p += kSmallThreads) {
+        const double dd = double(dl[p]) - mean;
+        lv += dd * dd;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lv += __shfl_xor_sync(0xffffffffu, lv, o);
+    __syncthreads();
+    if (lane == 0) red[warp] = lv;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kSmallThreads / 32; ++w) s += red[w];
+        sd_s = sqrt(s / double(g.P));
+    }
+    __syncthreads();
+    const double sd = sd_s;
+    for (int p = tid; p < g.P; p += kSmallThreads)
+        norm[size_t(line) * g.P + p] = (sd < 1e-12) ? 0.f : float((double(dl[p]) - mean) / sd);
+}
+
+}  // namespace
+
+bool small_path(const Geometry& g) { return g.D <= 16; }
+
+SmallLaunch plan_small(const Geometry& g) {
+    SmallLaunch sm{};
+    int ch = 256;
+    while (ch > 32 && size_t(2) * ch * g.B * 4 > 100 * 1024) ch /= 2;
+    sm.CH = ch;
+    const int NT = g.D * (g.D + 1) / 2;
+    sm.smem_stats = align_up(size_t(2) * ch * g.B * 4, 16) + size_t(8) * (g.D + NT) * 8;
+    sm.smem_score = size_t(g.P) * 4;
+    return sm;
+}
+
+void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x, int n_per_stream, int in_stride,
+                        int n_lines_total, double* stats, float* vcache, cudaStream_t st) {
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaFuncSetAttribute(stats_small_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(stats_small_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_done = true;
+    }
+    SmallArgs a{g, sm, x, n_per_stream, in_stride, stats, vcache};
+    if (g.D <= 8)
+        stats_small_kernel<8><<<n_lines_total, kSmallThreads, sm.smem_stats, st>>>(a);
+    else
+        stats_small_kernel<16><<<n_lines_total, kSmallThreads, sm.smem_stats, st>>>(a);
+}
+
+void launch_score_small(const Geometry& g, const SmallLaunch& sm, const double* stats, const double* prior,
+                        const float* whiten, const float* vcache, int n_lines_total, float* raw, float* norm,
+                        cudaStream_t st) {
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaFuncSetAttribute(score_small_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(score_small_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_done = true;
+    }
+    if (g.D <= 8)
+        score_small_kernel<8><<<n_lines_total, kSmallThreads, sm.smem_score, st>>>(g, stats, prior, whiten, vcache,
+                                                                                   raw, norm);
+    else
+        score_small_kernel<16><<<n_lines_total, kSmallThreads, sm.smem_score, st>>>(g, stats, prior, whiten, vcache,
+                                                                                    raw, norm);
+}
+
+}  // namespace erxk
