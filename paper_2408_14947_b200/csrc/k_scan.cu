@@ -38,34 +38,41 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
     if (!incremental) {
         const double om = 1.0 - alpha;
         double state = in[e];
-        // the line statistics do not depend on the recurrence: load them 8 lines at a time
-        // (independent loads in flight), then run the sequential EMA in registers
-        constexpr int kB = 8;
-        for (int t0 = 0; t0 < n; t0 += kB) {
-            double stat[kB];
+        // the line statistics do not depend on the recurrence: they are loaded a batch
+        // ahead (double-buffered registers) so the sequential EMA never waits on memory
+        constexpr int kB = 16;
+        double cur[kB], nxt[kB];
+        auto load = [&](int t0, double* buf) {
 #pragma unroll
             for (int u = 0; u < kB; ++u) {
                 const int t = t0 + u;
-                stat[u] = 0.0;
+                buf[u] = 0.0;
                 if (t < n) {
                     const double* st = stats + (l0 + t) * SS;
-                    stat[u] = (e < D) ? mu_hat(st, e) : k_hat(st);
+                    buf[u] = (e < D) ? mu_hat(st, e) : k_hat(st);
                 }
             }
+        };
+        load(0, cur);
+        for (int t0 = 0; t0 < n; t0 += kB) {
+            if (t0 + kB < n) load(t0 + kB, nxt);
 #pragma unroll
             for (int u = 0; u < kB; ++u) {
                 const int t = t0 + u;
-                if (t >= n) break;
-                double pr;
-                if (!initialized && t == 0) {
-                    pr = stat[u];
-                    state = stat[u];
-                } else {
-                    pr = state;
-                    state = __dadd_rn(__dmul_rn(om, state), __dmul_rn(alpha, stat[u]));
+                if (t < n) {
+                    double pr;
+                    if (!initialized && t == 0) {
+                        pr = cur[u];
+                        state = cur[u];
+                    } else {
+                        pr = state;
+                        state = __dadd_rn(__dmul_rn(om, state), __dmul_rn(alpha, cur[u]));
+                    }
+                    prior[(l0 + t) * g.SE + e] = pr;
                 }
-                prior[(l0 + t) * g.SE + e] = pr;
             }
+#pragma unroll
+            for (int u = 0; u < kB; ++u) cur[u] = nxt[u];
         }
         st_out[size_t(s) * g.SE + e] = state;
     } else {

@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(kSmallThreads) stats_small_kernel(SmallArgs a)
     const int NT = D * (D + 1) / 2;
     float* stage = reinterpret_cast<float*>(smem);                                  // [2][CH][B]
     double* red = reinterpret_cast<double*>(smem + align_up(size_t(2) * sm.CH * B * 4, 16));  // [8 warps][D + NT]
+    float* vs = reinterpret_cast<float*>(red + 8 * (D + NT));                                  // [CH][DM]
     __shared__ double cen_s[16];
     const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
     float* vc = a.vcache + size_t(line) * D * g.P;
@@ -68,9 +69,6 @@ __global__ void __launch_bounds__(kSmallThreads) stats_small_kernel(SmallArgs a)
     issue(0);
     __syncthreads();
     constexpr int DT = DM * (DM + 1) / 2;
-    double cen[DM];
-#pragma unroll
-    for (int j = 0; j < DM; ++j) cen[j] = (j < D) ? cen_s[j] : 0.0;
 
     // per-thread partial sums over its pixels (few per thread), fp32 -> fp64 at the end
     float s1[DM], s2[DT];
@@ -89,26 +87,30 @@ __global__ void __launch_bounds__(kSmallThreads) stats_small_kernel(SmallArgs a)
         __syncthreads();
         const int c0 = c * sm.CH, n = min(sm.CH, g.P - c0);
         const float* st = stage + (c & 1) * sm.CH * B;
-        for (int pp = tid; pp < n; pp += kSmallThreads) {
+        // projection: one (dim, pixel) item per thread, consecutive threads on consecutive
+        // pixels of one dim (coalesced cache writes, warp-uniform nnz loop bounds)
+        for (int i = tid; i < n * D; i += kSmallThreads) {
+            const int j = i / n, pp = i - j * n;
             const float* row = st + pp * B;
+            double z;
+            if (g.srp) {
+                z = 0.0;
+                for (int k = g.srp_ptr[j]; k < g.srp_ptr[j + 1]; ++k)
+                    z += double(row[g.srp_band[k]]) * double(g.srp_w[k]);
+                z *= g.srp_scale;
+            } else {
+                z = double(row[j]);
+            }
+            const float v = float(z - cen_s[j]);
+            vs[pp * DM + j] = v;
+            vc[size_t(j) * g.P + c0 + pp] = v;
+        }
+        __syncthreads();
+        // rank-1 updates: one pixel per thread
+        for (int pp = tid; pp < n; pp += kSmallThreads) {
             float v[DM];
 #pragma unroll
-            for (int j = 0; j < DM; ++j) {
-                v[j] = 0.f;
-                if (j < D) {
-                    double z;
-                    if (g.srp) {
-                        z = 0.0;
-                        for (int k = g.srp_ptr[j]; k < g.srp_ptr[j + 1]; ++k)
-                            z += double(row[g.srp_band[k]]) * double(g.srp_w[k]);
-                        z *= g.srp_scale;
-                    } else {
-                        z = double(row[j]);
-                    }
-                    v[j] = float(z - cen[j]);
-                    vc[size_t(j) * g.P + c0 + pp] = v[j];
-                }
-            }
+            for (int j = 0; j < DM; ++j) v[j] = (j < D) ? vs[pp * DM + j] : 0.f;
 #pragma unroll
             for (int i = 0; i < DM; ++i) {
                 s1[i] += v[i];
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(kSmallThreads) stats_small_kernel(SmallArgs a)
                 for (int j = 0; j <= i; ++j) s2[i * (i + 1) / 2 + j] = fmaf(v[i], v[j], s2[i * (i + 1) / 2 + j]);
             }
         }
-        __syncthreads();  // stage (c & 1) is refilled at iteration c + 1
+        __syncthreads();  // stage (c & 1) and vs are refilled at iteration c + 1
     }
     // block reduction in fp64: warp shuffles, then one partial per warp in smem (fixed order)
     const int lane = tid & 31, warp = tid >> 5;
@@ -247,10 +249,10 @@ bool small_path(const Geometry& g) { return g.D <= 16; }
 SmallLaunch plan_small(const Geometry& g) {
     SmallLaunch sm{};
     int ch = 256;
-    while (ch > 32 && size_t(2) * ch * g.B * 4 > 100 * 1024) ch /= 2;
+    while (ch > 32 && size_t(2) * ch * g.B * 4 > 120 * 1024) ch /= 2;
     sm.CH = ch;
     const int NT = g.D * (g.D + 1) / 2;
-    sm.smem_stats = align_up(size_t(2) * ch * g.B * 4, 16) + size_t(8) * (g.D + NT) * 8;
+    sm.smem_stats = align_up(size_t(2) * ch * g.B * 4, 16) + size_t(8) * (g.D + NT) * 8 + size_t(ch) * 16 * 4;
     sm.smem_score = size_t(g.P) * 4;
     return sm;
 }
@@ -260,12 +262,15 @@ void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x
     static bool attr_done = false;
     if (!attr_done) {
         cudaFuncSetAttribute(stats_small_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(stats_small_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(stats_small_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_done = true;
     }
     SmallArgs a{g, sm, x, n_per_stream, in_stride, stats, vcache};
     if (g.D <= 8)
         stats_small_kernel<8><<<n_lines_total, kSmallThreads, sm.smem_stats, st>>>(a);
+    else if (g.D <= 12)
+        stats_small_kernel<12><<<n_lines_total, kSmallThreads, sm.smem_stats, st>>>(a);
     else
         stats_small_kernel<16><<<n_lines_total, kSmallThreads, sm.smem_stats, st>>>(a);
 }
