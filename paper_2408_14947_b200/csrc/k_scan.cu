@@ -42,16 +42,21 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
         // ahead (double-buffered registers) so the sequential EMA never waits on memory
         constexpr int kB = 16;
         double cur[kB], nxt[kB];
+        // branch-free loads (clamped line index, select after) so all 3 x kB loads issue back to back
+        const bool is_mu = e < D;
+        const int o0 = is_mu ? e : 2 * D + (e - D), o1 = D + a, o2 = D + b;
         auto load = [&](int t0, double* buf) {
+            double x0[kB], x1[kB], x2[kB];
 #pragma unroll
             for (int u = 0; u < kB; ++u) {
-                const int t = t0 + u;
-                buf[u] = 0.0;
-                if (t < n) {
-                    const double* st = stats + (l0 + t) * SS;
-                    buf[u] = (e < D) ? mu_hat(st, e) : k_hat(st);
-                }
+                const double* st = stats + (l0 + min(t0 + u, n - 1)) * SS;
+                x0[u] = __ldg(st + o0);
+                x1[u] = __ldg(st + o1);
+                x2[u] = __ldg(st + o2);
             }
+#pragma unroll
+            for (int u = 0; u < kB; ++u)
+                buf[u] = is_mu ? x0[u] + x1[u] * invP : (x0[u] - x1[u] * x2[u] * invP) * invP1;
         };
         load(0, cur);
         for (int t0 = 0; t0 < n; t0 += kB) {

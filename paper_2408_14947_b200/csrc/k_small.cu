@@ -43,16 +43,10 @@ __global__ void __launch_bounds__(kSmallThreads) stats_small_kernel(SmallArgs a)
     double* red = reinterpret_cast<double*>(smem + align_up(size_t(2) * sm.CH * B * 4, 16));  // [8 warps][D + NT]
     float* vs = reinterpret_cast<float*>(red + 8 * (D + NT));                                  // [CH][DM]
     __shared__ double cen_s[16];
+    __shared__ double zc[32 * 16];
     const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
     float* vc = a.vcache + size_t(line) * D * g.P;
-
-    // centre: fp64 mean of the first min(32, P) projected pixels
-    if (tid < D) {
-        const int n0 = min(32, g.P);
-        double s = 0.0;
-        for (int pp = 0; pp < n0; ++pp) s += proj(g, xl + size_t(pp) * B, tid);
-        cen_s[tid] = s / double(n0);
-    }
+    const int n0 = min(32, g.P);
     const bool use_async = (B % 4) == 0;
     const int nchunks = (g.P + sm.CH - 1) / sm.CH;
     auto issue = [&](int c) {
@@ -87,6 +81,29 @@ __global__ void __launch_bounds__(kSmallThreads) stats_small_kernel(SmallArgs a)
         __syncthreads();
         const int c0 = c * sm.CH, n = min(sm.CH, g.P - c0);
         const float* st = stage + (c & 1) * sm.CH * B;
+        if (c == 0) {  // centre: fp64 mean of the first min(32, P) projected pixels, from the staged chunk
+            for (int i = tid; i < n0 * D; i += kSmallThreads) {
+                const int j = i / n0, pp = i - j * n0;
+                const float* row = st + pp * B;
+                double z;
+                if (g.srp) {
+                    z = 0.0;
+                    for (int k = g.srp_ptr[j]; k < g.srp_ptr[j + 1]; ++k)
+                        z += double(row[g.srp_band[k]]) * double(g.srp_w[k]);
+                    z *= g.srp_scale;
+                } else {
+                    z = double(row[j]);
+                }
+                zc[pp * 16 + j] = z;
+            }
+            __syncthreads();
+            if (tid < D) {
+                double s = 0.0;
+                for (int pp = 0; pp < n0; ++pp) s += zc[pp * 16 + tid];
+                cen_s[tid] = s / double(n0);
+            }
+            __syncthreads();
+        }
         // projection: one (dim, pixel) item per thread, consecutive threads on consecutive
         // pixels of one dim (coalesced cache writes, warp-uniform nnz loop bounds)
         for (int i = tid; i < n * D; i += kSmallThreads) {

@@ -74,17 +74,17 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
             const int r = i / (g.Dp - g.D), c = g.D + i % (g.Dp - g.D);
             vbuf0[size_t(r) * g.Dp + spos(c, g.nb)] = 0.f;
         }
-    {
-        const int n0 = min(32, g.P);
-        for (int j = tid; j < g.D; j += nt) {
+    const int n0 = min(32, g.P);
+    const bool use_async = !g.srp && (g.B % 4 == 0);
+    for (int j = tid; j < g.D; j += nt) {
+        colsum[j] = 0.0;
+        if (!use_async) {  // projected centre straight from global; the async path takes it from chunk 0
             double s = 0.0;
             for (int pp = 0; pp < n0; ++pp) s += proj(g, xl + size_t(pp) * g.B, j);
             cen[j] = float(s / double(n0));
-            colsum[j] = 0.0;
         }
     }
 
-    const bool use_async = !g.srp && (g.B % 4 == 0);
     const int nchunks = (g.P + sl.CH - 1) / sl.CH;
     auto issue = [&](int c) {
         const int c0 = c * sl.CH, n = min(sl.CH, g.P - c0);
@@ -121,8 +121,13 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
             for (int k = 0; k < 4; ++k) {
                 const int j = tid + k * nt;
                 if (j < g.D) {
-                    const float cj = cen[j];
                     float* col = v + spos(j, g.nb);
+                    if (c == 0) {  // centre: fp64 mean of the first n0 staged (raw) pixels of this dim
+                        double s = 0.0;
+                        for (int pp = 0; pp < n0; ++pp) s += double(col[size_t(pp) * g.Dp]);
+                        cen[j] = float(s / double(n0));
+                    }
+                    const float cj = cen[j];
                     float s = 0.f;
 #pragma unroll 4
                     for (int pp = 0; pp < n; ++pp) {
