@@ -244,16 +244,18 @@ def run_ours(args):
         e2e_steps = max(2, min(args.steps, 8))
         eng2 = pkg.Engine(cfg, B, n_streams=S, window_lines=T, device=local)
         eng2.set_factor_precision(args.factor)
+        eng2.set_host_groups(args.host_groups)
         pin = torch.from_numpy(np.ascontiguousarray(host[:, :T])).pin_memory().numpy()
+        outb = (np.empty((S, T, P)), np.empty((S, T, P)))  # caller-owned ScoredLine payload buffers
         for k in range(2):
             eng2.push(pin, k * T)
-            eng2.pop()
+            eng2.pop(out=outb)
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
         for k in range(e2e_steps):
             eng2.push(pin, (k + 2) * T)
-            _, _, r_, n_ = eng2.pop()
+            _, _, r_, n_ = eng2.pop(out=outb)
         el = time.perf_counter() - t0
         el_t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{local}")
         if dist:
@@ -437,6 +439,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip the single-stream / latency side measurements")
+    ap.add_argument("--host-groups", type=int, default=0, help="stream groups per host window (0 auto)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -136,6 +136,11 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
  * (default) the FFMA kernel.  erx_get_option reports whether the tensor
  * kernel is in use. */
 #define ERX_OPT_STATS_TENSOR 2
+/* ERX_OPT_HOST_GROUPS: stream groups per host window of erx_push_host (the
+ * host->device copy of group g+1 overlaps the kernels of group g).  0 (default)
+ * sizes the groups at >= 8 MB of input each, 1..8 forces that count
+ * (results are identical for every count: streams are independent). */
+#define ERX_OPT_HOST_GROUPS 3
 int erx_set_option(erx_engine* e, int option, int64_t value);
 int64_t erx_get_option(const erx_engine* e, int option);
 

@@ -23,6 +23,7 @@ NUM_KERNELS = 5
 KERNEL_NAMES = ("stats", "scan", "factor", "score", "normalize")
 OPT_FACTOR_PRECISION = 1
 OPT_STATS_TENSOR = 2
+OPT_HOST_GROUPS = 3
 
 
 class ErxConfigC(C.Structure):

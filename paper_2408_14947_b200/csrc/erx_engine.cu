@@ -13,7 +13,9 @@
 #include <cstdio>
 #include <cstring>
 #include <deque>
+#include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/erx_b200.h"
@@ -24,12 +26,22 @@ using erxk::Geometry;
 
 namespace {
 
+// One scored window of the drop-in path: pinned host arrays [S][n][P] written
+// by the device-to-host copies directly (no re-packing per line).  Blocks are
+// recycled through the engine's pool once every row has been popped.
+struct ResultBlock {
+    float* raw = nullptr;
+    float* norm = nullptr;
+    size_t cap = 0;  // floats per array
+    uint32_t n = 0, P = 0;
+};
+
 struct ScoredRow {
     int64_t index;
     uint8_t warmup;
-    uint32_t P;               // pixels of this line
-    std::vector<float> raw;   // [S][P]
-    std::vector<float> norm;  // [S][P]
+    uint32_t P;                        // pixels of this line
+    uint32_t t;                        // row of the block
+    std::shared_ptr<ResultBlock> blk;  // raw / norm of all streams
 };
 
 struct Timing {
@@ -81,9 +93,14 @@ struct erx_engine {
 
     // pinned host staging (drop-in path)
     float* h_lines = nullptr;
-    float* h_raw = nullptr;
-    float* h_norm = nullptr;
     int* h_status = nullptr;
+    // drop-in path streams: host->device copies and device->host result copies run
+    // beside the compute stream, one stream group at a time (run_host_window)
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    static constexpr int kMaxGroups = 8;
+    cudaEvent_t ev_in[kMaxGroups] = {}, ev_out[kMaxGroups] = {};
+    std::vector<ResultBlock*> block_pool;
+    int host_groups = 0;  // ERX_OPT_HOST_GROUPS (0 auto)
 
     bool initialized = false;
     int64_t lines_seen = 0;
@@ -187,15 +204,19 @@ void free_window(erx_engine* e) {
     cudaFree(e->d_vcache);
     e->d_vcache = nullptr;
     cudaFreeHost(e->h_lines);
-    cudaFreeHost(e->h_raw);
-    cudaFreeHost(e->h_norm);
     cudaFreeHost(e->h_status);
     e->d_lines = nullptr;
     e->d_stats = e->d_prior = e->d_work = nullptr;
     e->d_white = e->d_raw = e->d_norm = nullptr;
     e->d_status = nullptr;
-    e->h_lines = e->h_raw = e->h_norm = nullptr;
+    e->h_lines = nullptr;
     e->h_status = nullptr;
+}
+
+void free_block(ResultBlock* b) {
+    cudaFreeHost(b->raw);
+    cudaFreeHost(b->norm);
+    delete b;
 }
 
 // (Re)plan the geometry for P pixels and size the window buffers.
@@ -239,74 +260,151 @@ int ensure_host_staging(erx_engine* e) {
     const size_t L = size_t(e->S) * e->T;
     CU(cudaMalloc(&e->d_lines, L * e->P * e->B * sizeof(float)));
     CU(cudaMallocHost(&e->h_lines, L * e->P * e->B * sizeof(float)));
-    CU(cudaMallocHost(&e->h_raw, L * e->P * sizeof(float)));
-    CU(cudaMallocHost(&e->h_norm, L * e->P * sizeof(float)));
     CU(cudaMallocHost(&e->h_status, L * sizeof(int)));
+    if (!e->h2d) {
+        CU(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
+        CU(cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking));
+        for (int k = 0; k < erx_engine::kMaxGroups; ++k) {
+            CU(cudaEventCreateWithFlags(&e->ev_in[k], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&e->ev_out[k], cudaEventDisableTiming));
+        }
+    }
     return ERX_OK;
 }
 
-// Enqueue the five-kernel window pipeline for n lines per stream.
-int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride, float* raw, float* norm) {
+// A pinned result block for S x n lines of P pixels (pool-recycled).
+std::shared_ptr<ResultBlock> take_block(erx_engine* e, uint32_t n) {
+    const size_t need = size_t(e->S) * e->T * e->P;
+    ResultBlock* b = nullptr;
+    while (!e->block_pool.empty() && !b) {
+        b = e->block_pool.back();
+        e->block_pool.pop_back();
+        if (b->cap < need) {
+            free_block(b);
+            b = nullptr;
+        }
+    }
+    if (!b) {
+        b = new ResultBlock();
+        if (cudaMallocHost(&b->raw, need * sizeof(float)) != cudaSuccess ||
+            cudaMallocHost(&b->norm, need * sizeof(float)) != cudaSuccess) {
+            free_block(b);
+            return nullptr;
+        }
+        b->cap = need;
+    }
+    b->n = n;
+    b->P = e->P;
+    auto* pool = &e->block_pool;
+    return std::shared_ptr<ResultBlock>(b, [pool](ResultBlock* x) { pool->push_back(x); });
+}
+
+// Enqueue the five-kernel window pipeline for n lines of streams [s0, s0 + ns).
+// x points at stream 0 of the window (stream stride in_stride lines); every
+// per-line buffer holds line (s, t) at s * n + t, so a stream range is a
+// contiguous line range and the groups are independent (no cross-stream data).
+int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride, float* raw, float* norm,
+                   uint32_t s0, uint32_t ns) {
     const Geometry& g = e->geo;
-    const int L = int(e->S * n);
-    const int line_base = int(e->lines_seen * e->S);
+    const int L = int(ns * n);
+    const size_t l0 = size_t(s0) * n;
+    const int line_base = int(e->lines_seen * e->S + l0);
+    const float* xg = x + size_t(s0) * in_stride * g.P * g.B;
+    double* stats = e->d_stats + l0 * (g.SE + g.D);
+    double* prior = e->d_prior + l0 * g.SE;
+    const double* st_in = e->d_state[e->cur] + size_t(s0) * g.SE;
+    double* st_out = e->d_state[e->cur ^ 1] + size_t(s0) * g.SE;
+    double* work = e->d_work ? e->d_work + l0 * 2 * size_t(g.Dp) * g.Dp : nullptr;
+    float* white = e->d_white + l0 * erxk::whiten_floats_per_line(g);
+    float* vcache = e->d_vcache ? e->d_vcache + l0 * size_t(g.D) * g.P : nullptr;
+    int* status = e->d_status + l0;
+    float* rawg = raw + l0 * g.P;
+    float* normg = norm + l0 * g.P;
     timed(e, ERX_KERNEL_STATS, [&] {
         if (e->small)
-            erxk::launch_stats_small(g, e->smp, x, int(n), int(in_stride), L, e->d_stats, e->d_vcache, e->stream);
+            erxk::launch_stats_small(g, e->smp, xg, int(n), int(in_stride), L, stats, vcache, e->stream);
         else if (e->stats_tensor && erxk::stats_tc_eligible(g))
-            erxk::launch_stats_tc(g, x, int(n), int(in_stride), L, e->d_stats, e->stream);
+            erxk::launch_stats_tc(g, xg, int(n), int(in_stride), L, stats, e->stream);
         else
-            erxk::launch_stats(g, e->sl, x, int(n), int(in_stride), L, e->d_stats, e->stream);
+            erxk::launch_stats(g, e->sl, xg, int(n), int(in_stride), L, stats, e->stream);
     });
     timed(e, ERX_KERNEL_SCAN, [&] {
-        erxk::launch_scan(g, e->d_stats, e->d_prior, e->d_state[e->cur], e->d_state[e->cur ^ 1], int(e->S), int(n),
-                          e->initialized ? 1 : 0, e->cfg.alpha, e->cfg.use_incremental, e->welford_n, e->stream);
+        erxk::launch_scan(g, stats, prior, st_in, st_out, int(ns), int(n), e->initialized ? 1 : 0, e->cfg.alpha,
+                          e->cfg.use_incremental, e->welford_n, e->stream);
     });
     timed(e, ERX_KERNEL_FACTOR, [&] {
-        erxk::launch_factor(g, e->d_prior, L, e->cfg.epsilon, e->d_work, e->d_white, e->d_status, e->d_latch,
-                            line_base, e->factor_prec, e->stream);
+        erxk::launch_factor(g, prior, L, e->cfg.epsilon, work, white, status, e->d_latch, line_base, e->factor_prec,
+                            e->stream);
     });
     if (e->small) {  // score + normalisation fused
         timed(e, ERX_KERNEL_SCORE, [&] {
-            erxk::launch_score_small(g, e->smp, e->d_stats, e->d_prior, e->d_white, e->d_vcache, L, raw, norm,
-                                     e->stream);
+            erxk::launch_score_small(g, e->smp, stats, prior, white, vcache, L, rawg, normg, e->stream);
         });
     } else {
         timed(e, ERX_KERNEL_SCORE, [&] {
-            erxk::launch_score(g, e->sc, x, int(n), int(in_stride), e->d_prior, e->d_white, L, raw, e->stream);
+            erxk::launch_score(g, e->sc, xg, int(n), int(in_stride), prior, white, L, rawg, e->stream);
         });
-        timed(e, ERX_KERNEL_NORMALIZE, [&] { erxk::launch_normalize(g, raw, L, norm, e->stream); });
+        timed(e, ERX_KERNEL_NORMALIZE, [&] { erxk::launch_normalize(g, rawg, L, normg, e->stream); });
     }
     cudaError_t r = cudaGetLastError();
     if (r != cudaSuccess) return fail(e, ERX_ERR_DEVICE, std::string("kernel launch: ") + cudaGetErrorString(r));
+    return ERX_OK;
+}
+
+// The window's state transition, once all of its stream groups are enqueued.
+void commit_window(erx_engine* e, uint32_t n) {
     e->cur ^= 1;
     if (e->cfg.use_incremental) e->welford_n += int64_t(n) * e->P;
     e->initialized = true;
     e->lines_seen += n;
-    return ERX_OK;
 }
 
-// Score the staged partial/full window of the drop-in path and queue results.
-int run_host_window(erx_engine* e, bool staged = true) {
+// Stream groups of one host window: enough that the copy of group g+1 hides
+// the kernels of group g, few enough that each copy stays >= ~8 MB (full
+// PCIe efficiency) and each launch still fills the GPU.
+uint32_t host_groups(const erx_engine* e, uint32_t n) {
+    if (e->host_groups > 0) return std::min<uint32_t>(uint32_t(e->host_groups), e->S);
+    const double bytes = double(e->S) * n * e->P * e->B * sizeof(float);
+    uint32_t G = uint32_t(std::min(double(erx_engine::kMaxGroups), std::floor(bytes / (8.0 * 1024 * 1024))));
+    return std::max<uint32_t>(1, std::min<uint32_t>(G, e->S));
+}
+
+// Score one window of the drop-in path and queue its rows.  src holds stream s
+// at src + s * src_pitch floats (n lines of P x B each): the caller's buffer
+// (direct path) or the pinned staging buffer.  The window is cut into stream
+// groups: group g's host->device copy (h2d stream) overlaps the kernels of
+// group g-1 (compute stream), whose results drain on the d2h stream.  The call
+// returns when the whole window is scored and queued (the per-call contract of
+// the reference's process(); the source buffer is free again on return).
+int run_host_window(erx_engine* e, const float* src, size_t src_pitch) {
     if (e->fill == 0) return ERX_OK;
     const uint32_t n = e->fill;
     const size_t line_f = size_t(e->P) * e->B;
-    if (!staged) {
-        // already copied to d_lines by the caller
-    } else if (n == e->T) {
-        CU(cudaMemcpyAsync(e->d_lines, e->h_lines, size_t(e->S) * e->T * line_f * sizeof(float),
-                           cudaMemcpyHostToDevice, e->stream));
-    } else {
-        for (uint32_t s = 0; s < e->S; ++s)
-            CU(cudaMemcpyAsync(e->d_lines + size_t(s) * e->T * line_f, e->h_lines + size_t(s) * e->T * line_f,
-                               n * line_f * sizeof(float), cudaMemcpyHostToDevice, e->stream));
+    auto blk = take_block(e, n);
+    if (!blk) return fail(e, ERX_ERR_DEVICE, "cudaMallocHost (result block)");
+    const uint32_t G = host_groups(e, n);
+    for (uint32_t gi = 0; gi < G; ++gi) {
+        const uint32_t s0 = uint32_t(uint64_t(e->S) * gi / G), s1 = uint32_t(uint64_t(e->S) * (gi + 1) / G);
+        const uint32_t ns = s1 - s0;
+        if (!ns) continue;
+        CU(cudaMemcpy2DAsync(e->d_lines + size_t(s0) * e->T * line_f, size_t(e->T) * line_f * sizeof(float),
+                             src + size_t(s0) * src_pitch, src_pitch * sizeof(float), n * line_f * sizeof(float), ns,
+                             cudaMemcpyHostToDevice, e->h2d));
+        CU(cudaEventRecord(e->ev_in[gi], e->h2d));
+        CU(cudaStreamWaitEvent(e->stream, e->ev_in[gi], 0));
+        int st = enqueue_window(e, e->d_lines, n, e->T, e->d_raw, e->d_norm, s0, ns);
+        if (st) return st;
+        CU(cudaEventRecord(e->ev_out[gi], e->stream));
+        CU(cudaStreamWaitEvent(e->d2h, e->ev_out[gi], 0));
+        const size_t l0 = size_t(s0) * n, nl = size_t(ns) * n;
+        CU(cudaMemcpyAsync(blk->raw + l0 * e->P, e->d_raw + l0 * e->P, nl * e->P * sizeof(float),
+                           cudaMemcpyDeviceToHost, e->d2h));
+        CU(cudaMemcpyAsync(blk->norm + l0 * e->P, e->d_norm + l0 * e->P, nl * e->P * sizeof(float),
+                           cudaMemcpyDeviceToHost, e->d2h));
+        CU(cudaMemcpyAsync(e->h_status + l0, e->d_status + l0, nl * sizeof(int), cudaMemcpyDeviceToHost, e->d2h));
     }
-    int st = enqueue_window(e, e->d_lines, n, e->T, e->d_raw, e->d_norm);
-    if (st) return st;
-    const size_t L = size_t(e->S) * n;
-    CU(cudaMemcpyAsync(e->h_raw, e->d_raw, L * e->P * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
-    CU(cudaMemcpyAsync(e->h_norm, e->d_norm, L * e->P * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
-    CU(cudaMemcpyAsync(e->h_status, e->d_status, L * sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+    commit_window(e, n);
+    CU(cudaStreamSynchronize(e->d2h));
     CU(cudaStreamSynchronize(e->stream));
     // first failing line in emission order (then stream order)
     int bad_t = -1, bad_piv = -1;
@@ -323,14 +421,8 @@ int run_host_window(erx_engine* e, bool staged = true) {
         row.index = e->win_index[t];
         row.warmup = (row.index < int64_t(e->cfg.buffer_len)) ? 1 : 0;
         row.P = e->P;
-        row.raw.resize(size_t(e->S) * e->P);
-        row.norm.resize(size_t(e->S) * e->P);
-        for (uint32_t s = 0; s < e->S; ++s) {
-            std::memcpy(row.raw.data() + size_t(s) * e->P, e->h_raw + (size_t(s) * n + t) * e->P,
-                        e->P * sizeof(float));
-            std::memcpy(row.norm.data() + size_t(s) * e->P, e->h_norm + (size_t(s) * n + t) * e->P,
-                        e->P * sizeof(float));
-        }
+        row.t = t;
+        row.blk = blk;
         e->queue.push_back(std::move(row));
     }
     e->fill = 0;
@@ -342,6 +434,10 @@ int run_host_window(erx_engine* e, bool staged = true) {
                         std::to_string(e->win_index[bad_t]) + " after epsilon escalation to 1e-1");
     }
     return ERX_OK;
+}
+
+int run_staged_window(erx_engine* e) {
+    return run_host_window(e, e->h_lines, size_t(e->T) * e->P * e->B);
 }
 
 }  // namespace
@@ -449,6 +545,10 @@ void erx_destroy(erx_engine* e) {
     if (!e) return;
     cudaSetDevice(e->device);
     if (e->stream) cudaStreamSynchronize(e->stream);
+    if (e->d2h) cudaStreamSynchronize(e->d2h);
+    e->queue.clear();  // returns result blocks to the pool
+    for (auto* b : e->block_pool) free_block(b);
+    e->block_pool.clear();
     free_window(e);
     cudaFree(e->d_srp_ptr);
     cudaFree(e->d_srp_band);
@@ -463,6 +563,12 @@ void erx_destroy(erx_engine* e) {
     for (auto ev : e->event_pool) cudaEventDestroy(ev);
     for (auto ev : e->user_ev)
         if (ev) cudaEventDestroy(ev);
+    for (int k = 0; k < erx_engine::kMaxGroups; ++k) {
+        if (e->ev_in[k]) cudaEventDestroy(e->ev_in[k]);
+        if (e->ev_out[k]) cudaEventDestroy(e->ev_out[k]);
+    }
+    if (e->h2d) cudaStreamDestroy(e->h2d);
+    if (e->d2h) cudaStreamDestroy(e->d2h);
     if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
 }
@@ -480,7 +586,7 @@ int erx_push_host(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t
     if (pixels < 2) return fail(e, ERX_ERR_DATA, "a line needs p >= 2 pixels (1/(p-1) covariance)");  // erx.hpp:39
     if (n_lines == 0) return ERX_OK;
     if (pixels != e->P || !e->d_stats) {
-        int st = run_host_window(e);
+        int st = run_staged_window(e);
         if (st) return st;
         st = configure(e, pixels);
         if (st) return st;
@@ -492,12 +598,9 @@ int erx_push_host(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t
     while (i < n_lines) {
         if (e->fill == 0 && n_lines - i >= e->T) {
             // a whole window straight from the caller's buffer (pinned memory: DMA; pageable: staged by CUDA)
-            for (uint32_t s = 0; s < e->S; ++s)
-                CU(cudaMemcpyAsync(e->d_lines + size_t(s) * e->T * line_f, lines + (size_t(s) * n_lines + i) * line_f,
-                                   size_t(e->T) * line_f * sizeof(float), cudaMemcpyHostToDevice, e->stream));
             for (uint32_t k = 0; k < e->T; ++k) e->win_index[k] = first_index + int64_t(i + k);
             e->fill = e->T;
-            st = run_host_window(e, /*staged=*/false);
+            st = run_host_window(e, lines + size_t(i) * line_f, size_t(n_lines) * line_f);
             if (st) return st;
             i += e->T;
             continue;
@@ -509,7 +612,7 @@ int erx_push_host(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t
         e->fill += 1;
         i += 1;
         if (e->fill == e->T) {
-            st = run_host_window(e, true);
+            st = run_staged_window(e);
             if (st) return st;
         }
     }
@@ -518,7 +621,7 @@ int erx_push_host(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t
 
 int erx_finish(erx_engine* e) {
     if (e->failed) return fail(e, ERX_ERR_STATE, "engine is in a failed state: " + e->err);
-    return run_host_window(e);
+    return run_staged_window(e);
 }
 
 uint32_t erx_ready(const erx_engine* e) {
@@ -535,16 +638,41 @@ uint32_t erx_next_pixels(const erx_engine* e) { return e->queue.empty() ? 0u : e
 
 int erx_pop(erx_engine* e, uint32_t max_lines, int64_t* index, uint8_t* warmup, double* raw, double* norm) {
     const uint32_t n = std::min<uint32_t>(max_lines, erx_ready(e));
+    if (!n) return 0;
+    const size_t P = e->queue.front().P;
     for (uint32_t k = 0; k < n; ++k) {
         const ScoredRow& r = e->queue[k];
-        const size_t P = r.P;
         if (index) index[k] = r.index;
         if (warmup) warmup[k] = r.warmup;
-        for (uint32_t s = 0; s < e->S; ++s)
-            for (size_t p = 0; p < P; ++p) {
-                if (raw) raw[(size_t(s) * n + k) * P + p] = double(r.raw[size_t(s) * P + p]);
-                if (norm) norm[(size_t(s) * n + k) * P + p] = double(r.norm[size_t(s) * P + p]);
+    }
+    // widen fp32 -> fp64 (ScoredLine payload), streams split across host threads for big pops
+    auto widen = [&](uint32_t s_lo, uint32_t s_hi) {
+        for (uint32_t k = 0; k < n; ++k) {
+            const ScoredRow& r = e->queue[k];
+            const ResultBlock& b = *r.blk;
+            for (uint32_t s = s_lo; s < s_hi; ++s) {
+                const float* fr = b.raw + (size_t(s) * b.n + r.t) * P;
+                const float* fn = b.norm + (size_t(s) * b.n + r.t) * P;
+                double* dr = raw ? raw + (size_t(s) * n + k) * P : nullptr;
+                double* dn = norm ? norm + (size_t(s) * n + k) * P : nullptr;
+                if (dr)
+                    for (size_t p = 0; p < P; ++p) dr[p] = double(fr[p]);
+                if (dn)
+                    for (size_t p = 0; p < P; ++p) dn[p] = double(fn[p]);
             }
+        }
+    };
+    const size_t elems = size_t(e->S) * n * P;
+    const uint32_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const uint32_t nt = std::min<uint32_t>({e->S, 8u, hw, uint32_t(elems >> 18) + 1});
+    if (nt <= 1) {
+        widen(0, e->S);
+    } else {
+        std::vector<std::thread> pool;
+        for (uint32_t i = 1; i < nt; ++i)
+            pool.emplace_back(widen, uint32_t(uint64_t(e->S) * i / nt), uint32_t(uint64_t(e->S) * (i + 1) / nt));
+        widen(0, uint32_t(e->S / nt));
+        for (auto& th : pool) th.join();
     }
     for (uint32_t k = 0; k < n; ++k) e->queue.pop_front();
     return int(n);
@@ -560,7 +688,10 @@ int erx_run_device(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_
     if (e->fill) return fail(e, ERX_ERR_STATE, "host lines pending; call erx_finish first");
     int st = configure(e, pixels);
     if (st) return st;
-    return enqueue_window(e, d_lines, n_lines, n_lines, d_raw, d_norm);
+    st = enqueue_window(e, d_lines, n_lines, n_lines, d_raw, d_norm, 0, e->S);
+    if (st) return st;
+    commit_window(e, n_lines);
+    return ERX_OK;
 }
 
 int erx_sync(erx_engine* e) {
@@ -625,6 +756,11 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
 uint64_t erx_launch_count(const erx_engine* e) { return e->launches; }
 
 int erx_set_option(erx_engine* e, int option, int64_t value) {
+    if (option == ERX_OPT_HOST_GROUPS) {
+        if (value < 0 || value > erx_engine::kMaxGroups) return fail(e, ERX_ERR_CONFIG, "host groups: 0..8");
+        e->host_groups = int(value);
+        return ERX_OK;
+    }
     if (option == ERX_OPT_STATS_TENSOR) {
         e->stats_tensor = value ? 1 : 0;
         return ERX_OK;
@@ -645,6 +781,7 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
 
 int64_t erx_get_option(const erx_engine* e, int option) {
     if (option == ERX_OPT_FACTOR_PRECISION) return e->d_stats ? e->factor_prec : e->factor_req;
+    if (option == ERX_OPT_HOST_GROUPS) return e->host_groups;
     if (option == ERX_OPT_STATS_TENSOR) return (e->stats_tensor && e->d_stats && erxk::stats_tc_eligible(e->geo)) ? 1 : 0;
     return -1;
 }

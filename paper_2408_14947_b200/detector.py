@@ -198,13 +198,26 @@ class Engine:
     def ready(self) -> int:
         return int(self._lib.erx_ready(self._h))
 
-    def pop(self, max_lines: Optional[int] = None):
+    def pop(self, max_lines: Optional[int] = None, out=None):
+        """Pop the leading ready lines: (index[n], warmup[n], raw[S][n][P], norm[S][n][P]) fp64.
+
+        `out` = (raw, norm) preallocated C-contiguous fp64 arrays of at least n x P
+        per stream reuses caller memory (views of the first n lines are returned)."""
         n = self.ready() if max_lines is None else min(max_lines, self.ready())
         P = int(self._lib.erx_next_pixels(self._h))
         idx = np.zeros(n, np.int64)
         wu = np.zeros(n, np.uint8)
-        raw = np.zeros((self.n_streams, n, P))
-        norm = np.zeros((self.n_streams, n, P))
+        if out is not None:
+            raw_o, norm_o = out
+            need = self.n_streams * n * P
+            if raw_o.dtype != np.float64 or norm_o.dtype != np.float64 or raw_o.size < need or norm_o.size < need \
+                    or not raw_o.flags.c_contiguous or not norm_o.flags.c_contiguous:
+                raise DataError("pop(out=...) needs two C-contiguous float64 arrays of >= S*n*P elements")
+            raw = raw_o.reshape(-1)[:need].reshape(self.n_streams, n, P)
+            norm = norm_o.reshape(-1)[:need].reshape(self.n_streams, n, P)
+        else:
+            raw = np.empty((self.n_streams, n, P))
+            norm = np.empty((self.n_streams, n, P))
         got = self._lib.erx_pop(self._h, n, _p(idx, C.c_int64), _p(wu, C.c_uint8), _p(raw, C.c_double),
                                 _p(norm, C.c_double))
         if got < 0:
@@ -246,6 +259,10 @@ class Engine:
     def set_stats_tensor(self, on: bool):
         """Use the tcgen05 stats kernel where eligible (default) or force the FFMA kernel."""
         self._check(self._lib.erx_set_option(self._h, L.OPT_STATS_TENSOR, int(on)))
+
+    def set_host_groups(self, groups: int):
+        """Stream groups per host window (0 auto; see ERX_OPT_HOST_GROUPS)."""
+        self._check(self._lib.erx_set_option(self._h, L.OPT_HOST_GROUPS, int(groups)))
 
     def stats_tensor(self) -> bool:
         return bool(self._lib.erx_get_option(self._h, L.OPT_STATS_TENSOR))

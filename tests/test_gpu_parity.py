@@ -112,6 +112,27 @@ def test_batched_streams_equal_single_streams(pkg):
         assert np.array_equal(raw[s], single)
 
 
+@pytest.mark.parametrize("groups", [2, 3, 5])
+def test_host_stream_groups_bitwise(pkg, groups):
+    """erx_push_host cut into stream groups (copy of group g+1 overlapping the
+    kernels of group g) scores bit-identically to one group, full and partial windows."""
+    S, n = 5, 20
+    lines = np.stack([pkg.gen_lines(pkg.gen_spec(3, s), 0, n)[0] for s in range(S)])
+    cfg = pkg.ErxConfig(no_srp=True)
+    res = []
+    for G in (1, groups):
+        eng = pkg.Engine(cfg, 108, n_streams=S, window_lines=8)
+        eng.set_host_groups(G)
+        eng.push(lines[:, :13], 0)   # one direct window + 5 staged lines
+        eng.push(lines[:, 13:], 13)  # staged completion + partial tail
+        eng.finish()
+        out = (np.empty(S * n * 640), np.empty(S * n * 640))
+        res.append(eng.pop(out=out))
+        eng.close()
+    assert res[0][0].tolist() == list(range(n)) and res[1][0].tolist() == list(range(n))
+    assert np.array_equal(res[0][2], res[1][2]) and np.array_equal(res[0][3], res[1][3])
+
+
 def test_device_path_equals_host_path(pkg):
     import torch
 
