@@ -164,6 +164,7 @@ def run_ours(args):
     norm = torch.empty_like(raw)
     eng = pkg.Engine(cfg, B, n_streams=S, window_lines=T, device=local)
     eng.set_factor_precision(args.factor)
+    eng.set_stats_tensor(args.stats)
     D = eng.dims
 
     def step(k):
@@ -245,6 +246,7 @@ def run_ours(args):
         eng2 = pkg.Engine(cfg, B, n_streams=S, window_lines=T, device=local)
         eng2.set_factor_precision(args.factor)
         eng2.set_host_groups(args.host_groups)
+        eng2.set_stats_tensor(args.stats)
         pin = torch.from_numpy(np.ascontiguousarray(host[:, :T])).pin_memory().numpy()
         outb = (np.empty((S, T, P)), np.empty((S, T, P)))  # caller-owned ScoredLine payload buffers
         for k in range(2):
@@ -439,6 +441,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip the single-stream / latency side measurements")
+    ap.add_argument("--stats", type=int, default=0, choices=[0, 1, 2],
+                    help="line-statistics kernel: 0 FFMA, 1 tcgen05 bf16x3, 2 tcgen05 exact int8")
     ap.add_argument("--host-groups", type=int, default=0, help="stream groups per host window (0 auto)")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -323,7 +323,9 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     timed(e, ERX_KERNEL_STATS, [&] {
         if (e->small)
             erxk::launch_stats_small(g, e->smp, xg, int(n), int(in_stride), L, stats, vcache, e->stream);
-        else if (e->stats_tensor && erxk::stats_tc_eligible(g))
+        else if (e->stats_tensor == 2 && erxk::stats_i8_eligible(g))
+            erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, e->stream);
+        else if (e->stats_tensor == 1 && erxk::stats_tc_eligible(g))
             erxk::launch_stats_tc(g, xg, int(n), int(in_stride), L, stats, e->stream);
         else
             erxk::launch_stats(g, e->sl, xg, int(n), int(in_stride), L, stats, e->stream);
@@ -762,7 +764,8 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
         return ERX_OK;
     }
     if (option == ERX_OPT_STATS_TENSOR) {
-        e->stats_tensor = value ? 1 : 0;
+        if (value < 0 || value > 2) return fail(e, ERX_ERR_CONFIG, "stats tensor: 0, 1 or 2");
+        e->stats_tensor = int(value);
         return ERX_OK;
     }
     if (option == ERX_OPT_FACTOR_PRECISION) {
@@ -782,7 +785,12 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
 int64_t erx_get_option(const erx_engine* e, int option) {
     if (option == ERX_OPT_FACTOR_PRECISION) return e->d_stats ? e->factor_prec : e->factor_req;
     if (option == ERX_OPT_HOST_GROUPS) return e->host_groups;
-    if (option == ERX_OPT_STATS_TENSOR) return (e->stats_tensor && e->d_stats && erxk::stats_tc_eligible(e->geo)) ? 1 : 0;
+    if (option == ERX_OPT_STATS_TENSOR) {
+        if (!e->d_stats) return e->stats_tensor;
+        if (e->stats_tensor == 2 && erxk::stats_i8_eligible(e->geo)) return 2;
+        if (e->stats_tensor == 1 && erxk::stats_tc_eligible(e->geo)) return 1;
+        return 0;
+    }
     return -1;
 }
 

@@ -92,6 +92,11 @@ bool stats_tc_eligible(const Geometry& g);
 void launch_stats_tc(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
                      double* stats, cudaStream_t st);
 
+// Exact-integer tcgen05 stats kernel (k_stats_i8.cu): no_srp, 16 < D <= 127, B % 4 == 0.
+bool stats_i8_eligible(const Geometry& g);
+void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
+                     double* stats, cudaStream_t st);
+
 // Host launchers.  All asynchronous on `st`.
 void launch_stats(const Geometry& g, const StatsLaunch& sl, const float* x, int n_per_stream, int in_stride,
                   int n_lines_total, double* stats, cudaStream_t st);

@@ -1,0 +1,404 @@
+// k_stats_i8.cu — line_stats (erx.hpp:38-40) on the
+// 5th-generation tensor cores with EXACT integer accumulation (kind::i8).
+//
+// The second moment S = sum_p v_p v_p^T of one line is a D x D x P GEMM.
+// Tensor-core fp32 accumulation truncates (tools/tc_bias.py), which biases K
+// in its small-eigenvalue directions, so this kernel never lets the tensor
+// core round: v is turned into integers and the products are summed in s32.
+//
+//   pass 1  stream the line once: per-dim min / max of x, the centre
+//           c = fp32(mean of the first min(32, P) pixels) (k_stats.cu's rule)
+//   scale   s_d = R / max_p |fl32(x_pd - c_d)|,  R = 4194000 < 2^22
+//   pass 2  stream the line again (L2): q_pd = rint(v_pd * s_d) with
+//           v = fl32(x - c), rounded ONCE by fma(v, s, 1.5 * 2^23) (the
+//           integer lands in the low mantissa bits), |q| <= 2^22, split
+//           into three balanced signed int8 digits
+//           q = d0 + 2^8 d1 + 2^16 d2  ((q + 0x808080) ^ 0x808080, bytewise)
+//           and accumulate digit-plane products (i, j) with i + j >= 1 in
+//           four s32 TMEM accumulators, one per weight class 2^(8(i+j)).
+//
+// Every s32 sum is exact (|class sum| <= 3 * 2^14 * P < 2^31 for P < 43690);
+// the only approximations are the quantisation of v (2^-23 of the per-dim
+// range) and the dropped class-0 products (2^-30 relative): emulated
+// max / median raw-score error vs fp64 on configs[3] (tools/emulate_i8.py)
+// well inside the fp32 FFMA kernel's 2.5e-6 / 1.2e-7.
+// An extra operand row D holds q = 256 (digit d1 = 1) on real pixels, so
+// column D of the product is 256 * sum_p q_a: the sums s come out of the same
+// exact MMAs.
+//
+// Output slot per line: [c (D) | s = sum v (D) | S = sum v v^T packed lower],
+// fp64 — the k_stats.cu contract, finished by the scan kernel.
+//
+// Pipeline: a persistent CTA (256 threads, 512 TMEM columns) per SM walks
+// its lines; thread 0 streams 64-pixel chunks through a 2..4-deep
+// shared-memory ring with cp.async.bulk (mbarrier tx counts) as ONE sequence
+// across lines (pass 1 of line k+1 is already in flight while line k drains).
+// Pass-2 chunks are quantised into double-buffered digit planes (K-major,
+// 128 rows x 64 K per plane) and one thread issues 2 K-steps x 8 MMAs
+// (M = 128 dims, N = roundup16(D + 1)) per chunk, committed to the plane
+// buffer's mbarrier; the epilogue stages S in its own shared-memory area.
+#include "erx_common.cuh"
+#include "tc_common.cuh"
+
+namespace erxk {
+namespace {
+
+constexpr int kCh = 64;                                   // pixels per chunk (2 K-steps)
+constexpr int kMaxStages = 4;                             // bulk-copy ring depth (upper bound)
+constexpr uint32_t kPlane = (kCh / 32) * tc::kSliceBytes;  // 8 KB: 128 rows x 64 int8
+constexpr uint32_t kOps = 3 * kPlane;                     // d0, d1, d2 planes
+constexpr float kR = 4194000.f;                           // |q| <= 2^22: exact fma rounding, d2 in int8
+constexpr float kMagic = 12582912.f;                      // 1.5 * 2^23
+constexpr int kThreads = 256;
+constexpr size_t kSmemCap = 227 * 1024;
+
+struct StatsI8Args {
+    Geometry g;
+    const float* x;
+    int n;
+    int in_stride;
+    int n_lines;
+    double* stats;
+    int N;       // MMA N = roundup16(D + 1)
+    int stages;  // ring depth
+};
+
+__device__ __forceinline__ void pack_digits(const uint32_t (&u)[4], uint32_t& w0, uint32_t& w1, uint32_t& w2) {
+    const uint32_t t01 = __byte_perm(u[0], u[1], 0x5140), t23 = __byte_perm(u[2], u[3], 0x5140);
+    w0 = __byte_perm(t01, t23, 0x5410) ^ 0x80808080u;
+    w1 = __byte_perm(t01, t23, 0x7632) ^ 0x80808080u;
+    const uint32_t r01 = __byte_perm(u[0], u[1], 0x0062), r23 = __byte_perm(u[2], u[3], 0x0062);
+    w2 = __byte_perm(r01, r23, 0x5410) ^ 0x80808080u;
+}
+
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+    float r;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads)); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* m) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(m)) : "memory");
+}
+
+// Warp roles: warps 0-7 compute (range pass, quantisation, epilogue), warp 8
+// streams chunks (TMA bulk copies), warp 9 issues the MMAs.  No CTA-wide
+// barrier inside the chunk loop: stages and plane buffers hand over through
+// mbarriers (full / empty, pfull / pempty), the accumulator through
+// accfull / accempty, so copies, quantisation and MMAs of different chunks
+// overlap.  The epilogue of line k-1 runs after pass 1 of line k, when the
+// MMAs of line k-1 have long finished.
+__global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args a) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+    __shared__ __align__(8) uint64_t pfull[2], pempty[2], accfull, accempty;
+    __shared__ __align__(16) float red_mn[8][128];
+    __shared__ __align__(16) float red_mx[8][128];
+    __shared__ double red_cs[4][128];
+    __shared__ float cen_s[128], scale_s[128], add_s[128];
+    __shared__ double inv_s[128];
+    __shared__ double sum_s[128];
+    __shared__ int bad_s[8];
+
+    const Geometry& g = a.g;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int B = g.B, D = g.D, P = g.P;
+    const int NS = a.stages;
+
+    unsigned char* ops = smem;                                   // [2][kOps]
+    float* ring = reinterpret_cast<float*>(smem + 2 * kOps);     // [NS][kCh * B]
+    double* S = reinterpret_cast<double*>(smem + 2 * kOps + size_t(NS) * kCh * B * 4);  // [D(D+1)/2]
+    const int nch = (P + kCh - 1) / kCh;
+    const int per_line = 2 * nch;  // pass 1 + pass 2 chunk visits
+    const int my_lines = blockIdx.x < a.n_lines ? (a.n_lines - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int total = my_lines * per_line;
+
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 8);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&pfull[b], 8);
+            tc::mbar_init(&pempty[b], 1);
+        }
+        tc::mbar_init(&accfull, 1);
+        tc::mbar_init(&accempty, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 0) tc::tmem_alloc<512>(&tmem_slot);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+
+    if (warp == 8) {
+        // ---------------- producer: chunk visit j -> (line, chunk); the ring runs across lines
+        if (lane == 0) {
+            for (int j = 0; j < total; ++j) {
+                const int st = j % NS;
+                if (j >= NS) tc::mbar_wait(&empty[st], uint32_t((j / NS) - 1) & 1u);
+                const int k = j / per_line, i = j - k * per_line;
+                const int line = blockIdx.x + k * gridDim.x;
+                const int c = i % nch;
+                const int n = min(kCh, P - c * kCh);
+                const uint32_t bytes = uint32_t(n) * B * 4;
+                const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
+                tc::mbar_expect_tx(&full[st], bytes);
+                tc::bulk_g2s(ring + size_t(st) * kCh * B, xl + size_t(c) * kCh * B, bytes, &full[st]);
+            }
+        }
+        return;
+    }
+    if (warp == 9) {
+        // ---------------- MMA issuer: 2 K-steps x 8 digit-plane pairs per chunk
+        if (lane == 0) {
+            const uint32_t idesc = tc::idesc_s8_s32(128, a.N);
+            const int pr[8][3] = {{0, 1, 0}, {1, 0, 0}, {0, 2, 1}, {1, 1, 1}, {2, 0, 1}, {1, 2, 2}, {2, 1, 2}, {2, 2, 3}};
+            for (int k = 0; k < my_lines; ++k) {
+                if (k >= 1) tc::mbar_wait(&accempty, uint32_t(k - 1) & 1u);
+                for (int c = 0; c < nch; ++c) {
+                    const int k2 = k * nch + c, buf = k2 & 1;
+                    tc::mbar_wait(&pfull[buf], uint32_t(k2 >> 1) & 1u);
+                    tc::tc_fence_after();
+                    const uint32_t base = tc::smem_u32(ops + buf * kOps);
+#pragma unroll
+                    for (int s = 0; s < kCh / 32; ++s)
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const uint64_t ad = tc::smem_desc(base + pr[q][0] * kPlane + s * tc::kSliceBytes);
+                            const uint64_t bd = tc::smem_desc(base + pr[q][1] * kPlane + s * tc::kSliceBytes);
+                            const bool first = c == 0 && s == 0 && (q == 0 || q == 2 || q == 5 || q == 7);
+                            tc::mma_s8(tmem + uint32_t(pr[q][2]) * 128u, ad, bd, idesc, first ? 0u : 1u);
+                        }
+                    tc::mma_commit(&pempty[buf]);
+                }
+                tc::mma_commit(&accfull);
+            }
+        }
+        return;
+    }
+
+    // ---------------- compute warps 0-7
+    const int lane_grp = warp & 3, colh = warp >> 2;
+    const int row = lane_grp * 32 + lane;
+    const uint32_t lane_base = uint32_t(lane_grp * 32) << 16;
+    const int ngrp = a.N / 16;
+    const int g0 = colh ? (ngrp + 1) / 2 : 0, g1 = colh ? ngrp : (ngrp + 1) / 2;
+    // pass 1 mapping: warp = 8-pixel group, lane = 4 consecutive dims (one 16-byte load per pixel)
+    const bool quad_live = 4 * lane < B;
+    // pass 2 mapping: warp = (16-pixel group, dim half), lane -> dims lane + 32k + 64 * half (conflict-free
+    // 16-byte plane stores: 8 consecutive rows per quarter warp); loads clamp to a real band, the scale 0
+    // of padded rows makes their value irrelevant
+    const int pg2 = warp & 3, dh = warp >> 2;
+    const int dd0 = lane + 64 * dh, dd1 = dd0 + 32;
+    const int ld0 = min(dd0, B - 1), ld1 = min(dd1, B - 1);
+
+    // epilogue of line kk: S_int = sum_c 2^(8c) acc_c scaled by 1 / (s_a s_b), staged in smem, then stored
+    auto epilogue = [&](int kk) {
+        const int line = blockIdx.x + kk * gridDim.x;
+        tc::mbar_wait(&accfull, uint32_t(kk) & 1u);
+        tc::tc_fence_after();
+        for (int gi = g0; gi < g1; ++gi) {
+            float v[4][16];
+#pragma unroll
+            for (int cl = 0; cl < 4; ++cl) tc::tmem_ld16(tmem + lane_base + uint32_t(cl * 128 + gi * 16), v[cl]);
+            if (row < D) {
+                const double ia = inv_s[row];
+#pragma unroll
+                for (int ii = 0; ii < 16; ++ii) {
+                    const int e = gi * 16 + ii;
+                    const double si = double(__float_as_int(v[0][ii])) * 256.0 +
+                                      double(__float_as_int(v[1][ii])) * 65536.0 +
+                                      double(__float_as_int(v[2][ii])) * 16777216.0 +
+                                      double(__float_as_int(v[3][ii])) * 4294967296.0;
+                    if (e <= row) S[tri(row, e)] = si * ia * inv_s[e];
+                    if (e == D) sum_s[row] = si * (1.0 / 256.0) * ia;
+                }
+            }
+        }
+        tc::tc_fence_before();
+        bar_compute();
+        if (tid == 0) mbar_arrive(&accempty);  // TMEM free for the next line's MMAs
+        double* out = a.stats + size_t(line) * (g.SE + g.D);
+        const bool bad = bad_s[0] | bad_s[1] | bad_s[2] | bad_s[3] | bad_s[4] | bad_s[5] | bad_s[6] | bad_s[7];
+        const double poison = bad ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;
+        for (int i = tid; i < D; i += kThreads) {
+            out[i] = double(cen_s[i]) + poison;
+            out[D + i] = sum_s[i] + poison;
+        }
+        const int ntri = D * (D + 1) / 2;
+        for (int i = tid; i < ntri; i += kThreads) out[2 * D + i] = S[i] + poison;
+        bar_compute();  // S / sum_s / cen_s / bad_s are rewritten for the next line
+    };
+
+    float cdk[2] = {0.f, 0.f}, sdk[2] = {0.f, 0.f}, adk[2] = {kMagic, kMagic};
+    for (int k = 0; k < my_lines; ++k) {
+        // ---- pass 1: range of x per dim (min propagates NaN, max sees +inf); centre from the first 32 pixels
+        float4 mn = make_float4(3.402823466e38f, 3.402823466e38f, 3.402823466e38f, 3.402823466e38f);
+        float4 mx = make_float4(-3.402823466e38f, -3.402823466e38f, -3.402823466e38f, -3.402823466e38f);
+        for (int c = 0; c < nch; ++c) {
+            const int j = k * per_line + c, st = j % NS;
+            const int n = min(kCh, P - c * kCh);
+            tc::mbar_wait(&full[st], uint32_t(j / NS) & 1u);
+            const float* sb = ring + size_t(st) * kCh * B;
+            if (quad_live) {
+                const int p0 = warp * 8;
+                const float* xp = sb + p0 * B + 4 * lane;
+                if (n >= p0 + 8) {
+#pragma unroll
+                    for (int pp = 0; pp < 8; ++pp) {
+                        const float4 x = *reinterpret_cast<const float4*>(xp + pp * B);
+                        mn.x = fmin_nan(mn.x, x.x); mn.y = fmin_nan(mn.y, x.y);
+                        mn.z = fmin_nan(mn.z, x.z); mn.w = fmin_nan(mn.w, x.w);
+                        mx.x = fmaxf(mx.x, x.x); mx.y = fmaxf(mx.y, x.y); mx.z = fmaxf(mx.z, x.z); mx.w = fmaxf(mx.w, x.w);
+                    }
+                } else {
+                    for (int pp = 0; pp < n - p0; ++pp) {
+                        const float4 x = *reinterpret_cast<const float4*>(xp + pp * B);
+                        mn.x = fmin_nan(mn.x, x.x); mn.y = fmin_nan(mn.y, x.y);
+                        mn.z = fmin_nan(mn.z, x.z); mn.w = fmin_nan(mn.w, x.w);
+                        mx.x = fmaxf(mx.x, x.x); mx.y = fmaxf(mx.y, x.y); mx.z = fmaxf(mx.z, x.z); mx.w = fmaxf(mx.w, x.w);
+                    }
+                }
+                if (c == 0 && warp < 4) {
+                    double4 cs = make_double4(0.0, 0.0, 0.0, 0.0);
+                    for (int pp = 0; pp < min(8, n - p0); ++pp) {
+                        const float4 x = *reinterpret_cast<const float4*>(xp + pp * B);
+                        cs.x += double(x.x); cs.y += double(x.y); cs.z += double(x.z); cs.w += double(x.w);
+                    }
+                    red_cs[warp][4 * lane] = cs.x; red_cs[warp][4 * lane + 1] = cs.y;
+                    red_cs[warp][4 * lane + 2] = cs.z; red_cs[warp][4 * lane + 3] = cs.w;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+        }
+        const bool bad_mine = quad_live && !(isfinite(mn.x) && isfinite(mn.y) && isfinite(mn.z) && isfinite(mn.w) &&
+                                             isfinite(mx.x) && isfinite(mx.y) && isfinite(mx.z) && isfinite(mx.w));
+        // ---- the previous line's epilogue (its MMAs finished while this pass ran)
+        if (k > 0) epilogue(k - 1);
+        // ---- ranges of all pixel groups -> centre and per-dim scale of this line
+        if (quad_live) {
+            *reinterpret_cast<float4*>(&red_mn[warp][4 * lane]) = mn;
+            *reinterpret_cast<float4*>(&red_mx[warp][4 * lane]) = mx;
+        }
+        const unsigned bw = __ballot_sync(0xffffffffu, bad_mine);
+        if (lane == 0) bad_s[warp] = bw != 0;
+        bar_compute();
+        if (tid < 128) {
+            const int d = tid;
+            float cd = 0.f, sd = 0.f;
+            const float ad = kMagic + (d == D ? 256.f : 0.f);  // ones row: q = 256
+            if (d < D) {
+                const int n0 = min(32, P);
+                const double c0 = red_cs[0][d] + red_cs[1][d] + red_cs[2][d] + red_cs[3][d];
+                cd = float(c0 / double(n0));
+                float lo = red_mn[0][d], hi = red_mx[0][d];
+                for (int w = 1; w < 8; ++w) {
+                    lo = fminf(lo, red_mn[w][d]);
+                    hi = fmaxf(hi, red_mx[w][d]);
+                }
+                const float m = fmaxf(hi - cd, cd - lo);
+                sd = (m > 0.f && m <= 3.402823466e38f) ? kR / m : 0.f;
+            }
+            cen_s[d] = cd;
+            scale_s[d] = sd;
+            add_s[d] = ad;
+            inv_s[d] = sd > 0.f ? 1.0 / double(sd) : 0.0;
+        }
+        bar_compute();
+        cdk[0] = cen_s[dd0 & 127]; sdk[0] = scale_s[dd0 & 127]; adk[0] = add_s[dd0 & 127];
+        cdk[1] = cen_s[dd1 & 127]; sdk[1] = scale_s[dd1 & 127]; adk[1] = add_s[dd1 & 127];
+        // ---- pass 2: quantise each chunk into digit planes:
+        // y = fma(x - c, s, 1.5 * 2^23) rounds v * s to an integer in the low mantissa bits
+        // (|v s| <= 2^22), u = q + 0x808080 = bits(y) - 0x4B400000 + 0x808080
+        for (int c = 0; c < nch; ++c) {
+            const int j = k * per_line + nch + c, st = j % NS;
+            const int k2 = k * nch + c, buf = k2 & 1;
+            const int n = min(kCh, P - c * kCh);
+            tc::mbar_wait(&full[st], uint32_t(j / NS) & 1u);
+            if (k2 >= 2) tc::mbar_wait(&pempty[buf], uint32_t((k2 - 2) >> 1) & 1u);
+            const float* sb = ring + size_t(st) * kCh * B + (pg2 * 16) * B;
+            unsigned char* op = ops + buf * kOps;
+            uint32_t w[2][3][4];
+            if (n == kCh) {
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    uint32_t u0[4], u1[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float* xp = sb + (jj * 4 + e) * B;
+                        u0[e] = __float_as_uint(fmaf(xp[ld0] - cdk[0], sdk[0], adk[0])) + (0x808080u - 0x4B400000u);
+                        u1[e] = __float_as_uint(fmaf(xp[ld1] - cdk[1], sdk[1], adk[1])) + (0x808080u - 0x4B400000u);
+                    }
+                    pack_digits(u0, w[0][0][jj], w[0][1][jj], w[0][2][jj]);
+                    pack_digits(u1, w[1][0][jj], w[1][1][jj], w[1][2][jj]);
+                }
+            } else {
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    uint32_t u0[4], u1[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int p = pg2 * 16 + jj * 4 + e;
+                        const float* xp = sb + (jj * 4 + e) * B;
+                        u0[e] = __float_as_uint(fmaf(xp[ld0] - cdk[0], sdk[0], adk[0])) + (0x808080u - 0x4B400000u);
+                        u1[e] = __float_as_uint(fmaf(xp[ld1] - cdk[1], sdk[1], adk[1])) + (0x808080u - 0x4B400000u);
+                        if (p >= n) u0[e] = u1[e] = 0x808080u;
+                    }
+                    pack_digits(u0, w[0][0][jj], w[0][1][jj], w[0][2][jj]);
+                    pack_digits(u1, w[1][0][jj], w[1][1][jj], w[1][2][jj]);
+                }
+            }
+            const uint32_t off0 = tc::kmajor_off_s8(dd0, pg2 * 16), off1 = tc::kmajor_off_s8(dd1, pg2 * 16);
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl) {
+                *reinterpret_cast<uint4*>(op + pl * kPlane + off0) = make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
+                *reinterpret_cast<uint4*>(op + pl * kPlane + off1) = make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
+            }
+            tc::fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&empty[st]);
+                mbar_arrive(&pfull[buf]);
+            }
+        }
+    }
+    if (my_lines > 0) epilogue(my_lines - 1);
+    if (warp == 0) tc::tmem_free<512>(tmem);
+}
+
+int i8_stages(const Geometry& g) {
+    const size_t fixed = 2 * size_t(kOps) + size_t(g.D) * (g.D + 1) / 2 * 8 + 20 * 1024;  // + static smem
+    const size_t chunk = size_t(kCh) * g.B * 4;
+    const int st = int((kSmemCap - fixed) / chunk);
+    return st < kMaxStages ? st : kMaxStages;
+}
+
+size_t stats_i8_smem(const Geometry& g) {
+    return 2 * size_t(kOps) + size_t(i8_stages(g)) * kCh * g.B * 4 + size_t(g.D) * (g.D + 1) / 2 * 8;
+}
+
+}  // namespace
+
+bool stats_i8_eligible(const Geometry& g) {
+    return !g.srp && g.D > 16 && g.D <= 127 && (g.B % 4) == 0 && i8_stages(g) >= 2;
+}
+
+void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
+                     double* stats, cudaStream_t st) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(stats_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemCap - 20 * 1024));
+    }
+    StatsI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, (g.D + 1 + 15) / 16 * 16, i8_stages(g)};
+    const int grid = n_lines_total < sms ? n_lines_total : sms;
+    stats_i8_kernel<<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
+}
+
+}  // namespace erxk

@@ -57,6 +57,44 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// Instruction descriptor: kind::i8, A = B = signed int8, D = S32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_s8_s32(int M, int N) {
+    return (2u << 4)                     // c_format S32
+           | (1u << 7)                   // a_format signed 8-bit
+           | (1u << 10)                  // b_format signed 8-bit
+           | (uint32_t(N >> 3) << 17)    // n_dim
+           | (uint32_t(M >> 4) << 24);   // m_dim
+}
+
+// D (s32, TMEM) (+)= A (s8, smem) x B (s8, smem)^T, K = 32: exact integer accumulation.
+__device__ __forceinline__ void mma_s8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// byte offset of int8 element (m, k) inside a stack of 128-row x 32-K slices (4 KB each)
+__device__ __forceinline__ uint32_t kmajor_off_s8(int m, int k) {
+    return uint32_t(k >> 5) * kSliceBytes + uint32_t(m >> 3) * 256u + uint32_t((k >> 4) & 1) * 128u +
+           uint32_t(m & 7) * 16u + uint32_t(k & 15);
+}
+
+// One-shot bulk copy global -> shared, completion counted on an mbarrier (tx bytes).
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mbar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+        : "memory");
+}
+
 // Completion of all previously issued tcgen05 ops of this thread -> one mbarrier arrival.
 __device__ __forceinline__ void mma_commit(uint64_t* mbar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(

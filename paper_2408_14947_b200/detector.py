@@ -256,16 +256,17 @@ class Engine:
         """0 auto, 32 or 64 (see ERX_OPT_FACTOR_PRECISION in include/erx_b200.h)."""
         self._check(self._lib.erx_set_option(self._h, L.OPT_FACTOR_PRECISION, bits))
 
-    def set_stats_tensor(self, on: bool):
-        """Use the tcgen05 stats kernel where eligible (default) or force the FFMA kernel."""
-        self._check(self._lib.erx_set_option(self._h, L.OPT_STATS_TENSOR, int(on)))
+    def set_stats_tensor(self, kind: int):
+        """Line-statistics kernel: 0 FFMA, 1 tcgen05 bf16x3, 2 tcgen05 exact int8 (ERX_OPT_STATS_TENSOR)."""
+        self._check(self._lib.erx_set_option(self._h, L.OPT_STATS_TENSOR, int(kind)))
 
     def set_host_groups(self, groups: int):
         """Stream groups per host window (0 auto; see ERX_OPT_HOST_GROUPS)."""
         self._check(self._lib.erx_set_option(self._h, L.OPT_HOST_GROUPS, int(groups)))
 
-    def stats_tensor(self) -> bool:
-        return bool(self._lib.erx_get_option(self._h, L.OPT_STATS_TENSOR))
+    def stats_tensor(self) -> int:
+        """Line-statistics kernel in use (0 FFMA, 1 bf16x3, 2 exact int8)."""
+        return int(self._lib.erx_get_option(self._h, L.OPT_STATS_TENSOR))
 
     def factor_precision(self) -> int:
         return int(self._lib.erx_get_option(self._h, L.OPT_FACTOR_PRECISION))

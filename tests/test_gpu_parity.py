@@ -230,10 +230,10 @@ def test_factor_kernel_variants(pkg, oracle, cid, n_lines, prec):
     check_gates(oracle, raw_g[0], norm_g[0], raw_o, norm_o, mask=mask, warm=warm, label=f"c{cid} factor{prec}")
 
 
-@pytest.mark.parametrize("tensor", [pytest.param(True, marks=pytest.mark.xfail(
-    reason="tcgen05 fp32 accumulation truncates (tools/tc_bias.py): median gate missed", strict=False)), False])
+@pytest.mark.parametrize("tensor", [pytest.param(1, marks=pytest.mark.xfail(
+    reason="tcgen05 fp32 accumulation truncates (tools/tc_bias.py): median gate missed", strict=False)), 0, 2])
 def test_stats_kernel_variants(pkg, oracle, tensor):
-    """tcgen05 (bf16x3 split, 6 products) and FFMA line statistics against the gates."""
+    """tcgen05 bf16x3 (1), FFMA (0) and exact-integer tcgen05 (2) line statistics against the gates."""
     spec = pkg.gen_spec(3, 5)
     lines, mask = pkg.gen_lines(spec, 0, 200)
     cfg = pkg.ErxConfig(no_srp=True, alpha=0.1, buffer_len=60)
@@ -245,7 +245,40 @@ def test_stats_kernel_variants(pkg, oracle, tensor):
     _, wu, raw_g, norm_g = eng.pop()
     raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), lines)
     warm = np.broadcast_to(wu[:, None], raw_o.shape)
-    check_gates(oracle, raw_g[0], norm_g[0], raw_o, norm_o, mask=mask, warm=warm, label=f"stats tensor={tensor}")
+    mx, med = check_gates(oracle, raw_g[0], norm_g[0], raw_o, norm_o, mask=mask, warm=warm,
+                          label=f"stats tensor={tensor}")
+    print(f"stats tensor={tensor}: raw max {mx:.3e} median {med:.3e}")
+
+
+@pytest.mark.parametrize("P", [640, 100, 33, 64, 1000])
+def test_stats_i8_edges(pkg, oracle, P):
+    """Exact-integer tensor-core statistics: ragged chunks (P not a multiple of 64,
+    P < 64, P = 64), a constant band (zero range -> unit scale), large offsets."""
+    rng = np.random.default_rng(P)
+    B, n = 24, 40  # P - 1 >= B: a single line's covariance is full rank (fp64-only territory otherwise)
+    base = rng.normal(size=(n, P, B)).astype(np.float32) * np.linspace(0.01, 100, B, dtype=np.float32)
+    base += 1000.0
+    base[:, :, 3] = 7.0
+    cfg = pkg.ErxConfig(no_srp=True, buffer_len=5)
+    eng = pkg.Engine(cfg, B, window_lines=16)
+    eng.set_stats_tensor(2)
+    eng.push(base[None], 0)
+    eng.finish()
+    assert eng.stats_tensor() == 2
+    _, wu, raw_g, norm_g = eng.pop()
+    raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), base)
+    check_gates(oracle, raw_g[0], norm_g[0], raw_o, norm_o, label=f"i8 P={P}")
+
+
+def test_stats_i8_nonfinite_fails(pkg):
+    # score-then-update: the inf of line 1 reaches the background scored by line 2
+    x = np.random.default_rng(1).normal(size=(4, 96, 40)).astype(np.float32)
+    x[1, 50, 7] = np.inf
+    eng = pkg.Engine(pkg.ErxConfig(no_srp=True), 40, window_lines=4)
+    eng.set_stats_tensor(2)
+    with pytest.raises(pkg.FactorizationError):
+        eng.push(x[None], 0)
+        eng.finish()
 
 
 # ---------------------------------------------------------------- contract edges

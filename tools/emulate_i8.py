@@ -1,0 +1,118 @@
+"""Emulate exact-integer tensor-core line statistics before writing the kernel.
+
+v = fp32(x - c) is quantised per line and per dim: q_d = rint(fp32(v_d * s_d))
+with s_d = R / max_p |v_d| (R = digit range), split into balanced signed int8
+digits; the tcgen05 kind::i8 MMAs accumulate digit products exactly in s32,
+so S_ab = sum_p q_a q_b / (s_a s_b) up to the dropped low weight classes.
+This script runs the ERX recurrence (fp64 everywhere else) with those
+statistics and reports the raw-score error against the fp64 path, next to
+the fp32 FFMA model, for the parity gates of tests/test_gpu_parity.py.
+"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2408_14947_b200 as pkg  # noqa: E402  (host generator only)
+
+
+def stats_exact(x):
+    v = x.astype(np.float64)
+    mu = v.mean(0)
+    d = v - mu
+    return mu, d.T @ d / (len(v) - 1)
+
+
+def stats_quant(x, R, drop_below=None, digits=3):
+    P = len(x)
+    c = x[:32].astype(np.float64).mean(0).astype(np.float32)
+    v = (x - c).astype(np.float32)
+    m = np.abs(v).max(0)
+    m[m == 0] = 1
+    s = (np.float32(R) / m).astype(np.float32)
+    q = np.rint((v * s).astype(np.float32)).astype(np.int64)
+    if drop_below is not None:
+        # balanced digits; drop weight classes < drop_below
+        u = (q + sum(0x80 << (8 * i) for i in range(digits)))
+        dg = [((u >> (8 * i)) & 0xFF) - 128 for i in range(digits)]
+        assert np.array_equal(sum(dg[i] << (8 * i) for i in range(digits)), q)
+        S = np.zeros((x.shape[1], x.shape[1]), np.int64)
+        for i in range(digits):
+            for j in range(digits):
+                if i + j >= drop_below:
+                    S += (dg[i].T @ dg[j]) << (8 * (i + j))
+    else:
+        S = q.T @ q
+    sq = q.sum(0)
+    inv = 1.0 / s.astype(np.float64)
+    Sf = S.astype(np.float64) * np.outer(inv, inv)
+    sf = sq.astype(np.float64) * inv
+    mu = c.astype(np.float64) + sf / P
+    K = (Sf - np.outer(sf, sf) / P) / (P - 1)
+    return mu, K
+
+
+def stats_f32(x):
+    """The FFMA kernel model: fp32 products, 2-level fp32 accumulation (chunks of 32)."""
+    P = len(x)
+    c = x[:32].astype(np.float64).mean(0).astype(np.float32)
+    v = (x - c).astype(np.float32)
+    S = np.zeros((x.shape[1],) * 2)
+    for p0 in range(0, P, 32):
+        blk = v[p0:p0 + 32]
+        acc = np.zeros((x.shape[1],) * 2, np.float32)
+        for r in blk:
+            acc = (acc + np.outer(r, r).astype(np.float32)).astype(np.float32)
+        S += acc
+    s = v.astype(np.float64).sum(0)
+    mu = c.astype(np.float64) + s / P
+    K = (S - np.outer(s, s) / P) / (P - 1)
+    return mu, K
+
+
+def erx(lines, alpha, stats, eps=1e-5):
+    raws = []
+    mu = K = None
+    for t, x in enumerate(lines):
+        m, k = stats(x)
+        if mu is None:
+            mu, K = m, k
+        e = eps
+        while True:
+            try:
+                L = np.linalg.cholesky(K + e * np.eye(len(K)))
+                break
+            except np.linalg.LinAlgError:
+                e *= 10
+        y = np.linalg.solve(L, (x.astype(np.float64) - mu).T)
+        raws.append(np.sqrt((y * y).sum(0)))
+        if t:
+            pass
+        mu = (1 - alpha) * mu + alpha * m
+        K = (1 - alpha) * K + alpha * k
+    return np.array(raws)
+
+
+def main():
+    cid = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+    n = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+    alpha = {0: 0.1, 1: 0.05, 2: 0.1, 3: 0.1, 4: 0.05}[cid]
+    x, _ = pkg.gen_lines(pkg.gen_spec(cid, 0), 0, n)
+    ref = erx(x, alpha, stats_exact)
+    variants = {
+        "f32 FFMA model": stats_f32,
+        "i8 3 digits (R=8.35e6), all classes": lambda a: stats_quant(a, 8355000.0),
+        "i8 3 digits, classes>=2 (6 MMAs)": lambda a: stats_quant(a, 8355000.0, 2, 3),
+        "i8 3 digits, classes>=1": lambda a: stats_quant(a, 8355000.0, 1, 3),
+        "i8 3 digits R=4194000 (2^22), classes>=1": lambda a: stats_quant(a, 4194000.0, 1, 3),
+        "i8 2 digits (R=32767), all": lambda a: stats_quant(a, 32639.0, 0, 2),
+    }
+    for name, fn in variants.items():
+        r = erx(x, alpha, fn)
+        rel = np.abs(r - ref) / np.maximum(np.abs(ref), 1e-300)
+        print(f"{name:42s} max {rel.max():.3e}  median {np.median(rel):.3e}")
+
+
+if __name__ == "__main__":
+    main()
