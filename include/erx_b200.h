@@ -164,6 +164,11 @@ int erx_kernel_times(erx_engine* e, double* ms, uint64_t* launches);
 int erx_probe_fp32_tflops(erx_engine* e, double* reg_form, double* const_form);
 /* Same for the paired fma.rn.f32x2 (FFMA2) instruction. */
 int erx_probe_ffma2_tflops(erx_engine* e, double* tflops);
+/* Streaming global->shared throughput, GB/s (design probe): mode 0 cp.async.bulk
+ * ring (one issuing thread), 1 LDG.128 by 256 threads, 2 cp.async by 256 threads;
+ * chunk_bytes per stage (multiple of 1 KB), 1..8 stages, ctas_per_sm persistent CTAs. */
+int erx_probe_stream(erx_engine* e, int mode, uint32_t chunk_bytes, int stages, int ctas_per_sm, uint64_t bytes,
+                     double* gbs);
 /* tcgen05 self-test on device buffers: D[128][128] = A[128][K] . B[128][K]^T
  * from bf16 operands (split = 0) or the 3-way bf16 split with 6 products
  * (split = 1, fp32-accurate).  K a multiple of 16, <= 256. */

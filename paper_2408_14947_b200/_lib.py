@@ -92,6 +92,7 @@ SIGNATURES = {
     "erx_kernel_times": (C.c_int, [_vp, _dp, _u64p]),
     "erx_probe_fp32_tflops": (C.c_int, [_vp, _dp, _dp]),
     "erx_probe_ffma2_tflops": (C.c_int, [_vp, _dp]),
+    "erx_probe_stream": (C.c_int, [_vp, C.c_int, C.c_uint32, C.c_int, C.c_int, C.c_uint64, _dp]),
     "erx_tc_selftest": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, _vp]),
     "erx_event_record": (C.c_int, [_vp, C.c_int]),
     "erx_event_elapsed_ms": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_float)]),

@@ -844,6 +844,16 @@ int erx_tc_selftest(erx_engine* e, const float* dA, const float* dB, int K, int 
     return ERX_OK;
 }
 
+int erx_probe_stream(erx_engine* e, int mode, uint32_t chunk_bytes, int stages, int ctas_per_sm, uint64_t bytes,
+                     double* gbs) {
+    CU(cudaSetDevice(e->device));
+    if (mode < 0 || mode > 2 || stages < 1 || stages > 8 || chunk_bytes % 1024 || ctas_per_sm < 1)
+        return fail(e, ERX_ERR_CONFIG, "probe_stream: bad arguments");
+    *gbs = erxk::probe_stream_gbs(e->stream, mode, int(chunk_bytes), stages, ctas_per_sm, size_t(bytes));
+    CU(cudaGetLastError());
+    return ERX_OK;
+}
+
 int erx_probe_ffma2_tflops(erx_engine* e, double* tflops) {
     CU(cudaSetDevice(e->device));
     *tflops = erxk::probe_ffma2_tflops(e->stream);

@@ -114,6 +114,9 @@ void launch_normalize(const Geometry& g, const float* raw, int n_lines_total, fl
 void probe_ffma_tflops(cudaStream_t st, double* reg_form, double* const_form);
 // Measured paired-FFMA (fma.rn.f32x2) throughput, TFLOP/s counting 2 FMAs per lane.
 double probe_ffma2_tflops(cudaStream_t st);
+// Streaming throughput (GB/s) of a global->shared path (k_stream_probe.cu): mode 0 bulk-copy ring,
+// 1 LDG.128, 2 cp.async ring.
+double probe_stream_gbs(cudaStream_t st, int mode, int chunk_bytes, int stages, int ctas_per_sm, size_t bytes);
 // tcgen05 self-test: D[128][128] = A[128][K] B[128][K]^T (bf16, split = 1: 3-way split, 6 products).
 int tc_selftest(const float* dA, const float* dB, int K, int split, float* dD, cudaStream_t st);
 

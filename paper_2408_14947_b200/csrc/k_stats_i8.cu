@@ -37,6 +37,9 @@
 // 128 rows x 64 K per plane) and one thread issues 2 K-steps x 8 MMAs
 // (M = 128 dims, N = roundup16(D + 1)) per chunk, committed to the plane
 // buffer's mbarrier; the epilogue stages S in its own shared-memory area.
+#include <cstdio>
+#include <cstdlib>
+
 #include "erx_common.cuh"
 #include "tc_common.cuh"
 
@@ -44,13 +47,13 @@ namespace erxk {
 namespace {
 
 constexpr int kCh = 64;                                   // pixels per chunk (2 K-steps)
-constexpr int kMaxStages = 4;                             // bulk-copy ring depth (upper bound)
+constexpr int kMaxStages = 8;                             // bulk-copy ring depth (upper bound)
 constexpr uint32_t kPlane = (kCh / 32) * tc::kSliceBytes;  // 8 KB: 128 rows x 64 int8
 constexpr uint32_t kOps = 3 * kPlane;                     // d0, d1, d2 planes
 constexpr float kR = 4194000.f;                           // |q| <= 2^22: exact fma rounding, d2 in int8
 constexpr float kMagic = 12582912.f;                      // 1.5 * 2^23
 constexpr int kThreads = 256;
-constexpr size_t kSmemCap = 227 * 1024;
+constexpr size_t kSmemCap = 232448;  // 227 KB per CTA
 
 struct StatsI8Args {
     Geometry g;
@@ -61,6 +64,7 @@ struct StatsI8Args {
     double* stats;
     int N;       // MMA N = roundup16(D + 1)
     int stages;  // ring depth
+    int dbg;     // experiment knob (0 = normal)
 };
 
 __device__ __forceinline__ void pack_digits(const uint32_t (&u)[4], uint32_t& w0, uint32_t& w1, uint32_t& w2) {
@@ -75,6 +79,11 @@ __device__ __forceinline__ float fmin_nan(float a, float b) {
     float r;
     asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
     return r;
+}
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
 }
 __device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads)); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* m) {
@@ -108,11 +117,29 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
 
     unsigned char* ops = smem;                                   // [2][kOps]
     float* ring = reinterpret_cast<float*>(smem + 2 * kOps);     // [NS][kCh * B]
-    double* S = reinterpret_cast<double*>(smem + 2 * kOps + size_t(NS) * kCh * B * 4);  // [D(D+1)/2]
+    // S staging: over the plane buffers when it fits (the epilogue runs while they are idle)
+    const size_t tri_bytes = size_t(D) * (D + 1) / 2 * 8;
+    double* S = reinterpret_cast<double*>(tri_bytes <= 2 * kOps ? smem : smem + 2 * kOps + size_t(NS) * kCh * B * 4);
     const int nch = (P + kCh - 1) / kCh;
-    const int per_line = 2 * nch;  // pass 1 + pass 2 chunk visits
     const int my_lines = blockIdx.x < a.n_lines ? (a.n_lines - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int total = my_lines * per_line;
+
+    // Ring plan.  Chunk c of line k lives in slot slot(k, c % NS); pass 2 walks the chunks in
+    // DESCENDING order, so the last NS chunks of pass 1 are still resident (res0 = first resident
+    // chunk) and only chunks < res0 are loaded again.  The slot permutation alternates per line so
+    // the next line's first chunks land in the slots its predecessor frees first.  Every load into a
+    // slot has a per-slot sequence number: full[s] completes once per load, empty[s] once per release.
+    const int res0 = nch > NS ? nch - NS : 0;
+    auto cnt1 = [&](int r) { return r < nch ? (nch - 1 - r) / NS + 1 : 0; };
+    auto cnt2 = [&](int r) { return r < res0 ? (res0 - 1 - r) / NS + 1 : 0; };
+    auto slot = [&](int k, int r) { return (k & 1) ? NS - 1 - r : r; };
+    auto base = [&](int k, int sl) {
+        return ((k + 1) / 2) * (cnt1(sl) + cnt2(sl)) + (k / 2) * (cnt1(NS - 1 - sl) + cnt2(NS - 1 - sl));
+    };
+    auto idx1 = [&](int k, int c) { return base(k, slot(k, c % NS)) + c / NS; };
+    auto idx2 = [&](int k, int c) {
+        const int r = c % NS, m2 = r + ((res0 - 1 - r) / NS) * NS;
+        return base(k, slot(k, r)) + cnt1(r) + (m2 - c) / NS;
+    };
 
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -134,19 +161,21 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     const uint32_t tmem = tmem_slot;
 
     if (warp == 8) {
-        // ---------------- producer: chunk visit j -> (line, chunk); the ring runs across lines
+        // ---------------- producer: pass-1 chunks ascending, then the non-resident pass-2 chunks descending
         if (lane == 0) {
-            for (int j = 0; j < total; ++j) {
-                const int st = j % NS;
-                if (j >= NS) tc::mbar_wait(&empty[st], uint32_t((j / NS) - 1) & 1u);
-                const int k = j / per_line, i = j - k * per_line;
+            auto load = [&](int k, int c, int idx) {
+                const int st = slot(k, c % NS);
+                if (idx >= 1) tc::mbar_wait(&empty[st], uint32_t(idx - 1) & 1u);
                 const int line = blockIdx.x + k * gridDim.x;
-                const int c = i % nch;
                 const int n = min(kCh, P - c * kCh);
                 const uint32_t bytes = uint32_t(n) * B * 4;
                 const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
                 tc::mbar_expect_tx(&full[st], bytes);
                 tc::bulk_g2s(ring + size_t(st) * kCh * B, xl + size_t(c) * kCh * B, bytes, &full[st]);
+            };
+            for (int k = 0; k < my_lines; ++k) {
+                for (int c = 0; c < nch; ++c) load(k, c, idx1(k, c));
+                for (int c = res0 - 1; c >= 0; --c) load(k, c, idx2(k, c));
             }
         }
         return;
@@ -166,7 +195,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
 #pragma unroll
                     for (int s = 0; s < kCh / 32; ++s)
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) {
+                        for (int q = 0; q < 8; ++q) if (a.dbg < 2) {
                             const uint64_t ad = tc::smem_desc(base + pr[q][0] * kPlane + s * tc::kSliceBytes);
                             const uint64_t bd = tc::smem_desc(base + pr[q][1] * kPlane + s * tc::kSliceBytes);
                             const bool first = c == 0 && s == 0 && (q == 0 || q == 2 || q == 5 || q == 7);
@@ -201,18 +230,15 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
         tc::mbar_wait(&accfull, uint32_t(kk) & 1u);
         tc::tc_fence_after();
         for (int gi = g0; gi < g1; ++gi) {
-            float v[4][16];
-#pragma unroll
-            for (int cl = 0; cl < 4; ++cl) tc::tmem_ld16(tmem + lane_base + uint32_t(cl * 128 + gi * 16), v[cl]);
+            uint32_t v[4][16];
+            tc::tmem_ld16x4(tmem + lane_base + uint32_t(gi * 16), 128u, v);
             if (row < D) {
                 const double ia = inv_s[row];
 #pragma unroll
                 for (int ii = 0; ii < 16; ++ii) {
                     const int e = gi * 16 + ii;
-                    const double si = double(__float_as_int(v[0][ii])) * 256.0 +
-                                      double(__float_as_int(v[1][ii])) * 65536.0 +
-                                      double(__float_as_int(v[2][ii])) * 16777216.0 +
-                                      double(__float_as_int(v[3][ii])) * 4294967296.0;
+                    const double si = double(int(v[0][ii])) * 256.0 + double(int(v[1][ii])) * 65536.0 +
+                                      double(int(v[2][ii])) * 16777216.0 + double(int(v[3][ii])) * 4294967296.0;
                     if (e <= row) S[tri(row, e)] = si * ia * inv_s[e];
                     if (e == D) sum_s[row] = si * (1.0 / 256.0) * ia;
                 }
@@ -234,16 +260,19 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     };
 
     float cdk[2] = {0.f, 0.f}, sdk[2] = {0.f, 0.f}, adk[2] = {kMagic, kMagic};
+    uint64_t t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+    const bool trace = a.dbg == 10 && blockIdx.x == 0 && tid == 0;
     for (int k = 0; k < my_lines; ++k) {
+        if (trace) t0 = gtimer();
         // ---- pass 1: range of x per dim (min propagates NaN, max sees +inf); centre from the first 32 pixels
         float4 mn = make_float4(3.402823466e38f, 3.402823466e38f, 3.402823466e38f, 3.402823466e38f);
         float4 mx = make_float4(-3.402823466e38f, -3.402823466e38f, -3.402823466e38f, -3.402823466e38f);
         for (int c = 0; c < nch; ++c) {
-            const int j = k * per_line + c, st = j % NS;
+            const int st = slot(k, c % NS);
             const int n = min(kCh, P - c * kCh);
-            tc::mbar_wait(&full[st], uint32_t(j / NS) & 1u);
+            tc::mbar_wait(&full[st], uint32_t(idx1(k, c)) & 1u);
             const float* sb = ring + size_t(st) * kCh * B;
-            if (quad_live) {
+            if (quad_live && a.dbg != 1) {
                 const int p0 = warp * 8;
                 const float* xp = sb + p0 * B + 4 * lane;
                 if (n >= p0 + 8) {
@@ -273,12 +302,14 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                 }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
+            if (lane == 0 && c < res0) mbar_arrive(&empty[st]);  // resident chunks stay for pass 2
         }
         const bool bad_mine = quad_live && !(isfinite(mn.x) && isfinite(mn.y) && isfinite(mn.z) && isfinite(mn.w) &&
                                              isfinite(mx.x) && isfinite(mx.y) && isfinite(mx.z) && isfinite(mx.w));
         // ---- the previous line's epilogue (its MMAs finished while this pass ran)
+        if (trace) t1 = gtimer();
         if (k > 0) epilogue(k - 1);
+        if (trace) t2 = gtimer();
         // ---- ranges of all pixel groups -> centre and per-dim scale of this line
         if (quad_live) {
             *reinterpret_cast<float4*>(&red_mn[warp][4 * lane]) = mn;
@@ -311,19 +342,22 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
         bar_compute();
         cdk[0] = cen_s[dd0 & 127]; sdk[0] = scale_s[dd0 & 127]; adk[0] = add_s[dd0 & 127];
         cdk[1] = cen_s[dd1 & 127]; sdk[1] = scale_s[dd1 & 127]; adk[1] = add_s[dd1 & 127];
+        if (trace) t3 = gtimer();
         // ---- pass 2: quantise each chunk into digit planes:
         // y = fma(x - c, s, 1.5 * 2^23) rounds v * s to an integer in the low mantissa bits
         // (|v s| <= 2^22), u = q + 0x808080 = bits(y) - 0x4B400000 + 0x808080
-        for (int c = 0; c < nch; ++c) {
-            const int j = k * per_line + nch + c, st = j % NS;
-            const int k2 = k * nch + c, buf = k2 & 1;
+        for (int cc = 0; cc < nch; ++cc) {
+            const int c = nch - 1 - cc;
+            const int st = slot(k, c % NS);
+            const int k2 = k * nch + cc, buf = k2 & 1;
             const int n = min(kCh, P - c * kCh);
-            tc::mbar_wait(&full[st], uint32_t(j / NS) & 1u);
+            if (c < res0) tc::mbar_wait(&full[st], uint32_t(idx2(k, c)) & 1u);
             if (k2 >= 2) tc::mbar_wait(&pempty[buf], uint32_t((k2 - 2) >> 1) & 1u);
             const float* sb = ring + size_t(st) * kCh * B + (pg2 * 16) * B;
             unsigned char* op = ops + buf * kOps;
             uint32_t w[2][3][4];
-            if (n == kCh) {
+            if (a.dbg == 1) {
+            } else if (n == kCh) {
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) {
                     uint32_t u0[4], u1[4];
@@ -354,7 +388,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
             }
             const uint32_t off0 = tc::kmajor_off_s8(dd0, pg2 * 16), off1 = tc::kmajor_off_s8(dd1, pg2 * 16);
 #pragma unroll
-            for (int pl = 0; pl < 3; ++pl) {
+            for (int pl = 0; pl < 3; ++pl) if (a.dbg != 1) {
                 *reinterpret_cast<uint4*>(op + pl * kPlane + off0) = make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
                 *reinterpret_cast<uint4*>(op + pl * kPlane + off1) = make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
             }
@@ -365,20 +399,32 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                 mbar_arrive(&pfull[buf]);
             }
         }
+        if (trace) {
+            const uint64_t t4 = gtimer();
+            printf("i8 line %d: pass1 %.2f us, epilogue %.2f, scales %.2f, pass2 %.2f\n", k, (t1 - t0) * 1e-3,
+                   (t2 - t1) * 1e-3, (t3 - t2) * 1e-3, (t4 - t3) * 1e-3);
+        }
     }
     if (my_lines > 0) epilogue(my_lines - 1);
     if (warp == 0) tc::tmem_free<512>(tmem);
 }
 
+constexpr size_t kStaticSmem = 17 * 1024;  // static shared arrays of the kernel (ptxas: 16.0 KB)
+
+size_t i8_tri_extra(const Geometry& g) {  // S staging beyond the plane buffers it aliases when it fits
+    const size_t tri = size_t(g.D) * (g.D + 1) / 2 * 8;
+    return tri <= 2 * size_t(kOps) ? 0 : tri;
+}
+
 int i8_stages(const Geometry& g) {
-    const size_t fixed = 2 * size_t(kOps) + size_t(g.D) * (g.D + 1) / 2 * 8 + 20 * 1024;  // + static smem
+    const size_t fixed = 2 * size_t(kOps) + i8_tri_extra(g) + kStaticSmem;
     const size_t chunk = size_t(kCh) * g.B * 4;
     const int st = int((kSmemCap - fixed) / chunk);
     return st < kMaxStages ? st : kMaxStages;
 }
 
 size_t stats_i8_smem(const Geometry& g) {
-    return 2 * size_t(kOps) + size_t(i8_stages(g)) * kCh * g.B * 4 + size_t(g.D) * (g.D + 1) / 2 * 8;
+    return 2 * size_t(kOps) + size_t(i8_stages(g)) * kCh * g.B * 4 + i8_tri_extra(g);
 }
 
 }  // namespace
@@ -394,9 +440,20 @@ void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(stats_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemCap - 20 * 1024));
+        cudaFuncSetAttribute(stats_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemCap - kStaticSmem));
     }
-    StatsI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, (g.D + 1 + 15) / 16 * 16, i8_stages(g)};
+    static int dbg = -1;
+    if (dbg < 0) {
+        const char* e = getenv("ERX_I8_DEBUG");
+        dbg = e ? atoi(e) : 0;
+    }
+    static int stg = -1;
+    if (stg < 0) {
+        const char* f = getenv("ERX_I8_STAGES");
+        stg = f ? atoi(f) : 0;
+    }
+    const int nst = stg > 0 && stg < i8_stages(g) ? stg : i8_stages(g);
+    StatsI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, (g.D + 1 + 15) / 16 * 16, nst, dbg};
     const int grid = n_lines_total < sms ? n_lines_total : sms;
     stats_i8_kernel<<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
 }
