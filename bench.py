@@ -217,7 +217,15 @@ def run_ours(args):
     dk = kernels[dom]
     src = (f"measured FFMA probe on this GPU in this run (erx_probe_fp32_tflops: register-form "
            f"{reg_peak:.1f}, constant-form {const_peak:.1f} TFLOP/s; the larger is the peak)")
-    if alg[dom]["flops"] > 0 and dom in ("stats", "score") and no_srp:
+    tensor = eng.stats_tensor() == 2
+    if dom in ("stats", "score") and tensor:
+        # exact-integer tcgen05 kernels stream the line from HBM (the digit-plane MMAs are not the
+        # algorithmic flops): the bound is the line's bytes at the measured HBM bandwidth
+        roof = {"bound": "hbm", "kernel": dom, "achieved": dk["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": dk["gbs"] / pk["hbm_gbs"] if dk["gbs"] else None, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "algorithmic": f"{alg[dom]['bytes']} B/line x {S*T} lines/launch"}
+    elif alg[dom]["flops"] > 0 and dom in ("stats", "score") and no_srp:
         roof = {"bound": "fp32", "kernel": dom, "achieved": dk["tflops"], "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": dk["tflops"] / fp32_peak, "traffic": None, "peak_source": src,
                 "algorithmic": f"{alg[dom]['flops']:.4g} flop/line x {S*T} lines/launch"}
@@ -237,7 +245,10 @@ def run_ours(args):
     t_byte = alg["bytes_line"] / (pk["hbm_gbs"] * 1e9)
     roof_lines = 1.0 / max(t_flop, t_byte)
     roofline_line = {"lines_per_s_roofline_per_gpu": roof_lines, "bound": "fp32" if t_flop > t_byte else "hbm",
-                     "frac": (value / world) / roof_lines}
+                     "frac": (value / world) / roof_lines,
+                     "lines_per_s_hbm_bound_per_gpu": 1.0 / t_byte, "frac_of_hbm_bound": (value / world) * t_byte,
+                     "note": "fp32 bound = 2 P D^2 + D^3/3 flop/line at the measured FFMA peak; hbm bound = "
+                             "4 P B + 8 P bytes/line (read the line, write raw+norm) at MEASURED_PEAKS hbm_gbs"}
 
     # end-to-end through the public C ABI with HOST buffers (pinned), H2D + D2H inside the timed region
     e2e = None
@@ -281,7 +292,8 @@ def run_ours(args):
             "metric": "lines/sec (batched independent streams, aggregate over GPUs)",
             "value": value, "unit": "lines/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32 (FFMA stats/whitening) + f64 (scan, Cholesky, inverse)",
+            "vs_baseline": None, "dtype": ("f32 input; stats+score exact int8-digit tcgen05 (s32 TMEM), f32 factor, f64 scan/state"
+                      if tensor else "f32 (FFMA stats/whitening) + f64 (scan, Cholesky, inverse)"),
             "data": "synthetic: BASELINE.json configs[3] generator (include/erx_datagen.h), device pool >= 2x L2 replayed",
             "config": {"workload": f"configs[{cid}]", "streams": S_tot, "streams_per_gpu": S, "pixels": P,
                        "bands": B, "dims": D, "mode": "D=B (no_srp)" if no_srp else "d=5 SRP",
@@ -441,7 +453,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip the single-stream / latency side measurements")
-    ap.add_argument("--stats", type=int, default=0, choices=[0, 1, 2],
+    ap.add_argument("--stats", type=int, default=2, choices=[0, 1, 2],
                     help="line-statistics kernel: 0 FFMA, 1 tcgen05 bf16x3, 2 tcgen05 exact int8")
     ap.add_argument("--host-groups", type=int, default=0, help="stream groups per host window (0 auto)")
     args = ap.parse_args()

@@ -131,10 +131,14 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
  * kernel).  erx_get_option reports the precision in
  * use once the first line has fixed the geometry (0 = blocked fp64 path). */
 #define ERX_OPT_FACTOR_PRECISION 1
-/* ERX_OPT_STATS_TENSOR: 1 runs line_stats on the tcgen05 tensor cores where
- * eligible (full covariance, 32 < D <= 128; bf16x3 split, 6 products), 0
- * (default) the FFMA kernel.  erx_get_option reports whether the tensor
- * kernel is in use. */
+/* ERX_OPT_STATS_TENSOR: which kernels compute line_stats and the score.
+ *   2 (default) exact-integer tcgen05 path (kind::i8 digit planes, s32 TMEM
+ *     accumulation) for both where eligible (full covariance, 16 < D <= 127,
+ *     B % 4 == 0), the FFMA kernels elsewhere;
+ *   1 tcgen05 bf16x3 line statistics (fp32 TMEM accumulation truncates; kept
+ *     as a measured negative result);
+ *   0 the FFMA kernels.
+ * erx_get_option reports the kind in use once the geometry is fixed. */
 #define ERX_OPT_STATS_TENSOR 2
 /* ERX_OPT_HOST_GROUPS: stream groups per host window of erx_push_host (the
  * host->device copy of group g+1 overlaps the kernels of group g).  0 (default)

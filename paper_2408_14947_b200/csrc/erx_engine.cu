@@ -71,11 +71,11 @@ struct erx_engine {
     erxk::SmallLaunch smp{};
     bool small = false;       // D <= 16: stats_small / score_small path
     float* d_vcache = nullptr;  // [S*T][D][P] centred projections (small path)
+    float* d_vmax = nullptr;    // [S*T][D] per-dim |x - c| range (tensor path)
     int factor_req = 0;   // requested factor precision (0 auto, 32, 64)
-    // 1: tcgen05 bf16x3 stats kernel where eligible.  Off by default: the tensor
-    // core's fp32 accumulation truncates (measured -1.8e-8 relative per MMA,
-    // tools/tc_bias.py), which biases K in the noise subspace past the 1e-5 gate.
-    int stats_tensor = 0;
+    // ERX_OPT_STATS_TENSOR: 2 exact-integer tcgen05 stats + score where eligible (default), 1 tcgen05
+    // bf16x3 stats (fp32 TMEM accumulation truncates, tools/tc_bias.py), 0 FFMA kernels.
+    int stats_tensor = 2;
     int factor_prec = 0;  // precision in use (0 = blocked fp64 global path)
 
     // device buffers, capacity S*T lines
@@ -203,6 +203,8 @@ void free_window(erx_engine* e) {
     cudaFree(e->d_status);
     cudaFree(e->d_vcache);
     e->d_vcache = nullptr;
+    cudaFree(e->d_vmax);
+    e->d_vmax = nullptr;
     cudaFreeHost(e->h_lines);
     cudaFreeHost(e->h_status);
     e->d_lines = nullptr;
@@ -252,6 +254,7 @@ int configure(erx_engine* e, uint32_t P) {
     CU(cudaMalloc(&e->d_norm, L * P * sizeof(float)));
     CU(cudaMalloc(&e->d_status, L * sizeof(int)));
     if (e->small) CU(cudaMalloc(&e->d_vcache, L * size_t(g.D) * P * sizeof(float)));
+    if (erxk::stats_i8_eligible(g)) CU(cudaMalloc(&e->d_vmax, L * size_t(g.D) * sizeof(float)));
     return ERX_OK;
 }
 
@@ -317,14 +320,16 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     double* work = e->d_work ? e->d_work + l0 * 2 * size_t(g.Dp) * g.Dp : nullptr;
     float* white = e->d_white + l0 * erxk::whiten_floats_per_line(g);
     float* vcache = e->d_vcache ? e->d_vcache + l0 * size_t(g.D) * g.P : nullptr;
+    float* vmax = e->d_vmax ? e->d_vmax + l0 * size_t(g.D) : nullptr;
+    const bool tensor = e->stats_tensor == 2 && erxk::stats_i8_eligible(g) && erxk::score_i8_eligible(g);
     int* status = e->d_status + l0;
     float* rawg = raw + l0 * g.P;
     float* normg = norm + l0 * g.P;
     timed(e, ERX_KERNEL_STATS, [&] {
         if (e->small)
             erxk::launch_stats_small(g, e->smp, xg, int(n), int(in_stride), L, stats, vcache, e->stream);
-        else if (e->stats_tensor == 2 && erxk::stats_i8_eligible(g))
-            erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, e->stream);
+        else if (tensor)
+            erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, vmax, e->stream);
         else if (e->stats_tensor == 1 && erxk::stats_tc_eligible(g))
             erxk::launch_stats_tc(g, xg, int(n), int(in_stride), L, stats, e->stream);
         else
@@ -344,7 +349,10 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
         });
     } else {
         timed(e, ERX_KERNEL_SCORE, [&] {
-            erxk::launch_score(g, e->sc, xg, int(n), int(in_stride), prior, white, L, rawg, e->stream);
+            if (tensor)
+                erxk::launch_score_i8(g, xg, int(n), int(in_stride), stats, vmax, prior, white, L, rawg, e->stream);
+            else
+                erxk::launch_score(g, e->sc, xg, int(n), int(in_stride), prior, white, L, rawg, e->stream);
         });
         timed(e, ERX_KERNEL_NORMALIZE, [&] { erxk::launch_normalize(g, rawg, L, normg, e->stream); });
     }
@@ -787,7 +795,7 @@ int64_t erx_get_option(const erx_engine* e, int option) {
     if (option == ERX_OPT_HOST_GROUPS) return e->host_groups;
     if (option == ERX_OPT_STATS_TENSOR) {
         if (!e->d_stats) return e->stats_tensor;
-        if (e->stats_tensor == 2 && erxk::stats_i8_eligible(e->geo)) return 2;
+        if (e->stats_tensor == 2 && erxk::stats_i8_eligible(e->geo) && erxk::score_i8_eligible(e->geo)) return 2;
         if (e->stats_tensor == 1 && erxk::stats_tc_eligible(e->geo)) return 1;
         return 0;
     }

@@ -94,8 +94,14 @@ void launch_stats_tc(const Geometry& g, const float* x, int n_per_stream, int in
 
 // Exact-integer tcgen05 stats kernel (k_stats_i8.cu): no_srp, 16 < D <= 127, B % 4 == 0.
 bool stats_i8_eligible(const Geometry& g);
+// vmax (may be null): [line][D] max_p |fl32(x - c)|, the y range the score kernel needs.
 void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
-                     double* stats, cudaStream_t st);
+                     double* stats, float* vmax, cudaStream_t st);
+// Exact-integer tcgen05 score kernel (k_score_i8.cu); needs the stats_i8 centre and vmax.
+bool score_i8_eligible(const Geometry& g);
+void launch_score_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, const double* stats,
+                     const float* vmax, const double* prior, const float* whiten, int n_lines_total, float* raw,
+                     cudaStream_t st);
 
 // Host launchers.  All asynchronous on `st`.
 void launch_stats(const Geometry& g, const StatsLaunch& sl, const float* x, int n_per_stream, int in_stride,

@@ -37,9 +37,6 @@
 // 128 rows x 64 K per plane) and one thread issues 2 K-steps x 8 MMAs
 // (M = 128 dims, N = roundup16(D + 1)) per chunk, committed to the plane
 // buffer's mbarrier; the epilogue stages S in its own shared-memory area.
-#include <cstdio>
-#include <cstdlib>
-
 #include "erx_common.cuh"
 #include "tc_common.cuh"
 
@@ -62,9 +59,9 @@ struct StatsI8Args {
     int in_stride;
     int n_lines;
     double* stats;
+    float* vmax;  // [line][D] max_p |fl32(x - c)| (the score kernel's y range), may be null
     int N;       // MMA N = roundup16(D + 1)
     int stages;  // ring depth
-    int dbg;     // experiment knob (0 = normal)
 };
 
 __device__ __forceinline__ void pack_digits(const uint32_t (&u)[4], uint32_t& w0, uint32_t& w1, uint32_t& w2) {
@@ -79,11 +76,6 @@ __device__ __forceinline__ float fmin_nan(float a, float b) {
     float r;
     asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
     return r;
-}
-__device__ __forceinline__ uint64_t gtimer() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
 }
 __device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads)); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* m) {
@@ -195,7 +187,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
 #pragma unroll
                     for (int s = 0; s < kCh / 32; ++s)
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) if (a.dbg < 2) {
+                        for (int q = 0; q < 8; ++q) {
                             const uint64_t ad = tc::smem_desc(base + pr[q][0] * kPlane + s * tc::kSliceBytes);
                             const uint64_t bd = tc::smem_desc(base + pr[q][1] * kPlane + s * tc::kSliceBytes);
                             const bool first = c == 0 && s == 0 && (q == 0 || q == 2 || q == 5 || q == 7);
@@ -260,10 +252,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     };
 
     float cdk[2] = {0.f, 0.f}, sdk[2] = {0.f, 0.f}, adk[2] = {kMagic, kMagic};
-    uint64_t t0 = 0, t1 = 0, t2 = 0, t3 = 0;
-    const bool trace = a.dbg == 10 && blockIdx.x == 0 && tid == 0;
     for (int k = 0; k < my_lines; ++k) {
-        if (trace) t0 = gtimer();
         // ---- pass 1: range of x per dim (min propagates NaN, max sees +inf); centre from the first 32 pixels
         float4 mn = make_float4(3.402823466e38f, 3.402823466e38f, 3.402823466e38f, 3.402823466e38f);
         float4 mx = make_float4(-3.402823466e38f, -3.402823466e38f, -3.402823466e38f, -3.402823466e38f);
@@ -272,7 +261,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
             const int n = min(kCh, P - c * kCh);
             tc::mbar_wait(&full[st], uint32_t(idx1(k, c)) & 1u);
             const float* sb = ring + size_t(st) * kCh * B;
-            if (quad_live && a.dbg != 1) {
+            if (quad_live) {
                 const int p0 = warp * 8;
                 const float* xp = sb + p0 * B + 4 * lane;
                 if (n >= p0 + 8) {
@@ -307,9 +296,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
         const bool bad_mine = quad_live && !(isfinite(mn.x) && isfinite(mn.y) && isfinite(mn.z) && isfinite(mn.w) &&
                                              isfinite(mx.x) && isfinite(mx.y) && isfinite(mx.z) && isfinite(mx.w));
         // ---- the previous line's epilogue (its MMAs finished while this pass ran)
-        if (trace) t1 = gtimer();
         if (k > 0) epilogue(k - 1);
-        if (trace) t2 = gtimer();
         // ---- ranges of all pixel groups -> centre and per-dim scale of this line
         if (quad_live) {
             *reinterpret_cast<float4*>(&red_mn[warp][4 * lane]) = mn;
@@ -333,6 +320,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                 }
                 const float m = fmaxf(hi - cd, cd - lo);
                 sd = (m > 0.f && m <= 3.402823466e38f) ? kR / m : 0.f;
+                if (a.vmax) a.vmax[size_t(blockIdx.x + k * gridDim.x) * D + d] = m;
             }
             cen_s[d] = cd;
             scale_s[d] = sd;
@@ -342,7 +330,6 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
         bar_compute();
         cdk[0] = cen_s[dd0 & 127]; sdk[0] = scale_s[dd0 & 127]; adk[0] = add_s[dd0 & 127];
         cdk[1] = cen_s[dd1 & 127]; sdk[1] = scale_s[dd1 & 127]; adk[1] = add_s[dd1 & 127];
-        if (trace) t3 = gtimer();
         // ---- pass 2: quantise each chunk into digit planes:
         // y = fma(x - c, s, 1.5 * 2^23) rounds v * s to an integer in the low mantissa bits
         // (|v s| <= 2^22), u = q + 0x808080 = bits(y) - 0x4B400000 + 0x808080
@@ -356,8 +343,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
             const float* sb = ring + size_t(st) * kCh * B + (pg2 * 16) * B;
             unsigned char* op = ops + buf * kOps;
             uint32_t w[2][3][4];
-            if (a.dbg == 1) {
-            } else if (n == kCh) {
+            if (n == kCh) {
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) {
                     uint32_t u0[4], u1[4];
@@ -388,7 +374,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
             }
             const uint32_t off0 = tc::kmajor_off_s8(dd0, pg2 * 16), off1 = tc::kmajor_off_s8(dd1, pg2 * 16);
 #pragma unroll
-            for (int pl = 0; pl < 3; ++pl) if (a.dbg != 1) {
+            for (int pl = 0; pl < 3; ++pl) {
                 *reinterpret_cast<uint4*>(op + pl * kPlane + off0) = make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
                 *reinterpret_cast<uint4*>(op + pl * kPlane + off1) = make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
             }
@@ -398,11 +384,6 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                 mbar_arrive(&empty[st]);
                 mbar_arrive(&pfull[buf]);
             }
-        }
-        if (trace) {
-            const uint64_t t4 = gtimer();
-            printf("i8 line %d: pass1 %.2f us, epilogue %.2f, scales %.2f, pass2 %.2f\n", k, (t1 - t0) * 1e-3,
-                   (t2 - t1) * 1e-3, (t3 - t2) * 1e-3, (t4 - t3) * 1e-3);
         }
     }
     if (my_lines > 0) epilogue(my_lines - 1);
@@ -434,7 +415,7 @@ bool stats_i8_eligible(const Geometry& g) {
 }
 
 void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
-                     double* stats, cudaStream_t st) {
+                     double* stats, float* vmax, cudaStream_t st) {
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -442,18 +423,7 @@ void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(stats_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemCap - kStaticSmem));
     }
-    static int dbg = -1;
-    if (dbg < 0) {
-        const char* e = getenv("ERX_I8_DEBUG");
-        dbg = e ? atoi(e) : 0;
-    }
-    static int stg = -1;
-    if (stg < 0) {
-        const char* f = getenv("ERX_I8_STAGES");
-        stg = f ? atoi(f) : 0;
-    }
-    const int nst = stg > 0 && stg < i8_stages(g) ? stg : i8_stages(g);
-    StatsI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, (g.D + 1 + 15) / 16 * 16, nst, dbg};
+    StatsI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, vmax, (g.D + 1 + 15) / 16 * 16, i8_stages(g)};
     const int grid = n_lines_total < sms ? n_lines_total : sms;
     stats_i8_kernel<<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
 }

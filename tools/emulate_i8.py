@@ -71,7 +71,37 @@ def stats_f32(x):
     return mu, K
 
 
-def erx(lines, alpha, stats, eps=1e-5):
+def digits_product(A, B, digits=3, drop_below=2):
+    """Exact integer A @ B.T through balanced int8 digit planes, dropping weight classes < drop_below."""
+    off = sum(0x80 << (8 * i) for i in range(digits))
+    da = [(((A + off) >> (8 * i)) & 0xFF) - 128 for i in range(digits)]
+    db = [(((B + off) >> (8 * i)) & 0xFF) - 128 for i in range(digits)]
+    out = np.zeros((A.shape[0], B.shape[0]), np.int64)
+    for i in range(digits):
+        for j in range(digits):
+            if i + j >= drop_below:
+                out += (da[i] @ db[j].T) << (8 * (i + j))
+    return out
+
+
+def score_quant(x, mu, L, c, vmax, R=4194000.0, drop_below=2):
+    """k_score_i8 model: y = (x - c) - (mu - c) per-dim scaled, W' = L^-1 / s per-row scaled, digit MMAs."""
+    W = np.linalg.inv(L).astype(np.float32)
+    v = (x - c).astype(np.float32)
+    dc = (mu - c.astype(np.float64)).astype(np.float32)
+    y = (v - dc).astype(np.float32)
+    bound = (vmax + np.abs(dc)) * (1 + 2.0 ** -20)
+    bound[bound == 0] = 1
+    s = (np.float32(R) / bound.astype(np.float32)).astype(np.float32)
+    yq = np.rint(y.astype(np.float64) * s).astype(np.int64)
+    Wp = W / s[None, :]
+    r = (R / np.abs(Wp).max(1)).astype(np.float32)
+    Wq = np.rint(Wp * r[:, None]).astype(np.int64)
+    M = digits_product(yq, Wq, 3, drop_below).astype(np.float64) / r[None, :].astype(np.float64)
+    return np.sqrt((M * M).sum(1))
+
+
+def erx(lines, alpha, stats, eps=1e-5, qscore=False):
     raws = []
     mu = K = None
     for t, x in enumerate(lines):
@@ -85,8 +115,13 @@ def erx(lines, alpha, stats, eps=1e-5):
                 break
             except np.linalg.LinAlgError:
                 e *= 10
-        y = np.linalg.solve(L, (x.astype(np.float64) - mu).T)
-        raws.append(np.sqrt((y * y).sum(0)))
+        if qscore:
+            c = x[:32].astype(np.float64).mean(0).astype(np.float32)
+            vmax = np.abs((x - c).astype(np.float32)).max(0)
+            raws.append(score_quant(x, mu, L, c, vmax))
+        else:
+            y = np.linalg.solve(L, (x.astype(np.float64) - mu).T)
+            raws.append(np.sqrt((y * y).sum(0)))
         if t:
             pass
         mu = (1 - alpha) * mu + alpha * m
@@ -108,8 +143,10 @@ def main():
         "i8 3 digits R=4194000 (2^22), classes>=1": lambda a: stats_quant(a, 4194000.0, 1, 3),
         "i8 2 digits (R=32767), all": lambda a: stats_quant(a, 32639.0, 0, 2),
     }
+    variants["i8 stats + i8 score (classes>=2)"] = (lambda a: stats_quant(a, 4194000.0, 1, 3), True)
     for name, fn in variants.items():
-        r = erx(x, alpha, fn)
+        fn, q = fn if isinstance(fn, tuple) else (fn, False)
+        r = erx(x, alpha, fn, qscore=q)
         rel = np.abs(r - ref) / np.maximum(np.abs(ref), 1e-300)
         print(f"{name:42s} max {rel.max():.3e}  median {np.median(rel):.3e}")
 
