@@ -393,28 +393,27 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
                     }
             }
             __syncthreads();
-            // (c) trailing update A_IJ -= L_Ik L_Jk^T, k < J <= I < nb
+            // (c) trailing update A_IJ -= L_Ik L_Jk^T, k < J <= I < nb: one block ROW per thread (task =
+            //     pair x row), so the step's latency is 64 FMAs instead of 512 and all threads have work
             const int m = nb - k - 1;
-            const int npairs = m * (m + 1) / 2;
-            for (int q = tid; q < npairs; q += nt) {
-                int Ir = int((sqrtf(8.f * q + 1.f) - 1.f) * 0.5f);
-                while (Ir * (Ir + 1) / 2 > q) --Ir;
-                while ((Ir + 1) * (Ir + 2) / 2 <= q) ++Ir;
-                const int I = k + 1 + Ir, J = k + 1 + (q - Ir * (Ir + 1) / 2);
-                float b[kBlk][kBlk];
+            const int ntask = m * (m + 1) / 2 * kBlk;
+            for (int q = tid; q < ntask; q += nt) {
+                const int pq = q >> 3, r = q & 7;
+                int Ir = int((sqrtf(8.f * pq + 1.f) - 1.f) * 0.5f);
+                while (Ir * (Ir + 1) / 2 > pq) --Ir;
+                while ((Ir + 1) * (Ir + 2) / 2 <= pq) ++Ir;
+                const int I = k + 1 + Ir, J = k + 1 + (pq - Ir * (Ir + 1) / 2);
+                float a[kBlk], acc[kBlk];
+                ld8(A + (I * kBlk + r) * LD + k0, a);
+                ld8(A + (I * kBlk + r) * LD + J * kBlk, acc);
 #pragma unroll
-                for (int c = 0; c < kBlk; ++c) ld8(A + (J * kBlk + c) * LD + k0, b[c]);
+                for (int c = 0; c < kBlk; ++c) {
+                    float b[kBlk];
+                    ld8(A + (J * kBlk + c) * LD + k0, b);  // broadcast: the 8 threads of a pair share it
 #pragma unroll
-                for (int r = 0; r < kBlk; ++r) {
-                    float a[kBlk], acc[kBlk];
-                    ld8(A + (I * kBlk + r) * LD + k0, a);
-                    ld8(A + (I * kBlk + r) * LD + J * kBlk, acc);
-#pragma unroll
-                    for (int c = 0; c < kBlk; ++c)
-#pragma unroll
-                        for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], b[c][l], acc[c]);
-                    st8(A + (I * kBlk + r) * LD + J * kBlk, acc);
+                    for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], b[l], acc[c]);
                 }
+                st8(A + (I * kBlk + r) * LD + J * kBlk, acc);
             }
             __syncthreads();
         }
@@ -500,31 +499,29 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
                 ld8(Dinv + r * kBlk, row);
                 st8(A + (k0 + r) * LD + k0, row);
             }
-        // update block rows I > k: T_IJ -= L_Ik X_kJ (J < k), T_Ik = -L_Ik X_kk
-        const int ntask = (nb - k - 1) * (k + 1);
+        // update block rows I > k: T_IJ -= L_Ik X_kJ (J < k), T_Ik = -L_Ik X_kk; task = block x row
+        const int ntask = (nb - k - 1) * (k + 1) * kBlk;
         for (int q = tid; q < ntask; q += nt) {
-            const int I = k + 1 + q / (k + 1), J = q % (k + 1);
-            float xk[kBlk][kBlk];
+            const int tq = q >> 3, r = q & 7;
+            const int I = k + 1 + tq / (k + 1), J = tq % (k + 1);
             const float* xs = (J == k) ? Dinv : A + k0 * LD + J * kBlk;
             const int xld = (J == k) ? kBlk : LD;
+            float a[kBlk], acc[kBlk];
+            ld8(Lc + I * 64 + r * kBlk, a);
+            if (J == k) {
 #pragma unroll
-            for (int l = 0; l < kBlk; ++l) ld8(xs + l * xld, xk[l]);
-#pragma unroll
-            for (int r = 0; r < kBlk; ++r) {
-                float a[kBlk], acc[kBlk];
-                ld8(Lc + I * 64 + r * kBlk, a);
-                if (J == k) {
-#pragma unroll
-                    for (int c = 0; c < kBlk; ++c) acc[c] = 0.f;
-                } else {
-                    ld8(A + (I * kBlk + r) * LD + J * kBlk, acc);
-                }
-#pragma unroll
-                for (int c = 0; c < kBlk; ++c)
-#pragma unroll
-                    for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], xk[l][c], acc[c]);
-                st8(A + (I * kBlk + r) * LD + J * kBlk, acc);
+                for (int c = 0; c < kBlk; ++c) acc[c] = 0.f;
+            } else {
+                ld8(A + (I * kBlk + r) * LD + J * kBlk, acc);
             }
+#pragma unroll
+            for (int l = 0; l < kBlk; ++l) {
+                float xr[kBlk];
+                ld8(xs + l * xld, xr);  // broadcast across the task's 8 threads
+#pragma unroll
+                for (int c = 0; c < kBlk; ++c) acc[c] = fmaf(-a[l], xr[c], acc[c]);
+            }
+            st8(A + (I * kBlk + r) * LD + J * kBlk, acc);
         }
         __syncthreads();
     }
