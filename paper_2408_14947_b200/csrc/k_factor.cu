@@ -332,13 +332,32 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
     int fail;
     const int ntri = D * (D + 1) / 2;
     while (true) {
-        // fill: coalesced reads of the packed fp64 K (many loads in flight), padding = identity
-        for (int idx = tid; idx < ntri; idx += nt) {
-            int i = int((sqrtf(8.f * idx + 1.f) - 1.f) * 0.5f);
-            while (i * (i + 1) / 2 > idx) --i;
-            while ((i + 1) * (i + 2) / 2 <= idx) ++i;
-            const int j = idx - i * (i + 1) / 2;
-            A[i * LD + j] = float(__ldg(K + idx) + (i == j ? eps : 0.0));
+        // fill: coalesced reads of the packed fp64 K, 8 loads in flight per thread (the (i, j) of
+        // idx + nt follows from (i, j) of idx incrementally), padding = identity
+        {
+            int i = int((sqrtf(8.f * tid + 1.f) - 1.f) * 0.5f), j;
+            while (i * (i + 1) / 2 > tid) --i;
+            while ((i + 1) * (i + 2) / 2 <= tid) ++i;
+            j = tid - i * (i + 1) / 2;
+            for (int base = tid; base < ntri; base += 8 * nt) {
+                double v[8];
+                int ii[8], jj[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int idx = base + u * nt;
+                    v[u] = idx < ntri ? __ldg(K + idx) : 0.0;
+                    ii[u] = i;
+                    jj[u] = j;
+                    j += nt;  // advance (i, j) by nt packed positions
+                    while (j > i) {
+                        j -= i + 1;
+                        ++i;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (base + u * nt < ntri) A[ii[u] * LD + jj[u]] = float(v[u] + (ii[u] == jj[u] ? eps : 0.0));
+            }
         }
         for (int i = D + tid; i < Dp; i += nt)
             for (int j = 0; j <= i; ++j) A[i * LD + j] = (i == j) ? 1.f : 0.f;
