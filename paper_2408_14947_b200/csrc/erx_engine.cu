@@ -77,6 +77,8 @@ struct erx_engine {
     // bf16x3 stats (fp32 TMEM accumulation truncates, tools/tc_bias.py), 0 FFMA kernels.
     int stats_tensor = 2;
     int factor_prec = 0;  // precision in use (0 = blocked fp64 global path)
+    bool tensor = false;      // exact-integer tcgen05 stats + score in use (fixed at configure)
+    size_t white_stride = 0;  // floats per line of d_white (fp32 W blocks or int8 W planes)
 
     // device buffers, capacity S*T lines
     float* d_lines = nullptr;
@@ -245,11 +247,17 @@ int configure(erx_engine* e, uint32_t P) {
     e->small = erxk::small_path(g);
     if (e->small) e->smp = erxk::plan_small(g);
     e->factor_prec = erxk::factor_precision(g, e->factor_req);
+    // exact-integer tensor path: stats_i8 + factor writing int8 W planes + score_i8
+    e->tensor = e->stats_tensor == 2 && erxk::stats_i8_eligible(g) && erxk::score_i8_eligible(g) &&
+                e->factor_prec == 32;
+    e->white_stride = e->tensor ? erxk::wplanes_bytes_per_line() / sizeof(float) : erxk::whiten_floats_per_line(g);
     const size_t L = size_t(e->S) * e->T;
     CU(cudaMalloc(&e->d_stats, L * (g.SE + g.D) * sizeof(double)));  // [c | s | S] per line
     CU(cudaMalloc(&e->d_prior, L * g.SE * sizeof(double)));
     if (e->factor_prec == 0) CU(cudaMalloc(&e->d_work, L * 2 * size_t(g.Dp) * g.Dp * sizeof(double)));
-    CU(cudaMalloc(&e->d_white, L * erxk::whiten_floats_per_line(g) * sizeof(float)));
+    CU(cudaMalloc(&e->d_white, L * std::max(erxk::whiten_floats_per_line(g),
+                                            erxk::stats_i8_eligible(g) ? erxk::wplanes_bytes_per_line() / 4 : size_t(0)) *
+                                    sizeof(float)));
     CU(cudaMalloc(&e->d_raw, L * P * sizeof(float)));
     CU(cudaMalloc(&e->d_norm, L * P * sizeof(float)));
     CU(cudaMalloc(&e->d_status, L * sizeof(int)));
@@ -318,10 +326,10 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     const double* st_in = e->d_state[e->cur] + size_t(s0) * g.SE;
     double* st_out = e->d_state[e->cur ^ 1] + size_t(s0) * g.SE;
     double* work = e->d_work ? e->d_work + l0 * 2 * size_t(g.Dp) * g.Dp : nullptr;
-    float* white = e->d_white + l0 * erxk::whiten_floats_per_line(g);
+    float* white = e->d_white + l0 * e->white_stride;
     float* vcache = e->d_vcache ? e->d_vcache + l0 * size_t(g.D) * g.P : nullptr;
     float* vmax = e->d_vmax ? e->d_vmax + l0 * size_t(g.D) : nullptr;
-    const bool tensor = e->stats_tensor == 2 && erxk::stats_i8_eligible(g) && erxk::score_i8_eligible(g);
+    const bool tensor = e->tensor;
     int* status = e->d_status + l0;
     float* rawg = raw + l0 * g.P;
     float* normg = norm + l0 * g.P;
@@ -341,7 +349,7 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     });
     timed(e, ERX_KERNEL_FACTOR, [&] {
         erxk::launch_factor(g, prior, L, e->cfg.epsilon, work, white, status, e->d_latch, line_base, e->factor_prec,
-                            e->stream);
+                            e->stream, stats, tensor ? vmax : nullptr);
     });
     if (e->small) {  // score + normalisation fused
         timed(e, ERX_KERNEL_SCORE, [&] {
@@ -350,7 +358,8 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     } else {
         timed(e, ERX_KERNEL_SCORE, [&] {
             if (tensor)
-                erxk::launch_score_i8(g, xg, int(n), int(in_stride), stats, vmax, prior, white, L, rawg, e->stream);
+                erxk::launch_score_i8(g, xg, int(n), int(in_stride), stats, vmax, prior,
+                                      reinterpret_cast<const unsigned char*>(white), L, rawg, e->stream);
             else
                 erxk::launch_score(g, e->sc, xg, int(n), int(in_stride), prior, white, L, rawg, e->stream);
         });
@@ -774,6 +783,11 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
     if (option == ERX_OPT_STATS_TENSOR) {
         if (value < 0 || value > 2) return fail(e, ERX_ERR_CONFIG, "stats tensor: 0, 1 or 2");
         e->stats_tensor = int(value);
+        if (e->d_stats) {
+            const uint32_t P = e->P;
+            e->P = 0;  // re-plan (the tensor path changes the whitening operand's format)
+            return configure(e, P);
+        }
         return ERX_OK;
     }
     if (option == ERX_OPT_FACTOR_PRECISION) {
@@ -795,7 +809,7 @@ int64_t erx_get_option(const erx_engine* e, int option) {
     if (option == ERX_OPT_HOST_GROUPS) return e->host_groups;
     if (option == ERX_OPT_STATS_TENSOR) {
         if (!e->d_stats) return e->stats_tensor;
-        if (e->stats_tensor == 2 && erxk::stats_i8_eligible(e->geo) && erxk::score_i8_eligible(e->geo)) return 2;
+        if (e->tensor) return 2;
         if (e->stats_tensor == 1 && erxk::stats_tc_eligible(e->geo)) return 1;
         return 0;
     }

@@ -99,9 +99,11 @@ void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in
                      double* stats, float* vmax, cudaStream_t st);
 // Exact-integer tcgen05 score kernel (k_score_i8.cu); needs the stats_i8 centre and vmax.
 bool score_i8_eligible(const Geometry& g);
+// wplanes: the factor's int8 W planes (wplanes_bytes_per_line() per line).
+size_t wplanes_bytes_per_line();
 void launch_score_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, const double* stats,
-                     const float* vmax, const double* prior, const float* whiten, int n_lines_total, float* raw,
-                     cudaStream_t st);
+                     const float* vmax, const double* prior, const unsigned char* wplanes, int n_lines_total,
+                     float* raw, cudaStream_t st);
 
 // Host launchers.  All asynchronous on `st`.
 void launch_stats(const Geometry& g, const StatsLaunch& sl, const float* x, int n_per_stream, int in_stride,
@@ -110,8 +112,11 @@ void launch_scan(const Geometry& g, const double* stats, double* prior, const do
                  int n_streams, int n_per_stream, int initialized, double alpha, int incremental, int64_t n_seen0,
                  cudaStream_t st);
 // latch: {flag, line, pivot} of the first factorisation failure (sticky until the host clears it).
+// vmax != null (precision 32 only): write the tensor path's int8 W planes (k_factor.cu: write_wplanes,
+// i8::kWBytes per line) instead of the fp32 blocks.
 void launch_factor(const Geometry& g, const double* prior, int n_lines_total, double eps0, double* work,
-                   float* whiten, int* status, int* latch, int line_base, int precision, cudaStream_t st);
+                   float* whiten, int* status, int* latch, int line_base, int precision, cudaStream_t st,
+                   const double* stats = nullptr, const float* vmax = nullptr);
 void launch_score(const Geometry& g, const ScoreLaunch& sc, const float* x, int n_per_stream, int in_stride,
                   const double* prior, const float* whiten, int n_lines_total, float* raw, cudaStream_t st);
 void launch_normalize(const Geometry& g, const float* raw, int n_lines_total, float* norm, cudaStream_t st);

@@ -15,6 +15,7 @@
 #include <algorithm>
 
 #include "erx_common.cuh"
+#include "i8_common.cuh"
 
 namespace erxk {
 namespace {
@@ -36,6 +37,54 @@ __device__ __forceinline__ void write_wblocks(float* __restrict__ whiten, int li
         const int J = bq - I * (I + 1) / 2;
         const int i = I * kBlk + r, j = J * kBlk + c;
         Wp[idx] = (i < g.D && j <= i) ? get(i, j) : 0.f;
+    }
+}
+
+// The tensor path's whitening operand (k_score_i8.cu), written instead of the fp32 blocks:
+// W'_ij = W_ij / s_j folds the score's per-dim y scale into W, each row i is scaled by
+// r_i = R / max_j |W'_ij| and rounded once to three int8 digit planes laid out exactly as the
+// score kernel's MMA B operand (i8::kWBytes per line, followed by 256 / r_i per row).
+__device__ void write_wplanes(unsigned char* __restrict__ planes, int line, const Geometry& g, const float* A, int LD,
+                              const double* __restrict__ stats, const double* __restrict__ prior,
+                              const float* __restrict__ vmax) {
+    __shared__ float isc[128];
+    const int tid = threadIdx.x, nt = blockDim.x, D = g.D;
+    for (int d = tid; d < 128; d += nt) {
+        float v = 0.f;
+        if (d < D) {
+            const i8::YScale ys = i8::y_scale(stats + size_t(line) * (g.SE + g.D), prior + size_t(line) * g.SE,
+                                              vmax + size_t(line) * D, d);
+            v = ys.s > 0.f ? 1.f / ys.s : 0.f;
+        }
+        isc[d] = v;
+    }
+    __syncthreads();
+    unsigned char* out = planes + size_t(line) * i8::kWBytes;
+    float* invr = reinterpret_cast<float*>(out + 3 * i8::kWPlane);
+    for (int i = tid; i < 128; i += nt) {
+        float mx = 0.f;
+        if (i < D)
+            for (int j = 0; j <= i; ++j) mx = fmaxf(mx, fabsf(A[i * LD + j] * isc[j]));
+        const float r = (mx > 0.f && mx <= 3.402823466e38f) ? i8::kR / mx : 0.f;
+        invr[i] = r > 0.f ? 256.f / r : 0.f;
+        for (int run = 0; run < 8; ++run) {
+            uint32_t w[3][4];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                uint32_t u[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int j = run * 16 + q4 * 4 + e;
+                    const float wv = (i < D && j <= i) ? A[i * LD + j] * isc[j] : 0.f;
+                    u[e] = i8::quant_u(wv, r);
+                }
+                i8::pack_digits(u, w[0][q4], w[1][q4], w[2][q4]);
+            }
+            const uint32_t off = tc::kmajor_off_s8(i, run * 16);
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl)
+                *reinterpret_cast<uint4*>(out + pl * i8::kWPlane + off) = make_uint4(w[pl][0], w[pl][1], w[pl][2], w[pl][3]);
+        }
     }
 }
 
@@ -318,7 +367,9 @@ __device__ __forceinline__ void st8(float* p, const float* v) {
 
 __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const double* __restrict__ prior, double eps0,
                                                          float* __restrict__ whiten, int* __restrict__ status,
-                                                         int* __restrict__ latch, int line_base) {
+                                                         int* __restrict__ latch, int line_base,
+                                                         const double* __restrict__ stats,
+                                                         const float* __restrict__ vmax) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_fail;
     const int D = g.D, Dp = g.Dp, nb = g.nb, LD = Dp + 4;
@@ -544,7 +595,11 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
         }
         __syncthreads();
     }
-    write_wblocks(whiten, line, g, [&](int i, int j) { return A[i * LD + j]; });
+    if (vmax) {
+        write_wplanes(reinterpret_cast<unsigned char*>(whiten), line, g, A, LD, stats, prior, vmax);
+    } else {
+        write_wblocks(whiten, line, g, [&](int i, int j) { return A[i * LD + j]; });
+    }
     if (tid == 0) status[line] = -1;
 }
 
@@ -573,11 +628,13 @@ int factor_precision(const Geometry& g, int requested) {
 }
 
 void launch_factor(const Geometry& g, const double* prior, int n_lines_total, double eps0, double* work,
-                   float* whiten, int* status, int* latch, int line_base, int precision, cudaStream_t st) {
+                   float* whiten, int* status, int* latch, int line_base, int precision, cudaStream_t st,
+                   const double* stats, const float* vmax) {
     const size_t sm = factor_smem(g, precision);
     if (precision == 32) {
         cudaFuncSetAttribute(factor_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        factor_blk_kernel<<<n_lines_total, 128, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base);
+        factor_blk_kernel<<<n_lines_total, 128, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
+                                                          vmax);
     } else if (precision == 64) {
         cudaFuncSetAttribute(factor_smem_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         factor_smem_kernel<double><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base);

@@ -3,30 +3,31 @@
 // 5th-generation tensor cores with EXACT integer accumulation (kind::i8),
 // the companion of k_stats_i8.cu.
 //
-// For one line, m = W y_p with W = L^{-1} (fp32, packed lower 8x8 blocks from
-// k_factor.cu) and y_p = z_p - mu_{t-1}; delta_p = ||m||.  As one GEMM per
-// 128-pixel tile: D[p][i] = sum_j yq[p][j] * Wq[i][j] with
+// For one line, m = W y_p with W = L^{-1} and y_p = z_p - mu_{t-1};
+// delta_p = ||m||.  As one GEMM per 128-pixel tile:
+// D[p][i] = sum_j yq[p][j] * Wq[i][j] with
 //   y_pd  = fl32(fl32(x_pd - c_d) - fl32(mu_d - c_d))    (c: the stats centre)
 //   s_d   = R / bound_d,  bound_d = (max_p |x_pd - c_d| + |mu_d - c_d|)(1 + 2^-20)
 //           (max from k_stats_i8, so |y s| <= R without another pass)
 //   yq    = rint(y s),                 |yq| <= R = 4194000 < 2^22
-//   r_i   = R / max_j |W'_ij|,  W'_ij = fl32(W_ij * fl32(1 / s_j)),  Wq_ij = rint(W'_ij r_i)
+//   W'_ij = fl32(W_ij * fl32(1 / s_j)),  r_i = R / max_j |W'_ij|,  Wq_ij = rint(W'_ij r_i)
 //   m_i   = (sum_j yq_pj Wq_ij) / r_i
-// Both operands are split into three balanced signed int8 digits; digit-pair
-// products with weight class i + j >= 1 accumulate exactly in four s32 TMEM
-// accumulators (class 0 is 2^-30 relative and dropped).  Emulated raw-score
-// error vs fp64 on configs[3]: max 3.4e-6 / median 4.0e-7 (tools/emulate_i8.py;
-// classes >= 2 alone would give 2.3e-6 median, so class 1 stays).
+// (i8_common.cuh: y_scale; the factor kernel writes Wq as int8 digit planes,
+// k_factor.cu: write_wplanes).  Both operands are three balanced signed int8
+// digits; digit-pair products with weight class i + j >= 1 accumulate exactly
+// in four s32 TMEM accumulators (class 0 is 2^-30 relative and dropped).
+// Emulated raw-score error vs fp64 on configs[3]: max 3.4e-6 / median 4.0e-7
+// (tools/emulate_i8.py; classes >= 2 alone would give 2.3e-6 median).
 //
-// Pipeline: one persistent CTA per SM walks whole lines (the line's W planes
-// are built once, then its pixel tiles).  Warps 0-7 stage x with cp.async one
-// tile ahead (64 dims of one pixel per thread, private shared slots), quantise
-// into double-buffered y digit planes and run the epilogue (TMEM -> m_i -> delta);
-// warp 8 issues 4 K-steps x 8 digit pairs of M=128, N=roundup16(D), K=32
-// MMAs per tile.  The epilogue of tile t-1 runs after the quantisation of
-// tile t, while the MMAs of tile t wait only for the accumulator release.
+// Pipeline: one persistent CTA per SM walks whole lines.  Per line one bulk
+// copy brings the line's W planes (48 KB + row factors) into shared memory.
+// Warps 0-7 stage x with cp.async one tile ahead (64 dims of one pixel per
+// thread, private shared slots), quantise into double-buffered y digit planes
+// and run the epilogue (TMEM -> m_i -> delta); warp 8 issues 4 K-steps x 8
+// digit pairs of M=128, N=roundup16(D), K=32 MMAs per tile.  The epilogue of
+// tile t-1 runs after the quantisation of tile t.
 #include "erx_common.cuh"
-#include "tc_common.cuh"
+#include "i8_common.cuh"
 
 namespace erxk {
 namespace {
@@ -35,9 +36,8 @@ constexpr int kTile = 128;                          // pixels per tile (MMA M)
 constexpr int kKSteps = 4;                          // K = 128 dims
 constexpr uint32_t kPlane = kKSteps * tc::kSliceBytes;  // 16 KB: 128 rows x 128 int8
 constexpr uint32_t kOps = 3 * kPlane;               // three digit planes
-constexpr float kR = 4194000.f;
-constexpr float kMagic = 12582912.f;                // 1.5 * 2^23
 constexpr int kThreads = 256;
+static_assert(kPlane == i8::kWPlane, "W plane layout");
 
 struct ScoreI8Args {
     Geometry g;
@@ -45,27 +45,14 @@ struct ScoreI8Args {
     int n;
     int in_stride;
     int n_lines;
-    const double* stats;   // [c | s | S] per line (c = the centre used by k_stats_i8)
-    const float* vmax;     // [line][D] max_p |fl32(x - c)|
-    const double* prior;   // [line][SE]: mu_{t-1}, K_{t-1}
-    const float* W;        // packed lower 8x8 blocks per line
+    const double* stats;            // [c | s | S] per line (c = the centre used by k_stats_i8)
+    const float* vmax;              // [line][D] max_p |fl32(x - c)|
+    const double* prior;            // [line][SE]: mu_{t-1}, K_{t-1}
+    const unsigned char* wplanes;   // [line][i8::kWBytes]
     float* raw;
-    int N;                 // MMA N = roundup16(D)
+    int N;                          // MMA N = roundup16(D)
 };
 
-__device__ __forceinline__ void pack_digits(const uint32_t (&u)[4], uint32_t& w0, uint32_t& w1, uint32_t& w2) {
-    const uint32_t t01 = __byte_perm(u[0], u[1], 0x5140), t23 = __byte_perm(u[2], u[3], 0x5140);
-    w0 = __byte_perm(t01, t23, 0x5410) ^ 0x80808080u;
-    w1 = __byte_perm(t01, t23, 0x7632) ^ 0x80808080u;
-    const uint32_t r01 = __byte_perm(u[0], u[1], 0x0062), r23 = __byte_perm(u[2], u[3], 0x0062);
-    w2 = __byte_perm(r01, r23, 0x5410) ^ 0x80808080u;
-}
-__device__ __forceinline__ uint32_t quant_u(float v, float k) {  // q + 0x808080 with q = rint(v k), |v k| <= 2^22
-    return __float_as_uint(fmaf(v, k, kMagic)) + (0x808080u - 0x4B400000u);
-}
-__device__ __forceinline__ float i2f22(uint32_t a) {  // exact for |int(a)| < 2^22
-    return __uint_as_float(a + 0x4B400000u) - kMagic;
-}
 __device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads)); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* m) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(m)) : "memory");
@@ -84,7 +71,7 @@ __device__ __noinline__ void score_epilogue(uint32_t taddr, int g0, int g1, int 
         tc::tmem_ld16x4(taddr + uint32_t(gi * 16), 128u, v);
 #pragma unroll
         for (int ii = 0; ii < 16; ++ii) {
-            // m_int = 256 (a1 + 256 (a2 + 256 (a3 + 256 a4))); invr holds 256 / r_i (0 for padding).
+            // m_int = 256 (a1 + 256 (a2 + 256 (a3 + 256 a4))); invr holds 256 / r_i (0 for padding)
             float m = fmaf(float(int(v[3][ii])), 256.f, float(int(v[2][ii])));
             m = fmaf(m, 256.f, float(int(v[1][ii])));
             m = fmaf(m, 256.f, float(int(v[0][ii])));
@@ -104,8 +91,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) score_i8_kernel(ScoreI8Args 
     __shared__ uint32_t tmem_slot;
     __shared__ __align__(8) uint64_t wfull, pfull[2], pempty[2], accfull, accempty;
     __shared__ __align__(16) float cen_s[128], dc_s[128], sc_s[128];
-    __shared__ float invr_s[128], isc_s[128];
-    __shared__ float rmax_s[2][128];
+    __shared__ __align__(16) float invr_s[128];
     __shared__ float red_s[2][128];
 
     const Geometry& g = a.g;
@@ -117,7 +103,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) score_i8_kernel(ScoreI8Args 
     const int my_lines = blockIdx.x < a.n_lines ? (a.n_lines - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
     if (tid == 0) {
-        tc::mbar_init(&wfull, 8);
+        tc::mbar_init(&wfull, 1);
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&pfull[b], 8);
             tc::mbar_init(&pempty[b], 1);
@@ -174,7 +160,9 @@ __global__ void __launch_bounds__(kThreads + 32, 1) score_i8_kernel(ScoreI8Args 
     const int qp = tid & 127, qh = tid >> 7;  // quantisation: pixel, 64-dim half
     int t_all = 0;
 
-    auto epilogue = [&](int line, int t, int tall) {
+    auto epilogue = [&](int kk, int t, int tall) {
+        const int line = blockIdx.x + kk * int(gridDim.x);
+        if (t == 0) tc::mbar_wait(&wfull, uint32_t(kk) & 1u);  // the line's row factors have landed
         score_epilogue(tmem + lane_base, g0, g1, colh, row, tid, tall, &accfull, &accempty, invr_s, red_s[tall & 1],
                        t * kTile + row < P ? a.raw + size_t(line) * P + t * kTile + row : nullptr);
     };
@@ -195,85 +183,25 @@ __global__ void __launch_bounds__(kThreads + 32, 1) score_i8_kernel(ScoreI8Args 
     if (my_lines > 0) issue_x(blockIdx.x, 0);
     for (int k = 0; k < my_lines; ++k) {
         const int line = blockIdx.x + k * gridDim.x;
-        const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
-        const double* st = a.stats + size_t(line) * (g.SE + g.D);
-        const double* mu = a.prior + size_t(line) * g.SE;
-        // ---- per-dim constants of this line (the previous line's epilogue has drained the MMAs)
-        if (k > 0) epilogue(line - int(gridDim.x), ntile - 1, t_all - 1);
+        // ---- the previous line's last epilogue drains its MMAs; then the W planes may be replaced
+        if (k > 0) epilogue(k - 1, ntile - 1, t_all - 1);
+        if (tid == 0) {
+            const unsigned char* src = a.wplanes + size_t(line) * i8::kWBytes;
+            tc::mbar_expect_tx(&wfull, i8::kWBytes);
+            tc::bulk_g2s(wops, src, 3 * i8::kWPlane, &wfull);
+            tc::bulk_g2s(invr_s, src + 3 * i8::kWPlane, 128 * 4, &wfull);
+        }
         if (tid < 128) {
             const int d = tid;
-            float c = 0.f, dc = 0.f, s = 0.f;
-            if (d < D) {
-                c = float(st[d]);
-                dc = float(mu[d] - st[d]);
-                const float bound = (a.vmax[size_t(line) * D + d] + fabsf(dc)) * (1.f + 9.5367431640625e-07f);
-                s = (bound > 0.f && bound <= 3.402823466e38f) ? kR / bound : 0.f;
-            }
-            cen_s[d] = c;
-            dc_s[d] = dc;
-            sc_s[d] = s;
-            isc_s[d] = s > 0.f ? 1.f / s : 0.f;
+            i8::YScale ys{0.f, 0.f, 0.f};
+            if (d < D)
+                ys = i8::y_scale(a.stats + size_t(line) * (g.SE + g.D), a.prior + size_t(line) * g.SE,
+                                 a.vmax + size_t(line) * D, d);
+            cen_s[d] = ys.c;
+            dc_s[d] = ys.dc;
+            sc_s[d] = ys.s;
         }
         bar_compute();
-        // ---- W digit planes: row i = qp, columns j in [64 qh, 64 qh + 64).  Loads are unconditional
-        // (clamped addresses, selects after) so they overlap; the row max and the quantisation each
-        // re-read the row (L1/L2 hits), 16 values at a time.
-        {
-            const int i = qp;
-            const float* Wl = a.W + size_t(line) * (g.nb * (g.nb + 1) / 2) * 64;
-            const int ic = min(i, D - 1), I = ic >> 3;
-            const float* wrow = Wl + (I * (I + 1) / 2) * 64 + (ic & 7);
-            auto wprime = [&](int jj, float wraw) {  // W'_ij = W_ij / s_j (0 outside the lower triangle)
-                const int j = qh * 64 + jj;
-                return (i < D && j <= i) ? wraw * isc_s[j] : 0.f;
-            };
-            float mx = 0.f;
-#pragma unroll 1
-            for (int run = 0; run < 4; ++run) {
-                float wv[16];
-                const float* wr = wrow;
-                asm volatile("" : "+l"(wr));  // keep address arithmetic per run (no 64 live addresses)
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const int j = min(qh * 64 + run * 16 + e, ic);
-                    wv[e] = __ldg(wr + (j >> 3) * 64 + (j & 7) * 8);
-                }
-#pragma unroll
-                for (int e = 0; e < 16; ++e) mx = fmaxf(mx, fabsf(wprime(run * 16 + e, wv[e])));
-            }
-            rmax_s[qh][i] = mx;
-            bar_compute();
-            const float rm = fmaxf(rmax_s[0][i], rmax_s[1][i]);
-            const float r = (rm > 0.f && rm <= 3.402823466e38f) ? kR / rm : 0.f;
-            if (qh == 0) invr_s[i] = r > 0.f ? 256.f / r : 0.f;
-            bar_compute();  // rmax_s read, invr_s visible to every epilogue of this line
-#pragma unroll 1
-            for (int run = 0; run < 4; ++run) {
-                float wv[16];
-                const float* wr = wrow;
-                asm volatile("" : "+l"(wr));  // keep address arithmetic per run (no 64 live addresses)
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const int j = min(qh * 64 + run * 16 + e, ic);
-                    wv[e] = __ldg(wr + (j >> 3) * 64 + (j & 7) * 8);
-                }
-                uint32_t w[3][4];
-#pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {
-                    uint32_t u[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) u[e] = quant_u(wprime(run * 16 + q4 * 4 + e, wv[q4 * 4 + e]), r);
-                    pack_digits(u, w[0][q4], w[1][q4], w[2][q4]);
-                }
-                const uint32_t off = tc::kmajor_off_s8(i, qh * 64 + run * 16);
-#pragma unroll
-                for (int pl = 0; pl < 3; ++pl)
-                    *reinterpret_cast<uint4*>(wops + pl * kPlane + off) = make_uint4(w[pl][0], w[pl][1], w[pl][2], w[pl][3]);
-            }
-            tc::fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&wfull);
-        }
         // ---- pixel tiles
         for (int t = 0; t < ntile; ++t, ++t_all) {
             const int buf = t_all & 1;
@@ -293,31 +221,32 @@ __global__ void __launch_bounds__(kThreads + 32, 1) score_i8_kernel(ScoreI8Args 
                     const float4 e4 = *reinterpret_cast<const float4*>(&dc_s[d0]);
                     const float4 s4 = *reinterpret_cast<const float4*>(&sc_s[d0]);
                     uint32_t u[4];
-                    u[0] = quant_u((x4.x - c4.x) - e4.x, s4.x);
-                    u[1] = quant_u((x4.y - c4.y) - e4.y, s4.y);
-                    u[2] = quant_u((x4.z - c4.z) - e4.z, s4.z);
-                    u[3] = quant_u((x4.w - c4.w) - e4.w, s4.w);
+                    u[0] = i8::quant_u((x4.x - c4.x) - e4.x, s4.x);
+                    u[1] = i8::quant_u((x4.y - c4.y) - e4.y, s4.y);
+                    u[2] = i8::quant_u((x4.z - c4.z) - e4.z, s4.z);
+                    u[3] = i8::quant_u((x4.w - c4.w) - e4.w, s4.w);
                     if (!pv) u[0] = u[1] = u[2] = u[3] = 0x808080u;
-                    pack_digits(u, w[0][q4], w[1][q4], w[2][q4]);
+                    i8::pack_digits(u, w[0][q4], w[1][q4], w[2][q4]);
                 }
                 const uint32_t off = tc::kmajor_off_s8(qp, qh * 64 + run * 16);
 #pragma unroll
                 for (int pl = 0; pl < 3; ++pl)
                     *reinterpret_cast<uint4*>(op + pl * kPlane + off) = make_uint4(w[pl][0], w[pl][1], w[pl][2], w[pl][3]);
             }
-            // prefetch the next tile (of this line or the next one) into the same private slots
+            tc::fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pfull[buf]);
+            // prefetch the next tile (of this line or the next one) into the same private slots; issued
+            // after the proxy fence, which would otherwise wait for these copies to land
             {
                 const int tn = t + 1 < ntile ? t + 1 : 0;
                 const int ln = t + 1 < ntile ? line : line + int(gridDim.x);
                 if (t + 1 < ntile || k + 1 < my_lines) issue_x(ln, tn);
             }
-            tc::fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&pfull[buf]);
-            if (t > 0) epilogue(line, t - 1, t_all - 1);
+            if (t > 0) epilogue(k, t - 1, t_all - 1);
         }
     }
-    if (my_lines > 0) epilogue(blockIdx.x + (my_lines - 1) * int(gridDim.x), ntile - 1, t_all - 1);
+    if (my_lines > 0) epilogue(my_lines - 1, ntile - 1, t_all - 1);
     tc::tc_fence_before();
     bar_compute();
     if (warp == 0) tc::tmem_free<512>(tmem);
@@ -325,11 +254,13 @@ __global__ void __launch_bounds__(kThreads + 32, 1) score_i8_kernel(ScoreI8Args 
 
 }  // namespace
 
-bool score_i8_eligible(const Geometry& g) { return !g.srp && g.D > 16 && g.D <= 128 && (g.B % 4) == 0; }
+size_t wplanes_bytes_per_line() { return i8::kWBytes; }
+
+bool score_i8_eligible(const Geometry& g) { return !g.srp && g.D > 16 && g.D <= 127 && (g.B % 4) == 0; }
 
 void launch_score_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, const double* stats,
-                     const float* vmax, const double* prior, const float* whiten, int n_lines_total, float* raw,
-                     cudaStream_t st) {
+                     const float* vmax, const double* prior, const unsigned char* wplanes, int n_lines_total,
+                     float* raw, cudaStream_t st) {
     static int sms = 0;
     const size_t smem = 3 * size_t(kOps) + 16 * size_t(kThreads) * 16;  // W + 2 y plane sets + x staging
     if (!sms) {
@@ -338,7 +269,7 @@ void launch_score_i8(const Geometry& g, const float* x, int n_per_stream, int in
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(score_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     }
-    ScoreI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, vmax, prior, whiten, raw, (g.D + 15) / 16 * 16};
+    ScoreI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, vmax, prior, wplanes, raw, (g.D + 15) / 16 * 16};
     const int grid = n_lines_total < sms ? n_lines_total : sms;
     score_i8_kernel<<<grid, kThreads + 32, smem, st>>>(a);
 }
