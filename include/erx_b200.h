@@ -177,6 +177,10 @@ int erx_probe_stream(erx_engine* e, int mode, uint32_t chunk_bytes, int stages, 
  * from bf16 operands (split = 0) or the 3-way bf16 split with 6 products
  * (split = 1, fp32-accurate).  K a multiple of 16, <= 256. */
 int erx_tc_selftest(erx_engine* e, const float* dA, const float* dB, int K, int split, float* dD);
+/* kind::i8 check (exact s32): D[128][N] = A[128][K] B[N][K]^T with A staged K-major or MN-major
+ * (a_mn; layout strides ms / ks between 16-row M groups / 8-row K groups, descriptor lbo / sbo). */
+int erx_tc_selftest_i8(erx_engine* e, const int8_t* dA, const int8_t* dB, int K, int N, int a_mn, int ms, int ks,
+                       int lbo, int sbo, int* dD);
 
 /* CUDA events on the engine stream, for callers timing device work. */
 int erx_event_record(erx_engine* e, int slot);

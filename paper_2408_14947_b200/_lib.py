@@ -94,6 +94,7 @@ SIGNATURES = {
     "erx_probe_ffma2_tflops": (C.c_int, [_vp, _dp]),
     "erx_probe_stream": (C.c_int, [_vp, C.c_int, C.c_uint32, C.c_int, C.c_int, C.c_uint64, _dp]),
     "erx_tc_selftest": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, _vp]),
+    "erx_tc_selftest_i8": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp]),
     "erx_event_record": (C.c_int, [_vp, C.c_int]),
     "erx_event_elapsed_ms": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_float)]),
     "erx_host_alloc": (C.c_void_p, [C.c_size_t]),

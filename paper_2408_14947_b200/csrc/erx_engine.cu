@@ -858,6 +858,15 @@ int erx_probe_fp32_tflops(erx_engine* e, double* reg_form, double* const_form) {
     return ERX_OK;
 }
 
+int erx_tc_selftest_i8(erx_engine* e, const int8_t* dA, const int8_t* dB, int K, int N, int a_mn, int ms, int ks,
+                       int lbo, int sbo, int* dD) {
+    CU(cudaSetDevice(e->device));
+    if (K < 32 || K % 32 || K > 128 || N < 16 || N > 128 || N % 16) return fail(e, ERX_ERR_CONFIG, "tc_selftest_i8 shape");
+    CU(cudaError_t(erxk::tc_selftest_i8(dA, dB, K, N, a_mn, ms, ks, lbo, sbo, dD, e->stream)));
+    CU(cudaStreamSynchronize(e->stream));
+    return ERX_OK;
+}
+
 int erx_tc_selftest(erx_engine* e, const float* dA, const float* dB, int K, int split, float* dD) {
     CU(cudaSetDevice(e->device));
     if (K % 16 || K < 16 || K > 256) return fail(e, ERX_ERR_CONFIG, "K must be a multiple of 16 in [16, 256]");

@@ -130,5 +130,8 @@ double probe_ffma2_tflops(cudaStream_t st);
 double probe_stream_gbs(cudaStream_t st, int mode, int chunk_bytes, int stages, int ctas_per_sm, size_t bytes);
 // tcgen05 self-test: D[128][128] = A[128][K] B[128][K]^T (bf16, split = 1: 3-way split, 6 products).
 int tc_selftest(const float* dA, const float* dB, int K, int split, float* dD, cudaStream_t st);
+// kind::i8 self-test: D[128][N] = A[128][K] B[N][K]^T (s32), A K-major or MN-major with (ms, ks) layout strides.
+int tc_selftest_i8(const int8_t* dA, const int8_t* dB, int K, int N, int a_mn, int ms, int ks, int lbo, int sbo,
+                   int* dD, cudaStream_t st);
 
 }  // namespace erxk

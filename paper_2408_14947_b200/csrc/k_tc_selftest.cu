@@ -75,7 +75,75 @@ __global__ void __launch_bounds__(128) tc_selftest_kernel(const float* __restric
     if (warp == 0) tc::tmem_free<128>(tmem);
 }
 
+// int8 check: D[128][N] (s32) = A[128][K] . B[N][K]^T, K = 32 * ksteps.  A is laid out either
+// K-major (kmajor_off_s8) or MN-major: K-step s, 16-row M group mg, 8-row K group kg at
+// s * 4096 + mg * ms + kg * ks (+ row * 16 + m % 16), described with (lbo, sbo).
+__global__ void __launch_bounds__(128) tc_selftest_i8_kernel(const int8_t* __restrict__ A, const int8_t* __restrict__ B,
+                                                             int K, int N, int a_mn, int ms, int ks, int lbo, int sbo,
+                                                             int* __restrict__ D) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t mbar;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int ksteps = K / 32;
+    unsigned char* pa = smem;
+    unsigned char* pb = smem + ksteps * 4096;
+    for (int m = tid; m < 128; m += 128)
+        for (int k = 0; k < K; ++k) {
+            uint32_t off;
+            if (a_mn) {
+                const int s = k >> 5, kg = (k & 31) >> 3, r = k & 7, mg = m >> 4;
+                off = uint32_t(s * 4096 + mg * ms + kg * ks + r * 16 + (m & 15));
+            } else {
+                off = tc::kmajor_off_s8(m, k);
+            }
+            pa[off] = uint8_t(A[m * K + k]);
+        }
+    for (int n = tid; n < N; n += 128)
+        for (int k = 0; k < K; ++k) pb[tc::kmajor_off_s8(n, k)] = uint8_t(B[n * K + k]);
+    if (warp == 0) tc::tmem_alloc<256>(&tmem_slot);
+    if (tid == 0) {
+        tc::mbar_init(&mbar, 1);
+        tc::fence_barrier_init();
+    }
+    tc::fence_proxy_async();
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    if (tid == 0) {
+        const uint32_t idesc = tc::idesc_s8_s32(128, N, a_mn != 0, false);
+        for (int s = 0; s < ksteps; ++s) {
+            const uint64_t ad = a_mn ? tc::smem_desc_ls(tc::smem_u32(pa) + s * 4096, uint32_t(lbo), uint32_t(sbo))
+                                     : tc::smem_desc(tc::smem_u32(pa) + s * 4096);
+            const uint64_t bd = tc::smem_desc(tc::smem_u32(pb) + s * 4096);
+            tc::mma_s8(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
+        }
+        tc::mma_commit(&mbar);
+    }
+    tc::mbar_wait(&mbar, 0);
+    tc::tc_fence_after();
+    const int row = warp * 32 + (tid & 31);
+    for (int c0 = 0; c0 < N; c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(c0), v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) D[row * N + c0 + i] = __float_as_int(v[i]);
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<256>(tmem);
+}
+
 }  // namespace
+
+int tc_selftest_i8(const int8_t* dA, const int8_t* dB, int K, int N, int a_mn, int ms, int ks, int lbo, int sbo,
+                   int* dD, cudaStream_t st) {
+    const size_t smem = 2 * size_t(K / 32) * 4096;
+    cudaFuncSetAttribute(tc_selftest_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    tc_selftest_i8_kernel<<<1, 128, smem, st>>>(dA, dB, K, N, a_mn, ms, ks, lbo, sbo, dD);
+    return int(cudaGetLastError());
+}
 
 int tc_selftest(const float* dA, const float* dB, int K, int split, float* dD, cudaStream_t st) {
     const size_t smem = 6 * size_t(K / 16) * tc::kSliceBytes;

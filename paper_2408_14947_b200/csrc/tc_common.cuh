@@ -39,6 +39,18 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
     return d;
 }
 
+// General no-swizzle descriptor: lbo / sbo in bytes (multiples of 16).  For a K-major operand
+// LBO is the stride between the two 16-byte K halves of a core-matrix pair and SBO between 8-row
+// groups; for an MN-major operand LBO steps between 8-row K groups and SBO between 16-byte MN groups.
+__device__ __forceinline__ uint64_t smem_desc_ls(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFF);
+    d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+    d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+    d |= uint64_t(1) << 46;
+    return d;
+}
+
 // Instruction descriptor: kind::f16, A = B = BF16, D = F32, both K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
     return (1u << 4)                     // c_format F32
@@ -57,11 +69,13 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-// Instruction descriptor: kind::i8, A = B = signed int8, D = S32, both K-major.
-__host__ __device__ constexpr uint32_t idesc_s8_s32(int M, int N) {
+// Instruction descriptor: kind::i8, A = B = signed int8, D = S32; K-major unless a_mn / b_mn.
+__host__ __device__ constexpr uint32_t idesc_s8_s32(int M, int N, bool a_mn = false, bool b_mn = false) {
     return (2u << 4)                     // c_format S32
            | (1u << 7)                   // a_format signed 8-bit
            | (1u << 10)                  // b_format signed 8-bit
+           | (uint32_t(a_mn) << 15)      // a_major (1 = MN-major)
+           | (uint32_t(b_mn) << 16)      // b_major
            | (uint32_t(N >> 3) << 17)    // n_dim
            | (uint32_t(M >> 4) << 24);   // m_dim
 }

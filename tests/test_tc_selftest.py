@@ -29,3 +29,32 @@ def test_tcgen05_bf16_gemm(K):
         d = dd.cpu().numpy().astype(np.float64)
         err = np.abs(d - ref).max() / np.abs(ref).max()
         assert err < tol, (split, err)
+
+
+def _i8_gemm(pkg, eng, a, b, a_mn, ms=512, ks=128, lbo=128, sbo=512):
+    import torch
+
+    K, N = a.shape[1], b.shape[0]
+    da = torch.from_numpy(a).cuda()
+    db = torch.from_numpy(b).cuda()
+    dd = torch.zeros((128, N), dtype=torch.int32, device="cuda")
+    st = pkg.lib().erx_tc_selftest_i8(eng._h, C.c_void_p(da.data_ptr()), C.c_void_p(db.data_ptr()), K, N, a_mn, ms,
+                                      ks, lbo, sbo, C.c_void_p(dd.data_ptr()))
+    assert st == 0, pkg.lib().erx_last_error(eng._h)
+    return dd.cpu().numpy().astype(np.int64)
+
+
+@pytest.mark.parametrize("K,N", [(32, 112), (128, 112), (64, 128)])
+def test_tcgen05_i8_exact(K, N):
+    """kind::i8 MMAs accumulate exactly in s32, for K-major and MN-major A operands (the
+    MN-major layout is the score kernel's v-plane tile: 16-pixel groups 512 B apart, 8-dim groups
+    128 B apart; LBO steps along K, SBO along M)."""
+    import paper_2408_14947_b200 as pkg
+
+    rng = np.random.default_rng(K + N)
+    a = rng.integers(-128, 128, size=(128, K)).astype(np.int8)
+    b = rng.integers(-128, 128, size=(N, K)).astype(np.int8)
+    ref = a.astype(np.int64) @ b.astype(np.int64).T
+    eng = pkg.Engine(pkg.ErxConfig(no_srp=True), 8)
+    assert np.array_equal(_i8_gemm(pkg, eng, a, b, 0), ref)
+    assert np.array_equal(_i8_gemm(pkg, eng, a, b, 1), ref)

@@ -84,7 +84,7 @@ def digits_product(A, B, digits=3, drop_below=2):
     return out
 
 
-def score_quant(x, mu, L, c, vmax, R=4194000.0, drop_below=2):
+def score_quant(x, mu, L, c, vmax, R=4194000.0, drop_below=1):
     """k_score_i8 model: y = (x - c) - (mu - c) per-dim scaled, W' = L^-1 / s per-row scaled, digit MMAs."""
     W = np.linalg.inv(L).astype(np.float32)
     v = (x - c).astype(np.float32)
@@ -98,6 +98,24 @@ def score_quant(x, mu, L, c, vmax, R=4194000.0, drop_below=2):
     r = (R / np.abs(Wp).max(1)).astype(np.float32)
     Wq = np.rint(Wp * r[:, None]).astype(np.int64)
     M = digits_product(yq, Wq, 3, drop_below).astype(np.float64) / r[None, :].astype(np.float64)
+    return np.sqrt((M * M).sum(1))
+
+
+def score_quant_v(x, mu, L, c, vmax, R=4194000.0, drop_below=1):
+    """Score from the STATS' quantised v = x - c (per-dim scale R / vmax) and a per-line correction:
+    m = W y = W v - W (mu - c); W' = W / s_v per-row quantised; W (mu - c) in fp64."""
+    W = np.linalg.inv(L).astype(np.float32)
+    v = (x - c).astype(np.float32)
+    vm = vmax.copy()
+    vm[vm == 0] = 1
+    s = (np.float32(R) / vm.astype(np.float32)).astype(np.float32)
+    vq = np.rint(v.astype(np.float64) * s).astype(np.int64)
+    Wp = (W * (np.float32(1) / s)[None, :]).astype(np.float32)
+    r = (R / np.abs(Wp).max(1)).astype(np.float32)
+    Wq = np.rint(Wp.astype(np.float64) * r[:, None]).astype(np.int64)
+    Mv = (digits_product(vq, Wq, 3, drop_below).astype(np.float64) * (1.0 / r[None, :].astype(np.float64))).astype(np.float32)
+    corr = (W.astype(np.float64) @ (mu - c.astype(np.float64))).astype(np.float32)
+    M = (Mv - corr[None, :]).astype(np.float64)
     return np.sqrt((M * M).sum(1))
 
 
@@ -118,7 +136,7 @@ def erx(lines, alpha, stats, eps=1e-5, qscore=False):
         if qscore:
             c = x[:32].astype(np.float64).mean(0).astype(np.float32)
             vmax = np.abs((x - c).astype(np.float32)).max(0)
-            raws.append(score_quant(x, mu, L, c, vmax))
+            raws.append((score_quant_v if qscore == "v" else score_quant)(x, mu, L, c, vmax))
         else:
             y = np.linalg.solve(L, (x.astype(np.float64) - mu).T)
             raws.append(np.sqrt((y * y).sum(0)))
@@ -143,7 +161,8 @@ def main():
         "i8 3 digits R=4194000 (2^22), classes>=1": lambda a: stats_quant(a, 4194000.0, 1, 3),
         "i8 2 digits (R=32767), all": lambda a: stats_quant(a, 32639.0, 0, 2),
     }
-    variants["i8 stats + i8 score (classes>=2)"] = (lambda a: stats_quant(a, 4194000.0, 1, 3), True)
+    variants["i8 stats + i8 score (classes>=1)"] = (lambda a: stats_quant(a, 4194000.0, 1, 3), True)
+    variants["i8 stats + score from stats' v planes"] = (lambda a: stats_quant(a, 4194000.0, 1, 3), "v")
     for name, fn in variants.items():
         fn, q = fn if isinstance(fn, tuple) else (fn, False)
         r = erx(x, alpha, fn, qscore=q)
