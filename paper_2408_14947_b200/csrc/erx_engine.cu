@@ -72,6 +72,7 @@ struct erx_engine {
     bool small = false;       // D <= 16: stats_small / score_small path
     float* d_vcache = nullptr;  // [S*T][D][P] centred projections (small path)
     float* d_vmax = nullptr;    // [S*T][D] per-dim |x - c| range (tensor path)
+    unsigned char* d_vplanes = nullptr;  // [S*T][tiles][48 KB] quantised v digit planes (tensor path)
     int factor_req = 0;   // requested factor precision (0 auto, 32, 64)
     // ERX_OPT_STATS_TENSOR: 2 exact-integer tcgen05 stats + score where eligible (default), 1 tcgen05
     // bf16x3 stats (fp32 TMEM accumulation truncates, tools/tc_bias.py), 0 FFMA kernels.
@@ -207,6 +208,8 @@ void free_window(erx_engine* e) {
     e->d_vcache = nullptr;
     cudaFree(e->d_vmax);
     e->d_vmax = nullptr;
+    cudaFree(e->d_vplanes);
+    e->d_vplanes = nullptr;
     cudaFreeHost(e->h_lines);
     cudaFreeHost(e->h_status);
     e->d_lines = nullptr;
@@ -263,6 +266,7 @@ int configure(erx_engine* e, uint32_t P) {
     CU(cudaMalloc(&e->d_status, L * sizeof(int)));
     if (e->small) CU(cudaMalloc(&e->d_vcache, L * size_t(g.D) * P * sizeof(float)));
     if (erxk::stats_i8_eligible(g)) CU(cudaMalloc(&e->d_vmax, L * size_t(g.D) * sizeof(float)));
+    if (e->tensor) CU(cudaMalloc(&e->d_vplanes, L * erxk::vplanes_bytes_per_line(g)));
     return ERX_OK;
 }
 
@@ -329,6 +333,7 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     float* white = e->d_white + l0 * e->white_stride;
     float* vcache = e->d_vcache ? e->d_vcache + l0 * size_t(g.D) * g.P : nullptr;
     float* vmax = e->d_vmax ? e->d_vmax + l0 * size_t(g.D) : nullptr;
+    unsigned char* vplanes = e->d_vplanes ? e->d_vplanes + l0 * erxk::vplanes_bytes_per_line(g) : nullptr;
     const bool tensor = e->tensor;
     int* status = e->d_status + l0;
     float* rawg = raw + l0 * g.P;
@@ -337,7 +342,7 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
         if (e->small)
             erxk::launch_stats_small(g, e->smp, xg, int(n), int(in_stride), L, stats, vcache, e->stream);
         else if (tensor)
-            erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, vmax, e->stream);
+            erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, vmax, vplanes, e->stream);
         else if (e->stats_tensor == 1 && erxk::stats_tc_eligible(g))
             erxk::launch_stats_tc(g, xg, int(n), int(in_stride), L, stats, e->stream);
         else
@@ -358,8 +363,7 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     } else {
         timed(e, ERX_KERNEL_SCORE, [&] {
             if (tensor)
-                erxk::launch_score_i8(g, xg, int(n), int(in_stride), stats, vmax, prior,
-                                      reinterpret_cast<const unsigned char*>(white), L, rawg, e->stream);
+                erxk::launch_score_i8(g, vplanes, reinterpret_cast<const unsigned char*>(white), L, rawg, e->stream);
             else
                 erxk::launch_score(g, e->sc, xg, int(n), int(in_stride), prior, white, L, rawg, e->stream);
         });

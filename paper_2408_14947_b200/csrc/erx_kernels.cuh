@@ -94,15 +94,15 @@ void launch_stats_tc(const Geometry& g, const float* x, int n_per_stream, int in
 
 // Exact-integer tcgen05 stats kernel (k_stats_i8.cu): no_srp, 16 < D <= 127, B % 4 == 0.
 bool stats_i8_eligible(const Geometry& g);
-// vmax (may be null): [line][D] max_p |fl32(x - c)|, the y range the score kernel needs.
+// vmax / vplanes (may be null): [line][D] max_p |fl32(x - c)| and the score's v digit planes
+// (vplanes_bytes_per_line per line).
 void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
-                     double* stats, float* vmax, cudaStream_t st);
-// Exact-integer tcgen05 score kernel (k_score_i8.cu); needs the stats_i8 centre and vmax.
+                     double* stats, float* vmax, unsigned char* vplanes, cudaStream_t st);
+// Exact-integer tcgen05 score kernel (k_score_i8.cu): v planes from stats_i8, W planes from the factor.
 bool score_i8_eligible(const Geometry& g);
-// wplanes: the factor's int8 W planes (wplanes_bytes_per_line() per line).
 size_t wplanes_bytes_per_line();
-void launch_score_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, const double* stats,
-                     const float* vmax, const double* prior, const unsigned char* wplanes, int n_lines_total,
+size_t vplanes_bytes_per_line(const Geometry& g);
+void launch_score_i8(const Geometry& g, const unsigned char* vplanes, const unsigned char* wplanes, int n_lines_total,
                      float* raw, cudaStream_t st);
 
 // Host launchers.  All asynchronous on `st`.

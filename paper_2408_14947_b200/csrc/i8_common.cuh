@@ -15,10 +15,27 @@ namespace i8 {
 constexpr float kR = 4194000.f;      // quantisation range, < 2^22
 constexpr float kMagic = 12582912.f;  // 1.5 * 2^23
 
-// W planes as the score kernel's MMA B operand: 3 digit planes x 4 K-slices x 128 rows x 32 B,
-// then 128 fp32 row factors 256 / r_i.  One line's block is copied to shared memory as is.
+// W planes as the score kernel's MMA B operand (K-major): 3 digit planes x 4 K-slices x 128 rows
+// x 32 B, then 128 fp32 row factors 256 / r_i and 128 fp32 offsets (W (mu - c))_i.  One line's
+// block is copied to shared memory as is.
 constexpr uint32_t kWPlane = 4 * tc::kSliceBytes;  // 16 KB
-constexpr uint32_t kWBytes = 3 * kWPlane + 128 * 4;
+constexpr uint32_t kWAux = 2 * 128 * 4;
+constexpr uint32_t kWBytes = 3 * kWPlane + kWAux;
+
+// v planes as the score kernel's MMA A operand, MN-major (M = 128 pixels of a tile, K = 128 dims):
+// per digit plane, K-step s (32 dims) at s * 4096, 16-pixel group mg at mg * 512 (descriptor SBO),
+// 8-dim group kg at kg * 128 (LBO), dim row d % 8 at 16 B, pixel % 16 the byte.
+constexpr uint32_t kVPlane = 16384;
+constexpr uint32_t kTileBytes = 3 * kVPlane;  // one 128-pixel tile
+__host__ __device__ constexpr uint32_t vplane_off(int plane, int d, int p) {  // p: pixel within the tile (16-aligned)
+    return uint32_t(plane) * kVPlane + uint32_t(d >> 5) * 4096u + uint32_t(p >> 4) * 512u + uint32_t((d & 31) >> 3) * 128u +
+           uint32_t(d & 7) * 16u + uint32_t(p & 15);
+}
+
+// The stats kernel's per-dim v scale, recomputed bit-identically by the factor's plane writer.
+__device__ __forceinline__ float v_scale(float vmax) {
+    return (vmax > 0.f && vmax <= 3.402823466e38f) ? kR / vmax : 0.f;
+}
 
 __device__ __forceinline__ uint32_t quant_u(float v, float k) {  // q + 0x808080, q = rint(v k)
     return __float_as_uint(fmaf(v, k, kMagic)) + (0x808080u - 0x4B400000u);

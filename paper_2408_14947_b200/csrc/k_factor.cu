@@ -40,33 +40,45 @@ __device__ __forceinline__ void write_wblocks(float* __restrict__ whiten, int li
     }
 }
 
-// The tensor path's whitening operand (k_score_i8.cu), written instead of the fp32 blocks:
-// W'_ij = W_ij / s_j folds the score's per-dim y scale into W, each row i is scaled by
-// r_i = R / max_j |W'_ij| and rounded once to three int8 digit planes laid out exactly as the
-// score kernel's MMA B operand (i8::kWBytes per line, followed by 256 / r_i per row).
+// The tensor path's whitening operand (k_score_i8.cu), written instead of the fp32 blocks.  The
+// score multiplies the STATS' quantised v = x - c (per-dim scale s_j = i8::v_scale(vmax_j)), so
+//   m_i = sum_j W_ij (v_j - dc_j) = sum_j W'_ij (v_j s_j) - (W dc)_i,  W'_ij = W_ij / s_j,
+// dc = mu_{t-1} - c.  Each row of W' is scaled by r_i = R / max_j |W'_ij| and rounded once to three
+// int8 digit planes laid out as the score kernel's K-major MMA B operand; the block ends with
+// 256 / r_i and (W dc)_i (fp64 sum) per row (i8::kWBytes per line).
 __device__ void write_wplanes(unsigned char* __restrict__ planes, int line, const Geometry& g, const float* A, int LD,
                               const double* __restrict__ stats, const double* __restrict__ prior,
                               const float* __restrict__ vmax) {
     __shared__ float isc[128];
+    __shared__ double dcs[128];
     const int tid = threadIdx.x, nt = blockDim.x, D = g.D;
     for (int d = tid; d < 128; d += nt) {
         float v = 0.f;
+        double dc = 0.0;
         if (d < D) {
-            const i8::YScale ys = i8::y_scale(stats + size_t(line) * (g.SE + g.D), prior + size_t(line) * g.SE,
-                                              vmax + size_t(line) * D, d);
-            v = ys.s > 0.f ? 1.f / ys.s : 0.f;
+            const float s = i8::v_scale(vmax[size_t(line) * D + d]);
+            v = s > 0.f ? 1.f / s : 0.f;
+            dc = prior[size_t(line) * g.SE + d] - stats[size_t(line) * (g.SE + g.D) + d];
         }
         isc[d] = v;
+        dcs[d] = dc;
     }
     __syncthreads();
     unsigned char* out = planes + size_t(line) * i8::kWBytes;
     float* invr = reinterpret_cast<float*>(out + 3 * i8::kWPlane);
+    float* wdc = invr + 128;
     for (int i = tid; i < 128; i += nt) {
         float mx = 0.f;
+        double cr = 0.0;
         if (i < D)
-            for (int j = 0; j <= i; ++j) mx = fmaxf(mx, fabsf(A[i * LD + j] * isc[j]));
+            for (int j = 0; j <= i; ++j) {
+                const float w = A[i * LD + j];
+                mx = fmaxf(mx, fabsf(w * isc[j]));
+                cr += double(w) * dcs[j];
+            }
         const float r = (mx > 0.f && mx <= 3.402823466e38f) ? i8::kR / mx : 0.f;
         invr[i] = r > 0.f ? 256.f / r : 0.f;
+        wdc[i] = float(cr);
         for (int run = 0; run < 8; ++run) {
             uint32_t w[3][4];
 #pragma unroll

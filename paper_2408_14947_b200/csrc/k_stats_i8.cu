@@ -38,6 +38,7 @@
 // (M = 128 dims, N = roundup16(D + 1)) per chunk, committed to the plane
 // buffer's mbarrier; the epilogue stages S in its own shared-memory area.
 #include "erx_common.cuh"
+#include "i8_common.cuh"
 #include "tc_common.cuh"
 
 namespace erxk {
@@ -60,6 +61,7 @@ struct StatsI8Args {
     int n_lines;
     double* stats;
     float* vmax;  // [line][D] max_p |fl32(x - c)| (the score kernel's y range), may be null
+    unsigned char* vplanes;  // [line][tile][3][i8::kTileBytes / 3]: v digit planes for k_score_i8, may be null
     int N;       // MMA N = roundup16(D + 1)
     int stages;  // ring depth
 };
@@ -113,6 +115,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     const size_t tri_bytes = size_t(D) * (D + 1) / 2 * 8;
     double* S = reinterpret_cast<double*>(tri_bytes <= 2 * kOps ? smem : smem + 2 * kOps + size_t(NS) * kCh * B * 4);
     const int nch = (P + kCh - 1) / kCh;
+    const int ntile_v = (P + 127) / 128;  // score tiles per line (v planes)
     const int my_lines = blockIdx.x < a.n_lines ? (a.n_lines - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
     // Ring plan.  Chunk c of line k lives in slot slot(k, c % NS); pass 2 walks the chunks in
@@ -319,7 +322,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                     hi = fmaxf(hi, red_mx[w][d]);
                 }
                 const float m = fmaxf(hi - cd, cd - lo);
-                sd = (m > 0.f && m <= 3.402823466e38f) ? kR / m : 0.f;
+                sd = i8::v_scale(m);
                 if (a.vmax) a.vmax[size_t(blockIdx.x + k * gridDim.x) * D + d] = m;
             }
             cen_s[d] = cd;
@@ -384,6 +387,20 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                 mbar_arrive(&empty[st]);
                 mbar_arrive(&pfull[buf]);
             }
+            if (a.vplanes) {
+                // the same digits, as the score kernel's MN-major A operand (i8::vplane_off): one warp
+                // writes 2 x 512 contiguous bytes per plane
+                const int line = blockIdx.x + k * gridDim.x;
+                const int gp = c * kCh + pg2 * 16;
+                unsigned char* vt = a.vplanes + (size_t(line) * ntile_v + (gp >> 7)) * i8::kTileBytes;
+#pragma unroll
+                for (int pl = 0; pl < 3; ++pl) {
+                    *reinterpret_cast<uint4*>(vt + i8::vplane_off(pl, dd0, gp & 127)) =
+                        make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
+                    *reinterpret_cast<uint4*>(vt + i8::vplane_off(pl, dd1, gp & 127)) =
+                        make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
+                }
+            }
         }
     }
     if (my_lines > 0) epilogue(my_lines - 1);
@@ -415,7 +432,7 @@ bool stats_i8_eligible(const Geometry& g) {
 }
 
 void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
-                     double* stats, float* vmax, cudaStream_t st) {
+                     double* stats, float* vmax, unsigned char* vplanes, cudaStream_t st) {
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -423,7 +440,8 @@ void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(stats_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemCap - kStaticSmem));
     }
-    StatsI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, vmax, (g.D + 1 + 15) / 16 * 16, i8_stages(g)};
+    StatsI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, vmax, vplanes, (g.D + 1 + 15) / 16 * 16,
+                  i8_stages(g)};
     const int grid = n_lines_total < sms ? n_lines_total : sms;
     stats_i8_kernel<<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
 }
