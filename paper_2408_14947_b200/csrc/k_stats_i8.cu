@@ -29,14 +29,17 @@
 // Output slot per line: [c (D) | s = sum v (D) | S = sum v v^T packed lower],
 // fp64 — the k_stats.cu contract, finished by the scan kernel.
 //
-// Pipeline: a persistent CTA (256 threads, 512 TMEM columns) per SM walks
-// its lines; thread 0 streams 64-pixel chunks through a 2..4-deep
-// shared-memory ring with cp.async.bulk (mbarrier tx counts) as ONE sequence
-// across lines (pass 1 of line k+1 is already in flight while line k drains).
-// Pass-2 chunks are quantised into double-buffered digit planes (K-major,
-// 128 rows x 64 K per plane) and one thread issues 2 K-steps x 8 MMAs
-// (M = 128 dims, N = roundup16(D + 1)) per chunk, committed to the plane
-// buffer's mbarrier; the epilogue stages S in its own shared-memory area.
+// Pipeline: a persistent CTA (256 compute threads + a producer warp + an MMA
+// warp, 512 TMEM columns) per SM walks its lines.  Step k interleaves, chunk
+// by chunk, pass 1 of line k (HBM) with pass 2 of line k-1 (the same chunks
+// again, from L2), so the range pass streams under the quantise / MMA work of
+// the previous line.  Thread 0 of the producer warp issues 64-pixel
+// cp.async.bulk copies into a 5-deep ring (mbarrier tx counts); pass-2 chunks
+// are quantised into double-buffered digit planes (K-major, 128 rows x 64 K
+// per plane); the MMA warp issues 2 K-steps x 8 MMAs (M = 128 dims,
+// N = roundup16(D + 1)) per chunk; the epilogue stages S over the idle plane
+// buffers.  With the score kernel in use, pass 2 also writes its digits to
+// global memory as that kernel's MN-major A operand (i8_common.cuh).
 #include "erx_common.cuh"
 #include "i8_common.cuh"
 #include "tc_common.cuh"
@@ -118,24 +121,9 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     const int ntile_v = (P + 127) / 128;  // score tiles per line (v planes)
     const int my_lines = blockIdx.x < a.n_lines ? (a.n_lines - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
-    // Ring plan.  Chunk c of line k lives in slot slot(k, c % NS); pass 2 walks the chunks in
-    // DESCENDING order, so the last NS chunks of pass 1 are still resident (res0 = first resident
-    // chunk) and only chunks < res0 are loaded again.  The slot permutation alternates per line so
-    // the next line's first chunks land in the slots its predecessor frees first.  Every load into a
-    // slot has a per-slot sequence number: full[s] completes once per load, empty[s] once per release.
-    const int res0 = nch > NS ? nch - NS : 0;
-    auto cnt1 = [&](int r) { return r < nch ? (nch - 1 - r) / NS + 1 : 0; };
-    auto cnt2 = [&](int r) { return r < res0 ? (res0 - 1 - r) / NS + 1 : 0; };
-    auto slot = [&](int k, int r) { return (k & 1) ? NS - 1 - r : r; };
-    auto base = [&](int k, int sl) {
-        return ((k + 1) / 2) * (cnt1(sl) + cnt2(sl)) + (k / 2) * (cnt1(NS - 1 - sl) + cnt2(NS - 1 - sl));
-    };
-    auto idx1 = [&](int k, int c) { return base(k, slot(k, c % NS)) + c / NS; };
-    auto idx2 = [&](int k, int c) {
-        const int r = c % NS, m2 = r + ((res0 - 1 - r) / NS) * NS;
-        return base(k, slot(k, r)) + cnt1(r) + (m2 - c) / NS;
-    };
-
+    // Ring: chunk loads in one sequence, slot j % NS.  Step k interleaves pass 1 (range) of line k
+    // with pass 2 (quantise + MMA) of line k-1, chunk by chunk, so the HBM stream of one line runs
+    // under the tensor-core work of the previous one; pass-2 chunks are re-read from L2.
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
             tc::mbar_init(&full[s], 1);
@@ -156,22 +144,25 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     const uint32_t tmem = tmem_slot;
 
     if (warp == 8) {
-        // ---------------- producer: pass-1 chunks ascending, then the non-resident pass-2 chunks descending
+        // ---------------- producer: the interleaved chunk sequence of the compute warps
         if (lane == 0) {
-            auto load = [&](int k, int c, int idx) {
-                const int st = slot(k, c % NS);
-                if (idx >= 1) tc::mbar_wait(&empty[st], uint32_t(idx - 1) & 1u);
+            int j = 0;
+            auto load = [&](int k, int c) {
+                const int st = j % NS;
+                if (j >= NS) tc::mbar_wait(&empty[st], uint32_t(j / NS - 1) & 1u);
                 const int line = blockIdx.x + k * gridDim.x;
                 const int n = min(kCh, P - c * kCh);
                 const uint32_t bytes = uint32_t(n) * B * 4;
                 const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
                 tc::mbar_expect_tx(&full[st], bytes);
                 tc::bulk_g2s(ring + size_t(st) * kCh * B, xl + size_t(c) * kCh * B, bytes, &full[st]);
+                ++j;
             };
-            for (int k = 0; k < my_lines; ++k) {
-                for (int c = 0; c < nch; ++c) load(k, c, idx1(k, c));
-                for (int c = res0 - 1; c >= 0; --c) load(k, c, idx2(k, c));
-            }
+            for (int k = 0; k <= my_lines; ++k)
+                for (int c = 0; c < nch; ++c) {
+                    if (k < my_lines) load(k, c);
+                    if (k >= 1) load(k - 1, c);
+                }
         }
         return;
     }
@@ -255,52 +246,126 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     };
 
     float cdk[2] = {0.f, 0.f}, sdk[2] = {0.f, 0.f}, adk[2] = {kMagic, kMagic};
-    for (int k = 0; k < my_lines; ++k) {
-        // ---- pass 1: range of x per dim (min propagates NaN, max sees +inf); centre from the first 32 pixels
+    int j = 0;  // position in the chunk sequence (as the producer's)
+    for (int k = 0; k <= my_lines; ++k) {
+        const bool do1 = k < my_lines, do2 = k >= 1;
         float4 mn = make_float4(3.402823466e38f, 3.402823466e38f, 3.402823466e38f, 3.402823466e38f);
         float4 mx = make_float4(-3.402823466e38f, -3.402823466e38f, -3.402823466e38f, -3.402823466e38f);
         for (int c = 0; c < nch; ++c) {
-            const int st = slot(k, c % NS);
             const int n = min(kCh, P - c * kCh);
-            tc::mbar_wait(&full[st], uint32_t(idx1(k, c)) & 1u);
-            const float* sb = ring + size_t(st) * kCh * B;
-            if (quad_live) {
-                const int p0 = warp * 8;
-                const float* xp = sb + p0 * B + 4 * lane;
-                if (n >= p0 + 8) {
+            if (do1) {
+                // ---- pass 1 of line k: range of x per dim (min propagates NaN, max sees +inf); centre
+                const int st = j % NS;
+                tc::mbar_wait(&full[st], uint32_t(j / NS) & 1u);
+                ++j;
+                const float* sb = ring + size_t(st) * kCh * B;
+                if (quad_live) {
+                    const int p0 = warp * 8;
+                    const float* xp = sb + p0 * B + 4 * lane;
+                    if (n >= p0 + 8) {
 #pragma unroll
-                    for (int pp = 0; pp < 8; ++pp) {
-                        const float4 x = *reinterpret_cast<const float4*>(xp + pp * B);
-                        mn.x = fmin_nan(mn.x, x.x); mn.y = fmin_nan(mn.y, x.y);
-                        mn.z = fmin_nan(mn.z, x.z); mn.w = fmin_nan(mn.w, x.w);
-                        mx.x = fmaxf(mx.x, x.x); mx.y = fmaxf(mx.y, x.y); mx.z = fmaxf(mx.z, x.z); mx.w = fmaxf(mx.w, x.w);
+                        for (int pp = 0; pp < 8; ++pp) {
+                            const float4 x = *reinterpret_cast<const float4*>(xp + pp * B);
+                            mn.x = fmin_nan(mn.x, x.x); mn.y = fmin_nan(mn.y, x.y);
+                            mn.z = fmin_nan(mn.z, x.z); mn.w = fmin_nan(mn.w, x.w);
+                            mx.x = fmaxf(mx.x, x.x); mx.y = fmaxf(mx.y, x.y); mx.z = fmaxf(mx.z, x.z); mx.w = fmaxf(mx.w, x.w);
+                        }
+                    } else {
+                        for (int pp = 0; pp < n - p0; ++pp) {
+                            const float4 x = *reinterpret_cast<const float4*>(xp + pp * B);
+                            mn.x = fmin_nan(mn.x, x.x); mn.y = fmin_nan(mn.y, x.y);
+                            mn.z = fmin_nan(mn.z, x.z); mn.w = fmin_nan(mn.w, x.w);
+                            mx.x = fmaxf(mx.x, x.x); mx.y = fmaxf(mx.y, x.y); mx.z = fmaxf(mx.z, x.z); mx.w = fmaxf(mx.w, x.w);
+                        }
+                    }
+                    if (c == 0 && warp < 4) {
+                        double4 cs = make_double4(0.0, 0.0, 0.0, 0.0);
+                        for (int pp = 0; pp < min(8, n - p0); ++pp) {
+                            const float4 x = *reinterpret_cast<const float4*>(xp + pp * B);
+                            cs.x += double(x.x); cs.y += double(x.y); cs.z += double(x.z); cs.w += double(x.w);
+                        }
+                        red_cs[warp][4 * lane] = cs.x; red_cs[warp][4 * lane + 1] = cs.y;
+                        red_cs[warp][4 * lane + 2] = cs.z; red_cs[warp][4 * lane + 3] = cs.w;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
+            }
+            if (do2) {
+                // ---- pass 2 of line k-1: quantise the chunk into digit planes:
+                // y = fma(x - c, s, 1.5 * 2^23) rounds v * s to an integer in the low mantissa bits
+                // (|v s| <= 2^22), u = q + 0x808080 = bits(y) - 0x4B400000 + 0x808080
+                const int st = j % NS;
+                const int k2 = (k - 1) * nch + c, buf = k2 & 1;
+                tc::mbar_wait(&full[st], uint32_t(j / NS) & 1u);
+                ++j;
+                if (k2 >= 2) tc::mbar_wait(&pempty[buf], uint32_t((k2 - 2) >> 1) & 1u);
+                const float* sb = ring + size_t(st) * kCh * B + (pg2 * 16) * B;
+                unsigned char* op = ops + buf * kOps;
+                uint32_t w[2][3][4];
+                if (n == kCh) {
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        uint32_t u0[4], u1[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float* xp = sb + (jj * 4 + e) * B;
+                            u0[e] = __float_as_uint(fmaf(xp[ld0] - cdk[0], sdk[0], adk[0])) + (0x808080u - 0x4B400000u);
+                            u1[e] = __float_as_uint(fmaf(xp[ld1] - cdk[1], sdk[1], adk[1])) + (0x808080u - 0x4B400000u);
+                        }
+                        pack_digits(u0, w[0][0][jj], w[0][1][jj], w[0][2][jj]);
+                        pack_digits(u1, w[1][0][jj], w[1][1][jj], w[1][2][jj]);
                     }
                 } else {
-                    for (int pp = 0; pp < n - p0; ++pp) {
-                        const float4 x = *reinterpret_cast<const float4*>(xp + pp * B);
-                        mn.x = fmin_nan(mn.x, x.x); mn.y = fmin_nan(mn.y, x.y);
-                        mn.z = fmin_nan(mn.z, x.z); mn.w = fmin_nan(mn.w, x.w);
-                        mx.x = fmaxf(mx.x, x.x); mx.y = fmaxf(mx.y, x.y); mx.z = fmaxf(mx.z, x.z); mx.w = fmaxf(mx.w, x.w);
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        uint32_t u0[4], u1[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int p = pg2 * 16 + jj * 4 + e;
+                            const float* xp = sb + (jj * 4 + e) * B;
+                            u0[e] = __float_as_uint(fmaf(xp[ld0] - cdk[0], sdk[0], adk[0])) + (0x808080u - 0x4B400000u);
+                            u1[e] = __float_as_uint(fmaf(xp[ld1] - cdk[1], sdk[1], adk[1])) + (0x808080u - 0x4B400000u);
+                            if (p >= n) u0[e] = u1[e] = 0x808080u;
+                        }
+                        pack_digits(u0, w[0][0][jj], w[0][1][jj], w[0][2][jj]);
+                        pack_digits(u1, w[1][0][jj], w[1][1][jj], w[1][2][jj]);
                     }
                 }
-                if (c == 0 && warp < 4) {
-                    double4 cs = make_double4(0.0, 0.0, 0.0, 0.0);
-                    for (int pp = 0; pp < min(8, n - p0); ++pp) {
-                        const float4 x = *reinterpret_cast<const float4*>(xp + pp * B);
-                        cs.x += double(x.x); cs.y += double(x.y); cs.z += double(x.z); cs.w += double(x.w);
+                const uint32_t off0 = tc::kmajor_off_s8(dd0, pg2 * 16), off1 = tc::kmajor_off_s8(dd1, pg2 * 16);
+#pragma unroll
+                for (int pl = 0; pl < 3; ++pl) {
+                    *reinterpret_cast<uint4*>(op + pl * kPlane + off0) = make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
+                    *reinterpret_cast<uint4*>(op + pl * kPlane + off1) = make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
+                }
+                tc::fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&empty[st]);
+                    mbar_arrive(&pfull[buf]);
+                }
+                if (a.vplanes) {
+                    // the same digits, as the score kernel's MN-major A operand (i8::vplane_off): one warp
+                    // writes 2 x 512 contiguous bytes per plane
+                    const int line = blockIdx.x + (k - 1) * gridDim.x;
+                    const int gp = c * kCh + pg2 * 16;
+                    unsigned char* vt = a.vplanes + (size_t(line) * ntile_v + (gp >> 7)) * i8::kTileBytes;
+#pragma unroll
+                    for (int pl = 0; pl < 3; ++pl) {
+                        *reinterpret_cast<uint4*>(vt + i8::vplane_off(pl, dd0, gp & 127)) =
+                            make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
+                        *reinterpret_cast<uint4*>(vt + i8::vplane_off(pl, dd1, gp & 127)) =
+                            make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
                     }
-                    red_cs[warp][4 * lane] = cs.x; red_cs[warp][4 * lane + 1] = cs.y;
-                    red_cs[warp][4 * lane + 2] = cs.z; red_cs[warp][4 * lane + 3] = cs.w;
                 }
             }
-            __syncwarp();
-            if (lane == 0 && c < res0) mbar_arrive(&empty[st]);  // resident chunks stay for pass 2
         }
+        // ---- line k-1 is complete: its epilogue (reads bad_s / cen_s / inv_s of line k-1)
+        if (do2) epilogue(k - 1);
+        if (!do1) break;
+        // ---- ranges of all pixel groups -> centre and per-dim scale of line k
         const bool bad_mine = quad_live && !(isfinite(mn.x) && isfinite(mn.y) && isfinite(mn.z) && isfinite(mn.w) &&
                                              isfinite(mx.x) && isfinite(mx.y) && isfinite(mx.z) && isfinite(mx.w));
-        // ---- the previous line's epilogue (its MMAs finished while this pass ran)
-        if (k > 0) epilogue(k - 1);
-        // ---- ranges of all pixel groups -> centre and per-dim scale of this line
         if (quad_live) {
             *reinterpret_cast<float4*>(&red_mn[warp][4 * lane]) = mn;
             *reinterpret_cast<float4*>(&red_mx[warp][4 * lane]) = mx;
@@ -333,77 +398,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
         bar_compute();
         cdk[0] = cen_s[dd0 & 127]; sdk[0] = scale_s[dd0 & 127]; adk[0] = add_s[dd0 & 127];
         cdk[1] = cen_s[dd1 & 127]; sdk[1] = scale_s[dd1 & 127]; adk[1] = add_s[dd1 & 127];
-        // ---- pass 2: quantise each chunk into digit planes:
-        // y = fma(x - c, s, 1.5 * 2^23) rounds v * s to an integer in the low mantissa bits
-        // (|v s| <= 2^22), u = q + 0x808080 = bits(y) - 0x4B400000 + 0x808080
-        for (int cc = 0; cc < nch; ++cc) {
-            const int c = nch - 1 - cc;
-            const int st = slot(k, c % NS);
-            const int k2 = k * nch + cc, buf = k2 & 1;
-            const int n = min(kCh, P - c * kCh);
-            if (c < res0) tc::mbar_wait(&full[st], uint32_t(idx2(k, c)) & 1u);
-            if (k2 >= 2) tc::mbar_wait(&pempty[buf], uint32_t((k2 - 2) >> 1) & 1u);
-            const float* sb = ring + size_t(st) * kCh * B + (pg2 * 16) * B;
-            unsigned char* op = ops + buf * kOps;
-            uint32_t w[2][3][4];
-            if (n == kCh) {
-#pragma unroll
-                for (int jj = 0; jj < 4; ++jj) {
-                    uint32_t u0[4], u1[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float* xp = sb + (jj * 4 + e) * B;
-                        u0[e] = __float_as_uint(fmaf(xp[ld0] - cdk[0], sdk[0], adk[0])) + (0x808080u - 0x4B400000u);
-                        u1[e] = __float_as_uint(fmaf(xp[ld1] - cdk[1], sdk[1], adk[1])) + (0x808080u - 0x4B400000u);
-                    }
-                    pack_digits(u0, w[0][0][jj], w[0][1][jj], w[0][2][jj]);
-                    pack_digits(u1, w[1][0][jj], w[1][1][jj], w[1][2][jj]);
-                }
-            } else {
-#pragma unroll
-                for (int jj = 0; jj < 4; ++jj) {
-                    uint32_t u0[4], u1[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int p = pg2 * 16 + jj * 4 + e;
-                        const float* xp = sb + (jj * 4 + e) * B;
-                        u0[e] = __float_as_uint(fmaf(xp[ld0] - cdk[0], sdk[0], adk[0])) + (0x808080u - 0x4B400000u);
-                        u1[e] = __float_as_uint(fmaf(xp[ld1] - cdk[1], sdk[1], adk[1])) + (0x808080u - 0x4B400000u);
-                        if (p >= n) u0[e] = u1[e] = 0x808080u;
-                    }
-                    pack_digits(u0, w[0][0][jj], w[0][1][jj], w[0][2][jj]);
-                    pack_digits(u1, w[1][0][jj], w[1][1][jj], w[1][2][jj]);
-                }
-            }
-            const uint32_t off0 = tc::kmajor_off_s8(dd0, pg2 * 16), off1 = tc::kmajor_off_s8(dd1, pg2 * 16);
-#pragma unroll
-            for (int pl = 0; pl < 3; ++pl) {
-                *reinterpret_cast<uint4*>(op + pl * kPlane + off0) = make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
-                *reinterpret_cast<uint4*>(op + pl * kPlane + off1) = make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
-            }
-            tc::fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&empty[st]);
-                mbar_arrive(&pfull[buf]);
-            }
-            if (a.vplanes) {
-                // the same digits, as the score kernel's MN-major A operand (i8::vplane_off): one warp
-                // writes 2 x 512 contiguous bytes per plane
-                const int line = blockIdx.x + k * gridDim.x;
-                const int gp = c * kCh + pg2 * 16;
-                unsigned char* vt = a.vplanes + (size_t(line) * ntile_v + (gp >> 7)) * i8::kTileBytes;
-#pragma unroll
-                for (int pl = 0; pl < 3; ++pl) {
-                    *reinterpret_cast<uint4*>(vt + i8::vplane_off(pl, dd0, gp & 127)) =
-                        make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
-                    *reinterpret_cast<uint4*>(vt + i8::vplane_off(pl, dd1, gp & 127)) =
-                        make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
-                }
-            }
-        }
     }
-    if (my_lines > 0) epilogue(my_lines - 1);
     if (warp == 0) tc::tmem_free<512>(tmem);
 }
 
