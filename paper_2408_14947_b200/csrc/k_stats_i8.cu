@@ -223,8 +223,12 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
 #pragma unroll
                 for (int ii = 0; ii < 16; ++ii) {
                     const int e = gi * 16 + ii;
-                    const double si = double(int(v[0][ii])) * 256.0 + double(int(v[1][ii])) * 65536.0 +
-                                      double(int(v[2][ii])) * 16777216.0 + double(int(v[3][ii])) * 4294967296.0;
+                    // S_int = 2^8 a1 + 2^16 a2 + 2^24 a3 + 2^32 a4, exact in int64, one conversion
+                    const long long si_i = (static_cast<long long>(int(v[3][ii])) << 32) +
+                                           (static_cast<long long>(int(v[2][ii])) << 24) +
+                                           (static_cast<long long>(int(v[1][ii])) << 16) +
+                                           (static_cast<long long>(int(v[0][ii])) << 8);
+                    const double si = double(si_i);
                     if (e <= row) S[tri(row, e)] = si * ia * inv_s[e];
                     if (e == D) sum_s[row] = si * (1.0 / 256.0) * ia;
                 }
