@@ -147,7 +147,9 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
         // ---------------- producer: the interleaved chunk sequence of the compute warps
         if (lane == 0) {
             int j = 0;
-            auto load = [&](int k, int c) {
+            // pass-1 chunks are read again one line later (pass 2): keep them in L2
+            const uint64_t keep = tc::policy_evict_last(), drop = tc::policy_evict_first();
+            auto load = [&](int k, int c, bool again) {
                 const int st = j % NS;
                 if (j >= NS) tc::mbar_wait(&empty[st], uint32_t(j / NS - 1) & 1u);
                 const int line = blockIdx.x + k * gridDim.x;
@@ -155,13 +157,14 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                 const uint32_t bytes = uint32_t(n) * B * 4;
                 const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
                 tc::mbar_expect_tx(&full[st], bytes);
-                tc::bulk_g2s(ring + size_t(st) * kCh * B, xl + size_t(c) * kCh * B, bytes, &full[st]);
+                tc::bulk_g2s_hint(ring + size_t(st) * kCh * B, xl + size_t(c) * kCh * B, bytes, &full[st],
+                                  again ? keep : drop);
                 ++j;
             };
             for (int k = 0; k <= my_lines; ++k)
                 for (int c = 0; c < nch; ++c) {
-                    if (k < my_lines) load(k, c);
-                    if (k >= 1) load(k - 1, c);
+                    if (k < my_lines) load(k, c, true);
+                    if (k >= 1) load(k - 1, c, false);
                 }
         }
         return;
@@ -354,12 +357,13 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                     const int line = blockIdx.x + (k - 1) * gridDim.x;
                     const int gp = c * kCh + pg2 * 16;
                     unsigned char* vt = a.vplanes + (size_t(line) * ntile_v + (gp >> 7)) * i8::kTileBytes;
+                    const uint64_t stream_out = tc::policy_evict_first();  // do not push x out of L2
 #pragma unroll
                     for (int pl = 0; pl < 3; ++pl) {
-                        *reinterpret_cast<uint4*>(vt + i8::vplane_off(pl, dd0, gp & 127)) =
-                            make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
-                        *reinterpret_cast<uint4*>(vt + i8::vplane_off(pl, dd1, gp & 127)) =
-                            make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
+                        tc::st16_hint(vt + i8::vplane_off(pl, dd0, gp & 127),
+                                      make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]), stream_out);
+                        tc::st16_hint(vt + i8::vplane_off(pl, dd1, gp & 127),
+                                      make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]), stream_out);
                     }
                 }
             }
