@@ -69,25 +69,37 @@ __device__ void write_wplanes(unsigned char* __restrict__ planes, int line, cons
     float* wdc = invr + 128;
     for (int i = tid; i < 128; i += nt) {
         float mx = 0.f;
-        double cr = 0.0;
-        if (i < D)
-            for (int j = 0; j <= i; ++j) {
-                const float w = A[i * LD + j];
-                mx = fmaxf(mx, fabsf(w * isc[j]));
-                cr += double(w) * dcs[j];
+        double cr[4] = {0.0, 0.0, 0.0, 0.0};  // four partial sums: no 108-long dependent DFMA chain
+        if (i < D) {
+            const float* Ai = A + i * LD;  // rows are 16-byte aligned (LD = Dp + 4)
+            for (int j0 = 0; j0 <= i; j0 += 4) {
+                const float4 w4 = *reinterpret_cast<const float4*>(Ai + j0);
+                const float w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int j = j0 + e;
+                    const float wv = j <= i ? w[e] : 0.f;
+                    mx = fmaxf(mx, fabsf(wv * isc[j]));
+                    cr[e] += double(wv) * dcs[j];
+                }
             }
+        }
         const float r = (mx > 0.f && mx <= 3.402823466e38f) ? i8::kR / mx : 0.f;
         invr[i] = r > 0.f ? 256.f / r : 0.f;
-        wdc[i] = float(cr);
+        wdc[i] = float((cr[0] + cr[1]) + (cr[2] + cr[3]));
         for (int run = 0; run < 8; ++run) {
             uint32_t w[3][4];
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
+                const int j0 = run * 16 + q4 * 4;
+                float4 w4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (i < D && j0 <= i) w4 = *reinterpret_cast<const float4*>(A + i * LD + j0);
+                const float wr[4] = {w4.x, w4.y, w4.z, w4.w};
                 uint32_t u[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const int j = run * 16 + q4 * 4 + e;
-                    const float wv = (i < D && j <= i) ? A[i * LD + j] * isc[j] : 0.f;
+                    const int j = j0 + e;
+                    const float wv = (i < D && j <= i) ? wr[e] * isc[j] : 0.f;
                     u[e] = i8::quant_u(wv, r);
                 }
                 i8::pack_digits(u, w[0][q4], w[1][q4], w[2][q4]);
@@ -395,18 +407,18 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
     int fail;
     const int ntri = D * (D + 1) / 2;
     while (true) {
-        // fill: coalesced reads of the packed fp64 K, 8 loads in flight per thread (the (i, j) of
+        // fill: coalesced reads of the packed fp64 K, 16 loads in flight per thread (the (i, j) of
         // idx + nt follows from (i, j) of idx incrementally), padding = identity
         {
             int i = int((sqrtf(8.f * tid + 1.f) - 1.f) * 0.5f), j;
             while (i * (i + 1) / 2 > tid) --i;
             while ((i + 1) * (i + 2) / 2 <= tid) ++i;
             j = tid - i * (i + 1) / 2;
-            for (int base = tid; base < ntri; base += 8 * nt) {
-                double v[8];
-                int ii[8], jj[8];
+            for (int base = tid; base < ntri; base += 16 * nt) {
+                double v[16];
+                int ii[16], jj[16];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < 16; ++u) {
                     const int idx = base + u * nt;
                     v[u] = idx < ntri ? __ldg(K + idx) : 0.0;
                     ii[u] = i;
@@ -418,7 +430,7 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
+                for (int u = 0; u < 16; ++u)
                     if (base + u * nt < ntri) A[ii[u] * LD + jj[u]] = float(v[u] + (ii[u] == jj[u] ? eps : 0.0));
             }
         }
