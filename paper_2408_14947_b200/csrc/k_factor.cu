@@ -46,7 +46,8 @@ __device__ __forceinline__ void write_wblocks(float* __restrict__ whiten, int li
 // dc = mu_{t-1} - c.  Each row of W' is scaled by r_i = R / max_j |W'_ij| and rounded once to three
 // int8 digit planes laid out as the score kernel's K-major MMA B operand; the block ends with
 // 256 / r_i and (W dc)_i (fp64 sum) per row (i8::kWBytes per line).
-__device__ void write_wplanes(unsigned char* __restrict__ planes, int line, const Geometry& g, const float* A, int LD,
+template <typename ElPtr>
+__device__ void write_wplanes(unsigned char* __restrict__ planes, int line, const Geometry& g, ElPtr el,
                               const double* __restrict__ stats, const double* __restrict__ prior,
                               const float* __restrict__ vmax) {
     __shared__ float isc[128];
@@ -71,9 +72,8 @@ __device__ void write_wplanes(unsigned char* __restrict__ planes, int line, cons
         float mx = 0.f;
         double cr[4] = {0.0, 0.0, 0.0, 0.0};  // four partial sums: no 108-long dependent DFMA chain
         if (i < D) {
-            const float* Ai = A + i * LD;  // rows are 16-byte aligned (LD = Dp + 4)
-            for (int j0 = 0; j0 <= i; j0 += 4) {
-                const float4 w4 = *reinterpret_cast<const float4*>(Ai + j0);
+            for (int j0 = 0; j0 <= i; j0 += 4) {  // 4 consecutive j of one block row: 16-byte aligned
+                const float4 w4 = *reinterpret_cast<const float4*>(el(i, j0));
                 const float w[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
@@ -93,7 +93,7 @@ __device__ void write_wplanes(unsigned char* __restrict__ planes, int line, cons
             for (int q4 = 0; q4 < 4; ++q4) {
                 const int j0 = run * 16 + q4 * 4;
                 float4 w4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (i < D && j0 <= i) w4 = *reinterpret_cast<const float4*>(A + i * LD + j0);
+                if (i < D && j0 <= i) w4 = *reinterpret_cast<const float4*>(el(i, j0));
                 const float wr[4] = {w4.x, w4.y, w4.z, w4.w};
                 uint32_t u[4];
 #pragma unroll
@@ -389,16 +389,20 @@ __device__ __forceinline__ void st8(float* p, const float* v) {
     *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
 }
 
-__global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const double* __restrict__ prior, double eps0,
+__global__ void __launch_bounds__(64) factor_blk_kernel(Geometry g, const double* __restrict__ prior, double eps0,
                                                          float* __restrict__ whiten, int* __restrict__ status,
                                                          int* __restrict__ latch, int line_base,
                                                          const double* __restrict__ stats,
                                                          const float* __restrict__ vmax) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_fail;
-    const int D = g.D, Dp = g.Dp, nb = g.nb, LD = Dp + 4;
-    float* A = reinterpret_cast<float*>(smem);  // [Dp][LD]; padding dims carry an identity block
-    float* Lc = A + size_t(Dp) * LD;            // [nb][64]: copy of a block column (inverse)
+    const int D = g.D, Dp = g.Dp, nb = g.nb;
+    // packed lower 8x8 blocks, row-major inside a block: block (I, J) at tri(I, J) * 64, row r at r * 8;
+    // padding dims carry an identity block
+    float* A = reinterpret_cast<float*>(smem);
+    auto BP = [&](int I, int J) { return A + (I * (I + 1) / 2 + J) * 64; };
+    auto EL = [&](int i, int j) { return BP(i >> 3, j >> 3) + (i & 7) * kBlk + (j & 7); };
+    float* Lc = A + size_t(nb * (nb + 1) / 2) * 64;  // [nb][64]: copy of a block column (inverse)
     float* Dinv = Lc + size_t(nb) * 64;         // [64]: inverse of a diagonal block
     const int line = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
     const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
@@ -431,21 +435,21 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
                 }
 #pragma unroll
                 for (int u = 0; u < 16; ++u)
-                    if (base + u * nt < ntri) A[ii[u] * LD + jj[u]] = float(v[u] + (ii[u] == jj[u] ? eps : 0.0));
+                    if (base + u * nt < ntri) *EL(ii[u], jj[u]) = float(v[u] + (ii[u] == jj[u] ? eps : 0.0));
             }
         }
         for (int i = D + tid; i < Dp; i += nt)
-            for (int j = 0; j <= i; ++j) A[i * LD + j] = (i == j) ? 1.f : 0.f;
+            for (int j = 0; j <= i; ++j) *EL(i, j) = (i == j) ? 1.f : 0.f;
         __syncthreads();
         fail = -1;
         for (int k = 0; k < nb; ++k) {
             const int k0 = k * kBlk;
-            float* Bk = A + k0 * LD + k0;
+            float* Bk = BP(k, k);
             // (a) every thread factors the 8x8 diagonal block in registers (redundant, no barrier;
             //     the pivot test is uniform across the CTA)
             float L[kBlk][kBlk], rd[kBlk];
 #pragma unroll
-            for (int r = 0; r < kBlk; ++r) ld8(Bk + r * LD, L[r]);
+            for (int r = 0; r < kBlk; ++r) ld8(Bk + r * kBlk, L[r]);
 #pragma unroll
             for (int j = 0; j < kBlk; ++j) {
                 float d = L[j][j];
@@ -466,7 +470,7 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
             if (fail >= 0) break;
             // (b) panel: L_Ik = A_Ik L_kk^{-T}, one row per thread, L_kk from registers
             for (int i = k0 + kBlk + tid; i < Dp; i += nt) {
-                float* row = A + i * LD + k0;
+                float* row = BP(i >> 3, k) + (i & 7) * kBlk;
                 float a[kBlk], x[kBlk];
                 ld8(row, a);
 #pragma unroll
@@ -483,7 +487,7 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
                 for (int r = 0; r < kBlk; ++r)
                     if (lane == r) {
 #pragma unroll
-                        for (int c = 0; c <= r; ++c) Bk[r * LD + c] = L[r][c];
+                        for (int c = 0; c <= r; ++c) Bk[r * kBlk + c] = L[r][c];
                     }
             }
             __syncthreads();
@@ -498,16 +502,16 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
                 while ((Ir + 1) * (Ir + 2) / 2 <= pq) ++Ir;
                 const int I = k + 1 + Ir, J = k + 1 + (pq - Ir * (Ir + 1) / 2);
                 float a[kBlk], acc[kBlk];
-                ld8(A + (I * kBlk + r) * LD + k0, a);
-                ld8(A + (I * kBlk + r) * LD + J * kBlk, acc);
+                ld8(BP(I, k) + r * kBlk, a);
+                ld8(BP(I, J) + r * kBlk, acc);
 #pragma unroll
                 for (int c = 0; c < kBlk; ++c) {
                     float b[kBlk];
-                    ld8(A + (J * kBlk + c) * LD + k0, b);  // broadcast: the 8 threads of a pair share it
+                    ld8(BP(J, k) + c * kBlk, b);  // broadcast: the 8 threads of a pair share it
 #pragma unroll
                     for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], b[l], acc[c]);
                 }
-                st8(A + (I * kBlk + r) * LD + J * kBlk, acc);
+                st8(BP(I, J) + r * kBlk, acc);
             }
             __syncthreads();
         }
@@ -531,11 +535,11 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
     // J < k, holds T_IJ = -sum_{m<k} L_Im X_mJ; block (I, J >= k) still holds L.
     for (int k = 0; k < nb; ++k) {
         const int k0 = k * kBlk;
-        const float* Bk = A + k0 * LD + k0;
+        const float* Bk = BP(k, k);
         // block column k below the diagonal is overwritten by this step's update: keep a copy
         for (int idx = tid; idx < (nb - k - 1) * 64; idx += nt) {
             const int I = k + 1 + idx / 64, rc = idx % 64;
-            Lc[I * 64 + rc] = A[(I * kBlk + rc / kBlk) * LD + k0 + rc % kBlk];
+            Lc[I * 64 + rc] = BP(I, k)[rc];
         }
         // finalise block row k: X_kJ = L_kk^{-1} T_kJ (J < k), X_kk = L_kk^{-1}; the 8x8 inverse
         // is recomputed in registers by each finalising thread (no serial phase, no barrier)
@@ -543,7 +547,7 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
             float Lr[kBlk][kBlk], Di[kBlk][kBlk], rl[kBlk];
 #pragma unroll
             for (int r = 0; r < kBlk; ++r) {
-                ld8(Bk + r * LD, Lr[r]);
+                ld8(Bk + r * kBlk, Lr[r]);
                 rl[r] = 1.f / Lr[r][r];
             }
 #pragma unroll
@@ -573,7 +577,7 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
 #pragma unroll
                 for (int l = 0; l < kBlk; ++l) {
                     float srow[kBlk];
-                    ld8(A + (k0 + l) * LD + J * kBlk, srow);
+                    ld8(BP(k, J) + l * kBlk, srow);
 #pragma unroll
                     for (int r = l; r < kBlk; ++r)
 #pragma unroll
@@ -581,8 +585,8 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
                 }
             }
             // X_kk goes to scratch: other finalising threads are still reading L_kk
-            float* dst = (J == k) ? Dinv : A + k0 * LD + J * kBlk;
-            const int ld = (J == k) ? kBlk : LD;
+            float* dst = (J == k) ? Dinv : BP(k, J);
+            const int ld = kBlk;
 #pragma unroll
             for (int r = 0; r < kBlk; ++r) st8(dst + r * ld, t[r]);
         }
@@ -591,22 +595,22 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
             for (int r = 0; r < kBlk; ++r) {
                 float row[kBlk];
                 ld8(Dinv + r * kBlk, row);
-                st8(A + (k0 + r) * LD + k0, row);
+                st8(BP(k, k) + r * kBlk, row);
             }
         // update block rows I > k: T_IJ -= L_Ik X_kJ (J < k), T_Ik = -L_Ik X_kk; task = block x row
         const int ntask = (nb - k - 1) * (k + 1) * kBlk;
         for (int q = tid; q < ntask; q += nt) {
             const int tq = q >> 3, r = q & 7;
             const int I = k + 1 + tq / (k + 1), J = tq % (k + 1);
-            const float* xs = (J == k) ? Dinv : A + k0 * LD + J * kBlk;
-            const int xld = (J == k) ? kBlk : LD;
+            const float* xs = (J == k) ? Dinv : BP(k, J);
+            const int xld = kBlk;
             float a[kBlk], acc[kBlk];
             ld8(Lc + I * 64 + r * kBlk, a);
             if (J == k) {
 #pragma unroll
                 for (int c = 0; c < kBlk; ++c) acc[c] = 0.f;
             } else {
-                ld8(A + (I * kBlk + r) * LD + J * kBlk, acc);
+                ld8(BP(I, J) + r * kBlk, acc);
             }
 #pragma unroll
             for (int l = 0; l < kBlk; ++l) {
@@ -615,14 +619,15 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
 #pragma unroll
                 for (int c = 0; c < kBlk; ++c) acc[c] = fmaf(-a[l], xr[c], acc[c]);
             }
-            st8(A + (I * kBlk + r) * LD + J * kBlk, acc);
+            st8(BP(I, J) + r * kBlk, acc);
         }
         __syncthreads();
     }
     if (vmax) {
-        write_wplanes(reinterpret_cast<unsigned char*>(whiten), line, g, A, LD, stats, prior, vmax);
+        write_wplanes(reinterpret_cast<unsigned char*>(whiten), line, g, [&](int i, int j) { return EL(i, j); }, stats,
+                      prior, vmax);
     } else {
-        write_wblocks(whiten, line, g, [&](int i, int j) { return A[i * LD + j]; });
+        write_wblocks(whiten, line, g, [&](int i, int j) { return *EL(i, j); });
     }
     if (tid == 0) status[line] = -1;
 }
@@ -630,7 +635,7 @@ __global__ void __launch_bounds__(128) factor_blk_kernel(Geometry g, const doubl
 }  // namespace
 
 size_t factor_blk_smem(const Geometry& g) {
-    return size_t(g.Dp) * (g.Dp + 4) * 4 + size_t(g.nb) * 64 * 4 + 64 * 4;
+    return (size_t(g.nb) * (g.nb + 1) / 2 + g.nb + 1) * 64 * 4;  // packed blocks + Lc + Dinv
 }
 
 size_t factor_smem(const Geometry& g, int precision) {
@@ -657,7 +662,7 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
     const size_t sm = factor_smem(g, precision);
     if (precision == 32) {
         cudaFuncSetAttribute(factor_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        factor_blk_kernel<<<n_lines_total, 128, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
+        factor_blk_kernel<<<n_lines_total, 64, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
                                                           vmax);
     } else if (precision == 64) {
         cudaFuncSetAttribute(factor_smem_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
