@@ -687,7 +687,7 @@ int erx_pop(erx_engine* e, uint32_t max_lines, int64_t* index, uint8_t* warmup, 
     };
     const size_t elems = size_t(e->S) * n * P;
     const uint32_t hw = std::max(1u, std::thread::hardware_concurrency());
-    const uint32_t nt = std::min<uint32_t>({e->S, 8u, hw, uint32_t(elems >> 18) + 1});
+    const uint32_t nt = std::min<uint32_t>({e->S, 16u, hw, uint32_t(elems >> 17) + 1});
     if (nt <= 1) {
         widen(0, e->S);
     } else {
