@@ -17,9 +17,9 @@
 // accumulators to delta.  Emulated raw-score error vs fp64 on configs[3]:
 // max 3.3e-6 / median 4.4e-7 (tools/emulate_i8.py, "score from stats' v planes").
 //
-// Warp roles (persistent CTA per SM, whole lines): warps 0-7 epilogue
-// (TMEM -> m_i -> delta), warp 8 producer (bulk copies: per line the W block
-// into a double buffer, per tile the v planes into a 2-deep ring), warp 9
+// Warp roles (persistent CTA per SM, whole lines): warps 0-15 epilogue
+// (TMEM -> m_i -> delta), warp 16 producer (bulk copies: per line the W block
+// into a double buffer, per tile the v planes into a 2-deep ring), warp 17
 // MMA issuer.  All hand-offs are mbarriers.
 #include "erx_common.cuh"
 #include "i8_common.cuh"
@@ -29,7 +29,8 @@ namespace {
 
 constexpr int kTile = 128;                          // pixels per tile (MMA M)
 constexpr int kKSteps = 4;                          // K = 128 dims
-constexpr int kThreads = 256;                       // epilogue threads
+constexpr int kThreads = 512;                       // epilogue threads (16 warps)
+constexpr int kEW = kThreads / 32;
 constexpr int kStages = 2;                          // v-plane tile ring
 static_assert(i8::kVPlane == kKSteps * tc::kSliceBytes, "v plane layout");
 
@@ -52,7 +53,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
     __shared__ uint32_t tmem_slot;
     __shared__ __align__(8) uint64_t wfull[2], wempty[2], tfull[kStages], tempty[kStages], accfull, accempty;
     __shared__ __align__(16) float aux_s[2][2 * 128];  // per line parity: 256 / r_i, then (W (mu - c))_i
-    __shared__ float red_s[2][128];
+    __shared__ float red_s[2][3][128];
 
     const Geometry& g = a.g;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
     tc::tc_fence_after();
     const uint32_t tmem = tmem_slot;
 
-    if (warp == 8) {
+    if (warp == kEW) {
         // ---------------- producer: W block of line k (double-buffered), then its tiles
         if (lane == 0) {
             int j = 0;
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
         }
         return;
     }
-    if (warp == 9) {
+    if (warp == kEW + 1) {
         // ---------------- MMA issuer
         if (lane == 0) {
             const uint32_t idesc = tc::idesc_s8_s32(128, a.N, /*a_mn=*/true, /*b_mn=*/false);
@@ -140,12 +141,12 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
         return;
     }
 
-    // ---------------- epilogue warps 0-7: thread = (pixel row of the tile, column half)
+    // ---------------- epilogue warps 0-15: thread = (pixel row of the tile, column quarter)
     const int row = (warp & 3) * 32 + lane;
     const uint32_t taddr = tmem + (uint32_t((warp & 3) * 32) << 16);
-    const int colh = warp >> 2;
+    const int colq = warp >> 2;
     const int ngrp = a.N / 16;
-    const int g0 = colh ? (ngrp + 1) / 2 : 0, g1 = colh ? ngrp : (ngrp + 1) / 2;
+    const int g0 = colq * ngrp / 4, g1 = (colq + 1) * ngrp / 4;
     int j = 0;
     for (int k = 0; k < my_lines; ++k) {
         const int line = blockIdx.x + k * gridDim.x;
@@ -172,11 +173,12 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
                 }
             }
             tc::tc_fence_before();
-            if (colh) red_s[j & 1][row] = acc;
+            if (colq) red_s[j & 1][colq - 1][row] = acc;
             bar_compute();
             if (tid == 0) mbar_arrive(&accempty);
             const int p = t * kTile + row;
-            if (!colh && p < P) a.raw[size_t(line) * P + p] = sqrtf(acc + red_s[j & 1][row]);
+            if (!colq && p < P)
+                a.raw[size_t(line) * P + p] = sqrtf(acc + red_s[j & 1][0][row] + red_s[j & 1][1][row] + red_s[j & 1][2][row]);
         }
     }
     tc::tc_fence_before();
