@@ -270,6 +270,36 @@ def test_stats_i8_edges(pkg, oracle, P):
     check_gates(oracle, raw_g[0], norm_g[0], raw_o, norm_o, label=f"i8 P={P}")
 
 
+@pytest.mark.parametrize("B", [20, 64, 96, 124])
+def test_tensor_path_band_counts(pkg, oracle, B):
+    """The exact-integer tensor path across its eligible widths (N = roundup16(D+1) up to 128,
+    K-steps 1..4, ones row in the last N group) on drifting multi-stream data, two windows."""
+    rng = np.random.default_rng(B)
+    S, n, P = 3, 48, 256
+    mix = rng.normal(size=(S, 1, 1, B)).astype(np.float32)
+    x = (rng.normal(size=(S, n, P, B)) * np.linspace(0.2, 3.0, B) + 5.0 + mix
+         + np.linspace(0, 1, n)[None, :, None, None]).astype(np.float32)
+    cfg = pkg.ErxConfig(no_srp=True, buffer_len=8, alpha=0.2)
+    eng = pkg.Engine(cfg, B, n_streams=S, window_lines=24)
+    eng.push(x, 0)
+    eng.finish()
+    assert eng.stats_tensor() == 2
+    _, _, raw_g, norm_g = eng.pop()
+    for s in range(S):
+        raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), x[s])
+        check_gates(oracle, raw_g[s], norm_g[s], raw_o, norm_o, label=f"tensor B={B} s{s}")
+
+
+def test_tensor_path_falls_back_where_ineligible(pkg):
+    """B % 4 != 0 (no 16-byte rows), D > 127 and D <= 16 take the FFMA / small kernels."""
+    for B, ok in ((50, False), (130, False), (12, False), (108, True)):
+        eng = pkg.Engine(pkg.ErxConfig(no_srp=True), B, window_lines=2)
+        x = np.random.default_rng(B).normal(size=(1, 2, 160, B)).astype(np.float32)
+        eng.push(x, 0)
+        eng.finish()
+        assert (eng.stats_tensor() == 2) == ok, B
+
+
 def test_stats_i8_nonfinite_fails(pkg):
     # score-then-update: the inf of line 1 reaches the background scored by line 2
     x = np.random.default_rng(1).normal(size=(4, 96, 40)).astype(np.float32)
