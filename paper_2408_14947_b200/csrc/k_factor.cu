@@ -482,7 +482,10 @@ __global__ void __launch_bounds__(64) factor_blk_kernel(Geometry g, const double
                 }
                 st8(row, x);
             }
-            if (warp == nw - 1) {  // the factored diagonal block (lower part) for the inverse phase
+            __syncthreads();
+            // the factored diagonal block (lower part) for the inverse phase: written only after the
+            // barrier, since every thread reads the unfactored block in (a)
+            if (warp == nw - 1) {
 #pragma unroll
                 for (int r = 0; r < kBlk; ++r)
                     if (lane == r) {
@@ -490,7 +493,6 @@ __global__ void __launch_bounds__(64) factor_blk_kernel(Geometry g, const double
                         for (int c = 0; c <= r; ++c) Bk[r * kBlk + c] = L[r][c];
                     }
             }
-            __syncthreads();
             // (c) trailing update A_IJ -= L_Ik L_Jk^T, k < J <= I < nb: one block ROW per thread (task =
             //     pair x row), so the step's latency is 64 FMAs instead of 512 and all threads have work
             const int m = nb - k - 1;

@@ -133,6 +133,30 @@ def test_host_stream_groups_bitwise(pkg, groups):
     assert np.array_equal(res[0][2], res[1][2]) and np.array_equal(res[0][3], res[1][3])
 
 
+def test_full_window_is_deterministic(pkg):
+    """A configs[3]-sized window (32 streams x 16 lines, 1280 CTAs per factor launch) run twice gives
+    bit-identical scores: catches shared-memory races that small cases rarely hit."""
+    import torch
+
+    S, T, P, B = 32, 16, 640, 108
+    lines = np.stack([pkg.gen_lines(pkg.gen_spec(3, s), 0, 2 * T, threads=8, want_mask=False)[0] for s in range(S)])
+    x = torch.from_numpy(lines).cuda()
+    outs = []
+    for rep in range(2):
+        eng = pkg.Engine(pkg.ErxConfig(no_srp=True, alpha=0.1), B, n_streams=S, window_lines=T)
+        raw = torch.empty((S, T, P), dtype=torch.float32, device="cuda")
+        norm = torch.empty_like(raw)
+        res = []
+        for w in range(2):
+            xw = x[:, w * T:(w + 1) * T].contiguous()
+            eng.run_device(xw.data_ptr(), T, P, raw.data_ptr(), norm.data_ptr(), first_index=w * T)
+            eng.sync()
+            res.append(raw.cpu().numpy().copy())
+        outs.append(np.stack(res))
+        eng.close()
+    assert np.array_equal(outs[0], outs[1])
+
+
 def test_device_path_equals_host_path(pkg):
     import torch
 
