@@ -46,6 +46,35 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r01_ncu_full_tensor.txt")
+NCU_NAMES = {"stats": ("stats_i8_kernel", "stats_kernel", "stats_small"), "score": ("score_i8_kernel", "score_kernel"),
+             "factor": ("factor_blk_kernel",), "scan": ("scan_kernel",), "normalize": ("normalize_kernel",)}
+
+
+def ncu_traffic(kernel):
+    """DRAM bytes per launch (read + write) of `kernel` from the committed ncu --set full summary
+    (tools/ncu_summary.py output), or None when it has no entry for it."""
+    try:
+        text = open(NCU_SUMMARY).read()
+    except OSError:
+        return None
+    for block in text.split("== ")[1:]:
+        name = block.split("\n", 1)[0]
+        if not any(n in name for n in NCU_NAMES.get(kernel, ())):
+            continue
+        vals = {}
+        for line in block.splitlines()[1:]:
+            parts = line.split()
+            if len(parts) >= 3 and parts[0] in ("dram_read", "dram_write"):
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(parts[2], None)
+                if scale:
+                    vals[parts[0]] = float(parts[1]) * scale
+        if len(vals) == 2:
+            return {"bytes": vals["dram_read"] + vals["dram_write"],
+                    "source": os.path.relpath(NCU_SUMMARY, ROOT) + f" ({name.strip()}, one launch, ncu --set full)"}
+    return None
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -240,6 +269,11 @@ def run_ours(args):
                 "frac": dk["gbs"] / pk["hbm_gbs"] if dk["gbs"] else None, "traffic": None,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                 "algorithmic": f"{alg[dom]['bytes']} B/line x {S*T} lines/launch"}
+    tr = ncu_traffic(dom)
+    if tr:
+        roof["traffic"] = tr["bytes"]
+        roof["traffic_source"] = tr["source"]
+        roof["algorithmic_bytes"] = alg[dom]["bytes"] * S * T
     # whole-pipeline roofline per the north star: slower of flops@peak and bytes@HBM per line
     t_flop = alg["flops_line"] / (fp32_peak * 1e12)
     t_byte = alg["bytes_line"] / (pk["hbm_gbs"] * 1e9)
