@@ -456,9 +456,12 @@ __global__ void __launch_bounds__(64) factor_blk_kernel(Geometry g, const double
 #pragma unroll
                 for (int l = 0; l < j; ++l) d -= L[j][l] * L[j][l];
                 if (!(d > 0.f) && fail < 0) fail = k0 + j;
-                const float s = sqrtf(d);
+                // 1/sqrt(d) from MUFU.RSQ plus one Newton step (~1 ulp), s = d / sqrt(d)
+                float rs = rsqrtf(d);
+                rs = rs * fmaf(-0.5f * d * rs, rs, 1.5f);
+                const float s = d * rs;
                 L[j][j] = s;
-                rd[j] = 1.f / s;
+                rd[j] = rs;
 #pragma unroll
                 for (int r = j + 1; r < kBlk; ++r) {
                     float v = L[r][j];
@@ -550,7 +553,7 @@ __global__ void __launch_bounds__(64) factor_blk_kernel(Geometry g, const double
 #pragma unroll
             for (int r = 0; r < kBlk; ++r) {
                 ld8(Bk + r * kBlk, Lr[r]);
-                rl[r] = 1.f / Lr[r][r];
+                rl[r] = __frcp_rn(Lr[r][r]);
             }
 #pragma unroll
             for (int c = 0; c < kBlk; ++c) {
