@@ -73,6 +73,7 @@ struct erx_engine {
     float* d_vcache = nullptr;  // [S*T][D][P] centred projections (small path)
     float* d_vmax = nullptr;    // [S*T][D] per-dim |x - c| range (tensor path)
     unsigned char* d_vplanes = nullptr;  // [S*T][tiles][48 KB] quantised v digit planes (tensor path)
+    float* d_kblk = nullptr;    // [S*T][nb(nb+1)/2][64] pre-update K as fp32 blocks (blocked fp32 factor)
     int factor_req = 0;   // requested factor precision (0 auto, 32, 64)
     // ERX_OPT_STATS_TENSOR: 2 exact-integer tcgen05 stats + score where eligible (default), 1 tcgen05
     // bf16x3 stats (fp32 TMEM accumulation truncates, tools/tc_bias.py), 0 FFMA kernels.
@@ -210,6 +211,8 @@ void free_window(erx_engine* e) {
     e->d_vmax = nullptr;
     cudaFree(e->d_vplanes);
     e->d_vplanes = nullptr;
+    cudaFree(e->d_kblk);
+    e->d_kblk = nullptr;
     cudaFreeHost(e->h_lines);
     cudaFreeHost(e->h_status);
     e->d_lines = nullptr;
@@ -267,6 +270,7 @@ int configure(erx_engine* e, uint32_t P) {
     if (e->small) CU(cudaMalloc(&e->d_vcache, L * size_t(g.D) * P * sizeof(float)));
     if (erxk::stats_i8_eligible(g)) CU(cudaMalloc(&e->d_vmax, L * size_t(g.D) * sizeof(float)));
     if (e->tensor) CU(cudaMalloc(&e->d_vplanes, L * erxk::vplanes_bytes_per_line(g)));
+    if (e->factor_prec == 32) CU(cudaMalloc(&e->d_kblk, L * erxk::whiten_floats_per_line(g) * sizeof(float)));
     return ERX_OK;
 }
 
@@ -334,6 +338,7 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     float* vcache = e->d_vcache ? e->d_vcache + l0 * size_t(g.D) * g.P : nullptr;
     float* vmax = e->d_vmax ? e->d_vmax + l0 * size_t(g.D) : nullptr;
     unsigned char* vplanes = e->d_vplanes ? e->d_vplanes + l0 * erxk::vplanes_bytes_per_line(g) : nullptr;
+    float* kblk = e->d_kblk ? e->d_kblk + l0 * erxk::whiten_floats_per_line(g) : nullptr;
     const bool tensor = e->tensor;
     int* status = e->d_status + l0;
     float* rawg = raw + l0 * g.P;
@@ -350,11 +355,11 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     });
     timed(e, ERX_KERNEL_SCAN, [&] {
         erxk::launch_scan(g, stats, prior, st_in, st_out, int(ns), int(n), e->initialized ? 1 : 0, e->cfg.alpha,
-                          e->cfg.use_incremental, e->welford_n, e->stream);
+                          e->cfg.use_incremental, e->welford_n, e->stream, kblk);
     });
     timed(e, ERX_KERNEL_FACTOR, [&] {
         erxk::launch_factor(g, prior, L, e->cfg.epsilon, work, white, status, e->d_latch, line_base, e->factor_prec,
-                            e->stream, stats, tensor ? vmax : nullptr);
+                            e->stream, stats, tensor ? vmax : nullptr, kblk);
     });
     if (e->small) {  // score + normalisation fused
         timed(e, ERX_KERNEL_SCORE, [&] {

@@ -108,15 +108,17 @@ void launch_score_i8(const Geometry& g, const unsigned char* vplanes, const unsi
 // Host launchers.  All asynchronous on `st`.
 void launch_stats(const Geometry& g, const StatsLaunch& sl, const float* x, int n_per_stream, int in_stride,
                   int n_lines_total, double* stats, cudaStream_t st);
+// kblk (may be null): write the pre-update covariance as fp32 packed lower 8x8 blocks (row-major
+// inside a block, nb(nb+1)/2 * 64 floats per line) instead of fp64 into prior (the mean stays fp64).
 void launch_scan(const Geometry& g, const double* stats, double* prior, const double* state_in, double* state_out,
                  int n_streams, int n_per_stream, int initialized, double alpha, int incremental, int64_t n_seen0,
-                 cudaStream_t st);
+                 cudaStream_t st, float* kblk = nullptr);
 // latch: {flag, line, pivot} of the first factorisation failure (sticky until the host clears it).
 // vmax != null (precision 32 only): write the tensor path's int8 W planes (k_factor.cu: write_wplanes,
 // i8::kWBytes per line) instead of the fp32 blocks.
 void launch_factor(const Geometry& g, const double* prior, int n_lines_total, double eps0, double* work,
                    float* whiten, int* status, int* latch, int line_base, int precision, cudaStream_t st,
-                   const double* stats = nullptr, const float* vmax = nullptr);
+                   const double* stats = nullptr, const float* vmax = nullptr, const float* kblk = nullptr);
 void launch_score(const Geometry& g, const ScoreLaunch& sc, const float* x, int n_per_stream, int in_stride,
                   const double* prior, const float* whiten, int n_lines_total, float* raw, cudaStream_t st);
 void launch_normalize(const Geometry& g, const float* raw, int n_lines_total, float* norm, cudaStream_t st);

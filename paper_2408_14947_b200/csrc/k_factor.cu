@@ -393,7 +393,8 @@ __global__ void __launch_bounds__(64) factor_blk_kernel(Geometry g, const double
                                                          float* __restrict__ whiten, int* __restrict__ status,
                                                          int* __restrict__ latch, int line_base,
                                                          const double* __restrict__ stats,
-                                                         const float* __restrict__ vmax) {
+                                                         const float* __restrict__ vmax,
+                                                         const float* __restrict__ kblk) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_fail;
     const int D = g.D, Dp = g.Dp, nb = g.nb;
@@ -411,6 +412,23 @@ __global__ void __launch_bounds__(64) factor_blk_kernel(Geometry g, const double
     int fail;
     const int ntri = D * (D + 1) / 2;
     while (true) {
+        if (kblk) {
+            // fill from the scan's fp32 block image: a straight 16-byte copy, then + eps on the
+            // diagonal and zeros above it inside the diagonal blocks
+            const int nfl = nb * (nb + 1) / 2 * 64;
+            const float4* src = reinterpret_cast<const float4*>(kblk + size_t(line) * nfl);
+            for (int q = tid; q < nfl / 4; q += nt) cp_async16(A + 4 * q, src + q);
+            cp_async_commit();
+            cp_async_wait<0>();
+            __syncthreads();
+            const float fe = float(eps);
+            for (int q = tid; q < nb * 64; q += nt) {
+                const int kk = q >> 6, r = (q >> 3) & 7, c = q & 7;
+                float* p = BP(kk, kk) + r * kBlk + c;
+                if (c > r) *p = 0.f;
+                else if (c == r && kk * kBlk + r < D) *p += fe;
+            }
+        } else {
         // fill: coalesced reads of the packed fp64 K, 16 loads in flight per thread (the (i, j) of
         // idx + nt follows from (i, j) of idx incrementally), padding = identity
         {
@@ -438,6 +456,8 @@ __global__ void __launch_bounds__(64) factor_blk_kernel(Geometry g, const double
                     if (base + u * nt < ntri) *EL(ii[u], jj[u]) = float(v[u] + (ii[u] == jj[u] ? eps : 0.0));
             }
         }
+        }
+        __syncthreads();
         for (int i = D + tid; i < Dp; i += nt)
             for (int j = 0; j <= i; ++j) *EL(i, j) = (i == j) ? 1.f : 0.f;
         __syncthreads();
@@ -663,12 +683,12 @@ int factor_precision(const Geometry& g, int requested) {
 
 void launch_factor(const Geometry& g, const double* prior, int n_lines_total, double eps0, double* work,
                    float* whiten, int* status, int* latch, int line_base, int precision, cudaStream_t st,
-                   const double* stats, const float* vmax) {
+                   const double* stats, const float* vmax, const float* kblk) {
     const size_t sm = factor_smem(g, precision);
     if (precision == 32) {
         cudaFuncSetAttribute(factor_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         factor_blk_kernel<<<n_lines_total, 64, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
-                                                          vmax);
+                                                          vmax, kblk);
     } else if (precision == 64) {
         cudaFuncSetAttribute(factor_smem_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         factor_smem_kernel<double><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base);

@@ -22,7 +22,8 @@ __device__ __forceinline__ void unpack_tri(int k, int& a, int& b) {
 __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __restrict__ stats,
                                                    double* __restrict__ prior, const double* __restrict__ st_in,
                                                    double* __restrict__ st_out, int n, int initialized,
-                                                   double alpha, int incremental, int64_t n_seen0) {
+                                                   double alpha, int incremental, int64_t n_seen0,
+                                                   float* __restrict__ kblk) {
     const int s = blockIdx.y;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= g.SE) return;
@@ -30,6 +31,17 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
     const double P = double(g.P), invP = 1.0 / P, invP1 = 1.0 / (P - 1.0);
     int a = e, b = e;
     if (e >= D) unpack_tri(e - D, a, b);
+    // with kblk, the pre-update covariance goes out as fp32 packed lower 8x8 blocks (the blocked
+    // factor's shared-memory image) and only the mean as fp64
+    const int nblk = g.nb * (g.nb + 1) / 2;
+    const bool to_blk = kblk != nullptr && e >= D;
+    const int boff = ((a >> 3) * ((a >> 3) + 1) / 2 + (b >> 3)) * 64 + (a & 7) * 8 + (b & 7);
+    auto put = [&](size_t l, double pr) {
+        if (to_blk)
+            kblk[l * nblk * 64 + boff] = float(pr);
+        else
+            prior[l * g.SE + e] = pr;
+    };
     const double* in = st_in + size_t(s) * g.SE;
     const size_t l0 = size_t(s) * n;
     // line statistics of line l, this element (and the two means it couples)
@@ -73,7 +85,7 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
                         pr = state;
                         state = __dadd_rn(__dmul_rn(om, state), __dmul_rn(alpha, cur[u]));
                     }
-                    prior[(l0 + t) * g.SE + e] = pr;
+                    put(l0 + t, pr);
                 }
             }
 #pragma unroll
@@ -110,7 +122,7 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
                 mb += db * (nb / nn);
                 nseen = nn;
             }
-            prior[l * g.SE + e] = pr;
+            put(l, pr);
         }
         st_out[size_t(s) * g.SE + e] = (e < D) ? ma : cov;
     }
@@ -120,10 +132,10 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
 
 void launch_scan(const Geometry& g, const double* stats, double* prior, const double* state_in, double* state_out,
                  int n_streams, int n_per_stream, int initialized, double alpha, int incremental, int64_t n_seen0,
-                 cudaStream_t st) {
+                 cudaStream_t st, float* kblk) {
     dim3 grid((g.SE + 127) / 128, n_streams);
     scan_kernel<<<grid, 128, 0, st>>>(g, stats, prior, state_in, state_out, n_per_stream, initialized, alpha,
-                                      incremental, n_seen0);
+                                      incremental, n_seen0, kblk);
 }
 
 }  // namespace erxk
