@@ -111,6 +111,12 @@ int erx_pop(erx_engine* e, uint32_t max_lines, int64_t* index, uint8_t* warmup, 
  */
 int erx_run_device(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t pixels, const float* d_lines,
                    float* d_raw, float* d_norm);
+/* Background update only: line statistics and the EMA / Welford scan over
+ * n_lines device-resident lines, no factor and no scores.  With
+ * erx_set_state it is the building block of the line-range split of one
+ * stream across devices (paper_2408_14947_b200/sharding.py:
+ * range summary from a zero background, carry chain, then scoring). */
+int erx_advance_device(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t pixels, const float* d_lines);
 int erx_sync(erx_engine* e);
 void* erx_cuda_stream(erx_engine* e);
 

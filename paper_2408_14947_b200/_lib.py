@@ -80,6 +80,7 @@ SIGNATURES = {
     "erx_next_pixels": (C.c_uint32, [_vp]),
     "erx_pop": (C.c_int, [_vp, C.c_uint32, _i64p, _u8p, _dp, _dp]),
     "erx_run_device": (C.c_int, [_vp, C.c_int64, C.c_uint32, C.c_uint32, _vp, _vp, _vp]),
+    "erx_advance_device": (C.c_int, [_vp, C.c_int64, C.c_uint32, C.c_uint32, _vp]),
     "erx_sync": (C.c_int, [_vp]),
     "erx_cuda_stream": (C.c_void_p, [_vp]),
     "erx_get_state": (C.c_int, [_vp, C.c_uint32, _dp, _dp, _i64p, _i64p, C.POINTER(C.c_int)]),

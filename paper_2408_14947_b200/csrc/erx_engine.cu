@@ -323,7 +323,7 @@ std::shared_ptr<ResultBlock> take_block(erx_engine* e, uint32_t n) {
 // per-line buffer holds line (s, t) at s * n + t, so a stream range is a
 // contiguous line range and the groups are independent (no cross-stream data).
 int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride, float* raw, float* norm,
-                   uint32_t s0, uint32_t ns) {
+                   uint32_t s0, uint32_t ns, bool score = true) {
     const Geometry& g = e->geo;
     const int L = int(ns * n);
     const size_t l0 = size_t(s0) * n;
@@ -341,8 +341,8 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     float* kblk = e->d_kblk ? e->d_kblk + l0 * erxk::whiten_floats_per_line(g) : nullptr;
     const bool tensor = e->tensor;
     int* status = e->d_status + l0;
-    float* rawg = raw + l0 * g.P;
-    float* normg = norm + l0 * g.P;
+    float* rawg = raw ? raw + l0 * g.P : nullptr;
+    float* normg = norm ? norm + l0 * g.P : nullptr;
     timed(e, ERX_KERNEL_STATS, [&] {
         if (e->small)
             erxk::launch_stats_small(g, e->smp, xg, int(n), int(in_stride), L, stats, vcache, e->stream);
@@ -357,6 +357,11 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
         erxk::launch_scan(g, stats, prior, st_in, st_out, int(ns), int(n), e->initialized ? 1 : 0, e->cfg.alpha,
                           e->cfg.use_incremental, e->welford_n, e->stream, kblk);
     });
+    if (!score) {  // background update only (erx_advance_device): statistics and the scan
+        cudaError_t r = cudaGetLastError();
+        if (r != cudaSuccess) return fail(e, ERX_ERR_DEVICE, std::string("kernel launch: ") + cudaGetErrorString(r));
+        return ERX_OK;
+    }
     timed(e, ERX_KERNEL_FACTOR, [&] {
         erxk::launch_factor(g, prior, L, e->cfg.epsilon, work, white, status, e->d_latch, line_base, e->factor_prec,
                             e->stream, stats, tensor ? vmax : nullptr, kblk);
@@ -717,6 +722,21 @@ int erx_run_device(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_
     int st = configure(e, pixels);
     if (st) return st;
     st = enqueue_window(e, d_lines, n_lines, n_lines, d_raw, d_norm, 0, e->S);
+    if (st) return st;
+    commit_window(e, n_lines);
+    return ERX_OK;
+}
+
+int erx_advance_device(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t pixels, const float* d_lines) {
+    (void)first_index;
+    if (e->failed) return fail(e, ERX_ERR_STATE, "engine is in a failed state: " + e->err);
+    if (pixels < 2) return fail(e, ERX_ERR_DATA, "a line needs p >= 2 pixels (1/(p-1) covariance)");
+    if (n_lines == 0) return ERX_OK;
+    if (n_lines > e->T) return fail(e, ERX_ERR_CONFIG, "n_lines exceeds the engine window");
+    if (e->fill) return fail(e, ERX_ERR_STATE, "host lines pending; call erx_finish first");
+    int st = configure(e, pixels);
+    if (st) return st;
+    st = enqueue_window(e, d_lines, n_lines, n_lines, nullptr, nullptr, 0, e->S, /*score=*/false);
     if (st) return st;
     commit_window(e, n_lines);
     return ERX_OK;

@@ -230,6 +230,11 @@ class Engine:
         self._check(self._lib.erx_run_device(self._h, first_index, n_lines, pixels, C.c_void_p(d_lines),
                                              C.c_void_p(d_raw), C.c_void_p(d_norm)))
 
+    def advance_device(self, d_lines: int, n_lines: int, pixels: int, first_index: int = 0):
+        """Background update only (statistics + scan, no scores): erx_advance_device."""
+        self.pixels = pixels
+        self._check(self._lib.erx_advance_device(self._h, first_index, n_lines, pixels, C.c_void_p(d_lines)))
+
     def sync(self):
         self._check(self._lib.erx_sync(self._h))
 

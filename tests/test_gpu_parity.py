@@ -390,3 +390,60 @@ def test_errors(pkg):
     assert e.value.pivot >= 0 and e.value.exit_code() == 3
     with pytest.raises(pkg.DeviceError):  # sticky failed state (ERX_ERR_STATE)
         det.process(pkg.SpectralLine(1, np.ones((8, 3), np.float32)), [])
+
+
+@pytest.mark.parametrize("incremental", [False, True])
+def test_line_range_split_matches_unsplit(pkg, oracle, incremental):
+    """One stream split into three line ranges (sharding.carry_chain): each range is
+    summarised from a zero background with erx_advance_device, the chained carry is installed with
+    erx_set_state, and the ranges scored independently match the unsplit run (and the oracle)."""
+    import torch
+
+    from paper_2408_14947_b200.sharding import carry_chain, line_ranges
+
+    rng = np.random.default_rng(7 + incremental)
+    n, P, B, T = 60, 256, 24, 8
+    x = (rng.normal(size=(n, P, B)) * np.linspace(0.5, 2.0, B) + 3.0
+         + np.linspace(0, 2, n)[:, None, None]).astype(np.float32)
+    cfg = pkg.ErxConfig(no_srp=True, alpha=0.1, use_incremental=incremental, buffer_len=5)
+    dx = torch.from_numpy(x).cuda()
+
+    def run(eng, rows, do_score):
+        out = []
+        for s in range(rows.start, rows.stop, T):
+            m = min(T, rows.stop - s)
+            xs = dx[s:s + m].contiguous()
+            if do_score:
+                raw = torch.empty((m, P), dtype=torch.float32, device="cuda")
+                eng.run_device(xs.data_ptr(), m, P, raw.data_ptr(), torch.empty_like(raw).data_ptr(), first_index=s)
+                eng.sync()
+                out.append(raw.cpu().numpy())
+            else:
+                eng.advance_device(xs.data_ptr(), m, P, first_index=s)
+                eng.sync()
+        return np.concatenate(out) if out else None
+
+    full = run(pkg.Engine(cfg, B, window_lines=T), range(0, n), True)
+    ranges = line_ranges(n, 3)
+    summaries = []
+    for r, rows in enumerate(ranges):
+        eng = pkg.Engine(cfg, B, window_lines=T)
+        if r > 0:
+            eng.set_state(0, np.zeros(B), np.zeros((B, B)), lines_seen=rows.start, welford_n=0)
+        run(eng, rows, False)
+        st = eng.state()
+        summaries.append({"lines": len(rows), "n": st.welford_n, "mu": st.mu, "cov": st.cov})
+    carries = carry_chain(summaries, cfg.alpha, incremental)
+    parts = []
+    for r, rows in enumerate(ranges):
+        eng = pkg.Engine(cfg, B, window_lines=T)
+        if r > 0:
+            c = carries[r]
+            eng.set_state(0, c["mu"], c["cov"], lines_seen=rows.start, welford_n=int(c.get("n", 0)))
+        parts.append(run(eng, rows, True))
+    split = np.concatenate(parts)
+    rel = np.abs(split - full) / np.maximum(np.abs(full), 1e-30)
+    assert np.median(rel) < 1e-6 and rel.max() < 1e-4, (np.median(rel), rel.max())
+    raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), x)
+    rel_o = np.abs(split - raw_o) / np.maximum(np.abs(raw_o), 1e-30)
+    assert rel_o.max() <= RAW_MAX and np.median(rel_o) <= RAW_MED
