@@ -686,14 +686,14 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
                    const double* stats, const float* vmax, const float* kblk) {
     const size_t sm = factor_smem(g, precision);
     if (precision == 32) {
-        cudaFuncSetAttribute(factor_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        ensure_smem(factor_blk_kernel, sm);
         factor_blk_kernel<<<n_lines_total, 64, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
                                                           vmax, kblk);
     } else if (precision == 64) {
-        cudaFuncSetAttribute(factor_smem_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        ensure_smem(factor_smem_kernel<double>, sm);
         factor_smem_kernel<double><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base);
     } else {
-        cudaFuncSetAttribute(factor_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        ensure_smem(factor_global_kernel, sm);
         factor_global_kernel<<<n_lines_total, 256, sm, st>>>(g, prior, eps0, work, whiten, status, latch,
                                                                line_base);
     }

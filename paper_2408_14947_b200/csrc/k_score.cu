@@ -194,10 +194,8 @@ size_t whiten_floats_per_line(const Geometry& g) { return size_t(g.nb) * (g.nb +
 
 void launch_score(const Geometry& g, const ScoreLaunch& sc, const float* x, int n_per_stream, int in_stride,
                   const double* prior, const float* whiten, int n_lines_total, float* raw, cudaStream_t st) {
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        attr_done = true;
+    {
+        ensure_smem(score_kernel, 220 * 1024);
     }
     ScoreArgs a{g, sc, x, n_per_stream, in_stride, prior, whiten, raw};
     score_kernel<<<n_lines_total * sc.tiles, sc.threads, sc.smem, st>>>(a);

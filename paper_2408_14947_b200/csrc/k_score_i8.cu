@@ -195,14 +195,9 @@ bool score_i8_eligible(const Geometry& g) { return !g.srp && g.D > 16 && g.D <= 
 
 void launch_score_i8(const Geometry& g, const unsigned char* vplanes, const unsigned char* wplanes, int n_lines_total,
                      float* raw, cudaStream_t st) {
-    static int sms = 0;
     const size_t smem = 2 * 3 * size_t(i8::kWPlane) + kStages * size_t(i8::kTileBytes);
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(score_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    }
+    const int sms = sm_count();
+    ensure_smem(score_i8_kernel, smem);
     ScoreI8Args a{g, n_lines_total, vplanes, wplanes, raw, (g.D + 15) / 16 * 16};
     const int grid = n_lines_total < sms ? n_lines_total : sms;
     score_i8_kernel<<<grid, kThreads + 64, smem, st>>>(a);

@@ -276,12 +276,10 @@ SmallLaunch plan_small(const Geometry& g) {
 
 void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x, int n_per_stream, int in_stride,
                         int n_lines_total, double* stats, float* vcache, cudaStream_t st) {
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaFuncSetAttribute(stats_small_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(stats_small_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(stats_small_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_done = true;
+    {
+        ensure_smem(stats_small_kernel<8>, 200 * 1024);
+        ensure_smem(stats_small_kernel<12>, 200 * 1024);
+        ensure_smem(stats_small_kernel<16>, 200 * 1024);
     }
     SmallArgs a{g, sm, x, n_per_stream, in_stride, stats, vcache};
     if (g.D <= 8)
@@ -295,11 +293,9 @@ void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x
 void launch_score_small(const Geometry& g, const SmallLaunch& sm, const double* stats, const double* prior,
                         const float* whiten, const float* vcache, int n_lines_total, float* raw, float* norm,
                         cudaStream_t st) {
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaFuncSetAttribute(score_small_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(score_small_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_done = true;
+    {
+        ensure_smem(score_small_kernel<8>, 200 * 1024);
+        ensure_smem(score_small_kernel<16>, 200 * 1024);
     }
     if (g.D <= 8)
         score_small_kernel<8><<<n_lines_total, kSmallThreads, sm.smem_score, st>>>(g, stats, prior, whiten, vcache,

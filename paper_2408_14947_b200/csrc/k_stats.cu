@@ -277,10 +277,8 @@ StatsLaunch plan_stats(const Geometry& g) {
 
 void launch_stats(const Geometry& g, const StatsLaunch& sl, const float* x, int n_per_stream, int in_stride,
                   int n_lines_total, double* stats, cudaStream_t st) {
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaFuncSetAttribute(stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_done = true;
+    {
+        ensure_smem(stats_kernel, 200 * 1024);
     }
     StatsArgs a{g, sl, x, n_per_stream, in_stride, stats};
     stats_kernel<<<n_lines_total * sl.cpl, 128, sl.smem, st>>>(a);

@@ -436,13 +436,8 @@ bool stats_i8_eligible(const Geometry& g) {
 
 void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
                      double* stats, float* vmax, unsigned char* vplanes, cudaStream_t st) {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(stats_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemCap - kStaticSmem));
-    }
+    const int sms = sm_count();
+    ensure_smem(stats_i8_kernel, kSmemCap - kStaticSmem);
     StatsI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, vmax, vplanes, (g.D + 1 + 15) / 16 * 16,
                   i8_stages(g)};
     const int grid = n_lines_total < sms ? n_lines_total : sms;

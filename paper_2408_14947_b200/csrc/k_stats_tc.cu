@@ -177,12 +177,8 @@ size_t stats_tc_smem(const Geometry& g) {
 
 void launch_stats_tc(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
                      double* stats, cudaStream_t st) {
-    static bool attr_done = false;
     const size_t sm = stats_tc_smem(g);
-    if (!attr_done) {
-        cudaFuncSetAttribute(stats_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_done = true;
-    }
+    ensure_smem(stats_tc_kernel, 200 * 1024);
     StatsTcArgs a{g, x, n_per_stream, in_stride, stats};
     stats_tc_kernel<<<n_lines_total, 128, sm, st>>>(a);
 }
