@@ -481,7 +481,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--mode", default="full", choices=["full", "srp"])
-    ap.add_argument("--window", type=int, default=16)
+    ap.add_argument("--window", type=int, default=32)
     ap.add_argument("--factor", type=int, default=0, choices=[0, 1, 32, 64],
                     help="factor kernel precision (ERX_OPT_FACTOR_PRECISION)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
