@@ -389,7 +389,7 @@ __device__ __forceinline__ void st8(float* p, const float* v) {
     *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
 }
 
-__global__ void __launch_bounds__(64) factor_blk_kernel(Geometry g, const double* __restrict__ prior, double eps0,
+__global__ void __launch_bounds__(256) factor_blk_kernel(Geometry g, const double* __restrict__ prior, double eps0,
                                                          float* __restrict__ whiten, int* __restrict__ status,
                                                          int* __restrict__ latch, int line_base,
                                                          const double* __restrict__ stats,
@@ -687,7 +687,10 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
     const size_t sm = factor_smem(g, precision);
     if (precision == 32) {
         ensure_smem(factor_blk_kernel, sm);
-        factor_blk_kernel<<<n_lines_total, 64, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
+        // 64 threads per line fill the GPU with ~7 lines per SM; when a launch has fewer lines than
+        // SMs (lag-0 / small windows) more threads per line shorten each line's latency instead
+        const int threads = n_lines_total >= sm_count() ? 64 : 256;
+        factor_blk_kernel<<<n_lines_total, threads, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
                                                           vmax, kblk);
     } else if (precision == 64) {
         ensure_smem(factor_smem_kernel<double>, sm);
