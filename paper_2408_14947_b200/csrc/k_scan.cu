@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
         double state = in[e];
         // the line statistics do not depend on the recurrence: they are loaded a batch
         // ahead (double-buffered registers) so the sequential EMA never waits on memory
-        constexpr int kB = 16;
+        constexpr int kB = 8;
         double cur[kB], nxt[kB];
         // branch-free loads (clamped line index, select after) so all 3 x kB loads issue back to back
         const bool is_mu = e < D;
