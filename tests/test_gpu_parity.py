@@ -294,8 +294,8 @@ def test_stats_i8_edges(pkg, oracle, P):
     check_gates(oracle, raw_g[0], norm_g[0], raw_o, norm_o, label=f"i8 P={P}")
 
 
-@pytest.mark.parametrize("B", [20, 64, 96, 124])
-def test_tensor_path_band_counts(pkg, oracle, B):
+@pytest.mark.parametrize("B,incremental", [(20, False), (64, False), (96, True), (124, False), (124, True)])
+def test_tensor_path_band_counts(pkg, oracle, B, incremental):
     """The exact-integer tensor path across its eligible widths (N = roundup16(D+1) up to 128,
     K-steps 1..4, ones row in the last N group) on drifting multi-stream data, two windows."""
     rng = np.random.default_rng(B)
@@ -303,7 +303,7 @@ def test_tensor_path_band_counts(pkg, oracle, B):
     mix = rng.normal(size=(S, 1, 1, B)).astype(np.float32)
     x = (rng.normal(size=(S, n, P, B)) * np.linspace(0.2, 3.0, B) + 5.0 + mix
          + np.linspace(0, 1, n)[None, :, None, None]).astype(np.float32)
-    cfg = pkg.ErxConfig(no_srp=True, buffer_len=8, alpha=0.2)
+    cfg = pkg.ErxConfig(no_srp=True, buffer_len=8, alpha=0.2, use_incremental=incremental)
     eng = pkg.Engine(cfg, B, n_streams=S, window_lines=24)
     eng.push(x, 0)
     eng.finish()
@@ -311,7 +311,7 @@ def test_tensor_path_band_counts(pkg, oracle, B):
     _, _, raw_g, norm_g = eng.pop()
     for s in range(S):
         raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), x[s])
-        check_gates(oracle, raw_g[s], norm_g[s], raw_o, norm_o, label=f"tensor B={B} s{s}")
+        check_gates(oracle, raw_g[s], norm_g[s], raw_o, norm_o, label=f"tensor B={B} inc={incremental} s{s}")
 
 
 def test_tensor_path_falls_back_where_ineligible(pkg):
