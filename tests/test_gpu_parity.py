@@ -133,13 +133,17 @@ def test_host_stream_groups_bitwise(pkg, groups):
     assert np.array_equal(res[0][2], res[1][2]) and np.array_equal(res[0][3], res[1][3])
 
 
-def test_full_window_is_deterministic(pkg):
-    """A configs[3]-sized window (32 streams x 16 lines, 1280 CTAs per factor launch) run twice gives
-    bit-identical scores: catches shared-memory races that small cases rarely hit."""
+@pytest.mark.parametrize("cid,S,T", [(3, 32, 16), (1, 1, 160), (2, 1, 256), (4, 4, 8)])
+def test_full_window_is_deterministic(pkg, cid, S, T):
+    """Full-size windows run twice give bit-identical scores: the tensor path (configs[3]), the FFMA
+    kernels with the blocked fp32 factor (configs[1], D = 224), the small-D path (configs[2]) and
+    the fp64 global factor (configs[4], D = 448).  Catches shared-memory races that small cases
+    rarely hit."""
     import torch
 
-    S, T, P, B = 32, 16, 640, 108
-    lines = np.stack([pkg.gen_lines(pkg.gen_spec(3, s), 0, 2 * T, threads=8, want_mask=False)[0] for s in range(S)])
+    spec0 = pkg.gen_spec(cid, 0)
+    P, B = spec0.pixels, spec0.bands
+    lines = np.stack([pkg.gen_lines(pkg.gen_spec(cid, s), 0, 2 * T, threads=8, want_mask=False)[0] for s in range(S)])
     x = torch.from_numpy(lines).cuda()
     outs = []
     for rep in range(2):
