@@ -131,11 +131,12 @@ int erx_get_weights(const erx_engine* e, double* weights);
 int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double* cov, int64_t lines_seen,
                   int64_t welford_n);
 
-/* Engine options.  ERX_OPT_FACTOR_PRECISION: 0 auto (fp64 in shared memory
- * while the D x D factor fits, else fp32 in shared memory, else blocked fp64
- * over global memory), 64, 32, or 1 (force the blocked fp64 global-memory
- * kernel).  erx_get_option reports the precision in
- * use once the first line has fixed the geometry (0 = blocked fp64 path). */
+/* Engine options.  ERX_OPT_FACTOR_PRECISION: 0 auto (blocked fp32 in shared
+ * memory while the matrix fits, D <= 233, else blocked fp32 over the L2
+ * workspace), 32, 31 (force the fp32 L2 kernel), 64 (fp64 in shared memory,
+ * D <= 165, else the fp64 L2 kernel) or 1 (force the blocked fp64 L2 kernel).
+ * erx_get_option reports the kernel in use once the first line has fixed the
+ * geometry: 32, 31, 64 or 0 (blocked fp64 L2). */
 #define ERX_OPT_FACTOR_PRECISION 1
 /* ERX_OPT_STATS_TENSOR: which kernels compute line_stats and the score.
  *   2 (default) exact-integer tcgen05 path (kind::i8 digit planes, s32 TMEM

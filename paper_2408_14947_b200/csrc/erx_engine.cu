@@ -260,7 +260,7 @@ int configure(erx_engine* e, uint32_t P) {
     const size_t L = size_t(e->S) * e->T;
     CU(cudaMalloc(&e->d_stats, L * (g.SE + g.D) * sizeof(double)));  // [c | s | S] per line
     CU(cudaMalloc(&e->d_prior, L * g.SE * sizeof(double)));
-    if (e->factor_prec == 0) CU(cudaMalloc(&e->d_work, L * 2 * size_t(g.Dp) * g.Dp * sizeof(double)));
+    if (e->factor_prec == 0 || e->factor_prec == 31) CU(cudaMalloc(&e->d_work, L * 2 * size_t(g.Dp) * g.Dp * sizeof(double)));
     CU(cudaMalloc(&e->d_white, L * std::max(erxk::whiten_floats_per_line(g),
                                             erxk::stats_i8_eligible(g) ? erxk::wplanes_bytes_per_line() / 4 : size_t(0)) *
                                     sizeof(float)));
@@ -820,8 +820,8 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
         return ERX_OK;
     }
     if (option == ERX_OPT_FACTOR_PRECISION) {
-        if (value != 0 && value != 1 && value != 32 && value != 64)
-            return fail(e, ERX_ERR_CONFIG, "factor precision: 0, 1, 32 or 64");
+        if (value != 0 && value != 1 && value != 31 && value != 32 && value != 64)
+            return fail(e, ERX_ERR_CONFIG, "factor precision: 0, 1, 31, 32 or 64");
         e->factor_req = int(value);
         if (e->d_stats) {
             const uint32_t P = e->P;

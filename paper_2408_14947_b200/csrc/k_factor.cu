@@ -293,6 +293,239 @@ __global__ void __launch_bounds__(256) factor_global_kernel(Geometry g, const do
 }
 
 // ---------------------------------------------------------------------------
+// factor_big: fp32 blocked Cholesky and triangular inverse for D > 233 (the
+// matrix does not fit in shared memory): A and X live in the global (L2)
+// workspace, 256 threads per line, panel width 32.  Per step: the diagonal
+// block is factored by one warp with the rows in registers (shuffles for the
+// column broadcasts), the panel rows are solved one per thread and kept
+// transposed in shared memory, and the trailing update runs 8x8 register
+// tiles (two 16-byte shared loads per 64 FMAs) with one read-modify-write of
+// the tile in L2.  The inverse goes by block rows, one column per thread.
+// ---------------------------------------------------------------------------
+constexpr int kBB = 32;
+
+__device__ __forceinline__ float rsqrt_nr(float d) {
+    float rs = rsqrtf(d);
+    return rs * fmaf(-0.5f * d * rs, rs, 1.5f);
+}
+
+__global__ void __launch_bounds__(256) factor_big_kernel(Geometry g, const double* __restrict__ prior, double eps0,
+                                                         float* __restrict__ work, float* __restrict__ whiten,
+                                                         int* __restrict__ status, int* __restrict__ latch,
+                                                         int line_base) {
+    extern __shared__ __align__(16) float fsm[];
+    __shared__ int s_fail;
+    __shared__ float rd_s[kBB];
+    const int line = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int D = g.D, Dp = g.Dp;
+    const int LDT = Dp + 4;                  // row stride of the transposed panel / L row block
+    float* A = work + size_t(line) * 2 * Dp * Dp;
+    float* X = A + size_t(Dp) * Dp;
+    float* Lkk = fsm;                        // [32][33]
+    float* Pt = fsm + kBB * (kBB + 1);       // [32][LDT]: panel (transposed) / inverse: L row block (transposed)
+    const double* K = prior + size_t(line) * g.SE + D;
+    const int ntri = D * (D + 1) / 2;
+    double eps = eps0;
+    int fail = -1;
+    while (true) {
+        {   // fill the lower triangle (packed fp64 K -> fp32 A), incremental (i, j)
+            int i = int((sqrtf(8.f * tid + 1.f) - 1.f) * 0.5f), j;
+            while (i * (i + 1) / 2 > tid) --i;
+            while ((i + 1) * (i + 2) / 2 <= tid) ++i;
+            j = tid - i * (i + 1) / 2;
+            for (int idx = tid; idx < ntri; idx += nt) {
+                A[size_t(i) * Dp + j] = float(__ldg(K + idx) + (i == j ? eps : 0.0));
+                j += nt;
+                while (j > i) {
+                    j -= i + 1;
+                    ++i;
+                }
+            }
+        }
+        __syncthreads();
+        fail = -1;
+        for (int k0 = 0; k0 < D; k0 += kBB) {
+            const int kb = min(kBB, D - k0);
+            for (int idx = tid; idx < kBB * kBB; idx += nt) {
+                const int r = idx >> 5, c = idx & 31;
+                Lkk[r * (kBB + 1) + c] = (r < kb && c <= r) ? A[size_t(k0 + r) * Dp + k0 + c] : 0.f;
+            }
+            if (tid == 0) s_fail = -1;
+            __syncthreads();
+            if (warp == 0) {
+                // lane r holds row r; column j: broadcast the diagonal, scale the column, then update
+                // the trailing entries of every row with the column's values from their lanes
+                float row[kBB];
+#pragma unroll
+                for (int c = 0; c < kBB; ++c) row[c] = Lkk[lane * (kBB + 1) + c];
+                int f = -1;
+#pragma unroll
+                for (int jj = 0; jj < kBB; ++jj) {
+                    if (jj < kb && f < 0) {
+                        const float d = __shfl_sync(0xffffffffu, row[jj], jj);
+                        if (!(d > 0.f)) {
+                            f = k0 + jj;
+                        } else {
+                            const float rs = rsqrt_nr(d);
+                            if (lane == jj) {
+                                row[jj] = d * rs;
+                                rd_s[jj] = rs;
+                            } else if (lane > jj) {
+                                row[jj] *= rs;
+                            }
+#pragma unroll
+                            for (int c = jj + 1; c < kBB; ++c) {
+                                const float lcj = __shfl_sync(0xffffffffu, row[jj], c);
+                                if (lane >= c) row[c] = fmaf(-row[jj], lcj, row[c]);
+                            }
+                        }
+                    }
+                }
+                if (lane == 0) s_fail = f;
+                if (f < 0 && lane < kb) {
+#pragma unroll
+                    for (int c = 0; c < kBB; ++c) {
+                        const float v = c <= lane ? row[c] : 0.f;
+                        Lkk[lane * (kBB + 1) + c] = v;
+                        if (c <= lane) A[size_t(k0 + lane) * Dp + k0 + c] = v;
+                    }
+                }
+            }
+            __syncthreads();
+            fail = s_fail;
+            if (fail >= 0) break;
+            // panel: L_ik = A_ik L_kk^{-T}, one row per thread, kept transposed in shared memory
+            const int r0 = k0 + kb, nr = D - r0;
+            for (int rr = tid; rr < nr; rr += nt) {
+                float* arow = A + size_t(r0 + rr) * Dp + k0;
+                float x[kBB];
+#pragma unroll
+                for (int c = 0; c < kBB; ++c) {
+                    if (c < kb) {
+                        float s = arow[c];
+#pragma unroll
+                        for (int l = 0; l < c; ++l) s = fmaf(-x[l], Lkk[c * (kBB + 1) + l], s);
+                        x[c] = s * rd_s[c];
+                        arow[c] = x[c];
+                        Pt[c * LDT + rr] = x[c];
+                    } else {
+                        Pt[c * LDT + rr] = 0.f;
+                    }
+                }
+            }
+            // zero the transposed panel's padding rows so 8-row tiles read zeros
+            for (int idx = tid; idx < kBB * 8; idx += nt) Pt[(idx >> 3) * LDT + nr + (idx & 7)] = 0.f;
+            __syncthreads();
+            // trailing update A22 -= P P^T over the lower triangle, 8x8 register tiles
+            const int n8 = (nr + 7) / 8;
+            const int ntile = n8 * (n8 + 1) / 2;
+            for (int tix = tid; tix < ntile; tix += nt) {
+                int R = int((sqrtf(8.f * tix + 1.f) - 1.f) * 0.5f);
+                while (R * (R + 1) / 2 > tix) --R;
+                while ((R + 1) * (R + 2) / 2 <= tix) ++R;
+                const int C = tix - R * (R + 1) / 2;
+                float acc[8][8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int jx = 0; jx < 8; ++jx) acc[i][jx] = 0.f;
+                for (int l = 0; l < kb; ++l) {
+                    const float4 a0 = *reinterpret_cast<const float4*>(Pt + l * LDT + R * 8);
+                    const float4 a1 = *reinterpret_cast<const float4*>(Pt + l * LDT + R * 8 + 4);
+                    const float4 b0 = *reinterpret_cast<const float4*>(Pt + l * LDT + C * 8);
+                    const float4 b1 = *reinterpret_cast<const float4*>(Pt + l * LDT + C * 8 + 4);
+                    const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int jx = 0; jx < 8; ++jx) acc[i][jx] = fmaf(av[i], bv[jx], acc[i][jx]);
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int ri = R * 8 + i;
+                    if (ri < nr) {
+                        float* arow = A + size_t(r0 + ri) * Dp + r0 + C * 8;
+#pragma unroll
+                        for (int jx = 0; jx < 8; ++jx)
+                            if (C * 8 + jx <= ri) arow[jx] -= acc[i][jx];
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (fail < 0) break;
+        const double next = eps * 10.0;
+        if (!(next <= 1e-1 * (1.0 + 1e-9))) break;
+        eps = next;
+        __syncthreads();
+    }
+    if (fail >= 0) {
+        if (tid == 0) {
+            status[line] = fail;
+            if (atomicCAS(latch, 0, 1) == 0) {
+                latch[1] = line_base + line;
+                latch[2] = fail;
+            }
+        }
+        return;
+    }
+    // X = L^{-1} by block rows: X_I = L_II^{-1} (E_I - sum_{J<I} L_IJ X_J), one column per thread
+    for (int i0 = 0; i0 < D; i0 += kBB) {
+        const int ib = min(kBB, D - i0), ncol = i0 + ib;
+        __syncthreads();
+        for (int idx = tid; idx < kBB * ncol; idx += nt) {  // L row block, transposed: Pt[j][r] = L[i0+r][j]
+            const int j = idx / kBB, r = idx - j * kBB;
+            Pt[j * kBB + r] = (r < ib && j <= i0 + r) ? A[size_t(i0 + r) * Dp + j] : 0.f;
+        }
+        if (tid < kBB) rd_s[tid] = tid < ib ? 1.f / A[size_t(i0 + tid) * Dp + i0 + tid] : 0.f;
+        __syncthreads();
+        for (int c = tid; c < ncol; c += nt) {
+            float t[kBB];
+#pragma unroll
+            for (int r = 0; r < kBB; ++r) t[r] = (i0 + r == c) ? 1.f : 0.f;
+            // X[j][c] = 0 for j < c; the L2 loads of X go out 8 at a time ahead of their FMAs
+            for (int j0 = c; j0 < i0; j0 += 8) {
+                float xv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) xv[u] = (j0 + u < i0) ? X[size_t(j0 + u) * Dp + c] : 0.f;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (j0 + u < i0) {
+                        const float xj = xv[u];
+                        const float4* lt = reinterpret_cast<const float4*>(Pt + (j0 + u) * kBB);
+#pragma unroll
+                        for (int q = 0; q < kBB / 4; ++q) {
+                            const float4 l4 = lt[q];
+                            t[4 * q] = fmaf(-l4.x, xj, t[4 * q]);
+                            t[4 * q + 1] = fmaf(-l4.y, xj, t[4 * q + 1]);
+                            t[4 * q + 2] = fmaf(-l4.z, xj, t[4 * q + 2]);
+                            t[4 * q + 3] = fmaf(-l4.w, xj, t[4 * q + 3]);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < kBB; ++r) {
+                if (r < ib) {
+                    float sres = t[r];
+#pragma unroll
+                    for (int l = 0; l < r; ++l) sres = fmaf(-Pt[(i0 + l) * kBB + r], t[l], sres);
+                    t[r] = (i0 + r < c) ? 0.f : sres * rd_s[r];
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < kBB; ++r)
+                if (r < ib) X[size_t(i0 + r) * Dp + c] = t[r];
+        }
+    }
+    __syncthreads();
+    write_wblocks(whiten, line, g, [&](int i, int j) { return X[size_t(i) * Dp + j]; });
+    if (tid == 0) status[line] = -1;
+}
+
+// ---------------------------------------------------------------------------
 // shared-memory resident factorisation (D <= 233)
 // ---------------------------------------------------------------------------
 template <typename T>
@@ -666,6 +899,7 @@ size_t factor_blk_smem(const Geometry& g) {
 size_t factor_smem(const Geometry& g, int precision) {
     if (precision == 64) return size_t(g.D) * (g.D + 1) * 8;
     if (precision == 32) return factor_blk_smem(g);
+    if (precision == 31) return (size_t(kBB) * (kBB + 1) + size_t(kBB) * (g.Dp + 4)) * 4;
     // global path: panel + diagonal block, or the inverse's row block
     size_t chol = size_t(kNB) * (kNB + 1) * 8 + size_t(std::max(g.D, 1)) * (kNB + 1) * 8;
     size_t inv = size_t(kNB) * (g.D + 1) * 8;
@@ -677,7 +911,9 @@ int factor_precision(const Geometry& g, int requested) {
     const bool blk_fits = factor_blk_smem(g) <= cap;
     const bool f64_fits = size_t(g.D) * (g.D + 1) * 8 <= cap;
     if (requested == 64 && f64_fits) return 64;
+    if (requested == 31) return 31;
     if ((requested == 32 || requested == 0) && blk_fits) return 32;
+    if (requested == 32 || requested == 0) return 31;  // blocked fp32 over global memory (large D)
     return 0;  // blocked fp64 over global memory
 }
 
@@ -695,6 +931,10 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
     } else if (precision == 64) {
         ensure_smem(factor_smem_kernel<double>, sm);
         factor_smem_kernel<double><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base);
+    } else if (precision == 31) {
+        ensure_smem(factor_big_kernel, sm);
+        factor_big_kernel<<<n_lines_total, 256, sm, st>>>(g, prior, eps0, reinterpret_cast<float*>(work), whiten,
+                                                          status, latch, line_base);
     } else {
         ensure_smem(factor_global_kernel, sm);
         factor_global_kernel<<<n_lines_total, 256, sm, st>>>(g, prior, eps0, work, whiten, status, latch,

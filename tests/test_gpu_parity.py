@@ -239,9 +239,9 @@ def test_config4_subset(pkg, oracle, no_srp):
 
 
 @pytest.mark.parametrize("cid,n_lines", [(0, 240), (1, 120)])
-@pytest.mark.parametrize("prec", [64, 32, 1])
+@pytest.mark.parametrize("prec", [64, 32, 31, 1])
 def test_factor_kernel_variants(pkg, oracle, cid, n_lines, prec):
-    """Every factor path (fp64 / fp32 shared-memory, blocked fp64 global) meets the gates."""
+    """Every factor path (fp64 / fp32 shared-memory, blocked fp32 / fp64 over L2) meets the gates."""
     spec = pkg.gen_spec(cid)
     lines, mask = pkg.gen_lines(spec, 0, n_lines)
     alpha = 0.1 if cid == 0 else 0.05
@@ -250,7 +250,7 @@ def test_factor_kernel_variants(pkg, oracle, cid, n_lines, prec):
     eng.set_factor_precision(prec)
     eng.push(lines[None], 0)
     eng.finish()
-    want = {64: 64 if cid == 0 else 0, 32: 32, 1: 0}[prec]  # fp64 D=224 does not fit smem -> blocked
+    want = {64: 64 if cid == 0 else 0, 32: 32, 31: 31, 1: 0}[prec]  # fp64 D=224 does not fit smem -> blocked
     assert eng.factor_precision() == want
     _, wu, raw_g, norm_g = eng.pop()
     raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), lines)
