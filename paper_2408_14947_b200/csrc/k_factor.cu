@@ -295,52 +295,158 @@ __global__ void __launch_bounds__(256) factor_global_kernel(Geometry g, const do
 // ---------------------------------------------------------------------------
 // factor_big: fp32 blocked Cholesky and triangular inverse for D > 233 (the
 // matrix does not fit in shared memory): A and X live in the global (L2)
-// workspace, 256 threads per line, panel width 32.  Per step: the diagonal
-// block is factored by one warp with the rows in registers (shuffles for the
-// column broadcasts), the panel rows are solved one per thread and kept
-// transposed in shared memory, and the trailing update runs 8x8 register
-// tiles (two 16-byte shared loads per 64 FMAs) with one read-modify-write of
-// the tile in L2.  The inverse goes by block rows, one column per thread.
+// workspace, 256 threads per line, panel width 32.  Cholesky step k: the
+// diagonal block is factored by one warp with the rows in registers (shuffles
+// for the column broadcasts) and inverted by the same warp (Di = L_kk^{-1},
+// which is also X's diagonal block); the panel rows become A_ik Di^T, one row
+// per thread, kept transposed in shared memory; the trailing update runs 8x8
+// register tiles (two 16-byte shared loads per 64 FMAs) with one
+// read-modify-write of the tile in L2.  The inverse is right-looking by block
+// rows with the same tiles: step k finishes X_kJ = Di T_kJ and pushes
+// T_IJ -= L_Ik X_kJ into every block row below.
 // ---------------------------------------------------------------------------
 constexpr int kBB = 32;
+constexpr int kLD = kBB + 1;
 
 __device__ __forceinline__ float rsqrt_nr(float d) {
     float rs = rsqrtf(d);
     return rs * fmaf(-0.5f * d * rs, rs, 1.5f);
 }
 
+// Di = Lkk^{-1} for one 32x32 lower block (rows/cols past the block size are identity in Lkk and
+// come out identity): lane c computes column c by forward substitution, four partial sums per row
+// split the FMA chains.  Entries above the diagonal come out exactly 0.
+__device__ __forceinline__ void tri_inv32_warp(const float* __restrict__ Lkk, float* __restrict__ Di, int lane) {
+    float col[kBB];
+#pragma unroll
+    for (int r = 0; r < kBB; ++r) {
+        float s[4] = {r == lane ? 1.f : 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int l = 0; l < r; ++l) s[l & 3] = fmaf(-Lkk[r * kLD + l], col[l], s[l & 3]);
+        col[r] = ((s[0] + s[1]) + (s[2] + s[3])) / Lkk[r * kLD + r];
+    }
+#pragma unroll
+    for (int r = 0; r < kBB; ++r) Di[r * kLD + lane] = col[r];
+}
+
+// C[rows r0.., cols 0..ncol) op= Pt^T Bk over l < 32 as 8x8 register tiles: Pt is [32][LDT]
+// (row l holds the 32-column factor block transposed), Bk is [32][ldb] (row l of the right-hand
+// block row).  A warp takes 8 row tiles x 4 column tiles: the B reads of a warp are one 128-byte
+// wavefront and the A reads two.  init_from: columns >= init_from are written (-acc), the rest
+// read-modify-written (-= acc); lower: only entries on or below the diagonal (trailing update).
+__device__ __forceinline__ void tile_update(const float* __restrict__ Pt, int LDT, const float* __restrict__ Bk,
+                                            int ldb, float* __restrict__ C, int ldc, int nr, int ncol, int init_from,
+                                            bool lower, int warp, int lane, int nwarps) {
+    const int nR = (nr + 7) / 8, nC = ncol / 8;
+    const int wR = (nR + 7) / 8, wC = (nC + 3) / 4;
+    for (int wb = warp; wb < wR * wC; wb += nwarps) {
+        const int wr = wb / wC, wc = wb - wr * wC;
+        const int R = wr * 8 + (lane >> 2), Cc = wc * 4 + (lane & 3);
+        if (R >= nR || Cc >= nC || (lower && Cc > R)) continue;
+        float acc[8][8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int jx = 0; jx < 8; ++jx) acc[i][jx] = 0.f;
+#pragma unroll 4
+        for (int l = 0; l < kBB; ++l) {
+            const float4 a0 = *reinterpret_cast<const float4*>(Pt + l * LDT + R * 8);
+            const float4 a1 = *reinterpret_cast<const float4*>(Pt + l * LDT + R * 8 + 4);
+            const float4 b0 = *reinterpret_cast<const float4*>(Bk + l * ldb + Cc * 8);
+            const float4 b1 = *reinterpret_cast<const float4*>(Bk + l * ldb + Cc * 8 + 4);
+            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int jx = 0; jx < 8; ++jx) acc[i][jx] = fmaf(av[i], bv[jx], acc[i][jx]);
+        }
+        const bool init = Cc * 8 >= init_from;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int ri = R * 8 + i;
+            if (ri >= nr) continue;
+            float4* crow = reinterpret_cast<float4*>(C + size_t(ri) * ldc + Cc * 8);
+            if (lower && Cc == R) {  // diagonal tile: lower triangle only
+                float* cr = C + size_t(ri) * ldc + Cc * 8;
+#pragma unroll
+                for (int jx = 0; jx < 8; ++jx)
+                    if (jx <= i) cr[jx] -= acc[i][jx];
+                continue;
+            }
+            float4 v0, v1;
+            if (init) {
+                v0 = make_float4(-acc[i][0], -acc[i][1], -acc[i][2], -acc[i][3]);
+                v1 = make_float4(-acc[i][4], -acc[i][5], -acc[i][6], -acc[i][7]);
+            } else {
+                v0 = crow[0];
+                v1 = crow[1];
+                v0.x -= acc[i][0], v0.y -= acc[i][1], v0.z -= acc[i][2], v0.w -= acc[i][3];
+                v1.x -= acc[i][4], v1.y -= acc[i][5], v1.z -= acc[i][6], v1.w -= acc[i][7];
+            }
+            crow[0] = v0;
+            crow[1] = v1;
+        }
+    }
+}
+
+// Load the 32-column block of rows r0..r0+nr of M (cols k0..k0+31) transposed into Pt[c][rr]
+// (rows up to roundup8(nr) zero-padded).  Lanes take 4 rows x 8 columns: 32-byte row segments
+// from L2 and conflict-free shared stores for any LDT = 4 (mod 8).
+__device__ __forceinline__ void load_panel_t(float* __restrict__ Pt, int LDT, const float* __restrict__ M, int ldm,
+                                             int r0, int k0, int nr, int tid, int nt) {
+    const int nr8 = (nr + 7) & ~7;
+    for (int idx = tid; idx < nr8 * kBB; idx += nt) {
+        const int q = idx >> 5, ln = idx & 31;
+        const int c = (q & 3) * 8 + (ln & 7), rr = (q >> 2) * 4 + (ln >> 3);
+        Pt[c * LDT + rr] = rr < nr ? M[size_t(r0 + rr) * ldm + k0 + c] : 0.f;
+    }
+}
+
 __global__ void __launch_bounds__(256) factor_big_kernel(Geometry g, const double* __restrict__ prior, double eps0,
                                                          float* __restrict__ work, float* __restrict__ whiten,
                                                          int* __restrict__ status, int* __restrict__ latch,
-                                                         int line_base) {
+                                                         int line_base, bool xk_smem) {
     extern __shared__ __align__(16) float fsm[];
     __shared__ int s_fail;
-    __shared__ float rd_s[kBB];
     const int line = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
-    const int lane = tid & 31, warp = tid >> 5;
+    const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
     const int D = g.D, Dp = g.Dp;
-    const int LDT = Dp + 4;                  // row stride of the transposed panel / L row block
+    const int LDT = Dp + 4;                  // row stride of the transposed panels / staged block rows
     float* A = work + size_t(line) * 2 * Dp * Dp;
     float* X = A + size_t(Dp) * Dp;
     float* Lkk = fsm;                        // [32][33]
-    float* Pt = fsm + kBB * (kBB + 1);       // [32][LDT]: panel (transposed) / inverse: L row block (transposed)
+    float* Di = Lkk + kBB * kLD;             // [32][33] L_kk^{-1}
+    float* Pt = Di + kBB * kLD;              // [32][LDT]: panel / L column block (transposed), T_k staging
+    float* Xk = Pt + kBB * LDT;              // [32][LDT]: finished X block row (xk_smem)
     const double* K = prior + size_t(line) * g.SE + D;
     const int ntri = D * (D + 1) / 2;
     double eps = eps0;
     int fail = -1;
     while (true) {
-        {   // fill the lower triangle (packed fp64 K -> fp32 A), incremental (i, j)
+        {   // fill the lower triangle (packed fp64 K -> fp32 A), 8 loads in flight per thread
             int i = int((sqrtf(8.f * tid + 1.f) - 1.f) * 0.5f), j;
             while (i * (i + 1) / 2 > tid) --i;
             while ((i + 1) * (i + 2) / 2 <= tid) ++i;
             j = tid - i * (i + 1) / 2;
-            for (int idx = tid; idx < ntri; idx += nt) {
-                A[size_t(i) * Dp + j] = float(__ldg(K + idx) + (i == j ? eps : 0.0));
-                j += nt;
-                while (j > i) {
-                    j -= i + 1;
-                    ++i;
+            for (int idx = tid; idx < ntri; idx += 8 * nt) {
+                double kv[8];
+                int iu[8], ju[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    iu[u] = i;
+                    ju[u] = j;
+                    kv[u] = idx + u * nt < ntri ? __ldg(K + idx + u * nt) : 0.0;
+                    j += nt;
+                    while (j > i) {
+                        j -= i + 1;
+                        ++i;
+                    }
                 }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (idx + u * nt < ntri)
+                        A[size_t(iu[u]) * Dp + ju[u]] = float(kv[u] + (iu[u] == ju[u] ? eps : 0.0));
             }
         }
         __syncthreads();
@@ -349,7 +455,7 @@ __global__ void __launch_bounds__(256) factor_big_kernel(Geometry g, const doubl
             const int kb = min(kBB, D - k0);
             for (int idx = tid; idx < kBB * kBB; idx += nt) {
                 const int r = idx >> 5, c = idx & 31;
-                Lkk[r * (kBB + 1) + c] = (r < kb && c <= r) ? A[size_t(k0 + r) * Dp + k0 + c] : 0.f;
+                Lkk[r * kLD + c] = r < kb ? (c <= r ? A[size_t(k0 + r) * Dp + k0 + c] : 0.f) : (r == c ? 1.f : 0.f);
             }
             if (tid == 0) s_fail = -1;
             __syncthreads();
@@ -358,7 +464,7 @@ __global__ void __launch_bounds__(256) factor_big_kernel(Geometry g, const doubl
                 // the trailing entries of every row with the column's values from their lanes
                 float row[kBB];
 #pragma unroll
-                for (int c = 0; c < kBB; ++c) row[c] = Lkk[lane * (kBB + 1) + c];
+                for (int c = 0; c < kBB; ++c) row[c] = Lkk[lane * kLD + c];
                 int f = -1;
 #pragma unroll
                 for (int jj = 0; jj < kBB; ++jj) {
@@ -370,7 +476,6 @@ __global__ void __launch_bounds__(256) factor_big_kernel(Geometry g, const doubl
                             const float rs = rsqrt_nr(d);
                             if (lane == jj) {
                                 row[jj] = d * rs;
-                                rd_s[jj] = rs;
                             } else if (lane > jj) {
                                 row[jj] *= rs;
                             }
@@ -383,76 +488,56 @@ __global__ void __launch_bounds__(256) factor_big_kernel(Geometry g, const doubl
                     }
                 }
                 if (lane == 0) s_fail = f;
-                if (f < 0 && lane < kb) {
+                if (f < 0) {  // f is warp-uniform (the pivot is broadcast)
+                    if (lane < kb) {
 #pragma unroll
-                    for (int c = 0; c < kBB; ++c) {
-                        const float v = c <= lane ? row[c] : 0.f;
-                        Lkk[lane * (kBB + 1) + c] = v;
-                        if (c <= lane) A[size_t(k0 + lane) * Dp + k0 + c] = v;
+                        for (int c = 0; c < kBB; ++c) {
+                            const float v = c <= lane ? row[c] : 0.f;
+                            Lkk[lane * kLD + c] = v;
+                            if (c <= lane) A[size_t(k0 + lane) * Dp + k0 + c] = v;
+                        }
                     }
+                    __syncwarp();
+                    tri_inv32_warp(Lkk, Di, lane);
+                    __syncwarp();
+                    if (lane < kb)  // X_kk = Di (zeros above the diagonal)
+                        for (int r = 0; r < kb; ++r) X[size_t(k0 + r) * Dp + k0 + lane] = Di[r * kLD + lane];
                 }
             }
             __syncthreads();
             fail = s_fail;
             if (fail >= 0) break;
-            // panel: L_ik = A_ik L_kk^{-T}, one row per thread, kept transposed in shared memory
-            const int r0 = k0 + kb, nr = D - r0;
+            // panel: L_ik = A_ik L_kk^{-T} = A_ik Di^T, one row per thread, kept transposed in shared memory
+            const int r0 = k0 + kb, nr = D - r0;  // nr > 0 implies kb == 32
             for (int rr = tid; rr < nr; rr += nt) {
-                float* arow = A + size_t(r0 + rr) * Dp + k0;
-                float x[kBB];
+                float4* arow = reinterpret_cast<float4*>(A + size_t(r0 + rr) * Dp + k0);
+                float av[kBB], x[kBB];
+#pragma unroll
+                for (int q = 0; q < kBB / 4; ++q) {
+                    const float4 v = arow[q];
+                    av[4 * q] = v.x, av[4 * q + 1] = v.y, av[4 * q + 2] = v.z, av[4 * q + 3] = v.w;
+                }
 #pragma unroll
                 for (int c = 0; c < kBB; ++c) {
-                    if (c < kb) {
-                        float s = arow[c];
+                    float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-                        for (int l = 0; l < c; ++l) s = fmaf(-x[l], Lkk[c * (kBB + 1) + l], s);
-                        x[c] = s * rd_s[c];
-                        arow[c] = x[c];
-                        Pt[c * LDT + rr] = x[c];
-                    } else {
-                        Pt[c * LDT + rr] = 0.f;
+                    for (int l = 0; l <= c; ++l) {
+                        if (l & 1) s1 = fmaf(av[l], Di[c * kLD + l], s1);
+                        else s0 = fmaf(av[l], Di[c * kLD + l], s0);
                     }
+                    x[c] = s0 + s1;
+                    Pt[c * LDT + rr] = x[c];
                 }
+#pragma unroll
+                for (int q = 0; q < kBB / 4; ++q) arow[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
             }
             // zero the transposed panel's padding rows so 8-row tiles read zeros
             for (int idx = tid; idx < kBB * 8; idx += nt) Pt[(idx >> 3) * LDT + nr + (idx & 7)] = 0.f;
             __syncthreads();
-            // trailing update A22 -= P P^T over the lower triangle, 8x8 register tiles
-            const int n8 = (nr + 7) / 8;
-            const int ntile = n8 * (n8 + 1) / 2;
-            for (int tix = tid; tix < ntile; tix += nt) {
-                int R = int((sqrtf(8.f * tix + 1.f) - 1.f) * 0.5f);
-                while (R * (R + 1) / 2 > tix) --R;
-                while ((R + 1) * (R + 2) / 2 <= tix) ++R;
-                const int C = tix - R * (R + 1) / 2;
-                float acc[8][8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-#pragma unroll
-                    for (int jx = 0; jx < 8; ++jx) acc[i][jx] = 0.f;
-                for (int l = 0; l < kb; ++l) {
-                    const float4 a0 = *reinterpret_cast<const float4*>(Pt + l * LDT + R * 8);
-                    const float4 a1 = *reinterpret_cast<const float4*>(Pt + l * LDT + R * 8 + 4);
-                    const float4 b0 = *reinterpret_cast<const float4*>(Pt + l * LDT + C * 8);
-                    const float4 b1 = *reinterpret_cast<const float4*>(Pt + l * LDT + C * 8 + 4);
-                    const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-                    for (int i = 0; i < 8; ++i)
-#pragma unroll
-                        for (int jx = 0; jx < 8; ++jx) acc[i][jx] = fmaf(av[i], bv[jx], acc[i][jx]);
-                }
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int ri = R * 8 + i;
-                    if (ri < nr) {
-                        float* arow = A + size_t(r0 + ri) * Dp + r0 + C * 8;
-#pragma unroll
-                        for (int jx = 0; jx < 8; ++jx)
-                            if (C * 8 + jx <= ri) arow[jx] -= acc[i][jx];
-                    }
-                }
-            }
+            // trailing update A22 -= P P^T over the lower triangle
+            if (nr > 0)
+                tile_update(Pt, LDT, Pt, LDT, A + size_t(r0) * Dp + r0, Dp, nr, (nr + 7) & ~7, 1 << 30, true, warp,
+                            lane, nw);
             __syncthreads();
         }
         if (fail < 0) break;
@@ -471,53 +556,49 @@ __global__ void __launch_bounds__(256) factor_big_kernel(Geometry g, const doubl
         }
         return;
     }
-    // X = L^{-1} by block rows: X_I = L_II^{-1} (E_I - sum_{J<I} L_IJ X_J), one column per thread
-    for (int i0 = 0; i0 < D; i0 += kBB) {
-        const int ib = min(kBB, D - i0), ncol = i0 + ib;
+    // X = L^{-1}, right-looking by block rows.  Before step k, X's block row k holds
+    // T_kJ = -sum_{m<k} L_km X_mJ (J < k) and X_kk = Di (written by the factor); step k finishes
+    // X_kJ = Di T_kJ and pushes T_IJ -= L_Ik X_kJ into every block row I > k.
+    for (int k0 = 0; k0 < D; k0 += kBB) {
+        const int kb = min(kBB, D - k0), r0 = k0 + kb, nr = D - r0;
         __syncthreads();
-        for (int idx = tid; idx < kBB * ncol; idx += nt) {  // L row block, transposed: Pt[j][r] = L[i0+r][j]
-            const int j = idx / kBB, r = idx - j * kBB;
-            Pt[j * kBB + r] = (r < ib && j <= i0 + r) ? A[size_t(i0 + r) * Dp + j] : 0.f;
+        for (int idx = tid; idx < kBB * kBB; idx += nt) {
+            const int r = idx >> 5, c = idx & 31;
+            Di[r * kLD + c] = (r < kb && c < kb) ? X[size_t(k0 + r) * Dp + k0 + c] : 0.f;
         }
-        if (tid < kBB) rd_s[tid] = tid < ib ? 1.f / A[size_t(i0 + tid) * Dp + i0 + tid] : 0.f;
+        for (int r = warp; r < kBB; r += nw)
+            for (int j = lane; j < k0; j += 32) Pt[r * LDT + j] = r < kb ? X[size_t(k0 + r) * Dp + j] : 0.f;
         __syncthreads();
-        for (int c = tid; c < ncol; c += nt) {
+        float* xk = xk_smem ? Xk : X + size_t(k0) * Dp;
+        const int ldx = xk_smem ? LDT : Dp;
+        for (int j = tid; j < k0; j += nt) {  // X_kJ = Di T_kJ, one column per thread
             float t[kBB];
 #pragma unroll
-            for (int r = 0; r < kBB; ++r) t[r] = (i0 + r == c) ? 1.f : 0.f;
-            // X[j][c] = 0 for j < c; the L2 loads of X go out 8 at a time ahead of their FMAs
-            for (int j0 = c; j0 < i0; j0 += 8) {
-                float xv[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) xv[u] = (j0 + u < i0) ? X[size_t(j0 + u) * Dp + c] : 0.f;
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (j0 + u < i0) {
-                        const float xj = xv[u];
-                        const float4* lt = reinterpret_cast<const float4*>(Pt + (j0 + u) * kBB);
-#pragma unroll
-                        for (int q = 0; q < kBB / 4; ++q) {
-                            const float4 l4 = lt[q];
-                            t[4 * q] = fmaf(-l4.x, xj, t[4 * q]);
-                            t[4 * q + 1] = fmaf(-l4.y, xj, t[4 * q + 1]);
-                            t[4 * q + 2] = fmaf(-l4.z, xj, t[4 * q + 2]);
-                            t[4 * q + 3] = fmaf(-l4.w, xj, t[4 * q + 3]);
-                        }
-                    }
-                }
-            }
+            for (int l = 0; l < kBB; ++l) t[l] = Pt[l * LDT + j];
 #pragma unroll
             for (int r = 0; r < kBB; ++r) {
-                if (r < ib) {
-                    float sres = t[r];
+                float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-                    for (int l = 0; l < r; ++l) sres = fmaf(-Pt[(i0 + l) * kBB + r], t[l], sres);
-                    t[r] = (i0 + r < c) ? 0.f : sres * rd_s[r];
+                for (int l = 0; l <= r; ++l) {
+                    if (l & 1) s1 = fmaf(Di[r * kLD + l], t[l], s1);
+                    else s0 = fmaf(Di[r * kLD + l], t[l], s0);
+                }
+                if (r < kb) {
+                    if (xk_smem) Xk[r * LDT + j] = s0 + s1;
+                    X[size_t(k0 + r) * Dp + j] = s0 + s1;
                 }
             }
-#pragma unroll
-            for (int r = 0; r < kBB; ++r)
-                if (r < ib) X[size_t(i0 + r) * Dp + c] = t[r];
+        }
+        if (xk_smem)
+            for (int idx = tid; idx < kBB * kBB; idx += nt) {
+                const int r = idx >> 5, c = idx & 31;
+                Xk[r * LDT + k0 + c] = Di[r * kLD + c];
+            }
+        if (nr > 0) {
+            __syncthreads();  // T_k staging read out of Pt
+            load_panel_t(Pt, LDT, A, Dp, r0, k0, nr, tid, nt);
+            __syncthreads();
+            tile_update(Pt, LDT, xk, ldx, X + size_t(r0) * Dp, Dp, nr, k0 + kb, k0, false, warp, lane, nw);
         }
     }
     __syncthreads();
@@ -896,10 +977,14 @@ size_t factor_blk_smem(const Geometry& g) {
     return (size_t(g.nb) * (g.nb + 1) / 2 + g.nb + 1) * 64 * 4;  // packed blocks + Lc + Dinv
 }
 
+// factor_big: Lkk + Di, the transposed panel, and (when it fits) the finished X block row
+size_t factor_big_smem(const Geometry& g, bool xk) { return (2 * size_t(kBB) * kLD + (xk ? 2 : 1) * size_t(kBB) * (g.Dp + 4)) * 4; }
+bool factor_big_xk(const Geometry& g) { return factor_big_smem(g, true) <= 220 * 1024; }
+
 size_t factor_smem(const Geometry& g, int precision) {
     if (precision == 64) return size_t(g.D) * (g.D + 1) * 8;
     if (precision == 32) return factor_blk_smem(g);
-    if (precision == 31) return (size_t(kBB) * (kBB + 1) + size_t(kBB) * (g.Dp + 4)) * 4;
+    if (precision == 31) return factor_big_smem(g, factor_big_xk(g));
     // global path: panel + diagonal block, or the inverse's row block
     size_t chol = size_t(kNB) * (kNB + 1) * 8 + size_t(std::max(g.D, 1)) * (kNB + 1) * 8;
     size_t inv = size_t(kNB) * (g.D + 1) * 8;
@@ -911,9 +996,10 @@ int factor_precision(const Geometry& g, int requested) {
     const bool blk_fits = factor_blk_smem(g) <= cap;
     const bool f64_fits = size_t(g.D) * (g.D + 1) * 8 <= cap;
     if (requested == 64 && f64_fits) return 64;
-    if (requested == 31) return 31;
+    const bool big_fits = factor_big_smem(g, false) <= cap;
+    if (requested == 31 && big_fits) return 31;
     if ((requested == 32 || requested == 0) && blk_fits) return 32;
-    if (requested == 32 || requested == 0) return 31;  // blocked fp32 over global memory (large D)
+    if ((requested == 32 || requested == 0 || requested == 31) && big_fits) return 31;  // fp32 over L2 (large D)
     return 0;  // blocked fp64 over global memory
 }
 
@@ -934,7 +1020,7 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
     } else if (precision == 31) {
         ensure_smem(factor_big_kernel, sm);
         factor_big_kernel<<<n_lines_total, 256, sm, st>>>(g, prior, eps0, reinterpret_cast<float*>(work), whiten,
-                                                          status, latch, line_base);
+                                                          status, latch, line_base, factor_big_xk(g));
     } else {
         ensure_smem(factor_global_kernel, sm);
         factor_global_kernel<<<n_lines_total, 256, sm, st>>>(g, prior, eps0, work, whiten, status, latch,
