@@ -13,6 +13,7 @@
 //   factor_global_kernel (1, and any D beyond the above)  blocked (panel 32)
 //       fp64 over an L2-resident global workspace.
 #include <algorithm>
+#include <cstdlib>
 
 #include "erx_common.cuh"
 #include "i8_common.cuh"
@@ -49,9 +50,8 @@ __device__ __forceinline__ void write_wblocks(float* __restrict__ whiten, int li
 template <typename ElPtr>
 __device__ void write_wplanes(unsigned char* __restrict__ planes, int line, const Geometry& g, ElPtr el,
                               const double* __restrict__ stats, const double* __restrict__ prior,
-                              const float* __restrict__ vmax) {
-    __shared__ float isc[128];
-    __shared__ double dcs[128];
+                              const float* __restrict__ vmax, float* isc, double* dcs) {
+    // isc / dcs: 128 floats / 128 doubles of the caller's shared memory
     const int tid = threadIdx.x, nt = blockDim.x, D = g.D;
     for (int d = tid; d < 128; d += nt) {
         float v = 0.f;
@@ -87,22 +87,25 @@ __device__ void write_wplanes(unsigned char* __restrict__ planes, int line, cons
         const float r = (mx > 0.f && mx <= 3.402823466e38f) ? i8::kR / mx : 0.f;
         invr[i] = r > 0.f ? 256.f / r : 0.f;
         wdc[i] = float((cr[0] + cr[1]) + (cr[2] + cr[3]));
+        const int nrun = i < D ? i / 16 + 1 : 0;  // runs past the diagonal (or padding rows) are all-zero digits
         for (int run = 0; run < 8; ++run) {
-            uint32_t w[3][4];
+            uint32_t w[3][4] = {{0u, 0u, 0u, 0u}, {0u, 0u, 0u, 0u}, {0u, 0u, 0u, 0u}};
+            if (run < nrun) {
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-                const int j0 = run * 16 + q4 * 4;
-                float4 w4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (i < D && j0 <= i) w4 = *reinterpret_cast<const float4*>(el(i, j0));
-                const float wr[4] = {w4.x, w4.y, w4.z, w4.w};
-                uint32_t u[4];
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    const int j0 = run * 16 + q4 * 4;
+                    float4 w4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (j0 <= i) w4 = *reinterpret_cast<const float4*>(el(i, j0));
+                    const float wr[4] = {w4.x, w4.y, w4.z, w4.w};
+                    uint32_t u[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int j = j0 + e;
-                    const float wv = (i < D && j <= i) ? wr[e] * isc[j] : 0.f;
-                    u[e] = i8::quant_u(wv, r);
+                    for (int e = 0; e < 4; ++e) {
+                        const int j = j0 + e;
+                        const float wv = j <= i ? wr[e] * isc[j] : 0.f;
+                        u[e] = i8::quant_u(wv, r);
+                    }
+                    i8::pack_digits(u, w[0][q4], w[1][q4], w[2][q4]);
                 }
-                i8::pack_digits(u, w[0][q4], w[1][q4], w[2][q4]);
             }
             const uint32_t off = tc::kmajor_off_s8(i, run * 16);
 #pragma unroll
@@ -685,12 +688,16 @@ __global__ void __launch_bounds__(256) factor_smem_kernel(Geometry g, const doub
 
 // ---------------------------------------------------------------------------
 // fp32 blocked factorisation in shared memory (default for D <= 233): the
-// same 8x8 block grid as the stats / score kernels.  Cholesky: per block
-// column k, one warp factors the 8x8 diagonal block, the panel below is
-// solved row-parallel, and the trailing update runs one 8x8 block pair per
-// thread with register tiles (0.4 shared-memory accesses per FMA instead of
-// 3).  The inverse is computed in place by block rows with the same tiles.
-// ~7 barriers per block step instead of 5 per scalar step.
+// same 8x8 block grid as the stats / score kernels, Cholesky and inverse
+// merged into ONE right-looking sweep over the block columns (two barriers
+// per step).  Step k, with L_kk's inverse Di already in block (k, k):
+//   (b) panel rows: L_Ik = A_Ik Di^T (kept in Lc), and block (I, k) becomes
+//       T_Ik = -L_Ik Di; row finalisation: X_kJ = Di T_kJ (J < k);
+//   (c) Cholesky trailing update A_IJ -= L_Ik L_Jk^T (k < J <= I) and inverse
+//       update T_IJ -= L_Ik X_kJ (J < k), one block row per thread; the eight
+//       lanes that finish block (k+1, k+1) factor and invert it in registers
+//       (8-wide shuffles) for the next step.
+// At the end every block (I, J) holds X_IJ, X = L^{-1}.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void ld8(const float* p, float* v) {
     const float4 a = *reinterpret_cast<const float4*>(p);
@@ -701,6 +708,45 @@ __device__ __forceinline__ void ld8(const float* p, float* v) {
 __device__ __forceinline__ void st8(float* p, const float* v) {
     *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
     *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+// Eight lanes (one aligned 8-lane group, lane gl holding row gl of an updated diagonal block in
+// row[]) factor the block (Cholesky, 1/sqrt from MUFU.RSQ + one Newton step) and invert the
+// factor (lane c: column c by forward substitution).  Di goes to blk (row-major, zeros above the
+// diagonal), Di^T to dit.  Returns the first non-positive pivot (k0 + j) or -1, group-uniform.
+__device__ __forceinline__ int diag_factor8(float (&row)[kBlk], unsigned gmask, int gl, int k0, float* blk,
+                                            float* dit) {
+    int f = -1;
+    float rd[kBlk];
+#pragma unroll
+    for (int j = 0; j < kBlk; ++j) {
+        float d = __shfl_sync(gmask, row[j], j, kBlk);
+        if (!(d > 0.f)) {
+            if (f < 0) f = k0 + j;
+            d = 1.f;
+        }
+        const float rs = rsqrt_nr(d);
+        rd[j] = rs;
+        if (gl == j) row[j] = d * rs;
+        else if (gl > j) row[j] *= rs;
+#pragma unroll
+        for (int c = j + 1; c < kBlk; ++c) {
+            const float lcj = __shfl_sync(gmask, row[j], c, kBlk);
+            if (gl >= c) row[c] = fmaf(-row[j], lcj, row[c]);
+        }
+    }
+    float col[kBlk];
+#pragma unroll
+    for (int r = 0; r < kBlk; ++r) {
+        float s = (r == gl) ? 1.f : 0.f;
+#pragma unroll
+        for (int l = 0; l < r; ++l) s = fmaf(-__shfl_sync(gmask, row[l], r, kBlk), col[l], s);
+        col[r] = s * rd[r];  // 0 for r < gl
+    }
+#pragma unroll
+    for (int r = 0; r < kBlk; ++r) blk[r * kBlk + gl] = col[r];
+    st8(dit + gl * kBlk, col);
+    return f;
 }
 
 __global__ void __launch_bounds__(256) factor_blk_kernel(Geometry g, const double* __restrict__ prior, double eps0,
@@ -717,15 +763,17 @@ __global__ void __launch_bounds__(256) factor_blk_kernel(Geometry g, const doubl
     float* A = reinterpret_cast<float*>(smem);
     auto BP = [&](int I, int J) { return A + (I * (I + 1) / 2 + J) * 64; };
     auto EL = [&](int i, int j) { return BP(i >> 3, j >> 3) + (i & 7) * kBlk + (j & 7); };
-    float* Lc = A + size_t(nb * (nb + 1) / 2) * 64;  // [nb][64]: copy of a block column (inverse)
-    float* Dinv = Lc + size_t(nb) * 64;         // [64]: inverse of a diagonal block
+    float* Lc = A + size_t(nb * (nb + 1) / 2) * 64;  // [nb][64]: the current panel L_Ik
+    float* DiT = Lc + size_t(nb) * 64;          // [64]: Di^T of the current diagonal block
     const int line = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
-    const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    const int lane = tid & 31, gl = lane & 7;
+    const unsigned gmask = 0xffu << (lane & 24);
     const double* K = prior + size_t(line) * g.SE + D;
     double eps = eps0;
     int fail;
     const int ntri = D * (D + 1) / 2;
     while (true) {
+        if (tid == 0) s_fail = -1;
         if (kblk) {
             // fill from the scan's fp32 block image: a straight 16-byte copy, then + eps on the
             // diagonal and zeros above it inside the diagonal blocks
@@ -743,9 +791,8 @@ __global__ void __launch_bounds__(256) factor_blk_kernel(Geometry g, const doubl
                 else if (c == r && kk * kBlk + r < D) *p += fe;
             }
         } else {
-        // fill: coalesced reads of the packed fp64 K, 16 loads in flight per thread (the (i, j) of
-        // idx + nt follows from (i, j) of idx incrementally), padding = identity
-        {
+            // fill: coalesced reads of the packed fp64 K, 16 loads in flight per thread (the (i, j) of
+            // idx + nt follows from (i, j) of idx incrementally)
             int i = int((sqrtf(8.f * tid + 1.f) - 1.f) * 0.5f), j;
             while (i * (i + 1) / 2 > tid) --i;
             while ((i + 1) * (i + 2) / 2 <= tid) ++i;
@@ -770,89 +817,113 @@ __global__ void __launch_bounds__(256) factor_blk_kernel(Geometry g, const doubl
                     if (base + u * nt < ntri) *EL(ii[u], jj[u]) = float(v[u] + (ii[u] == jj[u] ? eps : 0.0));
             }
         }
-        }
         __syncthreads();
-        for (int i = D + tid; i < Dp; i += nt)
+        for (int i = D + tid; i < Dp; i += nt)  // padding dims: identity
             for (int j = 0; j <= i; ++j) *EL(i, j) = (i == j) ? 1.f : 0.f;
         __syncthreads();
-        fail = -1;
-        for (int k = 0; k < nb; ++k) {
-            const int k0 = k * kBlk;
-            float* Bk = BP(k, k);
-            // (a) every thread factors the 8x8 diagonal block in registers (redundant, no barrier;
-            //     the pivot test is uniform across the CTA)
-            float L[kBlk][kBlk], rd[kBlk];
+        if (tid < kBlk) {  // block (0, 0)
+            float row[kBlk];
+            ld8(BP(0, 0) + gl * kBlk, row);
+            const int f = diag_factor8(row, gmask, gl, 0, BP(0, 0), DiT);
+            if (gl == 0 && f >= 0) s_fail = f;
+        }
+        __syncthreads();
+        fail = s_fail;
+        for (int k = 0; k < nb && fail < 0; ++k) {
+            const float* Di = BP(k, k);
+            // (b) panel rows I > k (tasks 0 ..) and finalisation of block row k (J < k)
+            const int npan = (nb - k - 1) * kBlk;
+            for (int q = tid; q < npan + k * kBlk; q += nt) {
+                const int r = q & 7;
+                if (q < npan) {
+                    const int I = k + 1 + (q >> 3);
+                    float* blk = BP(I, k) + r * kBlk;
+                    float a[kBlk], x[kBlk], t[kBlk];
+                    ld8(blk, a);
 #pragma unroll
-            for (int r = 0; r < kBlk; ++r) ld8(Bk + r * kBlk, L[r]);
+                    for (int c = 0; c < kBlk; ++c) {
+                        float d[kBlk];
+                        ld8(Di + c * kBlk, d);
+                        float s = 0.f;
 #pragma unroll
-            for (int j = 0; j < kBlk; ++j) {
-                float d = L[j][j];
-#pragma unroll
-                for (int l = 0; l < j; ++l) d -= L[j][l] * L[j][l];
-                if (!(d > 0.f) && fail < 0) fail = k0 + j;
-                // 1/sqrt(d) from MUFU.RSQ plus one Newton step (~1 ulp), s = d / sqrt(d)
-                float rs = rsqrtf(d);
-                rs = rs * fmaf(-0.5f * d * rs, rs, 1.5f);
-                const float s = d * rs;
-                L[j][j] = s;
-                rd[j] = rs;
-#pragma unroll
-                for (int r = j + 1; r < kBlk; ++r) {
-                    float v = L[r][j];
-#pragma unroll
-                    for (int l = 0; l < j; ++l) v -= L[r][l] * L[j][l];
-                    L[r][j] = v * rd[j];
-                }
-            }
-            if (fail >= 0) break;
-            // (b) panel: L_Ik = A_Ik L_kk^{-T}, one row per thread, L_kk from registers
-            for (int i = k0 + kBlk + tid; i < Dp; i += nt) {
-                float* row = BP(i >> 3, k) + (i & 7) * kBlk;
-                float a[kBlk], x[kBlk];
-                ld8(row, a);
-#pragma unroll
-                for (int c = 0; c < kBlk; ++c) {
-                    float s = a[c];
-#pragma unroll
-                    for (int l = 0; l < c; ++l) s -= x[l] * L[c][l];
-                    x[c] = s * rd[c];
-                }
-                st8(row, x);
-            }
-            __syncthreads();
-            // the factored diagonal block (lower part) for the inverse phase: written only after the
-            // barrier, since every thread reads the unfactored block in (a)
-            if (warp == nw - 1) {
-#pragma unroll
-                for (int r = 0; r < kBlk; ++r)
-                    if (lane == r) {
-#pragma unroll
-                        for (int c = 0; c <= r; ++c) Bk[r * kBlk + c] = L[r][c];
+                        for (int l = 0; l <= c; ++l) s = fmaf(a[l], d[l], s);
+                        x[c] = s;
                     }
-            }
-            // (c) trailing update A_IJ -= L_Ik L_Jk^T, k < J <= I < nb: one block ROW per thread (task =
-            //     pair x row), so the step's latency is 64 FMAs instead of 512 and all threads have work
-            const int m = nb - k - 1;
-            const int ntask = m * (m + 1) / 2 * kBlk;
-            for (int q = tid; q < ntask; q += nt) {
-                const int pq = q >> 3, r = q & 7;
-                int Ir = int((sqrtf(8.f * pq + 1.f) - 1.f) * 0.5f);
-                while (Ir * (Ir + 1) / 2 > pq) --Ir;
-                while ((Ir + 1) * (Ir + 2) / 2 <= pq) ++Ir;
-                const int I = k + 1 + Ir, J = k + 1 + (pq - Ir * (Ir + 1) / 2);
-                float a[kBlk], acc[kBlk];
-                ld8(BP(I, k) + r * kBlk, a);
-                ld8(BP(I, J) + r * kBlk, acc);
+                    st8(Lc + I * 64 + r * kBlk, x);
 #pragma unroll
-                for (int c = 0; c < kBlk; ++c) {
-                    float b[kBlk];
-                    ld8(BP(J, k) + c * kBlk, b);  // broadcast: the 8 threads of a pair share it
+                    for (int c = 0; c < kBlk; ++c) {
+                        float d[kBlk];
+                        ld8(DiT + c * kBlk, d);
+                        float s = 0.f;
 #pragma unroll
-                    for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], b[l], acc[c]);
+                        for (int l = c; l < kBlk; ++l) s = fmaf(x[l], d[l], s);
+                        t[c] = -s;
+                    }
+                    st8(blk, t);
+                } else {
+                    const int J = (q - npan) >> 3;
+                    float* blk = BP(k, J);
+                    float tr[kBlk][kBlk], acc[kBlk], d[kBlk];
+#pragma unroll
+                    for (int l = 0; l < kBlk; ++l) ld8(blk + l * kBlk, tr[l]);
+                    ld8(Di + r * kBlk, d);
+#pragma unroll
+                    for (int c = 0; c < kBlk; ++c) acc[c] = 0.f;
+#pragma unroll
+                    for (int l = 0; l < kBlk; ++l)
+#pragma unroll
+                        for (int c = 0; c < kBlk; ++c) acc[c] = fmaf(d[l], tr[l][c], acc[c]);  // d[l] = 0 for l > r
+                    __syncwarp(gmask);  // the group's reads of T_kJ precede its writes
+                    st8(blk + r * kBlk, acc);
                 }
-                st8(BP(I, J) + r * kBlk, acc);
             }
             __syncthreads();
+            // (c) trailing Cholesky pairs (I >= J > k), then inverse pairs (I > k, J < k); task = pair x row
+            const int m = nb - k - 1;
+            const int nchol = m * (m + 1) / 2 * kBlk;
+            for (int q = tid; q < nchol + m * k * kBlk; q += nt) {
+                const int r = q & 7;
+                float a[kBlk], acc[kBlk];
+                if (q < nchol) {
+                    const int pq = q >> 3;
+                    int Ir = int((sqrtf(8.f * pq + 1.f) - 1.f) * 0.5f);
+                    while (Ir * (Ir + 1) / 2 > pq) --Ir;
+                    while ((Ir + 1) * (Ir + 2) / 2 <= pq) ++Ir;
+                    const int I = k + 1 + Ir, J = k + 1 + (pq - Ir * (Ir + 1) / 2);
+                    float* blk = BP(I, J) + r * kBlk;
+                    ld8(Lc + I * 64 + r * kBlk, a);
+                    ld8(blk, acc);
+#pragma unroll
+                    for (int c = 0; c < kBlk; ++c) {
+                        float b[kBlk];
+                        ld8(Lc + J * 64 + c * kBlk, b);  // broadcast: the 8 threads of a pair share it
+#pragma unroll
+                        for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], b[l], acc[c]);
+                    }
+                    st8(blk, acc);
+                    if (pq == 0) {  // block (k+1, k+1) is final: factor + invert it for the next step
+                        const int f = diag_factor8(acc, gmask, gl, (k + 1) * kBlk, BP(k + 1, k + 1), DiT);
+                        if (gl == 0 && f >= 0) s_fail = f;
+                    }
+                } else {
+                    const int pq = (q - nchol) >> 3;
+                    const int I = k + 1 + pq / k, J = pq - (pq / k) * k;
+                    float* blk = BP(I, J) + r * kBlk;
+                    const float* xk = BP(k, J);
+                    ld8(Lc + I * 64 + r * kBlk, a);
+                    ld8(blk, acc);
+#pragma unroll
+                    for (int l = 0; l < kBlk; ++l) {
+                        float xr[kBlk];
+                        ld8(xk + l * kBlk, xr);  // broadcast across the task's 8 threads
+#pragma unroll
+                        for (int c = 0; c < kBlk; ++c) acc[c] = fmaf(-a[l], xr[c], acc[c]);
+                    }
+                    st8(blk, acc);
+                }
+            }
+            __syncthreads();
+            fail = s_fail;
         }
         if (fail < 0) break;
         const double next = eps * 10.0;
@@ -870,101 +941,9 @@ __global__ void __launch_bounds__(256) factor_blk_kernel(Geometry g, const doubl
         }
         return;
     }
-    // In-place inverse by block rows.  Before step k, block (I, J), I > k,
-    // J < k, holds T_IJ = -sum_{m<k} L_Im X_mJ; block (I, J >= k) still holds L.
-    for (int k = 0; k < nb; ++k) {
-        const int k0 = k * kBlk;
-        const float* Bk = BP(k, k);
-        // block column k below the diagonal is overwritten by this step's update: keep a copy
-        for (int idx = tid; idx < (nb - k - 1) * 64; idx += nt) {
-            const int I = k + 1 + idx / 64, rc = idx % 64;
-            Lc[I * 64 + rc] = BP(I, k)[rc];
-        }
-        // finalise block row k: X_kJ = L_kk^{-1} T_kJ (J < k), X_kk = L_kk^{-1}; the 8x8 inverse
-        // is recomputed in registers by each finalising thread (no serial phase, no barrier)
-        for (int J = tid; J <= k; J += nt) {
-            float Lr[kBlk][kBlk], Di[kBlk][kBlk], rl[kBlk];
-#pragma unroll
-            for (int r = 0; r < kBlk; ++r) {
-                ld8(Bk + r * kBlk, Lr[r]);
-                rl[r] = __frcp_rn(Lr[r][r]);
-            }
-#pragma unroll
-            for (int c = 0; c < kBlk; ++c) {
-                Di[c][c] = rl[c];
-#pragma unroll
-                for (int r = c + 1; r < kBlk; ++r) {
-                    float s = 0.f;
-#pragma unroll
-                    for (int l = c; l < r; ++l) s = fmaf(Lr[r][l], Di[l][c], s);
-                    Di[r][c] = -s * rl[r];
-                }
-#pragma unroll
-                for (int r = 0; r < c; ++r) Di[r][c] = 0.f;
-            }
-            float t[kBlk][kBlk];
-            if (J == k) {
-#pragma unroll
-                for (int r = 0; r < kBlk; ++r)
-#pragma unroll
-                    for (int c = 0; c < kBlk; ++c) t[r][c] = Di[r][c];
-            } else {
-#pragma unroll
-                for (int r = 0; r < kBlk; ++r)
-#pragma unroll
-                    for (int c = 0; c < kBlk; ++c) t[r][c] = 0.f;
-#pragma unroll
-                for (int l = 0; l < kBlk; ++l) {
-                    float srow[kBlk];
-                    ld8(BP(k, J) + l * kBlk, srow);
-#pragma unroll
-                    for (int r = l; r < kBlk; ++r)
-#pragma unroll
-                        for (int c = 0; c < kBlk; ++c) t[r][c] = fmaf(Di[r][l], srow[c], t[r][c]);
-                }
-            }
-            // X_kk goes to scratch: other finalising threads are still reading L_kk
-            float* dst = (J == k) ? Dinv : BP(k, J);
-            const int ld = kBlk;
-#pragma unroll
-            for (int r = 0; r < kBlk; ++r) st8(dst + r * ld, t[r]);
-        }
-        __syncthreads();
-        if (tid == 0)
-            for (int r = 0; r < kBlk; ++r) {
-                float row[kBlk];
-                ld8(Dinv + r * kBlk, row);
-                st8(BP(k, k) + r * kBlk, row);
-            }
-        // update block rows I > k: T_IJ -= L_Ik X_kJ (J < k), T_Ik = -L_Ik X_kk; task = block x row
-        const int ntask = (nb - k - 1) * (k + 1) * kBlk;
-        for (int q = tid; q < ntask; q += nt) {
-            const int tq = q >> 3, r = q & 7;
-            const int I = k + 1 + tq / (k + 1), J = tq % (k + 1);
-            const float* xs = (J == k) ? Dinv : BP(k, J);
-            const int xld = kBlk;
-            float a[kBlk], acc[kBlk];
-            ld8(Lc + I * 64 + r * kBlk, a);
-            if (J == k) {
-#pragma unroll
-                for (int c = 0; c < kBlk; ++c) acc[c] = 0.f;
-            } else {
-                ld8(BP(I, J) + r * kBlk, acc);
-            }
-#pragma unroll
-            for (int l = 0; l < kBlk; ++l) {
-                float xr[kBlk];
-                ld8(xs + l * xld, xr);  // broadcast across the task's 8 threads
-#pragma unroll
-                for (int c = 0; c < kBlk; ++c) acc[c] = fmaf(-a[l], xr[c], acc[c]);
-            }
-            st8(BP(I, J) + r * kBlk, acc);
-        }
-        __syncthreads();
-    }
     if (vmax) {
         write_wplanes(reinterpret_cast<unsigned char*>(whiten), line, g, [&](int i, int j) { return EL(i, j); }, stats,
-                      prior, vmax);
+                      prior, vmax, Lc, reinterpret_cast<double*>(Lc + 128));
     } else {
         write_wblocks(whiten, line, g, [&](int i, int j) { return *EL(i, j); });
     }
@@ -974,7 +953,8 @@ __global__ void __launch_bounds__(256) factor_blk_kernel(Geometry g, const doubl
 }  // namespace
 
 size_t factor_blk_smem(const Geometry& g) {
-    return (size_t(g.nb) * (g.nb + 1) / 2 + g.nb + 1) * 64 * 4;  // packed blocks + Lc + Dinv
+    // packed blocks + Lc + Di^T (the plane writer's 1.5 KB scratch reuses Lc + Di^T)
+    return (size_t(g.nb) * (g.nb + 1) / 2 + std::max(g.nb + 1, 6)) * 64 * 4;
 }
 
 // factor_big: Lkk + Di, the transposed panel, and (when it fits) the finished X block row
@@ -1011,7 +991,8 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
         ensure_smem(factor_blk_kernel, sm);
         // 64 threads per line fill the GPU with ~7 lines per SM; when a launch has fewer lines than
         // SMs (lag-0 / small windows) more threads per line shorten each line's latency instead
-        const int threads = n_lines_total >= sm_count() ? 64 : 256;
+        int threads = n_lines_total >= sm_count() ? 64 : 256;
+        if (const char* ev = getenv("ERX_FACTOR_THREADS")) threads = atoi(ev);  // EXPERIMENT
         factor_blk_kernel<<<n_lines_total, threads, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
                                                           vmax, kblk);
     } else if (precision == 64) {
