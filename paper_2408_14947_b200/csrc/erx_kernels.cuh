@@ -49,6 +49,7 @@ struct StatsLaunch {
     int npc;         // pairs per CTA
     int G;           // pixel groups per pair (threads per pair)
     int cpl;         // CTAs per line
+    int NT;          // threads per CTA
     size_t smem;     // dynamic shared memory bytes
 };
 

@@ -35,7 +35,7 @@ struct StatsArgs {
     double* stats;
 };
 
-__global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
+__global__ void __launch_bounds__(384) stats_kernel(StatsArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geometry& g = a.g;
     const StatsLaunch& sl = a.sl;
@@ -118,9 +118,8 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
             }
             __syncthreads();
             // centre in place and take the column sums (one thread per dim; fp32 per chunk)
-            for (int k = 0; k < 4; ++k) {
-                const int j = tid + k * nt;
-                if (j < g.D) {
+            for (int j = tid; j < g.D; j += nt) {
+                {
                     float* col = v + spos(j, g.nb);
                     if (c == 0) {  // centre: fp64 mean of the first n0 staged (raw) pixels of this dim
                         double s = 0.0;
@@ -144,9 +143,8 @@ __global__ void __launch_bounds__(128) stats_kernel(StatsArgs a) {
                 v[size_t(pp) * g.Dp + spos(j, g.nb)] = float(proj(g, xl + size_t(c0 + pp) * g.B, j) - double(cen[j]));
             }
             __syncthreads();
-            for (int k = 0; k < 4; ++k) {
-                const int j = tid + k * nt;
-                if (j < g.D) {
+            for (int j = tid; j < g.D; j += nt) {
+                {
                     const float* col = v + spos(j, g.nb);
                     float s = 0.f;
                     for (int pp = 0; pp < n; ++pp) s += col[size_t(pp) * g.Dp];
@@ -258,10 +256,14 @@ StatsLaunch plan_stats(const Geometry& g) {
         sl.G = 128 / sl.n_pairs;
         sl.npc = sl.n_pairs;
         sl.cpl = 1;
+        sl.NT = 128;
     } else {
+        // one thread per block pair, up to 384 threads (12 warps: the 165-register accumulators of
+        // 384 threads fill the register file) per CTA, the pairs split evenly over the line's CTAs
         sl.G = 1;
-        sl.npc = 128;
-        sl.cpl = (sl.n_pairs + 127) / 128;
+        sl.cpl = (sl.n_pairs + 383) / 384;
+        sl.npc = (sl.n_pairs + sl.cpl - 1) / sl.cpl;
+        sl.NT = (sl.npc + 31) / 32 * 32;
     }
     const size_t per_px = size_t(g.Dp) * 4 * 2;  // double buffered
     int ch = 64;
@@ -281,7 +283,7 @@ void launch_stats(const Geometry& g, const StatsLaunch& sl, const float* x, int 
         ensure_smem(stats_kernel, 200 * 1024);
     }
     StatsArgs a{g, sl, x, n_per_stream, in_stride, stats};
-    stats_kernel<<<n_lines_total * sl.cpl, 128, sl.smem, st>>>(a);
+    stats_kernel<<<n_lines_total * sl.cpl, sl.NT, sl.smem, st>>>(a);
 }
 
 }  // namespace erxk
