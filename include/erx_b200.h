@@ -10,6 +10,7 @@
  * Status codes are the reference's had::ErrorKind values (errors.hpp:12-18)
  * so a wrapper can rethrow the same exception types:
  *   ERX_OK 0, ERX_ERR_CONFIG 2 (ConfigError), ERX_ERR_DATA 3 (DataError),
+ *   ERX_ERR_METRIC 4 (MetricUndefinedError, metrics only),
  *   ERX_ERR_NUMERIC 5 (FactorizationError, pivot via erx_last_pivot),
  *   ERX_ERR_IO 6; plus ERX_ERR_DEVICE 16 for CUDA failures (no reference
  *   analogue) and ERX_ERR_STATE 17 for calls on a failed engine.
@@ -30,6 +31,7 @@ extern "C" {
 #define ERX_OK 0
 #define ERX_ERR_CONFIG 2
 #define ERX_ERR_DATA 3
+#define ERX_ERR_METRIC 4
 #define ERX_ERR_NUMERIC 5
 #define ERX_ERR_IO 6
 #define ERX_ERR_DEVICE 16
@@ -188,6 +190,23 @@ int erx_tc_selftest(erx_engine* e, const float* dA, const float* dB, int K, int 
  * (a_mn; layout strides ms / ks between 16-row M groups / 8-row K groups, descriptor lbo / sbo). */
 int erx_tc_selftest_i8(erx_engine* e, const int8_t* dA, const int8_t* dB, int K, int N, int a_mn, int ms, int ks,
                        int lbo, int sbo, int* dD);
+
+/* ---- parity-gate metrics on the device (k_metrics.cu) ----
+ * Exact ROC AUC of fp32 device scores against u8 labels (non-zero = anomaly),
+ * ties grouped into one ROC step: the AUC of had::roc_curve
+ * (metrics.hpp:25-28) / evaluate_run (metrics.hpp:54-58) over the elements
+ * with d_select[i] != 0 (NULL = all; e.g. the non-warmup pixels).  Computed
+ * from one device radix sort as an exact integer ratio.  ERX_ERR_METRIC when
+ * either class is empty (MetricUndefinedError).  npos / nneg may be NULL.
+ * stream: a cudaStream_t (NULL = legacy default stream); returns synchronised. */
+int erx_metrics_roc_auc(const float* d_scores, const uint8_t* d_labels, const uint8_t* d_select, size_t n,
+                        void* stream, double* auc, uint64_t* npos, uint64_t* nneg);
+/* Top-k set of fp32 device scores over the selected elements (the parity
+ * gates' top-1% anomaly set): d_mask[i] = 1 for the k largest
+ * (ties at the cutoff go to the lower index), else 0; *cutoff = the k-th
+ * largest score (may be NULL).  ERX_ERR_DATA when k exceeds the selection. */
+int erx_metrics_top_k(const float* d_scores, const uint8_t* d_select, size_t n, size_t k, void* stream,
+                      uint8_t* d_mask, float* cutoff);
 
 /* CUDA events on the engine stream, for callers timing device work. */
 int erx_event_record(erx_engine* e, int slot);

@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(_HERE, "liberx_b200.so")
 ERX_OK = 0
 ERX_ERR_CONFIG = 2
 ERX_ERR_DATA = 3
+ERX_ERR_METRIC = 4
 ERX_ERR_NUMERIC = 5
 ERX_ERR_IO = 6
 ERX_ERR_DEVICE = 16
@@ -96,6 +97,8 @@ SIGNATURES = {
     "erx_probe_stream": (C.c_int, [_vp, C.c_int, C.c_uint32, C.c_int, C.c_int, C.c_uint64, _dp]),
     "erx_tc_selftest": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, _vp]),
     "erx_tc_selftest_i8": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp]),
+    "erx_metrics_roc_auc": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _dp, _u64p, _u64p]),
+    "erx_metrics_top_k": (C.c_int, [_vp, _vp, C.c_size_t, C.c_size_t, _vp, _vp, _fp]),
     "erx_event_record": (C.c_int, [_vp, C.c_int]),
     "erx_event_elapsed_ms": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_float)]),
     "erx_host_alloc": (C.c_void_p, [C.c_size_t]),

@@ -66,6 +66,8 @@ def _raise(code: int, msg: str, pivot: int = -1):
         raise ConfigError(msg)
     if code == L.ERX_ERR_DATA:
         raise DataError(msg)
+    if code == L.ERX_ERR_METRIC:
+        raise MetricUndefinedError(msg)
     if code == L.ERX_ERR_NUMERIC:
         raise FactorizationError(pivot, msg)
     if code == L.ERX_ERR_IO:
