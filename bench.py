@@ -405,7 +405,54 @@ def secondary_measurements(pkg, args):
         out["latency"] = {"workload": "configs[0]: 384 px x 108 bands, window=1 (no lag), device-resident", **lat}
     except Exception as ex:
         out["latency"] = {"error": repr(ex)}
+    try:
+        out["metrics"] = metrics_measurement(pkg)
+    except Exception as ex:
+        out["metrics"] = {"error": repr(ex)}
     return out
+
+
+def metrics_measurement(pkg):
+    """Parity-gate metrics on the device at the c3 pooled size: the exact
+    tie-grouped ROC AUC and the top-1% set over 64 x (5000 - 99) x 640 non-warmup scores.
+    Synthetic stand-in scores (N(0,1), anomalies +3, 0.3% labelled; ties from fp32 rounding),
+    device-resident; CUDA events on the calling stream.  CPU reference: the oracle's roc_auc
+    (std::sort + trapezoid, 1 thread) on a 2 M-score sample."""
+    import torch
+    from paper_2408_14947_b200 import metrics
+
+    n = 64 * (5000 - 99) * 640
+    g = torch.Generator(device="cuda").manual_seed(0)
+    y = (torch.rand(n, device="cuda", generator=g) < 0.003).to(torch.uint8)
+    s = torch.randn(n, device="cuda", generator=g) + 3.0 * y.float()
+    st = torch.cuda.current_stream()
+    k = int(math.ceil(0.01 * n))
+    metrics.roc_auc(s, y, stream=st.cuda_stream)  # warm-up (allocator, module load)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record(st)
+    auc = metrics.roc_auc(s, y, stream=st.cuda_stream)
+    ev[1].record(st)
+    mask, cut = metrics.top_k(s, k, stream=st.cuda_stream)
+    ev[2].record(st)
+    torch.cuda.synchronize()
+    auc_ms, topk_ms = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+    res = {"workload": "c3 pooled non-warmup scores: 64 x 4901 lines x 640 px (synthetic stand-in)",
+           "scores": n, "auc": auc, "auc_ms": auc_ms, "auc_scores_per_s": n / (auc_ms / 1e3),
+           "top1pct_ms": topk_ms, "top1pct_k": k,
+           "algorithm": "4-pass 8-bit LSD radix sort (in-house kernels) + exact integer Mann-Whitney count"}
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle_ctypes
+        m = 2_000_000
+        hs, hy = s[:m].double().cpu().numpy(), y[:m].cpu().numpy()
+        t0 = time.perf_counter()
+        oracle_ctypes.roc_auc(hs, hy)
+        el = time.perf_counter() - t0
+        res["cpu_baseline"] = {"value": m / el, "unit": "scores/s", "cores": 1, "kind": "port",
+                               "sample": f"oracle roc_auc on the first {m} scores"}
+    except Exception as ex:
+        res["cpu_baseline"] = {"error": repr(ex)}
+    return res
 
 
 def cpu_baseline(cid, no_srp, seconds=12.0, threads=None):

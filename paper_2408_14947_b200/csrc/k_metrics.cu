@@ -21,6 +21,7 @@
 // payload; ties at the cutoff resolve to the lower index (stable sort).
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <utility>
 
 #include "erx_common.cuh"
@@ -232,23 +233,46 @@ inline unsigned blocks_for(size_t n, int t) { return unsigned((n + t - 1) / t); 
 
 // Workspace: keys/vals double-buffered (4 n words), scan flags/positions (2 n words), radix counts
 // (256 x tiles words) and scan temporaries.
+// The device buffer is cached per process (grow-only, one per device; calls serialise on a mutex)
+// so repeated evaluations do not pay cudaMalloc / cudaFree.
+struct WsCache {
+    std::mutex mu;
+    void* base[64] = {};
+    size_t bytes[64] = {};
+};
+WsCache& ws_cache() {
+    static WsCache c;
+    return c;
+}
+
 struct Ws {
     uint32_t *k0, *v0, *k1, *v1, *f, *p, *cnt, *tmp;
     unsigned long long* acc;
     void* base = nullptr;
     int ntiles = 0;
+    std::unique_lock<std::mutex> lock{ws_cache().mu};
+    cudaStream_t st = nullptr;
+    explicit Ws(cudaStream_t s) : st(s) {}
+    ~Ws() { cudaStreamSynchronize(st); }  // no work may still use the cached buffer on return
     bool alloc(size_t n) {
         ntiles = int((n + kTile - 1) / kTile);
         const size_t ncnt = size_t(256) * ntiles;
         const size_t words = 4 + 6 * n + ncnt + scan_tmp_words(std::max(n, ncnt));
-        if (cudaMalloc(&base, words * 4) != cudaSuccess) return false;
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+        WsCache& c = ws_cache();
+        if (c.bytes[dev] < words * 4) {
+            if (c.base[dev]) cudaFree(c.base[dev]);
+            c.base[dev] = nullptr;
+            c.bytes[dev] = 0;
+            if (cudaMalloc(&c.base[dev], words * 4) != cudaSuccess) return false;
+            c.bytes[dev] = words * 4;
+        }
+        base = c.base[dev];
         acc = static_cast<unsigned long long*>(base);
         uint32_t* w = static_cast<uint32_t*>(base) + 4;
         k0 = w; v0 = k0 + n; k1 = v0 + n; v1 = k1 + n; f = v1 + n; p = f + n; cnt = p + n; tmp = cnt + ncnt;
         return true;
-    }
-    ~Ws() {
-        if (base) cudaFree(base);
     }
 };
 
@@ -295,7 +319,7 @@ int erx_metrics_roc_auc(const float* d_scores, const uint8_t* d_labels, const ui
     *auc = 0.0;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (n == 0) return ERX_ERR_METRIC;
-    Ws w;
+    Ws w(st);
     if (!w.alloc(n)) return ERX_ERR_DEVICE;
     const size_t m = gather(w, d_scores, d_labels, d_select, n, false, true, st);
     if (m == 0) return ERX_ERR_METRIC;
@@ -336,7 +360,7 @@ int erx_metrics_top_k(const float* d_scores, const uint8_t* d_select, size_t n, 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (n == 0) return k == 0 ? ERX_OK : ERX_ERR_DATA;
     if (cudaMemsetAsync(d_mask, 0, n, st) != cudaSuccess) return ERX_ERR_DEVICE;
-    Ws w;
+    Ws w(st);
     if (!w.alloc(n)) return ERX_ERR_DEVICE;
     const size_t m = gather(w, d_scores, nullptr, d_select, n, true, false, st);
     if (k > m) return ERX_ERR_DATA;
