@@ -409,7 +409,41 @@ def secondary_measurements(pkg, args):
         out["metrics"] = metrics_measurement(pkg)
     except Exception as ex:
         out["metrics"] = {"error": repr(ex)}
+    try:
+        out["datagen"] = datagen_measurement(pkg)
+    except Exception as ex:
+        out["datagen"] = {"error": repr(ex)}
     return out
+
+
+def datagen_measurement(pkg):
+    """The input generator on the device vs the host generator (all host
+    threads): configs[3] lines of one stream, fp32 [n][640][108] + masks, CUDA events around
+    erx_gen_lines_device (which returns synchronised)."""
+    import torch
+
+    spec = pkg.gen_spec(3, 0)
+    n = 2048
+    out = torch.empty((n, spec.pixels, spec.bands), dtype=torch.float32, device="cuda")
+    mask = torch.empty((n, spec.pixels), dtype=torch.uint8, device="cuda")
+    pkg.gen_lines_device(spec, 0, n, out, mask)  # warm-up (module load, scratch allocation)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    pkg.gen_lines_device(spec, 0, n, out, mask, stream=st.cuda_stream)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    m = 256
+    t0 = time.perf_counter()
+    xh, _ = pkg.gen_lines(spec, 0, m)
+    el = time.perf_counter() - t0
+    xd = out[:m].cpu().numpy()
+    neq = int(np.count_nonzero(xd.view(np.int32) != xh.view(np.int32)))
+    return {"workload": f"configs[3] stream 0, lines 0..{n - 1} (640 px x 108 bands)", "lines_per_s": n / (ms / 1e3),
+            "gb_per_s_written": n * spec.pixels * spec.bands * 4 / (ms / 1e3) / 1e9,
+            "ms": ms, "host_lines_per_s": m / el, "host_threads": os.cpu_count(),
+            "values_differing_from_host": neq, "values_compared": int(xd.size)}
 
 
 def metrics_measurement(pkg):

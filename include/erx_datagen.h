@@ -48,6 +48,15 @@ int erx_gen_preset(int config_id, uint32_t stream, erx_gen_spec* out);
 int erx_gen_lines(const erx_gen_spec* spec, uint32_t first_line, uint32_t n_lines, float* out, uint8_t* mask,
                   int threads);
 
+/* The same lines generated on the device (k_datagen.cu): d_out [n][P][B] fp32 and
+ * d_mask [n][P] u8 (or NULL) in device memory, on `stream` (a cudaStream_t; NULL = the legacy
+ * default stream), returning when done.  Identical random streams and fp64 operation order as
+ * erx_gen_lines; only the last-place results of log / sin / cos may differ (fp32 values then
+ * differ by at most one ulp, rarely).  Returns 0 (ERX_OK), 2 bad spec, 3 if a Box-Muller u1 = 0
+ * draw occurred (host redraws; p = 2^-53 per pair), 16 on a CUDA error. */
+int erx_gen_lines_device(const erx_gen_spec* spec, uint32_t first_line, uint32_t n_lines, float* d_out,
+                         uint8_t* d_mask, void* stream);
+
 /* Host RNG restatement probes (had::mix_seed, had::Rng; rng.hpp:18-83), for
  * pinning against the reference's golden vectors.  kind: 0 next_u64 ->
  * u64_out, 1 uniform, 2 uniform_f32, 3 normal -> f64_out, 4 below(u64_out[i]). */

@@ -4,11 +4,11 @@ interface, as hand-written sm_100a CUDA behind a C ABI (include/erx_b200.h).
 """
 from .detector import (ConfigError, DataError, DeviceError, Engine, ErxConfig, ErxDetector, ErxState, Error,
                        FactorizationError, IoError, LineDetector, MetricUndefinedError, ScoredLine, SpectralLine,
-                       apply_threshold, gen_lines, gen_spec, generate_srp)
+                       apply_threshold, gen_lines, gen_lines_device, gen_spec, generate_srp)
 from ._lib import LIB_PATH, LibraryMissing, lib
 
 __all__ = [
     "ConfigError", "DataError", "DeviceError", "Engine", "ErxConfig", "ErxDetector", "ErxState", "Error",
     "FactorizationError", "IoError", "LineDetector", "MetricUndefinedError", "ScoredLine", "SpectralLine",
-    "apply_threshold", "gen_lines", "gen_spec", "generate_srp", "LIB_PATH", "LibraryMissing", "lib",
+    "apply_threshold", "gen_lines", "gen_lines_device", "gen_spec", "generate_srp", "LIB_PATH", "LibraryMissing", "lib",
 ]

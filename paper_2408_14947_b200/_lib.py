@@ -108,6 +108,7 @@ SIGNATURES = {
     "erx_copy": (C.c_int, [_vp, _vp, C.c_size_t, C.c_int, _vp]),
     "erx_gen_preset": (C.c_int, [C.c_int, C.c_uint32, C.POINTER(GenSpecC)]),
     "erx_gen_lines": (C.c_int, [C.POINTER(GenSpecC), C.c_uint32, C.c_uint32, _fp, _u8p, C.c_int]),
+    "erx_gen_lines_device": (C.c_int, [C.POINTER(GenSpecC), C.c_uint32, C.c_uint32, _vp, _vp, _vp]),
     "erx_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "erx_rng_probe": (None, [C.c_uint64, C.c_int, C.c_uint32, _u64p, _dp]),
 }

@@ -15,10 +15,13 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <thread>
 #include <vector>
 
 #include "../../include/erx_datagen.h"
+#include "datagen_plan.hpp"
 #include "host_rng.hpp"
 
 using erx_host::mix_seed;
@@ -126,6 +129,27 @@ Stream build(const erx_gen_spec& s) {
     return st;
 }
 
+// build() costs ~4 ms for c3 (a smooth spectrum per anomaly): keep the last few streams
+std::shared_ptr<const Stream> build_cached(const erx_gen_spec& in) {
+    erx_gen_spec s;
+    std::memset(&s, 0, sizeof(s));  // padding bytes zero: the cache compares whole structs
+    s.lines = in.lines; s.pixels = in.pixels; s.bands = in.bands; s.n_factors = in.n_factors;
+    s.loading_sd = in.loading_sd; s.noise_sd = in.noise_sd; s.base_kind = in.base_kind;
+    s.drift = in.drift; s.n_scene_changes = in.n_scene_changes;
+    for (int k = 0; k < 4; ++k) s.scene_change_line[k] = in.scene_change_line[k];
+    s.anomaly_frac = in.anomaly_frac; s.anomaly_kind = in.anomaly_kind; s.offset_sd = in.offset_sd;
+    s.mix_lo = in.mix_lo; s.mix_hi = in.mix_hi; s.seed = in.seed;
+    static std::mutex mu;
+    static std::vector<std::pair<erx_gen_spec, std::shared_ptr<const Stream>>> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto& e : cache)
+        if (std::memcmp(&e.first, &s, sizeof(s)) == 0) return e.second;
+    auto st = std::make_shared<const Stream>(build(s));
+    if (cache.size() >= 8) cache.erase(cache.begin());
+    cache.push_back({s, st});
+    return st;
+}
+
 void gen_line(const erx_gen_spec& s, const Stream& st, const std::vector<std::vector<std::pair<int, int>>>& hits,
               uint32_t t, uint32_t rel, float* out, uint8_t* mask) {
     const uint32_t B = s.bands, P = s.pixels, R = s.n_factors;
@@ -167,6 +191,56 @@ void gen_line(const erx_gen_spec& s, const Stream& st, const std::vector<std::ve
 }
 
 }  // namespace
+
+namespace erx_host {
+
+// The stream-level draws flattened for the device generator (k_datagen.cu): the same build()
+// and the same per-line hit lists as erx_gen_lines.
+int gen_plan(const erx_gen_spec& s, uint32_t first, uint32_t n, GenPlan& pl) {
+    if (s.pixels < 1 || s.bands < 1 || s.lines < 1) return 2;
+    const auto stp = build_cached(s);
+    const Stream& st = *stp;
+    pl.B = s.bands;
+    pl.P = s.pixels;
+    pl.R = s.n_factors;
+    pl.base.clear();
+    for (const auto& b : st.base) pl.base.insert(pl.base.end(), b.begin(), b.end());
+    pl.drift = st.drift;
+    pl.A = st.A;
+    pl.changes = st.changes;
+    std::vector<std::vector<std::pair<int, int>>> hits(n);
+    for (size_t i = 0; i < st.anoms.size(); ++i) {
+        const Anomaly& a = st.anoms[i];
+        for (const Cell& c : a.cells) {
+            const int64_t l = a.line0 + c.dl, p = a.pix0 + c.dp;
+            if (l < int64_t(first) || l >= int64_t(first) + n || p >= int64_t(s.pixels) || l >= int64_t(s.lines))
+                continue;
+            hits[size_t(l - first)].push_back({int(i), int(p)});
+        }
+    }
+    pl.hit_off.assign(1, 0u);
+    pl.hit_pix.clear();
+    pl.hit_anom.clear();
+    pl.anom_spec.clear();
+    pl.anom_f.clear();
+    std::vector<int> slot(st.anoms.size(), -1);
+    for (uint32_t l = 0; l < n; ++l) {
+        for (const auto& h : hits[l]) {
+            if (slot[h.first] < 0) {
+                slot[h.first] = int(pl.anom_f.size());
+                pl.anom_f.push_back(st.anoms[h.first].f);
+                const auto& sp = st.anoms[h.first].spec;
+                pl.anom_spec.insert(pl.anom_spec.end(), sp.begin(), sp.end());
+            }
+            pl.hit_pix.push_back(uint32_t(h.second));
+            pl.hit_anom.push_back(uint32_t(slot[h.first]));
+        }
+        pl.hit_off.push_back(uint32_t(pl.hit_pix.size()));
+    }
+    return 0;
+}
+
+}  // namespace erx_host
 
 extern "C" {
 
@@ -212,7 +286,8 @@ int erx_gen_preset(int id, uint32_t stream, erx_gen_spec* o) {
 int erx_gen_lines(const erx_gen_spec* spec, uint32_t first, uint32_t n, float* out, uint8_t* mask, int threads) {
     if (!spec || spec->pixels < 1 || spec->bands < 1 || spec->lines < 1) return 2;
     const erx_gen_spec s = *spec;
-    const Stream st = build(s);
+    const auto stp = build_cached(s);
+    const Stream& st = *stp;
     std::vector<std::vector<std::pair<int, int>>> hits(n);
     for (size_t i = 0; i < st.anoms.size(); ++i) {
         const Anomaly& a = st.anoms[i];

@@ -394,3 +394,19 @@ def gen_lines(spec, first: int, n: int, threads: int = 0, want_mask: bool = True
     if st:
         raise ConfigError("bad generator spec")
     return out, mask
+
+
+def gen_lines_device(spec, first: int, n: int, out=None, mask=None, want_mask: bool = True, stream: int = 0):
+    """The same lines generated on the device (erx_gen_lines_device): torch CUDA tensors
+    (fp32 [n][P][B], u8 [n][P] or None).  `out` / `mask` may be preallocated (contiguous)."""
+    import torch
+
+    if out is None:
+        out = torch.empty((n, spec.pixels, spec.bands), dtype=torch.float32, device="cuda")
+    if mask is None and want_mask:
+        mask = torch.empty((n, spec.pixels), dtype=torch.uint8, device="cuda")
+    st = L.lib().erx_gen_lines_device(C.byref(spec), first, n, out.data_ptr(),
+                                      mask.data_ptr() if mask is not None else None, stream or None)
+    if st:
+        _raise(st, f"gen_lines_device: status {st}")
+    return out, mask
