@@ -208,6 +208,35 @@ int erx_metrics_roc_auc(const float* d_scores, const uint8_t* d_labels, const ui
 int erx_metrics_top_k(const float* d_scores, const uint8_t* d_select, size_t n, size_t k, void* stream,
                       uint8_t* d_mask, float* cutoff);
 
+/* ---- HADC cube / mask files (hadc.cpp; SPEC.md:576-598 [MODULE] io) ----
+ * Little-endian container: "HADC", version u16 (1), lines / pixels / bands u32, dtype u8
+ * (1 = float32, 2 = u8 mask 0/1), layout u8 (1 = [line][pixel][band]), name_len u16 + UTF-8
+ * name, then exactly lines*pixels*bands elements.  Violations (bad magic / version / dtype /
+ * layout, zero sizes, payload length != declared, mask value > 1) return ERX_ERR_IO with the
+ * byte offset in erx_hadc_last_error (read_cube / read_mask errors). */
+typedef struct erx_hadc erx_hadc;
+typedef struct {
+    uint16_t version;
+    uint32_t lines, pixels, bands;
+    uint8_t dtype, layout;
+    uint16_t name_len;
+    char name[256]; /* NUL-terminated, truncated to 255 bytes */
+} erx_hadc_info;
+int erx_hadc_open(const char* path, erx_hadc** out, erx_hadc_info* info);
+/* Message of the last failure on h (h = NULL: of this thread's last failed erx_hadc_open). */
+const char* erx_hadc_last_error(const erx_hadc* h);
+/* Lines [first, first + n) into host memory (mask values checked). */
+int erx_hadc_read(erx_hadc* h, uint32_t first_line, uint32_t n_lines, void* dst);
+/* The same lines into device memory through two pinned ~16 MB stages: the file read of one
+ * chunk overlaps the H2D copy of the previous one on `stream` (a cudaStream_t, NULL = legacy
+ * default); returns when the copies are done. */
+int erx_hadc_read_device(erx_hadc* h, uint32_t first_line, uint32_t n_lines, void* d_dst, void* stream);
+void erx_hadc_close(erx_hadc* h);
+/* write_cube / write_mask (dtype 1 / 2); ERX_ERR_CONFIG for zero sizes, ERX_ERR_DATA for a mask
+ * value > 1, ERX_ERR_IO for file errors. */
+int erx_hadc_write(const char* path, const char* name, uint32_t lines, uint32_t pixels, uint32_t bands, int dtype,
+                   const void* data);
+
 /* CUDA events on the engine stream, for callers timing device work. */
 int erx_event_record(erx_engine* e, int slot);
 int erx_event_elapsed_ms(erx_engine* e, int slot_a, int slot_b, float* ms);

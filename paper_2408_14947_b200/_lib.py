@@ -60,6 +60,19 @@ class GenSpecC(C.Structure):
     ]
 
 
+class HadcInfoC(C.Structure):
+    _fields_ = [
+        ("version", C.c_uint16),
+        ("lines", C.c_uint32),
+        ("pixels", C.c_uint32),
+        ("bands", C.c_uint32),
+        ("dtype", C.c_uint8),
+        ("layout", C.c_uint8),
+        ("name_len", C.c_uint16),
+        ("name", C.c_char * 256),
+    ]
+
+
 # name -> (restype, argtypes)
 _vp, _dp, _fp, _u8p, _i64p, _u64p = C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_float), \
     C.POINTER(C.c_uint8), C.POINTER(C.c_int64), C.POINTER(C.c_uint64)
@@ -99,6 +112,12 @@ SIGNATURES = {
     "erx_tc_selftest_i8": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp]),
     "erx_metrics_roc_auc": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _dp, _u64p, _u64p]),
     "erx_metrics_top_k": (C.c_int, [_vp, _vp, C.c_size_t, C.c_size_t, _vp, _vp, _fp]),
+    "erx_hadc_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(HadcInfoC)]),
+    "erx_hadc_last_error": (C.c_char_p, [_vp]),
+    "erx_hadc_read": (C.c_int, [_vp, C.c_uint32, C.c_uint32, _vp]),
+    "erx_hadc_read_device": (C.c_int, [_vp, C.c_uint32, C.c_uint32, _vp, _vp]),
+    "erx_hadc_close": (None, [_vp]),
+    "erx_hadc_write": (C.c_int, [C.c_char_p, C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, _vp]),
     "erx_event_record": (C.c_int, [_vp, C.c_int]),
     "erx_event_elapsed_ms": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_float)]),
     "erx_host_alloc": (C.c_void_p, [C.c_size_t]),
