@@ -50,6 +50,7 @@ struct StatsLaunch {
     int G;           // pixel groups per pair (threads per pair)
     int cpl;         // CTAs per line
     int NT;          // threads per CTA
+    int minb;        // kernel variant: 1 (<= 384 threads) or 2 (<= 256 threads, two CTAs per SM)
     size_t smem;     // dynamic shared memory bytes
 };
 

@@ -991,8 +991,7 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
         ensure_smem(factor_blk_kernel, sm);
         // 64 threads per line fill the GPU with ~7 lines per SM; when a launch has fewer lines than
         // SMs (lag-0 / small windows) more threads per line shorten each line's latency instead
-        int threads = n_lines_total >= sm_count() ? 64 : 256;
-        if (const char* ev = getenv("ERX_FACTOR_THREADS")) threads = atoi(ev);  // EXPERIMENT
+        const int threads = n_lines_total >= sm_count() ? 64 : 256;
         factor_blk_kernel<<<n_lines_total, threads, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
                                                           vmax, kblk);
     } else if (precision == 64) {

@@ -185,7 +185,9 @@ ScoreLaunch plan_score(const Geometry& g) {
     sc.tiles = (g.P + sc.PT - 1) / sc.PT;
     sc.smem = align_up((size_t(sc.PT) * sc.Dpad + size_t(g.nb) * sc.PT) * 4, 16) + align_up(size_t(g.Dp) * 8, 16);
     const size_t wbytes = size_t(g.nb) * (g.nb + 1) / 2 * 64 * 4;
-    sc.wsmem = (sc.smem + wbytes <= 200 * 1024) ? 1 : 0;  // stage W in smem when it fits (D <= ~240)
+    // stage W in smem when it is small (D <= ~180); a larger W would cost the CTA its SM-mates and
+    // reads better from L2 (configs[1], D = 224: 0.50 -> 0.445 ms per 256 lines)
+    sc.wsmem = (sc.smem + wbytes <= 200 * 1024 && wbytes <= 64 * 1024) ? 1 : 0;
     if (sc.wsmem) sc.smem += wbytes;
     return sc;
 }

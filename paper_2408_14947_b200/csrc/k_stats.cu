@@ -35,7 +35,8 @@ struct StatsArgs {
     double* stats;
 };
 
-__global__ void __launch_bounds__(384) stats_kernel(StatsArgs a) {
+template <int kMaxThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kMaxThreads, kMinBlocks) stats_kernel(StatsArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geometry& g = a.g;
     const StatsLaunch& sl = a.sl;
@@ -76,9 +77,11 @@ __global__ void __launch_bounds__(384) stats_kernel(StatsArgs a) {
         }
     const int n0 = min(32, g.P);
     const bool use_async = !g.srp && (g.B % 4 == 0);
+    // centre: fp64 mean of the first n0 (projected) pixels; from chunk 0 when it holds them all
+    const bool cen_in_chunk = use_async && sl.CH >= n0;
     for (int j = tid; j < g.D; j += nt) {
         colsum[j] = 0.0;
-        if (!use_async) {  // projected centre straight from global; the async path takes it from chunk 0
+        if (!cen_in_chunk) {
             double s = 0.0;
             for (int pp = 0; pp < n0; ++pp) s += proj(g, xl + size_t(pp) * g.B, j);
             cen[j] = float(s / double(n0));
@@ -121,7 +124,7 @@ __global__ void __launch_bounds__(384) stats_kernel(StatsArgs a) {
             for (int j = tid; j < g.D; j += nt) {
                 {
                     float* col = v + spos(j, g.nb);
-                    if (c == 0) {  // centre: fp64 mean of the first n0 staged (raw) pixels of this dim
+                    if (c == 0 && cen_in_chunk) {  // same sum, same order as the global path
                         double s = 0.0;
                         for (int pp = 0; pp < n0; ++pp) s += double(col[size_t(pp) * g.Dp]);
                         cen[j] = float(s / double(n0));
@@ -251,6 +254,7 @@ __global__ void __launch_bounds__(384) stats_kernel(StatsArgs a) {
 
 StatsLaunch plan_stats(const Geometry& g) {
     StatsLaunch sl{};
+    sl.minb = 1;
     sl.n_pairs = g.nb * (g.nb + 1) / 2;
     if (sl.n_pairs <= 64) {
         sl.G = 128 / sl.n_pairs;
@@ -258,17 +262,22 @@ StatsLaunch plan_stats(const Geometry& g) {
         sl.cpl = 1;
         sl.NT = 128;
     } else {
-        // one thread per block pair, up to 384 threads (12 warps: the 165-register accumulators of
-        // 384 threads fill the register file) per CTA, the pairs split evenly over the line's CTAs
+        // one thread per block pair, the pairs split evenly over the line's CTAs
+        // up to D = 255 (configs[1]): <= 256 threads and two CTAs per SM (the second-level
+        // accumulators spill to L1, touched once per chunk); beyond: up to 384 threads, one CTA
         sl.G = 1;
-        sl.cpl = (sl.n_pairs + 383) / 384;
+        const int maxnt = sl.n_pairs <= 512 ? 256 : 384;
+        sl.cpl = (sl.n_pairs + maxnt - 1) / maxnt;
         sl.npc = (sl.n_pairs + sl.cpl - 1) / sl.cpl;
         sl.NT = (sl.npc + 31) / 32 * 32;
+        sl.minb = maxnt <= 256 ? 2 : 1;
     }
     const size_t per_px = size_t(g.Dp) * 4 * 2;  // double buffered
     int ch = 64;
     if (sl.G > 1) ch = 256;
-    while (ch > 16 && size_t(ch) * per_px > 120 * 1024) ch /= 2;
+    size_t cap = 120 * 1024;
+    if (sl.minb == 2) cap = 96 * 1024;
+    while (ch > 16 && size_t(ch) * per_px > cap) ch /= 2;
     sl.CH = ch;
     size_t off = align_up(size_t(ch) * per_px, 16);
     const size_t red_bytes = (sl.G > 1) ? size_t(128) * 64 * 8 : 0;
@@ -279,11 +288,14 @@ StatsLaunch plan_stats(const Geometry& g) {
 
 void launch_stats(const Geometry& g, const StatsLaunch& sl, const float* x, int n_per_stream, int in_stride,
                   int n_lines_total, double* stats, cudaStream_t st) {
-    {
-        ensure_smem(stats_kernel, 200 * 1024);
-    }
     StatsArgs a{g, sl, x, n_per_stream, in_stride, stats};
-    stats_kernel<<<n_lines_total * sl.cpl, sl.NT, sl.smem, st>>>(a);
+    if (sl.minb == 2) {
+        ensure_smem(stats_kernel<256, 2>, 110 * 1024);
+        stats_kernel<256, 2><<<n_lines_total * sl.cpl, sl.NT, sl.smem, st>>>(a);
+    } else {
+        ensure_smem(stats_kernel<384, 1>, 200 * 1024);
+        stats_kernel<384, 1><<<n_lines_total * sl.cpl, sl.NT, sl.smem, st>>>(a);
+    }
 }
 
 }  // namespace erxk
