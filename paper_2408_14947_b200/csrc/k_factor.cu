@@ -989,9 +989,16 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
     const size_t sm = factor_smem(g, precision);
     if (precision == 32) {
         ensure_smem(factor_blk_kernel, sm);
-        // 64 threads per line fill the GPU with ~7 lines per SM; when a launch has fewer lines than
-        // SMs (lag-0 / small windows) more threads per line shorten each line's latency instead
-        const int threads = n_lines_total >= sm_count() ? 64 : 256;
+        // 64 threads per line when the SMs hold >= 6 lines each (configs[3]: 7 per SM by shared
+        // memory); with fewer resident lines (small windows, lag 0, or D > ~150 where a line's blocks
+        // take 100 KB: configs[1]) 256 threads per line shorten each line's latency instead
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int smem_sm = 0;
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        const int cap = std::max(1, int(size_t(smem_sm) / (sm + 1024)));
+        const int per_sm = (n_lines_total + sm_count() - 1) / sm_count();
+        const int threads = std::min(cap, per_sm) >= 6 ? 64 : 256;
         factor_blk_kernel<<<n_lines_total, threads, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
                                                           vmax, kblk);
     } else if (precision == 64) {
