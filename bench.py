@@ -292,24 +292,36 @@ def run_ours(args):
         eng2.set_factor_precision(args.factor)
         eng2.set_host_groups(args.host_groups)
         eng2.set_stats_tensor(args.stats)
+        eng2.set_async_host(not args.sync_host)
         pin = torch.from_numpy(np.ascontiguousarray(host[:, :T])).pin_memory().numpy()
         outb = (np.empty((S, T, P)), np.empty((S, T, P)))  # caller-owned ScoredLine payload buffers
+        popped = 0
         for k in range(2):
             eng2.push(pin, k * T)
+            eng2.pop(out=outb)
+        eng2.finish()
+        while eng2.ready():
             eng2.pop(out=outb)
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
         for k in range(e2e_steps):
+            # pipelined: this window's copy-in overlaps the previous window's kernels and result
+            # copies; pop returns the previous window's ScoredLine payload
             eng2.push(pin, (k + 2) * T)
-            _, _, r_, n_ = eng2.pop(out=outb)
+            popped += eng2.pop(out=outb)[0].size
+        eng2.finish()
+        while eng2.ready():
+            popped += eng2.pop(out=outb)[0].size
         el = time.perf_counter() - t0
+        assert popped == T * e2e_steps, (popped, T * e2e_steps)
         el_t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{local}")
         if dist:
             dist.all_reduce(el_t, op=dist.ReduceOp.MAX)
         e2e = {"value": S_tot * T * e2e_steps / float(el_t.item()), "unit": "lines/s",
                "h2d_bytes_per_step": S * T * P * B * 4, "d2h_bytes_per_step": S * T * (P * 4 * 2 + 4),
-               "path": "erx_push_host (pinned) -> 5 kernels -> erx_pop (fp64 ScoredLine payload)"}
+               "path": "erx_push_host (pinned) -> 5 kernels -> erx_pop (fp64 ScoredLine payload)",
+               "pipelined": not args.sync_host}
         eng2.close()
     except Exception as ex:  # report, never hide
         e2e = {"error": repr(ex)}
@@ -571,6 +583,7 @@ def main():
     ap.add_argument("--stats", type=int, default=2, choices=[0, 1, 2],
                     help="line-statistics kernel: 0 FFMA, 1 tcgen05 bf16x3, 2 tcgen05 exact int8")
     ap.add_argument("--host-groups", type=int, default=0, help="stream groups per host window (0 auto)")
+    ap.add_argument("--sync-host", action="store_true", help="e2e without ERX_OPT_ASYNC_HOST (push waits for scores)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

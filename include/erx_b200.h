@@ -154,6 +154,15 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
  * sizes the groups at >= 8 MB of input each, 1..8 forces that count
  * (results are identical for every count: streams are independent). */
 #define ERX_OPT_HOST_GROUPS 3
+/* ERX_OPT_ASYNC_HOST: 0 (default) erx_push_host returns with every full window
+ * scored and queued; 1 it returns once the window's input is on the device
+ * (the source buffer is free) and the window stays in flight, so the next
+ * push's host->device copy overlaps its kernels and result copies.  In-flight
+ * windows are harvested by erx_ready / erx_pop (which wait for the oldest one
+ * only when nothing is queued), erx_finish and every state / device call; a
+ * FactorizationError is reported by the call that harvests it (erx_ready
+ * defers it to the next erx_pop / push / finish). */
+#define ERX_OPT_ASYNC_HOST 4
 int erx_set_option(erx_engine* e, int option, int64_t value);
 int64_t erx_get_option(const erx_engine* e, int option);
 

@@ -25,6 +25,7 @@ KERNEL_NAMES = ("stats", "scan", "factor", "score", "normalize")
 OPT_FACTOR_PRECISION = 1
 OPT_STATS_TENSOR = 2
 OPT_HOST_GROUPS = 3
+OPT_ASYNC_HOST = 4
 
 
 class ErxConfigC(C.Structure):

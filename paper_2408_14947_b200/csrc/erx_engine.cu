@@ -32,8 +32,18 @@ namespace {
 struct ResultBlock {
     float* raw = nullptr;
     float* norm = nullptr;
-    size_t cap = 0;  // floats per array
+    int* status = nullptr;  // [S][n] factor status per line (-1 ok, else the failing pivot)
+    size_t cap = 0;         // floats per array
     uint32_t n = 0, P = 0;
+};
+
+// A window of the host path whose kernels / result copies may still be running
+// (ERX_OPT_ASYNC_HOST): harvested into the queue once `done` has fired.
+struct PendingWindow {
+    std::shared_ptr<ResultBlock> blk;
+    uint32_t n = 0, P = 0;
+    std::vector<int64_t> index;
+    cudaEvent_t done = nullptr;
 };
 
 struct ScoredRow {
@@ -97,14 +107,18 @@ struct erx_engine {
 
     // pinned host staging (drop-in path)
     float* h_lines = nullptr;
-    int* h_status = nullptr;
     // drop-in path streams: host->device copies and device->host result copies run
     // beside the compute stream, one stream group at a time (run_host_window)
     cudaStream_t h2d = nullptr, d2h = nullptr;
     static constexpr int kMaxGroups = 8;
-    cudaEvent_t ev_in[kMaxGroups] = {}, ev_out[kMaxGroups] = {};
+    cudaEvent_t ev_in[kMaxGroups] = {}, ev_out[kMaxGroups] = {}, ev_d2h[kMaxGroups] = {};
+    int prev_groups = 0;  // stream groups of the previous host window (its events guard buffer reuse)
     std::vector<ResultBlock*> block_pool;
     int host_groups = 0;  // ERX_OPT_HOST_GROUPS (0 auto)
+    bool async_host = false;  // ERX_OPT_ASYNC_HOST
+    std::deque<PendingWindow> pending;
+    std::vector<cudaEvent_t> done_pool;
+    int pending_err = 0;  // a failure found by erx_ready, reported by the next call that can return it
 
     bool initialized = false;
     int64_t lines_seen = 0;
@@ -214,24 +228,26 @@ void free_window(erx_engine* e) {
     cudaFree(e->d_kblk);
     e->d_kblk = nullptr;
     cudaFreeHost(e->h_lines);
-    cudaFreeHost(e->h_status);
     e->d_lines = nullptr;
     e->d_stats = e->d_prior = e->d_work = nullptr;
     e->d_white = e->d_raw = e->d_norm = nullptr;
     e->d_status = nullptr;
     e->h_lines = nullptr;
-    e->h_status = nullptr;
 }
 
 void free_block(ResultBlock* b) {
     cudaFreeHost(b->raw);
     cudaFreeHost(b->norm);
+    cudaFreeHost(b->status);
     delete b;
 }
+
+int drain_pending(erx_engine* e);
 
 // (Re)plan the geometry for P pixels and size the window buffers.
 int configure(erx_engine* e, uint32_t P) {
     CU(cudaSetDevice(e->device));
+    if (int st = drain_pending(e)) return st;  // in-flight host windows use the buffers
     if (P == e->P && e->d_stats) return ERX_OK;
     CU(cudaStreamSynchronize(e->stream));
     free_window(e);
@@ -279,13 +295,13 @@ int ensure_host_staging(erx_engine* e) {
     const size_t L = size_t(e->S) * e->T;
     CU(cudaMalloc(&e->d_lines, L * e->P * e->B * sizeof(float)));
     CU(cudaMallocHost(&e->h_lines, L * e->P * e->B * sizeof(float)));
-    CU(cudaMallocHost(&e->h_status, L * sizeof(int)));
     if (!e->h2d) {
         CU(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
         CU(cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking));
         for (int k = 0; k < erx_engine::kMaxGroups; ++k) {
             CU(cudaEventCreateWithFlags(&e->ev_in[k], cudaEventDisableTiming));
             CU(cudaEventCreateWithFlags(&e->ev_out[k], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&e->ev_d2h[k], cudaEventDisableTiming));
         }
     }
     return ERX_OK;
@@ -306,7 +322,8 @@ std::shared_ptr<ResultBlock> take_block(erx_engine* e, uint32_t n) {
     if (!b) {
         b = new ResultBlock();
         if (cudaMallocHost(&b->raw, need * sizeof(float)) != cudaSuccess ||
-            cudaMallocHost(&b->norm, need * sizeof(float)) != cudaSuccess) {
+            cudaMallocHost(&b->norm, need * sizeof(float)) != cudaSuccess ||
+            cudaMallocHost(&b->status, size_t(e->S) * e->T * sizeof(int)) != cudaSuccess) {
             free_block(b);
             return nullptr;
         }
@@ -402,13 +419,76 @@ uint32_t host_groups(const erx_engine* e, uint32_t n) {
     return std::max<uint32_t>(1, std::min<uint32_t>(G, e->S));
 }
 
-// Score one window of the drop-in path and queue its rows.  src holds stream s
-// at src + s * src_pitch floats (n lines of P x B each): the caller's buffer
-// (direct path) or the pinned staging buffer.  The window is cut into stream
-// groups: group g's host->device copy (h2d stream) overlaps the kernels of
-// group g-1 (compute stream), whose results drain on the d2h stream.  The call
-// returns when the whole window is scored and queued (the per-call contract of
-// the reference's process(); the source buffer is free again on return).
+// Move finished host windows into the queue, oldest first.  block_oldest: wait
+// for the oldest pending window (the others are taken only if already done).
+// A window with a failing line queues the lines before it, fails the engine
+// and drops every later window.
+int harvest(erx_engine* e, bool block_oldest) {
+    while (!e->pending.empty()) {
+        PendingWindow& pw = e->pending.front();
+        if (block_oldest) {
+            CU(cudaEventSynchronize(pw.done));
+            block_oldest = false;
+        } else {
+            const cudaError_t q = cudaEventQuery(pw.done);
+            if (q == cudaErrorNotReady) break;
+            if (q != cudaSuccess) return fail(e, ERX_ERR_DEVICE, std::string("host window: ") + cudaGetErrorString(q));
+        }
+        const uint32_t n = pw.n;
+        int bad_t = -1, bad_piv = -1;  // first failing line in emission order (then stream order)
+        for (uint32_t t = 0; t < n && bad_t < 0; ++t)
+            for (uint32_t s = 0; s < e->S; ++s)
+                if (pw.blk->status[s * n + t] >= 0) {
+                    bad_t = int(t);
+                    bad_piv = pw.blk->status[s * n + t];
+                    break;
+                }
+        const uint32_t good = bad_t < 0 ? n : uint32_t(bad_t);
+        for (uint32_t t = 0; t < good; ++t) {
+            ScoredRow row;
+            row.index = pw.index[t];
+            row.warmup = (row.index < int64_t(e->cfg.buffer_len)) ? 1 : 0;
+            row.P = pw.P;
+            row.t = t;
+            row.blk = pw.blk;
+            e->queue.push_back(std::move(row));
+        }
+        const int64_t bad_index = bad_t >= 0 ? pw.index[bad_t] : -1;
+        e->done_pool.push_back(pw.done);
+        e->pending.pop_front();
+        if (bad_t >= 0) {
+            cudaStreamSynchronize(e->d2h);  // later windows are dropped: let their copies land first
+            cudaStreamSynchronize(e->stream);
+            for (auto& later : e->pending) e->done_pool.push_back(later.done);
+            e->pending.clear();
+            e->failed = true;
+            e->pivot = bad_piv;
+            return fail(e, ERX_ERR_NUMERIC,
+                        "Cholesky of K + eps*I failed at pivot " + std::to_string(bad_piv) + " for line index " +
+                            std::to_string(bad_index) + " after epsilon escalation to 1e-1");
+        }
+    }
+    return ERX_OK;
+}
+
+int drain_pending(erx_engine* e) {
+    while (!e->pending.empty()) {
+        const int st = harvest(e, true);
+        if (st) return st;
+    }
+    return ERX_OK;
+}
+
+// Score one window of the drop-in path.  src holds stream s at src + s *
+// src_pitch floats (n lines of P x B each): the caller's buffer (direct path)
+// or the pinned staging buffer.  The window is cut into stream groups: group
+// g's host->device copy (h2d stream) overlaps the kernels of group g-1
+// (compute stream), whose results drain on the d2h stream.  The call returns
+// once the input is on the device (the source buffer is free again, the
+// per-call contract of the reference's process()); by default it also waits
+// for the scores and queues them, with ERX_OPT_ASYNC_HOST the window stays in
+// flight (its copy-in then overlaps the previous window's kernels and result
+// copies) until erx_ready / erx_pop / erx_finish harvest it.
 int run_host_window(erx_engine* e, const float* src, size_t src_pitch) {
     if (e->fill == 0) return ERX_OK;
     const uint32_t n = e->fill;
@@ -416,15 +496,21 @@ int run_host_window(erx_engine* e, const float* src, size_t src_pitch) {
     auto blk = take_block(e, n);
     if (!blk) return fail(e, ERX_ERR_DEVICE, "cudaMallocHost (result block)");
     const uint32_t G = host_groups(e, n);
+    const int pg = e->prev_groups;
     for (uint32_t gi = 0; gi < G; ++gi) {
         const uint32_t s0 = uint32_t(uint64_t(e->S) * gi / G), s1 = uint32_t(uint64_t(e->S) * (gi + 1) / G);
         const uint32_t ns = s1 - s0;
         if (!ns) continue;
+        // the previous window's group (or, with another grouping, all of it) must be done with
+        // d_lines before this copy overwrites it, and its results must have left d_raw / d_norm
+        const int prev = pg == int(G) ? int(gi) : pg - 1;
+        if (pg) CU(cudaStreamWaitEvent(e->h2d, e->ev_out[prev], 0));
         CU(cudaMemcpy2DAsync(e->d_lines + size_t(s0) * e->T * line_f, size_t(e->T) * line_f * sizeof(float),
                              src + size_t(s0) * src_pitch, src_pitch * sizeof(float), n * line_f * sizeof(float), ns,
                              cudaMemcpyHostToDevice, e->h2d));
         CU(cudaEventRecord(e->ev_in[gi], e->h2d));
         CU(cudaStreamWaitEvent(e->stream, e->ev_in[gi], 0));
+        if (pg) CU(cudaStreamWaitEvent(e->stream, e->ev_d2h[prev], 0));
         int st = enqueue_window(e, e->d_lines, n, e->T, e->d_raw, e->d_norm, s0, ns);
         if (st) return st;
         CU(cudaEventRecord(e->ev_out[gi], e->stream));
@@ -434,39 +520,27 @@ int run_host_window(erx_engine* e, const float* src, size_t src_pitch) {
                            cudaMemcpyDeviceToHost, e->d2h));
         CU(cudaMemcpyAsync(blk->norm + l0 * e->P, e->d_norm + l0 * e->P, nl * e->P * sizeof(float),
                            cudaMemcpyDeviceToHost, e->d2h));
-        CU(cudaMemcpyAsync(e->h_status + l0, e->d_status + l0, nl * sizeof(int), cudaMemcpyDeviceToHost, e->d2h));
+        CU(cudaMemcpyAsync(blk->status + l0, e->d_status + l0, nl * sizeof(int), cudaMemcpyDeviceToHost, e->d2h));
+        CU(cudaEventRecord(e->ev_d2h[gi], e->d2h));
     }
     commit_window(e, n);
-    CU(cudaStreamSynchronize(e->d2h));
-    CU(cudaStreamSynchronize(e->stream));
-    // first failing line in emission order (then stream order)
-    int bad_t = -1, bad_piv = -1;
-    for (uint32_t t = 0; t < n && bad_t < 0; ++t)
-        for (uint32_t s = 0; s < e->S; ++s)
-            if (e->h_status[s * n + t] >= 0) {
-                bad_t = int(t);
-                bad_piv = e->h_status[s * n + t];
-                break;
-            }
-    const uint32_t good = bad_t < 0 ? n : uint32_t(bad_t);
-    for (uint32_t t = 0; t < good; ++t) {
-        ScoredRow row;
-        row.index = e->win_index[t];
-        row.warmup = (row.index < int64_t(e->cfg.buffer_len)) ? 1 : 0;
-        row.P = e->P;
-        row.t = t;
-        row.blk = blk;
-        e->queue.push_back(std::move(row));
+    e->prev_groups = int(G);
+    PendingWindow pw;
+    pw.blk = blk;
+    pw.n = n;
+    pw.P = e->P;
+    pw.index.assign(e->win_index.begin(), e->win_index.begin() + n);
+    if (!e->done_pool.empty()) {
+        pw.done = e->done_pool.back();
+        e->done_pool.pop_back();
+    } else {
+        CU(cudaEventCreateWithFlags(&pw.done, cudaEventDisableTiming));
     }
+    CU(cudaEventRecord(pw.done, e->d2h));
+    e->pending.push_back(std::move(pw));
     e->fill = 0;
-    if (bad_t >= 0) {
-        e->failed = true;
-        e->pivot = bad_piv;
-        return fail(e, ERX_ERR_NUMERIC,
-                    "Cholesky of K + eps*I failed at pivot " + std::to_string(bad_piv) + " for line index " +
-                        std::to_string(e->win_index[bad_t]) + " after epsilon escalation to 1e-1");
-    }
-    return ERX_OK;
+    CU(cudaStreamSynchronize(e->h2d));  // the source buffer is free again
+    return e->async_host ? ERX_OK : drain_pending(e);
 }
 
 int run_staged_window(erx_engine* e) {
@@ -579,6 +653,10 @@ void erx_destroy(erx_engine* e) {
     cudaSetDevice(e->device);
     if (e->stream) cudaStreamSynchronize(e->stream);
     if (e->d2h) cudaStreamSynchronize(e->d2h);
+    for (auto& pw : e->pending) cudaEventDestroy(pw.done);
+    e->pending.clear();
+    for (auto ev : e->done_pool) cudaEventDestroy(ev);
+    e->done_pool.clear();
     e->queue.clear();  // returns result blocks to the pool
     for (auto* b : e->block_pool) free_block(b);
     e->block_pool.clear();
@@ -599,6 +677,7 @@ void erx_destroy(erx_engine* e) {
     for (int k = 0; k < erx_engine::kMaxGroups; ++k) {
         if (e->ev_in[k]) cudaEventDestroy(e->ev_in[k]);
         if (e->ev_out[k]) cudaEventDestroy(e->ev_out[k]);
+        if (e->ev_d2h[k]) cudaEventDestroy(e->ev_d2h[k]);
     }
     if (e->h2d) cudaStreamDestroy(e->h2d);
     if (e->d2h) cudaStreamDestroy(e->d2h);
@@ -612,9 +691,17 @@ int erx_dims(const erx_engine* e) { return e->D; }
 uint32_t erx_streams(const erx_engine* e) { return e->S; }
 uint32_t erx_window(const erx_engine* e) { return e->T; }
 
+int report_pending(erx_engine* e) {
+    const int st = e->pending_err;
+    e->pending_err = 0;
+    return st;
+}
+
 int erx_push_host(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t pixels, uint32_t bands,
                   const float* lines) {
+    if (int st = report_pending(e)) return st;
     if (e->failed) return fail(e, ERX_ERR_STATE, "engine is in a failed state: " + e->err);
+    if (int st = harvest(e, false)) return st;
     if (bands != e->B) return fail(e, ERX_ERR_CONFIG, "band count mismatch");  // projection.hpp:31-32
     if (pixels < 2) return fail(e, ERX_ERR_DATA, "a line needs p >= 2 pixels (1/(p-1) covariance)");  // erx.hpp:39
     if (n_lines == 0) return ERX_OK;
@@ -653,11 +740,23 @@ int erx_push_host(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t
 }
 
 int erx_finish(erx_engine* e) {
+    if (int st = report_pending(e)) return st;
     if (e->failed) return fail(e, ERX_ERR_STATE, "engine is in a failed state: " + e->err);
-    return run_staged_window(e);
+    if (int st = run_staged_window(e)) return st;
+    return drain_pending(e);
 }
 
-uint32_t erx_ready(const erx_engine* e) {
+// Harvest finished host windows; when nothing is queued, wait for the oldest in-flight one.
+void ready_harvest(erx_engine* e) {
+    if (e->pending_err || e->failed) return;
+    int st = harvest(e, false);
+    if (!st && e->queue.empty() && !e->pending.empty()) st = harvest(e, true);
+    if (st) e->pending_err = st;
+}
+
+uint32_t erx_ready(const erx_engine* ce) {
+    erx_engine* e = const_cast<erx_engine*>(ce);  // opaque handle: harvesting is not observable state
+    ready_harvest(e);
     // the leading run of queued lines that share one pixel count
     uint32_t n = 0;
     for (const auto& r : e->queue) {
@@ -671,7 +770,7 @@ uint32_t erx_next_pixels(const erx_engine* e) { return e->queue.empty() ? 0u : e
 
 int erx_pop(erx_engine* e, uint32_t max_lines, int64_t* index, uint8_t* warmup, double* raw, double* norm) {
     const uint32_t n = std::min<uint32_t>(max_lines, erx_ready(e));
-    if (!n) return 0;
+    if (!n) return -report_pending(e);
     const size_t P = e->queue.front().P;
     for (uint32_t k = 0; k < n; ++k) {
         const ScoredRow& r = e->queue[k];
@@ -714,6 +813,9 @@ int erx_pop(erx_engine* e, uint32_t max_lines, int64_t* index, uint8_t* warmup, 
 int erx_run_device(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t pixels, const float* d_lines,
                    float* d_raw, float* d_norm) {
     (void)first_index;
+    if (int st = report_pending(e)) return st;
+    if (!e->failed)
+        if (int st = drain_pending(e)) return st;
     if (e->failed) return fail(e, ERX_ERR_STATE, "engine is in a failed state: " + e->err);
     if (pixels < 2) return fail(e, ERX_ERR_DATA, "a line needs p >= 2 pixels (1/(p-1) covariance)");
     if (n_lines == 0) return ERX_OK;
@@ -729,6 +831,9 @@ int erx_run_device(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_
 
 int erx_advance_device(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t pixels, const float* d_lines) {
     (void)first_index;
+    if (int st = report_pending(e)) return st;
+    if (!e->failed)
+        if (int st = drain_pending(e)) return st;
     if (e->failed) return fail(e, ERX_ERR_STATE, "engine is in a failed state: " + e->err);
     if (pixels < 2) return fail(e, ERX_ERR_DATA, "a line needs p >= 2 pixels (1/(p-1) covariance)");
     if (n_lines == 0) return ERX_OK;
@@ -743,6 +848,8 @@ int erx_advance_device(erx_engine* e, int64_t first_index, uint32_t n_lines, uin
 }
 
 int erx_sync(erx_engine* e) {
+    if (int st = report_pending(e)) return st;
+    if (int st = drain_pending(e)) return st;
     CU(cudaStreamSynchronize(e->stream));
     int latch[4];
     CU(cudaMemcpy(latch, e->d_latch, sizeof(latch), cudaMemcpyDeviceToHost));
@@ -766,6 +873,8 @@ int erx_get_state(erx_engine* e, uint32_t stream, double* mu, double* cov, int64
     if (!e->initialized || (!mu && !cov)) return ERX_OK;
     const int D = e->D, SE = D + D * (D + 1) / 2;
     std::vector<double> h(SE);
+    if (!e->failed)
+        if (int st = drain_pending(e)) return st;
     CU(cudaStreamSynchronize(e->stream));
     CU(cudaMemcpy(h.data(), e->d_state[e->cur] + size_t(stream) * SE, SE * sizeof(double), cudaMemcpyDeviceToHost));
     if (mu) std::memcpy(mu, h.data(), D * sizeof(double));
@@ -793,6 +902,7 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
     std::memcpy(h.data(), mu, D * sizeof(double));
     for (int i = 0; i < D; ++i)
         for (int j = 0; j <= i; ++j) h[D + erxk::tri(i, j)] = cov[size_t(i) * D + j];
+    if (int st = drain_pending(e)) return st;
     CU(cudaStreamSynchronize(e->stream));
     CU(cudaMemcpy(e->d_state[e->cur] + size_t(stream) * SE, h.data(), SE * sizeof(double), cudaMemcpyHostToDevice));
     e->initialized = true;
@@ -804,6 +914,13 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
 uint64_t erx_launch_count(const erx_engine* e) { return e->launches; }
 
 int erx_set_option(erx_engine* e, int option, int64_t value) {
+    if (option == ERX_OPT_ASYNC_HOST) {
+        if (value != 0 && value != 1) return fail(e, ERX_ERR_CONFIG, "async host: 0 or 1");
+        if (!value)
+            if (int st = drain_pending(e)) return st;
+        e->async_host = value != 0;
+        return ERX_OK;
+    }
     if (option == ERX_OPT_HOST_GROUPS) {
         if (value < 0 || value > erx_engine::kMaxGroups) return fail(e, ERX_ERR_CONFIG, "host groups: 0..8");
         e->host_groups = int(value);
@@ -836,6 +953,7 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
 int64_t erx_get_option(const erx_engine* e, int option) {
     if (option == ERX_OPT_FACTOR_PRECISION) return e->d_stats ? e->factor_prec : e->factor_req;
     if (option == ERX_OPT_HOST_GROUPS) return e->host_groups;
+    if (option == ERX_OPT_ASYNC_HOST) return e->async_host ? 1 : 0;
     if (option == ERX_OPT_STATS_TENSOR) {
         if (!e->d_stats) return e->stats_tensor;
         if (e->tensor) return 2;

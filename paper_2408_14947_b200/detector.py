@@ -271,6 +271,11 @@ class Engine:
         """Stream groups per host window (0 auto; see ERX_OPT_HOST_GROUPS)."""
         self._check(self._lib.erx_set_option(self._h, L.OPT_HOST_GROUPS, int(groups)))
 
+    def set_async_host(self, on: bool):
+        """Pipelined host path (ERX_OPT_ASYNC_HOST): push returns once the input is on the device;
+        windows are harvested by ready / pop / finish."""
+        self._check(self._lib.erx_set_option(self._h, L.OPT_ASYNC_HOST, 1 if on else 0))
+
     def stats_tensor(self) -> int:
         """Line-statistics kernel in use (0 FFMA, 1 bf16x3, 2 exact int8)."""
         return int(self._lib.erx_get_option(self._h, L.OPT_STATS_TENSOR))

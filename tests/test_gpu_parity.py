@@ -451,3 +451,56 @@ def test_line_range_split_matches_unsplit(pkg, oracle, incremental):
     raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), x)
     rel_o = np.abs(split - raw_o) / np.maximum(np.abs(raw_o), 1e-30)
     assert rel_o.max() <= RAW_MAX and np.median(rel_o) <= RAW_MED
+
+
+# ---------------------------------------------------------------- pipelined host path
+def test_async_host_matches_sync(pkg):
+    """ERX_OPT_ASYNC_HOST: same lines, same order, same scores and state as the synchronous path."""
+    spec = [pkg.gen_spec(3, s) for s in range(4)]
+    x = np.stack([pkg.gen_lines(sp, 0, 100)[0] for sp in spec])  # [S][L][P][B]
+    res = []
+    for on in (False, True):
+        eng = pkg.Engine(pkg.ErxConfig(alpha=0.1, no_srp=True), x.shape[3], n_streams=4, window_lines=16)
+        eng.set_async_host(on)
+        idx, raws = [], []
+        for k in range(0, 100, 24):  # ragged pushes: staged and direct windows
+            eng.push(x[:, k:k + 24], k)
+            while eng.ready():
+                i, _, r, _ = eng.pop()
+                idx.append(i)
+                raws.append(r)
+        eng.finish()
+        while eng.ready():
+            i, _, r, _ = eng.pop()
+            idx.append(i)
+            raws.append(r)
+        st = eng.state(2)
+        eng.close()
+        res.append((np.concatenate(idx), np.concatenate(raws, axis=1), st.cov))
+    np.testing.assert_array_equal(res[0][0], np.arange(100))
+    np.testing.assert_array_equal(res[1][0], res[0][0])
+    np.testing.assert_array_equal(res[1][1], res[0][1])
+    np.testing.assert_array_equal(res[1][2], res[0][2])
+
+
+def test_async_host_pipelines_and_reports_failure(pkg):
+    """In flight: pop after push returns the previous window; a failing line surfaces on a later call."""
+    x = np.random.default_rng(3).normal(size=(2, 64, 96, 40)).astype(np.float32)
+    eng = pkg.Engine(pkg.ErxConfig(no_srp=True), 40, n_streams=2, window_lines=16)
+    eng.set_async_host(True)
+    got = 0
+    for k in range(0, 64, 16):
+        eng.push(x[:, k:k + 16], k)
+        got += eng.pop()[0].size
+    eng.finish()
+    while eng.ready():
+        got += eng.pop()[0].size
+    assert got == 64
+    x[1, 40, 50, 7] = np.inf  # line 40 of stream 1 poisons the background of line 41
+    eng2 = pkg.Engine(pkg.ErxConfig(no_srp=True), 40, n_streams=2, window_lines=16)
+    eng2.set_async_host(True)
+    with pytest.raises(pkg.FactorizationError):
+        for k in range(0, 64, 16):
+            eng2.push(x[:, k:k + 16], k)
+            eng2.pop()
+        eng2.finish()
