@@ -13,12 +13,15 @@
 //                line in the same kernel (normalize_scores, detector.hpp:29-32).
 //
 // Stats slot contract as k_stats.cu: [c | s | S packed lower], fp64.
+#include <algorithm>
+
 #include "erx_common.cuh"
 
 namespace erxk {
 namespace {
 
-constexpr int kSmallThreads = 256;
+constexpr int kSmallThreads = 256;       // score_small
+constexpr int kStatsSmallThreads = 128;  // stats_small: 4 CTAs (lines) per SM keep more chunks in flight
 
 struct SmallArgs {
     Geometry g;
@@ -31,7 +34,7 @@ struct SmallArgs {
 };
 
 template <int DM>
-__global__ void __launch_bounds__(kSmallThreads) stats_small_kernel(SmallArgs a) {
+__global__ void __launch_bounds__(kStatsSmallThreads) stats_small_kernel(SmallArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geometry& g = a.g;
     const SmallLaunch& sm = a.sm;
@@ -40,8 +43,8 @@ __global__ void __launch_bounds__(kSmallThreads) stats_small_kernel(SmallArgs a)
     const int D = g.D, B = g.B;
     const int NT = D * (D + 1) / 2;
     float* stage = reinterpret_cast<float*>(smem);                                  // [2][CH][B]
-    double* red = reinterpret_cast<double*>(smem + align_up(size_t(2) * sm.CH * B * 4, 16));  // [8 warps][D + NT]
-    float* vs = reinterpret_cast<float*>(red + 8 * (D + NT));                                  // [CH][DM]
+    double* red = reinterpret_cast<double*>(smem + align_up(size_t(2) * sm.CH * B * 4, 16));  // [warps][D + NT]
+    float* vs = reinterpret_cast<float*>(red + (kStatsSmallThreads / 32) * (D + NT));          // [CH][DM]
     __shared__ double cen_s[16];
     __shared__ double zc[32 * 16];
     const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
@@ -54,9 +57,9 @@ __global__ void __launch_bounds__(kSmallThreads) stats_small_kernel(SmallArgs a)
         float* dst = stage + (c & 1) * sm.CH * B;
         const float* src = xl + size_t(c0) * B;
         if (use_async) {
-            for (int i = tid; i < n * B / 4; i += kSmallThreads) cp_async16(dst + 4 * i, src + 4 * i);
+            for (int i = tid; i < n * B / 4; i += kStatsSmallThreads) cp_async16(dst + 4 * i, src + 4 * i);
         } else {
-            for (int i = tid; i < n * B; i += kSmallThreads) dst[i] = __ldg(src + i);
+            for (int i = tid; i < n * B; i += kStatsSmallThreads) dst[i] = __ldg(src + i);
         }
         cp_async_commit();
     };
@@ -82,7 +85,7 @@ __global__ void __launch_bounds__(kSmallThreads) stats_small_kernel(SmallArgs a)
         const int c0 = c * sm.CH, n = min(sm.CH, g.P - c0);
         const float* st = stage + (c & 1) * sm.CH * B;
         if (c == 0) {  // centre: fp64 mean of the first min(32, P) projected pixels, from the staged chunk
-            for (int i = tid; i < n0 * D; i += kSmallThreads) {
+            for (int i = tid; i < n0 * D; i += kStatsSmallThreads) {
                 const int j = i / n0, pp = i - j * n0;
                 const float* row = st + pp * B;
                 double z;
@@ -106,7 +109,7 @@ __global__ void __launch_bounds__(kSmallThreads) stats_small_kernel(SmallArgs a)
         }
         // projection: one (dim, pixel) item per thread, consecutive threads on consecutive
         // pixels of one dim (coalesced cache writes, warp-uniform nnz loop bounds)
-        for (int i = tid; i < n * D; i += kSmallThreads) {
+        for (int i = tid; i < n * D; i += kStatsSmallThreads) {
             const int j = i / n, pp = i - j * n;
             const float* row = st + pp * B;
             double z;
@@ -124,7 +127,7 @@ __global__ void __launch_bounds__(kSmallThreads) stats_small_kernel(SmallArgs a)
         }
         __syncthreads();
         // rank-1 updates: one pixel per thread
-        for (int pp = tid; pp < n; pp += kSmallThreads) {
+        for (int pp = tid; pp < n; pp += kStatsSmallThreads) {
             float v[DM];
 #pragma unroll
             for (int j = 0; j < DM; ++j) v[j] = (j < D) ? vs[pp * DM + j] : 0.f;
@@ -161,9 +164,9 @@ __global__ void __launch_bounds__(kSmallThreads) stats_small_kernel(SmallArgs a)
             }
     __syncthreads();
     double* out = a.stats + size_t(line) * (g.SE + D);
-    for (int q = tid; q < NV; q += kSmallThreads) {
+    for (int q = tid; q < NV; q += kStatsSmallThreads) {
         double v = 0.0;
-        for (int w = 0; w < kSmallThreads / 32; ++w) v += red[w * NV + q];
+        for (int w = 0; w < kStatsSmallThreads / 32; ++w) v += red[w * NV + q];
         if (q < D) {
             out[q] = cen_s[q];
             out[D + q] = v;
@@ -265,11 +268,12 @@ bool small_path(const Geometry& g) { return g.D <= 16; }
 
 SmallLaunch plan_small(const Geometry& g) {
     SmallLaunch sm{};
-    int ch = 256;
-    while (ch > 32 && size_t(2) * ch * g.B * 4 > 120 * 1024) ch /= 2;
+    // two stage buffers of ~26 KB: four CTAs per SM (HBM-bound: lines in flight matter more than chunk size)
+    int ch = int(std::min<size_t>(256, std::max<size_t>(32, (size_t(26) * 1024) / (size_t(g.B) * 4))));
+    ch = ch / 4 * 4;
     sm.CH = ch;
     const int NT = g.D * (g.D + 1) / 2;
-    sm.smem_stats = align_up(size_t(2) * ch * g.B * 4, 16) + size_t(8) * (g.D + NT) * 8 + size_t(ch) * 16 * 4;
+    sm.smem_stats = align_up(size_t(2) * ch * g.B * 4, 16) + size_t(kStatsSmallThreads / 32) * (g.D + NT) * 8 + size_t(ch) * 16 * 4;
     sm.smem_score = size_t(g.P) * 4;
     return sm;
 }
@@ -283,11 +287,11 @@ void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x
     }
     SmallArgs a{g, sm, x, n_per_stream, in_stride, stats, vcache};
     if (g.D <= 8)
-        stats_small_kernel<8><<<n_lines_total, kSmallThreads, sm.smem_stats, st>>>(a);
+        stats_small_kernel<8><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
     else if (g.D <= 12)
-        stats_small_kernel<12><<<n_lines_total, kSmallThreads, sm.smem_stats, st>>>(a);
+        stats_small_kernel<12><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
     else
-        stats_small_kernel<16><<<n_lines_total, kSmallThreads, sm.smem_stats, st>>>(a);
+        stats_small_kernel<16><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
 }
 
 void launch_score_small(const Geometry& g, const SmallLaunch& sm, const double* stats, const double* prior,
