@@ -179,7 +179,9 @@ def run_ours(args):
     P, B = cfgd["pixels"], cfgd["bands"]
     no_srp = args.mode == "full"
     cfg = pkg.ErxConfig(no_srp=no_srp, alpha=cfgd["alpha"])
-    T = args.window
+    # window (lag) per stream: the given one, else ~2048 lines per GPU per window (T = 32 at N = 1,
+    # 256 at N = 8), so each GPU's launches stay full as the fixed 64 streams spread over more GPUs
+    T = args.window if args.window else min(max(32, 2048 // S), cfgd["lines"] // 2)
     line_bytes = P * B * 4
     n_win = max(2, math.ceil(2 * L2_BYTES / (S * T * line_bytes)))
     pool_lines = n_win * T
@@ -574,7 +576,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--mode", default="full", choices=["full", "srp"])
-    ap.add_argument("--window", type=int, default=32)
+    ap.add_argument("--window", type=int, default=0, help="lines per stream per window (0: ~2048 lines per GPU)")
     ap.add_argument("--factor", type=int, default=0, choices=[0, 1, 32, 64],
                     help="factor kernel precision (ERX_OPT_FACTOR_PRECISION)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
