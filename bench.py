@@ -174,7 +174,10 @@ def run_ours(args):
     S_tot = cfgd["streams"]
     if S_tot % world:
         raise SystemExit(f"{S_tot} streams do not shard evenly over {world} ranks")
-    my_streams = list(shard_streams(S_tot, world, rank))
+    if args.shard_of and world == 1:  # one rank's share of an N-GPU run, on this GPU (scaling evidence)
+        my_streams = list(shard_streams(S_tot, args.shard_of, 0))
+    else:
+        my_streams = list(shard_streams(S_tot, world, rank))
     S = len(my_streams)
     P, B = cfgd["pixels"], cfgd["bands"]
     no_srp = args.mode == "full"
@@ -219,7 +222,7 @@ def run_ours(args):
     launches = eng.launch_count() - launches0
     torch.cuda.synchronize()
     ms_max = max_over_ranks(ms, dist, device=f"cuda:{local}")
-    lines_total = S_tot * T * args.steps
+    lines_total = S * world * T * args.steps  # = S_tot * T * steps (one rank's share with --shard-of)
     value = lines_total / (ms_max / 1e3)
 
     # per-kernel device time (CUDA events on the engine stream), separate pass
@@ -320,7 +323,7 @@ def run_ours(args):
         el_t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{local}")
         if dist:
             dist.all_reduce(el_t, op=dist.ReduceOp.MAX)
-        e2e = {"value": S_tot * T * e2e_steps / float(el_t.item()), "unit": "lines/s",
+        e2e = {"value": S * world * T * e2e_steps / float(el_t.item()), "unit": "lines/s",
                "h2d_bytes_per_step": S * T * P * B * 4, "d2h_bytes_per_step": S * T * (P * 4 * 2 + 4),
                "path": "erx_push_host (pinned) -> 5 kernels -> erx_pop (fp64 ScoredLine payload)",
                "pipelined": not args.sync_host}
@@ -343,7 +346,9 @@ def run_ours(args):
             "vs_baseline": None, "dtype": ("f32 input; stats+score exact int8-digit tcgen05 (s32 TMEM), f32 factor, f64 scan/state"
                       if tensor else "f32 (FFMA stats/whitening) + f64 (scan, Cholesky, inverse)"),
             "data": "synthetic: BASELINE.json configs[3] generator (include/erx_datagen.h), device pool >= 2x L2 replayed",
-            "config": {"workload": f"configs[{cid}]", "streams": S_tot, "streams_per_gpu": S, "pixels": P,
+            "config": {"workload": f"configs[{cid}]" + (f", rank 0 share of {args.shard_of} GPUs" if args.shard_of
+                                                       and world == 1 else ""),
+                       "streams": S * world, "streams_per_gpu": S, "pixels": P,
                        "bands": B, "dims": D, "mode": "D=B (no_srp)" if no_srp else "d=5 SRP",
                        "alpha": cfgd["alpha"], "window_lines": T, "pool_lines_per_stream": pool_lines,
                        "factor_precision": eng.factor_precision(),
@@ -585,6 +590,8 @@ def main():
     ap.add_argument("--stats", type=int, default=2, choices=[0, 1, 2],
                     help="line-statistics kernel: 0 FFMA, 1 tcgen05 bf16x3, 2 tcgen05 exact int8")
     ap.add_argument("--host-groups", type=int, default=0, help="stream groups per host window (0 auto)")
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="N=1 only: run rank 0's stream share of an N-GPU job (value is per GPU)")
     ap.add_argument("--sync-host", action="store_true", help="e2e without ERX_OPT_ASYNC_HOST (push waits for scores)")
     args = ap.parse_args()
     if args.impl == "reference":
