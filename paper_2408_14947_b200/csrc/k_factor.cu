@@ -694,7 +694,8 @@ __global__ void __launch_bounds__(256) factor_smem_kernel(Geometry g, const doub
 //   (b) panel rows: L_Ik = A_Ik Di^T (kept in Lc), and block (I, k) becomes
 //       T_Ik = -L_Ik Di; row finalisation: X_kJ = Di T_kJ (J < k);
 //   (c) Cholesky trailing update A_IJ -= L_Ik L_Jk^T (k < J <= I) and inverse
-//       update T_IJ -= L_Ik X_kJ (J < k), one block row per thread; the eight
+//       update T_IJ -= L_Ik X_kJ (J < k), one block row per thread, four
+//       blocks of one block column per warp; the eight
 //       lanes that finish block (k+1, k+1) factor and invert it in registers
 //       (8-wide shuffles) for the next step.
 // At the end every block (I, J) holds X_IJ, X = L^{-1}.
@@ -709,11 +710,30 @@ __device__ __forceinline__ void st8(float* p, const float* v) {
     *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
     *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
 }
+// Element (r, c) of a shared-memory 8x8 block lives at r * 8 + (c ^ (r & 4)): rows 4-7 keep their two
+// 16-byte halves swapped, so the eight threads of a group reading eight different rows of one block
+// touch 32 distinct banks (the plain row-major layout puts rows r and r + 4 on the same banks).
+// Aligned groups of 4 columns stay contiguous (float4 reads of the plane writer are unaffected).
+__device__ __forceinline__ int swz(int r, int c) { return r * kBlk + (c ^ (r & 4)); }
+__device__ __forceinline__ void ld8r(const float* blk, int r, float* v) {  // row r, logical column order
+    const float* p = blk + r * kBlk;
+    const int h = r & 4;
+    const float4 a = *reinterpret_cast<const float4*>(p + h);
+    const float4 b = *reinterpret_cast<const float4*>(p + (h ^ 4));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void st8r(float* blk, int r, const float* v) {
+    float* p = blk + r * kBlk;
+    const int h = r & 4;
+    *reinterpret_cast<float4*>(p + h) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(p + (h ^ 4)) = make_float4(v[4], v[5], v[6], v[7]);
+}
 
 // Eight lanes (one aligned 8-lane group, lane gl holding row gl of an updated diagonal block in
 // row[]) factor the block (Cholesky, 1/sqrt from MUFU.RSQ + one Newton step) and invert the
-// factor (lane c: column c by forward substitution).  Di goes to blk (row-major, zeros above the
-// diagonal), Di^T to dit.  Returns the first non-positive pivot (k0 + j) or -1, group-uniform.
+// factor (lane c: column c by forward substitution).  Di goes to blk (swizzled rows, zeros above the
+// diagonal), Di^T to dit (plain rows).  Returns the first non-positive pivot (k0 + j) or -1, group-uniform.
 __device__ __forceinline__ int diag_factor8(float (&row)[kBlk], unsigned gmask, int gl, int k0, float* blk,
                                             float* dit) {
     int f = -1;
@@ -744,29 +764,38 @@ __device__ __forceinline__ int diag_factor8(float (&row)[kBlk], unsigned gmask, 
         col[r] = s * rd[r];  // 0 for r < gl
     }
 #pragma unroll
-    for (int r = 0; r < kBlk; ++r) blk[r * kBlk + gl] = col[r];
+    for (int r = 0; r < kBlk; ++r) blk[swz(r, gl)] = col[r];
     st8(dit + gl * kBlk, col);
     return f;
 }
 
-__global__ void __launch_bounds__(256) factor_blk_kernel(Geometry g, const double* __restrict__ prior, double eps0,
-                                                         float* __restrict__ whiten, int* __restrict__ status,
-                                                         int* __restrict__ latch, int line_base,
-                                                         const double* __restrict__ stats,
-                                                         const float* __restrict__ vmax,
-                                                         const float* __restrict__ kblk) {
+// fp32 blocked factor, one CTA of NT threads per line.  Phase (c) hands out work by warp: a warp
+// takes a segment of four vertically adjacent blocks (I0 .. I0 + 3, J) of one block column, lane group
+// g = lane / 8 block I0 + g, lane r = lane % 8 its row r, so the 16 broadcast row loads of the
+// column's right operand (L_Jk or X_kJ) are one address per warp.  The minimum-blocks bound keeps
+// 64- and 128-thread CTAs at <= 72 registers so the seven lines that fit shared memory (configs[3]) are
+// all resident.
+template <int NT>
+__global__ void __launch_bounds__(NT, NT >= 256 ? 3 : 7) factor_blk_kernel(Geometry g, const double* __restrict__ prior,
+                                                                          double eps0, float* __restrict__ whiten,
+                                                                          int* __restrict__ status,
+                                                                          int* __restrict__ latch, int line_base,
+                                                                          const double* __restrict__ stats,
+                                                                          const float* __restrict__ vmax,
+                                                                          const float* __restrict__ kblk) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_fail;
     const int D = g.D, Dp = g.Dp, nb = g.nb;
-    // packed lower 8x8 blocks, row-major inside a block: block (I, J) at tri(I, J) * 64, row r at r * 8;
-    // padding dims carry an identity block
+    // packed lower 8x8 blocks, swizzled rows (swz): block (I, J) at tri(I, J) * 64; padding dims carry
+    // an identity block
     float* A = reinterpret_cast<float*>(smem);
     auto BP = [&](int I, int J) { return A + (I * (I + 1) / 2 + J) * 64; };
-    auto EL = [&](int i, int j) { return BP(i >> 3, j >> 3) + (i & 7) * kBlk + (j & 7); };
-    float* Lc = A + size_t(nb * (nb + 1) / 2) * 64;  // [nb][64]: the current panel L_Ik
-    float* DiT = Lc + size_t(nb) * 64;          // [64]: Di^T of the current diagonal block
-    const int line = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
-    const int lane = tid & 31, gl = lane & 7;
+    auto EL = [&](int i, int j) { return BP(i >> 3, j >> 3) + swz(i & 7, j & 7); };
+    float* Lc = A + size_t(nb * (nb + 1) / 2) * 64;  // [nb][64]: the current panel L_Ik (swizzled rows)
+    float* DiT = Lc + size_t(nb) * 64;          // [64]: Di^T of the current diagonal block (plain rows)
+    const int line = blockIdx.x, tid = threadIdx.x;
+    constexpr int nt = NT, nw = NT / 32;
+    const int lane = tid & 31, gl = lane & 7, warp = tid >> 5, grp = lane >> 3;
     const unsigned gmask = 0xffu << (lane & 24);
     const double* K = prior + size_t(line) * g.SE + D;
     double eps = eps0;
@@ -775,8 +804,8 @@ __global__ void __launch_bounds__(256) factor_blk_kernel(Geometry g, const doubl
     while (true) {
         if (tid == 0) s_fail = -1;
         if (kblk) {
-            // fill from the scan's fp32 block image: a straight 16-byte copy, then + eps on the
-            // diagonal and zeros above it inside the diagonal blocks
+            // fill from the scan's fp32 block image (same swizzled layout): a straight 16-byte copy,
+            // then + eps on the diagonal and zeros above it inside the diagonal blocks
             const int nfl = nb * (nb + 1) / 2 * 64;
             const float4* src = reinterpret_cast<const float4*>(kblk + size_t(line) * nfl);
             for (int q = tid; q < nfl / 4; q += nt) cp_async16(A + 4 * q, src + q);
@@ -786,22 +815,23 @@ __global__ void __launch_bounds__(256) factor_blk_kernel(Geometry g, const doubl
             const float fe = float(eps);
             for (int q = tid; q < nb * 64; q += nt) {
                 const int kk = q >> 6, r = (q >> 3) & 7, c = q & 7;
-                float* p = BP(kk, kk) + r * kBlk + c;
+                float* p = BP(kk, kk) + swz(r, c);
                 if (c > r) *p = 0.f;
                 else if (c == r && kk * kBlk + r < D) *p += fe;
             }
         } else {
-            // fill: coalesced reads of the packed fp64 K, 16 loads in flight per thread (the (i, j) of
+            // fill: coalesced reads of the packed fp64 K, 1024 loads in flight per line (the (i, j) of
             // idx + nt follows from (i, j) of idx incrementally)
+            constexpr int kFill = 1024 / NT;
             int i = int((sqrtf(8.f * tid + 1.f) - 1.f) * 0.5f), j;
             while (i * (i + 1) / 2 > tid) --i;
             while ((i + 1) * (i + 2) / 2 <= tid) ++i;
             j = tid - i * (i + 1) / 2;
-            for (int base = tid; base < ntri; base += 16 * nt) {
-                double v[16];
-                int ii[16], jj[16];
+            for (int base = tid; base < ntri; base += kFill * nt) {
+                double v[kFill];
+                int ii[kFill], jj[kFill];
 #pragma unroll
-                for (int u = 0; u < 16; ++u) {
+                for (int u = 0; u < kFill; ++u) {
                     const int idx = base + u * nt;
                     v[u] = idx < ntri ? __ldg(K + idx) : 0.0;
                     ii[u] = i;
@@ -813,7 +843,7 @@ __global__ void __launch_bounds__(256) factor_blk_kernel(Geometry g, const doubl
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < 16; ++u)
+                for (int u = 0; u < kFill; ++u)
                     if (base + u * nt < ntri) *EL(ii[u], jj[u]) = float(v[u] + (ii[u] == jj[u] ? eps : 0.0));
             }
         }
@@ -823,7 +853,7 @@ __global__ void __launch_bounds__(256) factor_blk_kernel(Geometry g, const doubl
         __syncthreads();
         if (tid < kBlk) {  // block (0, 0)
             float row[kBlk];
-            ld8(BP(0, 0) + gl * kBlk, row);
+            ld8r(BP(0, 0), gl, row);
             const int f = diag_factor8(row, gmask, gl, 0, BP(0, 0), DiT);
             if (gl == 0 && f >= 0) s_fail = f;
         }
@@ -831,25 +861,26 @@ __global__ void __launch_bounds__(256) factor_blk_kernel(Geometry g, const doubl
         fail = s_fail;
         for (int k = 0; k < nb && fail < 0; ++k) {
             const float* Di = BP(k, k);
-            // (b) panel rows I > k (tasks 0 ..) and finalisation of block row k (J < k)
+            // (b) panel rows I > k (tasks 0 ..) and finalisation of block row k (J < k); Di and Di^T rows
+            // are broadcasts
             const int npan = (nb - k - 1) * kBlk;
             for (int q = tid; q < npan + k * kBlk; q += nt) {
                 const int r = q & 7;
                 if (q < npan) {
                     const int I = k + 1 + (q >> 3);
-                    float* blk = BP(I, k) + r * kBlk;
+                    float* blk = BP(I, k);
                     float a[kBlk], x[kBlk], t[kBlk];
-                    ld8(blk, a);
+                    ld8r(blk, r, a);
 #pragma unroll
                     for (int c = 0; c < kBlk; ++c) {
                         float d[kBlk];
-                        ld8(Di + c * kBlk, d);
+                        ld8r(Di, c, d);
                         float s = 0.f;
 #pragma unroll
                         for (int l = 0; l <= c; ++l) s = fmaf(a[l], d[l], s);
                         x[c] = s;
                     }
-                    st8(Lc + I * 64 + r * kBlk, x);
+                    st8r(Lc + I * 64, r, x);
 #pragma unroll
                     for (int c = 0; c < kBlk; ++c) {
                         float d[kBlk];
@@ -859,67 +890,75 @@ __global__ void __launch_bounds__(256) factor_blk_kernel(Geometry g, const doubl
                         for (int l = c; l < kBlk; ++l) s = fmaf(x[l], d[l], s);
                         t[c] = -s;
                     }
-                    st8(blk, t);
+                    st8r(blk, r, t);
                 } else {
                     const int J = (q - npan) >> 3;
                     float* blk = BP(k, J);
-                    float tr[kBlk][kBlk], acc[kBlk], d[kBlk];
-#pragma unroll
-                    for (int l = 0; l < kBlk; ++l) ld8(blk + l * kBlk, tr[l]);
-                    ld8(Di + r * kBlk, d);
+                    float acc[kBlk], d[kBlk];
+                    ld8r(Di, r, d);
 #pragma unroll
                     for (int c = 0; c < kBlk; ++c) acc[c] = 0.f;
 #pragma unroll
-                    for (int l = 0; l < kBlk; ++l)
+                    for (int l = 0; l < kBlk; ++l) {
+                        float tr[kBlk];
+                        ld8r(blk, l, tr);  // broadcast across the group
 #pragma unroll
-                        for (int c = 0; c < kBlk; ++c) acc[c] = fmaf(d[l], tr[l][c], acc[c]);  // d[l] = 0 for l > r
+                        for (int c = 0; c < kBlk; ++c) acc[c] = fmaf(d[l], tr[c], acc[c]);  // d[l] = 0 for l > r
+                    }
                     __syncwarp(gmask);  // the group's reads of T_kJ precede its writes
-                    st8(blk + r * kBlk, acc);
+                    st8r(blk, r, acc);
                 }
             }
             __syncthreads();
-            // (c) trailing Cholesky pairs (I >= J > k), then inverse pairs (I > k, J < k); task = pair x row
-            const int m = nb - k - 1;
-            const int nchol = m * (m + 1) / 2 * kBlk;
-            for (int q = tid; q < nchol + m * k * kBlk; q += nt) {
-                const int r = q & 7;
+            // (c) trailing Cholesky update A_IJ -= L_Ik L_Jk^T (I >= J > k), then inverse update
+            // T_IJ -= L_Ik X_kJ (I > k, J < k), by column segments of four blocks (one per warp)
+            {
+                const int r = gl;
+                int seg = 0;
                 float a[kBlk], acc[kBlk];
-                if (q < nchol) {
-                    const int pq = q >> 3;
-                    int Ir = int((sqrtf(8.f * pq + 1.f) - 1.f) * 0.5f);
-                    while (Ir * (Ir + 1) / 2 > pq) --Ir;
-                    while ((Ir + 1) * (Ir + 2) / 2 <= pq) ++Ir;
-                    const int I = k + 1 + Ir, J = k + 1 + (pq - Ir * (Ir + 1) / 2);
-                    float* blk = BP(I, J) + r * kBlk;
-                    ld8(Lc + I * 64 + r * kBlk, a);
-                    ld8(blk, acc);
+                for (int J = k + 1; J < nb; ++J) {
+                    const float* bj = Lc + J * 64;
+                    for (int I0 = J; I0 < nb; I0 += 4, ++seg) {
+                        if ((seg & (nw - 1)) != warp) continue;
+                        const int I = I0 + grp;
+                        if (I < nb) {
+                            float* blk = BP(I, J);
+                            ld8r(Lc + I * 64, r, a);
+                            ld8r(blk, r, acc);
 #pragma unroll
-                    for (int c = 0; c < kBlk; ++c) {
-                        float b[kBlk];
-                        ld8(Lc + J * 64 + c * kBlk, b);  // broadcast: the 8 threads of a pair share it
+                            for (int c = 0; c < kBlk; ++c) {
+                                float b[kBlk];
+                                ld8r(bj, c, b);  // one address per warp
 #pragma unroll
-                        for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], b[l], acc[c]);
+                                for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], b[l], acc[c]);
+                            }
+                            st8r(blk, r, acc);
+                            if (I == k + 1 && J == k + 1) {  // block (k+1, k+1) is final: factor + invert it
+                                const int f = diag_factor8(acc, gmask, gl, (k + 1) * kBlk, blk, DiT);
+                                if (gl == 0 && f >= 0) s_fail = f;
+                            }
+                        }
                     }
-                    st8(blk, acc);
-                    if (pq == 0) {  // block (k+1, k+1) is final: factor + invert it for the next step
-                        const int f = diag_factor8(acc, gmask, gl, (k + 1) * kBlk, BP(k + 1, k + 1), DiT);
-                        if (gl == 0 && f >= 0) s_fail = f;
-                    }
-                } else {
-                    const int pq = (q - nchol) >> 3;
-                    const int I = k + 1 + pq / k, J = pq - (pq / k) * k;
-                    float* blk = BP(I, J) + r * kBlk;
+                }
+                for (int J = 0; J < k; ++J) {
                     const float* xk = BP(k, J);
-                    ld8(Lc + I * 64 + r * kBlk, a);
-                    ld8(blk, acc);
+                    for (int I0 = k + 1; I0 < nb; I0 += 4, ++seg) {
+                        if ((seg & (nw - 1)) != warp) continue;
+                        const int I = I0 + grp;
+                        if (I < nb) {
+                            float* blk = BP(I, J);
+                            ld8r(Lc + I * 64, r, a);
+                            ld8r(blk, r, acc);
 #pragma unroll
-                    for (int l = 0; l < kBlk; ++l) {
-                        float xr[kBlk];
-                        ld8(xk + l * kBlk, xr);  // broadcast across the task's 8 threads
+                            for (int l = 0; l < kBlk; ++l) {
+                                float xr[kBlk];
+                                ld8r(xk, l, xr);  // one address per warp
 #pragma unroll
-                        for (int c = 0; c < kBlk; ++c) acc[c] = fmaf(-a[l], xr[c], acc[c]);
+                                for (int c = 0; c < kBlk; ++c) acc[c] = fmaf(-a[l], xr[c], acc[c]);
+                            }
+                            st8r(blk, r, acc);
+                        }
                     }
-                    st8(blk, acc);
                 }
             }
             __syncthreads();
@@ -988,7 +1027,9 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
                    const double* stats, const float* vmax, const float* kblk) {
     const size_t sm = factor_smem(g, precision);
     if (precision == 32) {
-        ensure_smem(factor_blk_kernel, sm);
+        ensure_smem(factor_blk_kernel<64>, sm);
+        ensure_smem(factor_blk_kernel<128>, sm);
+        ensure_smem(factor_blk_kernel<256>, sm);
         // 64 threads per line when the SMs hold >= 6 lines each (configs[3]: 7 per SM by shared
         // memory); with fewer resident lines (small windows, lag 0, or D > ~150 where a line's blocks
         // take 100 KB: configs[1]) 256 threads per line shorten each line's latency instead
@@ -998,9 +1039,17 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
         cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
         const int cap = std::max(1, int(size_t(smem_sm) / (sm + 1024)));
         const int per_sm = (n_lines_total + sm_count() - 1) / sm_count();
-        const int threads = std::min(cap, per_sm) >= 6 ? 64 : 256;
-        factor_blk_kernel<<<n_lines_total, threads, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
-                                                          vmax, kblk);
+        int threads = std::min(cap, per_sm) >= 6 ? 64 : 256;
+        if (const char* ev = getenv("ERX_FACTOR_THREADS")) threads = atoi(ev);  // tuning experiments
+        if (threads == 64)
+            factor_blk_kernel<64><<<n_lines_total, 64, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
+                                                                 vmax, kblk);
+        else if (threads == 128)
+            factor_blk_kernel<128><<<n_lines_total, 128, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base,
+                                                                   stats, vmax, kblk);
+        else
+            factor_blk_kernel<256><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base,
+                                                                   stats, vmax, kblk);
     } else if (precision == 64) {
         ensure_smem(factor_smem_kernel<double>, sm);
         factor_smem_kernel<double><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base);

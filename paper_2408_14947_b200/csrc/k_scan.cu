@@ -35,7 +35,8 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
     // factor's shared-memory image) and only the mean as fp64
     const int nblk = g.nb * (g.nb + 1) / 2;
     const bool to_blk = kblk != nullptr && e >= D;
-    const int boff = ((a >> 3) * ((a >> 3) + 1) / 2 + (b >> 3)) * 64 + (a & 7) * 8 + (b & 7);
+    // the factor's swizzled block rows (k_factor.cu: swz): element (r, c) at r * 8 + (c ^ (r & 4))
+    const int boff = ((a >> 3) * ((a >> 3) + 1) / 2 + (b >> 3)) * 64 + (a & 7) * 8 + ((b & 7) ^ (a & 4));
     auto put = [&](size_t l, double pr) {
         if (to_blk)
             kblk[l * nblk * 64 + boff] = float(pr);
