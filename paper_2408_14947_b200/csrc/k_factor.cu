@@ -710,6 +710,7 @@ __device__ __forceinline__ void st8(float* p, const float* v) {
     *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
     *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
 }
+constexpr int kLcLd = 72;  // panel block stride (floats): rows of blocks J and J + 1..3 on different banks
 // Element (r, c) of a shared-memory 8x8 block lives at r * 8 + (c ^ (r & 4)): rows 4-7 keep their two
 // 16-byte halves swapped, so the eight threads of a group reading eight different rows of one block
 // touch 32 distinct banks (the plain row-major layout puts rows r and r + 4 on the same banks).
@@ -769,10 +770,7 @@ __device__ __forceinline__ int diag_factor8(float (&row)[kBlk], unsigned gmask, 
     return f;
 }
 
-// fp32 blocked factor, one CTA of NT threads per line.  Phase (c) hands out work by warp: a warp
-// takes a segment of four vertically adjacent blocks (I0 .. I0 + 3, J) of one block column, lane group
-// g = lane / 8 block I0 + g, lane r = lane % 8 its row r, so the 16 broadcast row loads of the
-// column's right operand (L_Jk or X_kJ) are one address per warp.  The minimum-blocks bound keeps
+// fp32 blocked factor, one CTA of NT threads per line.  The minimum-blocks bound keeps
 // 64- and 128-thread CTAs at <= 72 registers so the seven lines that fit shared memory (configs[3]) are
 // all resident.
 template <int NT>
@@ -791,8 +789,8 @@ __global__ void __launch_bounds__(NT, NT >= 256 ? 3 : 7) factor_blk_kernel(Geome
     float* A = reinterpret_cast<float*>(smem);
     auto BP = [&](int I, int J) { return A + (I * (I + 1) / 2 + J) * 64; };
     auto EL = [&](int i, int j) { return BP(i >> 3, j >> 3) + swz(i & 7, j & 7); };
-    float* Lc = A + size_t(nb * (nb + 1) / 2) * 64;  // [nb][64]: the current panel L_Ik (swizzled rows)
-    float* DiT = Lc + size_t(nb) * 64;          // [64]: Di^T of the current diagonal block (plain rows)
+    float* Lc = A + size_t(nb * (nb + 1) / 2) * 64;  // [nb][kLcLd]: the current panel L_Ik (swizzled rows)
+    float* DiT = Lc + size_t(nb) * kLcLd;       // [64]: Di^T of the current diagonal block (plain rows)
     const int line = blockIdx.x, tid = threadIdx.x;
     constexpr int nt = NT, nw = NT / 32;
     const int lane = tid & 31, gl = lane & 7, warp = tid >> 5, grp = lane >> 3;
@@ -880,7 +878,7 @@ __global__ void __launch_bounds__(NT, NT >= 256 ? 3 : 7) factor_blk_kernel(Geome
                         for (int l = 0; l <= c; ++l) s = fmaf(a[l], d[l], s);
                         x[c] = s;
                     }
-                    st8r(Lc + I * 64, r, x);
+                    st8r(Lc + I * kLcLd, r, x);
 #pragma unroll
                     for (int c = 0; c < kBlk; ++c) {
                         float d[kBlk];
@@ -911,52 +909,69 @@ __global__ void __launch_bounds__(NT, NT >= 256 ? 3 : 7) factor_blk_kernel(Geome
             }
             __syncthreads();
             // (c) trailing Cholesky update A_IJ -= L_Ik L_Jk^T (I >= J > k), then inverse update
-            // T_IJ -= L_Ik X_kJ (I > k, J < k), by column segments of four blocks (one per warp)
+            // T_IJ -= L_Ik X_kJ (I > k, J < k).  Task = (block pair, row r = tid % 8); pairs run
+            // column-major (stride nt / 8, decoded incrementally), so the four lane groups of a warp
+            // mostly share J and the 16 right-operand row loads are one address per warp (Lc rows
+            // of neighbouring J sit on different banks: stride kLcLd)
             {
+                constexpr int step = nt / kBlk;
                 const int r = gl;
-                int seg = 0;
+                const int m = nb - k - 1;
                 float a[kBlk], acc[kBlk];
-                for (int J = k + 1; J < nb; ++J) {
-                    const float* bj = Lc + J * 64;
-                    for (int I0 = J; I0 < nb; I0 += 4, ++seg) {
-                        if ((seg & (nw - 1)) != warp) continue;
-                        const int I = I0 + grp;
-                        if (I < nb) {
-                            float* blk = BP(I, J);
-                            ld8r(Lc + I * 64, r, a);
-                            ld8r(blk, r, acc);
+                int jr = 0, ir = tid >> 3;  // trailing pair: column jr, row ir (relative to k + 1), ir >= jr
+                while (ir >= m && jr < m) {
+                    ir = ir - m + jr + 1;
+                    ++jr;
+                }
+                for (; jr < m;) {
+                    const int I = k + 1 + ir, J = k + 1 + jr;
+                    float* blk = BP(I, J);
+                    const float* bj = Lc + J * kLcLd;
+                    ld8r(Lc + I * kLcLd, r, a);
+                    ld8r(blk, r, acc);
 #pragma unroll
-                            for (int c = 0; c < kBlk; ++c) {
-                                float b[kBlk];
-                                ld8r(bj, c, b);  // one address per warp
+                    for (int c = 0; c < kBlk; ++c) {
+                        float b[kBlk];
+                        ld8r(bj, c, b);
 #pragma unroll
-                                for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], b[l], acc[c]);
-                            }
-                            st8r(blk, r, acc);
-                            if (I == k + 1 && J == k + 1) {  // block (k+1, k+1) is final: factor + invert it
-                                const int f = diag_factor8(acc, gmask, gl, (k + 1) * kBlk, blk, DiT);
-                                if (gl == 0 && f >= 0) s_fail = f;
-                            }
-                        }
+                        for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], b[l], acc[c]);
+                    }
+                    st8r(blk, r, acc);
+                    if (ir == 0) {  // block (k+1, k+1) is final: factor + invert it for the next step
+                        const int f = diag_factor8(acc, gmask, gl, (k + 1) * kBlk, blk, DiT);
+                        if (gl == 0 && f >= 0) s_fail = f;
+                    }
+                    ir += step;
+                    while (ir >= m && jr < m) {
+                        ir = ir - m + jr + 1;
+                        ++jr;
                     }
                 }
-                for (int J = 0; J < k; ++J) {
-                    const float* xk = BP(k, J);
-                    for (int I0 = k + 1; I0 < nb; I0 += 4, ++seg) {
-                        if ((seg & (nw - 1)) != warp) continue;
-                        const int I = I0 + grp;
-                        if (I < nb) {
-                            float* blk = BP(I, J);
-                            ld8r(Lc + I * 64, r, a);
-                            ld8r(blk, r, acc);
+                // inverse pairs: the flat index continues past the m (m + 1) / 2 trailing pairs
+                if (k > 0 && m > 0) {
+                    int J;
+                    // ir - m + jr + 1 overshoots as if column m had rows from m: rebase to the inverse range
+                    ir = ir - jr;  // == flat index past the trailing pairs (jr == m here)
+                    J = ir / m;
+                    ir -= J * m;
+                    for (; J < k;) {
+                        const int I = k + 1 + ir;
+                        float* blk = BP(I, J);
+                        const float* xk = BP(k, J);
+                        ld8r(Lc + I * kLcLd, r, a);
+                        ld8r(blk, r, acc);
 #pragma unroll
-                            for (int l = 0; l < kBlk; ++l) {
-                                float xr[kBlk];
-                                ld8r(xk, l, xr);  // one address per warp
+                        for (int l = 0; l < kBlk; ++l) {
+                            float xr[kBlk];
+                            ld8r(xk, l, xr);
 #pragma unroll
-                                for (int c = 0; c < kBlk; ++c) acc[c] = fmaf(-a[l], xr[c], acc[c]);
-                            }
-                            st8r(blk, r, acc);
+                            for (int c = 0; c < kBlk; ++c) acc[c] = fmaf(-a[l], xr[c], acc[c]);
+                        }
+                        st8r(blk, r, acc);
+                        ir += step;
+                        while (ir >= m) {
+                            ir -= m;
+                            ++J;
                         }
                     }
                 }
@@ -992,8 +1007,8 @@ __global__ void __launch_bounds__(NT, NT >= 256 ? 3 : 7) factor_blk_kernel(Geome
 }  // namespace
 
 size_t factor_blk_smem(const Geometry& g) {
-    // packed blocks + Lc + Di^T (the plane writer's 1.5 KB scratch reuses Lc + Di^T)
-    return (size_t(g.nb) * (g.nb + 1) / 2 + std::max(g.nb + 1, 6)) * 64 * 4;
+    // packed blocks + Lc (kLcLd per block) + Di^T (the plane writer's 1.5 KB scratch reuses Lc + Di^T)
+    return (size_t(g.nb) * (g.nb + 1) / 2 * 64 + std::max<size_t>(size_t(g.nb) * kLcLd + 64, 6 * 64)) * 4;
 }
 
 // factor_big: Lkk + Di, the transposed panel, and (when it fits) the finished X block row
@@ -1030,7 +1045,7 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
         ensure_smem(factor_blk_kernel<64>, sm);
         ensure_smem(factor_blk_kernel<128>, sm);
         ensure_smem(factor_blk_kernel<256>, sm);
-        // 64 threads per line when the SMs hold >= 6 lines each (configs[3]: 7 per SM by shared
+        // 128 threads per line when the SMs hold >= 6 lines each (configs[3]: 7 per SM by shared
         // memory); with fewer resident lines (small windows, lag 0, or D > ~150 where a line's blocks
         // take 100 KB: configs[1]) 256 threads per line shorten each line's latency instead
         int dev = 0;
@@ -1039,7 +1054,7 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
         cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
         const int cap = std::max(1, int(size_t(smem_sm) / (sm + 1024)));
         const int per_sm = (n_lines_total + sm_count() - 1) / sm_count();
-        int threads = std::min(cap, per_sm) >= 6 ? 64 : 256;
+        int threads = std::min(cap, per_sm) >= 6 ? 128 : 256;
         if (const char* ev = getenv("ERX_FACTOR_THREADS")) threads = atoi(ev);  // tuning experiments
         if (threads == 64)
             factor_blk_kernel<64><<<n_lines_total, 64, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
