@@ -773,8 +773,8 @@ __device__ __forceinline__ int diag_factor8(float (&row)[kBlk], unsigned gmask, 
 // fp32 blocked factor, one CTA of NT threads per line.  The minimum-blocks bound keeps
 // 64- and 128-thread CTAs at <= 72 registers so the seven lines that fit shared memory (configs[3]) are
 // all resident.
-template <int NT>
-__global__ void __launch_bounds__(NT, NT >= 256 ? 3 : 7) factor_blk_kernel(Geometry g, const double* __restrict__ prior,
+template <int NT, int MB>
+__global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const double* __restrict__ prior,
                                                                           double eps0, float* __restrict__ whiten,
                                                                           int* __restrict__ status,
                                                                           int* __restrict__ latch, int line_base,
@@ -919,6 +919,25 @@ __global__ void __launch_bounds__(NT, NT >= 256 ? 3 : 7) factor_blk_kernel(Geome
                 const int m = nb - k - 1;
                 float a[kBlk], acc[kBlk];
                 int jr = 0, ir = tid >> 3;  // trailing pair: column jr, row ir (relative to k + 1), ir >= jr
+                if (ir == 0 && m > 0) {
+                    // pair 0 = block (k+1, k+1) first, outside the loop (keeps the loop's registers low):
+                    // update, then factor + invert it for the next step
+                    float* blk = BP(k + 1, k + 1);
+                    const float* bj = Lc + (k + 1) * kLcLd;
+                    ld8r(bj, r, a);
+                    ld8r(blk, r, acc);
+#pragma unroll
+                    for (int c = 0; c < kBlk; ++c) {
+                        float b[kBlk];
+                        ld8r(bj, c, b);
+#pragma unroll
+                        for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], b[l], acc[c]);
+                    }
+                    st8r(blk, r, acc);
+                    const int f = diag_factor8(acc, gmask, gl, (k + 1) * kBlk, blk, DiT);
+                    if (gl == 0 && f >= 0) s_fail = f;
+                    ir = step;
+                }
                 while (ir >= m && jr < m) {
                     ir = ir - m + jr + 1;
                     ++jr;
@@ -937,10 +956,6 @@ __global__ void __launch_bounds__(NT, NT >= 256 ? 3 : 7) factor_blk_kernel(Geome
                         for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], b[l], acc[c]);
                     }
                     st8r(blk, r, acc);
-                    if (ir == 0) {  // block (k+1, k+1) is final: factor + invert it for the next step
-                        const int f = diag_factor8(acc, gmask, gl, (k + 1) * kBlk, blk, DiT);
-                        if (gl == 0 && f >= 0) s_fail = f;
-                    }
                     ir += step;
                     while (ir >= m && jr < m) {
                         ir = ir - m + jr + 1;
@@ -1042,9 +1057,9 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
                    const double* stats, const float* vmax, const float* kblk) {
     const size_t sm = factor_smem(g, precision);
     if (precision == 32) {
-        ensure_smem(factor_blk_kernel<64>, sm);
-        ensure_smem(factor_blk_kernel<128>, sm);
-        ensure_smem(factor_blk_kernel<256>, sm);
+        ensure_smem(factor_blk_kernel<64, 7>, sm);
+        ensure_smem(factor_blk_kernel<128, 7>, sm);
+        ensure_smem(factor_blk_kernel<256, 3>, sm);
         // 128 threads per line when the SMs hold >= 6 lines each (configs[3]: 7 per SM by shared
         // memory); with fewer resident lines (small windows, lag 0, or D > ~150 where a line's blocks
         // take 100 KB: configs[1]) 256 threads per line shorten each line's latency instead
@@ -1057,13 +1072,13 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
         int threads = std::min(cap, per_sm) >= 6 ? 128 : 256;
         if (const char* ev = getenv("ERX_FACTOR_THREADS")) threads = atoi(ev);  // tuning experiments
         if (threads == 64)
-            factor_blk_kernel<64><<<n_lines_total, 64, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
+            factor_blk_kernel<64, 7><<<n_lines_total, 64, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
                                                                  vmax, kblk);
         else if (threads == 128)
-            factor_blk_kernel<128><<<n_lines_total, 128, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base,
+            factor_blk_kernel<128, 7><<<n_lines_total, 128, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base,
                                                                    stats, vmax, kblk);
         else
-            factor_blk_kernel<256><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base,
+            factor_blk_kernel<256, 3><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base,
                                                                    stats, vmax, kblk);
     } else if (precision == 64) {
         ensure_smem(factor_smem_kernel<double>, sm);
