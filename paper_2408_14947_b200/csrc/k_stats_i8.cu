@@ -94,6 +94,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* m) {
 // accfull / accempty, so copies, quantisation and MMAs of different chunks
 // overlap.  The epilogue of line k-1 runs after pass 1 of line k, when the
 // MMAs of line k-1 have long finished.
+// kBT > 0: the band count as a compile-time constant (the pixel stride of every shared-memory chunk
+// access folds into immediate offsets); 0: runtime g.B
+template <int kBT>
 __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args a) {
     extern __shared__ __align__(1024) unsigned char smem[];
     __shared__ uint32_t tmem_slot;
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
 
     const Geometry& g = a.g;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int B = g.B, D = g.D, P = g.P;
+    const int B = kBT > 0 ? kBT : g.B, D = g.D, P = g.P;
     const int NS = a.stages;
 
     unsigned char* ops = smem;                                   // [2][kOps]
@@ -437,11 +440,15 @@ bool stats_i8_eligible(const Geometry& g) {
 void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
                      double* stats, float* vmax, unsigned char* vplanes, cudaStream_t st) {
     const int sms = sm_count();
-    ensure_smem(stats_i8_kernel, kSmemCap - kStaticSmem);
+    ensure_smem(stats_i8_kernel<0>, kSmemCap - kStaticSmem);
+    ensure_smem(stats_i8_kernel<108>, kSmemCap - kStaticSmem);
     StatsI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, vmax, vplanes, (g.D + 1 + 15) / 16 * 16,
                   i8_stages(g)};
     const int grid = n_lines_total < sms ? n_lines_total : sms;
-    stats_i8_kernel<<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
+    if (g.B == 108)  // configs[0] / configs[3]
+        stats_i8_kernel<108><<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
+    else
+        stats_i8_kernel<0><<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
 }
 
 }  // namespace erxk
