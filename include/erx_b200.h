@@ -163,6 +163,11 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
  * FactorizationError is reported by the call that harvests it (erx_ready
  * defers it to the next erx_pop / push / finish). */
 #define ERX_OPT_ASYNC_HOST 4
+/* ERX_OPT_FACTOR_THREADS: threads per line of the blocked fp32 shared-memory
+ * factor (precision 32).  0 (default) picks 128 when every SM holds >= 6 lines
+ * of a launch, else 256; 64, 128 or 256 force that CTA size (same results to
+ * rounding; a tuning and test hook). */
+#define ERX_OPT_FACTOR_THREADS 5
 int erx_set_option(erx_engine* e, int option, int64_t value);
 int64_t erx_get_option(const erx_engine* e, int option);
 

@@ -26,6 +26,7 @@ OPT_FACTOR_PRECISION = 1
 OPT_STATS_TENSOR = 2
 OPT_HOST_GROUPS = 3
 OPT_ASYNC_HOST = 4
+OPT_FACTOR_THREADS = 5
 
 
 class ErxConfigC(C.Structure):

@@ -89,6 +89,7 @@ struct erx_engine {
     // bf16x3 stats (fp32 TMEM accumulation truncates, tools/tc_bias.py), 0 FFMA kernels.
     int stats_tensor = 2;
     int factor_prec = 0;  // precision in use (0 = blocked fp64 global path)
+    int factor_threads = 0;  // ERX_OPT_FACTOR_THREADS (0 auto)
     bool tensor = false;      // exact-integer tcgen05 stats + score in use (fixed at configure)
     size_t white_stride = 0;  // floats per line of d_white (fp32 W blocks or int8 W planes)
 
@@ -381,7 +382,7 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     }
     timed(e, ERX_KERNEL_FACTOR, [&] {
         erxk::launch_factor(g, prior, L, e->cfg.epsilon, work, white, status, e->d_latch, line_base, e->factor_prec,
-                            e->stream, stats, tensor ? vmax : nullptr, kblk);
+                            e->stream, stats, tensor ? vmax : nullptr, kblk, e->factor_threads);
     });
     if (e->small) {  // score + normalisation fused
         timed(e, ERX_KERNEL_SCORE, [&] {
@@ -921,6 +922,12 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
         e->async_host = value != 0;
         return ERX_OK;
     }
+    if (option == ERX_OPT_FACTOR_THREADS) {
+        if (value != 0 && value != 64 && value != 128 && value != 256)
+            return fail(e, ERX_ERR_CONFIG, "factor threads: 0, 64, 128 or 256");
+        e->factor_threads = int(value);
+        return ERX_OK;
+    }
     if (option == ERX_OPT_HOST_GROUPS) {
         if (value < 0 || value > erx_engine::kMaxGroups) return fail(e, ERX_ERR_CONFIG, "host groups: 0..8");
         e->host_groups = int(value);
@@ -953,6 +960,7 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
 int64_t erx_get_option(const erx_engine* e, int option) {
     if (option == ERX_OPT_FACTOR_PRECISION) return e->d_stats ? e->factor_prec : e->factor_req;
     if (option == ERX_OPT_HOST_GROUPS) return e->host_groups;
+    if (option == ERX_OPT_FACTOR_THREADS) return e->factor_threads;
     if (option == ERX_OPT_ASYNC_HOST) return e->async_host ? 1 : 0;
     if (option == ERX_OPT_STATS_TENSOR) {
         if (!e->d_stats) return e->stats_tensor;

@@ -120,7 +120,8 @@ void launch_scan(const Geometry& g, const double* stats, double* prior, const do
 // i8::kWBytes per line) instead of the fp32 blocks.
 void launch_factor(const Geometry& g, const double* prior, int n_lines_total, double eps0, double* work,
                    float* whiten, int* status, int* latch, int line_base, int precision, cudaStream_t st,
-                   const double* stats = nullptr, const float* vmax = nullptr, const float* kblk = nullptr);
+                   const double* stats = nullptr, const float* vmax = nullptr, const float* kblk = nullptr,
+                   int blk_threads = 0);
 void launch_score(const Geometry& g, const ScoreLaunch& sc, const float* x, int n_per_stream, int in_stride,
                   const double* prior, const float* whiten, int n_lines_total, float* raw, cudaStream_t st);
 void launch_normalize(const Geometry& g, const float* raw, int n_lines_total, float* norm, cudaStream_t st);

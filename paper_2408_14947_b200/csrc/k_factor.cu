@@ -1054,7 +1054,7 @@ int factor_precision(const Geometry& g, int requested) {
 
 void launch_factor(const Geometry& g, const double* prior, int n_lines_total, double eps0, double* work,
                    float* whiten, int* status, int* latch, int line_base, int precision, cudaStream_t st,
-                   const double* stats, const float* vmax, const float* kblk) {
+                   const double* stats, const float* vmax, const float* kblk, int blk_threads) {
     const size_t sm = factor_smem(g, precision);
     if (precision == 32) {
         ensure_smem(factor_blk_kernel<64, 7>, sm);
@@ -1070,7 +1070,7 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
         const int cap = std::max(1, int(size_t(smem_sm) / (sm + 1024)));
         const int per_sm = (n_lines_total + sm_count() - 1) / sm_count();
         int threads = std::min(cap, per_sm) >= 6 ? 128 : 256;
-        if (const char* ev = getenv("ERX_FACTOR_THREADS")) threads = atoi(ev);  // tuning experiments
+        if (blk_threads) threads = blk_threads;  // ERX_OPT_FACTOR_THREADS
         if (threads == 64)
             factor_blk_kernel<64, 7><<<n_lines_total, 64, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
                                                                  vmax, kblk);

@@ -263,6 +263,10 @@ class Engine:
         """0 auto, 32 or 64 (see ERX_OPT_FACTOR_PRECISION in include/erx_b200.h)."""
         self._check(self._lib.erx_set_option(self._h, L.OPT_FACTOR_PRECISION, bits))
 
+    def set_factor_threads(self, threads: int):
+        """Threads per line of the blocked fp32 factor: 0 auto, 64, 128 or 256 (ERX_OPT_FACTOR_THREADS)."""
+        self._check(self._lib.erx_set_option(self._h, L.OPT_FACTOR_THREADS, int(threads)))
+
     def set_stats_tensor(self, kind: int):
         """Line-statistics kernel: 0 FFMA, 1 tcgen05 bf16x3, 2 tcgen05 exact int8 (ERX_OPT_STATS_TENSOR)."""
         self._check(self._lib.erx_set_option(self._h, L.OPT_STATS_TENSOR, int(kind)))

@@ -258,6 +258,25 @@ def test_factor_kernel_variants(pkg, oracle, cid, n_lines, prec):
     check_gates(oracle, raw_g[0], norm_g[0], raw_o, norm_o, mask=mask, warm=warm, label=f"c{cid} factor{prec}")
 
 
+@pytest.mark.parametrize("threads", [64, 128, 256])
+def test_factor_blk_cta_sizes(pkg, oracle, threads):
+    """The blocked fp32 factor at every CTA size (ERX_OPT_FACTOR_THREADS) meets the gates on a
+    full-occupancy window (configs[3] streams: 16 x 32 lines) and agrees across sizes to rounding."""
+    spec = pkg.gen_spec(3)
+    streams = list(range(16))
+    lines = np.stack([pkg.gen_lines(spec, s, 32)[0] for s in streams])
+    cfg = pkg.ErxConfig(no_srp=True, alpha=0.1, buffer_len=4)
+    eng = pkg.Engine(cfg, spec.bands, n_streams=len(streams), window_lines=32)
+    eng.set_factor_threads(threads)
+    eng.push(lines, 0)
+    eng.finish()
+    assert eng.factor_precision() == 32
+    _, wu, raw_g, norm_g = eng.pop()
+    for i in (0, 7, 15):
+        raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), lines[i])
+        check_gates(oracle, raw_g[i], norm_g[i], raw_o, norm_o, label=f"factor threads {threads} stream {i}")
+
+
 @pytest.mark.parametrize("tensor", [pytest.param(1, marks=pytest.mark.xfail(
     reason="tcgen05 fp32 accumulation truncates (tools/tc_bias.py): median gate missed", strict=False)), 0, 2])
 def test_stats_kernel_variants(pkg, oracle, tensor):
