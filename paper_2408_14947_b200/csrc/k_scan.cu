@@ -12,6 +12,13 @@
 namespace erxk {
 namespace {
 
+// mu_hat = c + s / P or K_hat = (S - s_a s_b / P) / (P - 1) from the stats slot values x0 (c or S),
+// x1, x2 (s_a, s_b); explicit roundings (no FMA contraction) so every scan variant agrees bitwise
+__device__ __forceinline__ double finish_stat(bool is_mu, double x0, double x1, double x2, double invP, double invP1) {
+    return is_mu ? __dadd_rn(x0, __dmul_rn(x1, invP))
+                 : __dmul_rn(__dsub_rn(x0, __dmul_rn(__dmul_rn(x1, x2), invP)), invP1);
+}
+
 __device__ __forceinline__ void unpack_tri(int k, int& a, int& b) {
     a = int((sqrt(8.0 * k + 1.0) - 1.0) * 0.5);
     while (a * (a + 1) / 2 > k) --a;
@@ -69,7 +76,7 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
             }
 #pragma unroll
             for (int u = 0; u < kB; ++u)
-                buf[u] = is_mu ? x0[u] + x1[u] * invP : (x0[u] - x1[u] * x2[u] * invP) * invP1;
+                buf[u] = finish_stat(is_mu, x0[u], x1[u], x2[u], invP, invP1);
         };
         load(0, cur);
         for (int t0 = 0; t0 < n; t0 += kB) {
@@ -129,11 +136,141 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Few elements, long windows (a single stream at small D: configs[2] has 20
+// state elements and up to thousands of lines per window): the element-
+// parallel kernel above runs one warp through every line, each step waiting on
+// its own global loads.  Here one CTA takes 32 elements of one stream; per
+// chunk of TC lines the other warps finish the line statistics into shared memory
+// (all loads in flight at once) and write back the chunk before last, while
+// warp 0 runs the recurrence over the previous chunk from shared memory.  The
+// per-element arithmetic and its order are exactly the kernel above's (EMA
+// mode), so the results are bit-identical.
+// ---------------------------------------------------------------------------
+template <int TC, int NTH, int kU>
+__global__ void __launch_bounds__(NTH) scan_chunk_kernel(Geometry g, const double* __restrict__ stats,
+                                                         double* __restrict__ prior, const double* __restrict__ st_in,
+                                                         double* __restrict__ st_out, int n, int initialized,
+                                                         double alpha, float* __restrict__ kblk) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* kh = reinterpret_cast<double*>(smem);  // [2][TC][32] finished line statistics
+    double* ps = kh + 2 * TC * 32;                 // [2][TC][32] pre-update background
+    __shared__ int o0_s[32], o1_s[32], o2_s[32], boff_s[32];
+    const int s = blockIdx.y, e0 = blockIdx.x * 32;
+    const int ne = min(32, g.SE - e0);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int D = g.D, SS = g.SE + g.D;
+    const double P = double(g.P), invP = 1.0 / P, invP1 = 1.0 / (P - 1.0);
+    const int nblk = g.nb * (g.nb + 1) / 2;
+    if (tid < 32) {
+        const int e = e0 + min(tid, ne - 1);
+        int a = e, b = e;
+        if (e >= D) unpack_tri(e - D, a, b);
+        const bool is_mu = e < D;
+        o0_s[tid] = is_mu ? e : 2 * D + (e - D);
+        o1_s[tid] = D + a;
+        o2_s[tid] = D + b;
+        boff_s[tid] = (kblk != nullptr && e >= D)
+                          ? ((a >> 3) * ((a >> 3) + 1) / 2 + (b >> 3)) * 64 + (a & 7) * 8 + ((b & 7) ^ (a & 4))
+                          : -1;
+    }
+    __syncthreads();
+    const size_t l0 = size_t(s) * n;
+    const int nch = (n + TC - 1) / TC;
+    double state = (lane < ne) ? st_in[size_t(s) * g.SE + e0 + lane] : 0.0;
+    const double om = 1.0 - alpha;
+    for (int it = 0; it <= nch + 1; ++it) {
+        if (warp == 0) {
+            // recurrence over chunk it - 1
+            const int c = it - 1;
+            if (c >= 0 && c < nch) {
+                const double* kc = kh + (c & 1) * TC * 32;
+                double* pc = ps + (c & 1) * TC * 32;
+                const int nt = min(TC, n - c * TC);
+#pragma unroll 8
+                for (int t = 0; t < nt; ++t) {
+                    const double cur = kc[t * 32 + lane];
+                    double pr;
+                    if (!initialized && c == 0 && t == 0) {
+                        pr = cur;
+                        state = cur;
+                    } else {
+                        pr = state;
+                        state = __dadd_rn(__dmul_rn(om, state), __dmul_rn(alpha, cur));
+                    }
+                    pc[t * 32 + lane] = pr;
+                }
+            }
+        } else {
+            const int q0 = tid - 32, nq = NTH - 32;
+            // finish the line statistics of chunk it
+            if (it < nch) {
+                double* kc = kh + (it & 1) * TC * 32;
+                const int nt = min(TC, n - it * TC);
+                // batches of kU items per thread: all 3 kU loads in flight before any is used
+                for (int qb = q0; qb < nt * 32; qb += kU * nq) {
+                    double x0[kU], x1[kU], x2[kU];
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        const int q = min(qb + u * nq, nt * 32 - 1);
+                        const int t = q >> 5, j = q & 31;
+                        const double* st = stats + (l0 + size_t(it) * TC + t) * SS;
+                        x0[u] = __ldg(st + o0_s[j]);
+                        x1[u] = __ldg(st + o1_s[j]);
+                        x2[u] = __ldg(st + o2_s[j]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        const int q = qb + u * nq;
+                        if (q < nt * 32) kc[q] = finish_stat(e0 + (q & 31) < D, x0[u], x1[u], x2[u], invP, invP1);
+                    }
+                }
+            }
+            // write back chunk it - 2
+            const int c = it - 2;
+            if (c >= 0) {
+                const double* pc = ps + (c & 1) * TC * 32;
+                const int nt = min(TC, n - c * TC);
+                for (int q = q0; q < nt * 32; q += nq) {
+                    const int t = q >> 5, j = q & 31;
+                    if (j >= ne) continue;
+                    const size_t l = l0 + size_t(c) * TC + t;
+                    if (boff_s[j] >= 0)
+                        kblk[l * nblk * 64 + boff_s[j]] = float(pc[q]);
+                    else
+                        prior[l * g.SE + e0 + j] = pc[q];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (warp == 0 && lane < ne) st_out[size_t(s) * g.SE + e0 + lane] = state;
+}
+
 }  // namespace
 
 void launch_scan(const Geometry& g, const double* stats, double* prior, const double* state_in, double* state_out,
                  int n_streams, int n_per_stream, int initialized, double alpha, int incremental, int64_t n_seen0,
                  cudaStream_t st, float* kblk) {
+    const int blocks_plain = (g.SE + 127) / 128 * n_streams;
+    if (!incremental && blocks_plain < 2 * sm_count() && n_per_stream >= 64) {
+        // too few elements to hide the per-line load latency: chunked variant
+        dim3 grid((g.SE + 31) / 32, n_streams);
+        const int ctas = int(grid.x * grid.y);
+        if (ctas <= sm_count()) {
+            const size_t sm = 2 * size_t(2) * 128 * 32 * sizeof(double);
+            ensure_smem(scan_chunk_kernel<128, 512, 9>, sm);  // 4096 items per chunk: one batch per thread
+            scan_chunk_kernel<128, 512, 9><<<grid, 512, sm, st>>>(g, stats, prior, state_in, state_out, n_per_stream,
+                                                           initialized, alpha, kblk);
+        } else {
+            const size_t sm = 2 * size_t(2) * 32 * 32 * sizeof(double);
+            ensure_smem(scan_chunk_kernel<32, 256, 5>, sm);  // 1024 items per chunk
+            scan_chunk_kernel<32, 256, 5><<<grid, 256, sm, st>>>(g, stats, prior, state_in, state_out, n_per_stream,
+                                                         initialized, alpha, kblk);
+        }
+        return;
+    }
     dim3 grid((g.SE + 127) / 128, n_streams);
     scan_kernel<<<grid, 128, 0, st>>>(g, stats, prior, state_in, state_out, n_per_stream, initialized, alpha,
                                       incremental, n_seen0, kblk);

@@ -98,6 +98,23 @@ def test_window_size_is_bitwise_invariant(pkg):
         assert np.array_equal(run_gpu(pkg, cfg, lines, w)[0], ref)
 
 
+@pytest.mark.parametrize("cid,no_srp", [(2, False), (2, True), (0, True)])
+def test_chunked_scan_matches_plain_scan(pkg, oracle, cid, no_srp):
+    """Single-stream windows of >= 64 lines take the chunked scan (k_scan.cu: scan_chunk_kernel; one
+    CTA per 32 state elements, 128- or 32-line chunks); short windows the element-parallel one.  Same
+    arithmetic in the same order: bit-identical scores, and the oracle's gates."""
+    spec = pkg.gen_spec(cid)
+    n = 300
+    lines, mask = pkg.gen_lines(spec, 0, n)
+    cfg = pkg.ErxConfig(no_srp=no_srp, alpha=0.1, buffer_len=20)
+    ref = run_gpu(pkg, cfg, lines, 16)  # 16-line windows: plain scan
+    for w in (64, 150, 300):            # chunked scan, ragged last chunk
+        got = run_gpu(pkg, cfg, lines, w)
+        assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1]), f"window {w}"
+    raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), lines)
+    check_gates(oracle, ref[0], ref[1], raw_o, norm_o, label=f"c{cid} chunked scan")
+
+
 def test_batched_streams_equal_single_streams(pkg):
     S, n = 3, 24
     lines = np.stack([pkg.gen_lines(pkg.gen_spec(3, s), 0, n)[0] for s in range(S)])
