@@ -73,6 +73,7 @@ struct erx_engine {
     int* d_srp_band = nullptr;
     float* d_srp_sign = nullptr;
     double srp_scale = 1.0;
+    int srp_wmax = 0;  // max nonzeros per output dim
 
     uint32_t P = 0;  // pixels (set by the first line)
     Geometry geo{};
@@ -265,6 +266,7 @@ int configure(erx_engine* e, uint32_t P) {
     g.srp_band = e->d_srp_band;
     g.srp_w = e->d_srp_sign;
     g.srp_scale = e->srp_scale;
+    g.srp_wmax = e->srp_wmax;
     e->sl = erxk::plan_stats(g);
     e->sc = erxk::plan_score(g);
     e->small = erxk::small_path(g);
@@ -625,6 +627,7 @@ int erx_create(const erx_config* cfg, uint32_t bands, uint32_t n_streams, uint32
             }
         }
         ptr[e->D] = int(band.size());
+        for (int j = 0; j < e->D; ++j) e->srp_wmax = std::max(e->srp_wmax, ptr[j + 1] - ptr[j]);
     }
     const size_t nnz = std::max<size_t>(band.size(), 1);
     if (cudaMalloc(&e->d_srp_ptr, ptr.size() * sizeof(int)) != cudaSuccess ||

@@ -41,6 +41,7 @@ struct Geometry {
     const int* srp_band;   // [nnz] band index
     const float* srp_w;    // [nnz] sign of the weight (+1 / -1)
     double srp_scale;      // |w| = sqrt(s)/sqrt(d); z_j = scale * sum_k sign_k x_k (fp64)
+    int srp_wmax;          // max nonzeros of one output dim (the small path's padded table width)
 };
 
 struct StatsLaunch {
@@ -55,7 +56,8 @@ struct StatsLaunch {
 };
 
 struct SmallLaunch {
-    int CH;             // pixels staged per chunk
+    int CH;             // pixels per warp chunk (identity projection)
+    int CH2;            // pixels per shared stage (SRP variant)
     size_t smem_stats;
     size_t smem_score;
 };

@@ -7,7 +7,10 @@
 //                pixel once (project_line, projection.hpp:31-34; fp64 sums),
 //                accumulates sum(v) and sum(v v^T) with v = z - c
 //                (line_stats, erx.hpp:38-40), and writes v (fp32, dim-major)
-//                to a small per-line cache — D floats per pixel instead of B;
+//                to a small per-line cache — D floats per pixel instead of B.
+//                Identity projection (narrow lines, configs[2]): warps stream
+//                their own chunks, a lane per pixel, no per-chunk barrier;
+//                SRP (d = 5 default): (dim, pixel) items over shared stages;
 //   score_small  one CTA per line: reads the cache, whitens with W = L^{-1}
 //                (forward_substitute, linalg.hpp:21), and z-normalises the
 //                line in the same kernel (normalize_scores, detector.hpp:29-32).
@@ -21,7 +24,7 @@ namespace erxk {
 namespace {
 
 constexpr int kSmallThreads = 256;       // score_small
-constexpr int kStatsSmallThreads = 128;  // stats_small: 4 CTAs (lines) per SM keep more chunks in flight
+constexpr int kStatsSmallThreads = 128;  // stats_small: 4 warps per line, two lines per SM
 
 struct SmallArgs {
     Geometry g;
@@ -33,17 +36,182 @@ struct SmallArgs {
     float* vcache;  // [line][D][P]
 };
 
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem_src));
+}
+
+// One CTA (kStatsSmallThreads / 32 warps) per line.  The warps stream the line's pixel chunks
+// round-robin, each through its own double-buffered cp.async stage (no CTA barrier inside the line):
+// a lane projects whole pixels (every output dim, fp64), writes v = z - c to the cache and keeps fp32
+// partial sums of v and v v^T; one barrier at the end reduces the warps' partials in fixed order.
+// Warp 0 derives the centre c (fp64 mean of the first min(32, P) projected pixels) while the first
+// chunks load.
 template <int DM>
 __global__ void __launch_bounds__(kStatsSmallThreads) stats_small_kernel(SmallArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int kW = kStatsSmallThreads / 32;
+    constexpr int DT = DM * (DM + 1) / 2;
     const Geometry& g = a.g;
-    const SmallLaunch& sm = a.sm;
+    const int line = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int D = g.D, B = g.B, P = g.P;
+    const int CH = a.sm.CH;  // pixels per warp chunk
+    float* buf = reinterpret_cast<float*>(smem) + size_t(warp) * 2 * CH * B;  // [2][CH][B] per warp
+    const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
+    float* vc = a.vcache + size_t(line) * D * P;
+
+    __shared__ double cen_s[DM];
+    // SRP table padded to srp_wmax entries per dim (weight 0 past a dim's nonzeros, band = its first
+    // band), [DM][wmax] in shared memory after the stages: the dims' chains interleave, and a zero
+    // term leaves the fp64 sum unchanged (same value as the sequential CSC sum)
+    const int WM = g.srp ? g.srp_wmax : 0;
+    double* ew = reinterpret_cast<double*>(smem + a.sm.smem_stats - size_t(DM) * WM * 12);
+    int* eb = reinterpret_cast<int*>(ew + DM * WM);
+    auto zrow = [&](const float* row, double (&z)[DM]) {  // all projected dims of a pixel row, fp64
+        if (g.srp) {
+            double acc[DM];
+#pragma unroll
+            for (int j = 0; j < DM; ++j) acc[j] = 0.0;
+            for (int k = 0; k < WM; ++k) {
+#pragma unroll
+                for (int j = 0; j < DM; ++j)
+                    if (j < D) acc[j] += double(row[eb[j * WM + k]]) * ew[j * WM + k];
+            }
+#pragma unroll
+            for (int j = 0; j < DM; ++j) z[j] = acc[j] * g.srp_scale;
+        } else {
+#pragma unroll
+            for (int j = 0; j < DM; ++j) z[j] = (j < D) ? double(row[j]) : 0.0;
+        }
+    };
+    const int nck = (P + CH - 1) / CH;
+    auto issue = [&](int ci, int b) {
+        const int p0 = ci * CH, n = min(CH, P - p0);
+        const float* src = xl + size_t(p0) * B;
+        float* dst = buf + b * CH * B;
+        const int nfl = n * B;
+        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && (nfl & 3) == 0) {
+            for (int i = lane; i < nfl / 4; i += 32) cp_async16(dst + 4 * i, src + 4 * i);
+        } else {
+            for (int i = lane; i < nfl; i += 32) cp_async4(dst + i, src + i);
+        }
+        cp_async_commit();
+    };
+    // each warp keeps two chunks in flight: chunk ci in stage it & 1, refilled with ci + 2 kW
+    if (warp < nck) issue(warp, 0);
+    if (warp + kW < nck) issue(warp + kW, 1);
+    for (int q = tid; q < D * WM; q += kStatsSmallThreads) {
+        const int j = q / WM, k = q - j * WM;
+        const int b0 = __ldg(g.srp_ptr + j), nz = __ldg(g.srp_ptr + j + 1) - b0;
+        eb[j * WM + k] = nz > 0 ? __ldg(g.srp_band + b0 + (k < nz ? k : 0)) : 0;
+        ew[j * WM + k] = k < nz ? double(__ldg(g.srp_w + b0 + k)) : 0.0;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // centre: lane p < n0 projects pixel p (from warp 0's first staged chunk when it holds them,
+        // else from global memory), fp64 butterfly sum
+        const int n0 = min(32, P);
+        const bool staged = CH >= n0;
+        if (staged) {
+            if (kW < nck) cp_async_wait<1>();
+            else cp_async_wait<0>();
+            __syncwarp();
+        }
+        double z[DM];
+        const int pl = min(lane, n0 - 1);
+        zrow(staged ? buf + pl * B : xl + size_t(pl) * B, z);
+#pragma unroll
+        for (int j = 0; j < DM; ++j) {
+            double v = lane < n0 ? z[j] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0 && j < D) cen_s[j] = v / double(n0);
+        }
+    }
+    __syncthreads();
+    float s1[DM], s2[DT];
+#pragma unroll
+    for (int j = 0; j < DM; ++j) s1[j] = 0.f;
+#pragma unroll
+    for (int j = 0; j < DT; ++j) s2[j] = 0.f;
+    for (int ci = warp, it = 0; ci < nck; ci += kW, ++it) {
+        if (ci + kW < nck) cp_async_wait<1>();
+        else cp_async_wait<0>();
+        __syncwarp();
+        const float* st = buf + (it & 1) * CH * B;
+        const int p0 = ci * CH, n = min(CH, P - p0);
+        for (int pp = lane; pp < n; pp += 32) {
+            double z[DM];
+            zrow(st + pp * B, z);
+            float v[DM];
+#pragma unroll
+            for (int j = 0; j < DM; ++j) {
+                v[j] = 0.f;
+                if (j < D) {
+                    v[j] = float(z[j] - cen_s[j]);
+                    vc[size_t(j) * P + p0 + pp] = v[j];
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < DM; ++i) {
+                s1[i] += v[i];
+#pragma unroll
+                for (int j = 0; j <= i; ++j) s2[i * (i + 1) / 2 + j] = fmaf(v[i], v[j], s2[i * (i + 1) / 2 + j]);
+            }
+        }
+        __syncwarp();  // the stage is refilled next
+        if (ci + 2 * kW < nck) issue(ci + 2 * kW, it & 1);
+    }
+    // warp partials in fp64 (over the stage buffers, once every warp is done with them), then the
+    // warps in fixed order
+    const int NT = D * (D + 1) / 2, NV = D + NT;
+    double (*red)[DM + DT] = reinterpret_cast<double (*)[DM + DT]>(smem);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < DM; ++i) {
+        double v = double(s1[i]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && i < D) red[warp][i] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < DM; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+            double v = double(s2[i * (i + 1) / 2 + j]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0 && i < D) red[warp][D + i * (i + 1) / 2 + j] = v;
+        }
+    __syncthreads();
+    double* out = a.stats + size_t(line) * (g.SE + D);
+    for (int q = tid; q < NV; q += kStatsSmallThreads) {
+        double v = 0.0;
+        for (int w = 0; w < kW; ++w) v += red[w][q];
+        if (q < D) {
+            out[q] = cen_s[q];
+            out[D + q] = v;
+        } else {
+            out[2 * D + (q - D)] = v;
+        }
+    }
+}
+
+// SRP variant (the reference default, d = 5): one CTA per line, all threads share each staged chunk;
+// work items are (dim, pixel) pairs, consecutive threads on consecutive pixels of one dim, so a thread
+// sums only its dim's nonzeros (measured faster than whole-pixel lanes when B >> D: configs[3] d = 5
+// 0.180 vs 0.252 ms per 2048 lines).
+template <int DM>
+__global__ void __launch_bounds__(kStatsSmallThreads) stats_small_srp_kernel(SmallArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Geometry& g = a.g;
+    const SmallLaunch& sm = a.sm;  // sm.CH2: pixels per stage
     const int line = blockIdx.x;
     const int tid = threadIdx.x;
     const int D = g.D, B = g.B;
     const int NT = D * (D + 1) / 2;
     float* stage = reinterpret_cast<float*>(smem);                                  // [2][CH][B]
-    double* red = reinterpret_cast<double*>(smem + align_up(size_t(2) * sm.CH * B * 4, 16));  // [warps][D + NT]
+    double* red = reinterpret_cast<double*>(smem + align_up(size_t(2) * sm.CH2 * B * 4, 16));  // [warps][D + NT]
     float* vs = reinterpret_cast<float*>(red + (kStatsSmallThreads / 32) * (D + NT));          // [CH][DM]
     __shared__ double cen_s[16];
     __shared__ double zc[32 * 16];
@@ -51,10 +219,10 @@ __global__ void __launch_bounds__(kStatsSmallThreads) stats_small_kernel(SmallAr
     float* vc = a.vcache + size_t(line) * D * g.P;
     const int n0 = min(32, g.P);
     const bool use_async = (B % 4) == 0;
-    const int nchunks = (g.P + sm.CH - 1) / sm.CH;
+    const int nchunks = (g.P + sm.CH2 - 1) / sm.CH2;
     auto issue = [&](int c) {
-        const int c0 = c * sm.CH, n = min(sm.CH, g.P - c0);
-        float* dst = stage + (c & 1) * sm.CH * B;
+        const int c0 = c * sm.CH2, n = min(sm.CH2, g.P - c0);
+        float* dst = stage + (c & 1) * sm.CH2 * B;
         const float* src = xl + size_t(c0) * B;
         if (use_async) {
             for (int i = tid; i < n * B / 4; i += kStatsSmallThreads) cp_async16(dst + 4 * i, src + 4 * i);
@@ -82,8 +250,8 @@ __global__ void __launch_bounds__(kStatsSmallThreads) stats_small_kernel(SmallAr
             cp_async_wait<0>();
         }
         __syncthreads();
-        const int c0 = c * sm.CH, n = min(sm.CH, g.P - c0);
-        const float* st = stage + (c & 1) * sm.CH * B;
+        const int c0 = c * sm.CH2, n = min(sm.CH2, g.P - c0);
+        const float* st = stage + (c & 1) * sm.CH2 * B;
         if (c == 0) {  // centre: fp64 mean of the first min(32, P) projected pixels, from the staged chunk
             for (int i = tid; i < n0 * D; i += kStatsSmallThreads) {
                 const int j = i / n0, pp = i - j * n0;
@@ -268,12 +436,27 @@ bool small_path(const Geometry& g) { return g.D <= 16; }
 
 SmallLaunch plan_small(const Geometry& g) {
     SmallLaunch sm{};
-    // two stage buffers of ~26 KB: four CTAs per SM (HBM-bound: lines in flight matter more than chunk size)
-    int ch = int(std::min<size_t>(256, std::max<size_t>(32, (size_t(26) * 1024) / (size_t(g.B) * 4))));
-    ch = ch / 4 * 4;
+    // per-warp stages of <= 13.5 KB: 4 warps x 2 stages = 108 KB, two lines per SM; a lane owns one
+    // pixel of a chunk (chunks of 32 pixels, or a multiple of 32 up to 256 for narrow lines, fewer
+    // than 32 for wide ones)
+    int ch = int(std::min<size_t>(256, std::max<size_t>(4, size_t(13824) / (size_t(g.B) * 4))));
+    if (ch >= 32) ch = ch / 32 * 32;
     sm.CH = ch;
-    const int NT = g.D * (g.D + 1) / 2;
-    sm.smem_stats = align_up(size_t(2) * ch * g.B * 4, 16) + size_t(kStatsSmallThreads / 32) * (g.D + NT) * 8 + size_t(ch) * 16 * 4;
+    // SRP variant: two shared stages of ~26 KB (four CTAs per SM)
+    int ch2 = int(std::min<size_t>(256, std::max<size_t>(32, (size_t(26) * 1024) / (size_t(g.B) * 4))));
+    ch2 = ch2 / 4 * 4;
+    sm.CH2 = ch2;
+    if (g.srp) {
+        const int NT = g.D * (g.D + 1) / 2;
+        sm.smem_stats = align_up(size_t(2) * ch2 * g.B * 4, 16) + size_t(kStatsSmallThreads / 32) * (g.D + NT) * 8 +
+                        size_t(ch2) * 16 * 4;
+        sm.smem_score = size_t(g.P) * 4;
+        return sm;
+    }
+    const int dm = g.D == 5 ? 5 : (g.D <= 8 ? 8 : (g.D <= 12 ? 12 : 16));  // the kernel's DM
+    sm.smem_stats = std::max(size_t(kStatsSmallThreads / 32) * 2 * ch * g.B * 4,
+                             size_t(kStatsSmallThreads / 32) * (dm + dm * (dm + 1) / 2) * 8) +
+                    size_t(dm) * (g.srp ? g.srp_wmax : 0) * 12;
     sm.smem_score = size_t(g.P) * 4;
     return sm;
 }
@@ -281,12 +464,27 @@ SmallLaunch plan_small(const Geometry& g) {
 void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x, int n_per_stream, int in_stride,
                         int n_lines_total, double* stats, float* vcache, cudaStream_t st) {
     {
+        ensure_smem(stats_small_srp_kernel<8>, 200 * 1024);
+        ensure_smem(stats_small_srp_kernel<12>, 200 * 1024);
+        ensure_smem(stats_small_srp_kernel<16>, 200 * 1024);
+        ensure_smem(stats_small_kernel<5>, 200 * 1024);
         ensure_smem(stats_small_kernel<8>, 200 * 1024);
         ensure_smem(stats_small_kernel<12>, 200 * 1024);
         ensure_smem(stats_small_kernel<16>, 200 * 1024);
     }
     SmallArgs a{g, sm, x, n_per_stream, in_stride, stats, vcache};
-    if (g.D <= 8)
+    if (g.srp) {
+        if (g.D <= 8)
+            stats_small_srp_kernel<8><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
+        else if (g.D <= 12)
+            stats_small_srp_kernel<12><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
+        else
+            stats_small_srp_kernel<16><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
+        return;
+    }
+    if (g.D == 5)  // the reference default, d = 5
+        stats_small_kernel<5><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
+    else if (g.D <= 8)
         stats_small_kernel<8><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
     else if (g.D <= 12)
         stats_small_kernel<12><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
