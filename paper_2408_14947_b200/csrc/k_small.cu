@@ -379,24 +379,36 @@ __global__ void __launch_bounds__(kSmallThreads) score_small_kernel(Geometry g, 
     __syncthreads();
     const float* vc = vcache + size_t(line) * D * g.P;
     double ls = 0.0;
-    for (int p = tid; p < g.P; p += kSmallThreads) {
-        float u[DM];
+    // kPX pixels per thread per pass, every cache load of the pass issued before the first is used
+    constexpr int kPX = DM <= 8 ? 4 : 2;
+    for (int p0 = tid; p0 < g.P; p0 += kPX * kSmallThreads) {
+        float u[kPX][DM];
 #pragma unroll
-        for (int j = 0; j < DM; ++j) u[j] = (j < D) ? vc[size_t(j) * g.P + p] - off[j] : 0.f;
-        float ssq = 0.f;
+        for (int x = 0; x < kPX; ++x) {
+            const int p = min(p0 + x * kSmallThreads, g.P - 1);
 #pragma unroll
-        for (int r = 0; r < DM; ++r) {
-            if (r < D) {
-                float m = 0.f;
+            for (int j = 0; j < DM; ++j) u[x][j] = (j < D) ? __ldg(vc + size_t(j) * g.P + p) - off[j] : 0.f;
+        }
 #pragma unroll
-                for (int c = 0; c <= r; ++c) m = fmaf(Wd[r][c], u[c], m);
-                ssq = fmaf(m, m, ssq);
+        for (int x = 0; x < kPX; ++x) {
+            const int p = p0 + x * kSmallThreads;
+            float ssq = 0.f;
+#pragma unroll
+            for (int r = 0; r < DM; ++r) {
+                if (r < D) {
+                    float m = 0.f;
+#pragma unroll
+                    for (int c = 0; c <= r; ++c) m = fmaf(Wd[r][c], u[x][c], m);
+                    ssq = fmaf(m, m, ssq);
+                }
+            }
+            if (p < g.P) {
+                const float d = sqrtf(ssq);
+                dl[p] = d;
+                raw[size_t(line) * g.P + p] = d;
+                ls += double(d);
             }
         }
-        const float d = sqrtf(ssq);
-        dl[p] = d;
-        raw[size_t(line) * g.P + p] = d;
-        ls += double(d);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
