@@ -366,39 +366,61 @@ def run_ours(args):
 
 
 def secondary_measurements(pkg, args):
-    """Single-stream numbers named by the metric (1 GPU): configs[1] throughput and
+    """Side numbers named by the metric (1 GPU): single-stream throughput on configs[1] and
+    configs[2], the batched configs[3] workload with the reference's default d = 5 projection, and
     configs[0] lag-0 per-line latency (north-star target < 1 ms at 108 bands)."""
     import torch
 
     out = {}
-    try:
-        cfgd = CONFIGS[1]
-        # a single stream only parallelises across the lines of a window: use a deep lag
-        P, B, T = cfgd["pixels"], cfgd["bands"], 256
-        for mode in ("full", "srp"):
-            n_win = max(2, math.ceil(2 * L2_BYTES / (T * P * B * 4)))
-            host = build_pool(pkg, 1, [0], n_win * T)
-            dev = torch.from_numpy(host[0]).cuda().view(n_win, T, P, B)
-            raw = torch.empty((T, P), dtype=torch.float32, device="cuda")
-            norm = torch.empty_like(raw)
-            eng = pkg.Engine(pkg.ErxConfig(no_srp=mode == "full", alpha=cfgd["alpha"]), B, 1, T)
+
+    def throughput(cid, T, modes, streams=(0,), K=20):
+        """lines/s of a device-resident window of T lines per stream (inputs cycled through a pool
+        >= 2x L2), per mode; also per-line HBM traffic vs the measured peak (4PB + 8P bytes/line)."""
+        cfgd = CONFIGS[cid]
+        P, B = cfgd["pixels"], cfgd["bands"]
+        S = len(streams)
+        n_win = max(2, math.ceil(2 * L2_BYTES / (S * T * P * B * 4)))
+        host = build_pool(pkg, cid, list(streams), n_win * T)
+        dev = torch.from_numpy(host).cuda().view(S, n_win, T, P, B).permute(1, 0, 2, 3, 4).contiguous()
+        raw = torch.empty((S, T, P), dtype=torch.float32, device="cuda")
+        norm = torch.empty_like(raw)
+        res = {}
+        for mode in modes:
+            eng = pkg.Engine(pkg.ErxConfig(no_srp=mode == "full", alpha=cfgd["alpha"]), B, S, T)
             for k in range(3):
-                eng.run_device(dev[k % n_win].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr())
+                eng.run_device(dev[k % n_win].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr(), first_index=k * T)
             eng.sync()
-            K = 20
             eng.event_record(0)
-            for k in range(K):
-                eng.run_device(dev[k % n_win].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr())
+            for k in range(3, 3 + K):
+                eng.run_device(dev[k % n_win].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr(), first_index=k * T)
             eng.event_record(1)
             ms = eng.event_elapsed_ms(0, 1)
             eng.sync()
-            lps = K * T / (ms / 1e3)
-            out.setdefault("single_stream", {"workload": "configs[1]: 1 stream, 640 px x 224 bands, alpha=0.05",
-                                             "window_lines": T})[mode] = {
-                "lines_per_s": lps, "pixel_bands_per_s": lps * P * B}
+            lps = K * S * T / (ms / 1e3)
+            gbs = lps * (4 * P * B + 8 * P) / 1e9
+            res[mode] = {"lines_per_s": lps, "pixel_bands_per_s": lps * P * B, "hbm_gbs_algorithmic": gbs,
+                         "hbm_frac": gbs / peaks()["hbm_gbs"]}
             eng.close()
+        del dev
+        return res
+
+    try:
+        # a single stream only parallelises across the lines of a window: use a deep lag
+        out["single_stream"] = {"workload": "configs[1]: 1 stream, 640 px x 224 bands, alpha=0.05",
+                                "window_lines": 256, **throughput(1, 256, ("full", "srp"))}
     except Exception as ex:
         out["single_stream"] = {"error": repr(ex)}
+    try:
+        out["single_stream_c2"] = {"workload": "configs[2]: 1 stream, 1024 px x 10 bands, alpha=0.1",
+                                   "window_lines": 2048, **throughput(2, 2048, ("full", "srp"))}
+    except Exception as ex:
+        out["single_stream_c2"] = {"error": repr(ex)}
+    try:
+        out["batched_srp"] = {"workload": "configs[3] with the reference default d = 5 SRP: 64 streams, "
+                                          "640 px x 108 bands, alpha=0.1", "window_lines": 32,
+                              **throughput(3, 32, ("srp",), streams=tuple(range(64)))}
+    except Exception as ex:
+        out["batched_srp"] = {"error": repr(ex)}
     try:
         cfgd = CONFIGS[0]
         P, B = cfgd["pixels"], cfgd["bands"]
