@@ -74,6 +74,7 @@ struct erx_engine {
     float* d_srp_sign = nullptr;
     double srp_scale = 1.0;
     int srp_wmax = 0;  // max nonzeros per output dim
+    int srp_nnz = 0;
 
     uint32_t P = 0;  // pixels (set by the first line)
     Geometry geo{};
@@ -267,6 +268,7 @@ int configure(erx_engine* e, uint32_t P) {
     g.srp_w = e->d_srp_sign;
     g.srp_scale = e->srp_scale;
     g.srp_wmax = e->srp_wmax;
+    g.srp_nnz = e->srp_nnz;
     e->sl = erxk::plan_stats(g);
     e->sc = erxk::plan_score(g);
     e->small = erxk::small_path(g);
@@ -628,6 +630,7 @@ int erx_create(const erx_config* cfg, uint32_t bands, uint32_t n_streams, uint32
         }
         ptr[e->D] = int(band.size());
         for (int j = 0; j < e->D; ++j) e->srp_wmax = std::max(e->srp_wmax, ptr[j + 1] - ptr[j]);
+        e->srp_nnz = ptr[e->D];
     }
     const size_t nnz = std::max<size_t>(band.size(), 1);
     if (cudaMalloc(&e->d_srp_ptr, ptr.size() * sizeof(int)) != cudaSuccess ||

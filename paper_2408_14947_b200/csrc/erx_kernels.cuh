@@ -42,6 +42,7 @@ struct Geometry {
     const float* srp_w;    // [nnz] sign of the weight (+1 / -1)
     double srp_scale;      // |w| = sqrt(s)/sqrt(d); z_j = scale * sum_k sign_k x_k (fp64)
     int srp_wmax;          // max nonzeros of one output dim (the small path's padded table width)
+    int srp_nnz;           // nonzeros of W
 };
 
 struct StatsLaunch {

@@ -215,6 +215,27 @@ __global__ void __launch_bounds__(kStatsSmallThreads) stats_small_srp_kernel(Sma
     float* vs = reinterpret_cast<float*>(red + (kStatsSmallThreads / 32) * (D + NT));          // [CH][DM]
     __shared__ double cen_s[16];
     __shared__ double zc[32 * 16];
+    // W's CSC in shared memory: weights (fp64) then bands, then the D + 1 column starts
+    double* sw = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(vs) + align_up(size_t(sm.CH2) * DM * 4, 16));
+    int* sb = reinterpret_cast<int*>(sw + g.srp_nnz);
+    int* sp = sb + g.srp_nnz;
+    for (int q = threadIdx.x; q < g.srp_nnz; q += kStatsSmallThreads) {
+        sw[q] = double(__ldg(g.srp_w + q));
+        sb[q] = __ldg(g.srp_band + q);
+    }
+    for (int q = threadIdx.x; q <= g.D; q += kStatsSmallThreads) sp[q] = g.srp ? __ldg(g.srp_ptr + q) : 0;
+    // z_j of a staged pixel row: two interleaved fp64 partial sums (halves the dependent chain)
+    auto srp_dot = [&](const float* row, int j) {
+        double z0 = 0.0, z1 = 0.0;
+        const int k1 = sp[j + 1];
+        int k = sp[j];
+        for (; k + 1 < k1; k += 2) {
+            z0 += double(row[sb[k]]) * sw[k];
+            z1 += double(row[sb[k + 1]]) * sw[k + 1];
+        }
+        if (k < k1) z0 += double(row[sb[k]]) * sw[k];
+        return (z0 + z1) * g.srp_scale;
+    };
     const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
     float* vc = a.vcache + size_t(line) * D * g.P;
     const int n0 = min(32, g.P);
@@ -256,15 +277,7 @@ __global__ void __launch_bounds__(kStatsSmallThreads) stats_small_srp_kernel(Sma
             for (int i = tid; i < n0 * D; i += kStatsSmallThreads) {
                 const int j = i / n0, pp = i - j * n0;
                 const float* row = st + pp * B;
-                double z;
-                if (g.srp) {
-                    z = 0.0;
-                    for (int k = g.srp_ptr[j]; k < g.srp_ptr[j + 1]; ++k)
-                        z += double(row[g.srp_band[k]]) * double(g.srp_w[k]);
-                    z *= g.srp_scale;
-                } else {
-                    z = double(row[j]);
-                }
+                const double z = g.srp ? srp_dot(row, j) : double(row[j]);
                 zc[pp * 16 + j] = z;
             }
             __syncthreads();
@@ -280,15 +293,7 @@ __global__ void __launch_bounds__(kStatsSmallThreads) stats_small_srp_kernel(Sma
         for (int i = tid; i < n * D; i += kStatsSmallThreads) {
             const int j = i / n, pp = i - j * n;
             const float* row = st + pp * B;
-            double z;
-            if (g.srp) {
-                z = 0.0;
-                for (int k = g.srp_ptr[j]; k < g.srp_ptr[j + 1]; ++k)
-                    z += double(row[g.srp_band[k]]) * double(g.srp_w[k]);
-                z *= g.srp_scale;
-            } else {
-                z = double(row[j]);
-            }
+            const double z = g.srp ? srp_dot(row, j) : double(row[j]);
             const float v = float(z - cen_s[j]);
             vs[pp * DM + j] = v;
             vc[size_t(j) * g.P + c0 + pp] = v;
@@ -460,8 +465,9 @@ SmallLaunch plan_small(const Geometry& g) {
     sm.CH2 = ch2;
     if (g.srp) {
         const int NT = g.D * (g.D + 1) / 2;
+        const int dm = g.D <= 8 ? 8 : (g.D <= 12 ? 12 : 16);
         sm.smem_stats = align_up(size_t(2) * ch2 * g.B * 4, 16) + size_t(kStatsSmallThreads / 32) * (g.D + NT) * 8 +
-                        size_t(ch2) * 16 * 4;
+                        align_up(size_t(ch2) * dm * 4, 16) + size_t(g.srp_nnz) * 12 + size_t(g.D + 1) * 4;
         sm.smem_score = size_t(g.P) * 4;
         return sm;
     }
