@@ -459,8 +459,9 @@ SmallLaunch plan_small(const Geometry& g) {
     int ch = int(std::min<size_t>(256, std::max<size_t>(4, size_t(13824) / (size_t(g.B) * 4))));
     if (ch >= 32) ch = ch / 32 * 32;
     sm.CH = ch;
-    // SRP variant: two shared stages of ~26 KB (four CTAs per SM)
-    int ch2 = int(std::min<size_t>(256, std::max<size_t>(32, (size_t(26) * 1024) / (size_t(g.B) * 4))));
+    // SRP variant: two shared stages of ~20 KB, five CTAs per SM at B = 108 (a sweep of 14-34 KB
+    // stages on configs[3] d = 5: 20 KB fastest, 0.132 ms per 2048 lines vs 0.170 at 26 KB)
+    int ch2 = int(std::min<size_t>(256, std::max<size_t>(32, (size_t(20) * 1024) / (size_t(g.B) * 4))));
     ch2 = ch2 / 4 * 4;
     sm.CH2 = ch2;
     if (g.srp) {
