@@ -254,7 +254,9 @@ void launch_scan(const Geometry& g, const double* stats, double* prior, const do
                  int n_streams, int n_per_stream, int initialized, double alpha, int incremental, int64_t n_seen0,
                  cudaStream_t st, float* kblk) {
     const int blocks_plain = (g.SE + 127) / 128 * n_streams;
-    if (!incremental && blocks_plain < 2 * sm_count() && n_per_stream >= 64) {
+    // (configs[3] on one GPU's share of 8: 376 plain blocks, T = 256 -> chunked 0.074 vs 0.092 ms;
+    // shares of 4 and 2 (752 / 1504 blocks) stay faster element-parallel)
+    if (!incremental && blocks_plain < 4 * sm_count() && n_per_stream >= 64) {
         // too few elements to hide the per-line load latency: chunked variant
         dim3 grid((g.SE + 31) / 32, n_streams);
         const int ctas = int(grid.x * grid.y);
