@@ -80,6 +80,7 @@ struct ScoreLaunch {
     int Dpad;        // smem row stride (floats), = 4 mod 32
     int tiles;       // CTAs per line
     int wsmem;       // 1: the line's W blocks are staged in shared memory
+    size_t slab_off; // wsmem == 0: byte offset of the per-step W block ring (k_score.cu: score_slabs)
     size_t smem;
 };
 

@@ -28,6 +28,105 @@ struct ScoreArgs {
     float* raw;
 };
 
+// W too large for shared memory (D > ~180: configs[1], configs[4]): group s walks its row-block pair
+// {s, nb-1-s} in nb + 1 block steps, step t touching one 8x8 block W(I_s(t), J_s(t)).  The CTA stages
+// the blocks of step t + 2 (one per group, 256 B each) into a 3-deep shared ring with cp.async while
+// it computes step t, so the FFMA2 loop reads W from shared memory instead of waiting on L2.
+constexpr int kSlabDepth = 3;
+__device__ __forceinline__ void slab_block(const Geometry& g, int s, int t, int& I, int& J) {
+    if (t <= s) {
+        I = s;
+        J = t;
+    } else {
+        I = g.nb - 1 - s;
+        J = t - s - 1;
+    }
+}
+__device__ void score_slabs(const Geometry& g, const ScoreLaunch& sc, const float* vt, float* red, const float* Wl,
+                            int s, int q) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int tid = threadIdx.x;
+    const int nsteps = g.nb + 1;
+    float* ring = reinterpret_cast<float*>(smem + sc.slab_off);  // [kSlabDepth][npairs][64]
+    const bool active = s < sc.npairs;
+    const bool single = active && (g.nb - 1 - s == s);  // middle row block of an odd nb: one pass
+    auto stage = [&](int t) {
+        if (active && t < nsteps && !(single && t > s)) {
+            int I, J;
+            slab_block(g, s, t, I, J);
+            const float* src = Wl + (size_t(I) * (I + 1) / 2 + J) * 64;
+            float* dst = ring + (size_t(t % kSlabDepth) * sc.npairs + s) * 64;
+            if (q < 16) cp_async16(dst + 4 * q, src + 4 * q);
+        }
+        cp_async_commit();
+    };
+    stage(0);
+    stage(1);
+    float2 acc[kBlk / 2][4];  // rows (2k, 2k+1) x pixel p
+    auto flush = [&](int I) {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            float ssq = 0.f;
+#pragma unroll
+            for (int k = 0; k < kBlk / 2; ++k) {
+                ssq = fmaf(acc[k][p].x, acc[k][p].x, ssq);
+                ssq = fmaf(acc[k][p].y, acc[k][p].y, ssq);
+            }
+            red[I * sc.PT + q + sc.G * p] = ssq;
+        }
+    };
+    auto zero = [&]() {
+#pragma unroll
+        for (int k = 0; k < kBlk / 2; ++k)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) acc[k][p] = make_float2(0.f, 0.f);
+    };
+    zero();
+    for (int t = 0; t < nsteps; ++t) {
+        stage(t + 2);
+        cp_async_wait<2>();
+        __syncthreads();  // step t's blocks (every group's) have landed
+        if (active && !(single && t > s)) {
+            int I, J;
+            slab_block(g, s, t, I, J);
+            float vb[kBlk][4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const float* row = vt + size_t(q + sc.G * p) * sc.Dpad + J * kBlk;
+                const float4 t0 = *reinterpret_cast<const float4*>(row);
+                const float4 t1 = *reinterpret_cast<const float4*>(row + 4);
+                vb[0][p] = t0.x;
+                vb[1][p] = t0.y;
+                vb[2][p] = t0.z;
+                vb[3][p] = t0.w;
+                vb[4][p] = t1.x;
+                vb[5][p] = t1.y;
+                vb[6][p] = t1.z;
+                vb[7][p] = t1.w;
+            }
+            const float* wb = ring + (size_t(t % kSlabDepth) * sc.npairs + s) * 64;
+#pragma unroll
+            for (int c = 0; c < kBlk; ++c) {
+                const float4 w0 = *reinterpret_cast<const float4*>(wb + c * 8);  // broadcast in the group
+                const float4 w1 = *reinterpret_cast<const float4*>(wb + c * 8 + 4);
+                const float2 wp[4] = {make_float2(w0.x, w0.y), make_float2(w0.z, w0.w), make_float2(w1.x, w1.y),
+                                      make_float2(w1.z, w1.w)};
+#pragma unroll
+                for (int k = 0; k < kBlk / 2; ++k)
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+                        acc[k][p] = __ffma2_rn(wp[k], make_float2(vb[c][p], vb[c][p]), acc[k][p]);
+            }
+            if (J == I) {  // row block I complete
+                flush(I);
+                zero();
+            }
+        }
+        __syncthreads();  // the ring slot of step t is refilled at step t + 1 (stage(t + 3))
+    }
+    cp_async_wait<0>();
+}
+
 __global__ void __launch_bounds__(512) score_kernel(ScoreArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geometry& g = a.g;
@@ -79,7 +178,9 @@ __global__ void __launch_bounds__(512) score_kernel(ScoreArgs a) {
     const int s = tid / sc.G;
     const int q = tid - s * sc.G;
     const float* Wsrc = sc.wsmem ? Ws : Wl;
-    if (s < sc.npairs) {
+    if (!sc.wsmem) {
+        score_slabs(g, sc, vt, red, Wl, s, q);
+    } else if (s < sc.npairs) {
         for (int h = 0; h < 2; ++h) {
             const int I = h == 0 ? s : g.nb - 1 - s;
             if (h == 1 && I == s) break;
@@ -188,7 +289,12 @@ ScoreLaunch plan_score(const Geometry& g) {
     // stage W in smem when it is small (D <= ~180); a larger W would cost the CTA its SM-mates and
     // reads better from L2 (configs[1], D = 224: 0.50 -> 0.445 ms per 256 lines)
     sc.wsmem = (sc.smem + wbytes <= 200 * 1024 && wbytes <= 64 * 1024) ? 1 : 0;
-    if (sc.wsmem) sc.smem += wbytes;
+    if (sc.wsmem) {
+        sc.smem += wbytes;
+    } else {  // W blocks staged per step (score_slabs)
+        sc.slab_off = sc.smem;
+        sc.smem += size_t(kSlabDepth) * sc.npairs * 64 * 4;
+    }
     return sc;
 }
 
