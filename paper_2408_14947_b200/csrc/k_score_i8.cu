@@ -108,14 +108,18 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
     if (warp == kEW + 1) {
         // ---------------- MMA issuer
         if (lane == 0) {
-            const uint32_t idesc = tc::idesc_s8_s32(128, a.N, /*a_mn=*/true, /*b_mn=*/false);
-            // W is lower triangular: K-steps s >= 2 (input dims >= 64) only reach output rows >= 64, so
-            // they run at N = a.N - 64 into accumulator columns 64.. (B operand from W row 64: 8 core
-            // matrix groups of 256 B on)
-            const int Nhi = a.N - 64;
-            const uint32_t idesc_hi = tc::idesc_s8_s32(128, Nhi > 0 ? Nhi : 16, /*a_mn=*/true, /*b_mn=*/false);
             // (v digit, W digit, class - 1), v digit + W digit >= 1
             const int pr[8][3] = {{0, 1, 0}, {1, 0, 0}, {0, 2, 1}, {1, 1, 1}, {2, 0, 1}, {1, 2, 2}, {2, 1, 2}, {2, 2, 3}};
+            // W is lower triangular: K-step s (input dims 32s .. 32s + 31) only reaches output rows
+            // >= 32s, so it runs at N_s = a.N - 32s into accumulator columns 32s.. with the B operand
+            // from W row 32s (4s core-matrix groups of 256 B on): 256 instead of 448 MMA columns at
+            // D = 108
+            uint32_t idesc_s[kKSteps];
+#pragma unroll
+            for (int s = 0; s < kKSteps; ++s) {
+                const int ns = a.N - 32 * s;
+                idesc_s[s] = tc::idesc_s8_s32(128, ns > 0 ? ns : 16, /*a_mn=*/true, /*b_mn=*/false);
+            }
             int j = 0;
             for (int k = 0; k < my_lines; ++k) {
                 const int wb = k & 1;
@@ -129,16 +133,15 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
                     const uint32_t vbase = tc::smem_u32(vops + st * i8::kTileBytes);
 #pragma unroll
                     for (int s = 0; s < kKSteps; ++s) {
-                        const bool hi = s >= 2 && Nhi > 0;  // rows >= 64 only
-                        if (s >= 2 && Nhi <= 0) break;      // D <= 64: nothing above dim 63
+                        if (a.N - 32 * s <= 0) break;  // no output row reaches these dims
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
                             const uint64_t ad =
                                 tc::smem_desc_ls(vbase + pr[q][0] * i8::kVPlane + s * tc::kSliceBytes, 128u, 512u);
                             const uint64_t bd = tc::smem_desc(wbase + pr[q][1] * i8::kWPlane + s * tc::kSliceBytes +
-                                                              (hi ? 2048u : 0u));
+                                                              uint32_t(s) * 1024u);
                             const bool first = s == 0 && (q == 0 || q == 2 || q == 5 || q == 7);
-                            tc::mma_s8(tmem + uint32_t(pr[q][2]) * 128u + (hi ? 64u : 0u), ad, bd, hi ? idesc_hi : idesc,
+                            tc::mma_s8(tmem + uint32_t(pr[q][2]) * 128u + uint32_t(32 * s), ad, bd, idesc_s[s],
                                        first ? 0u : 1u);
                         }
                     }
