@@ -367,8 +367,9 @@ def run_ours(args):
 
 def secondary_measurements(pkg, args):
     """Side numbers named by the metric (1 GPU): single-stream throughput on configs[1] and
-    configs[2], the batched configs[3] workload with the reference's default d = 5 projection, and
-    configs[0] lag-0 per-line latency (north-star target < 1 ms at 108 bands)."""
+    configs[2], the batched configs[3] workload with the reference's default d = 5 projection, the
+    batched configs[4] (448 bands) workload, and configs[0] lag-0 per-line latency (north-star
+    target < 1 ms at 108 bands)."""
     import torch
 
     out = {}
@@ -421,6 +422,11 @@ def secondary_measurements(pkg, args):
                               **throughput(3, 32, ("srp",), streams=tuple(range(64)))}
     except Exception as ex:
         out["batched_srp"] = {"error": repr(ex)}
+    try:
+        out["batched_c4"] = {"workload": "configs[4]: 4 streams, 1280 px x 448 bands, alpha=0.05, D = B",
+                             "window_lines": 32, **throughput(4, 32, ("full",), streams=(0, 1, 2, 3), K=10)}
+    except Exception as ex:
+        out["batched_c4"] = {"error": repr(ex)}
     try:
         cfgd = CONFIGS[0]
         P, B = cfgd["pixels"], cfgd["bands"]

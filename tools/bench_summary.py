@@ -16,6 +16,6 @@ for path in sys.argv[1:]:
     for k, v in d["kernels"].items():
         tf = v.get("tflops")
         print(f"   {k:10s} {v['ms_per_launch']:.3f} ms  share {v['share']:.3f}  {tf and round(tf, 2)} TF/s")
-    for k in ("single_stream", "single_stream_c2", "batched_srp", "latency"):
+    for k in ("single_stream", "single_stream_c2", "batched_srp", "batched_c4", "latency"):
         if k in d:
             print("  ", k, json.dumps(d[k])[:300])
