@@ -30,9 +30,11 @@ struct ScoreArgs {
 
 // W too large for shared memory (D > ~180: configs[1], configs[4]): group s walks its row-block pair
 // {s, nb-1-s} in nb + 1 block steps, step t touching one 8x8 block W(I_s(t), J_s(t)).  The CTA stages
-// the blocks of step t + 2 (one per group, 256 B each) into a 3-deep shared ring with cp.async while
-// it computes step t, so the FFMA2 loop reads W from shared memory instead of waiting on L2.
-constexpr int kSlabDepth = 3;
+// the blocks of step t + 2 (one per group, 256 B each) into a 4-deep shared ring with cp.async while
+// it computes step t, so the FFMA2 loop reads W from shared memory instead of waiting on L2.  One
+// barrier per step: the slot refilled at step t was last read at step t - 2, which every thread
+// finished before the barrier of step t - 1.
+constexpr int kSlabDepth = 4;
 __device__ __forceinline__ void slab_block(const Geometry& g, int s, int t, int& I, int& J) {
     if (t <= s) {
         I = s;
@@ -122,7 +124,6 @@ __device__ void score_slabs(const Geometry& g, const ScoreLaunch& sc, const floa
                 zero();
             }
         }
-        __syncthreads();  // the ring slot of step t is refilled at step t + 1 (stage(t + 3))
     }
     cp_async_wait<0>();
 }
