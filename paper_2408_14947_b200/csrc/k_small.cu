@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kStatsSmallThreads) stats_small_srp_kernel(Sma
 
 // score_small + normalize.  W: packed lower 8x8 blocks (column-major inside).
 template <int DM>
-__global__ void __launch_bounds__(kSmallThreads) score_small_kernel(Geometry g, const double* __restrict__ stats,
+__global__ void __launch_bounds__(kSmallThreads, 4) score_small_kernel(Geometry g, const double* __restrict__ stats,
                                                                     const double* __restrict__ prior,
                                                                     const float* __restrict__ Wp,
                                                                     const float* __restrict__ vcache,
@@ -516,11 +516,15 @@ void launch_score_small(const Geometry& g, const SmallLaunch& sm, const double* 
                         cudaStream_t st) {
     {
         ensure_smem(score_small_kernel<8>, 200 * 1024);
+        ensure_smem(score_small_kernel<12>, 200 * 1024);
         ensure_smem(score_small_kernel<16>, 200 * 1024);
     }
     if (g.D <= 8)
         score_small_kernel<8><<<n_lines_total, kSmallThreads, sm.smem_score, st>>>(g, stats, prior, whiten, vcache,
                                                                                    raw, norm);
+    else if (g.D <= 12)
+        score_small_kernel<12><<<n_lines_total, kSmallThreads, sm.smem_score, st>>>(g, stats, prior, whiten, vcache,
+                                                                                    raw, norm);
     else
         score_small_kernel<16><<<n_lines_total, kSmallThreads, sm.smem_score, st>>>(g, stats, prior, whiten, vcache,
                                                                                     raw, norm);
