@@ -23,14 +23,22 @@ constexpr uint32_t kWAux = 2 * 128 * 4;
 constexpr uint32_t kWBytes = 3 * kWPlane + kWAux;
 
 // v planes as the score kernel's MMA A operand, MN-major (M = 128 pixels of a tile, K = 128 dims):
-// per digit plane, K-step s (32 dims) at s * 4096, 16-pixel group mg at mg * 512 (descriptor SBO),
-// 8-dim group kg at kg * 128 (LBO), dim row d % 8 at 16 B, pixel % 16 the byte.
+// per digit plane, K-step s (32 dims) at s * 4096, 8-dim group kg at kg * 1024 (descriptor LBO),
+// 16-pixel group mg at mg * 128 (SBO), dim row d % 8 at 16 B, pixel % 16 the byte.  Dims are
+// the slow index inside a K-step, so the dims a line never uses (>= 16 * ceil((D + 1) / 16)) form one
+// contiguous tail of each plane that is neither written nor read (vplane_used_bytes).
 constexpr uint32_t kVPlane = 16384;
 constexpr uint32_t kTileBytes = 3 * kVPlane;  // one 128-pixel tile
+constexpr uint32_t kVLbo = 1024, kVSbo = 128;
 __host__ __device__ constexpr uint32_t vplane_off(int plane, int d, int p) {  // p: pixel within the tile (16-aligned)
-    return uint32_t(plane) * kVPlane + uint32_t(d >> 5) * 4096u + uint32_t(p >> 4) * 512u + uint32_t((d & 31) >> 3) * 128u +
-           uint32_t(d & 7) * 16u + uint32_t(p & 15);
+    return uint32_t(plane) * kVPlane + uint32_t(d >> 5) * 4096u + uint32_t((d & 31) >> 3) * kVLbo +
+           uint32_t(p >> 4) * kVSbo + uint32_t(d & 7) * 16u + uint32_t(p & 15);
 }
+// leading bytes of each plane that hold dims 0 .. D (the ones row included), in 16-dim units
+__host__ __device__ constexpr uint32_t vplane_used_bytes(int D) {
+    return ((D + 1 + 15) / 16) * 2048u < kVPlane ? ((D + 1 + 15) / 16) * 2048u : kVPlane;
+}
+__host__ __device__ constexpr int vplane_used_dims(int D) { return int(vplane_used_bytes(D) / 2048u) * 16; }
 
 // The stats kernel's per-dim v scale, recomputed bit-identically by the factor's plane writer.
 __device__ __forceinline__ float v_scale(float vmax) {

@@ -97,9 +97,14 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
                 for (int t = 0; t < ntile; ++t, ++j) {
                     const int st = j % kStages;
                     if (j >= kStages) tc::mbar_wait(&tempty[st], uint32_t((j / kStages) - 1) & 1u);
-                    tc::mbar_expect_tx(&tfull[st], i8::kTileBytes);
-                    tc::bulk_g2s(vops + st * i8::kTileBytes, a.vplanes + (size_t(line) * ntile + t) * i8::kTileBytes,
-                                 i8::kTileBytes, &tfull[st]);
+                    // only the planes' used head (dims 0 .. D); the MMA reads the stale tail against W's
+                    // zero columns
+                    const uint32_t vb = i8::vplane_used_bytes(a.g.D);
+                    tc::mbar_expect_tx(&tfull[st], 3 * vb);
+                    const unsigned char* src = a.vplanes + (size_t(line) * ntile + t) * i8::kTileBytes;
+                    for (int pl = 0; pl < 3; ++pl)
+                        tc::bulk_g2s(vops + st * i8::kTileBytes + pl * i8::kVPlane, src + pl * i8::kVPlane, vb,
+                                     &tfull[st]);
                 }
             }
         }
@@ -137,7 +142,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
                             const uint64_t ad =
-                                tc::smem_desc_ls(vbase + pr[q][0] * i8::kVPlane + s * tc::kSliceBytes, 128u, 512u);
+                                tc::smem_desc_ls(vbase + pr[q][0] * i8::kVPlane + s * tc::kSliceBytes, i8::kVLbo, i8::kVSbo);
                             const uint64_t bd = tc::smem_desc(wbase + pr[q][1] * i8::kWPlane + s * tc::kSliceBytes +
                                                               uint32_t(s) * 1024u);
                             const bool first = s == 0 && (q == 0 || q == 2 || q == 5 || q == 7);

@@ -361,12 +361,15 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                     const int gp = c * kCh + pg2 * 16;
                     unsigned char* vt = a.vplanes + (size_t(line) * ntile_v + (gp >> 7)) * i8::kTileBytes;
                     const uint64_t stream_out = tc::policy_evict_first();  // do not push x out of L2
+                    const int used = i8::vplane_used_dims(D);  // the score never reads dims beyond
 #pragma unroll
                     for (int pl = 0; pl < 3; ++pl) {
-                        tc::st16_hint(vt + i8::vplane_off(pl, dd0, gp & 127),
-                                      make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]), stream_out);
-                        tc::st16_hint(vt + i8::vplane_off(pl, dd1, gp & 127),
-                                      make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]), stream_out);
+                        if (dd0 < used)
+                            tc::st16_hint(vt + i8::vplane_off(pl, dd0, gp & 127),
+                                          make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]), stream_out);
+                        if (dd1 < used)
+                            tc::st16_hint(vt + i8::vplane_off(pl, dd1, gp & 127),
+                                          make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]), stream_out);
                     }
                 }
             }
