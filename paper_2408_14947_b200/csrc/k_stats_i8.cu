@@ -437,7 +437,8 @@ size_t stats_i8_smem(const Geometry& g) {
 }  // namespace
 
 bool stats_i8_eligible(const Geometry& g) {
-    return !g.srp && g.D > 16 && g.D <= 127 && (g.B % 4) == 0 && i8_stages(g) >= 2;
+    // P < 43690: every s32 class sum (<= 3 digit pairs x 2^14 x P) stays exact
+    return !g.srp && g.D > 16 && g.D <= 127 && (g.B % 4) == 0 && g.P < 43690 && i8_stages(g) >= 2;
 }
 
 void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,

@@ -364,6 +364,24 @@ def test_tensor_path_falls_back_where_ineligible(pkg):
         assert (eng.stats_tensor() == 2) == ok, B
 
 
+def test_wide_lines_leave_the_integer_path(pkg, oracle):
+    """P >= 43690 pixels would overflow the exact s32 class sums of the tensor path (3 x 2^14 x P): such
+    lines take the FFMA kernels, and still meet the gates (P = 45000, B = 108, 6 lines)."""
+    P, B, n = 45000, 108, 6
+    rng = np.random.default_rng(7)
+    base = rng.uniform(0.05, 0.6, size=B)
+    A = rng.normal(0, 0.02, size=(B, 8))
+    x = (base + rng.normal(size=(n, P, 8)) @ A.T + rng.normal(0, 0.005, size=(n, P, B))).astype(np.float32)
+    cfg = pkg.ErxConfig(no_srp=True, alpha=0.1, buffer_len=1)
+    eng = pkg.Engine(cfg, B, window_lines=3)
+    eng.push(x[None], 0)
+    eng.finish()
+    assert eng.stats_tensor() == 0
+    _, _, raw_g, norm_g = eng.pop()
+    raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), x)
+    check_gates(oracle, raw_g[0], norm_g[0], raw_o, norm_o, label="P=45000")
+
+
 def test_stats_i8_nonfinite_fails(pkg):
     # score-then-update: the inf of line 1 reaches the background scored by line 2
     x = np.random.default_rng(1).normal(size=(4, 96, 40)).astype(np.float32)
