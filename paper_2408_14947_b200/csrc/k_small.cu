@@ -48,7 +48,7 @@ __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) 
 // Warp 0 derives the centre c (fp64 mean of the first min(32, P) projected pixels) while the first
 // chunks load.
 template <int DM>
-__global__ void __launch_bounds__(kStatsSmallThreads) stats_small_kernel(SmallArgs a) {
+__global__ void __launch_bounds__(kStatsSmallThreads, DM <= 10 ? 4 : 1) stats_small_kernel(SmallArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int kW = kStatsSmallThreads / 32;
     constexpr int DT = DM * (DM + 1) / 2;
@@ -453,10 +453,9 @@ bool small_path(const Geometry& g) { return g.D <= 16; }
 
 SmallLaunch plan_small(const Geometry& g) {
     SmallLaunch sm{};
-    // per-warp stages of <= 13.5 KB: 4 warps x 2 stages = 108 KB, two lines per SM; a lane owns one
-    // pixel of a chunk (chunks of 32 pixels, or a multiple of 32 up to 256 for narrow lines, fewer
-    // than 32 for wide ones)
-    int ch = int(std::min<size_t>(256, std::max<size_t>(4, size_t(13824) / (size_t(g.B) * 4))));
+    // identity projection (B = D <= 16): per-warp stages of ~6 KB (4 warps x 2 stages = 48 KB, four
+    // lines per SM); a lane owns one pixel of a chunk (a multiple of 32 pixels)
+    int ch = int(std::min<size_t>(256, std::max<size_t>(4, size_t(6144) / (size_t(g.B) * 4))));
     if (ch >= 32) ch = ch / 32 * 32;
     sm.CH = ch;
     // SRP variant: two shared stages of ~20 KB, five CTAs per SM at B = 108 (a sweep of 14-34 KB
@@ -472,7 +471,7 @@ SmallLaunch plan_small(const Geometry& g) {
         sm.smem_score = size_t(g.P) * 4;
         return sm;
     }
-    const int dm = g.D == 5 ? 5 : (g.D <= 8 ? 8 : (g.D <= 12 ? 12 : 16));  // the kernel's DM
+    const int dm = (g.D == 5 || g.D == 10) ? g.D : (g.D <= 8 ? 8 : (g.D <= 12 ? 12 : 16));  // the kernel's DM
     sm.smem_stats = std::max(size_t(kStatsSmallThreads / 32) * 2 * ch * g.B * 4,
                              size_t(kStatsSmallThreads / 32) * (dm + dm * (dm + 1) / 2) * 8) +
                     size_t(dm) * (g.srp ? g.srp_wmax : 0) * 12;
@@ -488,6 +487,7 @@ void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x
         ensure_smem(stats_small_srp_kernel<16>, 200 * 1024);
         ensure_smem(stats_small_kernel<5>, 200 * 1024);
         ensure_smem(stats_small_kernel<8>, 200 * 1024);
+        ensure_smem(stats_small_kernel<10>, 200 * 1024);
         ensure_smem(stats_small_kernel<12>, 200 * 1024);
         ensure_smem(stats_small_kernel<16>, 200 * 1024);
     }
@@ -505,6 +505,8 @@ void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x
         stats_small_kernel<5><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
     else if (g.D <= 8)
         stats_small_kernel<8><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
+    else if (g.D == 10)  // configs[2]
+        stats_small_kernel<10><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
     else if (g.D <= 12)
         stats_small_kernel<12><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
     else
