@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
 // state elements and up to thousands of lines per window): the element-
 // parallel kernel above runs one warp through every line, each step waiting on
 // its own global loads.  Here one CTA takes 32 elements of one stream; per
-// chunk of TC lines the other warps finish the line statistics into shared memory
+// chunk of TC (192 or 32) lines the other warps finish the line statistics into shared memory
 // (all loads in flight at once) and write back the chunk before last, while
 // warp 0 runs the recurrence over the previous chunk from shared memory.  The
 // per-element arithmetic and its order are exactly the kernel above's (EMA
@@ -261,9 +261,9 @@ void launch_scan(const Geometry& g, const double* stats, double* prior, const do
         dim3 grid((g.SE + 31) / 32, n_streams);
         const int ctas = int(grid.x * grid.y);
         if (ctas <= sm_count()) {
-            const size_t sm = 2 * size_t(2) * 128 * 32 * sizeof(double);
-            ensure_smem(scan_chunk_kernel<128, 512, 9>, sm);  // 4096 items per chunk: one batch per thread
-            scan_chunk_kernel<128, 512, 9><<<grid, 512, sm, st>>>(g, stats, prior, state_in, state_out, n_per_stream,
+            const size_t sm = 2 * size_t(2) * 192 * 32 * sizeof(double);
+            ensure_smem(scan_chunk_kernel<192, 512, 13>, sm);  // 6144 items per chunk: one batch per thread
+            scan_chunk_kernel<192, 512, 13><<<grid, 512, sm, st>>>(g, stats, prior, state_in, state_out, n_per_stream,
                                                            initialized, alpha, kblk);
         } else {
             const size_t sm = 2 * size_t(2) * 32 * 32 * sizeof(double);
