@@ -518,11 +518,15 @@ void launch_score_small(const Geometry& g, const SmallLaunch& sm, const double* 
                         cudaStream_t st) {
     {
         ensure_smem(score_small_kernel<8>, 200 * 1024);
+        ensure_smem(score_small_kernel<5>, 200 * 1024);
         ensure_smem(score_small_kernel<10>, 200 * 1024);
         ensure_smem(score_small_kernel<12>, 200 * 1024);
         ensure_smem(score_small_kernel<16>, 200 * 1024);
     }
-    if (g.D <= 8)
+    if (g.D == 5)  // the reference default, d = 5
+        score_small_kernel<5><<<n_lines_total, kSmallThreads, sm.smem_score, st>>>(g, stats, prior, whiten, vcache,
+                                                                                   raw, norm);
+    else if (g.D <= 8)
         score_small_kernel<8><<<n_lines_total, kSmallThreads, sm.smem_score, st>>>(g, stats, prior, whiten, vcache,
                                                                                    raw, norm);
     else if (g.D == 10)  // configs[2]
