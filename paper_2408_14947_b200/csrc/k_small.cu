@@ -465,7 +465,7 @@ SmallLaunch plan_small(const Geometry& g) {
     sm.CH2 = ch2;
     if (g.srp) {
         const int NT = g.D * (g.D + 1) / 2;
-        const int dm = g.D == 5 ? 5 : (g.D <= 8 ? 8 : (g.D <= 12 ? 12 : 16));
+        const int dm = (g.D == 5 && g.B <= 128) ? 5 : (g.D <= 8 ? 8 : (g.D <= 12 ? 12 : 16));
         sm.smem_stats = align_up(size_t(2) * ch2 * g.B * 4, 16) + size_t(kStatsSmallThreads / 32) * (g.D + NT) * 8 +
                         align_up(size_t(ch2) * dm * 4, 16) + size_t(g.srp_nnz) * 12 + size_t(g.D + 1) * 4;
         sm.smem_score = size_t(g.P) * 4;
@@ -494,7 +494,7 @@ void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x
     }
     SmallArgs a{g, sm, x, n_per_stream, in_stride, stats, vcache};
     if (g.srp) {
-        if (g.D == 5)  // the reference default
+        if (g.D == 5 && g.B <= 128)  // the reference default (measured: DM = 8 is faster at B = 224)
             stats_small_srp_kernel<5><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
         else if (g.D <= 8)
             stats_small_srp_kernel<8><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
