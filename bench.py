@@ -244,7 +244,9 @@ def run_ours(args):
                          "tflops": a["flops"] * lines_per_launch / (per * 1e-3) / 1e12 if per > 0 else None,
                          "gbs": a["bytes"] * lines_per_launch / (per * 1e-3) / 1e9 if per > 0 else None}
     dom = max(kernels, key=lambda k: kernels[k]["share"])
-    reg_peak, const_peak = eng.probe_fp32_tflops()
+    from paper_2408_14947_b200 import probe
+
+    reg_peak, const_peak = probe.fp32_tflops(local, eng.cuda_stream)
     fp32_peak = max(reg_peak, const_peak)  # the larger (conservative) measured FFMA rate
     fprec = eng.factor_precision()
     pk = peaks()
@@ -539,21 +541,19 @@ def metrics_measurement(pkg):
 def cpu_baseline(cid, no_srp, seconds=12.0, threads=None):
     """fp64 oracle (port of the reference path) on a bounded sample of the same workload."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle_ctypes as orc
-
-    import paper_2408_14947_b200 as pkg
+    import oracle_ctypes as orc  # oracle library only: its own copy of the seeded generator, no product .so
 
     cfgd = CONFIGS[cid]
     cores = threads or os.cpu_count() or 1
     S = min(cfgd["streams"], cores) if cfgd["streams"] > 1 else 1
     use_threads = S
     ocfg = orc.OracleConfig(no_srp=no_srp, alpha=cfgd["alpha"])
-    probe = build_pool(pkg, cid, [0], 3)
+    probe = build_pool(orc, cid, [0], 3)
     t0 = time.perf_counter()
     orc.run_streams(ocfg, probe, threads=1, want_scores=False)
     per_line = (time.perf_counter() - t0) / 3
     n_lines = int(max(4, min(cfgd["lines"], seconds / max(per_line, 1e-6))))
-    pool = build_pool(pkg, cid, list(range(S)), n_lines)
+    pool = build_pool(orc, cid, list(range(S)), n_lines)
     t0 = time.perf_counter()
     orc.run_streams(ocfg, pool, threads=use_threads, want_scores=False)
     el = time.perf_counter() - t0
@@ -615,8 +615,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip the single-stream / latency side measurements")
-    ap.add_argument("--stats", type=int, default=2, choices=[0, 1, 2],
-                    help="line-statistics kernel: 0 FFMA, 1 tcgen05 bf16x3, 2 tcgen05 exact int8")
+    ap.add_argument("--stats", type=int, default=2, choices=[0, 2],
+                    help="line-statistics / score kernels: 0 FFMA, 2 tcgen05 exact int8 digits")
     ap.add_argument("--host-groups", type=int, default=0, help="stream groups per host window (0 auto)")
     ap.add_argument("--shard-of", type=int, default=0,
                     help="N=1 only: run rank 0's stream share of an N-GPU job (value is per GPU)")

@@ -144,9 +144,9 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
  *   2 (default) exact-integer tcgen05 path (kind::i8 digit planes, s32 TMEM
  *     accumulation) for both where eligible (full covariance, 16 < D <= 127,
  *     B % 4 == 0), the FFMA kernels elsewhere;
- *   1 tcgen05 bf16x3 line statistics (fp32 TMEM accumulation truncates; kept
- *     as a measured negative result);
  *   0 the FFMA kernels.
+ * (1, the round-1 bf16x3 tcgen05 statistics, is gone: fp32 TMEM accumulation
+ * truncates and missed the median gate; ERX_ERR_CONFIG.)
  * erx_get_option reports the kind in use once the geometry is fixed. */
 #define ERX_OPT_STATS_TENSOR 2
 /* ERX_OPT_HOST_GROUPS: stream groups per host window of erx_push_host (the
@@ -177,33 +177,13 @@ int64_t erx_get_option(const erx_engine* e, int option);
 #define ERX_KERNEL_FACTOR 2
 #define ERX_KERNEL_SCORE 3
 #define ERX_KERNEL_NORMALIZE 4
-#define ERX_NUM_KERNELS 5
+#define ERX_KERNEL_FIXUP 5  /* fp64 rescue of lines the fp32 factor lists (k_fixup.cu) */
+#define ERX_NUM_KERNELS 6
 uint64_t erx_launch_count(const erx_engine* e);
 /* When on, every kernel launch is bracketed by CUDA events on the engine stream. */
 int erx_set_profiling(erx_engine* e, int on);
 /* Per-kernel summed device ms and launch counts since profiling was enabled. */
 int erx_kernel_times(erx_engine* e, double* ms, uint64_t* launches);
-
-/* Measured FP32 FFMA throughput of the engine's device (TFLOP/s), the
- * roofline denominator for the FFMA-bound kernels: reg_form = register-tile
- * outer products (the kernels' own instruction shape), const_form = FFMA
- * with constant-bank operands (highest issue rate).  Either may be NULL. */
-int erx_probe_fp32_tflops(erx_engine* e, double* reg_form, double* const_form);
-/* Same for the paired fma.rn.f32x2 (FFMA2) instruction. */
-int erx_probe_ffma2_tflops(erx_engine* e, double* tflops);
-/* Streaming global->shared throughput, GB/s (design probe): mode 0 cp.async.bulk
- * ring (one issuing thread), 1 LDG.128 by 256 threads, 2 cp.async by 256 threads;
- * chunk_bytes per stage (multiple of 1 KB), 1..8 stages, ctas_per_sm persistent CTAs. */
-int erx_probe_stream(erx_engine* e, int mode, uint32_t chunk_bytes, int stages, int ctas_per_sm, uint64_t bytes,
-                     double* gbs);
-/* tcgen05 self-test on device buffers: D[128][128] = A[128][K] . B[128][K]^T
- * from bf16 operands (split = 0) or the 3-way bf16 split with 6 products
- * (split = 1, fp32-accurate).  K a multiple of 16, <= 256. */
-int erx_tc_selftest(erx_engine* e, const float* dA, const float* dB, int K, int split, float* dD);
-/* kind::i8 check (exact s32): D[128][N] = A[128][K] B[N][K]^T with A staged K-major or MN-major
- * (a_mn; layout strides ms / ks between 16-row M groups / 8-row K groups, descriptor lbo / sbo). */
-int erx_tc_selftest_i8(erx_engine* e, const int8_t* dA, const int8_t* dB, int K, int N, int a_mn, int ms, int ks,
-                       int lbo, int sbo, int* dD);
 
 /* ---- parity-gate metrics on the device (k_metrics.cu) ----
  * Exact ROC AUC of fp32 device scores against u8 labels (non-zero = anomaly),
@@ -225,9 +205,11 @@ int erx_metrics_top_k(const float* d_scores, const uint8_t* d_select, size_t n, 
 /* ---- HADC cube / mask files (hadc.cpp; SPEC.md:576-598 [MODULE] io) ----
  * Little-endian container: "HADC", version u16 (1), lines / pixels / bands u32, dtype u8
  * (1 = float32, 2 = u8 mask 0/1), layout u8 (1 = [line][pixel][band]), name_len u16 + UTF-8
- * name, then exactly lines*pixels*bands elements.  Violations (bad magic / version / dtype /
- * layout, zero sizes, payload length != declared, mask value > 1) return ERX_ERR_IO with the
- * byte offset in erx_hadc_last_error (read_cube / read_mask errors). */
+ * name, then exactly lines*pixels*bands elements.  Format violations (bad magic / version /
+ * dtype / layout, zero sizes, a size product overflowing 64 bits, payload length != declared,
+ * mask value > 1) return ERX_ERR_DATA — had::FormatError, kind data (errors.hpp:67-75) — with
+ * "at offset <n>" in erx_hadc_last_error (read_cube / read_mask errors);
+ * failing to open or read the file returns ERX_ERR_IO (had::IoError, errors.hpp:77-79). */
 typedef struct erx_hadc erx_hadc;
 typedef struct {
     uint16_t version;

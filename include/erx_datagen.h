@@ -48,6 +48,10 @@ int erx_gen_preset(int config_id, uint32_t stream, erx_gen_spec* out);
 int erx_gen_lines(const erx_gen_spec* spec, uint32_t first_line, uint32_t n_lines, float* out, uint8_t* mask,
                   int threads);
 
+/* The stream's scene-change lines as drawn (sorted; out holds up to 4): returns their count, or -1
+ * for a bad spec. */
+int erx_gen_scene_changes(const erx_gen_spec* spec, int64_t* out);
+
 /* The same lines generated on the device (k_datagen.cu): d_out [n][P][B] fp32 and
  * d_mask [n][P] u8 (or NULL) in device memory, on `stream` (a cudaStream_t; NULL = the legacy
  * default stream), returning when done.  Identical random streams and fp64 operation order as

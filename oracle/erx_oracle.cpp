@@ -407,6 +407,20 @@ int orc_erx_process(void* h, int64_t index, uint32_t p, uint32_t b, const float*
     return st;
 }
 
+// Install a background (mu, K, lines_seen, welford_n): the detector continues as if it had
+// reached this state itself.  ErxState is a plain value type (erx.hpp:27-34) that SPEC.md:337
+// lets move between threads between lines; tests use this to pin states the stream would only
+// reach by rounding accidents (an indefinite K that forces the eps escalation of SPEC.md:306).
+int orc_erx_set_state(void* h, const double* mu, const double* cov, int64_t lines_seen, int64_t welford_n) {
+    Erx* e = static_cast<Erx*>(h);
+    e->mu.assign(mu, mu + e->d);
+    e->cov.assign(cov, cov + size_t(e->d) * e->d);
+    e->lines_seen = lines_seen;
+    e->welford_n = welford_n;
+    e->initialized = true;
+    return 0;
+}
+
 int orc_erx_state(void* h, double* mu, double* cov, int64_t* lines_seen, int64_t* welford_n, int* initialized,
                   double* weights) {
     Erx* e = static_cast<Erx*>(h);

@@ -69,6 +69,16 @@ int orc_erx_process(void* h, int64_t index, uint32_t p, uint32_t b, const float*
 int orc_erx_state(void* h, double* mu, double* cov, int64_t* lines_seen, int64_t* welford_n, int* initialized,
                   double* weights);
 
+int orc_erx_set_state(void* h, const double* mu, const double* cov, int64_t lines_seen, int64_t welford_n);
+
+/* ---- input generator: the shared seeded BASELINE.json generator
+ * (paper_2408_14947_b200/csrc/datagen.cpp, compiled into this library too so
+ * the CPU baseline / reference arm needs no product library).  Same
+ * arguments as erx_gen_preset / erx_gen_lines (include/erx_datagen.h). ---- */
+int orc_gen_preset(int config_id, uint32_t stream, void* spec_out);
+int orc_gen_lines(const void* spec, uint32_t first_line, uint32_t n_lines, float* out, uint8_t* mask, int threads);
+int orc_gen_scene_changes(const void* spec, int64_t* out);
+
 /* Runs n_streams independent detectors over lines [S][L][P][B] with `threads`
  * host threads, one stream per thread at a time.  raw/norm
  * are [S][L][P]; either may be NULL.  Returns the first error code seen. */

@@ -30,6 +30,28 @@ class OrcConfig(C.Structure):
     ]
 
 
+class GenSpec(C.Structure):
+    """erx_gen_spec (include/erx_datagen.h): the seeded BASELINE.json generator's parameters."""
+    _fields_ = [
+        ("lines", C.c_uint32),
+        ("pixels", C.c_uint32),
+        ("bands", C.c_uint32),
+        ("n_factors", C.c_uint32),
+        ("loading_sd", C.c_double),
+        ("noise_sd", C.c_double),
+        ("base_kind", C.c_int32),
+        ("drift", C.c_double),
+        ("n_scene_changes", C.c_uint32),
+        ("scene_change_line", C.c_int64 * 4),
+        ("anomaly_frac", C.c_double),
+        ("anomaly_kind", C.c_int32),
+        ("offset_sd", C.c_double),
+        ("mix_lo", C.c_double),
+        ("mix_hi", C.c_double),
+        ("seed", C.c_uint64),
+    ]
+
+
 def build() -> str:
     """Compile the oracle library (g++ only; seconds)."""
     subprocess.run(["make", "-s", "-C", _HERE, "all"], check=True)
@@ -85,6 +107,14 @@ def lib():
         L.orc_erx_run_streams.restype = C.c_int
         L.orc_erx_run_streams.argtypes = [C.POINTER(OrcConfig), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                           fp, dp, dp, C.c_int]
+        L.orc_erx_set_state.restype = C.c_int
+        L.orc_erx_set_state.argtypes = [C.c_void_p, dp, dp, C.c_int64, C.c_int64]
+        L.orc_gen_preset.restype = C.c_int
+        L.orc_gen_preset.argtypes = [C.c_int, C.c_uint32, C.c_void_p]
+        L.orc_gen_lines.restype = C.c_int
+        L.orc_gen_lines.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, fp, u8p, C.c_int]
+        L.orc_gen_scene_changes.restype = C.c_int
+        L.orc_gen_scene_changes.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
         L.orc_roc_auc.restype = C.c_double
         L.orc_roc_auc.argtypes = [dp, u8p, C.c_size_t, C.POINTER(C.c_int)]
         _lib = L
@@ -257,6 +287,11 @@ class OracleErx:
             raise OracleError(st, msg.value.decode(), piv.value)
         return raw, norm, bool(wu[0])
 
+    def set_state(self, mu, cov, lines_seen: int, welford_n: int = 0):
+        mu = np.ascontiguousarray(mu, np.float64)
+        cov = np.ascontiguousarray(cov, np.float64)
+        lib().orc_erx_set_state(self._h, _p(mu, C.c_double), _p(cov, C.c_double), lines_seen, welford_n)
+
     def state(self):
         d = self.dims
         mu = np.zeros(d)
@@ -269,6 +304,34 @@ class OracleErx:
                             C.byref(ini), _p(w, C.c_double))
         return dict(mu=mu, cov=cov, lines_seen=ls.value, welford_n=wn.value, initialized=bool(ini.value),
                     weights=None if self._cfg.no_srp else w)
+
+
+def gen_spec(config_id: int, stream: int = 0) -> GenSpec:
+    """BASELINE.json configs[config_id] generator spec for one stream (erx_gen_preset)."""
+    s = GenSpec()
+    if lib().orc_gen_preset(config_id, stream, C.byref(s)):
+        raise OracleError(2, f"unknown BASELINE config id {config_id}")
+    return s
+
+
+def gen_lines(spec: GenSpec, first: int, n: int, threads: int = 0, want_mask: bool = True):
+    """Lines [first, first+n) of one synthetic stream: (fp32 [n][P][B], u8 mask [n][P] or None)."""
+    out = np.empty((n, spec.pixels, spec.bands), np.float32)
+    mask = np.empty((n, spec.pixels), np.uint8) if want_mask else None
+    st = lib().orc_gen_lines(C.byref(spec), first, n, _p(out, C.c_float),
+                             _p(mask, C.c_uint8) if want_mask else C.POINTER(C.c_uint8)(), threads)
+    if st:
+        raise OracleError(st, "bad generator spec")
+    return out, mask
+
+
+def gen_scene_changes(spec: GenSpec):
+    """The stream's scene-change lines as the generator drew them (sorted)."""
+    out = (C.c_int64 * 4)()
+    n = lib().orc_gen_scene_changes(C.byref(spec), out)
+    if n < 0:
+        raise OracleError(2, "bad generator spec")
+    return [int(out[i]) for i in range(n)]
 
 
 def run_stream(cfg: OracleConfig, lines: np.ndarray):

@@ -20,8 +20,8 @@ ERX_ERR_NUMERIC = 5
 ERX_ERR_IO = 6
 ERX_ERR_DEVICE = 16
 ERX_ERR_STATE = 17
-NUM_KERNELS = 5
-KERNEL_NAMES = ("stats", "scan", "factor", "score", "normalize")
+NUM_KERNELS = 6
+KERNEL_NAMES = ("stats", "scan", "factor", "score", "normalize", "fixup")
 OPT_FACTOR_PRECISION = 1
 OPT_STATS_TENSOR = 2
 OPT_HOST_GROUPS = 3
@@ -107,11 +107,6 @@ SIGNATURES = {
     "erx_get_option": (C.c_int64, [_vp, C.c_int]),
     "erx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "erx_kernel_times": (C.c_int, [_vp, _dp, _u64p]),
-    "erx_probe_fp32_tflops": (C.c_int, [_vp, _dp, _dp]),
-    "erx_probe_ffma2_tflops": (C.c_int, [_vp, _dp]),
-    "erx_probe_stream": (C.c_int, [_vp, C.c_int, C.c_uint32, C.c_int, C.c_int, C.c_uint64, _dp]),
-    "erx_tc_selftest": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, _vp]),
-    "erx_tc_selftest_i8": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp]),
     "erx_metrics_roc_auc": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _dp, _u64p, _u64p]),
     "erx_metrics_top_k": (C.c_int, [_vp, _vp, C.c_size_t, C.c_size_t, _vp, _vp, _fp]),
     "erx_hadc_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(HadcInfoC)]),
@@ -130,6 +125,7 @@ SIGNATURES = {
     "erx_gen_preset": (C.c_int, [C.c_int, C.c_uint32, C.POINTER(GenSpecC)]),
     "erx_gen_lines": (C.c_int, [C.POINTER(GenSpecC), C.c_uint32, C.c_uint32, _fp, _u8p, C.c_int]),
     "erx_gen_lines_device": (C.c_int, [C.POINTER(GenSpecC), C.c_uint32, C.c_uint32, _vp, _vp, _vp]),
+    "erx_gen_scene_changes": (C.c_int, [C.POINTER(GenSpecC), _i64p]),
     "erx_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "erx_rng_probe": (None, [C.c_uint64, C.c_int, C.c_uint32, _u64p, _dp]),
 }

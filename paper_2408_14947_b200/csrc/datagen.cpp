@@ -315,6 +315,13 @@ int erx_gen_lines(const erx_gen_spec* spec, uint32_t first, uint32_t n, float* o
     return 0;
 }
 
+int erx_gen_scene_changes(const erx_gen_spec* spec, int64_t* out) {
+    if (!spec || spec->pixels < 1 || spec->bands < 1 || spec->lines < 1) return -1;
+    const auto stp = build_cached(*spec);
+    for (size_t k = 0; k < stp->changes.size(); ++k) out[k] = stp->changes[k];
+    return int(stp->changes.size());
+}
+
 uint64_t erx_mix_seed(uint64_t seed, uint64_t n) { return mix_seed(seed, n); }
 
 void erx_rng_probe(uint64_t seed, int kind, uint32_t n, uint64_t* u64_out, double* f64_out) {

@@ -43,6 +43,27 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// Conditioning bound of the fp32 factor: a line whose Cholesky pivot L_ii^2 falls below
+// (K + eps I)_ii / kCondTau is factored again in fp64 (k_fixup.cu).  Emulated fp32 factor +
+// whitening against fp64: median raw-score error ~2e-9 x max_i A_ii / L_ii^2, so
+// 1e3 keeps the fp32 lines ~5x inside the 1e-5 median gate; every BASELINE config stays below ~500.
+constexpr float kCondTau = 1000.f;
+
+// Put a line the fp32 factor gave up on onto the fp64 rescue list ([0] count, [2..] lines).
+__device__ __forceinline__ void list_for_fixup(int* fixlist, int* status, int line) {
+    status[line] = -2;  // pending: the rescue writes the final status
+    const int pos = atomicAdd(fixlist, 1);
+    fixlist[2 + pos] = line;
+}
+
+// A line whose scores spread less than kFlatRel of their mean (e.g. a two-pixel line scored
+// against its own statistics: both deltas are equal, std = 0 in fp64) is normalised from fp32
+// deltas whose own rounding is then comparable to that spread; the fp64 rescue redoes it, so the
+// zero-variance rule (std < 1e-12 -> 0) is applied to fp64 deltas as the reference
+// does.  Real lines spread by tens of percent (delta ~ chi with D degrees of freedom).
+constexpr double kFlatRel = 1e-2;
+__device__ __forceinline__ bool flat_line(double mean, double sd) { return mean > 0.0 && sd < kFlatRel * mean; }
+
 // Per-device launch helpers.  Function attributes and SM counts are per device, so engines on
 // several GPUs in one process (or host threads) each get them set; the calls are idempotent.
 constexpr int kMaxDevices = 64;

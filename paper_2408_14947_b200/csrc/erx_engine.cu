@@ -87,8 +87,7 @@ struct erx_engine {
     unsigned char* d_vplanes = nullptr;  // [S*T][tiles][48 KB] quantised v digit planes (tensor path)
     float* d_kblk = nullptr;    // [S*T][nb(nb+1)/2][64] pre-update K as fp32 blocks (blocked fp32 factor)
     int factor_req = 0;   // requested factor precision (0 auto, 32, 64)
-    // ERX_OPT_STATS_TENSOR: 2 exact-integer tcgen05 stats + score where eligible (default), 1 tcgen05
-    // bf16x3 stats (fp32 TMEM accumulation truncates, tools/tc_bias.py), 0 FFMA kernels.
+    // ERX_OPT_STATS_TENSOR: 2 exact-integer tcgen05 stats + score where eligible (default), 0 FFMA kernels.
     int stats_tensor = 2;
     int factor_prec = 0;  // precision in use (0 = blocked fp64 global path)
     int factor_threads = 0;  // ERX_OPT_FACTOR_THREADS (0 auto)
@@ -106,7 +105,9 @@ struct erx_engine {
     float* d_raw = nullptr;
     float* d_norm = nullptr;
     int* d_status = nullptr;
-    int* d_latch = nullptr;
+    unsigned long long* d_latch = nullptr;  // {flag, line id, pivot} of the first device-path failure
+    int* d_fix = nullptr;        // fp64 rescue list of the fp32 factor ([0] count, [1] done, [2..] lines)
+    double* d_fixwork = nullptr; // the rescue's fp64 workspace
 
     // pinned host staging (drop-in path)
     float* h_lines = nullptr;
@@ -138,8 +139,8 @@ struct erx_engine {
     bool profiling = false;
     std::vector<Timing> timings;
     std::vector<cudaEvent_t> event_pool;
-    double kms[ERX_NUM_KERNELS] = {0, 0, 0, 0, 0};
-    uint64_t kcount[ERX_NUM_KERNELS] = {0, 0, 0, 0, 0};
+    double kms[ERX_NUM_KERNELS] = {};
+    uint64_t kcount[ERX_NUM_KERNELS] = {};
     cudaEvent_t user_ev[8] = {};
 };
 
@@ -230,6 +231,10 @@ void free_window(erx_engine* e) {
     e->d_vplanes = nullptr;
     cudaFree(e->d_kblk);
     e->d_kblk = nullptr;
+    cudaFree(e->d_fix);
+    e->d_fix = nullptr;
+    cudaFree(e->d_fixwork);
+    e->d_fixwork = nullptr;
     cudaFreeHost(e->h_lines);
     e->d_lines = nullptr;
     e->d_stats = e->d_prior = e->d_work = nullptr;
@@ -292,6 +297,10 @@ int configure(erx_engine* e, uint32_t P) {
     if (erxk::stats_i8_eligible(g)) CU(cudaMalloc(&e->d_vmax, L * size_t(g.D) * sizeof(float)));
     if (e->tensor) CU(cudaMalloc(&e->d_vplanes, L * erxk::vplanes_bytes_per_line(g)));
     if (e->factor_prec == 32) CU(cudaMalloc(&e->d_kblk, L * erxk::whiten_floats_per_line(g) * sizeof(float)));
+    // fp64 rescue list (fed by the fp32 factors and by the normalisation's flat-line check)
+    CU(cudaMalloc(&e->d_fix, (L + 2) * sizeof(int)));
+    CU(cudaMemset(e->d_fix, 0, (L + 2) * sizeof(int)));
+    CU(cudaMalloc(&e->d_fixwork, erxk::fixup_work_doubles(g, int(L)) * sizeof(double)));
     return ERX_OK;
 }
 
@@ -349,7 +358,7 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     const Geometry& g = e->geo;
     const int L = int(ns * n);
     const size_t l0 = size_t(s0) * n;
-    const int line_base = int(e->lines_seen * e->S + l0);
+    const long long line_base = (long long)(e->lines_seen) * e->S + (long long)(l0);
     const float* xg = x + size_t(s0) * in_stride * g.P * g.B;
     double* stats = e->d_stats + l0 * (g.SE + g.D);
     double* prior = e->d_prior + l0 * g.SE;
@@ -370,8 +379,6 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
             erxk::launch_stats_small(g, e->smp, xg, int(n), int(in_stride), L, stats, vcache, e->stream);
         else if (tensor)
             erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, vmax, vplanes, e->stream);
-        else if (e->stats_tensor == 1 && erxk::stats_tc_eligible(g))
-            erxk::launch_stats_tc(g, xg, int(n), int(in_stride), L, stats, e->stream);
         else
             erxk::launch_stats(g, e->sl, xg, int(n), int(in_stride), L, stats, e->stream);
     });
@@ -386,11 +393,12 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     }
     timed(e, ERX_KERNEL_FACTOR, [&] {
         erxk::launch_factor(g, prior, L, e->cfg.epsilon, work, white, status, e->d_latch, line_base, e->factor_prec,
-                            e->stream, stats, tensor ? vmax : nullptr, kblk, e->factor_threads);
+                            e->stream, e->d_fix, stats, tensor ? vmax : nullptr, kblk, e->factor_threads);
     });
     if (e->small) {  // score + normalisation fused
         timed(e, ERX_KERNEL_SCORE, [&] {
-            erxk::launch_score_small(g, e->smp, stats, prior, white, vcache, L, rawg, normg, e->stream);
+            erxk::launch_score_small(g, e->smp, stats, prior, white, vcache, L, rawg, normg, status, e->d_fix,
+                                     e->stream);
         });
     } else {
         timed(e, ERX_KERNEL_SCORE, [&] {
@@ -399,7 +407,15 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
             else
                 erxk::launch_score(g, e->sc, xg, int(n), int(in_stride), prior, white, L, rawg, e->stream);
         });
-        timed(e, ERX_KERNEL_NORMALIZE, [&] { erxk::launch_normalize(g, rawg, L, normg, e->stream); });
+        timed(e, ERX_KERNEL_NORMALIZE, [&] { erxk::launch_normalize(g, rawg, L, normg, status, e->d_fix, e->stream); });
+    }
+    {
+        timed(e, ERX_KERNEL_FIXUP, [&] {
+            erxk::FixupArgs fa{g, xg, int(n), int(in_stride), stats, st_in, e->initialized ? 1 : 0, e->cfg.alpha,
+                               e->cfg.use_incremental, (long long)(e->welford_n), e->cfg.epsilon, e->d_fix, e->d_fixwork,
+                               rawg, normg, status, e->d_latch, line_base};
+            erxk::launch_fixup(fa, L, e->stream);
+        });
     }
     cudaError_t r = cudaGetLastError();
     if (r != cudaSuccess) return fail(e, ERX_ERR_DEVICE, std::string("kernel launch: ") + cudaGetErrorString(r));
@@ -442,12 +458,17 @@ int harvest(erx_engine* e, bool block_oldest) {
         const uint32_t n = pw.n;
         int bad_t = -1, bad_piv = -1;  // first failing line in emission order (then stream order)
         for (uint32_t t = 0; t < n && bad_t < 0; ++t)
-            for (uint32_t s = 0; s < e->S; ++s)
+            for (uint32_t s = 0; s < e->S; ++s) {
+                if (pw.blk->status[s * n + t] == -2) {  // listed for the fp64 rescue, never rescued
+                    e->failed = true;
+                    return fail(e, ERX_ERR_DEVICE, "internal: a line listed for the fp64 rescue was not rescued");
+                }
                 if (pw.blk->status[s * n + t] >= 0) {
                     bad_t = int(t);
                     bad_piv = pw.blk->status[s * n + t];
                     break;
                 }
+            }
         const uint32_t good = bad_t < 0 ? n : uint32_t(bad_t);
         for (uint32_t t = 0; t < good; ++t) {
             ScoredRow row;
@@ -494,7 +515,20 @@ int drain_pending(erx_engine* e) {
 // for the scores and queues them, with ERX_OPT_ASYNC_HOST the window stays in
 // flight (its copy-in then overlaps the previous window's kernels and result
 // copies) until erx_ready / erx_pop / erx_finish harvest it.
+int run_host_window_body(erx_engine* e, const float* src, size_t src_pitch);
+
+// Any failure inside a host window leaves the engine failed with the window dropped (its lines
+// cannot be scored any more; the reference leaves continuation after a throw unspecified).
 int run_host_window(erx_engine* e, const float* src, size_t src_pitch) {
+    const int st = run_host_window_body(e, src, src_pitch);
+    if (st && e->fill) {
+        e->fill = 0;
+        e->failed = true;
+    }
+    return st;
+}
+
+int run_host_window_body(erx_engine* e, const float* src, size_t src_pitch) {
     if (e->fill == 0) return ERX_OK;
     const uint32_t n = e->fill;
     const size_t line_f = size_t(e->P) * e->B;
@@ -648,8 +682,8 @@ int erx_create(const erx_config* cfg, uint32_t bands, uint32_t n_streams, uint32
             return bail("cudaMalloc (state)");
         cudaMemset(e->d_state[k], 0, size_t(n_streams) * SE * sizeof(double));
     }
-    if (cudaMalloc(&e->d_latch, 4 * sizeof(int)) != cudaSuccess) return bail("cudaMalloc (latch)");
-    cudaMemset(e->d_latch, 0, 4 * sizeof(int));
+    if (cudaMalloc(&e->d_latch, 4 * sizeof(unsigned long long)) != cudaSuccess) return bail("cudaMalloc (latch)");
+    cudaMemset(e->d_latch, 0, 4 * sizeof(unsigned long long));
     for (auto& ev : e->user_ev) cudaEventCreate(&ev);
     *out = e;
     return ERX_OK;
@@ -732,6 +766,7 @@ int erx_push_host(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_t
             i += e->T;
             continue;
         }
+        if (e->fill >= e->T) return fail(e, ERX_ERR_STATE, "internal: staging window overfull");
         for (uint32_t s = 0; s < e->S; ++s)
             std::memcpy(e->h_lines + (size_t(s) * e->T + e->fill) * line_f,
                         lines + (size_t(s) * n_lines + i) * line_f, line_f * sizeof(float));
@@ -858,11 +893,11 @@ int erx_sync(erx_engine* e) {
     if (int st = report_pending(e)) return st;
     if (int st = drain_pending(e)) return st;
     CU(cudaStreamSynchronize(e->stream));
-    int latch[4];
+    unsigned long long latch[4];
     CU(cudaMemcpy(latch, e->d_latch, sizeof(latch), cudaMemcpyDeviceToHost));
     if (latch[0]) {
         e->failed = true;
-        e->pivot = latch[2];
+        e->pivot = int(latch[2]);
         return fail(e, ERX_ERR_NUMERIC, "Cholesky of K + eps*I failed at pivot " + std::to_string(latch[2]) +
                                             " (window line id " + std::to_string(latch[1]) + ")");
     }
@@ -940,7 +975,9 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
         return ERX_OK;
     }
     if (option == ERX_OPT_STATS_TENSOR) {
-        if (value < 0 || value > 2) return fail(e, ERX_ERR_CONFIG, "stats tensor: 0, 1 or 2");
+        if (value != 0 && value != 2) return fail(e, ERX_ERR_CONFIG, "stats tensor: 0 or 2");
+        if (int st = run_staged_window(e)) return st;  // staged lines are scored with the old plan
+        if (int st = drain_pending(e)) return st;
         e->stats_tensor = int(value);
         if (e->d_stats) {
             const uint32_t P = e->P;
@@ -952,6 +989,8 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
     if (option == ERX_OPT_FACTOR_PRECISION) {
         if (value != 0 && value != 1 && value != 31 && value != 32 && value != 64)
             return fail(e, ERX_ERR_CONFIG, "factor precision: 0, 1, 31, 32 or 64");
+        if (int st = run_staged_window(e)) return st;
+        if (int st = drain_pending(e)) return st;
         e->factor_req = int(value);
         if (e->d_stats) {
             const uint32_t P = e->P;
@@ -971,7 +1010,6 @@ int64_t erx_get_option(const erx_engine* e, int option) {
     if (option == ERX_OPT_STATS_TENSOR) {
         if (!e->d_stats) return e->stats_tensor;
         if (e->tensor) return 2;
-        if (e->stats_tensor == 1 && erxk::stats_tc_eligible(e->geo)) return 1;
         return 0;
     }
     return -1;
@@ -1006,50 +1044,6 @@ int erx_event_elapsed_ms(erx_engine* e, int a, int b, float* ms) {
     if (a < 0 || a >= 8 || b < 0 || b >= 8) return ERX_ERR_CONFIG;
     CU(cudaEventSynchronize(e->user_ev[b]));
     CU(cudaEventElapsedTime(ms, e->user_ev[a], e->user_ev[b]));
-    return ERX_OK;
-}
-
-int erx_probe_fp32_tflops(erx_engine* e, double* reg_form, double* const_form) {
-    CU(cudaSetDevice(e->device));
-    double r = 0, c = 0;
-    erxk::probe_ffma_tflops(e->stream, &r, &c);
-    if (reg_form) *reg_form = r;
-    if (const_form) *const_form = c;
-    CU(cudaGetLastError());
-    return ERX_OK;
-}
-
-int erx_tc_selftest_i8(erx_engine* e, const int8_t* dA, const int8_t* dB, int K, int N, int a_mn, int ms, int ks,
-                       int lbo, int sbo, int* dD) {
-    CU(cudaSetDevice(e->device));
-    if (K < 32 || K % 32 || K > 128 || N < 16 || N > 128 || N % 16) return fail(e, ERX_ERR_CONFIG, "tc_selftest_i8 shape");
-    CU(cudaError_t(erxk::tc_selftest_i8(dA, dB, K, N, a_mn, ms, ks, lbo, sbo, dD, e->stream)));
-    CU(cudaStreamSynchronize(e->stream));
-    return ERX_OK;
-}
-
-int erx_tc_selftest(erx_engine* e, const float* dA, const float* dB, int K, int split, float* dD) {
-    CU(cudaSetDevice(e->device));
-    if (K % 16 || K < 16 || K > 256) return fail(e, ERX_ERR_CONFIG, "K must be a multiple of 16 in [16, 256]");
-    CU(cudaError_t(erxk::tc_selftest(dA, dB, K, split, dD, e->stream)));
-    CU(cudaStreamSynchronize(e->stream));
-    return ERX_OK;
-}
-
-int erx_probe_stream(erx_engine* e, int mode, uint32_t chunk_bytes, int stages, int ctas_per_sm, uint64_t bytes,
-                     double* gbs) {
-    CU(cudaSetDevice(e->device));
-    if (mode < 0 || mode > 2 || stages < 1 || stages > 8 || chunk_bytes % 1024 || ctas_per_sm < 1)
-        return fail(e, ERX_ERR_CONFIG, "probe_stream: bad arguments");
-    *gbs = erxk::probe_stream_gbs(e->stream, mode, int(chunk_bytes), stages, ctas_per_sm, size_t(bytes));
-    CU(cudaGetLastError());
-    return ERX_OK;
-}
-
-int erx_probe_ffma2_tflops(erx_engine* e, double* tflops) {
-    CU(cudaSetDevice(e->device));
-    *tflops = erxk::probe_ffma2_tflops(e->stream);
-    CU(cudaGetLastError());
     return ERX_OK;
 }
 

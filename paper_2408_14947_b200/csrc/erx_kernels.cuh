@@ -70,7 +70,7 @@ void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x
                         int n_lines_total, double* stats, float* vcache, cudaStream_t st);
 void launch_score_small(const Geometry& g, const SmallLaunch& sm, const double* stats, const double* prior,
                         const float* whiten, const float* vcache, int n_lines_total, float* raw, float* norm,
-                        cudaStream_t st);
+                        int* status, int* fixlist, cudaStream_t st);
 
 struct ScoreLaunch {
     int npairs;      // row-block pairs {s, nb-1-s}
@@ -92,11 +92,6 @@ size_t whiten_floats_per_line(const Geometry& g);
 // shared-memory kernel in that precision, 0 the blocked fp64 global-memory kernel.
 int factor_precision(const Geometry& g, int requested);
 size_t factor_smem(const Geometry& g, int precision);
-
-// tcgen05 stats kernel (k_stats_tc.cu): no_srp, 32 < D <= 128, B % 4 == 0.
-bool stats_tc_eligible(const Geometry& g);
-void launch_stats_tc(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
-                     double* stats, cudaStream_t st);
 
 // Exact-integer tcgen05 stats kernel (k_stats_i8.cu): no_srp, 16 < D <= 127, B % 4 == 0.
 bool stats_i8_eligible(const Geometry& g);
@@ -121,26 +116,44 @@ void launch_scan(const Geometry& g, const double* stats, double* prior, const do
                  cudaStream_t st, float* kblk = nullptr);
 // latch: {flag, line, pivot} of the first factorisation failure (sticky until the host clears it).
 // vmax != null (precision 32 only): write the tensor path's int8 W planes (k_factor.cu: write_wplanes,
-// i8::kWBytes per line) instead of the fp32 blocks.
+// i8::kWBytes per line) instead of the fp32 blocks.  The fp32 factors (precision 32 / 31) put lines
+// they cannot take (failed or ill-conditioned pivot) on fixlist for launch_fixup instead of
+// escalating eps in fp32; the fp64 ones escalate and latch themselves.
 void launch_factor(const Geometry& g, const double* prior, int n_lines_total, double eps0, double* work,
-                   float* whiten, int* status, int* latch, int line_base, int precision, cudaStream_t st,
-                   const double* stats = nullptr, const float* vmax = nullptr, const float* kblk = nullptr,
-                   int blk_threads = 0);
+                   float* whiten, int* status, unsigned long long* latch, long long line_base, int precision,
+                   cudaStream_t st, int* fixlist, const double* stats = nullptr, const float* vmax = nullptr,
+                   const float* kblk = nullptr, int blk_threads = 0);
+
+// fp64 rescue of the lines on the fp32 factor's list (k_fixup.cu): background, factor with eps
+// escalation, whitening and normalisation of every listed line redone in fp64 from the line and the
+// window statistics; overwrites their raw / norm rows and writes their final status.
+struct FixupArgs {
+    Geometry g;
+    const float* x;          // window lines: line l = s * n + t at line_ptr(x, l, n, in_stride)
+    int n;
+    int in_stride;
+    const double* stats;     // [L][SE + D] the window's line statistics (k_stats.cu contract)
+    const double* st_in;     // [S][SE] background at the window start
+    int initialized;
+    double alpha;
+    int incremental;
+    long long n_seen0;
+    double eps0;
+    int* list;               // [0] count, [1] CTAs done, [2 ..] listed lines
+    double* work;            // fixup_work_doubles(g, L)
+    float* raw;
+    float* norm;
+    int* status;
+    unsigned long long* latch;
+    long long line_base;
+};
+int fixup_ctas(const Geometry& g, int n_lines_total);
+size_t fixup_work_doubles(const Geometry& g, int n_lines_total);
+void launch_fixup(const FixupArgs& a, int n_lines_total, cudaStream_t st);
 void launch_score(const Geometry& g, const ScoreLaunch& sc, const float* x, int n_per_stream, int in_stride,
                   const double* prior, const float* whiten, int n_lines_total, float* raw, cudaStream_t st);
-void launch_normalize(const Geometry& g, const float* raw, int n_lines_total, float* norm, cudaStream_t st);
-
-// Measured FP32 FFMA throughput of the current device (TFLOP/s, best of 5).
-void probe_ffma_tflops(cudaStream_t st, double* reg_form, double* const_form);
-// Measured paired-FFMA (fma.rn.f32x2) throughput, TFLOP/s counting 2 FMAs per lane.
-double probe_ffma2_tflops(cudaStream_t st);
-// Streaming throughput (GB/s) of a global->shared path (k_stream_probe.cu): mode 0 bulk-copy ring,
-// 1 LDG.128, 2 cp.async ring.
-double probe_stream_gbs(cudaStream_t st, int mode, int chunk_bytes, int stages, int ctas_per_sm, size_t bytes);
-// tcgen05 self-test: D[128][128] = A[128][K] B[128][K]^T (bf16, split = 1: 3-way split, 6 products).
-int tc_selftest(const float* dA, const float* dB, int K, int split, float* dD, cudaStream_t st);
-// kind::i8 self-test: D[128][N] = A[128][K] B[N][K]^T (s32), A K-major or MN-major with (ms, ks) layout strides.
-int tc_selftest_i8(const int8_t* dA, const int8_t* dB, int K, int N, int a_mn, int ms, int ks, int lbo, int sbo,
-                   int* dD, cudaStream_t st);
+// status / fixlist (may be null): lines whose scores are flat at fp32 resolution go to the fp64 rescue
+void launch_normalize(const Geometry& g, const float* raw, int n_lines_total, float* norm, int* status, int* fixlist,
+                      cudaStream_t st);
 
 }  // namespace erxk

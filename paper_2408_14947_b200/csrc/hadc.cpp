@@ -15,8 +15,10 @@
 //  19  layout   u8       1 = line-major [line][pixel][band]
 //  20  name_len u16, then name_len bytes of UTF-8 name
 //  22+name_len  payload, lines * pixels * bands * sizeof(dtype) bytes, nothing after it
-// Every violation is an IoError (ERX_ERR_IO) whose message carries the byte
-// offset ("format error with offset").
+// A malformed or truncated file is had::FormatError (errors.hpp:67-75, kind
+// data): ERX_ERR_DATA with "<what> at offset <n>" in the message (SPEC.md:585
+// "format error with offset").  Only failing to open or read the file is an
+// IoError (ERX_ERR_IO, errors.hpp:77-79).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -64,11 +66,11 @@ int open_impl(const char* path, erx_hadc* h) {
     if (got < kHeaderFixed) {
         std::snprintf(msg, sizeof msg, "%s: truncated header at offset %zu (need %u bytes)", path, got, kHeaderFixed);
         h->err = msg;
-        return ERX_ERR_IO;
+        return ERX_ERR_DATA;
     }
     if (std::memcmp(hdr, "HADC", 4) != 0) {
         h->err = std::string(path) + ": bad magic at offset 0";
-        return ERX_ERR_IO;
+        return ERX_ERR_DATA;
     }
     erx_hadc_info& in = h->info;
     in.version = rd<uint16_t>(hdr + 4);
@@ -81,7 +83,7 @@ int open_impl(const char* path, erx_hadc* h) {
     auto bad = [&](const char* what, int off) {
         std::snprintf(msg, sizeof msg, "%s: %s at offset %d", path, what, off);
         h->err = msg;
-        return ERX_ERR_IO;
+        return ERX_ERR_DATA;
     };
     if (in.version != 1) return bad("unsupported version", 4);
     if (in.lines == 0) return bad("lines = 0", 6);
@@ -95,7 +97,12 @@ int open_impl(const char* path, erx_hadc* h) {
     std::memset(in.name, 0, sizeof in.name);
     std::memcpy(in.name, name.data(), std::min<size_t>(nlen, sizeof in.name - 1));
     h->payload_off = kHeaderFixed + nlen;
-    const uint64_t payload = uint64_t(in.lines) * in.pixels * in.bands * elem_size(in.dtype);
+    uint64_t payload = 0;
+    if (__builtin_mul_overflow(uint64_t(in.lines), uint64_t(in.pixels), &payload) ||
+        __builtin_mul_overflow(payload, uint64_t(in.bands), &payload) ||
+        __builtin_mul_overflow(payload, uint64_t(elem_size(in.dtype)), &payload) ||
+        payload > (uint64_t(1) << 62))
+        return bad("declared payload size overflows", 6);
     std::fseek(h->f, 0, SEEK_END);
     const uint64_t size = uint64_t(std::ftell(h->f));
     if (size != h->payload_off + payload) {
@@ -103,7 +110,7 @@ int open_impl(const char* path, erx_hadc* h) {
                       path, (unsigned long long)h->payload_off, (unsigned long long)(size - h->payload_off),
                       (unsigned long long)payload);
         h->err = msg;
-        return ERX_ERR_IO;
+        return ERX_ERR_DATA;
     }
     return ERX_OK;
 }
@@ -131,7 +138,7 @@ int read_host(erx_hadc* h, uint32_t first, uint32_t n, void* dst) {
                 std::snprintf(msg, sizeof msg, "mask value %u at offset %llu", unsigned(p[i]),
                               (unsigned long long)(off + i));
                 h->err = msg;
-                return ERX_ERR_IO;
+                return ERX_ERR_DATA;
             }
     }
     return ERX_OK;

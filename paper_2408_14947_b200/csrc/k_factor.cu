@@ -16,6 +16,7 @@
 #include <cstdlib>
 
 #include "erx_common.cuh"
+#include "f64_factor.cuh"
 #include "i8_common.cuh"
 
 namespace erxk {
@@ -115,146 +116,10 @@ __device__ void write_wplanes(unsigned char* __restrict__ planes, int line, cons
     }
 }
 
-// ---------------------------------------------------------------------------
-// factor: L = chol(K_{t-1} + eps I) with eps escalation x10 up to 1e-1
-// (SPEC.md:306), then X = L^{-1}, written as fp32 W (Dp x Dp, zeros above the
-// diagonal and in the padding).  One CTA per line; fp64; blocked with panel
-// width kNB over a global (L2-resident) workspace; the diagonal block is
-// factored by one warp in shared memory.
-// ---------------------------------------------------------------------------
-__device__ int chol_blocked(double* __restrict__ A, int D, int Dp, double* Lkk, double* pnl, int* s_fail) {
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int lane = tid & 31, warp = tid >> 5;
-    constexpr int LD = kNB + 1;
-    for (int k0 = 0; k0 < D; k0 += kNB) {
-        const int kb = min(kNB, D - k0);
-        for (int idx = tid; idx < kb * kb; idx += nt) {
-            int r = idx / kb, c = idx - r * kb;
-            if (c <= r) Lkk[r * LD + c] = A[size_t(k0 + r) * Dp + k0 + c];
-        }
-        if (tid == 0) *s_fail = -1;
-        __syncthreads();
-        if (warp == 0) {
-            for (int j = 0; j < kb; ++j) {
-                __syncwarp();
-                const double djj = Lkk[j * LD + j];
-                if (!(djj > 0.0)) {
-                    if (lane == 0) *s_fail = k0 + j;
-                    break;
-                }
-                const double sq = sqrt(djj);
-                __syncwarp();
-                if (lane > j && lane < kb) Lkk[lane * LD + j] /= sq;
-                __syncwarp();
-                if (lane == j) Lkk[j * LD + j] = sq;
-                if (lane > j && lane < kb) {
-                    const double lij = Lkk[lane * LD + j];
-                    for (int c = j + 1; c <= lane; ++c) Lkk[lane * LD + c] -= lij * Lkk[c * LD + j];
-                }
-            }
-        }
-        __syncthreads();
-        if (*s_fail >= 0) return *s_fail;
-        for (int idx = tid; idx < kb * kb; idx += nt) {
-            int r = idx / kb, c = idx - r * kb;
-            if (c <= r) A[size_t(k0 + r) * Dp + k0 + c] = Lkk[r * LD + c];
-        }
-        // panel: rows below the diagonal block, L_ik = A_ik L_kk^{-T}
-        const int r0 = k0 + kb;
-        const int nr = D - r0;
-        for (int r = tid; r < nr; r += nt) {
-            double* prow = pnl + size_t(r) * LD;
-            const double* arow = A + size_t(r0 + r) * Dp + k0;
-            for (int c = 0; c < kb; ++c) {
-                double s = arow[c];
-                for (int l = 0; l < c; ++l) s -= prow[l] * Lkk[c * LD + l];
-                prow[c] = s / Lkk[c * LD + c];
-            }
-            double* w = A + size_t(r0 + r) * Dp + k0;
-            for (int c = 0; c < kb; ++c) w[c] = prow[c];
-        }
-        __syncthreads();
-        // trailing update A22 -= P P^T, 4x4 register tiles over the lower triangle
-        const int nt4 = (nr + 3) / 4;
-        const int ntile = nt4 * (nt4 + 1) / 2;
-        for (int tix = tid; tix < ntile; tix += nt) {
-            int R = int((sqrt(8.0 * tix + 1.0) - 1.0) * 0.5);
-            while (R * (R + 1) / 2 > tix) --R;
-            while ((R + 1) * (R + 2) / 2 <= tix) ++R;
-            const int C = tix - R * (R + 1) / 2;
-            double acc[4][4] = {};
-            for (int l = 0; l < kb; ++l) {
-                double av[4], bv[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    int ri = R * 4 + i, ci = C * 4 + i;
-                    av[i] = (ri < nr) ? pnl[size_t(ri) * LD + l] : 0.0;
-                    bv[i] = (ci < nr) ? pnl[size_t(ci) * LD + l] : 0.0;
-                }
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    int ri = R * 4 + i, ci = C * 4 + j;
-                    if (ri < nr && ci <= ri) A[size_t(r0 + ri) * Dp + r0 + ci] -= acc[i][j];
-                }
-        }
-        __syncthreads();
-    }
-    return -1;
-}
-
-// X = L^{-1} by block rows: X_I = L_II^{-1} (E_I - sum_{J<I} L_IJ X_J).
-__device__ void tri_inverse_blocked(const double* __restrict__ A, double* __restrict__ X, int D, int Dp,
-                                    double* Lrow) {
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int LDR = D + 1;
-    for (int i0 = 0; i0 < D; i0 += kNB) {
-        const int ib = min(kNB, D - i0);
-        const int ncol = i0 + ib;
-        for (int idx = tid; idx < ib * ncol; idx += nt) {
-            int r = idx / ncol, c = idx - r * ncol;
-            Lrow[r * LDR + c] = (c <= i0 + r) ? A[size_t(i0 + r) * Dp + c] : 0.0;
-        }
-        __syncthreads();
-        for (int c = tid; c < ncol; c += nt) {
-            double t[kNB];
-#pragma unroll
-            for (int r = 0; r < kNB; ++r) t[r] = (r < ib && i0 + r == c) ? 1.0 : 0.0;
-            const int jstart = c & ~31;  // warp-uniform start: row-wise (coalesced) loads of X
-            for (int j = jstart; j < i0; ++j) {
-                const double xj = (j >= c) ? X[size_t(j) * Dp + c] : 0.0;
-#pragma unroll
-                for (int r = 0; r < kNB; ++r)
-                    if (r < ib) t[r] = fma(-Lrow[r * LDR + j], xj, t[r]);
-            }
-#pragma unroll
-            for (int r = 0; r < kNB; ++r) {
-                if (r < ib) {
-                    double s = t[r];
-#pragma unroll
-                    for (int j = 0; j < r; ++j) s = fma(-Lrow[r * LDR + i0 + j], t[j], s);
-                    t[r] = s / Lrow[r * LDR + i0 + r];
-                    if (i0 + r < c) t[r] = 0.0;
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < kNB; ++r)
-                if (r < ib) X[size_t(i0 + r) * Dp + c] = t[r];
-        }
-        __syncthreads();
-    }
-}
-
 __global__ void __launch_bounds__(256) factor_global_kernel(Geometry g, const double* __restrict__ prior, double eps0,
                                                      double* __restrict__ work, float* __restrict__ whiten,
-                                                     int* __restrict__ status, int* __restrict__ latch,
-                                                     int line_base) {
+                                                     int* __restrict__ status, unsigned long long* __restrict__ latch,
+                                                     long long line_base) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_fail;
     const int line = blockIdx.x;
@@ -283,9 +148,9 @@ __global__ void __launch_bounds__(256) factor_global_kernel(Geometry g, const do
     if (fail >= 0) {
         if (tid == 0) {
             status[line] = fail;
-            if (atomicCAS(latch, 0, 1) == 0) {
-                latch[1] = line_base + line;
-                latch[2] = fail;
+            if (atomicCAS(latch, 0ull, 1ull) == 0ull) {
+                latch[1] = static_cast<unsigned long long>(line_base + line);
+                latch[2] = static_cast<unsigned long long>(fail);
             }
         }
         return;
@@ -408,8 +273,8 @@ __device__ __forceinline__ void load_panel_t(float* __restrict__ Pt, int LDT, co
 
 __global__ void __launch_bounds__(256) factor_big_kernel(Geometry g, const double* __restrict__ prior, double eps0,
                                                          float* __restrict__ work, float* __restrict__ whiten,
-                                                         int* __restrict__ status, int* __restrict__ latch,
-                                                         int line_base, bool xk_smem) {
+                                                         int* __restrict__ status, int* __restrict__ fixlist,
+                                                         bool xk_smem) {
     extern __shared__ __align__(16) float fsm[];
     __shared__ int s_fail;
     const int line = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
@@ -422,11 +287,12 @@ __global__ void __launch_bounds__(256) factor_big_kernel(Geometry g, const doubl
     float* Di = Lkk + kBB * kLD;             // [32][33] L_kk^{-1}
     float* Pt = Di + kBB * kLD;              // [32][LDT]: panel / L column block (transposed), T_k staging
     float* Xk = Pt + kBB * LDT;              // [32][LDT]: finished X block row (xk_smem)
+    float* dg = Xk + (xk_smem ? kBB * LDT : 0);  // [Dp]: diagonal of K + eps I (the conditioning test)
     const double* K = prior + size_t(line) * g.SE + D;
     const int ntri = D * (D + 1) / 2;
-    double eps = eps0;
+    const double eps = eps0;
     int fail = -1;
-    while (true) {
+    {
         {   // fill the lower triangle (packed fp64 K -> fp32 A), 8 loads in flight per thread
             int i = int((sqrtf(8.f * tid + 1.f) - 1.f) * 0.5f), j;
             while (i * (i + 1) / 2 > tid) --i;
@@ -448,8 +314,11 @@ __global__ void __launch_bounds__(256) factor_big_kernel(Geometry g, const doubl
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
-                    if (idx + u * nt < ntri)
-                        A[size_t(iu[u]) * Dp + ju[u]] = float(kv[u] + (iu[u] == ju[u] ? eps : 0.0));
+                    if (idx + u * nt < ntri) {
+                        const float v = float(kv[u] + (iu[u] == ju[u] ? eps : 0.0));
+                        A[size_t(iu[u]) * Dp + ju[u]] = v;
+                        if (iu[u] == ju[u]) dg[iu[u]] = v;
+                    }
             }
         }
         __syncthreads();
@@ -473,7 +342,7 @@ __global__ void __launch_bounds__(256) factor_big_kernel(Geometry g, const doubl
                 for (int jj = 0; jj < kBB; ++jj) {
                     if (jj < kb && f < 0) {
                         const float d = __shfl_sync(0xffffffffu, row[jj], jj);
-                        if (!(d > 0.f)) {
+                        if (!(d > 0.f) || d * kCondTau < dg[k0 + jj]) {  // failed or ill-conditioned: fp64
                             f = k0 + jj;
                         } else {
                             const float rs = rsqrt_nr(d);
@@ -543,20 +412,9 @@ __global__ void __launch_bounds__(256) factor_big_kernel(Geometry g, const doubl
                             lane, nw);
             __syncthreads();
         }
-        if (fail < 0) break;
-        const double next = eps * 10.0;
-        if (!(next <= 1e-1 * (1.0 + 1e-9))) break;
-        eps = next;
-        __syncthreads();
     }
-    if (fail >= 0) {
-        if (tid == 0) {
-            status[line] = fail;
-            if (atomicCAS(latch, 0, 1) == 0) {
-                latch[1] = line_base + line;
-                latch[2] = fail;
-            }
-        }
+    if (fail >= 0) {  // the fp64 rescue (k_fixup.cu) redoes this line, escalation included
+        if (tid == 0) list_for_fixup(fixlist, status, line);
         return;
     }
     // X = L^{-1}, right-looking by block rows.  Before step k, X's block row k holds
@@ -615,7 +473,7 @@ __global__ void __launch_bounds__(256) factor_big_kernel(Geometry g, const doubl
 template <typename T>
 __global__ void __launch_bounds__(256) factor_smem_kernel(Geometry g, const double* __restrict__ prior, double eps0,
                                                           float* __restrict__ whiten, int* __restrict__ status,
-                                                          int* __restrict__ latch, int line_base) {
+                                                          unsigned long long* __restrict__ latch, long long line_base) {
     extern __shared__ __align__(16) unsigned char smem[];
     T* A = reinterpret_cast<T*>(smem);
     const int D = g.D, LD = D + 1;  // odd leading dimension: conflict-free column walks
@@ -654,9 +512,9 @@ __global__ void __launch_bounds__(256) factor_smem_kernel(Geometry g, const doub
     if (fail >= 0) {
         if (tid == 0) {
             status[line] = fail;
-            if (atomicCAS(latch, 0, 1) == 0) {
-                latch[1] = line_base + line;
-                latch[2] = fail;
+            if (atomicCAS(latch, 0ull, 1ull) == 0ull) {
+                latch[1] = static_cast<unsigned long long>(line_base + line);
+                latch[2] = static_cast<unsigned long long>(fail);
             }
         }
         return;
@@ -734,15 +592,16 @@ __device__ __forceinline__ void st8r(float* blk, int r, const float* v) {
 // Eight lanes (one aligned 8-lane group, lane gl holding row gl of an updated diagonal block in
 // row[]) factor the block (Cholesky, 1/sqrt from MUFU.RSQ + one Newton step) and invert the
 // factor (lane c: column c by forward substitution).  Di goes to blk (swizzled rows, zeros above the
-// diagonal), Di^T to dit (plain rows).  Returns the first non-positive pivot (k0 + j) or -1, group-uniform.
+// diagonal), Di^T to dit (plain rows).  Returns the first pivot (k0 + j) that is non-positive or below
+// dg / kCondTau (dg: the diagonal of K + eps I), or -1, group-uniform.
 __device__ __forceinline__ int diag_factor8(float (&row)[kBlk], unsigned gmask, int gl, int k0, float* blk,
-                                            float* dit) {
+                                            float* dit, const float* dg) {
     int f = -1;
     float rd[kBlk];
 #pragma unroll
     for (int j = 0; j < kBlk; ++j) {
         float d = __shfl_sync(gmask, row[j], j, kBlk);
-        if (!(d > 0.f)) {
+        if (!(d > 0.f) || d * kCondTau < dg[k0 + j]) {
             if (f < 0) f = k0 + j;
             d = 1.f;
         }
@@ -777,7 +636,7 @@ template <int NT, int MB>
 __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const double* __restrict__ prior,
                                                                           double eps0, float* __restrict__ whiten,
                                                                           int* __restrict__ status,
-                                                                          int* __restrict__ latch, int line_base,
+                                                                          int* __restrict__ fixlist,
                                                                           const double* __restrict__ stats,
                                                                           const float* __restrict__ vmax,
                                                                           const float* __restrict__ kblk) {
@@ -791,15 +650,18 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
     auto EL = [&](int i, int j) { return BP(i >> 3, j >> 3) + swz(i & 7, j & 7); };
     float* Lc = A + size_t(nb * (nb + 1) / 2) * 64;  // [nb][kLcLd]: the current panel L_Ik (swizzled rows)
     float* DiT = Lc + size_t(nb) * kLcLd;       // [64]: Di^T of the current diagonal block (plain rows)
+    // [Dp]: diagonal of K + eps I for the conditioning test (past the plane writer's scratch, which reuses
+    // Lc + DiT after the factorisation)
+    float* dg = Lc + (size_t(nb) * kLcLd + 64 > 384 ? size_t(nb) * kLcLd + 64 : 384);
     const int line = blockIdx.x, tid = threadIdx.x;
     constexpr int nt = NT, nw = NT / 32;
     const int lane = tid & 31, gl = lane & 7, warp = tid >> 5, grp = lane >> 3;
     const unsigned gmask = 0xffu << (lane & 24);
     const double* K = prior + size_t(line) * g.SE + D;
-    double eps = eps0;
+    const double eps = eps0;
     int fail;
     const int ntri = D * (D + 1) / 2;
-    while (true) {
+    {
         if (tid == 0) s_fail = -1;
         if (kblk) {
             // fill from the scan's fp32 block image (same swizzled layout): a straight 16-byte copy,
@@ -814,8 +676,12 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
             for (int q = tid; q < nb * 64; q += nt) {
                 const int kk = q >> 6, r = (q >> 3) & 7, c = q & 7;
                 float* p = BP(kk, kk) + swz(r, c);
-                if (c > r) *p = 0.f;
-                else if (c == r && kk * kBlk + r < D) *p += fe;
+                if (c > r) {
+                    *p = 0.f;
+                } else if (c == r && kk * kBlk + r < D) {
+                    *p += fe;
+                    dg[kk * kBlk + r] = *p;
+                }
             }
         } else {
             // fill: coalesced reads of the packed fp64 K, 1024 loads in flight per line (the (i, j) of
@@ -842,17 +708,23 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
                 }
 #pragma unroll
                 for (int u = 0; u < kFill; ++u)
-                    if (base + u * nt < ntri) *EL(ii[u], jj[u]) = float(v[u] + (ii[u] == jj[u] ? eps : 0.0));
+                    if (base + u * nt < ntri) {
+                        const float fv = float(v[u] + (ii[u] == jj[u] ? eps : 0.0));
+                        *EL(ii[u], jj[u]) = fv;
+                        if (ii[u] == jj[u]) dg[ii[u]] = fv;
+                    }
             }
         }
         __syncthreads();
-        for (int i = D + tid; i < Dp; i += nt)  // padding dims: identity
+        for (int i = D + tid; i < Dp; i += nt) {  // padding dims: identity
             for (int j = 0; j <= i; ++j) *EL(i, j) = (i == j) ? 1.f : 0.f;
+            dg[i] = 1.f;
+        }
         __syncthreads();
         if (tid < kBlk) {  // block (0, 0)
             float row[kBlk];
             ld8r(BP(0, 0), gl, row);
-            const int f = diag_factor8(row, gmask, gl, 0, BP(0, 0), DiT);
+            const int f = diag_factor8(row, gmask, gl, 0, BP(0, 0), DiT, dg);
             if (gl == 0 && f >= 0) s_fail = f;
         }
         __syncthreads();
@@ -934,7 +806,7 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
                         for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], b[l], acc[c]);
                     }
                     st8r(blk, r, acc);
-                    const int f = diag_factor8(acc, gmask, gl, (k + 1) * kBlk, blk, DiT);
+                    const int f = diag_factor8(acc, gmask, gl, (k + 1) * kBlk, blk, DiT, dg);
                     if (gl == 0 && f >= 0) s_fail = f;
                     ir = step;
                 }
@@ -994,20 +866,9 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
             __syncthreads();
             fail = s_fail;
         }
-        if (fail < 0) break;
-        const double next = eps * 10.0;
-        if (!(next <= 1e-1 * (1.0 + 1e-9))) break;
-        eps = next;
-        __syncthreads();
     }
-    if (fail >= 0) {
-        if (tid == 0) {
-            status[line] = fail;
-            if (atomicCAS(latch, 0, 1) == 0) {
-                latch[1] = line_base + line;
-                latch[2] = fail;
-            }
-        }
+    if (fail >= 0) {  // the fp64 rescue (k_fixup.cu) redoes this line, escalation included
+        if (tid == 0) list_for_fixup(fixlist, status, line);
         return;
     }
     if (vmax) {
@@ -1023,11 +884,14 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
 
 size_t factor_blk_smem(const Geometry& g) {
     // packed blocks + Lc (kLcLd per block) + Di^T (the plane writer's 1.5 KB scratch reuses Lc + Di^T)
-    return (size_t(g.nb) * (g.nb + 1) / 2 * 64 + std::max<size_t>(size_t(g.nb) * kLcLd + 64, 6 * 64)) * 4;
+    // + the diagonal for the conditioning test
+    return (size_t(g.nb) * (g.nb + 1) / 2 * 64 + std::max<size_t>(size_t(g.nb) * kLcLd + 64, 6 * 64) + g.Dp) * 4;
 }
 
-// factor_big: Lkk + Di, the transposed panel, and (when it fits) the finished X block row
-size_t factor_big_smem(const Geometry& g, bool xk) { return (2 * size_t(kBB) * kLD + (xk ? 2 : 1) * size_t(kBB) * (g.Dp + 4)) * 4; }
+// factor_big: Lkk + Di, the transposed panel, (when it fits) the finished X block row, the diagonal
+size_t factor_big_smem(const Geometry& g, bool xk) {
+    return (2 * size_t(kBB) * kLD + (xk ? 2 : 1) * size_t(kBB) * (g.Dp + 4) + g.Dp) * 4;
+}
 bool factor_big_xk(const Geometry& g) { return factor_big_smem(g, true) <= 220 * 1024; }
 
 size_t factor_smem(const Geometry& g, int precision) {
@@ -1053,8 +917,9 @@ int factor_precision(const Geometry& g, int requested) {
 }
 
 void launch_factor(const Geometry& g, const double* prior, int n_lines_total, double eps0, double* work,
-                   float* whiten, int* status, int* latch, int line_base, int precision, cudaStream_t st,
-                   const double* stats, const float* vmax, const float* kblk, int blk_threads) {
+                   float* whiten, int* status, unsigned long long* latch, long long line_base, int precision,
+                   cudaStream_t st, int* fixlist, const double* stats, const float* vmax, const float* kblk,
+                   int blk_threads) {
     const size_t sm = factor_smem(g, precision);
     if (precision == 32) {
         ensure_smem(factor_blk_kernel<64, 7>, sm);
@@ -1072,21 +937,21 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
         int threads = std::min(cap, per_sm) >= 6 ? 128 : 256;
         if (blk_threads) threads = blk_threads;  // ERX_OPT_FACTOR_THREADS
         if (threads == 64)
-            factor_blk_kernel<64, 7><<<n_lines_total, 64, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base, stats,
+            factor_blk_kernel<64, 7><<<n_lines_total, 64, sm, st>>>(g, prior, eps0, whiten, status, fixlist, stats,
                                                                  vmax, kblk);
         else if (threads == 128)
-            factor_blk_kernel<128, 7><<<n_lines_total, 128, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base,
-                                                                   stats, vmax, kblk);
+            factor_blk_kernel<128, 7><<<n_lines_total, 128, sm, st>>>(g, prior, eps0, whiten, status, fixlist, stats,
+                                                                   vmax, kblk);
         else
-            factor_blk_kernel<256, 3><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base,
-                                                                   stats, vmax, kblk);
+            factor_blk_kernel<256, 3><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, fixlist, stats,
+                                                                   vmax, kblk);
     } else if (precision == 64) {
         ensure_smem(factor_smem_kernel<double>, sm);
         factor_smem_kernel<double><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base);
     } else if (precision == 31) {
         ensure_smem(factor_big_kernel, sm);
         factor_big_kernel<<<n_lines_total, 256, sm, st>>>(g, prior, eps0, reinterpret_cast<float*>(work), whiten,
-                                                          status, latch, line_base, factor_big_xk(g));
+                                                          status, fixlist, factor_big_xk(g));
     } else {
         ensure_smem(factor_global_kernel, sm);
         factor_global_kernel<<<n_lines_total, 256, sm, st>>>(g, prior, eps0, work, whiten, status, latch,

@@ -7,24 +7,10 @@
 //
 // Input per line (k_stats.cu): [c | s | S]; line statistics are finished
 // here:  mu_hat = c + s/P,  K_hat = (S - s_a s_b / P) / (P - 1).
-#include "erx_common.cuh"
+#include "scan_rec.cuh"
 
 namespace erxk {
 namespace {
-
-// mu_hat = c + s / P or K_hat = (S - s_a s_b / P) / (P - 1) from the stats slot values x0 (c or S),
-// x1, x2 (s_a, s_b); explicit roundings (no FMA contraction) so every scan variant agrees bitwise
-__device__ __forceinline__ double finish_stat(bool is_mu, double x0, double x1, double x2, double invP, double invP1) {
-    return is_mu ? __dadd_rn(x0, __dmul_rn(x1, invP))
-                 : __dmul_rn(__dsub_rn(x0, __dmul_rn(__dmul_rn(x1, x2), invP)), invP1);
-}
-
-__device__ __forceinline__ void unpack_tri(int k, int& a, int& b) {
-    a = int((sqrt(8.0 * k + 1.0) - 1.0) * 0.5);
-    while (a * (a + 1) / 2 > k) --a;
-    while ((a + 1) * (a + 2) / 2 <= k) ++a;
-    b = k - a * (a + 1) / 2;
-}
 
 __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __restrict__ stats,
                                                    double* __restrict__ prior, const double* __restrict__ st_in,
@@ -53,8 +39,8 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
     const double* in = st_in + size_t(s) * g.SE;
     const size_t l0 = size_t(s) * n;
     // line statistics of line l, this element (and the two means it couples)
-    auto mu_hat = [&](const double* st, int j) { return st[j] + st[D + j] * invP; };
-    auto k_hat = [&](const double* st) { return (st[2 * D + (e - D)] - st[D + a] * st[D + b] * invP) * invP1; };
+    auto mu_hat = [&](const double* st, int j) { return finish_stat(true, st[j], st[D + j], 0.0, invP, invP1); };
+    auto k_hat = [&](const double* st) { return finish_stat(false, st[2 * D + (e - D)], st[D + a], st[D + b], invP, invP1); };
     if (!incremental) {
         const double om = 1.0 - alpha;
         double state = in[e];
@@ -91,7 +77,7 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
                         state = cur[u];
                     } else {
                         pr = state;
-                        state = __dadd_rn(__dmul_rn(om, state), __dmul_rn(alpha, cur[u]));
+                        state = ema_step(state, cur[u], om, alpha);
                     }
                     put(l0 + t, pr);
                 }
@@ -101,37 +87,28 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
         }
         st_out[size_t(s) * g.SE + e] = state;
     } else {
-        double ma = in[a], mb = in[b];
-        double cov = (e >= D) ? in[e] : 0.0;
-        double nseen = double(n_seen0);
+        const bool is_cov = e >= D;
+        WelfordElem w{in[a], in[b], is_cov ? in[e] : 0.0, double(n_seen0)};
         const double nb = P;
         for (int t = 0; t < n; ++t) {
             const size_t l = l0 + t;
             const double* st = stats + l * SS;
             const double mha = mu_hat(st, a), mhb = mu_hat(st, b);
+            const double kh = is_cov ? k_hat(st) : 0.0;
             double pr;
             if (!initialized && t == 0) {
-                ma = mha;
-                mb = mhb;
-                if (e >= D) cov = k_hat(st);
-                nseen = nb;
-                pr = (e < D) ? ma : cov;
+                w.ma = mha;
+                w.mb = mhb;
+                if (is_cov) w.cov = kh;
+                w.nseen = nb;
+                pr = is_cov ? w.cov : w.ma;
             } else {
-                pr = (e < D) ? ma : cov;
-                const double na = nseen, nn = na + nb;
-                const double da = mha - ma, db = mhb - mb;
-                if (e >= D) {
-                    const double m2a = (na >= 2.0) ? cov * (na - 1.0) : 0.0;
-                    const double m2b = k_hat(st) * (nb - 1.0);
-                    const double m2 = m2a + m2b + da * db * (na * nb / nn);
-                    cov = (nn >= 2.0) ? m2 / (nn - 1.0) : 0.0;
-                }
-                ma += da * (nb / nn);
-                mb += db * (nb / nn);
-                nseen = nn;
+                pr = is_cov ? w.cov : w.ma;
+                welford_step(w, is_cov, mha, mhb, kh, nb);
             }
             put(l, pr);
         }
+        const double ma = w.ma, cov = w.cov;
         st_out[size_t(s) * g.SE + e] = (e < D) ? ma : cov;
     }
 }
@@ -197,7 +174,7 @@ __global__ void __launch_bounds__(NTH) scan_chunk_kernel(Geometry g, const doubl
                         state = cur;
                     } else {
                         pr = state;
-                        state = __dadd_rn(__dmul_rn(om, state), __dmul_rn(alpha, cur));
+                        state = ema_step(state, cur, om, alpha);
                     }
                     pc[t * 32 + lane] = pr;
                 }

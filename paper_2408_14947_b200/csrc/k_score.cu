@@ -250,7 +250,8 @@ __global__ void __launch_bounds__(512) score_kernel(ScoreArgs a) {
 // normalize_scores: per-line z-score, population std, std < 1e-12 -> zeros
 // (detector.hpp:29-32).  One warp per line, fp64.
 __global__ void __launch_bounds__(128) normalize_kernel(int P, const float* __restrict__ raw, int n_lines,
-                                                        float* __restrict__ norm) {
+                                                        float* __restrict__ norm, int* __restrict__ status,
+                                                        int* __restrict__ fixlist) {
     const int line = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (line >= n_lines) return;
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(128) normalize_kernel(int P, const float* __re
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     const double sd = sqrt(v / double(P));
+    if (lane == 0 && fixlist && flat_line(mean, sd) && status[line] != -2) list_for_fixup(fixlist, status, line);
     float* out = norm + size_t(line) * P;
     for (int i = lane; i < P; i += 32) out[i] = (sd < 1e-12) ? 0.f : float((double(r[i]) - mean) / sd);
 }
@@ -310,8 +312,9 @@ void launch_score(const Geometry& g, const ScoreLaunch& sc, const float* x, int 
     score_kernel<<<n_lines_total * sc.tiles, sc.threads, sc.smem, st>>>(a);
 }
 
-void launch_normalize(const Geometry& g, const float* raw, int n_lines_total, float* norm, cudaStream_t st) {
-    normalize_kernel<<<(n_lines_total + 3) / 4, 128, 0, st>>>(g.P, raw, n_lines_total, norm);
+void launch_normalize(const Geometry& g, const float* raw, int n_lines_total, float* norm, int* status, int* fixlist,
+                      cudaStream_t st) {
+    normalize_kernel<<<(n_lines_total + 3) / 4, 128, 0, st>>>(g.P, raw, n_lines_total, norm, status, fixlist);
 }
 
 }  // namespace erxk

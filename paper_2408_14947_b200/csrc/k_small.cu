@@ -48,7 +48,7 @@ __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) 
 // Warp 0 derives the centre c (fp64 mean of the first min(32, P) projected pixels) while the first
 // chunks load.
 template <int DM>
-__global__ void __launch_bounds__(kStatsSmallThreads, DM <= 10 ? 4 : 1) stats_small_kernel(SmallArgs a) {
+__global__ void __launch_bounds__(kStatsSmallThreads, DM <= 8 ? 4 : (DM <= 10 ? 2 : 1)) stats_small_kernel(SmallArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int kW = kStatsSmallThreads / 32;
     constexpr int DT = DM * (DM + 1) / 2;
@@ -129,11 +129,14 @@ __global__ void __launch_bounds__(kStatsSmallThreads, DM <= 10 ? 4 : 1) stats_sm
         }
     }
     __syncthreads();
-    float s1[DM], s2[DT];
+    // fp64 partial sums: the fp32 products v_a v_b are exact in fp64 (48-bit significands), so the
+    // only rounding left is v = fl32(z - c) itself (an ill-conditioned background, e.g. radiance-scale
+    // lines with little sensor noise, amplifies fp32 product rounding ~1e5-fold into the scores)
+    double s1[DM], s2[DT];
 #pragma unroll
-    for (int j = 0; j < DM; ++j) s1[j] = 0.f;
+    for (int j = 0; j < DM; ++j) s1[j] = 0.0;
 #pragma unroll
-    for (int j = 0; j < DT; ++j) s2[j] = 0.f;
+    for (int j = 0; j < DT; ++j) s2[j] = 0.0;
     for (int ci = warp, it = 0; ci < nck; ci += kW, ++it) {
         if (ci + kW < nck) cp_async_wait<1>();
         else cp_async_wait<0>();
@@ -154,9 +157,10 @@ __global__ void __launch_bounds__(kStatsSmallThreads, DM <= 10 ? 4 : 1) stats_sm
             }
 #pragma unroll
             for (int i = 0; i < DM; ++i) {
-                s1[i] += v[i];
+                const double vi = double(v[i]);
+                s1[i] += vi;
 #pragma unroll
-                for (int j = 0; j <= i; ++j) s2[i * (i + 1) / 2 + j] = fmaf(v[i], v[j], s2[i * (i + 1) / 2 + j]);
+                for (int j = 0; j <= i; ++j) s2[i * (i + 1) / 2 + j] = fma(vi, double(v[j]), s2[i * (i + 1) / 2 + j]);
             }
         }
         __syncwarp();  // the stage is refilled next
@@ -169,7 +173,7 @@ __global__ void __launch_bounds__(kStatsSmallThreads, DM <= 10 ? 4 : 1) stats_sm
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < DM; ++i) {
-        double v = double(s1[i]);
+        double v = s1[i];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0 && i < D) red[warp][i] = v;
@@ -178,7 +182,7 @@ __global__ void __launch_bounds__(kStatsSmallThreads, DM <= 10 ? 4 : 1) stats_sm
     for (int i = 0; i < DM; ++i)
 #pragma unroll
         for (int j = 0; j <= i; ++j) {
-            double v = double(s2[i * (i + 1) / 2 + j]);
+            double v = s2[i * (i + 1) / 2 + j];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
             if (lane == 0 && i < D) red[warp][D + i * (i + 1) / 2 + j] = v;
@@ -256,12 +260,12 @@ __global__ void __launch_bounds__(kStatsSmallThreads) stats_small_srp_kernel(Sma
     __syncthreads();
     constexpr int DT = DM * (DM + 1) / 2;
 
-    // per-thread partial sums over its pixels (few per thread), fp32 -> fp64 at the end
-    float s1[DM], s2[DT];
+    // per-thread partial sums over its pixels (few per thread), fp64 (exact products, as above)
+    double s1[DM], s2[DT];
 #pragma unroll
-    for (int j = 0; j < DM; ++j) s1[j] = 0.f;
+    for (int j = 0; j < DM; ++j) s1[j] = 0.0;
 #pragma unroll
-    for (int j = 0; j < DT; ++j) s2[j] = 0.f;
+    for (int j = 0; j < DT; ++j) s2[j] = 0.0;
 
     for (int c = 0; c < nchunks; ++c) {
         if (c + 1 < nchunks) {
@@ -306,9 +310,10 @@ __global__ void __launch_bounds__(kStatsSmallThreads) stats_small_srp_kernel(Sma
             for (int j = 0; j < DM; ++j) v[j] = (j < D) ? vs[pp * DM + j] : 0.f;
 #pragma unroll
             for (int i = 0; i < DM; ++i) {
-                s1[i] += v[i];
+                const double vi = double(v[i]);
+                s1[i] += vi;
 #pragma unroll
-                for (int j = 0; j <= i; ++j) s2[i * (i + 1) / 2 + j] = fmaf(v[i], v[j], s2[i * (i + 1) / 2 + j]);
+                for (int j = 0; j <= i; ++j) s2[i * (i + 1) / 2 + j] = fma(vi, double(v[j]), s2[i * (i + 1) / 2 + j]);
             }
         }
         __syncthreads();  // stage (c & 1) and vs are refilled at iteration c + 1
@@ -355,7 +360,8 @@ __global__ void __launch_bounds__(kSmallThreads, 4) score_small_kernel(Geometry 
                                                                     const double* __restrict__ prior,
                                                                     const float* __restrict__ Wp,
                                                                     const float* __restrict__ vcache,
-                                                                    float* __restrict__ raw, float* __restrict__ norm) {
+                                                                    float* __restrict__ raw, float* __restrict__ norm,
+                                                                    int* __restrict__ status, int* __restrict__ fixlist) {
     extern __shared__ __align__(16) unsigned char smem[];
     float* dl = reinterpret_cast<float*>(smem);  // raw scores of the line [P]
     __shared__ float Wd[16][16];
@@ -443,6 +449,7 @@ __global__ void __launch_bounds__(kSmallThreads, 4) score_small_kernel(Geometry 
     }
     __syncthreads();
     const double sd = sd_s;
+    if (tid == 0 && fixlist && flat_line(mean, sd) && status[line] != -2) list_for_fixup(fixlist, status, line);
     for (int p = tid; p < g.P; p += kSmallThreads)
         norm[size_t(line) * g.P + p] = (sd < 1e-12) ? 0.f : float((double(dl[p]) - mean) / sd);
 }
@@ -518,7 +525,7 @@ void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x
 
 void launch_score_small(const Geometry& g, const SmallLaunch& sm, const double* stats, const double* prior,
                         const float* whiten, const float* vcache, int n_lines_total, float* raw, float* norm,
-                        cudaStream_t st) {
+                        int* status, int* fixlist, cudaStream_t st) {
     {
         ensure_smem(score_small_kernel<8>, 200 * 1024);
         ensure_smem(score_small_kernel<5>, 200 * 1024);
@@ -528,19 +535,19 @@ void launch_score_small(const Geometry& g, const SmallLaunch& sm, const double* 
     }
     if (g.D == 5)  // the reference default, d = 5
         score_small_kernel<5><<<n_lines_total, kSmallThreads, sm.smem_score, st>>>(g, stats, prior, whiten, vcache,
-                                                                                   raw, norm);
+                                                                                   raw, norm, status, fixlist);
     else if (g.D <= 8)
         score_small_kernel<8><<<n_lines_total, kSmallThreads, sm.smem_score, st>>>(g, stats, prior, whiten, vcache,
-                                                                                   raw, norm);
+                                                                                   raw, norm, status, fixlist);
     else if (g.D == 10)  // configs[2]
         score_small_kernel<10><<<n_lines_total, kSmallThreads, sm.smem_score, st>>>(g, stats, prior, whiten, vcache,
-                                                                                    raw, norm);
+                                                                                    raw, norm, status, fixlist);
     else if (g.D <= 12)
         score_small_kernel<12><<<n_lines_total, kSmallThreads, sm.smem_score, st>>>(g, stats, prior, whiten, vcache,
-                                                                                    raw, norm);
+                                                                                    raw, norm, status, fixlist);
     else
         score_small_kernel<16><<<n_lines_total, kSmallThreads, sm.smem_score, st>>>(g, stats, prior, whiten, vcache,
-                                                                                    raw, norm);
+                                                                                    raw, norm, status, fixlist);
 }
 
 }  // namespace erxk

@@ -18,8 +18,10 @@
 //           four s32 TMEM accumulators, one per weight class 2^(8(i+j)).
 //
 // Every s32 sum is exact (|class sum| <= 3 * 2^14 * P < 2^31 for P < 43690);
-// the only approximations are the quantisation of v (2^-23 of the per-dim
-// range) and the dropped class-0 products (2^-30 relative): emulated
+// the class-0 products d0 d0 are summed exactly on the diagonal by the
+// quantiser (int32) and dropped off it; the only approximations are the
+// quantisation of v (2^-23 of the per-dim range) and the dropped off-diagonal
+// class-0 products (zero-mean, 2^-30 relative): emulated
 // max / median raw-score error vs fp64 on configs[3] (tools/emulate_i8.py)
 // well inside the fp32 FFMA kernel's 2.5e-6 / 1.2e-7.
 // An extra operand row D holds q = 256 (digit d1 = 1) on real pixels, so
@@ -109,6 +111,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     __shared__ double inv_s[128];
     __shared__ double sum_s[128];
     __shared__ int bad_s[8];
+    __shared__ int c0_s[4][128];  // per pixel group: sum_p d0^2 of each dim (the class-0 diagonal)
 
     const Geometry& g = a.g;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -234,8 +237,10 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                                            (static_cast<long long>(int(v[2][ii])) << 24) +
                                            (static_cast<long long>(int(v[1][ii])) << 16) +
                                            (static_cast<long long>(int(v[0][ii])) << 8);
-                    const double si = double(si_i);
-                    if (e <= row) S[tri(row, e)] = si * ia * inv_s[e];
+                    const double si = double(si_i);  // (the ones column: no class-0 term)
+                    const long long c0 = (e == row) ? (long long)(c0_s[0][row]) + c0_s[1][row] + c0_s[2][row] + c0_s[3][row]
+                                                    : 0ll;
+                    if (e <= row) S[tri(row, e)] = double(si_i + c0) * ia * inv_s[e];
                     if (e == D) sum_s[row] = si * (1.0 / 256.0) * ia;
                 }
             }
@@ -256,6 +261,11 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     };
 
     float cdk[2] = {0.f, 0.f}, sdk[2] = {0.f, 0.f}, adk[2] = {kMagic, kMagic};
+    // class-0 products (d0 d0, weight 1) are not accumulated by the MMAs; on the diagonal they are a
+    // systematic + sum_p d0^2 (~P 2^14 / 3 in q^2 units), which biases K's small eigenvalues when the
+    // background is ill-conditioned, so the quantiser sums them exactly here (off the diagonal they
+    // are zero-mean and stay dropped: 2^-30 relative)
+    int c0a = 0, c0b = 0;
     int j = 0;  // position in the chunk sequence (as the producer's)
     for (int k = 0; k <= my_lines; ++k) {
         const bool do1 = k < my_lines, do2 = k >= 1;
@@ -323,6 +333,12 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                             u0[e] = __float_as_uint(fmaf(xp[ld0] - cdk[0], sdk[0], adk[0])) + (0x808080u - 0x4B400000u);
                             u1[e] = __float_as_uint(fmaf(xp[ld1] - cdk[1], sdk[1], adk[1])) + (0x808080u - 0x4B400000u);
                         }
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int d0a = int(u0[e] & 0xffu) - 128, d0b = int(u1[e] & 0xffu) - 128;
+                            c0a += d0a * d0a;
+                            c0b += d0b * d0b;
+                        }
                         pack_digits(u0, w[0][0][jj], w[0][1][jj], w[0][2][jj]);
                         pack_digits(u1, w[1][0][jj], w[1][1][jj], w[1][2][jj]);
                     }
@@ -337,6 +353,9 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                             u0[e] = __float_as_uint(fmaf(xp[ld0] - cdk[0], sdk[0], adk[0])) + (0x808080u - 0x4B400000u);
                             u1[e] = __float_as_uint(fmaf(xp[ld1] - cdk[1], sdk[1], adk[1])) + (0x808080u - 0x4B400000u);
                             if (p >= n) u0[e] = u1[e] = 0x808080u;
+                            const int d0a = int(u0[e] & 0xffu) - 128, d0b = int(u1[e] & 0xffu) - 128;
+                            c0a += d0a * d0a;
+                            c0b += d0b * d0b;
                         }
                         pack_digits(u0, w[0][0][jj], w[0][1][jj], w[0][2][jj]);
                         pack_digits(u1, w[1][0][jj], w[1][1][jj], w[1][2][jj]);
@@ -374,8 +393,14 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                 }
             }
         }
-        // ---- line k-1 is complete: its epilogue (reads bad_s / cen_s / inv_s of line k-1)
-        if (do2) epilogue(k - 1);
+        // ---- line k-1 is complete: its epilogue (reads bad_s / cen_s / inv_s / c0_s of line k-1)
+        if (do2) {
+            c0_s[pg2][dd0] = c0a;
+            c0_s[pg2][dd1] = c0b;
+            c0a = c0b = 0;
+            bar_compute();
+            epilogue(k - 1);
+        }
         if (!do1) break;
         // ---- ranges of all pixel groups -> centre and per-dim scale of line k
         const bool bad_mine = quad_live && !(isfinite(mn.x) && isfinite(mn.y) && isfinite(mn.z) && isfinite(mn.w) &&
@@ -416,7 +441,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     if (warp == 0) tc::tmem_free<512>(tmem);
 }
 
-constexpr size_t kStaticSmem = 17 * 1024;  // static shared arrays of the kernel (ptxas: 16.0 KB)
+constexpr size_t kStaticSmem = 19 * 1024;  // static shared arrays of the kernel (ptxas: 18.0 KB)
 
 size_t i8_tri_extra(const Geometry& g) {  // S staging beyond the plane buffers it aliases when it fits
     const size_t tri = size_t(g.D) * (g.D + 1) / 2 * 8;

@@ -56,6 +56,15 @@ class IoError(Error):
     kind = 6
 
 
+class FormatError(DataError):
+    """Malformed or truncated file (errors.hpp:67-75): kind data, with the file and byte offset."""
+
+    def __init__(self, path: str, offset: int, msg: str):
+        super().__init__(f"{msg} (file '{path}', offset {offset})")
+        self.path = path
+        self.offset = offset
+
+
 class DeviceError(Error):
     """CUDA failure inside the engine (no reference analogue)."""
     kind = 16
@@ -300,12 +309,6 @@ class Engine:
         self._lib.erx_kernel_times(self._h, _p(ms, C.c_double), _p(n, C.c_uint64))
         return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(L.KERNEL_NAMES)}
 
-    def probe_fp32_tflops(self):
-        """(register-form, constant-form) measured FFMA TFLOP/s of this device."""
-        r, c = C.c_double(0), C.c_double(0)
-        self._check(self._lib.erx_probe_fp32_tflops(self._h, C.byref(r), C.byref(c)))
-        return float(r.value), float(c.value)
-
     def event_record(self, slot: int):
         self._check(self._lib.erx_event_record(self._h, slot))
 
@@ -403,6 +406,15 @@ def gen_lines(spec, first: int, n: int, threads: int = 0, want_mask: bool = True
     if st:
         raise ConfigError("bad generator spec")
     return out, mask
+
+
+def gen_scene_changes(spec):
+    """The stream's scene-change lines as the generator drew them (sorted)."""
+    out = (C.c_int64 * 4)()
+    n = L.lib().erx_gen_scene_changes(C.byref(spec), out)
+    if n < 0:
+        raise ConfigError("bad generator spec")
+    return [int(out[i]) for i in range(n)]
 
 
 def gen_lines_device(spec, first: int, n: int, out=None, mask=None, want_mask: bool = True, stream: int = 0):

@@ -1,17 +1,26 @@
 """HADC cube / mask files ([MODULE] io) over
 the C ABI (csrc/hadc.cpp): read_cube / write_cube / read_mask / write_mask
 with the reference's validation (bad magic, truncated payload, zero sizes,
-unsupported dtype, mask values other than 0/1 -> IoError carrying the byte
-offset), plus a reader that streams line ranges into host memory or, through
+unsupported dtype, mask values other than 0/1 -> FormatError, kind data,
+carrying the file and byte offset; failing to open / read -> IoError), plus a reader that streams line ranges into host memory or, through
 pinned double-buffered staging, straight into device memory for the engine.
 """
 import ctypes as C
+import re
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _lib as L
-from .detector import _raise
+from .detector import FormatError, _raise
+
+
+def _fail(st: int, msg: str, path: str):
+    """ERX_ERR_DATA from the reader is had::FormatError (errors.hpp:67-75): path + byte offset."""
+    if st == L.ERX_ERR_DATA:
+        m = re.search(r"at offset (\d+)", msg)
+        raise FormatError(str(path), int(m.group(1)) if m else -1, msg)
+    _raise(st, msg)
 
 DTYPE_F32 = 1
 DTYPE_U8 = 2
@@ -34,15 +43,16 @@ class HadcReader:
     def __init__(self, path: str):
         self._h = C.c_void_p()
         info = L.HadcInfoC()
+        self.path = str(path)
         st = L.lib().erx_hadc_open(str(path).encode(), C.byref(self._h), C.byref(info))
         if st:
-            _raise(st, L.lib().erx_hadc_last_error(None).decode(errors="replace"))
+            _fail(st, L.lib().erx_hadc_last_error(None).decode(errors="replace"), self.path)
         self.header = CubeHeader(info.version, info.lines, info.pixels, info.bands, info.dtype, info.layout,
                                  info.name.decode("utf-8", errors="replace"))
 
     def _check(self, st):
         if st:
-            _raise(st, L.lib().erx_hadc_last_error(self._h).decode(errors="replace"))
+            _fail(st, L.lib().erx_hadc_last_error(self._h).decode(errors="replace"), self.path)
 
     @property
     def np_dtype(self):
@@ -112,12 +122,12 @@ def write_mask(path: str, mask: np.ndarray, name: str = ""):
 def read_cube(path: str):
     with HadcReader(path) as r:
         if r.header.dtype != DTYPE_F32:
-            _raise(L.ERX_ERR_IO, f"{path}: not a cube (dtype {r.header.dtype}) at offset 18")
+            raise FormatError(str(path), 18, f"{path}: not a cube (dtype {r.header.dtype})")
         return r.header, r.read()
 
 
 def read_mask(path: str):
     with HadcReader(path) as r:
         if r.header.dtype != DTYPE_U8 or r.header.bands != 1:
-            _raise(L.ERX_ERR_IO, f"{path}: not a mask (dtype {r.header.dtype}, bands {r.header.bands}) at offset 14")
+            raise FormatError(str(path), 14, f"{path}: not a mask (dtype {r.header.dtype}, bands {r.header.bands})")
         return r.header, r.read()[:, :, 0]

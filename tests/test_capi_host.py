@@ -48,6 +48,31 @@ def test_exports_every_declared_symbol(pkg):
     assert isinstance(lib, ctypes.CDLL)
 
 
+def test_probe_library_exports_its_header(pkg):
+    """Design probes and tcgen05 self-tests live in liberx_probe.so (include/erx_probe.h), not in
+    the product library."""
+    from paper_2408_14947_b200 import probe
+
+    src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "erx_probe.h")).read(), flags=re.S)
+    names = {m.group(1) for m in re.finditer(r"\b(erx_[a-z0-9_]+)\s*\(", src)}
+    assert names == set(probe.SIGNATURES)
+    lib = probe.lib()
+    assert all(hasattr(lib, n) for n in names)
+    assert not any(hasattr(pkg.lib(), n) for n in names)
+
+
+def test_oracle_generator_is_bitwise_the_product_generator(pkg, oracle):
+    """The CPU baseline / reference arm generates its inputs with the oracle library's own copy of
+    the seeded generator (no product .so mapped): same bits as erx_gen_lines."""
+    for cid, s in ((0, 0), (1, 0), (2, 0), (3, 17), (4, 2)):
+        a, ma = oracle.gen_lines(oracle.gen_spec(cid, s), 5, 3, threads=2)
+        b, mb = pkg.gen_lines(pkg.gen_spec(cid, s), 5, 3, threads=2)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)) and np.array_equal(ma, mb), (cid, s)
+        assert oracle.gen_scene_changes(oracle.gen_spec(cid, s)) == pkg.gen_scene_changes(pkg.gen_spec(cid, s))
+    assert pkg.gen_scene_changes(pkg.gen_spec(1, 0)) == [5000]
+    assert len(pkg.gen_scene_changes(pkg.gen_spec(4, 3))) == 2
+
+
 def test_config_validation(pkg):  # erx.hpp:23, SPEC.md:262
     pkg.ErxConfig().validate(108)
     for kw in [dict(alpha=0.0), dict(alpha=1.01), dict(epsilon=0.0), dict(dims=0), dict(dims=109)]:

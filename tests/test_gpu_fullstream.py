@@ -1,0 +1,128 @@
+"""Full-length parity: whole BASELINE streams on the GPU against the fp64 oracle.
+
+The oracle ran once over the same streams on the build host
+(tests/golden/make_full_fixtures.py -> tests/golden/full_<case>.npz); the GPU
+side regenerates the identical inputs on the device (erx_gen_lines_device,
+bit-identical to the host generator) and scores them in the BENCHMARK's own
+geometry:
+
+  c3_dB / c3_d5   configs[3]: all 64 streams x 5,000 lines, window T = 32
+                  (bench.py's 2,048 lines per launch); streams {0, 31, 63} compared
+  c1_dB / c1_d5   configs[1]: 10,000 lines, window 256, the real line-5,000 scene change
+  c4_dB / c4_d5   configs[4]: all 4 streams x 3,000 lines, window 32, each stream's two
+                  drawn scene changes; stream 0 compared
+
+Gates (BASELINE.json north_star), over the whole stream(s):
+  * raw delta on the sampled lines (every 100th line + the lines after each
+    scene change): max relative error <= 1e-3, median <= 1e-5; norm within
+    1e-3 * max(1, |norm|);
+  * top-1% set of the pooled non-warmup norm scores: identical except for
+    oracle scores within 1e-3 * max(1, |cut|) of the cut (ties);
+  * AUC of the pooled non-warmup norm scores vs the injected labels: equal to 3 decimals.
+Per-case numbers are appended as JSON lines to $ERX_PARITY_LOG when it is set
+(the round's parity table, profiles/)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CASES = ["c3_dB", "c3_d5", "c1_dB", "c1_d5", "c4_dB", "c4_d5"]
+
+
+def load(case):
+    f = np.load(os.path.join(HERE, "golden", f"full_{case}.npz"))
+    meta = json.loads(str(f["meta"]))
+    return f, meta
+
+
+def run_case(pkg, case):
+    import torch
+
+    f, meta = load(case)
+    cid, n, T = meta["config"], meta["lines"], meta["window"]
+    S_all = {3: 64, 1: 1, 4: 4}[cid]
+    cmp_streams = meta["streams"]
+    specs = [pkg.gen_spec(cid, s) for s in range(S_all)]
+    P, B = specs[0].pixels, specs[0].bands
+    buf = meta["buffer_len"]
+    cfg = pkg.ErxConfig(no_srp=meta["no_srp"], alpha=meta["alpha"], buffer_len=buf)
+    eng = pkg.Engine(cfg, B, n_streams=S_all, window_lines=T)
+    samp = f["samp_lines"]
+    where = {int(t): i for i, t in enumerate(samp)}
+    C = len(cmp_streams)
+    raw_s = np.zeros((C, samp.size, P), np.float32)
+    norm_s = np.zeros((C, samp.size, P), np.float32)
+    pooled = np.zeros((C, n - buf, P), np.float32)
+    labels = np.zeros((C, n - buf, P), np.uint8)
+    x_full = torch.empty((S_all, T, P, B), dtype=torch.float32, device="cuda")
+    m_full = torch.empty((C, T, P), dtype=torch.uint8, device="cuda")
+    raw = torch.empty((S_all, T, P), dtype=torch.float32, device="cuda")
+    norm = torch.empty_like(raw)
+    for w0 in range(0, n, T):
+        m = min(T, n - w0)
+        x = x_full if m == T else torch.empty((S_all, m, P, B), dtype=torch.float32, device="cuda")
+        for s in range(S_all):
+            ci = cmp_streams.index(s) if s in cmp_streams else -1
+            pkg.gen_lines_device(specs[s], w0, m, out=x[s], mask=m_full[ci, :m] if ci >= 0 else None,
+                                 want_mask=ci >= 0)
+        r = raw[:, :m] if m == T else torch.empty((S_all, m, P), dtype=torch.float32, device="cuda")
+        nn = norm[:, :m] if m == T else torch.empty_like(r)
+        torch.cuda.synchronize()
+        eng.run_device(x.data_ptr(), m, P, r.data_ptr(), nn.data_ptr(), first_index=w0)
+        eng.sync()
+        rh = r[cmp_streams].cpu().numpy()
+        nh = nn[cmp_streams].cpu().numpy()
+        mh = m_full[:, :m].cpu().numpy()
+        for u in range(m):
+            t = w0 + u
+            if t in where:
+                raw_s[:, where[t]] = rh[:, u]
+                norm_s[:, where[t]] = nh[:, u]
+            if t >= buf:
+                pooled[:, t - buf] = nh[:, u]
+                labels[:, t - buf] = mh[:, u]
+    eng.close()
+    return f, meta, raw_s, norm_s, pooled.ravel(), labels.ravel()
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_full_stream_parity(case, oracle):
+    import paper_2408_14947_b200 as pkg
+
+    f, meta, raw_s, norm_s, pooled, labels = run_case(pkg, case)
+    raw_o = f["raw"].astype(np.float64)
+    norm_o = f["norm"].astype(np.float64)
+    rel = np.abs(raw_s - raw_o) / np.maximum(np.abs(raw_o), 1e-30)
+    nerr = np.abs(norm_s - norm_o) / np.maximum(1.0, np.abs(norm_o))
+    k = int(f["k"])
+    top_idx, top_val = f["top_idx"].astype(np.int64), f["top_val"].astype(np.float64)
+    cut = top_val[k - 1]
+    band = 1e-3 * max(1.0, abs(cut))
+    gpu_top = np.argpartition(-pooled, k - 1)[:k]
+    o_top = top_idx[:k]
+    o_val = dict(zip(top_idx.tolist(), top_val.tolist()))
+    only_o = np.setdiff1d(o_top, gpu_top)
+    only_g = np.setdiff1d(gpu_top, o_top)
+    bad = [i for i in only_o.tolist() if abs(o_val[i] - cut) > band]
+    bad += [i for i in only_g.tolist() if i not in o_val or abs(o_val[i] - cut) > band]
+    auc_g = oracle.roc_auc(pooled.astype(np.float64), labels)
+    auc_o = float(f["auc"])
+    res = {"case": case, "config": meta["config"], "streams": meta["streams"], "lines": meta["lines"],
+           "mode": "D=B" if meta["no_srp"] else "d=5", "window": meta["window"],
+           "raw_rel_max": float(rel.max()), "raw_rel_median": float(np.median(rel)),
+           "norm_err_max": float(nerr.max()), "sampled_lines": int(raw_s.shape[1]),
+           "pooled_scores": int(pooled.size), "top1pct_k": k, "top1pct_sym_diff": int(only_o.size + only_g.size),
+           "top1pct_beyond_ties": len(bad), "auc_gpu": auc_g, "auc_oracle": auc_o}
+    log = os.environ.get("ERX_PARITY_LOG")
+    if log:
+        with open(log, "a") as fh:
+            fh.write(json.dumps(res) + "\n")
+    print(json.dumps(res))
+    assert rel.max() <= 1e-3 and np.median(rel) <= 1e-5, res
+    assert nerr.max() <= 1e-3, res
+    assert not bad, res
+    assert round(auc_g, 3) == round(auc_o, 3), res

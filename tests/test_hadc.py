@@ -36,7 +36,7 @@ def test_cube_round_trip_bit_identical(tmp_path, hadc):
 
 
 def test_mask_round_trip_and_values(tmp_path, hadc):
-    from paper_2408_14947_b200 import DataError, IoError
+    from paper_2408_14947_b200 import DataError, FormatError
 
     m = (np.random.default_rng(1).random((4, 9)) < 0.3).astype(np.uint8)
     p = tmp_path / "m.hadc"
@@ -48,40 +48,45 @@ def test_mask_round_trip_and_values(tmp_path, hadc):
     raw = bytearray(p.read_bytes())
     raw[22 + 5] = 2  # mask value 2 on read -> validation error with its offset
     p.write_bytes(bytes(raw))
-    with pytest.raises(IoError, match="offset 27"):
+    with pytest.raises(FormatError, match="offset 27") as e:
         hadc.read_mask(p)
+    assert e.value.offset == 27 and isinstance(e.value, DataError) and e.value.exit_code() == 3
 
 
 def test_truncated_payload(tmp_path, hadc):
-    from paper_2408_14947_b200 import IoError
+    from paper_2408_14947_b200 import FormatError
 
     p = tmp_path / "t.hadc"
     hadc.write_cube(p, np.ones((3, 4, 2), np.float32))
     p.write_bytes(p.read_bytes()[:-1])
-    with pytest.raises(IoError, match="length mismatch at offset 22"):
+    with pytest.raises(FormatError, match="length mismatch at offset 22"):
         hadc.read_cube(p)
 
 
 def test_header_validation(tmp_path, hadc):
-    from paper_2408_14947_b200 import ConfigError, IoError
+    from paper_2408_14947_b200 import ConfigError, FormatError, IoError
 
     with pytest.raises(ConfigError):
         hadc.write_cube(tmp_path / "z.hadc", np.ones((0, 4, 2), np.float32))
     hdr = b"HADC" + struct.pack("<HIIIBBH", 1, 0, 4, 2, 1, 1, 0)
     (tmp_path / "l0.hadc").write_bytes(hdr)
-    with pytest.raises(IoError, match="lines = 0 at offset 6"):
+    with pytest.raises(FormatError, match="lines = 0 at offset 6"):
         hadc.read_cube(tmp_path / "l0.hadc")
     (tmp_path / "mg.hadc").write_bytes(b"HADX" + hdr[4:])
-    with pytest.raises(IoError, match="bad magic at offset 0"):
+    with pytest.raises(FormatError, match="bad magic at offset 0"):
         hadc.read_cube(tmp_path / "mg.hadc")
     (tmp_path / "dt.hadc").write_bytes(b"HADC" + struct.pack("<HIIIBBH", 1, 1, 1, 1, 7, 1, 0) + b"\0")
-    with pytest.raises(IoError, match="unsupported dtype at offset 18"):
+    with pytest.raises(FormatError, match="unsupported dtype at offset 18"):
         hadc.read_cube(tmp_path / "dt.hadc")
     (tmp_path / "v.hadc").write_bytes(b"HADC" + struct.pack("<HIIIBBH", 2, 1, 1, 1, 1, 1, 0) + b"\0" * 4)
-    with pytest.raises(IoError, match="unsupported version at offset 4"):
+    with pytest.raises(FormatError, match="unsupported version at offset 4"):
         hadc.read_cube(tmp_path / "v.hadc")
     with pytest.raises(IoError, match="cannot open"):
         hadc.read_cube(tmp_path / "missing.hadc")
+    # a header whose lines x pixels x bands x 4 wraps 64 bits is rejected, not read
+    (tmp_path / "ov.hadc").write_bytes(b"HADC" + struct.pack("<HIIIBBH", 1, 0xFFFFFFFF, 0xFFFFFFFF, 0xFFFFFFFF, 1, 1, 0))
+    with pytest.raises(FormatError, match="overflows at offset 6"):
+        hadc.read_cube(tmp_path / "ov.hadc")
 
 
 def test_line_ranges(tmp_path, hadc):

@@ -8,9 +8,8 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import paper_2408_14947_b200 as pkg
+from paper_2408_14947_b200 import probe  # noqa: E402
 
-eng = pkg.Engine(pkg.ErxConfig(no_srp=True), 8)
 for K in (16, 64, 256):
     for lo, hi in ((0.5, 1.0), (-1.0, 1.0)):
         rng = np.random.default_rng(K)
@@ -20,8 +19,8 @@ for K in (16, 64, 256):
         da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
         for split in (1,):
             dd = torch.zeros((128, 128), dtype=torch.float32, device="cuda")
-            pkg.lib().erx_tc_selftest(eng._h, C.c_void_p(da.data_ptr()), C.c_void_p(db.data_ptr()), K, split,
-                                      C.c_void_p(dd.data_ptr()))
+            probe.lib().erx_tc_selftest(0, None, C.c_void_p(da.data_ptr()), C.c_void_p(db.data_ptr()), K, split,
+                                        C.c_void_p(dd.data_ptr()))
             d = dd.cpu().numpy().astype(np.float64)
             # fp32-rounded exact result for comparison
             rel = (d - ref) / np.abs(ref).max()
