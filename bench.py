@@ -13,8 +13,17 @@ L2 by the previous one.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config 3] [--mode full|srp] [--window T]
 
+`--gpus N` without a torchrun environment re-launches itself under
+`torch.distributed.run` with N ranks (one per GPU, NCCL, 127.0.0.1); each rank
+scores its shard of the streams, the device times are max-reduced and the
+per-stream results are gathered to rank 0 (the path's only collective).
+`--dry-run` runs the same rank / timing / gather logic with a CPU stub engine
+over gloo (tests/test_bench_ranks.py).
+
 `--impl reference` times the fp64 CPU restatement of the reference path
-(oracle/, "port": the reference ships declarations only) on the host cores.
+(oracle/, "port": the reference ships declarations only) on the host cores; it
+maps only the oracle library (which carries its own copy of the seeded
+generator), never a product library.
 """
 from __future__ import annotations
 
@@ -22,9 +31,9 @@ import argparse
 import json
 import math
 import os
+import socket
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -44,6 +53,60 @@ L2_BYTES = 126 * 1024 * 1024
 
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def workload(cid, mode, world, window=0):
+    """The benchmark workload of BASELINE.json configs[cid] at `world` ranks: (config dict shared by both
+    arms, streams per rank, window T).  The window (lag per stream) defaults to ~2048 lines per GPU
+    (T = 32 at N = 1, 256 at N = 8) so each GPU's launches stay full as the fixed streams spread out."""
+    cfgd = CONFIGS[cid]
+    S_tot = cfgd["streams"]
+    S = max(1, S_tot // world)
+    T = window if window else min(max(32, 2048 // S), cfgd["lines"] // 2)
+    no_srp = mode == "full"
+    config = {"workload": f"configs[{cid}]", "streams": S_tot, "streams_per_gpu": S, "pixels": cfgd["pixels"],
+              "bands": cfgd["bands"], "dims": cfgd["bands"] if no_srp else 5,
+              "mode": "D=B (no_srp)" if no_srp else "d=5 SRP", "alpha": cfgd["alpha"], "window_lines": T,
+              "lines_per_stream": cfgd["lines"],
+              "l2": "inputs larger than L2: device pool >= 2x L2, one window per step"}
+    return config, S, T
+
+
+def free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args):
+    """--gpus N outside torchrun: re-exec under torch.distributed.run with N ranks on this node."""
+    env = dict(os.environ)
+    if not args.dry_run:
+        env.setdefault("NCCL_DEBUG", "INFO")  # the communicator's rank count shows in the log
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+class StubEngine:
+    """--dry-run: the engine's step / timing surface on the CPU (a fixed per-line reduction), so the
+    rank, timing and gather logic of run_ours runs over gloo without a GPU."""
+
+    def __init__(self, S, T, P, B):
+        self.S, self.T, self.P = S, T, P
+        self.raw = np.zeros((S, T, P))
+        self.t = [0.0] * 8
+        self.launches = 0
+
+    def run_device(self, x, k):
+        self.raw = x.sum(axis=-1, dtype=np.float64) + k  # [S][T][P]
+        self.launches += 5
+
+    def event_record(self, slot):
+        self.t[slot] = time.perf_counter()
+
+    def event_elapsed_ms(self, a, b):
+        return (self.t[b] - self.t[a]) * 1e3
 
 
 NCU_SUMMARY = os.path.join(ROOT, "profiles", "r01_ncu_full_tensor.txt")
@@ -88,11 +151,14 @@ class ClockSampler:
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, enabled: bool = True):
         self.device = device
         self.proc = None
+        self.enabled = enabled
 
     def __enter__(self):
+        if not self.enabled:
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -143,6 +209,7 @@ def algorithmic(cfgd, D, srp_nnz=0):
         # scan: reads [c | s | S] and writes the pre-update (mu, K) per line, fp64
         "scan": dict(flops=0, bytes=8 * (2 * D + D * (D + 1) // 2) + 8 * (D + D * (D + 1) // 2)),
         "normalize": dict(flops=0, bytes=8 * P),
+        "fixup": dict(flops=0, bytes=0),  # fp64 rescue: no listed lines on the BASELINE configs
     }
 
 
@@ -156,74 +223,115 @@ def build_pool(pkg, cid, streams, lines_per_stream, threads=0):
 
 
 def run_ours(args):
-    import torch
-
-    import paper_2408_14947_b200 as pkg
-
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    dry = args.dry_run
+    if not dry:
+        import torch
+
+        import paper_2408_14947_b200 as pkg
+
+        torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if dry else "nccl")
     cid = args.config
     cfgd = CONFIGS[cid]
-    from paper_2408_14947_b200.sharding import max_over_ranks, shard_streams
+    from paper_2408_14947_b200.sharding import gather_stream_results, max_over_ranks, shard_streams
 
     S_tot = cfgd["streams"]
     if S_tot % world:
         raise SystemExit(f"{S_tot} streams do not shard evenly over {world} ranks")
-    if args.shard_of and world == 1:  # one rank's share of an N-GPU run, on this GPU (scaling evidence)
-        my_streams = list(shard_streams(S_tot, args.shard_of, 0))
-    else:
-        my_streams = list(shard_streams(S_tot, world, rank))
-    S = len(my_streams)
+    shard_n = args.shard_of if (args.shard_of and world == 1) else world  # --shard-of: one rank's share on 1 GPU
+    my_streams = list(shard_streams(S_tot, shard_n, 0 if shard_n != world else rank))
+    config, S, T = workload(cid, args.mode, shard_n, args.window)
+    assert S == len(my_streams)
     P, B = cfgd["pixels"], cfgd["bands"]
     no_srp = args.mode == "full"
-    cfg = pkg.ErxConfig(no_srp=no_srp, alpha=cfgd["alpha"])
-    # window (lag) per stream: the given one, else ~2048 lines per GPU per window (T = 32 at N = 1,
-    # 256 at N = 8), so each GPU's launches stay full as the fixed 64 streams spread over more GPUs
-    T = args.window if args.window else min(max(32, 2048 // S), cfgd["lines"] // 2)
     line_bytes = P * B * 4
-    n_win = max(2, math.ceil(2 * L2_BYTES / (S * T * line_bytes)))
-    pool_lines = n_win * T
-    t0 = time.time()
-    host = build_pool(pkg, cid, my_streams, pool_lines)
-    gen_s = time.time() - t0
-    dev = torch.from_numpy(host).to(f"cuda:{local}")
-    # windows laid out [win][S][T][P][B] so each step reads one contiguous block
-    dev = dev.view(S, n_win, T, P, B).permute(1, 0, 2, 3, 4).contiguous()
-    raw = torch.empty((S, T, P), dtype=torch.float32, device=f"cuda:{local}")
-    norm = torch.empty_like(raw)
-    eng = pkg.Engine(cfg, B, n_streams=S, window_lines=T, device=local)
-    eng.set_factor_precision(args.factor)
-    eng.set_stats_tensor(args.stats)
-    D = eng.dims
+    dev_str = "cpu" if dry else f"cuda:{local}"
+    if dry:  # a small CPU pool of the real generator's lines (the oracle library's copy of it)
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle_ctypes as orc
 
-    def step(k):
-        w = k % n_win
-        eng.run_device(dev[w].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr(), first_index=k * T)
+        n_win = 2
+        pool_lines = n_win * T
+        t0 = time.time()
+        host = build_pool(orc, cid, my_streams, pool_lines, threads=1)
+        gen_s = time.time() - t0
+        dev = host.reshape(S, n_win, T, P, B).transpose(1, 0, 2, 3, 4).copy()
+        eng = StubEngine(S, T, P, B)
+        D = B if no_srp else 5
+
+        def step(k):
+            eng.run_device(dev[k % n_win], k)
+    else:
+        n_win = max(2, math.ceil(2 * L2_BYTES / (S * T * line_bytes)))
+        pool_lines = n_win * T
+        t0 = time.time()
+        host = build_pool(pkg, cid, my_streams, pool_lines)
+        gen_s = time.time() - t0
+        dev = torch.from_numpy(host).to(dev_str)
+        # windows laid out [win][S][T][P][B] so each step reads one contiguous block
+        dev = dev.view(S, n_win, T, P, B).permute(1, 0, 2, 3, 4).contiguous()
+        raw = torch.empty((S, T, P), dtype=torch.float32, device=dev_str)
+        norm = torch.empty_like(raw)
+        cfg = pkg.ErxConfig(no_srp=no_srp, alpha=cfgd["alpha"])
+        eng = pkg.Engine(cfg, B, n_streams=S, window_lines=T, device=local)
+        eng.set_factor_precision(args.factor)
+        eng.set_stats_tensor(args.stats)
+        D = eng.dims
+
+        def step(k):
+            w = k % n_win
+            eng.run_device(dev[w].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr(), first_index=k * T)
+
+    def sync():
+        if not dry:
+            eng.sync()
+            torch.cuda.synchronize()
 
     for k in range(args.warmup):
         step(k)
-    eng.sync()
-    torch.cuda.synchronize()
+    sync()
     if dist:
         dist.barrier()
-    launches0 = eng.launch_count()
-    with ClockSampler(local) as clk:
+    launches0 = eng.launches if dry else eng.launch_count()
+    with ClockSampler(local, enabled=not dry) as clk:
         eng.event_record(0)
         for k in range(args.steps):
             step(args.warmup + k)
         eng.event_record(1)
         ms = eng.event_elapsed_ms(0, 1)
-    eng.sync()
-    launches = eng.launch_count() - launches0
-    torch.cuda.synchronize()
-    ms_max = max_over_ranks(ms, dist, device=f"cuda:{local}")
+    sync()
+    launches = (eng.launches if dry else eng.launch_count()) - launches0
+    ms_max = max_over_ranks(ms, dist, device=dev_str)
     lines_total = S * world * T * args.steps  # = S_tot * T * steps (one rank's share with --shard-of)
     value = lines_total / (ms_max / 1e3)
+    # the final gather (the path's only collective): per-stream results of the last window to every
+    # rank, checked complete on rank 0 (here the fp64 sum of each stream's raw scores)
+    last = eng.raw if dry else raw.double().sum(dim=(1, 2)).cpu().numpy()
+    local_res = {sid: np.array([float(np.sum(last[i]))]) for i, sid in enumerate(my_streams)}
+    if shard_n != world:  # --shard-of: the other ranks' shares are not run
+        gathered = {"streams": len(my_streams), "note": f"rank 0 share of {shard_n} only"}
+    else:
+        allres = gather_stream_results(local_res, S_tot, dist)
+        gathered = {"streams": len(allres), "checksum": float(sum(float(a[0]) for a in allres)),
+                    "via": ("all_gather_object over " + ("gloo" if dry else "NCCL")) if dist else "local"}
+    if dry:
+        if rank == 0:
+            line = {"metric": "lines/sec (batched independent streams, aggregate over GPUs)", "value": value,
+                    "unit": "lines/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                    "ms_per_step": ms_max / args.steps, "ms_per_rank_max": ms_max, "higher_is_better": True,
+                    "scaling": "strong", "vs_baseline": None, "dry_run": True, "config": config,
+                    "gather": gathered, "gpu_launches": 0, "gen_seconds": gen_s,
+                    "data": "synthetic: BASELINE.json generator; CPU stub engine (no kernels)"}
+            print(json.dumps(line), flush=True)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
 
     # per-kernel device time (CUDA events on the engine stream), separate pass
     eng.set_profiling(True)
@@ -241,8 +349,8 @@ def run_ours(args):
         lines_per_launch = S * T
         a = alg[name]
         kernels[name] = {"ms_per_launch": per, "share": kms / total_k, "launches": cnt,
-                         "tflops": a["flops"] * lines_per_launch / (per * 1e-3) / 1e12 if per > 0 else None,
-                         "gbs": a["bytes"] * lines_per_launch / (per * 1e-3) / 1e9 if per > 0 else None}
+                         "tflops": a["flops"] * lines_per_launch / (per * 1e-3) / 1e12 if per > 0 and a["flops"] else None,
+                         "gbs": a["bytes"] * lines_per_launch / (per * 1e-3) / 1e9 if per > 0 and a["bytes"] else None}
     dom = max(kernels, key=lambda k: kernels[k]["share"])
     from paper_2408_14947_b200 import probe
 
@@ -327,9 +435,16 @@ def run_ours(args):
             dist.all_reduce(el_t, op=dist.ReduceOp.MAX)
         e2e = {"value": S * world * T * e2e_steps / float(el_t.item()), "unit": "lines/s",
                "h2d_bytes_per_step": S * T * P * B * 4, "d2h_bytes_per_step": S * T * (P * 4 * 2 + 4),
-               "path": "erx_push_host (pinned) -> 5 kernels -> erx_pop (fp64 ScoredLine payload)",
+               "path": "erx_push_host (pinned) -> 6 kernels -> erx_pop (fp64 ScoredLine payload)",
                "pipelined": not args.sync_host}
         eng2.close()
+        # the e2e path's own bound: the line's bytes over the measured pinned host->device bandwidth
+        pc = pcie_bandwidth(local)
+        e2e["pcie"] = pc
+        if pc.get("h2d_gbs"):
+            bound = pc["h2d_gbs"] * 1e9 / (P * B * 4)  # lines/s per GPU the H2D copy alone allows
+            e2e["pcie_bound_lines_per_s"] = bound * world
+            e2e["frac_of_pcie_bound"] = e2e["value"] / (bound * world)
     except Exception as ex:  # report, never hide
         e2e = {"error": repr(ex)}
 
@@ -347,14 +462,12 @@ def run_ours(args):
             "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": ("f32 input; stats+score exact int8-digit tcgen05 (s32 TMEM), f32 factor, f64 scan/state"
                       if tensor else "f32 (FFMA stats/whitening) + f64 (scan, Cholesky, inverse)"),
-            "data": "synthetic: BASELINE.json configs[3] generator (include/erx_datagen.h), device pool >= 2x L2 replayed",
-            "config": {"workload": f"configs[{cid}]" + (f", rank 0 share of {args.shard_of} GPUs" if args.shard_of
-                                                       and world == 1 else ""),
-                       "streams": S * world, "streams_per_gpu": S, "pixels": P,
-                       "bands": B, "dims": D, "mode": "D=B (no_srp)" if no_srp else "d=5 SRP",
-                       "alpha": cfgd["alpha"], "window_lines": T, "pool_lines_per_stream": pool_lines,
-                       "factor_precision": eng.factor_precision(),
-                       "l2": "inputs larger than L2: device pool >= 2x L2, one window per step"},
+            "data": f"synthetic: BASELINE.json configs[{cid}] generator (include/erx_datagen.h), device pool >= 2x L2 replayed",
+            "config": config,
+            "engine": {"factor_precision": eng.factor_precision(), "stats_kernel": "tcgen05 kind::i8" if tensor
+                       else "FFMA", "pool_lines_per_stream": pool_lines, "dims": D,
+                       "shard": f"rank 0 share of {args.shard_of} GPUs" if shard_n != world else "own"},
+            "gather": gathered,
             "pixel_bands_per_s": value * P * B,
             "roofline": roof, "roofline_line": roofline_line, "kernels": kernels,
             "e2e": e2e, "clocks": clk.summary(), "gpu_launches": int(launches),
@@ -455,6 +568,10 @@ def secondary_measurements(pkg, args):
     except Exception as ex:
         out["latency"] = {"error": repr(ex)}
     try:
+        out["dropin_single_stream"] = dropin_measurement()
+    except Exception as ex:
+        out["dropin_single_stream"] = {"error": repr(ex)}
+    try:
         out["metrics"] = metrics_measurement(pkg)
     except Exception as ex:
         out["metrics"] = {"error": repr(ex)}
@@ -463,6 +580,21 @@ def secondary_measurements(pkg, args):
     except Exception as ex:
         out["datagen"] = {"error": repr(ex)}
     return out
+
+
+def dropin_measurement(lines=2000):
+    """The drop-in single-stream e2e number: configs[0] through the C++ had::ErxDetector::process
+    (include/hadkit/erx.hpp -> C ABI) one host line per call, wall clock from the first line fed to
+    the last ScoredLine (tools/dropin_bench.cpp), at lag 32 and lag 0."""
+    import tempfile
+
+    lib = os.path.join(ROOT, "paper_2408_14947_b200")
+    exe = os.path.join(tempfile.mkdtemp(), "dropin_bench")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tools", "dropin_bench.cpp"), "-L", lib, "-l:liberx_b200.so",
+                    f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    out = subprocess.run([exe, str(lines)], check=True, capture_output=True, text=True, timeout=600).stdout
+    return json.loads(out.strip().splitlines()[-1])
 
 
 def datagen_measurement(pkg):
@@ -570,11 +702,15 @@ def cpu_baseline(cid, no_srp, seconds=12.0, threads=None):
 
 
 def run_reference(args):
+    """The reference path on the host cores: the fp64 C++ restatement (oracle/erx_oracle.cpp, the
+    reference ships declarations only) through its own C API, all host threads, one stream per thread;
+    each step a bounded sample of the same workload.  Maps the oracle library only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     cid = args.config
     no_srp = args.mode == "full"
+    config, _, _ = workload(cid, args.mode, world, args.window)
     samples = []
     cores = os.cpu_count() or 1
     last = None
@@ -584,21 +720,59 @@ def run_reference(args):
             samples.append(r["value"])
         last = r
     value = float(np.mean(samples))
-    cfgd = CONFIGS[cid]
     line = {
         "impl": "reference", "metric": "lines/sec (batched independent streams, aggregate over GPUs)",
         "value": value, "unit": "lines/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: BASELINE.json configs generator",
-        "config": {"workload": f"configs[{cid}]", "streams": cfgd["streams"], "pixels": cfgd["pixels"],
-                   "bands": cfgd["bands"], "mode": "D=B (no_srp)" if no_srp else "d=5 SRP"},
+        "data": f"synthetic: BASELINE.json configs[{cid}] generator (the oracle library's copy)",
+        "config": config,
         "cpu_baseline": {"value": value, "unit": "lines/s", "cores": last["cores"], "kind": "port",
-                         "sample": last["sample"]},
+                         "sample": last["sample"], "cpu_model": last.get("cpu_model")},
         "e2e": {"value": value, "unit": "lines/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference ships headers only (no bodies, no Eigen); timed path is the fp64 C++ restatement "
-                "oracle/erx_oracle.cpp through its own C API",
+                "oracle/erx_oracle.cpp through its own C API (naive scalar fp64, one stream per host thread)",
+        "libraries_mapped": mapped_libraries(),
     }
     print(json.dumps(line), flush=True)
+
+
+def mapped_libraries():
+    """This repository's shared libraries mapped into the process (/proc/self/maps)."""
+    out = set()
+    try:
+        for l in open("/proc/self/maps"):
+            path = l.split()[-1]
+            if path.startswith(ROOT) and ".so" in path:
+                out.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(out)
+
+
+def pcie_bandwidth(device, nbytes=256 << 20):
+    """Pinned host <-> device copy bandwidth (GB/s, best of 5) on this GPU: the e2e path's own peak."""
+    import torch
+
+    try:
+        h = torch.empty(nbytes // 4, dtype=torch.float32).pin_memory()
+        d = torch.empty(nbytes // 4, dtype=torch.float32, device=f"cuda:{device}")
+        st = torch.cuda.current_stream(device)
+        res = {}
+        for name, fn in (("h2d_gbs", lambda: d.copy_(h, non_blocking=True)),
+                         ("d2h_gbs", lambda: h.copy_(d, non_blocking=True))):
+            best = 0.0
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                fn()
+                e1.record(st)
+                e1.synchronize()
+                best = max(best, nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9)
+            res[name] = best
+        res["bytes"] = nbytes
+        return res
+    except Exception as ex:
+        return {"error": repr(ex)}
 
 
 def main():
@@ -621,7 +795,10 @@ def main():
     ap.add_argument("--shard-of", type=int, default=0,
                     help="N=1 only: run rank 0's stream share of an N-GPU job (value is per GPU)")
     ap.add_argument("--sync-host", action="store_true", help="e2e without ERX_OPT_ASYNC_HOST (push waits for scores)")
+    ap.add_argument("--dry-run", action="store_true", help="CPU stub engine over gloo: rank / timing / gather logic only")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liberx_b200.so")
+LIB_PATH = os.environ.get("ERX_B200_LIB", os.path.join(_HERE, "liberx_b200.so"))  # override: A/B builds
 
 ERX_OK = 0
 ERX_ERR_CONFIG = 2

@@ -85,6 +85,7 @@ struct erx_engine {
     float* d_vcache = nullptr;  // [S*T][D][P] centred projections (small path)
     float* d_vmax = nullptr;    // [S*T][D] per-dim |x - c| range (tensor path)
     unsigned char* d_vplanes = nullptr;  // [S*T][tiles][48 KB] quantised v digit planes (tensor path)
+    int* d_c0 = nullptr;        // [S*T][4][D] class-0 diagonal partials of the integer statistics (tensor path)
     float* d_kblk = nullptr;    // [S*T][nb(nb+1)/2][64] pre-update K as fp32 blocks (blocked fp32 factor)
     int factor_req = 0;   // requested factor precision (0 auto, 32, 64)
     // ERX_OPT_STATS_TENSOR: 2 exact-integer tcgen05 stats + score where eligible (default), 0 FFMA kernels.
@@ -229,6 +230,8 @@ void free_window(erx_engine* e) {
     e->d_vmax = nullptr;
     cudaFree(e->d_vplanes);
     e->d_vplanes = nullptr;
+    cudaFree(e->d_c0);
+    e->d_c0 = nullptr;
     cudaFree(e->d_kblk);
     e->d_kblk = nullptr;
     cudaFree(e->d_fix);
@@ -296,6 +299,7 @@ int configure(erx_engine* e, uint32_t P) {
     if (e->small) CU(cudaMalloc(&e->d_vcache, L * size_t(g.D) * P * sizeof(float)));
     if (erxk::stats_i8_eligible(g)) CU(cudaMalloc(&e->d_vmax, L * size_t(g.D) * sizeof(float)));
     if (e->tensor) CU(cudaMalloc(&e->d_vplanes, L * erxk::vplanes_bytes_per_line(g)));
+    if (e->tensor) CU(cudaMalloc(&e->d_c0, L * 4 * size_t(g.D) * sizeof(int)));
     if (e->factor_prec == 32) CU(cudaMalloc(&e->d_kblk, L * erxk::whiten_floats_per_line(g) * sizeof(float)));
     // fp64 rescue list (fed by the fp32 factors and by the normalisation's flat-line check)
     CU(cudaMalloc(&e->d_fix, (L + 2) * sizeof(int)));
@@ -370,6 +374,7 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     float* vmax = e->d_vmax ? e->d_vmax + l0 * size_t(g.D) : nullptr;
     unsigned char* vplanes = e->d_vplanes ? e->d_vplanes + l0 * erxk::vplanes_bytes_per_line(g) : nullptr;
     float* kblk = e->d_kblk ? e->d_kblk + l0 * erxk::whiten_floats_per_line(g) : nullptr;
+    int* c0 = (e->tensor && e->d_c0) ? e->d_c0 + l0 * 4 * size_t(g.D) : nullptr;
     const bool tensor = e->tensor;
     int* status = e->d_status + l0;
     float* rawg = raw ? raw + l0 * g.P : nullptr;
@@ -378,7 +383,7 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
         if (e->small)
             erxk::launch_stats_small(g, e->smp, xg, int(n), int(in_stride), L, stats, vcache, e->stream);
         else if (tensor)
-            erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, vmax, vplanes, e->stream);
+            erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, vmax, vplanes, c0, e->stream);
         else
             erxk::launch_stats(g, e->sl, xg, int(n), int(in_stride), L, stats, e->stream);
     });

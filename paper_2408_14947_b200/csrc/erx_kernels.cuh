@@ -97,8 +97,10 @@ size_t factor_smem(const Geometry& g, int precision);
 bool stats_i8_eligible(const Geometry& g);
 // vmax / vplanes (may be null): [line][D] max_p |fl32(x - c)| and the score's v digit planes
 // (vplanes_bytes_per_line per line).
+// c0: [line][4][D] int32 scratch for the class-0 diagonal partials (folded into S_aa by a second,
+// tiny kernel of this launcher).
 void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
-                     double* stats, float* vmax, unsigned char* vplanes, cudaStream_t st);
+                     double* stats, float* vmax, unsigned char* vplanes, int* c0, cudaStream_t st);
 // Exact-integer tcgen05 score kernel (k_score_i8.cu): v planes from stats_i8, W planes from the factor.
 bool score_i8_eligible(const Geometry& g);
 size_t wplanes_bytes_per_line();

@@ -67,6 +67,7 @@ struct StatsI8Args {
     double* stats;
     float* vmax;  // [line][D] max_p |fl32(x - c)| (the score kernel's y range), may be null
     unsigned char* vplanes;  // [line][tile][3][i8::kTileBytes / 3]: v digit planes for k_score_i8, may be null
+    int* c0;     // [line][4][D] class-0 diagonal partials sum_p d0^2 (q units), per pixel group
     int N;       // MMA N = roundup16(D + 1)
     int stages;  // ring depth
 };
@@ -106,12 +107,12 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     __shared__ __align__(8) uint64_t pfull[2], pempty[2], accfull, accempty;
     __shared__ __align__(16) float red_mn[8][128];
     __shared__ __align__(16) float red_mx[8][128];
+
     __shared__ double red_cs[4][128];
     __shared__ float cen_s[128], scale_s[128], add_s[128];
     __shared__ double inv_s[128];
     __shared__ double sum_s[128];
     __shared__ int bad_s[8];
-    __shared__ int c0_s[4][128];  // per pixel group: sum_p d0^2 of each dim (the class-0 diagonal)
 
     const Geometry& g = a.g;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -238,9 +239,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                                            (static_cast<long long>(int(v[1][ii])) << 16) +
                                            (static_cast<long long>(int(v[0][ii])) << 8);
                     const double si = double(si_i);  // (the ones column: no class-0 term)
-                    const long long c0 = (e == row) ? (long long)(c0_s[0][row]) + c0_s[1][row] + c0_s[2][row] + c0_s[3][row]
-                                                    : 0ll;
-                    if (e <= row) S[tri(row, e)] = double(si_i + c0) * ia * inv_s[e];
+                    if (e <= row) S[tri(row, e)] = si * ia * inv_s[e];
                     if (e == D) sum_s[row] = si * (1.0 / 256.0) * ia;
                 }
             }
@@ -263,8 +262,10 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     float cdk[2] = {0.f, 0.f}, sdk[2] = {0.f, 0.f}, adk[2] = {kMagic, kMagic};
     // class-0 products (d0 d0, weight 1) are not accumulated by the MMAs; on the diagonal they are a
     // systematic + sum_p d0^2 (~P 2^14 / 3 in q^2 units), which biases K's small eigenvalues when the
-    // background is ill-conditioned, so the quantiser sums them exactly here (off the diagonal they
-    // are zero-mean and stay dropped: 2^-30 relative)
+    // background is ill-conditioned, so the quantiser sums them exactly here (one dp4a per 4 digits)
+    // and leaves the four pixel-group partials per dim in c0 [line][4][D]; c0_fold_kernel adds them to
+    // the diagonal of the stats slot.  Off the diagonal they are zero-mean and stay dropped (2^-30
+    // relative).
     int c0a = 0, c0b = 0;
     int j = 0;  // position in the chunk sequence (as the producer's)
     for (int k = 0; k <= my_lines; ++k) {
@@ -333,14 +334,11 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                             u0[e] = __float_as_uint(fmaf(xp[ld0] - cdk[0], sdk[0], adk[0])) + (0x808080u - 0x4B400000u);
                             u1[e] = __float_as_uint(fmaf(xp[ld1] - cdk[1], sdk[1], adk[1])) + (0x808080u - 0x4B400000u);
                         }
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int d0a = int(u0[e] & 0xffu) - 128, d0b = int(u1[e] & 0xffu) - 128;
-                            c0a += d0a * d0a;
-                            c0b += d0b * d0b;
-                        }
                         pack_digits(u0, w[0][0][jj], w[0][1][jj], w[0][2][jj]);
                         pack_digits(u1, w[1][0][jj], w[1][1][jj], w[1][2][jj]);
+                        // d0 plane words hold 4 signed digits: one dp4a sums their squares
+                        c0a = __dp4a(int(w[0][0][jj]), int(w[0][0][jj]), c0a);
+                        c0b = __dp4a(int(w[1][0][jj]), int(w[1][0][jj]), c0b);
                     }
                 } else {
 #pragma unroll
@@ -353,12 +351,11 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                             u0[e] = __float_as_uint(fmaf(xp[ld0] - cdk[0], sdk[0], adk[0])) + (0x808080u - 0x4B400000u);
                             u1[e] = __float_as_uint(fmaf(xp[ld1] - cdk[1], sdk[1], adk[1])) + (0x808080u - 0x4B400000u);
                             if (p >= n) u0[e] = u1[e] = 0x808080u;
-                            const int d0a = int(u0[e] & 0xffu) - 128, d0b = int(u1[e] & 0xffu) - 128;
-                            c0a += d0a * d0a;
-                            c0b += d0b * d0b;
                         }
                         pack_digits(u0, w[0][0][jj], w[0][1][jj], w[0][2][jj]);
                         pack_digits(u1, w[1][0][jj], w[1][1][jj], w[1][2][jj]);
+                        c0a = __dp4a(int(w[0][0][jj]), int(w[0][0][jj]), c0a);
+                        c0b = __dp4a(int(w[1][0][jj]), int(w[1][0][jj]), c0b);
                     }
                 }
                 const uint32_t off0 = tc::kmajor_off_s8(dd0, pg2 * 16), off1 = tc::kmajor_off_s8(dd1, pg2 * 16);
@@ -372,6 +369,12 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                 if (lane == 0) {
                     mbar_arrive(&empty[st]);
                     mbar_arrive(&pfull[buf]);
+                }
+                if (c == nch - 1) {  // the line's class-0 diagonal partials (consumed by the scan)
+                    int* c0l = a.c0 + size_t(blockIdx.x + (k - 1) * gridDim.x) * 4 * D + pg2 * D;
+                    if (dd0 < D) c0l[dd0] = c0a;
+                    if (dd1 < D) c0l[dd1] = c0b;
+                    c0a = c0b = 0;
                 }
                 if (a.vplanes) {
                     // the same digits, as the score kernel's MN-major A operand (i8::vplane_off): one warp
@@ -395,10 +398,6 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
         }
         // ---- line k-1 is complete: its epilogue (reads bad_s / cen_s / inv_s / c0_s of line k-1)
         if (do2) {
-            c0_s[pg2][dd0] = c0a;
-            c0_s[pg2][dd1] = c0b;
-            c0a = c0b = 0;
-            bar_compute();
             epilogue(k - 1);
         }
         if (!do1) break;
@@ -441,7 +440,22 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     if (warp == 0) tc::tmem_free<512>(tmem);
 }
 
-constexpr size_t kStaticSmem = 19 * 1024;  // static shared arrays of the kernel (ptxas: 18.0 KB)
+// S_aa += sum_p d0_a^2 / s_a^2 for every (line, dim): the class-0 diagonal the MMAs leave out, from the
+// quantiser's four pixel-group partials (exact int32 sums), scaled exactly as the epilogue scales S.
+__global__ void __launch_bounds__(256) c0_fold_kernel(int D, int SS, int n_lines, const int* __restrict__ c0,
+                                                      const float* __restrict__ vmax, double* __restrict__ stats) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_lines * D) return;
+    const int line = i / D, a = i - line * D;
+    const float s = i8::v_scale(vmax[i]);
+    if (!(s > 0.f)) return;
+    const int* p = c0 + size_t(line) * 4 * D + a;
+    const long long q = (long long)(p[0]) + p[D] + p[2 * D] + p[3 * D];
+    const double inv = 1.0 / double(s);
+    stats[size_t(line) * SS + 2 * D + tri(a, a)] += double(q) * inv * inv;
+}
+
+constexpr size_t kStaticSmem = 17 * 1024;  // static shared arrays of the kernel (ptxas: 16.0 KB)
 
 size_t i8_tri_extra(const Geometry& g) {  // S staging beyond the plane buffers it aliases when it fits
     const size_t tri = size_t(g.D) * (g.D + 1) / 2 * 8;
@@ -467,17 +481,19 @@ bool stats_i8_eligible(const Geometry& g) {
 }
 
 void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
-                     double* stats, float* vmax, unsigned char* vplanes, cudaStream_t st) {
+                     double* stats, float* vmax, unsigned char* vplanes, int* c0, cudaStream_t st) {
     const int sms = sm_count();
     ensure_smem(stats_i8_kernel<0>, kSmemCap - kStaticSmem);
     ensure_smem(stats_i8_kernel<108>, kSmemCap - kStaticSmem);
-    StatsI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, vmax, vplanes, (g.D + 1 + 15) / 16 * 16,
+    StatsI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, vmax, vplanes, c0, (g.D + 1 + 15) / 16 * 16,
                   i8_stages(g)};
     const int grid = n_lines_total < sms ? n_lines_total : sms;
     if (g.B == 108)  // configs[0] / configs[3]
         stats_i8_kernel<108><<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
     else
         stats_i8_kernel<0><<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
+    const int items = n_lines_total * g.D;
+    c0_fold_kernel<<<(items + 255) / 256, 256, 0, st>>>(g.D, g.SE + g.D, n_lines_total, c0, vmax, stats);
 }
 
 }  // namespace erxk

@@ -1,15 +1,18 @@
 // Drop-in check: code written against the reference interface
-// (had::ErxDetector / had::LineDetector / had::SpectralLine / had::ScoredLine,
-// proj/include/hadkit/{erx,detector,cube}.hpp) compiled against
-// include/erx_b200/hadkit_b200.hpp and linked to liberx_b200.so.  Runs the
+// (had::ErxDetector / had::LineDetector / had::SpectralLine / had::ScoredLine and
+// the free functions of proj/include/hadkit/{erx,detector,cube,projection}.hpp),
+// including the reference's own include paths ("hadkit/erx.hpp"), compiled
+// against include/ and linked to liberx_b200.so.  Runs the
 // reference line-scan loop (SPEC.md:642-650 shape) on a generated cube and
 // prints one JSON summary line for tests/test_cpp_mirror.py.
 #include <cmath>
 #include <cstdio>
 #include <vector>
 
-#include "erx_b200/hadkit_b200.hpp"
 #include "erx_datagen.h"
+#include "hadkit/detector.hpp"
+#include "hadkit/erx.hpp"
+#include "hadkit/projection.hpp"
 
 static int run_loop(had::LineDetector& det, const std::vector<float>& cube, std::uint32_t lines, std::uint32_t p,
                     std::uint32_t b, std::vector<had::ScoredLine>& out) {
@@ -63,6 +66,30 @@ int main() {
         fact_err = int(e.kind());
         pivot = e.pivot;
     }
+    // the reference's free functions (detector.hpp:32, projection.hpp:15-34, erx.hpp:38-47)
+    const std::vector<double> nz = had::normalize_scores(out.back().raw);
+    double nz_err = 0.0;
+    for (size_t i = 0; i < nz.size(); ++i) nz_err = std::fmax(nz_err, std::fabs(nz[i] - out.back().norm[i]));
+    had::ErxDetector srp_det(had::ErxConfig{.dims = 5, .seed = 7}, B, 4);
+    std::vector<had::ScoredLine> o2;
+    for (std::uint32_t t = 0; t < 5; ++t) srp_det.process(had::SpectralLine{std::int64_t(t), P, B, cube.data() + size_t(t) * P * B}, o2);
+    srp_det.finish(o2);
+    const auto w = had::generate_srp(B, 5, 7);
+    const bool w_same = srp_det.state().weights.weights.v == w.weights.v && srp_det.state().weights.nonzero_count() == w.nonzero_count();
+    const auto z = had::project_line(had::SpectralLine{0, P, B, cube.data()}, w);
+    auto [mh, kh] = had::erx::line_stats(z);
+    had::ErxState es;
+    es.mu = mh;
+    es.cov = kh;
+    had::erx::ema_update(es, mh, kh, 0.3);
+    const bool ema_fixed = es.mu.v == mh.v;  // EMA of a state with its own statistics is a fixed point
+    const auto thr = had::erx::apply_threshold({-1.0, 0.0, 2.0}, 1.0);
+    const bool ident = had::identity_projection(B).nonzero_count() == B && had::identity_projection(B).identity;
+    std::printf("{\"normalize_err\": %.3e, \"srp_weights_match\": %s, \"z_rows\": %ld, \"z_cols\": %ld, "
+                "\"stats_d\": %ld, \"ema_fixed\": %s, \"threshold\": [%d, %d, %d], \"identity_ok\": %s, "
+                "\"srp_lines\": %d}\n",
+                nz_err, w_same ? "true" : "false", z.rows(), z.cols(), kh.rows(), ema_fixed ? "true" : "false",
+                thr[0], thr[1], thr[2], ident ? "true" : "false", int(o2.size()));
     std::printf("{\"lines\": %d, \"order_ok\": %s, \"name\": \"%s\", \"norm_mean\": %.3e, \"lines_seen\": %lld, "
                 "\"dims\": %ld, \"warmup0\": %s, \"config_exit\": %d, \"data_exit\": %d, \"numeric_kind\": %d, "
                 "\"pivot\": %d}\n",

@@ -26,6 +26,10 @@ def test_cpp_mirror_compiles_and_links(tmp_path):
 @pytest.mark.gpu
 def test_cpp_mirror_runs_line_scan_loop(tmp_path):
     out = subprocess.run([build(tmp_path)], check=True, capture_output=True, text=True).stdout
+    f = json.loads(out.strip().splitlines()[-2])  # the reference's free functions through the mirror
+    assert f["normalize_err"] < 1e-5 and f["srp_weights_match"] and f["ema_fixed"] and f["identity_ok"]
+    assert (f["z_rows"], f["z_cols"], f["stats_d"]) == (384, 5, 5) and f["threshold"] == [0, 0, 1]
+    assert f["srp_lines"] == 5
     r = json.loads(out.strip().splitlines()[-1])
     assert r["lines"] == 40 and r["order_ok"] and r["name"] == "erx" and r["warmup0"]
     assert abs(r["norm_mean"]) < 1e-5 and r["lines_seen"] == 40 and r["dims"] == 108
