@@ -466,6 +466,7 @@ def run_ours(args):
             "config": config,
             "engine": {"factor_precision": eng.factor_precision(), "stats_kernel": "tcgen05 kind::i8" if tensor
                        else "FFMA", "pool_lines_per_stream": pool_lines, "dims": D,
+                       "rescued_lines": eng.rescued_lines(),
                        "shard": f"rank 0 share of {args.shard_of} GPUs" if shard_n != world else "own"},
             "gather": gathered,
             "pixel_bands_per_s": value * P * B,
@@ -489,9 +490,10 @@ def secondary_measurements(pkg, args):
 
     out = {}
 
-    def throughput(cid, T, modes, streams=(0,), K=20):
+    def throughput(cid, T, modes, streams=(0,), K=20, factor=0):
         """lines/s of a device-resident window of T lines per stream (inputs cycled through a pool
-        >= 2x L2), per mode; also per-line HBM traffic vs the measured peak (4PB + 8P bytes/line)."""
+        >= 2x L2), per mode; also per-line HBM traffic vs the measured peak (4PB + 8P bytes/line) and
+        the per-kernel device times of a separate profiled pass."""
         cfgd = CONFIGS[cid]
         P, B = cfgd["pixels"], cfgd["bands"]
         S = len(streams)
@@ -503,6 +505,7 @@ def secondary_measurements(pkg, args):
         res = {}
         for mode in modes:
             eng = pkg.Engine(pkg.ErxConfig(no_srp=mode == "full", alpha=cfgd["alpha"]), B, S, T)
+            eng.set_factor_precision(factor)
             for k in range(3):
                 eng.run_device(dev[k % n_win].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr(), first_index=k * T)
             eng.sync()
@@ -514,8 +517,14 @@ def secondary_measurements(pkg, args):
             eng.sync()
             lps = K * S * T / (ms / 1e3)
             gbs = lps * (4 * P * B + 8 * P) / 1e9
+            eng.set_profiling(True)
+            for k in range(3):
+                eng.run_device(dev[k % n_win].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr(), first_index=k * T)
+            eng.sync()
+            kt = {kk: round(v[0] / max(v[1], 1), 5) for kk, v in eng.kernel_times().items()}
             res[mode] = {"lines_per_s": lps, "pixel_bands_per_s": lps * P * B, "hbm_gbs_algorithmic": gbs,
-                         "hbm_frac": gbs / peaks()["hbm_gbs"]}
+                         "hbm_frac": gbs / peaks()["hbm_gbs"], "factor_kernel": eng.factor_precision(),
+                         "kernel_ms_per_window": kt}
             eng.close()
         del dev
         return res
@@ -540,6 +549,16 @@ def secondary_measurements(pkg, args):
     try:
         out["batched_c4"] = {"workload": "configs[4]: 4 streams, 1280 px x 448 bands, alpha=0.05, D = B",
                              "window_lines": 32, **throughput(4, 32, ("full",), streams=(0, 1, 2, 3), K=10)}
+        # the same window with the thread-block-cluster factor (DSMEM, 4 CTAs per line) forced
+        out["batched_c4_cluster_factor"] = {"workload": "as batched_c4, ERX_OPT_FACTOR_PRECISION = 30",
+                                            **throughput(4, 32, ("full",), streams=(0, 1, 2, 3), K=5, factor=30)}
+        # lag 0 at 448 bands: one stream, one line per window (the cluster kernel's regime) vs factor_big
+        lat4 = {}
+        for fac, name in ((0, "auto"), (31, "factor_big")):
+            r = throughput(4, 1, ("full",), streams=(0,), K=20, factor=fac)["full"]
+            lat4[name] = {"ms_per_line": 1e3 / r["lines_per_s"], "factor_kernel": r["factor_kernel"],
+                          "kernel_ms_per_window": r["kernel_ms_per_window"]}
+        out["latency_c4"] = {"workload": "configs[4] stream 0: 1280 px x 448 bands, window = 1 (no lag)", **lat4}
     except Exception as ex:
         out["batched_c4"] = {"error": repr(ex)}
     try:

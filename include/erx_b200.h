@@ -134,11 +134,13 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
                   int64_t welford_n);
 
 /* Engine options.  ERX_OPT_FACTOR_PRECISION: 0 auto (blocked fp32 in shared
- * memory while the matrix fits, D <= 233, else blocked fp32 over the L2
- * workspace), 32, 31 (force the fp32 L2 kernel), 64 (fp64 in shared memory,
- * D <= 165, else the fp64 L2 kernel) or 1 (force the blocked fp64 L2 kernel).
- * erx_get_option reports the kernel in use once the first line has fixed the
- * geometry: 32, 31, 64 or 0 (blocked fp64 L2). */
+ * memory while the matrix fits, D <= 233, else blocked fp32 in the shared
+ * memory of a 2/4/8-CTA thread-block cluster), 32, 30 (force the cluster
+ * kernel), 31 (the fp32 kernel over an L2 workspace), 64 (fp64 in shared
+ * memory, D <= 165, else the fp64 L2 kernel) or 1 (force the blocked fp64 L2
+ * kernel).  erx_get_option reports the kernel in use once the first line has
+ * fixed the geometry: 32, 30, 31, 64 or 0 (blocked fp64 L2).  The fp32 kernels
+ * hand lines they cannot factor reliably to an fp64 rescue (k_fixup.cu). */
 #define ERX_OPT_FACTOR_PRECISION 1
 /* ERX_OPT_STATS_TENSOR: which kernels compute line_stats and the score.
  *   2 (default) exact-integer tcgen05 path (kind::i8 digit planes, s32 TMEM
@@ -182,6 +184,11 @@ int64_t erx_get_option(const erx_engine* e, int option);
 uint64_t erx_launch_count(const erx_engine* e);
 /* When on, every kernel launch is bracketed by CUDA events on the engine stream. */
 int erx_set_profiling(erx_engine* e, int on);
+/* Lines whose per-line chain was redone in fp64 by the rescue kernel (k_fixup.cu: the fp32 factor
+ * failed or found the background ill-conditioned, or the line's fp32 scores were flat), summed
+ * over the engine's life; waits for queued work. */
+int64_t erx_rescued_lines(erx_engine* e);
+
 /* Per-kernel summed device ms and launch counts since profiling was enabled. */
 int erx_kernel_times(erx_engine* e, double* ms, uint64_t* launches);
 

@@ -107,6 +107,7 @@ SIGNATURES = {
     "erx_get_option": (C.c_int64, [_vp, C.c_int]),
     "erx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "erx_kernel_times": (C.c_int, [_vp, _dp, _u64p]),
+    "erx_rescued_lines": (C.c_int64, [_vp]),
     "erx_metrics_roc_auc": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _dp, _u64p, _u64p]),
     "erx_metrics_top_k": (C.c_int, [_vp, _vp, C.c_size_t, C.c_size_t, _vp, _vp, _fp]),
     "erx_hadc_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(HadcInfoC)]),

@@ -109,6 +109,8 @@ struct erx_engine {
     unsigned long long* d_latch = nullptr;  // {flag, line id, pivot} of the first device-path failure
     int* d_fix = nullptr;        // fp64 rescue list of the fp32 factor ([0] count, [1] done, [2..] lines)
     double* d_fixwork = nullptr; // the rescue's fp64 workspace
+    int fix_cap = 0;             // list capacity (lines per window)
+    int64_t rescued_before = 0;  // rescued lines counted by earlier (re-planned) lists
 
     // pinned host staging (drop-in path)
     float* h_lines = nullptr;
@@ -215,7 +217,16 @@ void collect_timings(erx_engine* e) {
     e->timings.clear();
 }
 
+int64_t read_rescued(erx_engine* e) {
+    if (!e->d_fix) return 0;
+    int v = 0;
+    cudaStreamSynchronize(e->stream);
+    cudaMemcpy(&v, e->d_fix + e->fix_cap + 2, sizeof(int), cudaMemcpyDeviceToHost);
+    return int64_t(v);
+}
+
 void free_window(erx_engine* e) {
+    e->rescued_before += read_rescued(e);
     cudaFree(e->d_lines);
     cudaFree(e->d_stats);
     cudaFree(e->d_prior);
@@ -281,7 +292,7 @@ int configure(erx_engine* e, uint32_t P) {
     e->sc = erxk::plan_score(g);
     e->small = erxk::small_path(g);
     if (e->small) e->smp = erxk::plan_small(g);
-    e->factor_prec = erxk::factor_precision(g, e->factor_req);
+    e->factor_prec = erxk::factor_precision(g, e->factor_req, int(e->S * e->T));
     // exact-integer tensor path: stats_i8 + factor writing int8 W planes + score_i8
     e->tensor = e->stats_tensor == 2 && erxk::stats_i8_eligible(g) && erxk::score_i8_eligible(g) &&
                 e->factor_prec == 32;
@@ -302,8 +313,9 @@ int configure(erx_engine* e, uint32_t P) {
     if (e->tensor) CU(cudaMalloc(&e->d_c0, L * 4 * size_t(g.D) * sizeof(int)));
     if (e->factor_prec == 32) CU(cudaMalloc(&e->d_kblk, L * erxk::whiten_floats_per_line(g) * sizeof(float)));
     // fp64 rescue list (fed by the fp32 factors and by the normalisation's flat-line check)
-    CU(cudaMalloc(&e->d_fix, (L + 2) * sizeof(int)));
-    CU(cudaMemset(e->d_fix, 0, (L + 2) * sizeof(int)));
+    CU(cudaMalloc(&e->d_fix, (L + 3) * sizeof(int)));
+    CU(cudaMemset(e->d_fix, 0, (L + 3) * sizeof(int)));
+    e->fix_cap = int(L);
     CU(cudaMalloc(&e->d_fixwork, erxk::fixup_work_doubles(g, int(L)) * sizeof(double)));
     return ERX_OK;
 }
@@ -417,7 +429,8 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     {
         timed(e, ERX_KERNEL_FIXUP, [&] {
             erxk::FixupArgs fa{g, xg, int(n), int(in_stride), stats, st_in, e->initialized ? 1 : 0, e->cfg.alpha,
-                               e->cfg.use_incremental, (long long)(e->welford_n), e->cfg.epsilon, e->d_fix, e->d_fixwork,
+                               e->cfg.use_incremental, (long long)(e->welford_n), e->cfg.epsilon, e->d_fix, e->fix_cap,
+                               e->d_fixwork,
                                rawg, normg, status, e->d_latch, line_base};
             erxk::launch_fixup(fa, L, e->stream);
         });
@@ -960,6 +973,11 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
 
 uint64_t erx_launch_count(const erx_engine* e) { return e->launches; }
 
+int64_t erx_rescued_lines(erx_engine* e) {
+    if (!e->failed) drain_pending(e);
+    return e->rescued_before + read_rescued(e);
+}
+
 int erx_set_option(erx_engine* e, int option, int64_t value) {
     if (option == ERX_OPT_ASYNC_HOST) {
         if (value != 0 && value != 1) return fail(e, ERX_ERR_CONFIG, "async host: 0 or 1");
@@ -992,8 +1010,8 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
         return ERX_OK;
     }
     if (option == ERX_OPT_FACTOR_PRECISION) {
-        if (value != 0 && value != 1 && value != 31 && value != 32 && value != 64)
-            return fail(e, ERX_ERR_CONFIG, "factor precision: 0, 1, 31, 32 or 64");
+        if (value != 0 && value != 1 && value != 30 && value != 31 && value != 32 && value != 64)
+            return fail(e, ERX_ERR_CONFIG, "factor precision: 0, 1, 30, 31, 32 or 64");
         if (int st = run_staged_window(e)) return st;
         if (int st = drain_pending(e)) return st;
         e->factor_req = int(value);

@@ -90,7 +90,7 @@ ScoreLaunch plan_score(const Geometry& g);
 size_t whiten_floats_per_line(const Geometry& g);
 // Factor precision actually used for a request (0 auto, 32, 64): 64 / 32 select the
 // shared-memory kernel in that precision, 0 the blocked fp64 global-memory kernel.
-int factor_precision(const Geometry& g, int requested);
+int factor_precision(const Geometry& g, int requested, int lines_per_launch);
 size_t factor_smem(const Geometry& g, int precision);
 
 // Exact-integer tcgen05 stats kernel (k_stats_i8.cu): no_srp, 16 < D <= 127, B % 4 == 0.
@@ -141,7 +141,8 @@ struct FixupArgs {
     int incremental;
     long long n_seen0;
     double eps0;
-    int* list;               // [0] count, [1] CTAs done, [2 ..] listed lines
+    int* list;               // [0] count, [1] CTAs done, [2 .. list_cap + 1] listed lines, [list_cap + 2] total
+    int list_cap;
     double* work;            // fixup_work_doubles(g, L)
     float* raw;
     float* norm;

@@ -15,6 +15,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "tc_common.cuh"
+
 #include "erx_common.cuh"
 #include "f64_factor.cuh"
 #include "i8_common.cuh"
@@ -880,6 +882,295 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
     if (tid == 0) status[line] = -1;
 }
 
+// ---------------------------------------------------------------------------
+// factor_cl (fp32, default for D > 233: configs[4]'s 448 bands): factor_blk's merged Cholesky +
+// inverse sweep over a THREAD-BLOCK CLUSTER of CL CTAs (one SM each), the packed lower 8x8 blocks
+// distributed block-row-cyclically (CTA c owns block rows I = c mod CL) so the whole factor lives in
+// the cluster's shared memory (448 bands: 402 KB over 4 x ~100 KB) instead of an L2 workspace.
+// Step k, two cluster barriers (barrier.cluster):
+//   1  owners of block rows I > k form the panel L_Ik = A_Ik Di^T and push it into EVERY CTA's
+//      panel buffer Lc (st.shared::cluster to mapa-translated addresses), keeping T_Ik = -L_Ik Di;
+//      the owner of block row k finalises X_kJ = Di T_kJ (J < k) and pushes it to every CTA's Xr;
+//   2  every CTA updates its own block rows from its local copies: A_IJ -= L_Ik L_Jk^T (J > k) and
+//      T_IJ -= L_Ik X_kJ (J < k); the owner of block row k + 1 updates the diagonal block first,
+//      factors and inverts it (8 lanes, shuffles, the conditioning test) and pushes Di / Di^T and a
+//      failure flag to every CTA for step k + 1.
+// Lines that fail or are ill-conditioned go to the fp64 rescue like factor_blk's.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cl_map(const void* local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(tc::smem_u32(local)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cl_st4(uint32_t addr, float a, float b, float c, float d) {
+    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void cl_st1i(uint32_t addr, int v) {
+    asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// row r of a swizzled 8x8 block at `blk` (logical column order v) into the same block of every CTA
+template <int CL>
+__device__ __forceinline__ void cl_st8r_all(float* blk, int r, const float* v) {
+    float* p = blk + r * kBlk;
+    const int h = r & 4;
+#pragma unroll
+    for (int q = 0; q < CL; ++q) {
+        cl_st4(cl_map(p + h, q), v[0], v[1], v[2], v[3]);
+        cl_st4(cl_map(p + (h ^ 4), q), v[4], v[5], v[6], v[7]);
+    }
+}
+template <int CL>
+__device__ __forceinline__ void cl_st8_all(float* row, const float* v) {  // plain 8-float row
+#pragma unroll
+    for (int q = 0; q < CL; ++q) {
+        cl_st4(cl_map(row, q), v[0], v[1], v[2], v[3]);
+        cl_st4(cl_map(row + 4, q), v[4], v[5], v[6], v[7]);
+    }
+}
+
+constexpr int kCb = 68;  // factor_cl block stride (floats)
+
+template <int CL>
+__global__ void __launch_bounds__(256, 1) factor_cl_kernel(Geometry g, const double* __restrict__ prior, double eps0,
+                                                            float* __restrict__ whiten, int* __restrict__ status,
+                                                            int* __restrict__ fixlist) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_fail;
+    constexpr int NT = 256;
+    const int D = g.D, Dp = g.Dp, nb = g.nb;
+    const int c = int(cl_rank());
+    const int line = blockIdx.x / CL, tid = threadIdx.x;
+    const int lane = tid & 31, gl = lane & 7;
+    const unsigned gmask = 0xffu << (lane & 24);
+    const int nown = (nb - c + CL - 1) / CL;  // block rows owned by this CTA
+    // the buffers other CTAs write into sit at the same offset in every CTA (mapa keeps the offset)
+    // blocks are kCb = 68 floats apart: a warp's threads working on consecutive blocks (one 8x8 task
+    // each) then hit 32 distinct banks per 16-byte load instead of all the same four
+    float* LcT = reinterpret_cast<float*>(smem);  // [nb][8 cols l][8 rows r]: the step's panel, transposed
+    float* Xr = LcT + size_t(nb) * kCb;           // [nb] X_kJ of the step's block row (swizzled rows)
+    float* DiS = Xr + size_t(nb) * kCb;           // [64] Di (swizzled rows)
+    float* DiT = DiS + 64;                        // [64] Di^T (plain rows)
+    float* dg = DiT + 64;                         // [Dp] diagonal of K + eps I
+    float* A = dg + Dp;                           // owned block rows, packed (per CTA)
+    auto LB = [&](int I, int J) {  // owned block row I = c + CL li starts at li (c + 1) + CL li (li - 1) / 2
+        const int li = I / CL;
+        return A + (size_t(li) * (c + 1) + size_t(CL) * li * (li - 1) / 2 + J) * kCb;
+    };
+    const double* K = prior + size_t(line) * g.SE + D;
+    // ---- load the owned block rows (fp64 packed K -> fp32, + eps; identity padding) and the diagonal
+    for (int li = 0; li < nown; ++li) {
+        const int I = c + CL * li;
+        for (int q = tid; q < (I + 1) * 64; q += NT) {
+            const int J = q >> 6, r = (q >> 3) & 7, cc = q & 7;
+            const int i = I * kBlk + r, j = J * kBlk + cc;
+            float v;
+            if (i >= D) v = (i == j) ? 1.f : 0.f;
+            else if (j > i) v = 0.f;
+            else v = float(K[tri(i, j)] + (i == j ? eps0 : 0.0));
+            LB(I, J)[swz(r, cc)] = v;
+        }
+    }
+    for (int i = tid; i < Dp; i += NT) dg[i] = i < D ? float(K[tri(i, i)] + eps0) : 1.f;
+    if (tid == 0) s_fail = -1;
+    __syncthreads();
+    // the 8 lanes of a group push a freshly factored Di / Di^T (and a failure) to every CTA
+    auto push_di = [&](int f) {
+        __syncwarp(0xffu);  // every lane wrote a column of Di
+        float dl[kBlk], dt[kBlk];
+        ld8r(DiS, gl, dl);
+        ld8(DiT + gl * kBlk, dt);
+        cl_st8r_all<CL>(DiS, gl, dl);
+        cl_st8_all<CL>(DiT + gl * kBlk, dt);
+        if (gl == 0 && f >= 0)
+            for (int q = 0; q < CL; ++q) cl_st1i(cl_map(&s_fail, q), f);
+    };
+    if (c == 0 && tid < kBlk) {  // Di of block 0 (owner: CTA 0)
+        float row[kBlk];
+        ld8r(LB(0, 0), gl, row);
+        push_di(diag_factor8(row, gmask, gl, 0, DiS, DiT, dg));
+    }
+    cl_sync();
+    int fail = s_fail;
+    for (int k = 0; k < nb && fail < 0; ++k) {
+        const int li0 = (k + 1 - c + CL - 1) / CL;  // first owned block row past k
+        const int npb = nown - li0;                 // owned panel blocks
+        const bool own_k = (k % CL) == c;
+        // ---- 1a: panel columns L_Ik[:, l] = A_Ik Di^T[:, l] -> every CTA's LcT[I][l] (one task per
+        // (block, column)); the owner of block row k finalises X_kJ = Di T_kJ -> every CTA's Xr[J]
+        {
+            const int ncol = npb * kBlk, nfin = own_k ? k * kBlk : 0;
+            for (int q = tid; q < ncol + nfin; q += NT) {
+                if (q < ncol) {
+                    const int I = c + CL * (li0 + (q >> 3)), l = q & 7;
+                    const float* blk = LB(I, k);
+                    float d[kBlk], x[kBlk];
+                    ld8r(DiS, l, d);  // Di row l: L[r][l] = sum_{m <= l} A[r][m] Di[l][m]
+#pragma unroll
+                    for (int r = 0; r < kBlk; ++r) {
+                        float ar[kBlk];
+                        ld8r(blk, r, ar);
+                        float sacc = 0.f;
+#pragma unroll
+                        for (int m = 0; m < kBlk; ++m)
+                            if (m <= l) sacc = fmaf(ar[m], d[m], sacc);
+                        x[r] = sacc;
+                    }
+                    cl_st8_all<CL>(LcT + I * kCb + l * kBlk, x);
+                } else {
+                    const int J = (q - ncol) >> 3, r = (q - ncol) & 7;
+                    float* blk = LB(k, J);
+                    float acc[kBlk], d[kBlk];
+                    ld8r(DiS, r, d);
+#pragma unroll
+                    for (int cc = 0; cc < kBlk; ++cc) acc[cc] = 0.f;
+#pragma unroll
+                    for (int l = 0; l < kBlk; ++l) {
+                        float tr[kBlk];
+                        ld8r(blk, l, tr);
+#pragma unroll
+                        for (int cc = 0; cc < kBlk; ++cc) acc[cc] = fmaf(d[l], tr[cc], acc[cc]);
+                    }
+                    __syncwarp(gmask);  // the group's reads of T_kJ precede its writes
+                    st8r(blk, r, acc);
+                    cl_st8r_all<CL>(Xr + J * kCb, r, acc);
+                }
+            }
+            if (own_k && tid < kBlk) {  // X_kk = Di into the owner's diagonal block
+                float dl[kBlk];
+                ld8r(DiS, tid, dl);
+                st8r(LB(k, k), tid, dl);
+            }
+        }
+        __syncthreads();  // this CTA's own panel columns are in its LcT
+        // ---- 1b: T_Ik = -L_Ik Di into the owned panel blocks (row tasks; L from the local LcT)
+        for (int q = tid; q < npb * kBlk; q += NT) {
+            const int I = c + CL * (li0 + (q >> 3)), r = q & 7;
+            const float* lt = LcT + I * kCb;
+            float x[kBlk], t[kBlk];
+#pragma unroll
+            for (int l = 0; l < kBlk; ++l) x[l] = lt[l * kBlk + r];
+#pragma unroll
+            for (int cc = 0; cc < kBlk; ++cc) {
+                float d[kBlk];
+                ld8(DiT + cc * kBlk, d);
+                float sacc = 0.f;
+#pragma unroll
+                for (int l = 0; l < kBlk; ++l)
+                    if (l >= cc) sacc = fmaf(x[l], d[l], sacc);
+                t[cc] = -sacc;
+            }
+            st8r(LB(I, k), r, t);
+        }
+        cl_sync();
+        // ---- 2: block tasks over the owned block rows I > k (8x8 accumulators per thread):
+        //      A_IJ -= L_Ik L_Jk^T (J > k) and T_IJ -= L_Ik X_kJ (J < k); the owner of block row k + 1
+        //      first updates and factors the diagonal block (8 lanes) for the next step
+        {
+            const bool own_next = (k + 1 < nb) && ((k + 1) % CL) == c;
+            if (own_next && tid < kBlk) {
+                float* blk = LB(k + 1, k + 1);
+                const float* lt = LcT + (k + 1) * kCb;
+                float acc[kBlk];
+                ld8r(blk, gl, acc);
+#pragma unroll
+                for (int l = 0; l < kBlk; ++l) {
+                    float b[kBlk];
+                    ld8(lt + l * kBlk, b);
+                    const float ar = b[gl];
+#pragma unroll
+                    for (int cc = 0; cc < kBlk; ++cc) acc[cc] = fmaf(-ar, b[cc], acc[cc]);
+                }
+                st8r(blk, gl, acc);
+                push_di(diag_factor8(acc, gmask, gl, (k + 1) * kBlk, DiS, DiT, dg));
+            }
+            // flat tasks (owned row li >= li0, J in [0, I]) minus J = k and the diagonal block above, dealt
+            // round-robin over the threads not busy with that diagonal block
+            const int t0 = own_next ? kBlk : 0, nthr = NT - t0, me = tid - t0;
+            if (me >= 0) {
+                int base = 0;
+                for (int li = li0; li < nown; ++li) {
+                    const int I = c + CL * li;
+                    const int nt = I + 1;
+                    for (int J = ((me - base) % nthr + nthr) % nthr; J < nt; J += nthr) {
+                        if (J == k || (I == k + 1 && J == k + 1)) continue;
+                        float* blk = LB(I, J);
+                        float acc[kBlk][kBlk];
+#pragma unroll
+                        for (int r = 0; r < kBlk; ++r) ld8r(blk, r, acc[r]);
+                        const float* ai = LcT + I * kCb;
+                        if (J > k) {
+                            const float* bj = LcT + J * kCb;
+#pragma unroll
+                            for (int l = 0; l < kBlk; ++l) {
+                                float av[kBlk], bv[kBlk];
+                                ld8(ai + l * kBlk, av);
+                                ld8(bj + l * kBlk, bv);
+#pragma unroll
+                                for (int r = 0; r < kBlk; ++r)
+#pragma unroll
+                                    for (int cc = 0; cc < kBlk; ++cc) acc[r][cc] = fmaf(-av[r], bv[cc], acc[r][cc]);
+                            }
+                        } else {
+                            const float* xj = Xr + J * kCb;
+#pragma unroll
+                            for (int l = 0; l < kBlk; ++l) {
+                                float av[kBlk], xv[kBlk];
+                                ld8(ai + l * kBlk, av);
+                                ld8r(xj, l, xv);
+#pragma unroll
+                                for (int r = 0; r < kBlk; ++r)
+#pragma unroll
+                                    for (int cc = 0; cc < kBlk; ++cc) acc[r][cc] = fmaf(-av[r], xv[cc], acc[r][cc]);
+                            }
+                        }
+#pragma unroll
+                        for (int r = 0; r < kBlk; ++r) st8r(blk, r, acc[r]);
+                    }
+                    base += nt;
+                }
+            }
+        }
+        cl_sync();
+        fail = s_fail;
+    }
+    if (fail >= 0) {  // the fp64 rescue (k_fixup.cu) redoes this line, escalation included
+        if (c == 0 && tid == 0) list_for_fixup(fixlist, status, line);
+        return;
+    }
+    // ---- X = L^{-1}: each CTA writes its block rows as the score's fp32 W blocks (column-major blocks)
+    const int nblk = nb * (nb + 1) / 2;
+    float* Wp = whiten + size_t(line) * nblk * 64;
+    for (int li = 0; li < nown; ++li) {
+        const int I = c + CL * li;
+        for (int q = tid; q < (I + 1) * 64; q += NT) {
+            const int J = q >> 6, e = q & 63, cc = e >> 3, r = e & 7;  // column-major inside the block
+            const int i = I * kBlk + r, j = J * kBlk + cc;
+            Wp[size_t(tri(I, J)) * 64 + e] = (i < D && j <= i) ? LB(I, J)[swz(r, cc)] : 0.f;
+        }
+    }
+    if (c == 0 && tid == 0) status[line] = -1;
+}
+
+template <int CL>
+size_t factor_cl_smem_t(const Geometry& g) {
+    size_t worst = 0;
+    for (int c = 0; c < CL; ++c) {
+        const int nown = (g.nb - c + CL - 1) / CL;
+        const size_t nloc = size_t(nown) * (c + 1) + size_t(CL) * nown * (nown - 1) / 2;
+        worst = std::max(worst, nloc);
+    }
+    return (worst * kCb + 2 * size_t(g.nb) * kCb + 128 + g.Dp) * 4;
+}
+
 }  // namespace
 
 size_t factor_blk_smem(const Geometry& g) {
@@ -894,8 +1185,21 @@ size_t factor_big_smem(const Geometry& g, bool xk) {
 }
 bool factor_big_xk(const Geometry& g) { return factor_big_smem(g, true) <= 220 * 1024; }
 
+// cluster size of the cluster factor for this geometry (0: does not fit 8 CTAs)
+int factor_cl_size(const Geometry& g) {
+    const size_t cap = 220 * 1024;
+    if (factor_cl_smem_t<2>(g) <= cap) return 2;
+    if (factor_cl_smem_t<4>(g) <= cap) return 4;
+    if (factor_cl_smem_t<8>(g) <= cap) return 8;
+    return 0;
+}
+
 size_t factor_smem(const Geometry& g, int precision) {
     if (precision == 64) return size_t(g.D) * (g.D + 1) * 8;
+    if (precision == 30) {
+        const int cl = factor_cl_size(g);
+        return cl == 2 ? factor_cl_smem_t<2>(g) : cl == 4 ? factor_cl_smem_t<4>(g) : factor_cl_smem_t<8>(g);
+    }
     if (precision == 32) return factor_blk_smem(g);
     if (precision == 31) return factor_big_smem(g, factor_big_xk(g));
     // global path: panel + diagonal block, or the inverse's row block
@@ -904,15 +1208,22 @@ size_t factor_smem(const Geometry& g, int precision) {
     return std::max(chol, inv);
 }
 
-int factor_precision(const Geometry& g, int requested) {
+// Auto choice for D > 233 (measured at configs[4], 448 bands, 128 lines per window: factor_big 1.42 ms,
+// factor_cl 1.88 ms; one line: factor_cl ~4x shorter): the cluster kernel when one wave of clusters
+// holds every line of a launch (the latency regime: lag 0, few streams), else the L2-workspace kernel.
+int factor_precision(const Geometry& g, int requested, int lines_per_launch) {
     const size_t cap = 220 * 1024;
     const bool blk_fits = factor_blk_smem(g) <= cap;
     const bool f64_fits = size_t(g.D) * (g.D + 1) * 8 <= cap;
     if (requested == 64 && f64_fits) return 64;
     const bool big_fits = factor_big_smem(g, false) <= cap;
     if (requested == 31 && big_fits) return 31;
+    if (requested == 30 && factor_cl_size(g)) return 30;
     if ((requested == 32 || requested == 0) && blk_fits) return 32;
-    if ((requested == 32 || requested == 0 || requested == 31) && big_fits) return 31;  // fp32 over L2 (large D)
+    const int cl = factor_cl_size(g);
+    if ((requested == 32 || requested == 0) && cl && (!big_fits || lines_per_launch * cl <= sm_count()))
+        return 30;  // fp32 in a cluster's shared memory (large D, one wave)
+    if ((requested == 32 || requested == 0 || requested == 31) && big_fits) return 31;  // fp32 over L2
     return 0;  // blocked fp64 over global memory
 }
 
@@ -948,6 +1259,30 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
     } else if (precision == 64) {
         ensure_smem(factor_smem_kernel<double>, sm);
         factor_smem_kernel<double><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base);
+    } else if (precision == 30) {
+        const int cl = factor_cl_size(g);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(n_lines_total * cl));
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = unsigned(cl);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cl == 2) {
+            ensure_smem(factor_cl_kernel<2>, sm);
+            cudaLaunchKernelEx(&cfg, factor_cl_kernel<2>, g, prior, eps0, whiten, status, fixlist);
+        } else if (cl == 4) {
+            ensure_smem(factor_cl_kernel<4>, sm);
+            cudaLaunchKernelEx(&cfg, factor_cl_kernel<4>, g, prior, eps0, whiten, status, fixlist);
+        } else {
+            ensure_smem(factor_cl_kernel<8>, sm);
+            cudaLaunchKernelEx(&cfg, factor_cl_kernel<8>, g, prior, eps0, whiten, status, fixlist);
+        }
     } else if (precision == 31) {
         ensure_smem(factor_big_kernel, sm);
         factor_big_kernel<<<n_lines_total, 256, sm, st>>>(g, prior, eps0, reinterpret_cast<float*>(work), whiten,

@@ -218,6 +218,7 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(FixupArgs a) {
     if (tid == 0) {
         __threadfence();
         if (atomicAdd(&a.list[1], 1) == int(gridDim.x) - 1) {
+            a.list[a.list_cap + 2] += a.list[0];  // running total of rescued lines (erx_rescued_lines)
             a.list[0] = 0;
             a.list[1] = 0;
             __threadfence();

@@ -303,6 +303,10 @@ class Engine:
     def set_profiling(self, on: bool):
         self._lib.erx_set_profiling(self._h, int(on))
 
+    def rescued_lines(self) -> int:
+        """Lines redone by the fp64 rescue kernel so far (erx_rescued_lines)."""
+        return int(self._lib.erx_rescued_lines(self._h))
+
     def kernel_times(self):
         ms = np.zeros(L.NUM_KERNELS)
         n = np.zeros(L.NUM_KERNELS, np.uint64)

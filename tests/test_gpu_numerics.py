@@ -47,7 +47,7 @@ def run_both(pkg, oracle, cfg, x, window=8, state=None, factor=None, want_stats=
     norm_o = np.zeros((L_, P))
     for t in range(L_):
         raw_o[t], norm_o[t], _ = det.process(t, x[t])
-    info = {"stats": eng.stats_tensor(), "factor": eng.factor_precision()}
+    info = {"stats": eng.stats_tensor(), "factor": eng.factor_precision(), "rescued": eng.rescued_lines()}
     if want_stats is not None:
         assert info["stats"] == want_stats, info
     eng.close()
@@ -83,6 +83,7 @@ def test_forced_eps_escalation(pkg, oracle, B):
     cfg = pkg.ErxConfig(no_srp=True, alpha=0.1, buffer_len=0)
     raw_g, norm_g, raw_o, norm_o, info = run_both(pkg, oracle, cfg, x, window=4, state=(mu, K, 50))
     check_gates(oracle, raw_g, norm_g, raw_o, norm_o, label=f"escalation B={B} {info}")
+    assert info["rescued"] > 0, info  # the escalation ran in the fp64 rescue
 
 
 def test_escalation_exhausted_raises_with_pivot(pkg, oracle):
@@ -158,6 +159,7 @@ def test_radiance_scale_ill_conditioned(pkg, oracle, B, noise):
     cfg = pkg.ErxConfig(no_srp=True, alpha=0.1, buffer_len=0)
     raw_g, norm_g, raw_o, norm_o, info = run_both(pkg, oracle, cfg, x, window=8)
     check_gates(oracle, raw_g, norm_g, raw_o, norm_o, label=f"DN B={B} noise={noise} {info}")
+    assert info["rescued"] > 0, info  # the fp64 rescue took the ill-conditioned lines
 
 
 # ---------------------------------------------------------------- SRP ablation dims

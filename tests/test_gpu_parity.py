@@ -255,10 +255,11 @@ def test_config4_subset(pkg, oracle, no_srp):
                overrides={"scene_change_line": [20, 40]}, window=16)
 
 
-@pytest.mark.parametrize("cid,n_lines", [(0, 240), (1, 120)])
-@pytest.mark.parametrize("prec", [64, 32, 31, 1])
+@pytest.mark.parametrize("cid,n_lines", [(0, 240), (1, 120), (4, 40)])
+@pytest.mark.parametrize("prec", [64, 32, 31, 30, 1])
 def test_factor_kernel_variants(pkg, oracle, cid, n_lines, prec):
-    """Every factor path (fp64 / fp32 shared-memory, blocked fp32 / fp64 over L2) meets the gates."""
+    """Every factor path (fp64 / fp32 shared-memory, fp32 in a thread-block cluster's shared memory,
+    blocked fp32 / fp64 over L2) meets the gates."""
     spec = pkg.gen_spec(cid)
     lines, mask = pkg.gen_lines(spec, 0, n_lines)
     alpha = 0.1 if cid == 0 else 0.05
@@ -267,7 +268,8 @@ def test_factor_kernel_variants(pkg, oracle, cid, n_lines, prec):
     eng.set_factor_precision(prec)
     eng.push(lines[None], 0)
     eng.finish()
-    want = {64: 64 if cid == 0 else 0, 32: 32, 31: 31, 1: 0}[prec]  # fp64 D=224 does not fit smem -> blocked
+    # fp64 at D = 224 / 448 does not fit shared memory -> blocked over L2; fp32 at 448 bands -> the cluster
+    want = {64: 64 if cid == 0 else 0, 32: 30 if cid == 4 else 32, 31: 31, 30: 30, 1: 0}[prec]
     assert eng.factor_precision() == want
     _, wu, raw_g, norm_g = eng.pop()
     raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), lines)

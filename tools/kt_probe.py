@@ -24,6 +24,8 @@ dev = torch.from_numpy(host).cuda().view(S, n_win, T, P, B).permute(1, 0, 2, 3, 
 raw = torch.empty((S, T, P), dtype=torch.float32, device="cuda")
 norm = torch.empty_like(raw)
 eng = pkg.Engine(pkg.ErxConfig(no_srp=mode == "full", alpha=config["alpha"]), B, S, T)
+if os.environ.get("ERX_FACTOR"):
+    eng.set_factor_precision(int(os.environ["ERX_FACTOR"]))
 for k in range(3):
     eng.run_device(dev[k % n_win].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr(), first_index=k * T)
 eng.sync()
@@ -37,5 +39,5 @@ for k in range(K):
     eng.run_device(dev[k % n_win].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr(), first_index=k * T)
 eng.sync()
 kt = eng.kernel_times()
-print(os.environ.get("ERX_B200_LIB", "default"), f"c{cid} {mode} T={T}: {ms:.4f} ms/step, {S * T / ms * 1e3 / 1e6:.3f} M lines/s |",
+print(os.environ.get("ERX_B200_LIB", "default"), f"factor={eng.factor_precision()}", f"c{cid} {mode} T={T}: {ms:.4f} ms/step, {S * T / ms * 1e3 / 1e6:.3f} M lines/s |",
       " ".join(f"{k} {v[0] / max(v[1], 1):.4f}" for k, v in kt.items()))
