@@ -559,3 +559,32 @@ def test_async_host_pipelines_and_reports_failure(pkg):
             eng2.push(x[:, k:k + 16], k)
             eng2.pop()
         eng2.finish()
+
+
+# ---------------------------------------------------------------- race evidence (compute-sanitizer is closed here)
+@pytest.mark.parametrize("cid,S,n,P,windows,factor", [
+    (3, 6, 24, 640, (24, 8, 5, 1), 0),     # stats_i8 / score_i8 / factor_blk: different CTA <-> line maps
+    (3, 6, 24, 640, (24, 7), 0),
+    (1, 2, 12, 640, (12, 5, 1), 0),        # FFMA stats / score at 224 bands
+    (4, 2, 6, 1280, (6, 1), 30),           # thread-block-cluster factor
+    (2, 1, 300, 1024, (300, 64, 7), 0),    # chunked scan / small path
+])
+def test_window_partition_bitwise(pkg, cid, S, n, P, windows, factor):
+    """Every line's scores are a function of that line and its background only, so re-cutting the same
+    streams into different windows (different persistent-CTA line assignments, pipeline phases, ring
+    stages, cluster placements) must give bit-identical scores.  With compute-sanitizer closed on this
+    pool (profiles/r02_sanitizer_racecheck.txt), this is the race detector for the warp-specialised
+    mbarrier / TMEM kernels and the cluster kernel."""
+    x = np.stack([pkg.gen_lines(pkg.gen_spec(cid, s), 0, n)[0] for s in range(S)])
+    ref = None
+    for T in windows:
+        eng = pkg.Engine(pkg.ErxConfig(no_srp=True, alpha=0.1), x.shape[3], n_streams=S, window_lines=T)
+        eng.set_factor_precision(factor)
+        eng.push(x, 0)
+        eng.finish()
+        _, _, raw, norm = eng.pop()
+        eng.close()
+        if ref is None:
+            ref = (raw, norm)
+        else:
+            assert np.array_equal(raw, ref[0]) and np.array_equal(norm, ref[1]), f"window {T}"
