@@ -144,8 +144,9 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
 #define ERX_OPT_FACTOR_PRECISION 1
 /* ERX_OPT_STATS_TENSOR: which kernels compute line_stats and the score.
  *   2 (default) exact-integer tcgen05 path (kind::i8 digit planes, s32 TMEM
- *     accumulation) for both where eligible (full covariance, 16 < D <= 127,
- *     B % 4 == 0), the FFMA kernels elsewhere;
+ *     accumulation) where eligible (full covariance, B % 4 == 0): statistics and
+ *     score for 16 < D <= 127; statistics for 127 < D <= 512 (128-dim tile
+ *     pairs, 2D TMA boxes) with the FFMA score; the FFMA kernels elsewhere;
  *   0 the FFMA kernels.
  * (1, the round-1 bf16x3 tcgen05 statistics, is gone: fp32 TMEM accumulation
  * truncates and missed the median gate; ERX_ERR_CONFIG.)

@@ -93,6 +93,7 @@ struct erx_engine {
     int factor_prec = 0;  // precision in use (0 = blocked fp64 global path)
     int factor_threads = 0;  // ERX_OPT_FACTOR_THREADS (0 auto)
     bool tensor = false;      // exact-integer tcgen05 stats + score in use (fixed at configure)
+    bool wide_i8 = false;     // exact-integer tcgen05 stats for D > 127 (k_stats_i8t.cu; FFMA score)
     size_t white_stride = 0;  // floats per line of d_white (fp32 W blocks or int8 W planes)
 
     // device buffers, capacity S*T lines
@@ -296,6 +297,7 @@ int configure(erx_engine* e, uint32_t P) {
     // exact-integer tensor path: stats_i8 + factor writing int8 W planes + score_i8
     e->tensor = e->stats_tensor == 2 && erxk::stats_i8_eligible(g) && erxk::score_i8_eligible(g) &&
                 e->factor_prec == 32;
+    e->wide_i8 = !e->tensor && !e->small && e->stats_tensor == 2 && erxk::stats_i8t_eligible(g);
     e->white_stride = e->tensor ? erxk::wplanes_bytes_per_line() / sizeof(float) : erxk::whiten_floats_per_line(g);
     const size_t L = size_t(e->S) * e->T;
     CU(cudaMalloc(&e->d_stats, L * (g.SE + g.D) * sizeof(double)));  // [c | s | S] per line
@@ -391,14 +393,18 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     int* status = e->d_status + l0;
     float* rawg = raw ? raw + l0 * g.P : nullptr;
     float* normg = norm ? norm + l0 * g.P : nullptr;
+    int stats_rc = 0;
     timed(e, ERX_KERNEL_STATS, [&] {
         if (e->small)
             erxk::launch_stats_small(g, e->smp, xg, int(n), int(in_stride), L, stats, vcache, e->stream);
         else if (tensor)
             erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, vmax, vplanes, c0, e->stream);
+        else if (e->wide_i8)
+            stats_rc = erxk::launch_stats_i8t(g, xg, int(n), int(in_stride), int(ns), stats, nullptr, e->stream);
         else
             erxk::launch_stats(g, e->sl, xg, int(n), int(in_stride), L, stats, e->stream);
     });
+    if (stats_rc) return fail(e, ERX_ERR_DEVICE, "stats_i8t: cannot encode the TMA tensor map");
     timed(e, ERX_KERNEL_SCAN, [&] {
         erxk::launch_scan(g, stats, prior, st_in, st_out, int(ns), int(n), e->initialized ? 1 : 0, e->cfg.alpha,
                           e->cfg.use_incremental, e->welford_n, e->stream, kblk);
@@ -1032,7 +1038,7 @@ int64_t erx_get_option(const erx_engine* e, int option) {
     if (option == ERX_OPT_ASYNC_HOST) return e->async_host ? 1 : 0;
     if (option == ERX_OPT_STATS_TENSOR) {
         if (!e->d_stats) return e->stats_tensor;
-        if (e->tensor) return 2;
+        if (e->tensor || e->wide_i8) return 2;
         return 0;
     }
     return -1;

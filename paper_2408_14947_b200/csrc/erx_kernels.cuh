@@ -101,6 +101,12 @@ bool stats_i8_eligible(const Geometry& g);
 // tiny kernel of this launcher).
 void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
                      double* stats, float* vmax, unsigned char* vplanes, int* c0, cudaStream_t st);
+// Exact-integer tcgen05 stats for wide lines (k_stats_i8t.cu): no_srp, 127 < D <= 512, B % 4 == 0;
+// work items are the lower-triangle pairs of 128-dim tiles, 2D TMA boxes from the line.  Returns 0, or
+// non-zero when the tensor map could not be encoded (nothing launched).
+bool stats_i8t_eligible(const Geometry& g);
+int launch_stats_i8t(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_streams,
+                     double* stats, float* vmax, cudaStream_t st);
 // Exact-integer tcgen05 score kernel (k_score_i8.cu): v planes from stats_i8, W planes from the factor.
 bool score_i8_eligible(const Geometry& g);
 size_t wplanes_bytes_per_line();

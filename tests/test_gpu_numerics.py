@@ -107,9 +107,7 @@ def test_escalation_exhausted_raises_with_pivot(pkg, oracle):
 
 
 # ---------------------------------------------------------------- degenerate line statistics
-@pytest.mark.parametrize("B,P", [(12, 8), (64, 32), (108, 60), pytest.param(160, 100, marks=pytest.mark.xfail(
-    reason="D > 127 takes the FFMA statistics: fp32 products of v cost ~1e-4 of the near-null "
-           "eigenvalues (norm error 1.9e-3 > 1e-3); the exact-integer statistics cover D <= 127", strict=False))])
+@pytest.mark.parametrize("B,P", [(12, 8), (64, 32), (108, 60), (160, 100), (224, 150)])
 def test_rank_deficient_lines(pkg, oracle, B, P):
     """P - 1 < D: each line's covariance is rank P - 1; the first lines' backgrounds are
     eps-regularised and far from fp32 territory (every such line takes the fp64 rescue)."""
