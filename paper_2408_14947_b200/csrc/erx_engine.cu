@@ -84,7 +84,9 @@ struct erx_engine {
     bool small = false;       // D <= 16: stats_small / score_small path
     float* d_vcache = nullptr;  // [S*T][D][P] centred projections (small path)
     float* d_vmax = nullptr;    // [S*T][D] per-dim |x - c| range (tensor path)
-    unsigned char* d_vplanes = nullptr;  // [S*T][tiles][48 KB] quantised v digit planes (tensor path)
+    unsigned char* d_vplanes = nullptr;  // [S*T][tiles][48 KB] quantised v digit planes (tensor path; wide:
+                                         // [S*T][pixel tiles][dim tiles][48 KB])
+    unsigned char* d_wplw = nullptr;     // [S*T][wplanes_w_bytes] the wide score's int8 W operand
     int* d_c0 = nullptr;        // [S*T][4][D] class-0 diagonal partials of the integer statistics (tensor path)
     float* d_kblk = nullptr;    // [S*T][nb(nb+1)/2][64] pre-update K as fp32 blocks (blocked fp32 factor)
     int factor_req = 0;   // requested factor precision (0 auto, 32, 64)
@@ -93,7 +95,7 @@ struct erx_engine {
     int factor_prec = 0;  // precision in use (0 = blocked fp64 global path)
     int factor_threads = 0;  // ERX_OPT_FACTOR_THREADS (0 auto)
     bool tensor = false;      // exact-integer tcgen05 stats + score in use (fixed at configure)
-    bool wide_i8 = false;     // exact-integer tcgen05 stats for D > 127 (k_stats_i8t.cu; FFMA score)
+    bool wide_i8 = false;     // exact-integer tcgen05 stats + score for D > 127 (k_stats_i8t.cu, k_score_i8w.cu)
     size_t white_stride = 0;  // floats per line of d_white (fp32 W blocks or int8 W planes)
 
     // device buffers, capacity S*T lines
@@ -242,6 +244,8 @@ void free_window(erx_engine* e) {
     e->d_vmax = nullptr;
     cudaFree(e->d_vplanes);
     e->d_vplanes = nullptr;
+    cudaFree(e->d_wplw);
+    e->d_wplw = nullptr;
     cudaFree(e->d_c0);
     e->d_c0 = nullptr;
     cudaFree(e->d_kblk);
@@ -297,7 +301,8 @@ int configure(erx_engine* e, uint32_t P) {
     // exact-integer tensor path: stats_i8 + factor writing int8 W planes + score_i8
     e->tensor = e->stats_tensor == 2 && erxk::stats_i8_eligible(g) && erxk::score_i8_eligible(g) &&
                 e->factor_prec == 32;
-    e->wide_i8 = !e->tensor && !e->small && e->stats_tensor == 2 && erxk::stats_i8t_eligible(g);
+    e->wide_i8 = !e->tensor && !e->small && e->stats_tensor == 2 && erxk::stats_i8t_eligible(g) &&
+                 erxk::score_i8w_eligible(g);
     e->white_stride = e->tensor ? erxk::wplanes_bytes_per_line() / sizeof(float) : erxk::whiten_floats_per_line(g);
     const size_t L = size_t(e->S) * e->T;
     CU(cudaMalloc(&e->d_stats, L * (g.SE + g.D) * sizeof(double)));  // [c | s | S] per line
@@ -310,8 +315,12 @@ int configure(erx_engine* e, uint32_t P) {
     CU(cudaMalloc(&e->d_norm, L * P * sizeof(float)));
     CU(cudaMalloc(&e->d_status, L * sizeof(int)));
     if (e->small) CU(cudaMalloc(&e->d_vcache, L * size_t(g.D) * P * sizeof(float)));
-    if (erxk::stats_i8_eligible(g)) CU(cudaMalloc(&e->d_vmax, L * size_t(g.D) * sizeof(float)));
+    if (erxk::stats_i8_eligible(g) || e->wide_i8) CU(cudaMalloc(&e->d_vmax, L * size_t(g.D) * sizeof(float)));
     if (e->tensor) CU(cudaMalloc(&e->d_vplanes, L * erxk::vplanes_bytes_per_line(g)));
+    if (e->wide_i8) {
+        CU(cudaMalloc(&e->d_vplanes, L * erxk::vplanes_w_bytes_per_line(g)));
+        CU(cudaMalloc(&e->d_wplw, L * erxk::wplanes_w_bytes_per_line(g)));
+    }
     if (e->tensor) CU(cudaMalloc(&e->d_c0, L * 4 * size_t(g.D) * sizeof(int)));
     if (e->factor_prec == 32) CU(cudaMalloc(&e->d_kblk, L * erxk::whiten_floats_per_line(g) * sizeof(float)));
     // fp64 rescue list (fed by the fp32 factors and by the normalisation's flat-line check)
@@ -386,7 +395,9 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     float* white = e->d_white + l0 * e->white_stride;
     float* vcache = e->d_vcache ? e->d_vcache + l0 * size_t(g.D) * g.P : nullptr;
     float* vmax = e->d_vmax ? e->d_vmax + l0 * size_t(g.D) : nullptr;
-    unsigned char* vplanes = e->d_vplanes ? e->d_vplanes + l0 * erxk::vplanes_bytes_per_line(g) : nullptr;
+    const size_t vpl_line = e->wide_i8 ? erxk::vplanes_w_bytes_per_line(g) : erxk::vplanes_bytes_per_line(g);
+    unsigned char* vplanes = e->d_vplanes ? e->d_vplanes + l0 * vpl_line : nullptr;
+    unsigned char* wplw = e->d_wplw ? e->d_wplw + l0 * erxk::wplanes_w_bytes_per_line(g) : nullptr;
     float* kblk = e->d_kblk ? e->d_kblk + l0 * erxk::whiten_floats_per_line(g) : nullptr;
     int* c0 = (e->tensor && e->d_c0) ? e->d_c0 + l0 * 4 * size_t(g.D) : nullptr;
     const bool tensor = e->tensor;
@@ -400,7 +411,7 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
         else if (tensor)
             erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, vmax, vplanes, c0, e->stream);
         else if (e->wide_i8)
-            stats_rc = erxk::launch_stats_i8t(g, xg, int(n), int(in_stride), int(ns), stats, nullptr, e->stream);
+            stats_rc = erxk::launch_stats_i8t(g, xg, int(n), int(in_stride), int(ns), stats, vmax, vplanes, e->stream);
         else
             erxk::launch_stats(g, e->sl, xg, int(n), int(in_stride), L, stats, e->stream);
     });
@@ -425,9 +436,12 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
         });
     } else {
         timed(e, ERX_KERNEL_SCORE, [&] {
-            if (tensor)
+            if (tensor) {
                 erxk::launch_score_i8(g, vplanes, reinterpret_cast<const unsigned char*>(white), L, rawg, e->stream);
-            else
+            } else if (e->wide_i8) {
+                erxk::launch_wplanes_w(g, white, stats, prior, vmax, L, wplw, e->stream);
+                erxk::launch_score_i8w(g, vplanes, wplw, L, rawg, e->stream);
+            } else
                 erxk::launch_score(g, e->sc, xg, int(n), int(in_stride), prior, white, L, rawg, e->stream);
         });
         timed(e, ERX_KERNEL_NORMALIZE, [&] { erxk::launch_normalize(g, rawg, L, normg, status, e->d_fix, e->stream); });

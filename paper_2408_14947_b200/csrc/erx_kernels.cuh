@@ -106,7 +106,16 @@ void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in
 // non-zero when the tensor map could not be encoded (nothing launched).
 bool stats_i8t_eligible(const Geometry& g);
 int launch_stats_i8t(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_streams,
-                     double* stats, float* vmax, cudaStream_t st);
+                     double* stats, float* vmax, unsigned char* vplanes, cudaStream_t st);
+// Exact-integer tcgen05 score for wide lines (k_score_i8w.cu): the factor's fp32 W blocks are turned into
+// the int8 operand by launch_wplanes_w (any factor kernel), then the score reads the stats' v planes.
+bool score_i8w_eligible(const Geometry& g);
+size_t wplanes_w_bytes_per_line(const Geometry& g);
+size_t vplanes_w_bytes_per_line(const Geometry& g);
+void launch_wplanes_w(const Geometry& g, const float* whiten, const double* stats, const double* prior,
+                      const float* vmax, int n_lines_total, unsigned char* wpl, cudaStream_t st);
+void launch_score_i8w(const Geometry& g, const unsigned char* vplanes, const unsigned char* wplanes, int n_lines_total,
+                      float* raw, cudaStream_t st);
 // Exact-integer tcgen05 score kernel (k_score_i8.cu): v planes from stats_i8, W planes from the factor.
 bool score_i8_eligible(const Geometry& g);
 size_t wplanes_bytes_per_line();

@@ -77,8 +77,10 @@ struct StatsI8TArgs {
     int n_lines;
     int ntile;       // ceil(D / 128)
     int npair;       // ntile (ntile + 1) / 2
+    int nptile;      // 128-pixel tiles per line (v planes)
     double* stats;   // [line][c | s | S packed lower]
     float* vmax;     // [line][D] max_p |fl32(x - c)| (may be null)
+    unsigned char* vplanes;  // [line][pixel tile][dim tile][3][16 KB] v digit planes (k_score_i8w), may be null
 };
 
 __device__ __forceinline__ void pair_of(int p, int& mt, int& nt) {  // p -> (mt, nt), nt <= mt, row-major
@@ -299,6 +301,17 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8t_kernel(const __gri
                 for (int pl = 0; pl < 3; ++pl)
                     *reinterpret_cast<uint4*>(op + (set * 3 + pl) * kPlane + off) =
                         make_uint4(w[pl][0], w[pl][1], w[pl][2], w[pl][3]);
+                if (diag && a.vplanes) {
+                    // the same digits as the wide score's MN-major A operand (i8_common.cuh: vplane_off)
+                    const int p = c * kCh + h * 16;
+                    unsigned char* vt = a.vplanes +
+                                        ((size_t(line) * a.nptile + (p >> 7)) * a.ntile + m0 / kTile) * (3 * 16384);
+                    const uint64_t stream_out = tc::policy_evict_first();
+#pragma unroll
+                    for (int pl = 0; pl < 3; ++pl)
+                        tc::st16_hint(vt + i8::vplane_off(pl, d, p & 127), make_uint4(w[pl][0], w[pl][1], w[pl][2], w[pl][3]),
+                                      stream_out);
+                }
             }
             tc::fence_proxy_async();
             __syncwarp();
@@ -377,7 +390,7 @@ bool stats_i8t_eligible(const Geometry& g) {
 }
 
 int launch_stats_i8t(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_streams,
-                     double* stats, float* vmax, cudaStream_t st) {
+                     double* stats, float* vmax, unsigned char* vplanes, cudaStream_t st) {
     auto encode = tensor_map_encoder();
     if (!encode) return 1;
     // the window's lines as one 2D tensor: rows = pixels of every (stream, line slot), B floats each
@@ -391,7 +404,8 @@ int launch_stats_i8t(const Geometry& g, const float* x, int n_per_stream, int in
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return 2;
     const int ntile = (g.D + kTile - 1) / kTile;
-    StatsI8TArgs a{g, n_per_stream, in_stride, n_streams * n_per_stream, ntile, ntile * (ntile + 1) / 2, stats, vmax};
+    StatsI8TArgs a{g, n_per_stream, in_stride, n_streams * n_per_stream, ntile, ntile * (ntile + 1) / 2,
+                   (g.P + kTile - 1) / kTile, stats, vmax, vplanes};
     const int items = a.n_lines * a.npair;
     const int grid = items < sm_count() ? items : sm_count();
     ensure_smem(stats_i8t_kernel, kSmem);
