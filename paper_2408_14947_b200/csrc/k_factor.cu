@@ -937,7 +937,9 @@ __device__ __forceinline__ void cl_st8_all(float* row, const float* v) {  // pla
     }
 }
 
-constexpr int kCb = 68;  // factor_cl block stride (floats)
+constexpr int kCb = 68;  // factor_cl block stride (floats): consecutive blocks on distinct banks
+
+
 
 template <int CL>
 __global__ void __launch_bounds__(256, 1) factor_cl_kernel(Geometry g, const double* __restrict__ prior, double eps0,
