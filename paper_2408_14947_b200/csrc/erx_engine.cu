@@ -84,6 +84,7 @@ struct erx_engine {
     bool small = false;       // D <= 16: stats_small / score_small path
     float* d_vcache = nullptr;  // [S*T][D][P] centred projections (small path)
     float* d_vmax = nullptr;    // [S*T][D] per-dim |x - c| range (tensor path)
+    float* d_cen = nullptr;     // [S*T][D] per-dim centre (wide tensor path)
     unsigned char* d_vplanes = nullptr;  // [S*T][tiles][48 KB] quantised v digit planes (tensor path; wide:
                                          // [S*T][pixel tiles][dim tiles][48 KB])
     unsigned char* d_wplw = nullptr;     // [S*T][wplanes_w_bytes] the wide score's int8 W operand
@@ -242,6 +243,8 @@ void free_window(erx_engine* e) {
     e->d_vcache = nullptr;
     cudaFree(e->d_vmax);
     e->d_vmax = nullptr;
+    cudaFree(e->d_cen);
+    e->d_cen = nullptr;
     cudaFree(e->d_vplanes);
     e->d_vplanes = nullptr;
     cudaFree(e->d_wplw);
@@ -319,6 +322,7 @@ int configure(erx_engine* e, uint32_t P) {
     if (e->tensor) CU(cudaMalloc(&e->d_vplanes, L * erxk::vplanes_bytes_per_line(g)));
     if (e->wide_i8) {
         CU(cudaMalloc(&e->d_vplanes, L * erxk::vplanes_w_bytes_per_line(g)));
+        CU(cudaMalloc(&e->d_cen, L * size_t(g.D) * sizeof(float)));
         CU(cudaMalloc(&e->d_wplw, L * erxk::wplanes_w_bytes_per_line(g)));
     }
     if (e->tensor) CU(cudaMalloc(&e->d_c0, L * 4 * size_t(g.D) * sizeof(int)));
@@ -395,6 +399,7 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     float* white = e->d_white + l0 * e->white_stride;
     float* vcache = e->d_vcache ? e->d_vcache + l0 * size_t(g.D) * g.P : nullptr;
     float* vmax = e->d_vmax ? e->d_vmax + l0 * size_t(g.D) : nullptr;
+    float* cen = e->d_cen ? e->d_cen + l0 * size_t(g.D) : nullptr;
     const size_t vpl_line = e->wide_i8 ? erxk::vplanes_w_bytes_per_line(g) : erxk::vplanes_bytes_per_line(g);
     unsigned char* vplanes = e->d_vplanes ? e->d_vplanes + l0 * vpl_line : nullptr;
     unsigned char* wplw = e->d_wplw ? e->d_wplw + l0 * erxk::wplanes_w_bytes_per_line(g) : nullptr;
@@ -411,7 +416,8 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
         else if (tensor)
             erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, vmax, vplanes, c0, e->stream);
         else if (e->wide_i8)
-            stats_rc = erxk::launch_stats_i8t(g, xg, int(n), int(in_stride), int(ns), stats, vmax, vplanes, e->stream);
+            stats_rc = erxk::launch_stats_i8t(g, xg, int(n), int(in_stride), int(ns), stats, cen, vmax, vplanes,
+                                              e->stream);
         else
             erxk::launch_stats(g, e->sl, xg, int(n), int(in_stride), L, stats, e->stream);
     });

@@ -105,8 +105,9 @@ void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in
 // work items are the lower-triangle pairs of 128-dim tiles, 2D TMA boxes from the line.  Returns 0, or
 // non-zero when the tensor map could not be encoded (nothing launched).
 bool stats_i8t_eligible(const Geometry& g);
+// cen / vmax: [line][D] scratch the range pass fills (vmax is also the score's per-dim range).
 int launch_stats_i8t(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_streams,
-                     double* stats, float* vmax, unsigned char* vplanes, cudaStream_t st);
+                     double* stats, float* cen, float* vmax, unsigned char* vplanes, cudaStream_t st);
 // Exact-integer tcgen05 score for wide lines (k_score_i8w.cu): the factor's fp32 W blocks are turned into
 // the int8 operand by launch_wplanes_w (any factor kernel), then the score reads the stats' v planes.
 bool score_i8w_eligible(const Geometry& g);

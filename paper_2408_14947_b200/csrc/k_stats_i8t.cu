@@ -9,11 +9,12 @@
 // (mt, nt), nt <= mt — 3 items at 224 bands, 10 at 448 — each computing
 // S[mt dims][nt dims] over all pixels:
 //
-//   pass 1  the item's dims of every 32-pixel chunk (2D TMA boxes of 128 dims x
-//           32 pixels from the line: cp.async.bulk.tensor, zero fill past B):
-//           per-dim min / max and the centre c = fp32(mean of the first
-//           min(32, P) pixels) (k_stats.cu's rule)
-//   pass 2  the same chunks again (L2): v = fl32(x - c) rounded ONCE to
+//   range   (range_kernel, once per line for all dims) the centre c = fp32(mean
+//           of the first min(32, P) pixels) (k_stats.cu's rule) and the
+//           per-dim range max_p |fl32(x - c)|
+//   main    the item's dims of every 32-pixel chunk (2D TMA boxes of 128 dims x
+//           32 pixels from the line: cp.async.bulk.tensor, zero fill past B,
+//           L2 hits for all but the first item of a line): v = fl32(x - c) rounded ONCE to
 //           q = rint(v s_d), s_d = R / max|v|, R < 2^22, split into three
 //           balanced int8 digits (i8_common.cuh), written as the MMA's K-major
 //           A (mt dims) and B (nt dims) digit planes; 8 digit-pair MMAs
@@ -21,8 +22,7 @@
 //           s32 class accumulators
 //   epilogue  S = (sum_c 2^(8(c+1)) acc_c [+ class 0 on the diagonal]) / (s_a s_b)
 //           straight into the packed-lower stats slot; diagonal items also
-//           write c, s = sum v (the quantiser's exact int64 sum of q / s_d) and
-//           the per-dim range.
+//           write c and s = sum v (the quantiser's exact int64 sum of q / s_d).
 // Consecutive items are the pairs of one line, so the CTAs working on them run
 // together and all but the first read the line from L2.  Every s32 class sum
 // is exact (|class sum| <= 3 2^14 P < 2^31 for P < 43690); the class-0 digit
@@ -47,7 +47,7 @@ namespace {
 constexpr int kCh = 32;             // pixels per chunk (one K-step)
 constexpr int kTile = 128;          // dims per tile
 constexpr int kThreads = 256;       // compute threads
-constexpr int kStages = 4;          // TMA ring depth
+constexpr int kStages = 5;          // TMA ring depth
 constexpr uint32_t kBox = kCh * kTile * 4;     // one 128-dim x 32-pixel fp32 box (16 KB)
 constexpr uint32_t kPlane = tc::kSliceBytes;   // 128 rows x 32 K int8 (4 KB)
 constexpr uint32_t kOps = 6 * kPlane;          // A digit planes 0-2, B digit planes 0-2
@@ -79,7 +79,8 @@ struct StatsI8TArgs {
     int npair;       // ntile (ntile + 1) / 2
     int nptile;      // 128-pixel tiles per line (v planes)
     double* stats;   // [line][c | s | S packed lower]
-    float* vmax;     // [line][D] max_p |fl32(x - c)| (may be null)
+    const float* cen;  // [line][D] centre c (range_kernel)
+    const float* vmax; // [line][D] max_p |fl32(x - c)|, NaN for a dim with a non-finite value (range_kernel)
     unsigned char* vplanes;  // [line][pixel tile][dim tile][3][16 KB] v digit planes (k_score_i8w), may be null
 };
 
@@ -95,9 +96,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8t_kernel(const __gri
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint32_t tmem_slot;
     __shared__ __align__(8) uint64_t full[kStages], empty[kStages], pfull[2], pempty[2], accfull, accempty;
-    __shared__ float mn_s[2][2][kTile], mx_s[2][2][kTile];   // [set A/B][pixel half][dim]
-    __shared__ double cs_s[2][2][kTile];                     // first-32-pixel sums
-    __shared__ float cen_s[2][kTile], scl_s[2][kTile], vmx_s[2][kTile];
+    __shared__ float cen_s[2][kTile], scl_s[2][kTile];
     __shared__ double inv_s[2][kTile];
     __shared__ long long sq_s[2][kTile];   // sum_p q per dim (diagonal items), per pixel half
     __shared__ int c0_s[2][kTile];         // sum_p d0^2 per dim (diagonal items), per pixel half
@@ -147,7 +146,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8t_kernel(const __gri
     };
 
     if (warp == 8) {
-        // ---------------- producer: for each item, pass 1 then pass 2 over its chunks (A box [+ B box])
+        // ---------------- producer: for each item its chunks (A box [+ B box])
         if (lane == 0) {
             int j = 0;
             for (int k = 0; k < my_items; ++k) {
@@ -155,8 +154,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8t_kernel(const __gri
                 item_geo(k, line, m0, n0, mr, nr);
                 const bool diag = m0 == n0;
                 const int r0 = line_row(line);
-                for (int pass = 0; pass < 2; ++pass)
-                    for (int c = 0; c < nch; ++c) {
+                for (int c = 0; c < nch; ++c) {
                         const int st = j % kStages;
                         if (j >= kStages) tc::mbar_wait(&empty[st], uint32_t(j / kStages - 1) & 1u);
                         tc::mbar_expect_tx(&full[st], diag ? kBox : 2 * kBox);
@@ -164,7 +162,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8t_kernel(const __gri
                         tma_load_2d(dst, &tmap, m0, r0 + c * kCh, &full[st]);
                         if (!diag) tma_load_2d(dst + kBox, &tmap, n0, r0 + c * kCh, &full[st]);
                         ++j;
-                    }
+                }
             }
         }
         return;
@@ -209,55 +207,21 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8t_kernel(const __gri
         item_geo(k, line, m0, n0, mr, nr);
         const bool diag = m0 == n0;
         const int nsets = diag ? 1 : 2;
-        // ---- pass 1: ranges (and the centre) of both dim sets
-        float lo[2] = {3.402823466e38f, 3.402823466e38f}, hi[2] = {-3.402823466e38f, -3.402823466e38f};
-        double cs[2] = {0.0, 0.0};
-        for (int c = 0; c < nch; ++c) {
-            const int st = j % kStages;
-            tc::mbar_wait(&full[st], uint32_t(j / kStages) & 1u);
-            ++j;
-            const float* box = reinterpret_cast<const float*>(ring + size_t(st) * 2 * kBox);
-            const int n = min(kCh, P - c * kCh);
-            for (int set = 0; set < nsets; ++set) {
-                const float* bx = box + set * (kBox / 4);
-#pragma unroll 4
-                for (int e = 0; e < 16; ++e) {
-                    const int p = h * 16 + e;
-                    if (p < n) {
-                        const float x = bx[p * kTile + d];
-                        lo[set] = fmin_nan(lo[set], x);
-                        hi[set] = fmaxf(hi[set], x);
-                        if (c == 0) cs[set] += double(x);
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
-        }
-        for (int set = 0; set < nsets; ++set) {
-            mn_s[set][h][d] = lo[set];
-            mx_s[set][h][d] = hi[set];
-            cs_s[set][h][d] = cs[set];
-        }
+        // ---- the centre and range of both dim sets (range_kernel, one pass over the line before)
         if (tid == 0) bad_s = 0;
         bar_compute();
         if (tid < nsets * kTile) {
             const int set = tid >> 7, dd = tid & (kTile - 1);
             const int rdim = (set == 0 ? m0 : n0) + dd, rcount = set == 0 ? mr : nr;
-            float cd = 0.f, sc = 0.f, m = 0.f;
+            float cd = 0.f, sc = 0.f;
             if (dd < rcount) {
-                const int n0c = min(32, P);
-                cd = float((cs_s[set][0][dd] + cs_s[set][1][dd]) / double(n0c));
-                const float l = fmin_nan(mn_s[set][0][dd], mn_s[set][1][dd]);
-                const float hh = fmaxf(mx_s[set][0][dd], mx_s[set][1][dd]);
-                if (!(isfinite(l) && isfinite(hh))) bad_s = 1;
-                m = fmaxf(hh - cd, cd - l);
+                cd = a.cen[size_t(line) * D + rdim];
+                const float m = a.vmax[size_t(line) * D + rdim];
+                if (!(m >= 0.f && m <= 3.402823466e38f)) bad_s = 1;  // a non-finite value in this dim
                 sc = i8::v_scale(m);
             }
-            (void)rdim;
             cen_s[set][dd] = cd;
             scl_s[set][dd] = sc;
-            vmx_s[set][dd] = m;
             inv_s[set][dd] = sc > 0.f ? 1.0 / double(sc) : 0.0;
         }
         bar_compute();
@@ -363,11 +327,39 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8t_kernel(const __gri
             const long long q = sq_s[0][tid] + sq_s[1][tid];
             out[m0 + tid] = double(cen_s[0][tid]) + poison;
             out[D + m0 + tid] = double(q) * inv_s[0][tid] + poison;
-            if (a.vmax) a.vmax[size_t(line) * D + m0 + tid] = vmx_s[0][tid];
         }
         bar_compute();  // cen_s / inv_s / sq_s / c0_s / bad_s are rewritten by the next item
     }
     if (warp == 0) tc::tmem_free<512>(tmem);
+}
+
+// Per (line, dim): the centre c = fp32(fp64 mean of the first min(32, P) pixels) (k_stats.cu's rule) and
+// the range max_p |fl32(x - c)| (NaN when the dim holds a non-finite value), one pass over the line.
+__global__ void __launch_bounds__(256) range_kernel(Geometry g, const float* __restrict__ x, int n, int in_stride,
+                                                    float* __restrict__ cen, float* __restrict__ vmax) {
+    const int line = blockIdx.x, D = g.D, P = g.P;
+    const float* xl = line_ptr(x, line, n, in_stride, g);
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+        const int n0 = min(32, P);
+        double cs = 0.0;
+        float lo = 3.402823466e38f, hi = -3.402823466e38f;
+        for (int p = 0; p < n0; ++p) {
+            const float v = __ldg(xl + size_t(p) * g.B + d);
+            cs += double(v);
+            lo = fmin_nan(lo, v);
+            hi = fmaxf(hi, v);
+        }
+#pragma unroll 8
+        for (int p = n0; p < P; ++p) {
+            const float v = __ldg(xl + size_t(p) * g.B + d);
+            lo = fmin_nan(lo, v);
+            hi = fmaxf(hi, v);
+        }
+        const float c = float(cs / double(n0));
+        const bool fin = isfinite(lo) && isfinite(hi);
+        cen[size_t(line) * D + d] = c;
+        vmax[size_t(line) * D + d] = fin ? fmaxf(hi - c, c - lo) : __int_as_float(0x7fc00000);
+    }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -390,7 +382,7 @@ bool stats_i8t_eligible(const Geometry& g) {
 }
 
 int launch_stats_i8t(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_streams,
-                     double* stats, float* vmax, unsigned char* vplanes, cudaStream_t st) {
+                     double* stats, float* cen, float* vmax, unsigned char* vplanes, cudaStream_t st) {
     auto encode = tensor_map_encoder();
     if (!encode) return 1;
     // the window's lines as one 2D tensor: rows = pixels of every (stream, line slot), B floats each
@@ -405,7 +397,8 @@ int launch_stats_i8t(const Geometry& g, const float* x, int n_per_stream, int in
     if (r != CUDA_SUCCESS) return 2;
     const int ntile = (g.D + kTile - 1) / kTile;
     StatsI8TArgs a{g, n_per_stream, in_stride, n_streams * n_per_stream, ntile, ntile * (ntile + 1) / 2,
-                   (g.P + kTile - 1) / kTile, stats, vmax, vplanes};
+                   (g.P + kTile - 1) / kTile, stats, cen, vmax, vplanes};
+    range_kernel<<<a.n_lines, 256, 0, st>>>(g, x, n_per_stream, in_stride, cen, vmax);
     const int items = a.n_lines * a.npair;
     const int grid = items < sm_count() ? items : sm_count();
     ensure_smem(stats_i8t_kernel, kSmem);
