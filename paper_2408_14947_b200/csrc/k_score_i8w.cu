@@ -46,23 +46,26 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* m) {
 }
 
 // ---------------------------------------------------------------------------
-// W planes of one line (one CTA per line, a thread per output row at a time)
+// W planes: one CTA per (line, 128-row tile), a thread per output row; the row's loads are issued 8 at
+// a time (independent partial maxima / sums) so the scattered reads of the packed column-major blocks
+// overlap
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) wplanes_w_kernel(Geometry g, const float* __restrict__ whiten,
-                                                        const double* __restrict__ stats,
-                                                        const double* __restrict__ prior,
-                                                        const float* __restrict__ vmax,
-                                                        unsigned char* __restrict__ wpl) {
+__global__ void __launch_bounds__(kT) wplanes_w_kernel(Geometry g, const float* __restrict__ whiten,
+                                                       const double* __restrict__ stats,
+                                                       const double* __restrict__ prior,
+                                                       const float* __restrict__ vmax,
+                                                       unsigned char* __restrict__ wpl) {
     __shared__ float isc[512];
     __shared__ double dcs[512];
-    const int line = blockIdx.x, tid = threadIdx.x;
     const int D = g.D, nt = n_tiles(D), Dt = nt * kT;
+    const int line = blockIdx.x / nt, ti = blockIdx.x - line * nt, tid = threadIdx.x;
     const int nblk = g.nb * (g.nb + 1) / 2;
     const float* W = whiten + size_t(line) * nblk * 64;
     auto w = [&](int i, int j) {  // W_ij from the packed column-major 8x8 blocks (j <= i < D)
         return __ldg(W + size_t(tri(i >> 3, j >> 3)) * 64 + (j & 7) * 8 + (i & 7));
     };
-    for (int d = tid; d < Dt; d += blockDim.x) {
+    const int jmax = min(Dt, (ti + 1) * kT);
+    for (int d = tid; d < jmax; d += kT) {
         float v = 0.f;
         double dc = 0.0;
         if (d < D) {
@@ -77,42 +80,53 @@ __global__ void __launch_bounds__(256) wplanes_w_kernel(Geometry g, const float*
     unsigned char* out = wpl + size_t(line) * wplw_bytes(D);
     float* invr = reinterpret_cast<float*>(out + size_t(nt) * (nt + 1) / 2 * kPair);
     float* wdc = invr + Dt;
-    for (int i = tid; i < Dt; i += blockDim.x) {
-        float mx = 0.f;
-        double cr[4] = {0.0, 0.0, 0.0, 0.0};
-        if (i < D)
-            for (int j = 0; j <= i; ++j) {
-                const float wv = w(i, j);
-                mx = fmaxf(mx, fabsf(wv * isc[j]));
-                cr[j & 3] += double(wv) * dcs[j];
-            }
-        const float r = (mx > 0.f && mx <= 3.402823466e38f) ? i8::kR / mx : 0.f;
-        invr[i] = r > 0.f ? 256.f / r : 0.f;
-        wdc[i] = float((cr[0] + cr[1]) + (cr[2] + cr[3]));
-        const int ti = i / kT, il = i - ti * kT;
-        for (int kt = 0; kt <= ti; ++kt) {
-            unsigned char* blk = out + size_t(ti * (ti + 1) / 2 + kt) * kPair;
-            for (int run = 0; run < kT / 16; ++run) {
-                uint32_t wd[3][4] = {{0u, 0u, 0u, 0u}, {0u, 0u, 0u, 0u}, {0u, 0u, 0u, 0u}};
-                const int j0 = kt * kT + run * 16;
-                if (i < D && j0 <= i) {
+    const int il = tid, i = ti * kT + il;
+    float mx[8];
+    double cr[8];
 #pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) {
-                        uint32_t u[4];
+    for (int u = 0; u < 8; ++u) {
+        mx[u] = 0.f;
+        cr[u] = 0.0;
+    }
+    if (i < D) {
+        for (int j0 = 0; j0 <= i; j0 += 8) {
+            float wv[8];
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int j = j0 + q4 * 4 + e;
-                            const float wv = j <= i ? w(i, j) * isc[j] : 0.f;
-                            u[e] = i8::quant_u(wv, r);
-                        }
-                        i8::pack_digits(u, wd[0][q4], wd[1][q4], wd[2][q4]);
-                    }
+            for (int u = 0; u < 8; ++u) wv[u] = (j0 + u <= i) ? w(i, j0 + u) : 0.f;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (j0 + u <= i) {
+                    mx[u] = fmaxf(mx[u], fabsf(wv[u] * isc[j0 + u]));
+                    cr[u] += double(wv[u]) * dcs[j0 + u];
                 }
-                const uint32_t off = tc::kmajor_off_s8(il, run * 16);
-#pragma unroll
-                for (int pl = 0; pl < 3; ++pl)
-                    *reinterpret_cast<uint4*>(blk + pl * kPl + off) = make_uint4(wd[pl][0], wd[pl][1], wd[pl][2], wd[pl][3]);
             }
+        }
+    }
+    const float m = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+    const float r = (m > 0.f && m <= 3.402823466e38f) ? i8::kR / m : 0.f;
+    invr[i] = r > 0.f ? 256.f / r : 0.f;
+    wdc[i] = float(((cr[0] + cr[1]) + (cr[2] + cr[3])) + ((cr[4] + cr[5]) + (cr[6] + cr[7])));
+    for (int kt = 0; kt <= ti; ++kt) {
+        unsigned char* blk = out + size_t(ti * (ti + 1) / 2 + kt) * kPair;
+        for (int run = 0; run < kT / 16; ++run) {
+            uint32_t wd[3][4] = {{0u, 0u, 0u, 0u}, {0u, 0u, 0u, 0u}, {0u, 0u, 0u, 0u}};
+            const int j0 = kt * kT + run * 16;
+            if (i < D && j0 <= i) {
+                float wv[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) wv[e] = (j0 + e <= i) ? w(i, j0 + e) * isc[j0 + e] : 0.f;
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    uint32_t u[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) u[e] = i8::quant_u(wv[q4 * 4 + e], r);
+                    i8::pack_digits(u, wd[0][q4], wd[1][q4], wd[2][q4]);
+                }
+            }
+            const uint32_t off = tc::kmajor_off_s8(il, run * 16);
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl)
+                *reinterpret_cast<uint4*>(blk + pl * kPl + off) = make_uint4(wd[pl][0], wd[pl][1], wd[pl][2], wd[pl][3]);
         }
     }
 }
@@ -136,6 +150,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8w_kernel(ScoreI8WArg
     __shared__ uint32_t tmem_slot;
     __shared__ __align__(8) uint64_t full[kStages], empty[kStages], accfull, accempty;
     __shared__ float red_s[3][128];
+    __shared__ float aux_s[2 * 512];  // the item's line: 256 / r_i, then (W (mu - c))_i
 
     const Geometry& g = a.g;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -232,9 +247,14 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8w_kernel(ScoreI8WArg
     for (int k = 0; k < my_items; ++k) {
         const int it = blockIdx.x + k * gridDim.x;
         const int line = it / a.nptile, t = it - line * a.nptile;
-        const float* invr = reinterpret_cast<const float*>(a.wplanes + size_t(line) * wpl_line +
-                                                           size_t(NT) * (NT + 1) / 2 * kPair);
-        const float* wdc = invr + NT * kT;
+        {  // the line's row factors / offsets into shared memory (read 16 per accumulator group below)
+            const float* src = reinterpret_cast<const float*>(a.wplanes + size_t(line) * wpl_line +
+                                                              size_t(NT) * (NT + 1) / 2 * kPair);
+            for (int q = tid; q < 2 * NT * kT; q += kThreads) aux_s[q] = __ldg(src + q);
+            bar_compute();
+        }
+        const float* invr = aux_s;
+        const float* wdc = aux_s + NT * kT;
         float d2 = 0.f;
         for (int nt = 0; nt < NT; ++nt, ++acc_i) {
             const int N = (min(kT, D - nt * kT) + 15) / 16 * 16;
@@ -251,7 +271,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8w_kernel(ScoreI8WArg
                     float m = fmaf(float(int(v[3][ii])), 256.f, float(int(v[2][ii])));
                     m = fmaf(m, 256.f, float(int(v[1][ii])));
                     m = fmaf(m, 256.f, float(int(v[0][ii])));
-                    m = fmaf(m, __ldg(invr + i), -__ldg(wdc + i));
+                    m = fmaf(m, invr[i], -wdc[i]);
                     d2 = fmaf(m, m, d2);
                 }
             }
@@ -280,7 +300,7 @@ bool score_i8w_eligible(const Geometry& g) { return !g.srp && g.D > 127 && g.D <
 
 void launch_wplanes_w(const Geometry& g, const float* whiten, const double* stats, const double* prior,
                       const float* vmax, int n_lines_total, unsigned char* wpl, cudaStream_t st) {
-    wplanes_w_kernel<<<n_lines_total, 256, 0, st>>>(g, whiten, stats, prior, vmax, wpl);
+    wplanes_w_kernel<<<n_lines_total * n_tiles(g.D), kT, 0, st>>>(g, whiten, stats, prior, vmax, wpl);
 }
 
 void launch_score_i8w(const Geometry& g, const unsigned char* vplanes, const unsigned char* wplanes, int n_lines_total,

@@ -131,7 +131,9 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8t_kernel(const __gri
     const uint32_t tmem = tmem_slot;
 
     auto item_geo = [&](int k, int& line, int& m0, int& n0, int& mr, int& nr) {
-        const int it = blockIdx.x + k * gridDim.x;
+        // last line first: the range pass just streamed the window in line order, so its last lines are
+        // the ones still in L2
+        const int it = n_items - 1 - (blockIdx.x + k * gridDim.x);
         line = it / a.npair;
         int mt, nt;
         pair_of(it - line * a.npair, mt, nt);
@@ -337,28 +339,62 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8t_kernel(const __gri
 // the range max_p |fl32(x - c)| (NaN when the dim holds a non-finite value), one pass over the line.
 __global__ void __launch_bounds__(256) range_kernel(Geometry g, const float* __restrict__ x, int n, int in_stride,
                                                     float* __restrict__ cen, float* __restrict__ vmax) {
-    const int line = blockIdx.x, D = g.D, P = g.P;
+    // thread = (4-dim quad, pixel group of 4): 16-byte loads, 8 rows in flight per thread
+    __shared__ float lo_s[4][256], hi_s[4][256];
+    __shared__ double cs_s[4][256];
+    const int line = blockIdx.x, D = g.D, P = g.P, B = g.B;
     const float* xl = line_ptr(x, line, n, in_stride, g);
-    for (int d = threadIdx.x; d < D; d += blockDim.x) {
-        const int n0 = min(32, P);
-        double cs = 0.0;
-        float lo = 3.402823466e38f, hi = -3.402823466e38f;
-        for (int p = 0; p < n0; ++p) {
-            const float v = __ldg(xl + size_t(p) * g.B + d);
-            cs += double(v);
-            lo = fmin_nan(lo, v);
-            hi = fmaxf(hi, v);
+    const int nq = B / 4, tid = threadIdx.x;
+    const int n0 = min(32, P);
+    for (int q0 = 0; q0 < nq; q0 += 64) {
+        const int q = q0 + (tid & 63), pg = tid >> 6;
+        float4 lo = make_float4(3.402823466e38f, 3.402823466e38f, 3.402823466e38f, 3.402823466e38f);
+        float4 hi = make_float4(-3.402823466e38f, -3.402823466e38f, -3.402823466e38f, -3.402823466e38f);
+        double cs[4] = {0.0, 0.0, 0.0, 0.0};
+        if (q < nq) {
+            for (int p0 = pg; p0 < P; p0 += 32) {
+                float4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int p = p0 + 4 * u;
+                    v[u] = p < P ? __ldg(reinterpret_cast<const float4*>(xl + size_t(p) * B) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int p = p0 + 4 * u;
+                    if (p < P) {
+                        lo.x = fmin_nan(lo.x, v[u].x); lo.y = fmin_nan(lo.y, v[u].y);
+                        lo.z = fmin_nan(lo.z, v[u].z); lo.w = fmin_nan(lo.w, v[u].w);
+                        hi.x = fmaxf(hi.x, v[u].x); hi.y = fmaxf(hi.y, v[u].y);
+                        hi.z = fmaxf(hi.z, v[u].z); hi.w = fmaxf(hi.w, v[u].w);
+                        if (p < n0) {
+                            cs[0] += double(v[u].x); cs[1] += double(v[u].y);
+                            cs[2] += double(v[u].z); cs[3] += double(v[u].w);
+                        }
+                    }
+                }
+            }
         }
-#pragma unroll 8
-        for (int p = n0; p < P; ++p) {
-            const float v = __ldg(xl + size_t(p) * g.B + d);
-            lo = fmin_nan(lo, v);
-            hi = fmaxf(hi, v);
+        const int ql = tid & 63;
+        lo_s[pg][4 * ql] = lo.x; lo_s[pg][4 * ql + 1] = lo.y; lo_s[pg][4 * ql + 2] = lo.z; lo_s[pg][4 * ql + 3] = lo.w;
+        hi_s[pg][4 * ql] = hi.x; hi_s[pg][4 * ql + 1] = hi.y; hi_s[pg][4 * ql + 2] = hi.z; hi_s[pg][4 * ql + 3] = hi.w;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cs_s[pg][4 * ql + e] = cs[e];
+        __syncthreads();
+        {
+            {
+                const int dd = tid, d = 4 * q0 + dd;
+                if (d < D) {
+                    const float l = fmin_nan(fmin_nan(lo_s[0][dd], lo_s[1][dd]), fmin_nan(lo_s[2][dd], lo_s[3][dd]));
+                    const float h = fmaxf(fmaxf(hi_s[0][dd], hi_s[1][dd]), fmaxf(hi_s[2][dd], hi_s[3][dd]));
+                    const float c = float(((cs_s[0][dd] + cs_s[1][dd]) + (cs_s[2][dd] + cs_s[3][dd])) / double(n0));
+                    const bool fin = isfinite(l) && isfinite(h);
+                    cen[size_t(line) * D + d] = c;
+                    vmax[size_t(line) * D + d] = fin ? fmaxf(h - c, c - l) : __int_as_float(0x7fc00000);
+                }
+            }
         }
-        const float c = float(cs / double(n0));
-        const bool fin = isfinite(lo) && isfinite(hi);
-        cen[size_t(line) * D + d] = c;
-        vmax[size_t(line) * D + d] = fin ? fmaxf(hi - c, c - lo) : __int_as_float(0x7fc00000);
+        __syncthreads();
     }
 }
 
