@@ -570,20 +570,24 @@ def secondary_measurements(pkg, args):
         norm = torch.empty_like(raw)
         lat = {}
         for mode in ("full", "srp"):
-            eng = pkg.Engine(pkg.ErxConfig(no_srp=mode == "full"), B, 1, 1)
-            for k in range(5):
-                eng.run_device(dev[k].data_ptr(), 1, P, raw.data_ptr(), norm.data_ptr())
-            eng.sync()
-            K = 50
-            eng.event_record(0)
-            for k in range(K):
-                eng.run_device(dev[k % 64].data_ptr(), 1, P, raw.data_ptr(), norm.data_ptr())
-            eng.event_record(1)
-            ms = eng.event_elapsed_ms(0, 1)
-            eng.sync()
-            lat[mode] = {"ms_per_line": ms / K}
-            eng.close()
-        out["latency"] = {"workload": "configs[0]: 384 px x 108 bands, window=1 (no lag), device-resident", **lat}
+            for graphs in (True, False):
+                eng = pkg.Engine(pkg.ErxConfig(no_srp=mode == "full"), B, 1, 1)
+                eng.set_graphs(graphs)
+                # the caller streams lines through a 4-slot device ring (the graph cache holds 8 windows)
+                for k in range(8):
+                    eng.run_device(dev[k % 4].data_ptr(), 1, P, raw.data_ptr(), norm.data_ptr())
+                eng.sync()
+                K = 64
+                eng.event_record(0)
+                for k in range(K):
+                    eng.run_device(dev[k % 4].data_ptr(), 1, P, raw.data_ptr(), norm.data_ptr())
+                eng.event_record(1)
+                ms = eng.event_elapsed_ms(0, 1)
+                eng.sync()
+                lat[mode + ("" if graphs else "_no_graph")] = {"ms_per_line": ms / K}
+                eng.close()
+        out["latency"] = {"workload": "configs[0]: 384 px x 108 bands, window=1 (no lag), device-resident, "
+                                      "one CUDA-graph launch per line (and kernel-by-kernel for comparison)", **lat}
     except Exception as ex:
         out["latency"] = {"error": repr(ex)}
     try:

@@ -171,6 +171,11 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
  * of a launch, else 256; 64, 128 or 256 force that CTA size (same results to
  * rounding; a tuning and test hook). */
 #define ERX_OPT_FACTOR_THREADS 5
+/* ERX_OPT_GRAPHS: 1 (default) erx_run_device captures a window's launches once
+ * per (input, output, size) into a CUDA graph and replays it as one launch (the
+ * single-stream lag-0 path: one launch per line); 0 launches kernel by kernel.
+ * Per-kernel profiling (erx_set_profiling) bypasses the graphs. */
+#define ERX_OPT_GRAPHS 6
 int erx_set_option(erx_engine* e, int option, int64_t value);
 int64_t erx_get_option(const erx_engine* e, int option);
 

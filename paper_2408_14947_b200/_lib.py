@@ -27,6 +27,7 @@ OPT_STATS_TENSOR = 2
 OPT_HOST_GROUPS = 3
 OPT_ASYNC_HOST = 4
 OPT_FACTOR_THREADS = 5
+OPT_GRAPHS = 6
 
 
 class ErxConfigC(C.Structure):

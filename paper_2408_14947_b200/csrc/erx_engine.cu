@@ -103,8 +103,20 @@ struct erx_engine {
     float* d_lines = nullptr;
     double* d_stats = nullptr;
     double* d_prior = nullptr;
-    double* d_state[2] = {nullptr, nullptr};
-    int cur = 0;
+    double* d_state[2] = {nullptr, nullptr};  // halves of one allocation (d_state[1] = d_state[0] + S * SE)
+    int cur = 0;                              // host mirror of d_meta->cur
+    erxk::WinMeta* d_meta = nullptr;          // device-resident window state (erx_kernels.cuh)
+    // CUDA graphs of the device path (erx_run_device): one captured window per (input, output, size) key
+    struct GraphEntry {
+        const float* x;
+        float* raw;
+        float* norm;
+        uint32_t n, P, in_stride;
+        cudaGraphExec_t exec;
+        uint64_t kernels;
+    };
+    std::vector<GraphEntry> graphs;
+    bool use_graphs = true;                   // ERX_OPT_GRAPHS
     double* d_work = nullptr;
     float* d_white = nullptr;
     float* d_raw = nullptr;
@@ -281,6 +293,8 @@ int configure(erx_engine* e, uint32_t P) {
     if (P == e->P && e->d_stats) return ERX_OK;
     CU(cudaStreamSynchronize(e->stream));
     free_window(e);
+    for (auto& ge : e->graphs) cudaGraphExecDestroy(ge.exec);  // they reference the old buffers
+    e->graphs.clear();
     e->P = P;
     Geometry& g = e->geo;
     g.P = int(P);
@@ -389,12 +403,10 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     const Geometry& g = e->geo;
     const int L = int(ns * n);
     const size_t l0 = size_t(s0) * n;
-    const long long line_base = (long long)(e->lines_seen) * e->S + (long long)(l0);
+    const erxk::StateRef sref{e->d_meta, e->d_state[0], size_t(e->S) * g.SE, size_t(s0) * g.SE};
     const float* xg = x + size_t(s0) * in_stride * g.P * g.B;
     double* stats = e->d_stats + l0 * (g.SE + g.D);
     double* prior = e->d_prior + l0 * g.SE;
-    const double* st_in = e->d_state[e->cur] + size_t(s0) * g.SE;
-    double* st_out = e->d_state[e->cur ^ 1] + size_t(s0) * g.SE;
     double* work = e->d_work ? e->d_work + l0 * 2 * size_t(g.Dp) * g.Dp : nullptr;
     float* white = e->d_white + l0 * e->white_stride;
     float* vcache = e->d_vcache ? e->d_vcache + l0 * size_t(g.D) * g.P : nullptr;
@@ -423,8 +435,8 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     });
     if (stats_rc) return fail(e, ERX_ERR_DEVICE, "stats_i8t: cannot encode the TMA tensor map");
     timed(e, ERX_KERNEL_SCAN, [&] {
-        erxk::launch_scan(g, stats, prior, st_in, st_out, int(ns), int(n), e->initialized ? 1 : 0, e->cfg.alpha,
-                          e->cfg.use_incremental, e->welford_n, e->stream, kblk);
+        erxk::launch_scan(g, stats, prior, sref, int(ns), int(n), e->cfg.alpha, e->cfg.use_incremental, e->stream,
+                          kblk);
     });
     if (!score) {  // background update only (erx_advance_device): statistics and the scan
         cudaError_t r = cudaGetLastError();
@@ -432,8 +444,9 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
         return ERX_OK;
     }
     timed(e, ERX_KERNEL_FACTOR, [&] {
-        erxk::launch_factor(g, prior, L, e->cfg.epsilon, work, white, status, e->d_latch, line_base, e->factor_prec,
-                            e->stream, e->d_fix, stats, tensor ? vmax : nullptr, kblk, e->factor_threads);
+        erxk::launch_factor(g, prior, L, e->cfg.epsilon, work, white, status, e->d_latch, e->d_meta, (long long)(e->S),
+                            (long long)(l0), e->factor_prec, e->stream, e->d_fix, stats, tensor ? vmax : nullptr, kblk,
+                            e->factor_threads);
     });
     if (e->small) {  // score + normalisation fused
         timed(e, ERX_KERNEL_SCORE, [&] {
@@ -454,10 +467,9 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     }
     {
         timed(e, ERX_KERNEL_FIXUP, [&] {
-            erxk::FixupArgs fa{g, xg, int(n), int(in_stride), stats, st_in, e->initialized ? 1 : 0, e->cfg.alpha,
-                               e->cfg.use_incremental, (long long)(e->welford_n), e->cfg.epsilon, e->d_fix, e->fix_cap,
-                               e->d_fixwork,
-                               rawg, normg, status, e->d_latch, line_base};
+            erxk::FixupArgs fa{g, xg, int(n), int(in_stride), stats, sref, e->cfg.alpha, e->cfg.use_incremental,
+                               e->cfg.epsilon, e->d_fix, e->fix_cap, e->d_fixwork, rawg, normg, status, e->d_latch,
+                               (long long)(e->S), (long long)(l0)};
             erxk::launch_fixup(fa, L, e->stream);
         });
     }
@@ -466,7 +478,12 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     return ERX_OK;
 }
 
-// The window's state transition, once all of its stream groups are enqueued.
+// The window's state transition, once all of its stream groups are enqueued: on the device (the next
+// window's kernels read it) and in the host mirror.
+void enqueue_advance(erx_engine* e, uint32_t n) {
+    erxk::launch_window_advance(e->d_meta, int(n), (long long)(e->P), e->cfg.use_incremental, e->stream);
+    e->launches += 1;
+}
 void commit_window(erx_engine* e, uint32_t n) {
     e->cur ^= 1;
     if (e->cfg.use_incremental) e->welford_n += int64_t(n) * e->P;
@@ -559,6 +576,50 @@ int drain_pending(erx_engine* e) {
 // for the scores and queues them, with ERX_OPT_ASYNC_HOST the window stays in
 // flight (its copy-in then overlaps the previous window's kernels and result
 // copies) until erx_ready / erx_pop / erx_finish harvest it.
+// One window of the device path.  Every per-window value the kernels need is either a buffer pointer
+// (fixed for a given input / output) or in the device-resident window state, so the window's launches
+// (6-8 kernels and the state advance) are captured once per (input, output, size) into a CUDA graph
+// and replayed as ONE launch: the single-stream lag-0 path costs one graph launch per line — the host
+// path's windows always qualify (fixed staging buffers), device-path callers when they reuse a few
+// buffers (an 8-entry cache) (ERX_OPT_GRAPHS; off while per-kernel profiling is on).
+int run_device_window(erx_engine* e, const float* d_lines, uint32_t n, uint32_t in_stride, float* d_raw,
+                      float* d_norm) {
+    if (!e->use_graphs || e->profiling) {
+        if (int st = enqueue_window(e, d_lines, n, in_stride, d_raw, d_norm, 0, e->S)) return st;
+        enqueue_advance(e, n);
+        return ERX_OK;
+    }
+    for (auto& ge : e->graphs)
+        if (ge.x == d_lines && ge.raw == d_raw && ge.norm == d_norm && ge.n == n && ge.P == e->P &&
+            ge.in_stride == in_stride) {
+            CU(cudaGraphLaunch(ge.exec, e->stream));
+            e->launches += ge.kernels;
+            return ERX_OK;
+        }
+    const uint64_t k0 = e->launches;
+    CU(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+    int st = enqueue_window(e, d_lines, n, in_stride, d_raw, d_norm, 0, e->S);
+    if (!st) enqueue_advance(e, n);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(e->stream, &graph);
+    if (st) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    if (ce != cudaSuccess) return fail(e, ERX_ERR_DEVICE, std::string("graph capture: ") + cudaGetErrorString(ce));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) return fail(e, ERX_ERR_DEVICE, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+    if (e->graphs.size() >= 8) {  // a small cache: callers cycle through a few buffers
+        cudaGraphExecDestroy(e->graphs.front().exec);
+        e->graphs.erase(e->graphs.begin());
+    }
+    e->graphs.push_back({d_lines, d_raw, d_norm, n, e->P, in_stride, exec, e->launches - k0});
+    CU(cudaGraphLaunch(exec, e->stream));
+    return ERX_OK;
+}
+
 int run_host_window_body(erx_engine* e, const float* src, size_t src_pitch);
 
 // Any failure inside a host window leaves the engine failed with the window dropped (its lines
@@ -594,7 +655,9 @@ int run_host_window_body(erx_engine* e, const float* src, size_t src_pitch) {
         CU(cudaEventRecord(e->ev_in[gi], e->h2d));
         CU(cudaStreamWaitEvent(e->stream, e->ev_in[gi], 0));
         if (pg) CU(cudaStreamWaitEvent(e->stream, e->ev_d2h[prev], 0));
-        int st = enqueue_window(e, e->d_lines, n, e->T, e->d_raw, e->d_norm, s0, ns);
+        // one group: the whole window (and the state advance) as one replayable graph
+        int st = G == 1 ? run_device_window(e, e->d_lines, n, e->T, e->d_raw, e->d_norm)
+                        : enqueue_window(e, e->d_lines, n, e->T, e->d_raw, e->d_norm, s0, ns);
         if (st) return st;
         CU(cudaEventRecord(e->ev_out[gi], e->stream));
         CU(cudaStreamWaitEvent(e->d2h, e->ev_out[gi], 0));
@@ -606,6 +669,7 @@ int run_host_window_body(erx_engine* e, const float* src, size_t src_pitch) {
         CU(cudaMemcpyAsync(blk->status + l0, e->d_status + l0, nl * sizeof(int), cudaMemcpyDeviceToHost, e->d2h));
         CU(cudaEventRecord(e->ev_d2h[gi], e->d2h));
     }
+    if (G > 1) enqueue_advance(e, n);
     commit_window(e, n);
     e->prev_groups = int(G);
     PendingWindow pw;
@@ -721,11 +785,12 @@ int erx_create(const erx_config* cfg, uint32_t bands, uint32_t n_streams, uint32
         cudaMemcpy(e->d_srp_sign, sign.data(), sign.size() * sizeof(float), cudaMemcpyHostToDevice);
     }
     const int SE = e->D + e->D * (e->D + 1) / 2;
-    for (int k = 0; k < 2; ++k) {
-        if (cudaMalloc(&e->d_state[k], size_t(n_streams) * SE * sizeof(double)) != cudaSuccess)
-            return bail("cudaMalloc (state)");
-        cudaMemset(e->d_state[k], 0, size_t(n_streams) * SE * sizeof(double));
-    }
+    if (cudaMalloc(&e->d_state[0], 2 * size_t(n_streams) * SE * sizeof(double)) != cudaSuccess)
+        return bail("cudaMalloc (state)");
+    cudaMemset(e->d_state[0], 0, 2 * size_t(n_streams) * SE * sizeof(double));
+    e->d_state[1] = e->d_state[0] + size_t(n_streams) * SE;
+    if (cudaMalloc(&e->d_meta, sizeof(erxk::WinMeta)) != cudaSuccess) return bail("cudaMalloc (meta)");
+    cudaMemset(e->d_meta, 0, sizeof(erxk::WinMeta));
     if (cudaMalloc(&e->d_latch, 4 * sizeof(unsigned long long)) != cudaSuccess) return bail("cudaMalloc (latch)");
     cudaMemset(e->d_latch, 0, 4 * sizeof(unsigned long long));
     for (auto& ev : e->user_ev) cudaEventCreate(&ev);
@@ -750,7 +815,9 @@ void erx_destroy(erx_engine* e) {
     cudaFree(e->d_srp_band);
     cudaFree(e->d_srp_sign);
     cudaFree(e->d_state[0]);
-    cudaFree(e->d_state[1]);
+    cudaFree(e->d_meta);
+    for (auto& ge : e->graphs) cudaGraphExecDestroy(ge.exec);
+    e->graphs.clear();
     cudaFree(e->d_latch);
     for (auto& t : e->timings) {
         cudaEventDestroy(t.a);
@@ -909,7 +976,7 @@ int erx_run_device(erx_engine* e, int64_t first_index, uint32_t n_lines, uint32_
     if (e->fill) return fail(e, ERX_ERR_STATE, "host lines pending; call erx_finish first");
     int st = configure(e, pixels);
     if (st) return st;
-    st = enqueue_window(e, d_lines, n_lines, n_lines, d_raw, d_norm, 0, e->S);
+    st = run_device_window(e, d_lines, n_lines, n_lines, d_raw, d_norm);
     if (st) return st;
     commit_window(e, n_lines);
     return ERX_OK;
@@ -929,6 +996,7 @@ int erx_advance_device(erx_engine* e, int64_t first_index, uint32_t n_lines, uin
     if (st) return st;
     st = enqueue_window(e, d_lines, n_lines, n_lines, nullptr, nullptr, 0, e->S, /*score=*/false);
     if (st) return st;
+    enqueue_advance(e, n_lines);
     commit_window(e, n_lines);
     return ERX_OK;
 }
@@ -994,6 +1062,8 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
     e->initialized = true;
     e->lines_seen = lines_seen;
     e->welford_n = welford_n;
+    const erxk::WinMeta m{lines_seen, welford_n, 1, e->cur};
+    CU(cudaMemcpy(e->d_meta, &m, sizeof(m), cudaMemcpyHostToDevice));
     return ERX_OK;
 }
 
@@ -1005,6 +1075,11 @@ int64_t erx_rescued_lines(erx_engine* e) {
 }
 
 int erx_set_option(erx_engine* e, int option, int64_t value) {
+    if (!e->graphs.empty()) {  // captured windows bake in the current options
+        cudaStreamSynchronize(e->stream);
+        for (auto& ge : e->graphs) cudaGraphExecDestroy(ge.exec);
+        e->graphs.clear();
+    }
     if (option == ERX_OPT_ASYNC_HOST) {
         if (value != 0 && value != 1) return fail(e, ERX_ERR_CONFIG, "async host: 0 or 1");
         if (!value)
@@ -1016,6 +1091,11 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
         if (value != 0 && value != 64 && value != 128 && value != 256)
             return fail(e, ERX_ERR_CONFIG, "factor threads: 0, 64, 128 or 256");
         e->factor_threads = int(value);
+        return ERX_OK;
+    }
+    if (option == ERX_OPT_GRAPHS) {
+        if (value != 0 && value != 1) return fail(e, ERX_ERR_CONFIG, "graphs: 0 or 1");
+        e->use_graphs = value != 0;
         return ERX_OK;
     }
     if (option == ERX_OPT_HOST_GROUPS) {
@@ -1054,6 +1134,7 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
 int64_t erx_get_option(const erx_engine* e, int option) {
     if (option == ERX_OPT_FACTOR_PRECISION) return e->d_stats ? e->factor_prec : e->factor_req;
     if (option == ERX_OPT_HOST_GROUPS) return e->host_groups;
+    if (option == ERX_OPT_GRAPHS) return e->use_graphs ? 1 : 0;
     if (option == ERX_OPT_FACTOR_THREADS) return e->factor_threads;
     if (option == ERX_OPT_ASYNC_HOST) return e->async_host ? 1 : 0;
     if (option == ERX_OPT_STATS_TENSOR) {

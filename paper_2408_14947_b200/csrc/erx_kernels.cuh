@@ -45,6 +45,26 @@ struct Geometry {
     int srp_nnz;           // nonzeros of W
 };
 
+// Per-engine window state, resident on the device so a captured window (CUDA graph) replays without
+// host-side parameters: the scan, factor and rescue read it, window_advance_kernel moves it on.
+struct WinMeta {
+    long long lines_seen;  // lines per stream before this window
+    long long welford_n;   // pixels folded into the background (incremental mode)
+    int initialized;       // the background exists (else the window's first line initialises it)
+    int cur;               // which half of the ping-pong state holds the background
+};
+// The window's background: state_base + cur * state_stride (+ stream group offset); the scan writes the
+// other half.
+struct StateRef {
+    const WinMeta* meta;
+    double* base;
+    size_t stride;   // doubles per half (S * SE)
+    size_t offset;   // the stream group's first element (s0 * SE)
+    __host__ __device__ const double* in() const { return base + size_t(meta->cur) * stride + offset; }
+    __host__ __device__ double* out() const { return base + size_t(meta->cur ^ 1) * stride + offset; }
+};
+void launch_window_advance(WinMeta* meta, int n_lines, long long pixels_per_line, int incremental, cudaStream_t st);
+
 struct StatsLaunch {
     int CH;          // pixels staged per chunk
     int n_pairs;     // lower-triangular 8x8 block pairs
@@ -129,18 +149,18 @@ void launch_stats(const Geometry& g, const StatsLaunch& sl, const float* x, int 
                   int n_lines_total, double* stats, cudaStream_t st);
 // kblk (may be null): write the pre-update covariance as fp32 packed lower 8x8 blocks (row-major
 // inside a block, nb(nb+1)/2 * 64 floats per line) instead of fp64 into prior (the mean stays fp64).
-void launch_scan(const Geometry& g, const double* stats, double* prior, const double* state_in, double* state_out,
-                 int n_streams, int n_per_stream, int initialized, double alpha, int incremental, int64_t n_seen0,
-                 cudaStream_t st, float* kblk = nullptr);
+void launch_scan(const Geometry& g, const double* stats, double* prior, StateRef state, int n_streams,
+                 int n_per_stream, double alpha, int incremental, cudaStream_t st, float* kblk = nullptr);
 // latch: {flag, line, pivot} of the first factorisation failure (sticky until the host clears it).
 // vmax != null (precision 32 only): write the tensor path's int8 W planes (k_factor.cu: write_wplanes,
 // i8::kWBytes per line) instead of the fp32 blocks.  The fp32 factors (precision 32 / 31) put lines
 // they cannot take (failed or ill-conditioned pivot) on fixlist for launch_fixup instead of
 // escalating eps in fp32; the fp64 ones escalate and latch themselves.
+// line ids in the latch: meta->lines_seen * line_mult + line_off + line (streams x window rows)
 void launch_factor(const Geometry& g, const double* prior, int n_lines_total, double eps0, double* work,
-                   float* whiten, int* status, unsigned long long* latch, long long line_base, int precision,
-                   cudaStream_t st, int* fixlist, const double* stats = nullptr, const float* vmax = nullptr,
-                   const float* kblk = nullptr, int blk_threads = 0);
+                   float* whiten, int* status, unsigned long long* latch, const WinMeta* meta, long long line_mult,
+                   long long line_off, int precision, cudaStream_t st, int* fixlist, const double* stats = nullptr,
+                   const float* vmax = nullptr, const float* kblk = nullptr, int blk_threads = 0);
 
 // fp64 rescue of the lines on the fp32 factor's list (k_fixup.cu): background, factor with eps
 // escalation, whitening and normalisation of every listed line redone in fp64 from the line and the
@@ -151,11 +171,9 @@ struct FixupArgs {
     int n;
     int in_stride;
     const double* stats;     // [L][SE + D] the window's line statistics (k_stats.cu contract)
-    const double* st_in;     // [S][SE] background at the window start
-    int initialized;
+    StateRef state;          // background at the window start (+ initialized / welford count in its meta)
     double alpha;
     int incremental;
-    long long n_seen0;
     double eps0;
     int* list;               // [0] count, [1] CTAs done, [2 .. list_cap + 1] listed lines, [list_cap + 2] total
     int list_cap;
@@ -164,7 +182,7 @@ struct FixupArgs {
     float* norm;
     int* status;
     unsigned long long* latch;
-    long long line_base;
+    long long line_mult, line_off;  // latch line id = meta->lines_seen * line_mult + line_off + line
 };
 int fixup_ctas(const Geometry& g, int n_lines_total);
 size_t fixup_work_doubles(const Geometry& g, int n_lines_total);

@@ -121,7 +121,8 @@ __device__ void write_wplanes(unsigned char* __restrict__ planes, int line, cons
 __global__ void __launch_bounds__(256) factor_global_kernel(Geometry g, const double* __restrict__ prior, double eps0,
                                                      double* __restrict__ work, float* __restrict__ whiten,
                                                      int* __restrict__ status, unsigned long long* __restrict__ latch,
-                                                     long long line_base) {
+                                                     const WinMeta* __restrict__ meta, long long line_mult,
+                                                     long long line_off) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_fail;
     const int line = blockIdx.x;
@@ -151,7 +152,7 @@ __global__ void __launch_bounds__(256) factor_global_kernel(Geometry g, const do
         if (tid == 0) {
             status[line] = fail;
             if (atomicCAS(latch, 0ull, 1ull) == 0ull) {
-                latch[1] = static_cast<unsigned long long>(line_base + line);
+                latch[1] = static_cast<unsigned long long>(meta->lines_seen * line_mult + line_off + line);
                 latch[2] = static_cast<unsigned long long>(fail);
             }
         }
@@ -475,7 +476,9 @@ __global__ void __launch_bounds__(256) factor_big_kernel(Geometry g, const doubl
 template <typename T>
 __global__ void __launch_bounds__(256) factor_smem_kernel(Geometry g, const double* __restrict__ prior, double eps0,
                                                           float* __restrict__ whiten, int* __restrict__ status,
-                                                          unsigned long long* __restrict__ latch, long long line_base) {
+                                                          unsigned long long* __restrict__ latch,
+                                                          const WinMeta* __restrict__ meta, long long line_mult,
+                                                          long long line_off) {
     extern __shared__ __align__(16) unsigned char smem[];
     T* A = reinterpret_cast<T*>(smem);
     const int D = g.D, LD = D + 1;  // odd leading dimension: conflict-free column walks
@@ -515,7 +518,7 @@ __global__ void __launch_bounds__(256) factor_smem_kernel(Geometry g, const doub
         if (tid == 0) {
             status[line] = fail;
             if (atomicCAS(latch, 0ull, 1ull) == 0ull) {
-                latch[1] = static_cast<unsigned long long>(line_base + line);
+                latch[1] = static_cast<unsigned long long>(meta->lines_seen * line_mult + line_off + line);
                 latch[2] = static_cast<unsigned long long>(fail);
             }
         }
@@ -1230,9 +1233,9 @@ int factor_precision(const Geometry& g, int requested, int lines_per_launch) {
 }
 
 void launch_factor(const Geometry& g, const double* prior, int n_lines_total, double eps0, double* work,
-                   float* whiten, int* status, unsigned long long* latch, long long line_base, int precision,
-                   cudaStream_t st, int* fixlist, const double* stats, const float* vmax, const float* kblk,
-                   int blk_threads) {
+                   float* whiten, int* status, unsigned long long* latch, const WinMeta* meta, long long line_mult,
+                   long long line_off, int precision, cudaStream_t st, int* fixlist, const double* stats,
+                   const float* vmax, const float* kblk, int blk_threads) {
     const size_t sm = factor_smem(g, precision);
     if (precision == 32) {
         ensure_smem(factor_blk_kernel<64, 7>, sm);
@@ -1260,7 +1263,8 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
                                                                    vmax, kblk);
     } else if (precision == 64) {
         ensure_smem(factor_smem_kernel<double>, sm);
-        factor_smem_kernel<double><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, line_base);
+        factor_smem_kernel<double><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, latch, meta,
+                                                                    line_mult, line_off);
     } else if (precision == 30) {
         const int cl = factor_cl_size(g);
         cudaLaunchConfig_t cfg = {};
@@ -1291,8 +1295,8 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
                                                           status, fixlist, factor_big_xk(g));
     } else {
         ensure_smem(factor_global_kernel, sm);
-        factor_global_kernel<<<n_lines_total, 256, sm, st>>>(g, prior, eps0, work, whiten, status, latch,
-                                                               line_base);
+        factor_global_kernel<<<n_lines_total, 256, sm, st>>>(g, prior, eps0, work, whiten, status, latch, meta,
+                                                               line_mult, line_off);
     }
 }
 

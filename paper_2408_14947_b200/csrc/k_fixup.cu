@@ -50,12 +50,14 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(FixupArgs a) {
     double* mu = reinterpret_cast<double*>(smem);   // [Dp]
     double* dyn = mu + Dp;                          // factor / inverse / scoring scratch
     const int count = a.list[0];
+    const int initialized = a.state.meta->initialized;
+    const long long n_seen0 = a.state.meta->welford_n;
     const double Pd = double(g.P), invP = 1.0 / Pd, invP1 = 1.0 / (Pd - 1.0), om = 1.0 - a.alpha;
     for (int q = blockIdx.x; q < count; q += gridDim.x) {
         const int line = a.list[2 + q];
         const int s = line / a.n, t = line - s * a.n;
         // ---- 1. pre-update background of line (s, t)
-        const double* in = a.st_in + size_t(s) * SE;
+        const double* in = a.state.in() + size_t(s) * SE;
         for (int e = tid; e < SE; e += nt) {
             const ScanElem el = scan_elem(D, e);
             double pr = 0.0;
@@ -64,7 +66,7 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(FixupArgs a) {
                 for (int u = 0; u <= t; ++u) {
                     const double* st = a.stats + (size_t(s) * a.n + u) * SS;
                     const double cur = finish_stat(el.is_mu, st[el.o0], st[el.o1], st[el.o2], invP, invP1);
-                    if (!a.initialized && u == 0) {
+                    if (!initialized && u == 0) {
                         pr = cur;
                         state = cur;
                     } else {
@@ -74,13 +76,13 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(FixupArgs a) {
                 }
             } else {
                 const bool is_cov = !el.is_mu;
-                WelfordElem w{in[el.a], in[el.b], is_cov ? in[e] : 0.0, double(a.n_seen0)};
+                WelfordElem w{in[el.a], in[el.b], is_cov ? in[e] : 0.0, double(n_seen0)};
                 for (int u = 0; u <= t; ++u) {
                     const double* st = a.stats + (size_t(s) * a.n + u) * SS;
                     const double mha = finish_stat(true, st[el.a], st[D + el.a], 0.0, invP, invP1);
                     const double mhb = finish_stat(true, st[el.b], st[D + el.b], 0.0, invP, invP1);
                     const double kh = is_cov ? finish_stat(false, st[el.o0], st[el.o1], st[el.o2], invP, invP1) : 0.0;
-                    if (!a.initialized && u == 0) {
+                    if (!initialized && u == 0) {
                         w.ma = mha;
                         w.mb = mhb;
                         if (is_cov) w.cov = kh;
@@ -99,7 +101,7 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(FixupArgs a) {
         }
         __syncthreads();
         const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
-        if (!a.initialized && t == 0) {
+        if (!initialized && t == 0) {
             // the initialising line is its own background (erx.hpp:54-55): its statistics straight
             // from the line in fp64 (line_stats, erx.hpp:38-40), not from the stats kernel's
             // centred / quantised sums — a two-pixel line scored against itself then has exactly
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(FixupArgs a) {
             if (tid == 0) {
                 a.status[line] = fail;
                 if (atomicCAS(a.latch, 0ull, 1ull) == 0ull) {
-                    a.latch[1] = static_cast<unsigned long long>(a.line_base + line);
+                    a.latch[1] = static_cast<unsigned long long>(a.state.meta->lines_seen * a.line_mult + a.line_off + line);
                     a.latch[2] = static_cast<unsigned long long>(fail);
                 }
             }

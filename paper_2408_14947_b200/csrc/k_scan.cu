@@ -13,10 +13,12 @@ namespace erxk {
 namespace {
 
 __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __restrict__ stats,
-                                                   double* __restrict__ prior, const double* __restrict__ st_in,
-                                                   double* __restrict__ st_out, int n, int initialized,
-                                                   double alpha, int incremental, int64_t n_seen0,
-                                                   float* __restrict__ kblk) {
+                                                   double* __restrict__ prior, StateRef sref, int n, double alpha,
+                                                   int incremental, float* __restrict__ kblk) {
+    const double* __restrict__ st_in = sref.in();
+    double* __restrict__ st_out = sref.out();
+    const int initialized = sref.meta->initialized;
+    const long long n_seen0 = sref.meta->welford_n;
     const int s = blockIdx.y;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= g.SE) return;
@@ -127,9 +129,11 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
 // ---------------------------------------------------------------------------
 template <int TC, int NTH, int kU>
 __global__ void __launch_bounds__(NTH) scan_chunk_kernel(Geometry g, const double* __restrict__ stats,
-                                                         double* __restrict__ prior, const double* __restrict__ st_in,
-                                                         double* __restrict__ st_out, int n, int initialized,
+                                                         double* __restrict__ prior, StateRef sref, int n,
                                                          double alpha, float* __restrict__ kblk) {
+    const double* __restrict__ st_in = sref.in();
+    double* __restrict__ st_out = sref.out();
+    const int initialized = sref.meta->initialized;
     extern __shared__ __align__(16) unsigned char smem[];
     double* kh = reinterpret_cast<double*>(smem);  // [2][TC][32] finished line statistics
     double* ps = kh + 2 * TC * 32;                 // [2][TC][32] pre-update background
@@ -225,11 +229,21 @@ __global__ void __launch_bounds__(NTH) scan_chunk_kernel(Geometry g, const doubl
     if (warp == 0 && lane < ne) st_out[size_t(s) * g.SE + e0 + lane] = state;
 }
 
+__global__ void window_advance_kernel(WinMeta* meta, int n_lines, long long pixels_per_line, int incremental) {
+    meta->lines_seen += n_lines;
+    if (incremental) meta->welford_n += (long long)(n_lines) * pixels_per_line;
+    meta->initialized = 1;
+    meta->cur ^= 1;
+}
+
 }  // namespace
 
-void launch_scan(const Geometry& g, const double* stats, double* prior, const double* state_in, double* state_out,
-                 int n_streams, int n_per_stream, int initialized, double alpha, int incremental, int64_t n_seen0,
-                 cudaStream_t st, float* kblk) {
+void launch_window_advance(WinMeta* meta, int n_lines, long long pixels_per_line, int incremental, cudaStream_t st) {
+    window_advance_kernel<<<1, 1, 0, st>>>(meta, n_lines, pixels_per_line, incremental);
+}
+
+void launch_scan(const Geometry& g, const double* stats, double* prior, StateRef state, int n_streams,
+                 int n_per_stream, double alpha, int incremental, cudaStream_t st, float* kblk) {
     const int blocks_plain = (g.SE + 127) / 128 * n_streams;
     // (configs[3] on one GPU's share of 8: 376 plain blocks, T = 256 -> chunked 0.074 vs 0.092 ms;
     // shares of 4 and 2 (752 / 1504 blocks) stay faster element-parallel)
@@ -240,19 +254,16 @@ void launch_scan(const Geometry& g, const double* stats, double* prior, const do
         if (ctas <= sm_count()) {
             const size_t sm = 2 * size_t(2) * 192 * 32 * sizeof(double);
             ensure_smem(scan_chunk_kernel<192, 512, 13>, sm);  // 6144 items per chunk: one batch per thread
-            scan_chunk_kernel<192, 512, 13><<<grid, 512, sm, st>>>(g, stats, prior, state_in, state_out, n_per_stream,
-                                                           initialized, alpha, kblk);
+            scan_chunk_kernel<192, 512, 13><<<grid, 512, sm, st>>>(g, stats, prior, state, n_per_stream, alpha, kblk);
         } else {
             const size_t sm = 2 * size_t(2) * 32 * 32 * sizeof(double);
             ensure_smem(scan_chunk_kernel<32, 256, 5>, sm);  // 1024 items per chunk
-            scan_chunk_kernel<32, 256, 5><<<grid, 256, sm, st>>>(g, stats, prior, state_in, state_out, n_per_stream,
-                                                         initialized, alpha, kblk);
+            scan_chunk_kernel<32, 256, 5><<<grid, 256, sm, st>>>(g, stats, prior, state, n_per_stream, alpha, kblk);
         }
         return;
     }
     dim3 grid((g.SE + 127) / 128, n_streams);
-    scan_kernel<<<grid, 128, 0, st>>>(g, stats, prior, state_in, state_out, n_per_stream, initialized, alpha,
-                                      incremental, n_seen0, kblk);
+    scan_kernel<<<grid, 128, 0, st>>>(g, stats, prior, state, n_per_stream, alpha, incremental, kblk);
 }
 
 }  // namespace erxk

@@ -284,6 +284,10 @@ class Engine:
         """Stream groups per host window (0 auto; see ERX_OPT_HOST_GROUPS)."""
         self._check(self._lib.erx_set_option(self._h, L.OPT_HOST_GROUPS, int(groups)))
 
+    def set_graphs(self, on: bool):
+        """Replay erx_run_device windows as CUDA graphs (ERX_OPT_GRAPHS, default on)."""
+        self._check(self._lib.erx_set_option(self._h, L.OPT_GRAPHS, int(bool(on))))
+
     def set_async_host(self, on: bool):
         """Pipelined host path (ERX_OPT_ASYNC_HOST): push returns once the input is on the device;
         windows are harvested by ready / pop / finish."""

@@ -588,3 +588,31 @@ def test_window_partition_bitwise(pkg, cid, S, n, P, windows, factor):
             ref = (raw, norm)
         else:
             assert np.array_equal(raw, ref[0]) and np.array_equal(norm, ref[1]), f"window {T}"
+
+
+def test_graph_replay_matches_launches(pkg):
+    """ERX_OPT_GRAPHS: a window captured once and replayed as a CUDA graph (device-resident window
+    state: background half, line count, Welford count, initialisation) gives the same bits as
+    kernel-by-kernel launches, across windows that reuse and alternate buffers, lag 0 and lag 8."""
+    import torch
+
+    spec = pkg.gen_spec(3, 2)
+    x = torch.from_numpy(pkg.gen_lines(spec, 0, 24)[0]).cuda()
+    for T, incremental in ((1, False), (8, False), (8, True)):
+        outs = []
+        for graphs in (False, True):
+            eng = pkg.Engine(pkg.ErxConfig(no_srp=True, use_incremental=incremental), 108, window_lines=T)
+            eng.set_graphs(graphs)
+            bufs = [torch.empty((T, 640), dtype=torch.float32, device="cuda") for _ in range(4)]
+            res = []
+            for w in range(24 // T):
+                r, nn = bufs[(2 * w) % 4], bufs[(2 * w + 1) % 4]  # two alternating output pairs
+                eng.run_device(x[w * T:(w + 1) * T].data_ptr(), T, 640, r.data_ptr(), nn.data_ptr(), first_index=w * T)
+                eng.sync()
+                res.append((r.cpu().numpy().copy(), nn.cpu().numpy().copy()))
+            st = eng.state()
+            outs.append((res, st.cov.copy(), st.lines_seen, st.welford_n))
+            eng.close()
+        for (a, b) in zip(outs[0][0], outs[1][0]):
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), (T, incremental)
+        assert np.array_equal(outs[0][1], outs[1][1]) and outs[0][2:] == outs[1][2:]
