@@ -327,10 +327,11 @@ def run_ours(args):
                     "scaling": "strong", "vs_baseline": None, "dry_run": True, "config": config,
                     "gather": gathered, "gpu_launches": 0, "gen_seconds": gen_s,
                     "data": "synthetic: BASELINE.json generator; CPU stub engine (no kernels)"}
-            print(json.dumps(line), flush=True)
         if dist:
             dist.barrier()
             dist.destroy_process_group()
+        if rank == 0:
+            print(json.dumps(line), flush=True)
         return
 
     # per-kernel device time (CUDA events on the engine stream), separate pass
@@ -475,10 +476,12 @@ def run_ours(args):
             "cpu_baseline": cpu, "gen_seconds": gen_s,
         }
         line.update(extra)
-        print(json.dumps(line), flush=True)
-    if dist:
+    if dist:  # tear the communicator down first: NCCL's own log lines must not follow the JSON line
         dist.barrier()
         dist.destroy_process_group()
+    if rank == 0:
+        sys.stdout.flush()
+        print(json.dumps(line), flush=True)
 
 
 def secondary_measurements(pkg, args):

@@ -46,84 +46,97 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* m) {
 }
 
 // ---------------------------------------------------------------------------
-// W planes: one CTA per (line, 128-row tile), a thread per output row; the row's loads are issued 8 at
-// a time (independent partial maxima / sums) so the scattered reads of the packed column-major blocks
-// overlap
+// W planes: one CTA per (line, 128-row tile), a thread per output row.  The row tile's W blocks are
+// staged 128 x 128 at a time (one dim tile kt) into a dense shared-memory tile with coalesced 16-byte
+// loads of the packed column-major 8x8 blocks: pass A over every kt gives each row's scale r_i and
+// (W dc)_i, pass B stages the tiles again and writes the int8 digit planes.
 // ---------------------------------------------------------------------------
+constexpr int kWLd = kT + 1;  // staged tile row stride (floats): row-wise reads by 32 rows hit 32 banks
+
 __global__ void __launch_bounds__(kT) wplanes_w_kernel(Geometry g, const float* __restrict__ whiten,
                                                        const double* __restrict__ stats,
                                                        const double* __restrict__ prior,
                                                        const float* __restrict__ vmax,
                                                        unsigned char* __restrict__ wpl) {
-    __shared__ float isc[512];
-    __shared__ double dcs[512];
+    extern __shared__ __align__(16) unsigned char smem[];
+    float* Wt = reinterpret_cast<float*>(smem);  // [128][kWLd] W[ti rows][kt cols], zero past the diagonal / D
+    __shared__ float isc[kT];
+    __shared__ double dcs[kT];
     const int D = g.D, nt = n_tiles(D), Dt = nt * kT;
     const int line = blockIdx.x / nt, ti = blockIdx.x - line * nt, tid = threadIdx.x;
     const int nblk = g.nb * (g.nb + 1) / 2;
     const float* W = whiten + size_t(line) * nblk * 64;
-    auto w = [&](int i, int j) {  // W_ij from the packed column-major 8x8 blocks (j <= i < D)
-        return __ldg(W + size_t(tri(i >> 3, j >> 3)) * 64 + (j & 7) * 8 + (i & 7));
-    };
-    const int jmax = min(Dt, (ti + 1) * kT);
-    for (int d = tid; d < jmax; d += kT) {
-        float v = 0.f;
-        double dc = 0.0;
-        if (d < D) {
-            const float s = i8::v_scale(vmax[size_t(line) * D + d]);
-            v = s > 0.f ? 1.f / s : 0.f;
-            dc = prior[size_t(line) * g.SE + d] - stats[size_t(line) * (g.SE + D) + d];
+    const int i = ti * kT + tid;  // this thread's row
+    auto stage = [&](int kt) {   // W[ti tile][kt tile] -> Wt (+ the kt tile's column scales)
+        __syncthreads();
+        // 16 x 16 blocks of 64 floats; block (bi, bj) valid when J <= I and the block exists (I < nb)
+        for (int q = tid; q < 16 * 16 * 16; q += kT) {
+            const int blk = q >> 4, part = q & 15;  // 16 float4 per block
+            const int bi = blk >> 4, bj = blk & 15;
+            const int I = ti * 16 + bi, J = kt * 16 + bj;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (J <= I && I < g.nb) v = __ldg(reinterpret_cast<const float4*>(W + size_t(tri(I, J)) * 64) + part);
+            // element e = c * 8 + r (column-major inside the block); part covers e = 4 part .. 4 part + 3
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = 4 * part + u, c = e >> 3, r = e & 7;
+                const int row = bi * 8 + r, col = bj * 8 + c;
+                const int gi = ti * kT + row, gj = kt * kT + col;
+                Wt[row * kWLd + col] = (gi < D && gj <= gi) ? vv[u] : 0.f;
+            }
         }
-        isc[d] = v;
-        dcs[d] = dc;
+        for (int d = tid; d < kT; d += kT) {
+            const int gd = kt * kT + d;
+            float v = 0.f;
+            double dc = 0.0;
+            if (gd < D) {
+                const float sc = i8::v_scale(vmax[size_t(line) * D + gd]);
+                v = sc > 0.f ? 1.f / sc : 0.f;
+                dc = prior[size_t(line) * g.SE + gd] - stats[size_t(line) * (g.SE + D) + gd];
+            }
+            isc[d] = v;
+            dcs[d] = dc;
+        }
+        __syncthreads();
+    };
+    // ---- pass A: the row's scale and offset over every dim tile
+    float mx = 0.f;
+    double cr[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int kt = 0; kt <= ti; ++kt) {
+        stage(kt);
+        const float* wr = Wt + tid * kWLd;
+#pragma unroll 4
+        for (int c = 0; c < kT; ++c) {
+            const float wv = wr[c];
+            mx = fmaxf(mx, fabsf(wv * isc[c]));
+            cr[c & 3] += double(wv) * dcs[c];
+        }
     }
-    __syncthreads();
+    const float r = (mx > 0.f && mx <= 3.402823466e38f) ? i8::kR / mx : 0.f;
     unsigned char* out = wpl + size_t(line) * wplw_bytes(D);
     float* invr = reinterpret_cast<float*>(out + size_t(nt) * (nt + 1) / 2 * kPair);
     float* wdc = invr + Dt;
-    const int il = tid, i = ti * kT + il;
-    float mx[8];
-    double cr[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-        mx[u] = 0.f;
-        cr[u] = 0.0;
-    }
-    if (i < D) {
-        for (int j0 = 0; j0 <= i; j0 += 8) {
-            float wv[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) wv[u] = (j0 + u <= i) ? w(i, j0 + u) : 0.f;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (j0 + u <= i) {
-                    mx[u] = fmaxf(mx[u], fabsf(wv[u] * isc[j0 + u]));
-                    cr[u] += double(wv[u]) * dcs[j0 + u];
-                }
-            }
-        }
-    }
-    const float m = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-    const float r = (m > 0.f && m <= 3.402823466e38f) ? i8::kR / m : 0.f;
     invr[i] = r > 0.f ? 256.f / r : 0.f;
-    wdc[i] = float(((cr[0] + cr[1]) + (cr[2] + cr[3])) + ((cr[4] + cr[5]) + (cr[6] + cr[7])));
+    wdc[i] = float((cr[0] + cr[1]) + (cr[2] + cr[3]));
+    // ---- pass B: the digit planes, one dim tile at a time
     for (int kt = 0; kt <= ti; ++kt) {
+        if (kt < ti || ti > 0) stage(kt);  // (the last staged tile is still there when ti == 0)
         unsigned char* blk = out + size_t(ti * (ti + 1) / 2 + kt) * kPair;
+        const float* wr = Wt + tid * kWLd;
         for (int run = 0; run < kT / 16; ++run) {
-            uint32_t wd[3][4] = {{0u, 0u, 0u, 0u}, {0u, 0u, 0u, 0u}, {0u, 0u, 0u, 0u}};
-            const int j0 = kt * kT + run * 16;
-            if (i < D && j0 <= i) {
-                float wv[16];
+            uint32_t wd[3][4];
 #pragma unroll
-                for (int e = 0; e < 16; ++e) wv[e] = (j0 + e <= i) ? w(i, j0 + e) * isc[j0 + e] : 0.f;
+            for (int q4 = 0; q4 < 4; ++q4) {
+                uint32_t u[4];
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {
-                    uint32_t u[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) u[e] = i8::quant_u(wv[q4 * 4 + e], r);
-                    i8::pack_digits(u, wd[0][q4], wd[1][q4], wd[2][q4]);
+                for (int e = 0; e < 4; ++e) {
+                    const int c = run * 16 + q4 * 4 + e;
+                    u[e] = i8::quant_u(wr[c] * isc[c], r);
                 }
+                i8::pack_digits(u, wd[0][q4], wd[1][q4], wd[2][q4]);
             }
-            const uint32_t off = tc::kmajor_off_s8(il, run * 16);
+            const uint32_t off = tc::kmajor_off_s8(tid, run * 16);
 #pragma unroll
             for (int pl = 0; pl < 3; ++pl)
                 *reinterpret_cast<uint4*>(blk + pl * kPl + off) = make_uint4(wd[pl][0], wd[pl][1], wd[pl][2], wd[pl][3]);
@@ -300,7 +313,9 @@ bool score_i8w_eligible(const Geometry& g) { return !g.srp && g.D > 127 && g.D <
 
 void launch_wplanes_w(const Geometry& g, const float* whiten, const double* stats, const double* prior,
                       const float* vmax, int n_lines_total, unsigned char* wpl, cudaStream_t st) {
-    wplanes_w_kernel<<<n_lines_total * n_tiles(g.D), kT, 0, st>>>(g, whiten, stats, prior, vmax, wpl);
+    const size_t sm = size_t(kT) * kWLd * 4;
+    ensure_smem(wplanes_w_kernel, sm);
+    wplanes_w_kernel<<<n_lines_total * n_tiles(g.D), kT, sm, st>>>(g, whiten, stats, prior, vmax, wpl);
 }
 
 void launch_score_i8w(const Geometry& g, const unsigned char* vplanes, const unsigned char* wplanes, int n_lines_total,
