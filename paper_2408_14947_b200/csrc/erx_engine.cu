@@ -434,6 +434,9 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
             erxk::launch_stats(g, e->sl, xg, int(n), int(in_stride), L, stats, e->stream);
     });
     if (stats_rc) return fail(e, ERX_ERR_DEVICE, "stats_i8t: cannot encode the TMA tensor map");
+#ifdef ERX_X_STATSONLY
+    return ERX_OK;  // A/B timing builds (tools/ab_build.sh): the statistics kernel alone
+#endif
     timed(e, ERX_KERNEL_SCAN, [&] {
         erxk::launch_scan(g, stats, prior, sref, int(ns), int(n), e->cfg.alpha, e->cfg.use_incremental, e->stream,
                           kblk);

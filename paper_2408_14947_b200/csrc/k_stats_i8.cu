@@ -153,12 +153,12 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     if (warp == 8) {
         // ---------------- producer: the interleaved chunk sequence of the compute warps
         if (lane == 0) {
-            int j = 0;
+            int st = 0;
+            uint32_t rnd = 0;  // ring slot and round of the next chunk (no integer division per chunk)
             // pass-1 chunks are read again one line later (pass 2): keep them in L2
             const uint64_t keep = tc::policy_evict_last(), drop = tc::policy_evict_first();
             auto load = [&](int k, int c, bool again) {
-                const int st = j % NS;
-                if (j >= NS) tc::mbar_wait(&empty[st], uint32_t(j / NS - 1) & 1u);
+                if (rnd >= 1) tc::mbar_wait(&empty[st], (rnd - 1) & 1u);
                 const int line = blockIdx.x + k * gridDim.x;
                 const int n = min(kCh, P - c * kCh);
                 const uint32_t bytes = uint32_t(n) * B * 4;
@@ -166,7 +166,10 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                 tc::mbar_expect_tx(&full[st], bytes);
                 tc::bulk_g2s_hint(ring + size_t(st) * kCh * B, xl + size_t(c) * kCh * B, bytes, &full[st],
                                   again ? keep : drop);
-                ++j;
+                if (++st == NS) {
+                    st = 0;
+                    ++rnd;
+                }
             };
             for (int k = 0; k <= my_lines; ++k)
                 for (int c = 0; c < nch; ++c) {
@@ -267,7 +270,14 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     // the diagonal of the stats slot.  Off the diagonal they are zero-mean and stay dropped (2^-30
     // relative).
     int c0a = 0, c0b = 0;
-    int j = 0;  // position in the chunk sequence (as the producer's)
+    int jst = 0;       // ring slot of the next chunk in the sequence (as the producer's)
+    uint32_t jph = 0;  // its full-barrier phase
+    auto next_slot = [&]() {
+        if (++jst == NS) {
+            jst = 0;
+            jph ^= 1u;
+        }
+    };
     for (int k = 0; k <= my_lines; ++k) {
         const bool do1 = k < my_lines, do2 = k >= 1;
         float4 mn = make_float4(3.402823466e38f, 3.402823466e38f, 3.402823466e38f, 3.402823466e38f);
@@ -276,9 +286,9 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
             const int n = min(kCh, P - c * kCh);
             if (do1) {
                 // ---- pass 1 of line k: range of x per dim (min propagates NaN, max sees +inf); centre
-                const int st = j % NS;
-                tc::mbar_wait(&full[st], uint32_t(j / NS) & 1u);
-                ++j;
+                const int st = jst;
+                tc::mbar_wait(&full[st], jph);
+                next_slot();
                 const float* sb = ring + size_t(st) * kCh * B;
                 if (quad_live) {
                     const int p0 = warp * 8;
@@ -316,10 +326,10 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                 // ---- pass 2 of line k-1: quantise the chunk into digit planes:
                 // y = fma(x - c, s, 1.5 * 2^23) rounds v * s to an integer in the low mantissa bits
                 // (|v s| <= 2^22), u = q + 0x808080 = bits(y) - 0x4B400000 + 0x808080
-                const int st = j % NS;
+                const int st = jst;
                 const int k2 = (k - 1) * nch + c, buf = k2 & 1;
-                tc::mbar_wait(&full[st], uint32_t(j / NS) & 1u);
-                ++j;
+                tc::mbar_wait(&full[st], jph);
+                next_slot();
                 if (k2 >= 2) tc::mbar_wait(&pempty[buf], uint32_t((k2 - 2) >> 1) & 1u);
                 const float* sb = ring + size_t(st) * kCh * B + (pg2 * 16) * B;
                 unsigned char* op = ops + buf * kOps;
