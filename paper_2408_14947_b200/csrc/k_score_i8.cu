@@ -51,7 +51,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* m) {
 __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args a) {
     extern __shared__ __align__(1024) unsigned char smem[];
     __shared__ uint32_t tmem_slot;
-    __shared__ __align__(8) uint64_t wfull[2], wempty[2], tfull[kStages], tempty[kStages], accfull, accempty;
+    __shared__ __align__(8) uint64_t wfull[2], wempty[2], tfull[kStages], tempty[kStages], accfull[2], accempty[2];
     __shared__ __align__(16) float aux_s[2][2 * 128];  // per line parity: 256 / r_i, then (W (mu - c))_i
     __shared__ float red_s[2][3][128];
 
@@ -72,8 +72,10 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
             tc::mbar_init(&tfull[b], 1);
             tc::mbar_init(&tempty[b], 1);
         }
-        tc::mbar_init(&accfull, 1);
-        tc::mbar_init(&accempty, 1);
+        for (int h = 0; h < 2; ++h) {
+            tc::mbar_init(&accfull[h], 1);
+            tc::mbar_init(&accempty[h], kEW);  // one arrival per epilogue warp
+        }
         tc::fence_barrier_init();
     }
     if (warp == 0) tc::tmem_alloc<512>(&tmem_slot);
@@ -133,25 +135,31 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
                 for (int t = 0; t < ntile; ++t, ++j) {
                     const int st = j % kStages;
                     tc::mbar_wait(&tfull[st], uint32_t(j / kStages) & 1u);
-                    if (j >= 1) tc::mbar_wait(&accempty, uint32_t(j - 1) & 1u);
-                    tc::tc_fence_after();
                     const uint32_t vbase = tc::smem_u32(vops + st * i8::kTileBytes);
+                    // classes 1-2 (pairs 0-4, TMEM columns 0-255) then classes 3-4 (pairs 5-7, columns
+                    // 256-511), each half with its own full / empty barriers: the epilogue reads one half
+                    // while the tensor core fills the other
 #pragma unroll
-                    for (int s = 0; s < kKSteps; ++s) {
-                        if (a.N - 32 * s <= 0) break;  // no output row reaches these dims
+                    for (int h = 0; h < 2; ++h) {
+                        if (j >= 1) tc::mbar_wait(&accempty[h], uint32_t(j - 1) & 1u);
+                        tc::tc_fence_after();
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const uint64_t ad =
-                                tc::smem_desc_ls(vbase + pr[q][0] * i8::kVPlane + s * tc::kSliceBytes, i8::kVLbo, i8::kVSbo);
-                            const uint64_t bd = tc::smem_desc(wbase + pr[q][1] * i8::kWPlane + s * tc::kSliceBytes +
-                                                              uint32_t(s) * 1024u);
-                            const bool first = s == 0 && (q == 0 || q == 2 || q == 5 || q == 7);
-                            tc::mma_s8(tmem + uint32_t(pr[q][2]) * 128u + uint32_t(32 * s), ad, bd, idesc_s[s],
-                                       first ? 0u : 1u);
+                        for (int s = 0; s < kKSteps; ++s) {
+                            if (a.N - 32 * s <= 0) break;  // no output row reaches these dims
+#pragma unroll
+                            for (int q = h ? 5 : 0; q < (h ? 8 : 5); ++q) {
+                                const uint64_t ad = tc::smem_desc_ls(vbase + pr[q][0] * i8::kVPlane + s * tc::kSliceBytes,
+                                                                     i8::kVLbo, i8::kVSbo);
+                                const uint64_t bd = tc::smem_desc(wbase + pr[q][1] * i8::kWPlane + s * tc::kSliceBytes +
+                                                                  uint32_t(s) * 1024u);
+                                const bool first = s == 0 && (q == 0 || q == 2 || q == 5 || q == 7);
+                                tc::mma_s8(tmem + uint32_t(pr[q][2]) * 128u + uint32_t(32 * s), ad, bd, idesc_s[s],
+                                           first ? 0u : 1u);
+                            }
                         }
+                        if (h) tc::mma_commit(&tempty[st]);
+                        tc::mma_commit(&accfull[h]);
                     }
-                    tc::mma_commit(&tempty[st]);
-                    tc::mma_commit(&accfull);
                 }
                 tc::mma_commit(&wempty[wb]);
             }
@@ -173,29 +181,53 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
         const float* invr = aux_s[wb];
         const float* wdc = aux_s[wb] + 128;
         for (int t = 0; t < ntile; ++t, ++j) {
-            tc::mbar_wait(&accfull, uint32_t(j) & 1u);
+            // half 0: classes 1-2 -> lo = a1 + 2^8 a2 (exact int32), released before half 1 is waited for
+            int lo[2][16];
+            tc::mbar_wait(&accfull[0], uint32_t(j) & 1u);
             tc::tc_fence_after();
-            float acc = 0.f;
-            for (int gi = g0; gi < g1; ++gi) {
-                uint32_t v[4][16];
-                tc::tmem_ld16x4(taddr + uint32_t(gi * 16), 128u, v);
 #pragma unroll
-                for (int ii = 0; ii < 16; ++ii) {
-                    const int i = gi * 16 + ii;
-                    // m_int = a1 + 2^8 a2 + 2^16 a3 + 2^24 a4 as (a1 + 2^8 a2) + 2^16 (a3 + 2^8 a4), both halves
-                    // exact in int32 (every class sum is below 2^22 for D <= 127: two int32 conversions instead
-                    // of four); invr = 256 / r_i (0 for padding rows)
-                    const int lo = int(v[0][ii]) + int(v[1][ii]) * 256;
-                    const int hi = int(v[2][ii]) + int(v[3][ii]) * 256;
-                    float m = fmaf(float(hi), 65536.f, float(lo));
-                    m = fmaf(m, invr[i], -wdc[i]);
-                    acc = fmaf(m, m, acc);
+            for (int u = 0; u < 2; ++u) {
+                if (g0 + u < g1) {
+                    uint32_t v[2][16];
+                    tc::tmem_ld16x2(taddr + uint32_t((g0 + u) * 16), 128u, v);
+#pragma unroll
+                    for (int ii = 0; ii < 16; ++ii) lo[u][ii] = int(v[0][ii]) + int(v[1][ii]) * 256;
                 }
             }
             tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&accempty[0]);
+            // half 1: classes 3-4 -> hi = a3 + 2^8 a4; m_int = lo + 2^16 hi (every class sum is below 2^22
+            // for D <= 127, so both halves are exact in int32); invr = 256 / r_i (0 for padding rows)
+            tc::mbar_wait(&accfull[1], uint32_t(j) & 1u);
+            tc::tc_fence_after();
+            float acc = 0.f;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                if (g0 + u < g1) {
+                    uint32_t v[2][16];
+                    tc::tmem_ld16x2(taddr + 256u + uint32_t((g0 + u) * 16), 128u, v);
+                    if (u == 1 || g0 + 1 >= g1) {  // the last load of this warp: release the half
+                        tc::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&accempty[1]);
+                    }
+#pragma unroll
+                    for (int ii = 0; ii < 16; ++ii) {
+                        const int i = (g0 + u) * 16 + ii;
+                        const int hi = int(v[0][ii]) + int(v[1][ii]) * 256;
+                        float m = fmaf(float(hi), 65536.f, float(lo[u][ii]));
+                        m = fmaf(m, invr[i], -wdc[i]);
+                        acc = fmaf(m, m, acc);
+                    }
+                }
+            }
+            if (g0 >= g1) {  // no columns for this warp
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&accempty[1]);
+            }
             if (colq) red_s[j & 1][colq - 1][row] = acc;
             bar_compute();
-            if (tid == 0) mbar_arrive(&accempty);
             const int p = t * kTile + row;
             if (!colq && p < P)
                 a.raw[size_t(line) * P + p] = sqrtf(acc + red_s[j & 1][0][row] + red_s[j & 1][1][row] + red_s[j & 1][2][row]);

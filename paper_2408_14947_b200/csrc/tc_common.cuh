@@ -205,6 +205,20 @@ __device__ __forceinline__ void tmem_ld16x4(uint32_t taddr, uint32_t stride, uin
         : "r"(taddr), "r"(taddr + stride), "r"(taddr + 2 * stride), "r"(taddr + 3 * stride));
 }
 
+// Two 16-column loads (columns c0, c0 + stride) and one wait.
+__device__ __forceinline__ void tmem_ld16x2(uint32_t taddr, uint32_t stride, uint32_t (&r)[2][16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%32];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%33];\n\t"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        : "=r"(r[0][0]), "=r"(r[0][1]), "=r"(r[0][2]), "=r"(r[0][3]), "=r"(r[0][4]), "=r"(r[0][5]), "=r"(r[0][6]),
+          "=r"(r[0][7]), "=r"(r[0][8]), "=r"(r[0][9]), "=r"(r[0][10]), "=r"(r[0][11]), "=r"(r[0][12]),
+          "=r"(r[0][13]), "=r"(r[0][14]), "=r"(r[0][15]), "=r"(r[1][0]), "=r"(r[1][1]), "=r"(r[1][2]),
+          "=r"(r[1][3]), "=r"(r[1][4]), "=r"(r[1][5]), "=r"(r[1][6]), "=r"(r[1][7]), "=r"(r[1][8]), "=r"(r[1][9]),
+          "=r"(r[1][10]), "=r"(r[1][11]), "=r"(r[1][12]), "=r"(r[1][13]), "=r"(r[1][14]), "=r"(r[1][15])
+        : "r"(taddr), "r"(taddr + stride));
+}
+
 // Split fp32 values into three bf16 planes (hi + mid + lo == v to ~2^-24
 // relative): the "bf16x3" operand of the 6-product fp32-accurate MMA.
 __device__ __forceinline__ void split3_bf16x2(float a, float b, uint32_t& h, uint32_t& m, uint32_t& l) {
