@@ -594,6 +594,19 @@ __device__ __forceinline__ void st8r(float* blk, int r, const float* v) {
     *reinterpret_cast<float4*>(p + (h ^ 4)) = make_float4(v[4], v[5], v[6], v[7]);
 }
 
+// acc[c] -= sum_l a[l] b[l] for one row c of the right operand, as paired FMAs (FFMA2) over l:
+// four fma.rn.f32x2 on (a[2i], a[2i+1]) and the row's (b[2i], b[2i+1]), then one add of the halves.
+__device__ __forceinline__ float dot8_sub(const float2 (&na)[4], const float (&b)[kBlk], float acc) {
+    float2 p = make_float2(acc, 0.f);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) p = __ffma2_rn(na[i], make_float2(b[2 * i], b[2 * i + 1]), p);
+    return p.x + p.y;
+}
+__device__ __forceinline__ void neg_pairs(const float (&a)[kBlk], float2 (&na)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) na[i] = make_float2(-a[2 * i], -a[2 * i + 1]);
+}
+
 // Eight lanes (one aligned 8-lane group, lane gl holding row gl of an updated diagonal block in
 // row[]) factor the block (Cholesky, 1/sqrt from MUFU.RSQ + one Newton step) and invert the
 // factor (lane c: column c by forward substitution).  Di goes to blk (swizzled rows, zeros above the
@@ -803,12 +816,13 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
                     const float* bj = Lc + (k + 1) * kLcLd;
                     ld8r(bj, r, a);
                     ld8r(blk, r, acc);
+                    float2 na[4];
+                    neg_pairs(a, na);
 #pragma unroll
                     for (int c = 0; c < kBlk; ++c) {
                         float b[kBlk];
                         ld8r(bj, c, b);
-#pragma unroll
-                        for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], b[l], acc[c]);
+                        acc[c] = dot8_sub(na, b, acc[c]);
                     }
                     st8r(blk, r, acc);
                     const int f = diag_factor8(acc, gmask, gl, (k + 1) * kBlk, blk, DiT, dg);
@@ -825,12 +839,13 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
                     const float* bj = Lc + J * kLcLd;
                     ld8r(Lc + I * kLcLd, r, a);
                     ld8r(blk, r, acc);
+                    float2 na[4];
+                    neg_pairs(a, na);
 #pragma unroll
                     for (int c = 0; c < kBlk; ++c) {
                         float b[kBlk];
                         ld8r(bj, c, b);
-#pragma unroll
-                        for (int l = 0; l < kBlk; ++l) acc[c] = fmaf(-a[l], b[l], acc[c]);
+                        acc[c] = dot8_sub(na, b, acc[c]);
                     }
                     st8r(blk, r, acc);
                     ir += step;
@@ -851,13 +866,27 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
                         float* blk = BP(I, J);
                         const float* xk = BP(k, J);
                         ld8r(Lc + I * kLcLd, r, a);
-                        ld8r(blk, r, acc);
+                        float2 acc2[4];
+                        {
+                            float t8[kBlk];
+                            ld8r(blk, r, t8);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) acc2[i] = make_float2(t8[2 * i], t8[2 * i + 1]);
+                        }
+                        // acc[c] -= a[l] X_kJ[l][c]: paired FMAs over column pairs (c, c + 1)
 #pragma unroll
                         for (int l = 0; l < kBlk; ++l) {
                             float xr[kBlk];
                             ld8r(xk, l, xr);
+                            const float2 nal = make_float2(-a[l], -a[l]);
 #pragma unroll
-                            for (int c = 0; c < kBlk; ++c) acc[c] = fmaf(-a[l], xr[c], acc[c]);
+                            for (int i = 0; i < 4; ++i)
+                                acc2[i] = __ffma2_rn(nal, make_float2(xr[2 * i], xr[2 * i + 1]), acc2[i]);
+                        }
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            acc[2 * i] = acc2[i].x;
+                            acc[2 * i + 1] = acc2[i].y;
                         }
                         st8r(blk, r, acc);
                         ir += step;
