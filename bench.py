@@ -539,6 +539,13 @@ def secondary_measurements(pkg, args):
     except Exception as ex:
         out["single_stream"] = {"error": repr(ex)}
     try:
+        # the same stream at a deeper lag (1024 lines, ~10 % of the stream): the per-line factor of one
+        # stream only fills the GPU with enough lines per window
+        out["single_stream_deep"] = {"workload": "configs[1]: 1 stream, 640 px x 224 bands, alpha=0.05",
+                                     "window_lines": 1024, **throughput(1, 1024, ("full",), K=10)}
+    except Exception as ex:
+        out["single_stream_deep"] = {"error": repr(ex)}
+    try:
         out["single_stream_c2"] = {"workload": "configs[2]: 1 stream, 1024 px x 10 bands, alpha=0.1",
                                    "window_lines": 2048, **throughput(2, 2048, ("full", "srp"))}
     except Exception as ex:
@@ -552,6 +559,8 @@ def secondary_measurements(pkg, args):
     try:
         out["batched_c4"] = {"workload": "configs[4]: 4 streams, 1280 px x 448 bands, alpha=0.05, D = B",
                              "window_lines": 32, **throughput(4, 32, ("full",), streams=(0, 1, 2, 3), K=10)}
+        out["batched_c4_deep"] = {"workload": "configs[4]: 4 streams, 1280 px x 448 bands, alpha=0.05, D = B",
+                                  "window_lines": 128, **throughput(4, 128, ("full",), streams=(0, 1, 2, 3), K=4)}
         # the same window with the thread-block-cluster factor (DSMEM, 4 CTAs per line) forced
         out["batched_c4_cluster_factor"] = {"workload": "as batched_c4, ERX_OPT_FACTOR_PRECISION = 30",
                                             **throughput(4, 32, ("full",), streams=(0, 1, 2, 3), K=5, factor=30)}
