@@ -31,7 +31,38 @@ constexpr int kTile = 128;                          // pixels per tile (MMA M)
 constexpr int kKSteps = 4;                          // K = 128 dims
 constexpr int kThreads = 512;                       // epilogue threads (16 warps)
 constexpr int kEW = kThreads / 32;
-constexpr int kStages = 2;                          // v-plane tile ring
+constexpr int kStages = 3;                          // v-plane tile ring
+constexpr uint32_t kVSlack = 2048;                  // the K-step-3 reads of the last plane run past its used head
+
+// Shared-memory images, compacted from the global layouts (i8_common.cuh):
+//  * v tile: the three planes' used heads vb = vplane_used_bytes(D) back to back (the MMA of K-step 3
+//    reads dims >= the used head from the next plane's bytes, against W's zero columns);
+//  * W planes: K-step s only reaches output rows >= 32 s (W lower triangular) and < N, so slice s keeps
+//    rows [32 s, N): (N - 32 s) x 32 B, whole 8-row core-matrix groups.
+struct SmemPlan {
+    uint32_t vb;       // bytes per v plane head
+    uint32_t wpb;      // bytes per compact W plane
+    uint32_t so[4];    // compact offset of W slice s (rows from 32 s)
+    uint32_t sl[4];    // its bytes (0: the slice reaches no row)
+};
+__host__ __device__ inline SmemPlan smem_plan(int D) {
+    SmemPlan sp{};
+    const int N = (D + 15) / 16 * 16;
+    sp.vb = i8::vplane_used_bytes(D);
+    uint32_t off = 0;
+    for (int s = 0; s < 4; ++s) {
+        const int rows = N - 32 * s;
+        sp.so[s] = off;
+        sp.sl[s] = rows > 0 ? uint32_t(rows) * 32u : 0u;
+        off += sp.sl[s];
+    }
+    sp.wpb = off;
+    return sp;
+}
+__host__ __device__ inline size_t score_i8_smem_bytes(int D) {
+    const SmemPlan sp = smem_plan(D);
+    return 2 * 3 * size_t(sp.wpb) + kStages * 3 * size_t(sp.vb) + kVSlack;
+}
 static_assert(i8::kVPlane == kKSteps * tc::kSliceBytes, "v plane layout");
 
 struct ScoreI8Args {
@@ -58,8 +89,9 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
     const Geometry& g = a.g;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int P = g.P;
-    unsigned char* wops = smem;                            // [2][3 planes x 16 KB] W' digit planes
-    unsigned char* vops = smem + 2 * 3 * i8::kWPlane;      // [kStages][48 KB] v digit planes
+    const SmemPlan sp = smem_plan(g.D);
+    unsigned char* wops = smem;                            // [2][3][wpb] compact W' digit planes
+    unsigned char* vops = smem + 2 * 3 * sp.wpb;           // [kStages][3][vb] v digit plane heads
     const int ntile = (P + kTile - 1) / kTile;
     const int my_lines = blockIdx.x < a.n_lines ? (a.n_lines - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
@@ -93,8 +125,13 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
                 const int wb = k & 1;
                 if (k >= 2) tc::mbar_wait(&wempty[wb], uint32_t((k - 2) >> 1) & 1u);  // MMAs of line k-2 done
                 const unsigned char* wsrc = a.wplanes + size_t(line) * i8::kWBytes;
-                tc::mbar_expect_tx(&wfull[wb], i8::kWBytes);
-                tc::bulk_g2s(wops + wb * 3 * i8::kWPlane, wsrc, 3 * i8::kWPlane, &wfull[wb]);
+                tc::mbar_expect_tx(&wfull[wb], 3 * sp.wpb + i8::kWAux);
+                for (int pl = 0; pl < 3; ++pl)
+                    for (int s = 0; s < kKSteps; ++s)
+                        if (sp.sl[s])
+                            tc::bulk_g2s(wops + (wb * 3 + pl) * sp.wpb + sp.so[s],
+                                         wsrc + pl * i8::kWPlane + s * tc::kSliceBytes + uint32_t(32 * s) * 32u,
+                                         sp.sl[s], &wfull[wb]);
                 tc::bulk_g2s(aux_s[wb], wsrc + 3 * i8::kWPlane, i8::kWAux, &wfull[wb]);
                 for (int t = 0; t < ntile; ++t, ++j) {
                     const int st = j % kStages;
@@ -105,7 +142,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
                     tc::mbar_expect_tx(&tfull[st], 3 * vb);
                     const unsigned char* src = a.vplanes + (size_t(line) * ntile + t) * i8::kTileBytes;
                     for (int pl = 0; pl < 3; ++pl)
-                        tc::bulk_g2s(vops + st * i8::kTileBytes + pl * i8::kVPlane, src + pl * i8::kVPlane, vb,
+                        tc::bulk_g2s(vops + (st * 3 + pl) * vb, src + pl * i8::kVPlane, vb,
                                      &tfull[st]);
                 }
             }
@@ -131,11 +168,11 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
             for (int k = 0; k < my_lines; ++k) {
                 const int wb = k & 1;
                 tc::mbar_wait(&wfull[wb], uint32_t(k >> 1) & 1u);
-                const uint32_t wbase = tc::smem_u32(wops + wb * 3 * i8::kWPlane);
+                const uint32_t wbase = tc::smem_u32(wops + wb * 3 * sp.wpb);
                 for (int t = 0; t < ntile; ++t, ++j) {
                     const int st = j % kStages;
                     tc::mbar_wait(&tfull[st], uint32_t(j / kStages) & 1u);
-                    const uint32_t vbase = tc::smem_u32(vops + st * i8::kTileBytes);
+                    const uint32_t vbase = tc::smem_u32(vops + st * 3 * sp.vb);
                     // classes 1-2 (pairs 0-4, TMEM columns 0-255) then classes 3-4 (pairs 5-7, columns
                     // 256-511), each half with its own full / empty barriers: the epilogue reads one half
                     // while the tensor core fills the other
@@ -148,10 +185,9 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
                             if (a.N - 32 * s <= 0) break;  // no output row reaches these dims
 #pragma unroll
                             for (int q = h ? 5 : 0; q < (h ? 8 : 5); ++q) {
-                                const uint64_t ad = tc::smem_desc_ls(vbase + pr[q][0] * i8::kVPlane + s * tc::kSliceBytes,
+                                const uint64_t ad = tc::smem_desc_ls(vbase + pr[q][0] * sp.vb + s * tc::kSliceBytes,
                                                                      i8::kVLbo, i8::kVSbo);
-                                const uint64_t bd = tc::smem_desc(wbase + pr[q][1] * i8::kWPlane + s * tc::kSliceBytes +
-                                                                  uint32_t(s) * 1024u);
+                                const uint64_t bd = tc::smem_desc(wbase + pr[q][1] * sp.wpb + sp.so[s]);
                                 const bool first = s == 0 && (q == 0 || q == 2 || q == 5 || q == 7);
                                 tc::mma_s8(tmem + uint32_t(pr[q][2]) * 128u + uint32_t(32 * s), ad, bd, idesc_s[s],
                                            first ? 0u : 1u);
@@ -247,7 +283,7 @@ bool score_i8_eligible(const Geometry& g) { return !g.srp && g.D > 16 && g.D <= 
 
 void launch_score_i8(const Geometry& g, const unsigned char* vplanes, const unsigned char* wplanes, int n_lines_total,
                      float* raw, cudaStream_t st) {
-    const size_t smem = 2 * 3 * size_t(i8::kWPlane) + kStages * size_t(i8::kTileBytes);
+    const size_t smem = score_i8_smem_bytes(g.D);
     const int sms = sm_count();
     ensure_smem(score_i8_kernel, smem);
     ScoreI8Args a{g, n_lines_total, vplanes, wplanes, raw, (g.D + 15) / 16 * 16};
