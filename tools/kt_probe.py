@@ -26,6 +26,8 @@ norm = torch.empty_like(raw)
 eng = pkg.Engine(pkg.ErxConfig(no_srp=mode == "full", alpha=config["alpha"]), B, S, T)
 if os.environ.get("ERX_FACTOR"):
     eng.set_factor_precision(int(os.environ["ERX_FACTOR"]))
+if os.environ.get("ERX_FACTOR_THREADS"):
+    eng.set_factor_threads(int(os.environ["ERX_FACTOR_THREADS"]))
 for k in range(3):
     eng.run_device(dev[k % n_win].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr(), first_index=k * T)
 eng.sync()
