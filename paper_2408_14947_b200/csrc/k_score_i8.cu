@@ -237,7 +237,8 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
             // for D <= 127, so both halves are exact in int32); invr = 256 / r_i (0 for padding rows)
             tc::mbar_wait(&accfull[1], uint32_t(j) & 1u);
             tc::tc_fence_after();
-            float acc = 0.f;
+            // column pairs (i, i + 1) as paired FMAs (fma.rn.f32x2); invr / wdc pairs are one 8-byte load each
+            float2 acc2 = make_float2(0.f, 0.f);
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 if (g0 + u < g1) {
@@ -249,15 +250,20 @@ __global__ void __launch_bounds__(kThreads + 64, 1) score_i8_kernel(ScoreI8Args 
                         if (lane == 0) mbar_arrive(&accempty[1]);
                     }
 #pragma unroll
-                    for (int ii = 0; ii < 16; ++ii) {
+                    for (int ii = 0; ii < 16; ii += 2) {
                         const int i = (g0 + u) * 16 + ii;
-                        const int hi = int(v[0][ii]) + int(v[1][ii]) * 256;
-                        float m = fmaf(float(hi), 65536.f, float(lo[u][ii]));
-                        m = fmaf(m, invr[i], -wdc[i]);
-                        acc = fmaf(m, m, acc);
+                        const float2 hi = make_float2(float(int(v[0][ii]) + int(v[1][ii]) * 256),
+                                                      float(int(v[0][ii + 1]) + int(v[1][ii + 1]) * 256));
+                        const float2 lo2 = make_float2(float(lo[u][ii]), float(lo[u][ii + 1]));
+                        const float2 r2 = *reinterpret_cast<const float2*>(invr + i);
+                        const float2 w2 = *reinterpret_cast<const float2*>(wdc + i);
+                        float2 m = __ffma2_rn(hi, make_float2(65536.f, 65536.f), lo2);
+                        m = __ffma2_rn(m, r2, make_float2(-w2.x, -w2.y));
+                        acc2 = __ffma2_rn(m, m, acc2);
                     }
                 }
             }
+            const float acc = acc2.x + acc2.y;
             if (g0 >= g1) {  // no columns for this warp
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&accempty[1]);
