@@ -117,6 +117,80 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
 
 
 // ---------------------------------------------------------------------------
+// Short windows (EMA, n <= kTileLines: the batched configs[3] geometry, 32 lines per stream): one CTA
+// takes 128 elements of one stream and first copies everything its recurrence reads into shared
+// memory with cp.async -- its elements' line values for all n lines and the prefix of each line's
+// sum vector s its elements touch -- so the sequential EMA never waits on global memory.  Same
+// per-element arithmetic and order as scan_kernel (bit-identical results).
+// ---------------------------------------------------------------------------
+constexpr int kTileLines = 64;
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem_src));
+}
+
+__global__ void __launch_bounds__(128) scan_tile_kernel(Geometry g, const double* __restrict__ stats,
+                                                        double* __restrict__ prior, StateRef sref, int n,
+                                                        double alpha, float* __restrict__ kblk) {
+    extern __shared__ __align__(16) double tsm[];
+    const double* __restrict__ st_in = sref.in();
+    double* __restrict__ st_out = sref.out();
+    const int initialized = sref.meta->initialized;
+    const int s = blockIdx.y, tid = threadIdx.x;
+    const int e0 = blockIdx.x * 128, e = e0 + tid;
+    const int D = g.D, SS = g.SE + g.D;
+    const double P = double(g.P), invP = 1.0 / P, invP1 = 1.0 / (P - 1.0);
+    // the sum-vector prefix this CTA touches: dims 0 .. amax (rows of its last covariance element)
+    const int e_last = min(e0 + 127, g.SE - 1);
+    int amax = e_last, bdummy = 0;
+    if (e_last >= D) unpack_tri(e_last - D, amax, bdummy);
+    if (e0 < D) amax = max(amax, min(e0 + 127, D - 1));
+    const int ns = amax + 1;
+    double* xv = tsm;             // [n][128] the elements' own line values (c_a or S_ab)
+    double* sv = tsm + n * 128;   // [n][ns] the line sums s_0 .. s_amax
+    const size_t l0 = size_t(s) * n;
+    int a = e, b = e;
+    if (e >= D) unpack_tri(e - D, a, b);
+    const bool live = e < g.SE;
+    const bool is_mu = e < D;
+    const int o0 = is_mu ? e : 2 * D + (e - D);
+    if (live)
+        for (int t = 0; t < n; ++t) cp_async8(xv + t * 128 + tid, stats + (l0 + t) * SS + o0);
+    for (int q = tid; q < n * ns; q += 128) {
+        const int t = q / ns, j = q - t * ns;
+        cp_async8(sv + q, stats + (l0 + t) * SS + D + j);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    if (!live) return;
+    const int nblk = g.nb * (g.nb + 1) / 2;
+    const bool to_blk = kblk != nullptr && e >= D;
+    const int boff = ((a >> 3) * ((a >> 3) + 1) / 2 + (b >> 3)) * 64 + (a & 7) * 8 + ((b & 7) ^ (a & 4));
+    const double om = 1.0 - alpha;
+    double state = st_in[size_t(s) * g.SE + e];
+#pragma unroll 4
+    for (int t = 0; t < n; ++t) {
+        const double* svt = sv + t * ns;
+        const double cur = finish_stat(is_mu, xv[t * 128 + tid], svt[a], svt[b], invP, invP1);
+        double pr;
+        if (!initialized && t == 0) {
+            pr = cur;
+            state = cur;
+        } else {
+            pr = state;
+            state = ema_step(state, cur, om, alpha);
+        }
+        if (to_blk)
+            kblk[(l0 + t) * nblk * 64 + boff] = float(pr);
+        else
+            prior[(l0 + t) * g.SE + e] = pr;
+    }
+    st_out[size_t(s) * g.SE + e] = state;
+}
+
+// ---------------------------------------------------------------------------
 // Few elements, long windows (a single stream at small D: configs[2] has 20
 // state elements and up to thousands of lines per window): the element-
 // parallel kernel above runs one warp through every line, each step waiting on
@@ -263,6 +337,12 @@ void launch_scan(const Geometry& g, const double* stats, double* prior, StateRef
         return;
     }
     dim3 grid((g.SE + 127) / 128, n_streams);
+    const size_t tile_smem = size_t(n_per_stream) * (128 + g.D) * sizeof(double);
+    if (!incremental && n_per_stream <= kTileLines && tile_smem <= 100 * 1024) {
+        ensure_smem(scan_tile_kernel, 100 * 1024);
+        scan_tile_kernel<<<grid, 128, tile_smem, st>>>(g, stats, prior, state, n_per_stream, alpha, kblk);
+        return;
+    }
     scan_kernel<<<grid, 128, 0, st>>>(g, stats, prior, state, n_per_stream, alpha, incremental, kblk);
 }
 
