@@ -176,6 +176,12 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
  * single-stream lag-0 path: one launch per line); 0 launches kernel by kernel.
  * Per-kernel profiling (erx_set_profiling) bypasses the graphs. */
 #define ERX_OPT_GRAPHS 6
+/* ERX_OPT_DEVICE_GROUPS: 0 (default) auto, 1 or 2.  erx_run_device runs a window of >= 2 streams
+ * as two stream groups on two CUDA streams (forked from and joined back into the engine stream, so
+ * the call's stream-ordered contract is unchanged), each with its own rescue list, so the small
+ * kernels and tails of one group overlap the other group's kernels; auto splits windows of >= 1024
+ * lines.  Per-kernel profiling runs one group. */
+#define ERX_OPT_DEVICE_GROUPS 7
 int erx_set_option(erx_engine* e, int option, int64_t value);
 int64_t erx_get_option(const erx_engine* e, int option);
 

@@ -28,6 +28,7 @@ OPT_HOST_GROUPS = 3
 OPT_ASYNC_HOST = 4
 OPT_FACTOR_THREADS = 5
 OPT_GRAPHS = 6
+OPT_DEVICE_GROUPS = 7
 
 
 class ErxConfigC(C.Structure):

@@ -126,6 +126,13 @@ struct erx_engine {
     int* d_fix = nullptr;        // fp64 rescue list of the fp32 factor ([0] count, [1] done, [2..] lines)
     double* d_fixwork = nullptr; // the rescue's fp64 workspace
     int fix_cap = 0;             // list capacity (lines per window)
+    size_t fixwork_doubles = 0;  // rescue workspace per device stream group
+    // the device path runs a window as two stream groups on two CUDA streams (ERX_OPT_DEVICE_GROUPS), each
+    // with its own rescue list / workspace, so one group's small kernels and tails overlap the other's
+    static constexpr int kDevGroups = 2;
+    int dev_groups = 0;          // 0 auto, 1 or 2
+    cudaStream_t stream2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t rescued_before = 0;  // rescued lines counted by earlier (re-planned) lists
 
     // pinned host staging (drop-in path)
@@ -235,10 +242,14 @@ void collect_timings(erx_engine* e) {
 
 int64_t read_rescued(erx_engine* e) {
     if (!e->d_fix) return 0;
-    int v = 0;
+    int64_t tot = 0;
     cudaStreamSynchronize(e->stream);
-    cudaMemcpy(&v, e->d_fix + e->fix_cap + 2, sizeof(int), cudaMemcpyDeviceToHost);
-    return int64_t(v);
+    for (int gi = 0; gi < erx_engine::kDevGroups; ++gi) {
+        int v = 0;
+        cudaMemcpy(&v, e->d_fix + size_t(gi) * (e->fix_cap + 3) + e->fix_cap + 2, sizeof(int), cudaMemcpyDeviceToHost);
+        tot += v;
+    }
+    return tot;
 }
 
 void free_window(erx_engine* e) {
@@ -342,10 +353,11 @@ int configure(erx_engine* e, uint32_t P) {
     if (e->tensor) CU(cudaMalloc(&e->d_c0, L * 4 * size_t(g.D) * sizeof(int)));
     if (e->factor_prec == 32) CU(cudaMalloc(&e->d_kblk, L * erxk::whiten_floats_per_line(g) * sizeof(float)));
     // fp64 rescue list (fed by the fp32 factors and by the normalisation's flat-line check)
-    CU(cudaMalloc(&e->d_fix, (L + 3) * sizeof(int)));
-    CU(cudaMemset(e->d_fix, 0, (L + 3) * sizeof(int)));
+    CU(cudaMalloc(&e->d_fix, erx_engine::kDevGroups * (L + 3) * sizeof(int)));
+    CU(cudaMemset(e->d_fix, 0, erx_engine::kDevGroups * (L + 3) * sizeof(int)));
     e->fix_cap = int(L);
-    CU(cudaMalloc(&e->d_fixwork, erxk::fixup_work_doubles(g, int(L)) * sizeof(double)));
+    e->fixwork_doubles = erxk::fixup_work_doubles(g, int(L));
+    CU(cudaMalloc(&e->d_fixwork, erx_engine::kDevGroups * e->fixwork_doubles * sizeof(double)));
     return ERX_OK;
 }
 
@@ -399,7 +411,11 @@ std::shared_ptr<ResultBlock> take_block(erx_engine* e, uint32_t n) {
 // per-line buffer holds line (s, t) at s * n + t, so a stream range is a
 // contiguous line range and the groups are independent (no cross-stream data).
 int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride, float* raw, float* norm,
-                   uint32_t s0, uint32_t ns, bool score = true) {
+                   uint32_t s0, uint32_t ns, bool score = true, int grp = 0) {
+    // grp: device stream group (run_device_window) -- its own CUDA stream, rescue list and workspace
+    cudaStream_t st = grp ? e->stream2 : e->stream;
+    int* fix = e->d_fix + size_t(grp) * (e->fix_cap + 3);
+    double* fixwork = e->d_fixwork + size_t(grp) * e->fixwork_doubles;
     const Geometry& g = e->geo;
     const int L = int(ns * n);
     const size_t l0 = size_t(s0) * n;
@@ -424,21 +440,21 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     int stats_rc = 0;
     timed(e, ERX_KERNEL_STATS, [&] {
         if (e->small)
-            erxk::launch_stats_small(g, e->smp, xg, int(n), int(in_stride), L, stats, vcache, e->stream);
+            erxk::launch_stats_small(g, e->smp, xg, int(n), int(in_stride), L, stats, vcache, st);
         else if (tensor)
-            erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, vmax, vplanes, c0, e->stream);
+            erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, vmax, vplanes, c0, st);
         else if (e->wide_i8)
             stats_rc = erxk::launch_stats_i8t(g, xg, int(n), int(in_stride), int(ns), stats, cen, vmax, vplanes,
-                                              e->stream);
+                                              st);
         else
-            erxk::launch_stats(g, e->sl, xg, int(n), int(in_stride), L, stats, e->stream);
+            erxk::launch_stats(g, e->sl, xg, int(n), int(in_stride), L, stats, st);
     });
     if (stats_rc) return fail(e, ERX_ERR_DEVICE, "stats_i8t: cannot encode the TMA tensor map");
 #ifdef ERX_X_STATSONLY
     return ERX_OK;  // A/B timing builds (tools/ab_build.sh): the statistics kernel alone
 #endif
     timed(e, ERX_KERNEL_SCAN, [&] {
-        erxk::launch_scan(g, stats, prior, sref, int(ns), int(n), e->cfg.alpha, e->cfg.use_incremental, e->stream,
+        erxk::launch_scan(g, stats, prior, sref, int(ns), int(n), e->cfg.alpha, e->cfg.use_incremental, st,
                           kblk);
     });
     if (!score) {  // background update only (erx_advance_device): statistics and the scan
@@ -448,32 +464,32 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     }
     timed(e, ERX_KERNEL_FACTOR, [&] {
         erxk::launch_factor(g, prior, L, e->cfg.epsilon, work, white, status, e->d_latch, e->d_meta, (long long)(e->S),
-                            (long long)(l0), e->factor_prec, e->stream, e->d_fix, stats, tensor ? vmax : nullptr, kblk,
+                            (long long)(l0), e->factor_prec, st, fix, stats, tensor ? vmax : nullptr, kblk,
                             e->factor_threads);
     });
     if (e->small) {  // score + normalisation fused
         timed(e, ERX_KERNEL_SCORE, [&] {
-            erxk::launch_score_small(g, e->smp, stats, prior, white, vcache, L, rawg, normg, status, e->d_fix,
-                                     e->stream);
+            erxk::launch_score_small(g, e->smp, stats, prior, white, vcache, L, rawg, normg, status, fix,
+                                     st);
         });
     } else {
         timed(e, ERX_KERNEL_SCORE, [&] {
             if (tensor) {
-                erxk::launch_score_i8(g, vplanes, reinterpret_cast<const unsigned char*>(white), L, rawg, e->stream);
+                erxk::launch_score_i8(g, vplanes, reinterpret_cast<const unsigned char*>(white), L, rawg, st);
             } else if (e->wide_i8) {
-                erxk::launch_wplanes_w(g, white, stats, prior, vmax, L, wplw, e->stream);
-                erxk::launch_score_i8w(g, vplanes, wplw, L, rawg, e->stream);
+                erxk::launch_wplanes_w(g, white, stats, prior, vmax, L, wplw, st);
+                erxk::launch_score_i8w(g, vplanes, wplw, L, rawg, st);
             } else
-                erxk::launch_score(g, e->sc, xg, int(n), int(in_stride), prior, white, L, rawg, e->stream);
+                erxk::launch_score(g, e->sc, xg, int(n), int(in_stride), prior, white, L, rawg, st);
         });
-        timed(e, ERX_KERNEL_NORMALIZE, [&] { erxk::launch_normalize(g, rawg, L, normg, status, e->d_fix, e->stream); });
+        timed(e, ERX_KERNEL_NORMALIZE, [&] { erxk::launch_normalize(g, rawg, L, normg, status, fix, st); });
     }
     {
         timed(e, ERX_KERNEL_FIXUP, [&] {
             erxk::FixupArgs fa{g, xg, int(n), int(in_stride), stats, sref, e->cfg.alpha, e->cfg.use_incremental,
-                               e->cfg.epsilon, e->d_fix, e->fix_cap, e->d_fixwork, rawg, normg, status, e->d_latch,
+                               e->cfg.epsilon, fix, e->fix_cap, fixwork, rawg, normg, status, e->d_latch,
                                (long long)(e->S), (long long)(l0)};
-            erxk::launch_fixup(fa, L, e->stream);
+            erxk::launch_fixup(fa, L, st);
         });
     }
     cudaError_t r = cudaGetLastError();
@@ -585,13 +601,32 @@ int drain_pending(erx_engine* e) {
 // and replayed as ONE launch: the single-stream lag-0 path costs one graph launch per line — the host
 // path's windows always qualify (fixed staging buffers), device-path callers when they reuse a few
 // buffers (an 8-entry cache) (ERX_OPT_GRAPHS; off while per-kernel profiling is on).
-int run_device_window(erx_engine* e, const float* d_lines, uint32_t n, uint32_t in_stride, float* d_raw,
-                      float* d_norm) {
-    if (!e->use_graphs || e->profiling) {
+// Both device stream groups of one window: group 0 on the engine stream, group 1 forked onto stream2
+// and joined back before the state advance (no shared buffers: per-line buffers are indexed by
+// stream, rescue lists and workspaces are per group).
+int enqueue_device_window(erx_engine* e, const float* d_lines, uint32_t n, uint32_t in_stride, float* d_raw,
+                          float* d_norm) {
+    const bool split = !e->profiling && e->S >= 2 &&
+                       (e->dev_groups == 2 || (e->dev_groups == 0 && uint64_t(e->S) * n >= 1024));
+    if (!split) {
         if (int st = enqueue_window(e, d_lines, n, in_stride, d_raw, d_norm, 0, e->S)) return st;
         enqueue_advance(e, n);
         return ERX_OK;
     }
+    const uint32_t sh = e->S / 2;
+    CU(cudaEventRecord(e->ev_fork, e->stream));
+    CU(cudaStreamWaitEvent(e->stream2, e->ev_fork, 0));
+    if (int st = enqueue_window(e, d_lines, n, in_stride, d_raw, d_norm, 0, sh, true, 0)) return st;
+    if (int st = enqueue_window(e, d_lines, n, in_stride, d_raw, d_norm, sh, e->S - sh, true, 1)) return st;
+    CU(cudaEventRecord(e->ev_join, e->stream2));
+    CU(cudaStreamWaitEvent(e->stream, e->ev_join, 0));
+    enqueue_advance(e, n);
+    return ERX_OK;
+}
+
+int run_device_window(erx_engine* e, const float* d_lines, uint32_t n, uint32_t in_stride, float* d_raw,
+                      float* d_norm) {
+    if (!e->use_graphs || e->profiling) return enqueue_device_window(e, d_lines, n, in_stride, d_raw, d_norm);
     for (auto& ge : e->graphs)
         if (ge.x == d_lines && ge.raw == d_raw && ge.norm == d_norm && ge.n == n && ge.P == e->P &&
             ge.in_stride == in_stride) {
@@ -601,8 +636,7 @@ int run_device_window(erx_engine* e, const float* d_lines, uint32_t n, uint32_t 
         }
     const uint64_t k0 = e->launches;
     CU(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
-    int st = enqueue_window(e, d_lines, n, in_stride, d_raw, d_norm, 0, e->S);
-    if (!st) enqueue_advance(e, n);
+    int st = enqueue_device_window(e, d_lines, n, in_stride, d_raw, d_norm);
     cudaGraph_t graph = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(e->stream, &graph);
     if (st) {
@@ -755,6 +789,10 @@ int erx_create(const erx_config* cfg, uint32_t bands, uint32_t n_streams, uint32
     if (r != cudaSuccess) return bail(std::string("cudaSetDevice: ") + cudaGetErrorString(r));
     r = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
     if (r != cudaSuccess) return bail(std::string("cudaStreamCreate: ") + cudaGetErrorString(r));
+    if (cudaStreamCreateWithFlags(&e->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return bail("cudaStreamCreate (device group stream)");
     // SRP weights (generate_srp, projection.hpp:26) -> CSC of signs per output dim
     std::vector<int> ptr(e->D + 1, 0), band;
     std::vector<float> sign;
@@ -835,6 +873,9 @@ void erx_destroy(erx_engine* e) {
         if (e->ev_d2h[k]) cudaEventDestroy(e->ev_d2h[k]);
     }
     if (e->h2d) cudaStreamDestroy(e->h2d);
+    if (e->stream2) cudaStreamDestroy(e->stream2);
+    if (e->ev_fork) cudaEventDestroy(e->ev_fork);
+    if (e->ev_join) cudaEventDestroy(e->ev_join);
     if (e->d2h) cudaStreamDestroy(e->d2h);
     if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
@@ -1096,6 +1137,11 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
         e->factor_threads = int(value);
         return ERX_OK;
     }
+    if (option == ERX_OPT_DEVICE_GROUPS) {
+        if (value < 0 || value > erx_engine::kDevGroups) return fail(e, ERX_ERR_CONFIG, "device groups: 0, 1 or 2");
+        e->dev_groups = int(value);
+        return ERX_OK;
+    }
     if (option == ERX_OPT_GRAPHS) {
         if (value != 0 && value != 1) return fail(e, ERX_ERR_CONFIG, "graphs: 0 or 1");
         e->use_graphs = value != 0;
@@ -1138,6 +1184,7 @@ int64_t erx_get_option(const erx_engine* e, int option) {
     if (option == ERX_OPT_FACTOR_PRECISION) return e->d_stats ? e->factor_prec : e->factor_req;
     if (option == ERX_OPT_HOST_GROUPS) return e->host_groups;
     if (option == ERX_OPT_GRAPHS) return e->use_graphs ? 1 : 0;
+    if (option == ERX_OPT_DEVICE_GROUPS) return e->dev_groups;
     if (option == ERX_OPT_FACTOR_THREADS) return e->factor_threads;
     if (option == ERX_OPT_ASYNC_HOST) return e->async_host ? 1 : 0;
     if (option == ERX_OPT_STATS_TENSOR) {

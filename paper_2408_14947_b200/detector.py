@@ -272,6 +272,10 @@ class Engine:
         """0 auto, 32 or 64 (see ERX_OPT_FACTOR_PRECISION in include/erx_b200.h)."""
         self._check(self._lib.erx_set_option(self._h, L.OPT_FACTOR_PRECISION, bits))
 
+    def set_device_groups(self, groups: int):
+        """Device stream groups per window: 0 auto, 1 or 2 (ERX_OPT_DEVICE_GROUPS)."""
+        self._check(self._lib.erx_set_option(self._h, L.OPT_DEVICE_GROUPS, int(groups)))
+
     def set_factor_threads(self, threads: int):
         """Threads per line of the blocked fp32 factor: 0 auto, 64, 128 or 256 (ERX_OPT_FACTOR_THREADS)."""
         self._check(self._lib.erx_set_option(self._h, L.OPT_FACTOR_THREADS, int(threads)))

@@ -26,6 +26,8 @@ norm = torch.empty_like(raw)
 eng = pkg.Engine(pkg.ErxConfig(no_srp=mode == "full", alpha=config["alpha"]), B, S, T)
 if os.environ.get("ERX_FACTOR"):
     eng.set_factor_precision(int(os.environ["ERX_FACTOR"]))
+if os.environ.get("ERX_DEVICE_GROUPS"):
+    eng.set_device_groups(int(os.environ["ERX_DEVICE_GROUPS"]))
 if os.environ.get("ERX_FACTOR_THREADS"):
     eng.set_factor_threads(int(os.environ["ERX_FACTOR_THREADS"]))
 for k in range(3):
