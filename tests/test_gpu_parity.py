@@ -616,3 +616,43 @@ def test_graph_replay_matches_launches(pkg):
         for (a, b) in zip(outs[0][0], outs[1][0]):
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), (T, incremental)
         assert np.array_equal(outs[0][1], outs[1][1]) and outs[0][2:] == outs[1][2:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("no_srp", [True, False])
+def test_device_groups_bitwise(pkg, no_srp):
+    """ERX_OPT_DEVICE_GROUPS: a window run as two stream groups on two CUDA streams (each with its own
+    rescue list) gives the same bits as one group, graphs on and off, with an ill-conditioned stream
+    among them so both groups' rescue lists are exercised."""
+    import torch
+
+    S, T, P, B = 8, 16, 256, 108
+    host = np.stack([pkg.gen_lines(pkg.gen_spec(3, s), 0, 2 * T)[0][:, :P] for s in range(S)])
+    # stream 5: radiance-scale lines with 1 DN of sensor noise (A_ii / L_ii^2 ~ 1e4): the fp64 rescue
+    # takes them (tests/test_gpu_numerics.py::test_radiance_scale_ill_conditioned)
+    rng = np.random.default_rng(5)
+    A = rng.normal(0, 0.05, size=(B, 3))
+    base = 0.3 + 0.2 * np.sin(np.linspace(0, 3, B))
+    host[5] = ((base + rng.normal(size=(2 * T, P, 3)) @ A.T + rng.normal(0, 1.0 / 3000.0, size=(2 * T, P, B)))
+               * 3000.0).astype(np.float32)
+    dev = torch.from_numpy(np.ascontiguousarray(host.reshape(S, 2, T, P, B).transpose(1, 0, 2, 3, 4))).cuda()
+    outs = []
+    for groups in (1, 2):
+        for graphs in (False, True):
+            eng = pkg.Engine(pkg.ErxConfig(no_srp=no_srp), B, S, T)
+            eng.set_device_groups(groups)
+            eng.set_graphs(graphs)
+            raw = torch.empty((S, T, P), dtype=torch.float32, device="cuda")
+            norm = torch.empty_like(raw)
+            res = []
+            for w in range(2):
+                eng.run_device(dev[w].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr(), first_index=w * T)
+                eng.sync()
+                res.append((raw.cpu().numpy().copy(), norm.cpu().numpy().copy()))
+            outs.append((res, eng.rescued_lines()))
+            eng.close()
+    for o in outs[1:]:
+        for a, b in zip(outs[0][0], o[0]):
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        assert o[1] == outs[0][1]
+    assert outs[0][1] > 0  # the rescue ran (in group 1 when split: streams 4-7)
