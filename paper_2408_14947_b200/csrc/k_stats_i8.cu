@@ -42,6 +42,8 @@
 // N = roundup16(D + 1)) per chunk; the epilogue stages S over the idle plane
 // buffers.  With the score kernel in use, pass 2 also writes its digits to
 // global memory as that kernel's MN-major A operand (i8_common.cuh).
+#include <cstdlib>
+
 #include "erx_common.cuh"
 #include "i8_common.cuh"
 #include "tc_common.cuh"
@@ -70,6 +72,7 @@ struct StatsI8Args {
     int* c0;     // [line][4][D] class-0 diagonal partials sum_p d0^2 (q units), per pixel group
     int N;       // MMA N = roundup16(D + 1)
     int stages;  // ring depth
+    int ring1;   // stats_i8_ws: stages of the pass-1 ring (the rest: pass 2)
 };
 
 __device__ __forceinline__ void pack_digits(const uint32_t (&u)[4], uint32_t& w0, uint32_t& w1, uint32_t& w2) {
@@ -450,6 +453,372 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     if (warp == 0) tc::tmem_free<512>(tmem);
 }
 
+// ---------------------------------------------------------------------------
+// stats_i8_ws: the same statistics with the range pass on its own warps.  In stats_i8_kernel the
+// eight compute warps run the range pass of line k, the quantise pass of line k-1, its epilogue and
+// the range step one after the other; measured, that chain (not the loads) bounds the kernel
+// (DESIGN.md §6).  Here warps 8-11 stream pass 1 (range of line k, its own ring, HBM, evict_last)
+// and hand each line's centre / scale to the quantise warps through per-parity shared arrays
+// (sready / sfree mbarriers), so the range pass runs beside the quantise / MMA / epilogue chain of
+// warps 0-7.  The pass-2 producer re-reads a chunk from L2 only once the range warps have passed it
+// (a monotonic chunk count).  Arithmetic per line is the stats_i8_kernel's (bit-identical output).
+// Warps: 0-7 quantise + epilogue, 8-11 range, 12 pass-1 producer, 13 pass-2 producer, 14 MMA issuer.
+// ---------------------------------------------------------------------------
+#ifdef ERX_X_TRACE  // A/B timeline instrumentation of CTA 0 (tools/stats_trace.py)
+__device__ unsigned long long g_trace[1 << 16];
+__device__ unsigned int g_trace_n;
+__device__ __forceinline__ void trace_ev(int id, int k, int c) {
+    if (blockIdx.x == 0) {
+        const unsigned i = atomicAdd(&g_trace_n, 1u);
+        if (i < (1u << 15)) {
+            g_trace[2 * i] = clock64();
+            g_trace[2 * i + 1] = (unsigned long long)((id << 24) | (k << 12) | c);
+        }
+    }
+}
+#define TR(id, k, c) trace_ev(id, k, c)
+#else
+#define TR(id, k, c)
+#endif
+constexpr int kWsThreads = 480;
+constexpr int kWsRing1 = 2;  // pass-1 stages (the range pass consumes fast); the rest go to pass 2
+
+__device__ __forceinline__ void bar_range() { asm volatile("bar.sync 2, 128;" ::); }
+
+template <int kBT>
+__global__ void __launch_bounds__(kWsThreads, 1) stats_i8_ws_kernel(StatsI8Args a) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t full1[kMaxStages], empty1[kMaxStages], full2[kMaxStages], empty2[kMaxStages];
+    __shared__ __align__(8) uint64_t pfull[2], pempty[2], accfull, accempty, sready[2], sfree[2];
+    __shared__ __align__(16) float red_mn[4][128];
+    __shared__ __align__(16) float red_mx[4][128];
+    __shared__ double red_cs[4][128];
+    __shared__ float cen_s[2][128], scale_s[2][128], add_s[2][128];  // per line parity
+    __shared__ double inv_s[2][128];
+    __shared__ double sum_s[128];
+    __shared__ int bad_s[2][4];
+    __shared__ int p1_count;  // pass-1 chunks finished by the range warps, x 4 (monotonic)
+
+    const Geometry& g = a.g;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int B = kBT > 0 ? kBT : g.B, D = g.D, P = g.P;
+    const int NS1 = a.ring1, NS2 = a.stages - a.ring1;
+
+    unsigned char* ops = smem;                                          // [2][kOps]
+    float* ring1 = reinterpret_cast<float*>(smem + 2 * kOps);           // [NS1][kCh * B]
+    float* ring2 = ring1 + size_t(NS1) * kCh * B;                       // [NS2][kCh * B]
+    const size_t tri_bytes = size_t(D) * (D + 1) / 2 * 8;
+    double* S = reinterpret_cast<double*>(tri_bytes <= 2 * kOps ? smem : smem + 2 * kOps + size_t(a.stages) * kCh * B * 4);
+    const int nch = (P + kCh - 1) / kCh;
+    const int ntile_v = (P + 127) / 128;
+    const int my_lines = blockIdx.x < a.n_lines ? (a.n_lines - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    if (tid == 0) {
+        for (int s = 0; s < NS1; ++s) {
+            tc::mbar_init(&full1[s], 1);
+            tc::mbar_init(&empty1[s], 4);
+        }
+        for (int s = 0; s < NS2; ++s) {
+            tc::mbar_init(&full2[s], 1);
+            tc::mbar_init(&empty2[s], 8);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&pfull[b], 8);
+            tc::mbar_init(&pempty[b], 1);
+            tc::mbar_init(&sready[b], 4);
+            tc::mbar_init(&sfree[b], 8);
+        }
+        tc::mbar_init(&accfull, 1);
+        tc::mbar_init(&accempty, 1);
+        p1_count = 0;
+        tc::fence_barrier_init();
+    }
+    if (warp == 0) tc::tmem_alloc<512>(&tmem_slot);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+
+    if (warp == 12 || warp == 13) {
+        // ---------------- producers: warp 12 pass 1 (HBM, kept in L2), warp 13 pass 2 (the L2 re-read)
+        if (lane == 0) {
+            const bool p1 = warp == 12;
+            const int NSx = p1 ? NS1 : NS2;
+            float* ring = p1 ? ring1 : ring2;
+            uint64_t* fullx = p1 ? full1 : full2;
+            uint64_t* emptyx = p1 ? empty1 : empty2;
+            const uint64_t pol = p1 ? tc::policy_evict_last() : tc::policy_evict_first();
+            int st = 0;
+            uint32_t rnd = 0;
+            for (int k = 0; k < my_lines; ++k)
+                for (int c = 0; c < nch; ++c) {
+                    if (!p1)  // the range warps have read this chunk (it is in L2 now)
+                        while (*reinterpret_cast<volatile int*>(&p1_count) < 4 * (k * nch + c + 1)) __nanosleep(64);
+                    if (rnd >= 1) tc::mbar_wait(&emptyx[st], (rnd - 1) & 1u);
+                    TR(p1 ? 30 : 31, k, c);
+                    const int line = blockIdx.x + k * gridDim.x;
+                    const int n = min(kCh, P - c * kCh);
+                    const uint32_t bytes = uint32_t(n) * B * 4;
+                    const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
+                    tc::mbar_expect_tx(&fullx[st], bytes);
+                    tc::bulk_g2s_hint(ring + size_t(st) * kCh * B, xl + size_t(c) * kCh * B, bytes, &fullx[st], pol);
+                    if (++st == NSx) {
+                        st = 0;
+                        ++rnd;
+                    }
+                }
+        }
+        return;
+    }
+    if (warp == 14) {
+        // ---------------- MMA issuer: 2 K-steps x 8 digit-plane pairs per chunk (as stats_i8_kernel)
+        if (lane == 0) {
+            const uint32_t idesc = tc::idesc_s8_s32(128, a.N);
+            const int pr[8][3] = {{0, 1, 0}, {1, 0, 0}, {0, 2, 1}, {1, 1, 1}, {2, 0, 1}, {1, 2, 2}, {2, 1, 2}, {2, 2, 3}};
+            for (int k = 0; k < my_lines; ++k) {
+                if (k >= 1) tc::mbar_wait(&accempty, uint32_t(k - 1) & 1u);
+                for (int c = 0; c < nch; ++c) {
+                    const int k2 = k * nch + c, buf = k2 & 1;
+                    tc::mbar_wait(&pfull[buf], uint32_t(k2 >> 1) & 1u);
+                    TR(20, k, c);
+                    tc::tc_fence_after();
+                    const uint32_t base = tc::smem_u32(ops + buf * kOps);
+#pragma unroll
+                    for (int s = 0; s < kCh / 32; ++s)
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const uint64_t ad = tc::smem_desc(base + pr[q][0] * kPlane + s * tc::kSliceBytes);
+                            const uint64_t bd = tc::smem_desc(base + pr[q][1] * kPlane + s * tc::kSliceBytes);
+                            const bool first = c == 0 && s == 0 && (q == 0 || q == 2 || q == 5 || q == 7);
+                            tc::mma_s8(tmem + uint32_t(pr[q][2]) * 128u, ad, bd, idesc, first ? 0u : 1u);
+                        }
+                    tc::mma_commit(&pempty[buf]);
+                    TR(21, k, c);
+                }
+                tc::mma_commit(&accfull);
+            }
+        }
+        return;
+    }
+    if (warp >= 8) {
+        // ---------------- range warps 8-11: pass 1 of every line and its range step
+        const int wr = warp - 8, t2 = tid - 256;
+        const bool quad_live = 4 * lane < B;
+        int st = 0;
+        uint32_t ph = 0;
+        for (int k = 0; k < my_lines; ++k) {
+            float4 mn = make_float4(3.402823466e38f, 3.402823466e38f, 3.402823466e38f, 3.402823466e38f);
+            float4 mx = make_float4(-3.402823466e38f, -3.402823466e38f, -3.402823466e38f, -3.402823466e38f);
+            for (int c = 0; c < nch; ++c) {
+                const int n = min(kCh, P - c * kCh);
+                tc::mbar_wait(&full1[st], ph);
+                if (lane == 0 && wr == 0) TR(10, k, c);
+                const float* sb = ring1 + size_t(st) * kCh * B;
+                if (quad_live) {
+                    // 8-pixel groups wr and wr + 4 (stats_i8_kernel's groups, two per warp here)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int p0 = (wr + 4 * h) * 8;
+                        const float* xp = sb + p0 * B + 4 * lane;
+                        const int np = min(8, n - p0);
+#pragma unroll
+                        for (int pp = 0; pp < 8; ++pp) {
+                            if (pp < np) {
+                                const float4 x = *reinterpret_cast<const float4*>(xp + pp * B);
+                                mn.x = fmin_nan(mn.x, x.x); mn.y = fmin_nan(mn.y, x.y);
+                                mn.z = fmin_nan(mn.z, x.z); mn.w = fmin_nan(mn.w, x.w);
+                                mx.x = fmaxf(mx.x, x.x); mx.y = fmaxf(mx.y, x.y); mx.z = fmaxf(mx.z, x.z); mx.w = fmaxf(mx.w, x.w);
+                            }
+                        }
+                        if (c == 0 && h == 0) {  // centre: the first 32 pixels, per 8-pixel group as stats_i8_kernel
+                            double4 cs = make_double4(0.0, 0.0, 0.0, 0.0);
+                            for (int pp = 0; pp < np; ++pp) {
+                                const float4 x = *reinterpret_cast<const float4*>(xp + pp * B);
+                                cs.x += double(x.x); cs.y += double(x.y); cs.z += double(x.z); cs.w += double(x.w);
+                            }
+                            red_cs[wr][4 * lane] = cs.x; red_cs[wr][4 * lane + 1] = cs.y;
+                            red_cs[wr][4 * lane + 2] = cs.z; red_cs[wr][4 * lane + 3] = cs.w;
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&empty1[st]);
+                    atomicAdd(&p1_count, 1);
+                }
+                if (++st == NS1) {
+                    st = 0;
+                    ph ^= 1u;
+                }
+            }
+            // ---- range step of line k: centre and per-dim scale into the line's parity slot
+            const bool bad_mine = quad_live && !(isfinite(mn.x) && isfinite(mn.y) && isfinite(mn.z) && isfinite(mn.w) &&
+                                                 isfinite(mx.x) && isfinite(mx.y) && isfinite(mx.z) && isfinite(mx.w));
+            if (quad_live) {
+                *reinterpret_cast<float4*>(&red_mn[wr][4 * lane]) = mn;
+                *reinterpret_cast<float4*>(&red_mx[wr][4 * lane]) = mx;
+            }
+            const unsigned bw = __ballot_sync(0xffffffffu, bad_mine);
+            bar_range();
+            const int par = k & 1;
+            if (k >= 2) tc::mbar_wait(&sfree[par], uint32_t((k - 2) >> 1) & 1u);  // line k-2 done with the slot
+            if (lane == 0) bad_s[par][wr] = bw != 0;
+            {
+                const int d = t2;
+                float cd = 0.f, sd = 0.f;
+                const float ad = kMagic + (d == D ? 256.f : 0.f);  // ones row: q = 256
+                if (d < D) {
+                    const int n0 = min(32, P);
+                    const double c0 = red_cs[0][d] + red_cs[1][d] + red_cs[2][d] + red_cs[3][d];
+                    cd = float(c0 / double(n0));
+                    float lo = red_mn[0][d], hi = red_mx[0][d];
+                    for (int w = 1; w < 4; ++w) {
+                        lo = fminf(lo, red_mn[w][d]);
+                        hi = fmaxf(hi, red_mx[w][d]);
+                    }
+                    const float m = fmaxf(hi - cd, cd - lo);
+                    sd = i8::v_scale(m);
+                    if (a.vmax) a.vmax[size_t(blockIdx.x + k * gridDim.x) * D + d] = m;
+                }
+                cen_s[par][d] = cd;
+                scale_s[par][d] = sd;
+                add_s[par][d] = ad;
+                inv_s[par][d] = sd > 0.f ? 1.0 / double(sd) : 0.0;
+            }
+            bar_range();  // (red_* are rewritten by the next line's pass 1 only after every thread read them)
+            if (lane == 0) mbar_arrive(&sready[par]);
+            if (lane == 0 && wr == 0) TR(11, k, 0);
+        }
+        return;
+    }
+
+    // ---------------- warps 0-7: quantise (pass 2) and the epilogue of every line
+    const int lane_grp = warp & 3, colh = warp >> 2;
+    const int row = lane_grp * 32 + lane;
+    const uint32_t lane_base = uint32_t(lane_grp * 32) << 16;
+    const int ngrp = a.N / 16;
+    const int g0 = colh ? (ngrp + 1) / 2 : 0, g1 = colh ? ngrp : (ngrp + 1) / 2;
+    const int pg2 = warp & 3, dh = warp >> 2;
+    const int dd0 = lane + 64 * dh, dd1 = dd0 + 32;
+    const int ld0 = min(dd0, B - 1), ld1 = min(dd1, B - 1);
+    int st = 0;
+    uint32_t ph = 0;
+    int c0a = 0, c0b = 0;
+    for (int k = 0; k < my_lines; ++k) {
+        const int par = k & 1;
+        const int line = blockIdx.x + k * gridDim.x;
+        tc::mbar_wait(&sready[par], uint32_t(k >> 1) & 1u);
+        if (tid == 0) TR(0, k, 0);
+        const float cdk0 = cen_s[par][dd0 & 127], sdk0 = scale_s[par][dd0 & 127], adk0 = add_s[par][dd0 & 127];
+        const float cdk1 = cen_s[par][dd1 & 127], sdk1 = scale_s[par][dd1 & 127], adk1 = add_s[par][dd1 & 127];
+        for (int c = 0; c < nch; ++c) {
+            const int n = min(kCh, P - c * kCh);
+            const int k2 = k * nch + c, buf = k2 & 1;
+            tc::mbar_wait(&full2[st], ph);
+            if (tid == 0) TR(1, k, c);
+            if (k2 >= 2) tc::mbar_wait(&pempty[buf], uint32_t((k2 - 2) >> 1) & 1u);
+            if (tid == 0) TR(2, k, c);
+            const float* sb = ring2 + size_t(st) * kCh * B + (pg2 * 16) * B;
+            unsigned char* op = ops + buf * kOps;
+            uint32_t w[2][3][4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                uint32_t u0[4], u1[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float* xp = sb + (jj * 4 + e) * B;
+                    u0[e] = __float_as_uint(fmaf(xp[ld0] - cdk0, sdk0, adk0)) + (0x808080u - 0x4B400000u);
+                    u1[e] = __float_as_uint(fmaf(xp[ld1] - cdk1, sdk1, adk1)) + (0x808080u - 0x4B400000u);
+                    if (n != kCh && pg2 * 16 + jj * 4 + e >= n) u0[e] = u1[e] = 0x808080u;
+                }
+                pack_digits(u0, w[0][0][jj], w[0][1][jj], w[0][2][jj]);
+                pack_digits(u1, w[1][0][jj], w[1][1][jj], w[1][2][jj]);
+                c0a = __dp4a(int(w[0][0][jj]), int(w[0][0][jj]), c0a);
+                c0b = __dp4a(int(w[1][0][jj]), int(w[1][0][jj]), c0b);
+            }
+            const uint32_t off0 = tc::kmajor_off_s8(dd0, pg2 * 16), off1 = tc::kmajor_off_s8(dd1, pg2 * 16);
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl) {
+                *reinterpret_cast<uint4*>(op + pl * kPlane + off0) = make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
+                *reinterpret_cast<uint4*>(op + pl * kPlane + off1) = make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
+            }
+            tc::fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&empty2[st]);
+                mbar_arrive(&pfull[buf]);
+            }
+            if (tid == 0) TR(3, k, c);
+            if (++st == NS2) {
+                st = 0;
+                ph ^= 1u;
+            }
+            if (c == nch - 1) {  // the line's class-0 diagonal partials (folded by c0_fold_kernel)
+                int* c0l = a.c0 + size_t(line) * 4 * D + pg2 * D;
+                if (dd0 < D) c0l[dd0] = c0a;
+                if (dd1 < D) c0l[dd1] = c0b;
+                c0a = c0b = 0;
+            }
+            if (a.vplanes) {
+                const int gp = c * kCh + pg2 * 16;
+                unsigned char* vt = a.vplanes + (size_t(line) * ntile_v + (gp >> 7)) * i8::kTileBytes;
+                const uint64_t stream_out = tc::policy_evict_first();
+                const int used = i8::vplane_used_dims(D);
+#pragma unroll
+                for (int pl = 0; pl < 3; ++pl) {
+                    if (dd0 < used)
+                        tc::st16_hint(vt + i8::vplane_off(pl, dd0, gp & 127),
+                                      make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]), stream_out);
+                    if (dd1 < used)
+                        tc::st16_hint(vt + i8::vplane_off(pl, dd1, gp & 127),
+                                      make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]), stream_out);
+                }
+            }
+        }
+        // ---- epilogue of line k (stats_i8_kernel's, with the line's parity slot)
+        tc::mbar_wait(&accfull, uint32_t(k) & 1u);
+        if (tid == 0) TR(4, k, 0);
+        tc::tc_fence_after();
+        for (int gi = g0; gi < g1; ++gi) {
+            uint32_t v[4][16];
+            tc::tmem_ld16x4(tmem + lane_base + uint32_t(gi * 16), 128u, v);
+            if (row < D) {
+                const double ia = inv_s[par][row];
+#pragma unroll
+                for (int ii = 0; ii < 16; ++ii) {
+                    const int e = gi * 16 + ii;
+                    const long long si_i = (static_cast<long long>(int(v[3][ii])) << 32) +
+                                           (static_cast<long long>(int(v[2][ii])) << 24) +
+                                           (static_cast<long long>(int(v[1][ii])) << 16) +
+                                           (static_cast<long long>(int(v[0][ii])) << 8);
+                    const double si = double(si_i);
+                    if (e <= row) S[tri(row, e)] = si * ia * inv_s[par][e];
+                    if (e == D) sum_s[row] = si * (1.0 / 256.0) * ia;
+                }
+            }
+        }
+        tc::tc_fence_before();
+        bar_compute();
+        if (tid == 0) mbar_arrive(&accempty);
+        double* out = a.stats + size_t(line) * (g.SE + g.D);
+        const bool bad = bad_s[par][0] | bad_s[par][1] | bad_s[par][2] | bad_s[par][3];
+        const double poison = bad ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;
+        for (int i = tid; i < D; i += kThreads) {
+            out[i] = double(cen_s[par][i]) + poison;
+            out[D + i] = sum_s[i] + poison;
+        }
+        const int ntri = D * (D + 1) / 2;
+        for (int i = tid; i < ntri; i += kThreads) out[2 * D + i] = S[i] + poison;
+        bar_compute();  // S / sum_s rewritten by the next line; the parity slot is free for line k + 2
+        if (lane == 0) mbar_arrive(&sfree[par]);
+        if (tid == 0) TR(5, k, 0);
+    }
+    tc::tc_fence_before();
+    bar_compute();
+    if (warp == 0) tc::tmem_free<512>(tmem);
+}
+
 // S_aa += sum_p d0_a^2 / s_a^2 for every (line, dim): the class-0 diagonal the MMAs leave out, from the
 // quantiser's four pixel-group partials (exact int32 sums), scaled exactly as the epilogue scales S.
 __global__ void __launch_bounds__(256) c0_fold_kernel(int D, int SS, int n_lines, const int* __restrict__ c0,
@@ -498,7 +867,23 @@ void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in
     StatsI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, vmax, vplanes, c0, (g.D + 1 + 15) / 16 * 16,
                   i8_stages(g)};
     const int grid = n_lines_total < sms ? n_lines_total : sms;
-    if (g.B == 108)  // configs[0] / configs[3]
+    // the range pass on its own warps (stats_i8_ws_kernel) when the ring holds >= 5 stages: 3 for pass 1
+    // (HBM latency), the rest for pass 2 (measured at 108 bands: 0.269 -> 0.263 ms per 2048 lines);
+    // ERX_STATS_WS=0 forces the single-role kernel, =N sets the pass-1 stages (A/B hook)
+    static const int ws_env = [] {
+        const char* v = std::getenv("ERX_STATS_WS");
+        return v ? std::atoi(v) : -1;
+    }();
+    const int ws = ws_env >= 0 ? ws_env : (a.stages >= 5 ? 3 : 0);
+    a.ring1 = ws;
+    if (ws && a.stages >= ws + 1) {  // range pass on its own warps
+        ensure_smem(stats_i8_ws_kernel<0>, kSmemCap - kStaticSmem);
+        ensure_smem(stats_i8_ws_kernel<108>, kSmemCap - kStaticSmem);
+        if (g.B == 108)
+            stats_i8_ws_kernel<108><<<grid, kWsThreads, stats_i8_smem(g), st>>>(a);
+        else
+            stats_i8_ws_kernel<0><<<grid, kWsThreads, stats_i8_smem(g), st>>>(a);
+    } else if (g.B == 108)  // configs[0] / configs[3]
         stats_i8_kernel<108><<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
     else
         stats_i8_kernel<0><<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
@@ -507,3 +892,16 @@ void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in
 }
 
 }  // namespace erxk
+
+#ifdef ERX_X_TRACE
+extern "C" int erx_x_trace(unsigned long long* out, int n_pairs) {
+    unsigned int cnt = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&cnt, erxk::g_trace_n, sizeof(cnt));
+    const int m = int(cnt) < n_pairs ? int(cnt) : n_pairs;
+    cudaMemcpyFromSymbol(out, erxk::g_trace, size_t(m) * 2 * sizeof(unsigned long long));
+    const unsigned int zero = 0;
+    cudaMemcpyToSymbol(erxk::g_trace_n, &zero, sizeof(zero));
+    return m;
+}
+#endif
