@@ -647,6 +647,23 @@ __device__ __forceinline__ int diag_factor8(float (&row)[kBlk], unsigned gmask, 
     return f;
 }
 
+#ifdef ERX_X_TRACE  // A/B timeline instrumentation of one CTA (tools/factor_trace.py)
+__device__ unsigned long long g_ftrace[1 << 14];
+__device__ unsigned int g_ftrace_n;
+__device__ __forceinline__ void ftrace(int id, int k, int t) {
+    if (blockIdx.x == 1000) {
+        const unsigned i = atomicAdd(&g_ftrace_n, 1u);
+        if (i < (1u << 13)) {
+            g_ftrace[2 * i] = clock64();
+            g_ftrace[2 * i + 1] = (unsigned long long)((id << 24) | (k << 12) | t);
+        }
+    }
+}
+#define FTR(id, k, t) ftrace(id, k, t)
+#else
+#define FTR(id, k, t)
+#endif
+
 // fp32 blocked factor, one CTA of NT threads per line.  The minimum-blocks bound keeps
 // 64- and 128-thread CTAs at <= 72 registers so the seven lines that fit shared memory (configs[3]) are
 // all resident.
@@ -747,7 +764,9 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
         }
         __syncthreads();
         fail = s_fail;
+        FTR(0, 0, tid);
         for (int k = 0; k < nb && fail < 0; ++k) {
+            FTR(1, k, tid);
             const float* Di = BP(k, k);
             // (b) panel rows I > k (tasks 0 ..) and finalisation of block row k (J < k); Di and Di^T rows
             // are broadcasts
@@ -797,19 +816,27 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
                     st8r(blk, r, acc);
                 }
             }
+            FTR(2, k, tid);
             __syncthreads();
+            FTR(3, k, tid);
             // (c) trailing Cholesky update A_IJ -= L_Ik L_Jk^T (I >= J > k), then inverse update
             // T_IJ -= L_Ik X_kJ (I > k, J < k).  Task = (block pair, row r = tid % 8); pairs run
             // column-major (stride nt / 8, decoded incrementally), so the four lane groups of a warp
             // mostly share J and the 16 right-operand row loads are one address per warp (Lc rows
             // of neighbouring J sit on different banks: stride kLcLd)
+            // Warp 0 owns pair 0 (block (k+1, k+1): update, then the 8-lane factor + inverse for the next
+            // step) and nothing else: its other lanes would wait out that divergent, shuffle-bound chain
+            // (measured ~6k cycles) before their own tasks and hold the step's barrier (the timeline in
+            // tools/factor_trace.py); the other warps take the remaining pairs with stride (nt - 32) / 8.
             {
-                constexpr int step = nt / kBlk;
+                constexpr int step = (nt - 32) / kBlk;
                 const int r = gl;
                 const int m = nb - k - 1;
                 float a[kBlk], acc[kBlk];
-                int jr = 0, ir = tid >> 3;  // trailing pair: column jr, row ir (relative to k + 1), ir >= jr
-                if (ir == 0 && m > 0) {
+                const bool dwarp = tid < 32;
+                // trailing pair: column jr, row ir (relative to k + 1), ir >= jr; flat index 0 is pair 0
+                int jr = 0, ir = dwarp ? 0 : (tid >> 3) - 3;
+                if (tid < kBlk && m > 0) {
                     // pair 0 = block (k+1, k+1) first, outside the loop (keeps the loop's registers low):
                     // update, then factor + invert it for the next step
                     float* blk = BP(k + 1, k + 1);
@@ -825,10 +852,12 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
                         acc[c] = dot8_sub(na, b, acc[c]);
                     }
                     st8r(blk, r, acc);
+                    FTR(5, k, tid);
                     const int f = diag_factor8(acc, gmask, gl, (k + 1) * kBlk, blk, DiT, dg);
+                    FTR(6, k, tid);
                     if (gl == 0 && f >= 0) s_fail = f;
-                    ir = step;
                 }
+                if (dwarp) jr = m;  // no trailing / inverse pairs for warp 0
                 while (ir >= m && jr < m) {
                     ir = ir - m + jr + 1;
                     ++jr;
@@ -855,7 +884,7 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
                     }
                 }
                 // inverse pairs: the flat index continues past the m (m + 1) / 2 trailing pairs
-                if (k > 0 && m > 0) {
+                if (k > 0 && m > 0 && !dwarp) {
                     int J;
                     // ir - m + jr + 1 overshoots as if column m had rows from m: rebase to the inverse range
                     ir = ir - jr;  // == flat index past the trailing pairs (jr == m here)
@@ -897,10 +926,12 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
                     }
                 }
             }
+            FTR(4, k, tid);
             __syncthreads();
             fail = s_fail;
         }
     }
+    FTR(7, 0, tid);
     if (fail >= 0) {  // the fp64 rescue (k_fixup.cu) redoes this line, escalation included
         if (tid == 0) list_for_fixup(fixlist, status, line);
         return;
@@ -911,6 +942,7 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
     } else {
         write_wblocks(whiten, line, g, [&](int i, int j) { return *EL(i, j); });
     }
+    FTR(8, 0, tid);
     if (tid == 0) status[line] = -1;
 }
 
@@ -1330,3 +1362,16 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
 }
 
 }  // namespace erxk
+
+#ifdef ERX_X_TRACE
+extern "C" int erx_x_ftrace(unsigned long long* out, int n_pairs) {
+    unsigned int cnt = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&cnt, erxk::g_ftrace_n, sizeof(cnt));
+    const int m = int(cnt) < n_pairs ? int(cnt) : n_pairs;
+    cudaMemcpyFromSymbol(out, erxk::g_ftrace, size_t(m) * 2 * sizeof(unsigned long long));
+    const unsigned int zero = 0;
+    cudaMemcpyToSymbol(erxk::g_ftrace_n, &zero, sizeof(zero));
+    return m;
+}
+#endif
