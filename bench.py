@@ -109,9 +109,10 @@ class StubEngine:
         return (self.t[b] - self.t[a]) * 1e3
 
 
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02_ncu_full_c3.txt")
-NCU_NAMES = {"stats": ("stats_i8_kernel", "stats_kernel", "stats_small"), "score": ("score_i8_kernel", "score_kernel"),
-             "factor": ("factor_blk_kernel",), "scan": ("scan_kernel",), "normalize": ("normalize_kernel",)}
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02c_ncu_full_c3.txt")  # one group of 2048 lines per launch
+NCU_NAMES = {"stats": ("stats_i8_ws_kernel", "stats_i8_kernel", "stats_kernel", "stats_small"),
+             "score": ("score_i8_kernel", "score_kernel"), "factor": ("factor_blk_kernel",),
+             "scan": ("scan_tile_kernel", "scan_kernel"), "normalize": ("normalize_kernel",)}
 
 
 def ncu_traffic(kernel):

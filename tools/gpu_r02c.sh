@@ -9,7 +9,7 @@ python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/ref_r02c.json
 python bench.py --steps 2 --warmup 3 --quick --no-cpu > gpurun_out/plain_launch.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_r02c.csv \
     python bench.py --steps 2 --warmup 3 --quick --no-cpu > gpurun_out/ncu_launch.log 2>&1; echo launches rc=$?
-python tools/kt_probe.py 3 full 0 3 > gpurun_out/plain_c3.log 2>&1 && \
+ERX_DEVICE_GROUPS=1 python tools/kt_probe.py 3 full 0 3 > gpurun_out/plain_c3.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"stats_i8_ws_kernel|stats_i8_kernel|c0_fold|scan_kernel|factor_blk|score_i8_kernel|normalize|fixup" \
-    -s 7 -c 7 -o gpurun_out/r02c_c3 python tools/kt_probe.py 3 full 0 3 > gpurun_out/ncu_c3.log 2>&1
+    -s 7 -c 7 -o gpurun_out/r02c_c3 env ERX_DEVICE_GROUPS=1 python tools/kt_probe.py 3 full 0 3 > gpurun_out/ncu_c3.log 2>&1
 echo ncu rc=$?
