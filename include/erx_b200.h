@@ -182,6 +182,10 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
  * kernels and tails of one group overlap the other group's kernels; auto splits windows of >= 1024
  * lines.  Per-kernel profiling runs one group. */
 #define ERX_OPT_DEVICE_GROUPS 7
+/* ERX_OPT_STATS_SPLIT: 3 (default), 0..3.  The exact-integer statistics (16 < D <= 127) run the range
+ * pass on its own warps with this many of the ring's stages (stats_i8_ws_kernel, where the ring holds
+ * two more); 0 runs the single-role kernel (stats_i8_kernel).  Bit-identical results. */
+#define ERX_OPT_STATS_SPLIT 8
 int erx_set_option(erx_engine* e, int option, int64_t value);
 int64_t erx_get_option(const erx_engine* e, int option);
 

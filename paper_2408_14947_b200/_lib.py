@@ -29,6 +29,7 @@ OPT_ASYNC_HOST = 4
 OPT_FACTOR_THREADS = 5
 OPT_GRAPHS = 6
 OPT_DEVICE_GROUPS = 7
+OPT_STATS_SPLIT = 8
 
 
 class ErxConfigC(C.Structure):

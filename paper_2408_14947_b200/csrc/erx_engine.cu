@@ -131,6 +131,7 @@ struct erx_engine {
     // with its own rescue list / workspace, so one group's small kernels and tails overlap the other's
     static constexpr int kDevGroups = 2;
     int dev_groups = 0;          // 0 auto, 1 or 2
+    int stats_split = 3;         // ERX_OPT_STATS_SPLIT: pass-1 stages of the split statistics kernel (0: single role)
     cudaStream_t stream2 = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t rescued_before = 0;  // rescued lines counted by earlier (re-planned) lists
@@ -442,7 +443,7 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
         if (e->small)
             erxk::launch_stats_small(g, e->smp, xg, int(n), int(in_stride), L, stats, vcache, st);
         else if (tensor)
-            erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, vmax, vplanes, c0, st);
+            erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, vmax, vplanes, c0, st, e->stats_split);
         else if (e->wide_i8)
             stats_rc = erxk::launch_stats_i8t(g, xg, int(n), int(in_stride), int(ns), stats, cen, vmax, vplanes,
                                               st);
@@ -1137,6 +1138,11 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
         e->factor_threads = int(value);
         return ERX_OK;
     }
+    if (option == ERX_OPT_STATS_SPLIT) {
+        if (value < 0 || value > 3) return fail(e, ERX_ERR_CONFIG, "stats split: 0..3");
+        e->stats_split = int(value);
+        return ERX_OK;
+    }
     if (option == ERX_OPT_DEVICE_GROUPS) {
         if (value < 0 || value > erx_engine::kDevGroups) return fail(e, ERX_ERR_CONFIG, "device groups: 0, 1 or 2");
         e->dev_groups = int(value);
@@ -1185,6 +1191,7 @@ int64_t erx_get_option(const erx_engine* e, int option) {
     if (option == ERX_OPT_HOST_GROUPS) return e->host_groups;
     if (option == ERX_OPT_GRAPHS) return e->use_graphs ? 1 : 0;
     if (option == ERX_OPT_DEVICE_GROUPS) return e->dev_groups;
+    if (option == ERX_OPT_STATS_SPLIT) return e->stats_split;
     if (option == ERX_OPT_FACTOR_THREADS) return e->factor_threads;
     if (option == ERX_OPT_ASYNC_HOST) return e->async_host ? 1 : 0;
     if (option == ERX_OPT_STATS_TENSOR) {

@@ -116,11 +116,13 @@ size_t factor_smem(const Geometry& g, int precision);
 // Exact-integer tcgen05 stats kernel (k_stats_i8.cu): no_srp, 16 < D <= 127, B % 4 == 0.
 bool stats_i8_eligible(const Geometry& g);
 // vmax / vplanes (may be null): [line][D] max_p |fl32(x - c)| and the score's v digit planes
-// (vplanes_bytes_per_line per line).
+// (vplanes_bytes_per_line per line).  ring1 > 0: the range pass on its own warps with ring1 of the
+// ring's stages (stats_i8_ws_kernel, where the ring holds ring1 + 2); 0: the single-role kernel.
 // c0: [line][4][D] int32 scratch for the class-0 diagonal partials (folded into S_aa by a second,
 // tiny kernel of this launcher).
 void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
-                     double* stats, float* vmax, unsigned char* vplanes, int* c0, cudaStream_t st);
+                     double* stats, float* vmax, unsigned char* vplanes, int* c0, cudaStream_t st,
+                     int ring1 = 3);
 // Exact-integer tcgen05 stats for wide lines (k_stats_i8t.cu): no_srp, 127 < D <= 512, B % 4 == 0;
 // work items are the lower-triangle pairs of 128-dim tiles, 2D TMA boxes from the line.  Returns 0, or
 // non-zero when the tensor map could not be encoded (nothing launched).

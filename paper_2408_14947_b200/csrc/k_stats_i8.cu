@@ -860,23 +860,18 @@ bool stats_i8_eligible(const Geometry& g) {
 }
 
 void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
-                     double* stats, float* vmax, unsigned char* vplanes, int* c0, cudaStream_t st) {
+                     double* stats, float* vmax, unsigned char* vplanes, int* c0, cudaStream_t st, int ring1) {
     const int sms = sm_count();
     ensure_smem(stats_i8_kernel<0>, kSmemCap - kStaticSmem);
     ensure_smem(stats_i8_kernel<108>, kSmemCap - kStaticSmem);
     StatsI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, vmax, vplanes, c0, (g.D + 1 + 15) / 16 * 16,
                   i8_stages(g)};
     const int grid = n_lines_total < sms ? n_lines_total : sms;
-    // the range pass on its own warps (stats_i8_ws_kernel) when the ring holds >= 5 stages: 3 for pass 1
-    // (HBM latency), the rest for pass 2 (measured at 108 bands: 0.269 -> 0.263 ms per 2048 lines);
-    // ERX_STATS_WS=0 forces the single-role kernel, =N sets the pass-1 stages (A/B hook)
-    static const int ws_env = [] {
-        const char* v = std::getenv("ERX_STATS_WS");
-        return v ? std::atoi(v) : -1;
-    }();
-    const int ws = ws_env >= 0 ? ws_env : (a.stages >= 5 ? 3 : 0);
+    // ring1 > 0: the range pass on its own warps (stats_i8_ws_kernel) with ring1 pass-1 stages, where
+    // the ring holds at least ring1 + 2 (ERX_OPT_STATS_SPLIT); 0: the single-role kernel
+    const int ws = (ring1 > 0 && a.stages >= ring1 + 2) ? ring1 : 0;
     a.ring1 = ws;
-    if (ws && a.stages >= ws + 1) {  // range pass on its own warps
+    if (ws) {  // range pass on its own warps
         ensure_smem(stats_i8_ws_kernel<0>, kSmemCap - kStaticSmem);
         ensure_smem(stats_i8_ws_kernel<108>, kSmemCap - kStaticSmem);
         if (g.B == 108)

@@ -272,6 +272,10 @@ class Engine:
         """0 auto, 32 or 64 (see ERX_OPT_FACTOR_PRECISION in include/erx_b200.h)."""
         self._check(self._lib.erx_set_option(self._h, L.OPT_FACTOR_PRECISION, bits))
 
+    def set_stats_split(self, ring1: int):
+        """Pass-1 stages of the split statistics kernel, 0 for the single-role kernel (ERX_OPT_STATS_SPLIT)."""
+        self._check(self._lib.erx_set_option(self._h, L.OPT_STATS_SPLIT, int(ring1)))
+
     def set_device_groups(self, groups: int):
         """Device stream groups per window: 0 auto, 1 or 2 (ERX_OPT_DEVICE_GROUPS)."""
         self._check(self._lib.erx_set_option(self._h, L.OPT_DEVICE_GROUPS, int(groups)))

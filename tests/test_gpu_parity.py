@@ -656,3 +656,31 @@ def test_device_groups_bitwise(pkg, no_srp):
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
         assert o[1] == outs[0][1]
     assert outs[0][1] > 0  # the rescue ran (in group 1 when split: streams 4-7)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cid,S,P,B", [(3, 8, 640, 108), (0, 1, 384, 108), (3, 4, 200, 40)])
+def test_stats_split_bitwise(pkg, cid, S, P, B):
+    """ERX_OPT_STATS_SPLIT: the statistics kernel with the range pass on its own warps (default, its own
+    HBM ring, per-parity scale hand-off) and the single-role kernel give the same bits — the split
+    changes only who reads what when, never the arithmetic."""
+    import torch
+
+    T = 16
+    host = np.stack([pkg.gen_lines(pkg.gen_spec(cid, s), 0, 2 * T)[0][:, :P, :B] for s in range(S)])
+    dev = torch.from_numpy(np.ascontiguousarray(host.reshape(S, 2, T, P, B).transpose(1, 0, 2, 3, 4))).cuda()
+    outs = []
+    for split in (0, 3):
+        eng = pkg.Engine(pkg.ErxConfig(no_srp=True), B, S, T)
+        eng.set_stats_split(split)
+        raw = torch.empty((S, T, P), dtype=torch.float32, device="cuda")
+        norm = torch.empty_like(raw)
+        res = []
+        for w in range(2):
+            eng.run_device(dev[w].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr(), first_index=w * T)
+            eng.sync()
+            res.append((raw.cpu().numpy().copy(), norm.cpu().numpy().copy()))
+        outs.append(res)
+        eng.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
