@@ -707,6 +707,7 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
     const double eps = eps0;
     int fail;
     const int ntri = D * (D + 1) / 2;
+    FTR(9, 0, tid);
     {
         if (tid == 0) s_fail = -1;
         if (kblk) {

@@ -49,5 +49,10 @@ for k in steps:
           f"{min(s4) - max(s3):6d}..{max(s4) - max(s3):6d} "
           f"{(min(ts(1) if False else s4) if False else 0):1d}"
           f" diag {((min(s5) - max(s3)) if s5 else -1):6d}..{((max(s6) - max(s3)) if s6 else -1):6d}")
-e7, e8 = [e[0] - t0 for e in ev if e[1] == 7], [e[0] - t0 for e in ev if e[1] == 8]
-print("sweep done", max(e7), "planes written", max(e8))
+def last(i):
+    v = [e[0] - t0 for e in ev if e[1] == i]
+    return max(v) if v else None
+def first(i):
+    v = [e[0] - t0 for e in ev if e[1] == i]
+    return min(v) if v else None
+print("kernel start", first(9), "sweep start", first(0), "sweep done", last(7), "planes written", last(8))
