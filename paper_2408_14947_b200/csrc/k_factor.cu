@@ -700,8 +700,8 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
     // Lc + DiT after the factorisation)
     float* dg = Lc + (size_t(nb) * kLcLd + 64 > 384 ? size_t(nb) * kLcLd + 64 : 384);
     const int line = blockIdx.x, tid = threadIdx.x;
-    constexpr int nt = NT, nw = NT / 32;
-    const int lane = tid & 31, gl = lane & 7, warp = tid >> 5, grp = lane >> 3;
+    constexpr int nt = NT;
+    const int lane = tid & 31, gl = lane & 7;
     const unsigned gmask = 0xffu << (lane & 24);
     const double* K = prior + size_t(line) * g.SE + D;
     const double eps = eps0;

@@ -55,7 +55,6 @@ constexpr int kCh = 64;                                   // pixels per chunk (2
 constexpr int kMaxStages = 8;                             // bulk-copy ring depth (upper bound)
 constexpr uint32_t kPlane = (kCh / 32) * tc::kSliceBytes;  // 8 KB: 128 rows x 64 int8
 constexpr uint32_t kOps = 3 * kPlane;                     // d0, d1, d2 planes
-constexpr float kR = 4194000.f;                           // |q| <= 2^22: exact fma rounding, d2 in int8
 constexpr float kMagic = 12582912.f;                      // 1.5 * 2^23
 constexpr int kThreads = 256;
 constexpr size_t kSmemCap = 232448;  // 227 KB per CTA
