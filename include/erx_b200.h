@@ -186,6 +186,17 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
  * pass on its own warps with this many of the ring's stages (stats_i8_ws_kernel, where the ring holds
  * two more); 0 runs the single-role kernel (stats_i8_kernel).  Bit-identical results. */
 #define ERX_OPT_STATS_SPLIT 8
+/* ERX_OPT_STATS_ONEPASS: 8 (default), 0, 2, 4, 8, 16 or 32.  The exact-integer statistics (16 < D <= 127)
+ * read every line ONCE: the per-dim quantisation range is predicted as this factor times the range of
+ * the line's first 64 pixels, every quantised value is checked against the digit range, and a line with
+ * any value outside (or a non-finite one) is redone by the two-pass kernel with its exact range
+ * (stats_i8_op_kernel, then stats_i8_kernel over the listed lines).  0 runs the two-pass kernels for
+ * every line (ERX_OPT_STATS_SPLIT picks which).  Lines of one chunk (<= 64 pixels) get their exact range
+ * either way.  Results per line depend on that line only (window cuts do not change a bit); the wider
+ * predicted range costs ~2.6 of the quantiser's 22 bits on a clean line.
+ * ERX_OPT_STATS_REDONE (read-only): lines the two-pass kernel has redone so far. */
+#define ERX_OPT_STATS_ONEPASS 9
+#define ERX_OPT_STATS_REDONE 10
 int erx_set_option(erx_engine* e, int option, int64_t value);
 int64_t erx_get_option(const erx_engine* e, int option);
 

@@ -30,6 +30,8 @@ OPT_FACTOR_THREADS = 5
 OPT_GRAPHS = 6
 OPT_DEVICE_GROUPS = 7
 OPT_STATS_SPLIT = 8
+OPT_STATS_ONEPASS = 9
+OPT_STATS_REDONE = 10
 
 
 class ErxConfigC(C.Structure):

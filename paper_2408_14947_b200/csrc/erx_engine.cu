@@ -89,6 +89,7 @@ struct erx_engine {
                                          // [S*T][pixel tiles][dim tiles][48 KB])
     unsigned char* d_wplw = nullptr;     // [S*T][wplanes_w_bytes] the wide score's int8 W operand
     int* d_c0 = nullptr;        // [S*T][4][D] class-0 diagonal partials of the integer statistics (tensor path)
+    int* d_redo = nullptr;      // [kDevGroups][S*T + 2] one-pass statistics: lines listed for the exact two-pass redo
     float* d_kblk = nullptr;    // [S*T][nb(nb+1)/2][64] pre-update K as fp32 blocks (blocked fp32 factor)
     int factor_req = 0;   // requested factor precision (0 auto, 32, 64)
     // ERX_OPT_STATS_TENSOR: 2 exact-integer tcgen05 stats + score where eligible (default), 0 FFMA kernels.
@@ -132,6 +133,8 @@ struct erx_engine {
     static constexpr int kDevGroups = 2;
     int dev_groups = 0;          // 0 auto, 1 or 2
     int stats_split = 3;         // ERX_OPT_STATS_SPLIT: pass-1 stages of the split statistics kernel (0: single role)
+    int stats_onepass = 8;       // ERX_OPT_STATS_ONEPASS: headroom of the one-pass statistics (0: the two-pass kernels)
+    int64_t redone_before = 0;   // redone lines counted by earlier (re-planned) lists
     cudaStream_t stream2 = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t rescued_before = 0;  // rescued lines counted by earlier (re-planned) lists
@@ -253,8 +256,21 @@ int64_t read_rescued(erx_engine* e) {
     return tot;
 }
 
+int64_t read_redone(erx_engine* e) {
+    if (!e->d_redo) return 0;
+    int64_t tot = 0;
+    cudaStreamSynchronize(e->stream);
+    for (int gi = 0; gi < erx_engine::kDevGroups; ++gi) {
+        int v = 0;
+        cudaMemcpy(&v, e->d_redo + size_t(gi) * (size_t(e->S) * e->T + 2) + 1, sizeof(int), cudaMemcpyDeviceToHost);
+        tot += v;
+    }
+    return tot;
+}
+
 void free_window(erx_engine* e) {
     e->rescued_before += read_rescued(e);
+    e->redone_before += read_redone(e);
     cudaFree(e->d_lines);
     cudaFree(e->d_stats);
     cudaFree(e->d_prior);
@@ -275,6 +291,8 @@ void free_window(erx_engine* e) {
     e->d_wplw = nullptr;
     cudaFree(e->d_c0);
     e->d_c0 = nullptr;
+    cudaFree(e->d_redo);
+    e->d_redo = nullptr;
     cudaFree(e->d_kblk);
     e->d_kblk = nullptr;
     cudaFree(e->d_fix);
@@ -352,6 +370,10 @@ int configure(erx_engine* e, uint32_t P) {
         CU(cudaMalloc(&e->d_wplw, L * erxk::wplanes_w_bytes_per_line(g)));
     }
     if (e->tensor) CU(cudaMalloc(&e->d_c0, L * 4 * size_t(g.D) * sizeof(int)));
+    if (e->tensor) {
+        CU(cudaMalloc(&e->d_redo, erx_engine::kDevGroups * (L + 2) * sizeof(int)));
+        CU(cudaMemset(e->d_redo, 0, erx_engine::kDevGroups * (L + 2) * sizeof(int)));
+    }
     if (e->factor_prec == 32) CU(cudaMalloc(&e->d_kblk, L * erxk::whiten_floats_per_line(g) * sizeof(float)));
     // fp64 rescue list (fed by the fp32 factors and by the normalisation's flat-line check)
     CU(cudaMalloc(&e->d_fix, erx_engine::kDevGroups * (L + 3) * sizeof(int)));
@@ -434,6 +456,7 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
     unsigned char* wplw = e->d_wplw ? e->d_wplw + l0 * erxk::wplanes_w_bytes_per_line(g) : nullptr;
     float* kblk = e->d_kblk ? e->d_kblk + l0 * erxk::whiten_floats_per_line(g) : nullptr;
     int* c0 = (e->tensor && e->d_c0) ? e->d_c0 + l0 * 4 * size_t(g.D) : nullptr;
+    int* redo = (e->d_redo && e->stats_onepass > 0) ? e->d_redo + size_t(grp) * (size_t(e->S) * e->T + 2) : nullptr;
     const bool tensor = e->tensor;
     int* status = e->d_status + l0;
     float* rawg = raw ? raw + l0 * g.P : nullptr;
@@ -443,7 +466,8 @@ int enqueue_window(erx_engine* e, const float* x, uint32_t n, uint32_t in_stride
         if (e->small)
             erxk::launch_stats_small(g, e->smp, xg, int(n), int(in_stride), L, stats, vcache, st);
         else if (tensor)
-            erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, vmax, vplanes, c0, st, e->stats_split);
+            erxk::launch_stats_i8(g, xg, int(n), int(in_stride), L, stats, vmax, vplanes, c0, st, e->stats_split,
+                                  redo, e->stats_onepass);
         else if (e->wide_i8)
             stats_rc = erxk::launch_stats_i8t(g, xg, int(n), int(in_stride), int(ns), stats, cen, vmax, vplanes,
                                               st);
@@ -1143,6 +1167,12 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
         e->stats_split = int(value);
         return ERX_OK;
     }
+    if (option == ERX_OPT_STATS_ONEPASS) {
+        if (value != 0 && value != 2 && value != 4 && value != 8 && value != 16 && value != 32)
+            return fail(e, ERX_ERR_CONFIG, "stats one-pass headroom: 0, 2, 4, 8, 16 or 32");
+        e->stats_onepass = int(value);
+        return ERX_OK;
+    }
     if (option == ERX_OPT_DEVICE_GROUPS) {
         if (value < 0 || value > erx_engine::kDevGroups) return fail(e, ERX_ERR_CONFIG, "device groups: 0, 1 or 2");
         e->dev_groups = int(value);
@@ -1192,6 +1222,8 @@ int64_t erx_get_option(const erx_engine* e, int option) {
     if (option == ERX_OPT_GRAPHS) return e->use_graphs ? 1 : 0;
     if (option == ERX_OPT_DEVICE_GROUPS) return e->dev_groups;
     if (option == ERX_OPT_STATS_SPLIT) return e->stats_split;
+    if (option == ERX_OPT_STATS_ONEPASS) return e->stats_onepass;
+    if (option == ERX_OPT_STATS_REDONE) return const_cast<erx_engine*>(e)->redone_before + read_redone(const_cast<erx_engine*>(e));
     if (option == ERX_OPT_FACTOR_THREADS) return e->factor_threads;
     if (option == ERX_OPT_ASYNC_HOST) return e->async_host ? 1 : 0;
     if (option == ERX_OPT_STATS_TENSOR) {

@@ -120,9 +120,12 @@ bool stats_i8_eligible(const Geometry& g);
 // ring's stages (stats_i8_ws_kernel, where the ring holds ring1 + 2); 0: the single-role kernel.
 // c0: [line][4][D] int32 scratch for the class-0 diagonal partials (folded into S_aa by a second,
 // tiny kernel of this launcher).
+// redo + headroom > 0: the one-pass kernel (stats_i8_op_kernel: range predicted as headroom x the range
+// of the line's first chunk) followed by the exact two-pass kernel over the lines it lists in redo
+// ([0] count, [1] running total, [2 ..] line ids; n_lines_total + 2 ints, zeroed once by the caller).
 void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
                      double* stats, float* vmax, unsigned char* vplanes, int* c0, cudaStream_t st,
-                     int ring1 = 3);
+                     int ring1 = 3, int* redo = nullptr, int headroom = 0);
 // Exact-integer tcgen05 stats for wide lines (k_stats_i8t.cu): no_srp, 127 < D <= 512, B % 4 == 0;
 // work items are the lower-triangle pairs of 128-dim tiles, 2D TMA boxes from the line.  Returns 0, or
 // non-zero when the tensor map could not be encoded (nothing launched).

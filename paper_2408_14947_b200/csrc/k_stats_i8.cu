@@ -57,6 +57,33 @@ constexpr uint32_t kPlane = (kCh / 32) * tc::kSliceBytes;  // 8 KB: 128 rows x 6
 constexpr uint32_t kOps = 3 * kPlane;                     // d0, d1, d2 planes
 constexpr float kMagic = 12582912.f;                      // 1.5 * 2^23
 constexpr int kThreads = 256;
+// Digit planes of one chunk in shared memory: per 32-pixel K-slice the three planes d0, d1, d2 one after
+// the other (128 rows x 32 B each, canonical K-major), so a B descriptor that starts at plane i and runs
+// past its 128 rows continues into plane i + 1: one MMA of N = 128 + N' multiplies an A plane with TWO
+// B planes and lands in two neighbouring class accumulators (128 TMEM columns apart).
+constexpr uint32_t kSliceOps = 3 * tc::kSliceBytes;
+__device__ __forceinline__ uint32_t plane_off(int m, int k) {  // int8 element (row m, pixel k) of plane 0
+    return uint32_t(k >> 5) * kSliceOps + uint32_t(m >> 3) * 256u + uint32_t((k >> 4) & 1) * 128u +
+           uint32_t(m & 7) * 16u + uint32_t(k & 15);
+}
+// The 8 digit-plane pairs (i, j), i + j >= 1, of one chunk (2 K-slices) as 5 MMAs per slice; class
+// i + j - 1 accumulates at TMEM column 128 (i + j - 1).  first: the line's first chunk (accumulators
+// are overwritten by the first MMA that reaches them).  Integer sums: any order gives the same bits.
+__device__ __forceinline__ void issue_chunk_mmas(uint32_t tmem, uint32_t base, int Nn, bool first) {
+    const uint32_t id_cat = tc::idesc_s8_s32(128, 128 + Nn), id_one = tc::idesc_s8_s32(128, Nn);
+#pragma unroll
+    for (int s = 0; s < kCh / 32; ++s) {
+        const uint32_t sb = base + s * kSliceOps;
+        const uint64_t d0 = tc::smem_desc(sb), d1 = tc::smem_desc(sb + tc::kSliceBytes),
+                       d2 = tc::smem_desc(sb + 2 * tc::kSliceBytes);
+        const uint32_t acc = (first && s == 0) ? 0u : 1u;
+        tc::mma_s8(tmem, d0, d1, id_cat, acc);         // (0,1) -> class 0, (0,2) -> class 1
+        tc::mma_s8(tmem, d1, d0, id_cat, 1u);          // (1,0) -> class 0, (1,1) -> class 1
+        tc::mma_s8(tmem + 256u, d1, d2, id_one, acc);  // (1,2) -> class 2
+        tc::mma_s8(tmem + 128u, d2, d0, id_cat, 1u);   // (2,0) -> class 1, (2,1) -> class 2
+        tc::mma_s8(tmem + 384u, d2, d2, id_one, acc);  // (2,2) -> class 3
+    }
+}
 constexpr size_t kSmemCap = 232448;  // 227 KB per CTA
 
 struct StatsI8Args {
@@ -72,7 +99,18 @@ struct StatsI8Args {
     int N;       // MMA N = roundup16(D + 1)
     int stages;  // ring depth
     int ring1;   // stats_i8_ws: stages of the pass-1 ring (the rest: pass 2)
+    // one-pass statistics (stats_i8_op_kernel): lines whose values leave the predicted range are listed
+    // here ([0] count of this launch, [1] running total, [2..] line ids) and redone by stats_i8_kernel,
+    // which then walks the list instead of the line range
+    int* redo;
+    float headroom;  // one-pass: range = headroom x the range of the line's first chunk (a power of two)
 };
+
+// line handled at step k of this CTA: the k-th of its share of the range, or of the redo list
+__device__ __forceinline__ int line_at(const StatsI8Args& a, bool listed, int k) {
+    const int i = blockIdx.x + k * gridDim.x;
+    return listed ? a.redo[2 + i] : i;
+}
 
 __device__ __forceinline__ void pack_digits(const uint32_t (&u)[4], uint32_t& w0, uint32_t& w1, uint32_t& w2) {
     const uint32_t t01 = __byte_perm(u[0], u[1], 0x5140), t23 = __byte_perm(u[2], u[3], 0x5140);
@@ -101,7 +139,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* m) {
 // MMAs of line k-1 have long finished.
 // kBT > 0: the band count as a compile-time constant (the pixel stride of every shared-memory chunk
 // access folds into immediate offsets); 0: runtime g.B
-template <int kBT>
+template <int kBT, bool kListed = false>
 __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args a) {
     extern __shared__ __align__(1024) unsigned char smem[];
     __shared__ uint32_t tmem_slot;
@@ -128,7 +166,10 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     double* S = reinterpret_cast<double*>(tri_bytes <= 2 * kOps ? smem : smem + 2 * kOps + size_t(NS) * kCh * B * 4);
     const int nch = (P + kCh - 1) / kCh;
     const int ntile_v = (P + 127) / 128;  // score tiles per line (v planes)
-    const int my_lines = blockIdx.x < a.n_lines ? (a.n_lines - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const bool listed = kListed;  // redo pass of the one-pass statistics: the lines of a.redo
+    const int n_lines = listed ? min(a.redo[0], a.n_lines) : a.n_lines;
+    const int my_lines = blockIdx.x < n_lines ? (n_lines - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (listed && my_lines == 0) return;  // (the usual case: nothing listed)
 
     // Ring: chunk loads in one sequence, slot j % NS.  Step k interleaves pass 1 (range) of line k
     // with pass 2 (quantise + MMA) of line k-1, chunk by chunk, so the HBM stream of one line runs
@@ -161,7 +202,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
             const uint64_t keep = tc::policy_evict_last(), drop = tc::policy_evict_first();
             auto load = [&](int k, int c, bool again) {
                 if (rnd >= 1) tc::mbar_wait(&empty[st], (rnd - 1) & 1u);
-                const int line = blockIdx.x + k * gridDim.x;
+                const int line = line_at(a, listed, k);
                 const int n = min(kCh, P - c * kCh);
                 const uint32_t bytes = uint32_t(n) * B * 4;
                 const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
@@ -184,8 +225,6 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     if (warp == 9) {
         // ---------------- MMA issuer: 2 K-steps x 8 digit-plane pairs per chunk
         if (lane == 0) {
-            const uint32_t idesc = tc::idesc_s8_s32(128, a.N);
-            const int pr[8][3] = {{0, 1, 0}, {1, 0, 0}, {0, 2, 1}, {1, 1, 1}, {2, 0, 1}, {1, 2, 2}, {2, 1, 2}, {2, 2, 3}};
             for (int k = 0; k < my_lines; ++k) {
                 if (k >= 1) tc::mbar_wait(&accempty, uint32_t(k - 1) & 1u);
                 for (int c = 0; c < nch; ++c) {
@@ -193,15 +232,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                     tc::mbar_wait(&pfull[buf], uint32_t(k2 >> 1) & 1u);
                     tc::tc_fence_after();
                     const uint32_t base = tc::smem_u32(ops + buf * kOps);
-#pragma unroll
-                    for (int s = 0; s < kCh / 32; ++s)
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const uint64_t ad = tc::smem_desc(base + pr[q][0] * kPlane + s * tc::kSliceBytes);
-                            const uint64_t bd = tc::smem_desc(base + pr[q][1] * kPlane + s * tc::kSliceBytes);
-                            const bool first = c == 0 && s == 0 && (q == 0 || q == 2 || q == 5 || q == 7);
-                            tc::mma_s8(tmem + uint32_t(pr[q][2]) * 128u, ad, bd, idesc, first ? 0u : 1u);
-                        }
+                    issue_chunk_mmas(tmem, base, a.N, c == 0);
                     tc::mma_commit(&pempty[buf]);
                 }
                 tc::mma_commit(&accfull);
@@ -227,7 +258,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
 
     // epilogue of line kk: S_int = sum_c 2^(8c) acc_c scaled by 1 / (s_a s_b), staged in smem, then stored
     auto epilogue = [&](int kk) {
-        const int line = blockIdx.x + kk * gridDim.x;
+        const int line = line_at(a, listed, kk);
         tc::mbar_wait(&accfull, uint32_t(kk) & 1u);
         tc::tc_fence_after();
         for (int gi = g0; gi < g1; ++gi) {
@@ -370,11 +401,11 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                         c0b = __dp4a(int(w[1][0][jj]), int(w[1][0][jj]), c0b);
                     }
                 }
-                const uint32_t off0 = tc::kmajor_off_s8(dd0, pg2 * 16), off1 = tc::kmajor_off_s8(dd1, pg2 * 16);
+                const uint32_t off0 = plane_off(dd0, pg2 * 16), off1 = plane_off(dd1, pg2 * 16);
 #pragma unroll
                 for (int pl = 0; pl < 3; ++pl) {
-                    *reinterpret_cast<uint4*>(op + pl * kPlane + off0) = make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
-                    *reinterpret_cast<uint4*>(op + pl * kPlane + off1) = make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
+                    *reinterpret_cast<uint4*>(op + pl * tc::kSliceBytes + off0) = make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
+                    *reinterpret_cast<uint4*>(op + pl * tc::kSliceBytes + off1) = make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
                 }
                 tc::fence_proxy_async();
                 __syncwarp();
@@ -383,7 +414,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                     mbar_arrive(&pfull[buf]);
                 }
                 if (c == nch - 1) {  // the line's class-0 diagonal partials (consumed by the scan)
-                    int* c0l = a.c0 + size_t(blockIdx.x + (k - 1) * gridDim.x) * 4 * D + pg2 * D;
+                    int* c0l = a.c0 + size_t(line_at(a, listed, k - 1)) * 4 * D + pg2 * D;
                     if (dd0 < D) c0l[dd0] = c0a;
                     if (dd1 < D) c0l[dd1] = c0b;
                     c0a = c0b = 0;
@@ -391,7 +422,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                 if (a.vplanes) {
                     // the same digits, as the score kernel's MN-major A operand (i8::vplane_off): one warp
                     // writes 2 x 512 contiguous bytes per plane
-                    const int line = blockIdx.x + (k - 1) * gridDim.x;
+                    const int line = line_at(a, listed, k - 1);
                     const int gp = c * kCh + pg2 * 16;
                     unsigned char* vt = a.vplanes + (size_t(line) * ntile_v + (gp >> 7)) * i8::kTileBytes;
                     const uint64_t stream_out = tc::policy_evict_first();  // do not push x out of L2
@@ -438,7 +469,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
                 }
                 const float m = fmaxf(hi - cd, cd - lo);
                 sd = i8::v_scale(m);
-                if (a.vmax) a.vmax[size_t(blockIdx.x + k * gridDim.x) * D + d] = m;
+                if (a.vmax) a.vmax[size_t(line_at(a, listed, k)) * D + d] = m;
             }
             cen_s[d] = cd;
             scale_s[d] = sd;
@@ -452,17 +483,6 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_kernel(StatsI8Args 
     if (warp == 0) tc::tmem_free<512>(tmem);
 }
 
-// ---------------------------------------------------------------------------
-// stats_i8_ws: the same statistics with the range pass on its own warps.  In stats_i8_kernel the
-// eight compute warps run the range pass of line k, the quantise pass of line k-1, its epilogue and
-// the range step one after the other; measured, that chain (not the loads) bounds the kernel
-// (DESIGN.md §6).  Here warps 8-11 stream pass 1 (range of line k, its own ring, HBM, evict_last)
-// and hand each line's centre / scale to the quantise warps through per-parity shared arrays
-// (sready / sfree mbarriers), so the range pass runs beside the quantise / MMA / epilogue chain of
-// warps 0-7.  The pass-2 producer re-reads a chunk from L2 only once the range warps have passed it
-// (a monotonic chunk count).  Arithmetic per line is the stats_i8_kernel's (bit-identical output).
-// Warps: 0-7 quantise + epilogue, 8-11 range, 12 pass-1 producer, 13 pass-2 producer, 14 MMA issuer.
-// ---------------------------------------------------------------------------
 #ifdef ERX_X_TRACE  // A/B timeline instrumentation of CTA 0 (tools/stats_trace.py)
 __device__ unsigned long long g_trace[1 << 16];
 __device__ unsigned int g_trace_n;
@@ -479,6 +499,318 @@ __device__ __forceinline__ void trace_ev(int id, int k, int c) {
 #else
 #define TR(id, k, c)
 #endif
+// ---------------------------------------------------------------------------
+// stats_i8_op: the same statistics in ONE pass over the line.  The two-pass kernels read every line
+// twice (range, then quantise) because the quantisation scale is the line's exact per-dim range; both
+// reads cross the L2 fabric, and with the digit planes written for the score kernel that traffic (not
+// the tensor core, not the quantiser) bounds them.  Here the scale is PREDICTED from the
+// line's first chunk: range_d = headroom x max over the first 64 pixels of |x_d - c_d| (headroom a
+// power of two, 8 by default; a line of one chunk gets its exact range, i.e. the two-pass result).  The
+// quantiser then runs straight off the HBM stream, every ring stage feeding it, and checks every
+// rounded value against the digit range [-2^22, 2^22] (two min / max per element on the fma result,
+// which also catches NaN and +-inf).  A line with any value outside is appended to a.redo and redone,
+// exactly, by stats_i8_kernel<., true> (the next launch on the stream); its outputs here are
+// overwritten.  A dim that is constant over the first chunk gets a huge quantiser scale (any later
+// deviation overflows and lists the line) while its statistics scale stays 0 as in the two-pass kernels.
+// Per line the result depends on that line only, so re-cutting the windows does not change a bit.
+// Cost: the predicted range is ~headroom / 1.3 wider than the exact one on a clean line, i.e. ~2.6 bits
+// of the 22 (tools/emulate_onepass.py; the parity gates hold with the margin recorded in DESIGN.md).
+// Warps: 0-7 range of chunk 0, quantise, epilogue; 8 producer; 9 MMA issuer (as stats_i8_kernel).
+// ---------------------------------------------------------------------------
+constexpr float kYLo = 8388608.f, kYHi = 16777216.f;  // kMagic -+ 2^22: the fma results of in-range values
+
+template <int kBT>
+__global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_op_kernel(StatsI8Args a) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+    __shared__ __align__(8) uint64_t pfull[2], pempty[2], accfull, accempty;
+    __shared__ __align__(16) float red_mn[8][128];
+    __shared__ __align__(16) float red_mx[8][128];
+    __shared__ double red_cs[4][128];
+    __shared__ float cen_s[128], scale_s[128], add_s[128];
+    __shared__ double inv_s[128];
+    __shared__ double sum_s[128];
+    __shared__ int bad_s[8];
+
+    const Geometry& g = a.g;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int B = kBT > 0 ? kBT : g.B, D = g.D, P = g.P;
+    const int NS = a.stages;
+
+    unsigned char* ops = smem;                                   // [2][kOps]
+    float* ring = reinterpret_cast<float*>(smem + 2 * kOps);     // [NS][kCh * B]
+    const size_t tri_bytes = size_t(D) * (D + 1) / 2 * 8;
+    double* S = reinterpret_cast<double*>(tri_bytes <= 2 * kOps ? smem : smem + 2 * kOps + size_t(NS) * kCh * B * 4);
+    const int nch = (P + kCh - 1) / kCh;
+    const int ntile_v = (P + 127) / 128;
+    const int my_lines = blockIdx.x < a.n_lines ? (a.n_lines - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 8);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&pfull[b], 8);
+            tc::mbar_init(&pempty[b], 1);
+        }
+        tc::mbar_init(&accfull, 1);
+        tc::mbar_init(&accempty, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 0) tc::tmem_alloc<512>(&tmem_slot);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+
+    if (warp == 8) {
+        // ---------------- producer: every chunk once, straight from HBM (nothing is read again)
+        if (lane == 0) {
+            int st = 0;
+            uint32_t rnd = 0;
+            const uint64_t drop = tc::policy_evict_first();
+            for (int k = 0; k < my_lines; ++k) {
+                const float* xl = line_ptr(a.x, blockIdx.x + k * gridDim.x, a.n, a.in_stride, g);
+                for (int c = 0; c < nch; ++c) {
+                    if (rnd >= 1) tc::mbar_wait(&empty[st], (rnd - 1) & 1u);
+                    TR(30, k, c);
+                    const uint32_t bytes = uint32_t(min(kCh, P - c * kCh)) * B * 4;
+                    tc::mbar_expect_tx(&full[st], bytes);
+                    tc::bulk_g2s_hint(ring + size_t(st) * kCh * B, xl + size_t(c) * kCh * B, bytes, &full[st], drop);
+                    if (++st == NS) {
+                        st = 0;
+                        ++rnd;
+                    }
+                }
+            }
+        }
+        return;
+    }
+    if (warp == 9) {
+        // ---------------- MMA issuer: 2 K-steps x 8 digit-plane pairs per chunk (as stats_i8_kernel)
+        if (lane == 0) {
+            for (int k = 0; k < my_lines; ++k) {
+                if (k >= 1) tc::mbar_wait(&accempty, uint32_t(k - 1) & 1u);
+                for (int c = 0; c < nch; ++c) {
+                    const int k2 = k * nch + c, buf = k2 & 1;
+                    tc::mbar_wait(&pfull[buf], uint32_t(k2 >> 1) & 1u);
+                    tc::tc_fence_after();
+                    const uint32_t base = tc::smem_u32(ops + buf * kOps);
+                    issue_chunk_mmas(tmem, base, a.N, c == 0);
+                    tc::mma_commit(&pempty[buf]);
+                }
+                tc::mma_commit(&accfull);
+            }
+        }
+        return;
+    }
+
+    // ---------------- compute warps 0-7
+    const int lane_grp = warp & 3, colh = warp >> 2;
+    const int row = lane_grp * 32 + lane;
+    const uint32_t lane_base = uint32_t(lane_grp * 32) << 16;
+    const int ngrp = a.N / 16;
+    const int g0 = colh ? (ngrp + 1) / 2 : 0, g1 = colh ? ngrp : (ngrp + 1) / 2;
+    const bool quad_live = 4 * lane < B;  // range mapping: warp = 8-pixel group, lane = 4 consecutive dims
+    const int pg2 = warp & 3, dh = warp >> 2;  // quantise mapping (stats_i8_kernel's)
+    const int dd0 = lane + 64 * dh, dd1 = dd0 + 32;
+    const int ld0 = min(dd0, B - 1), ld1 = min(dd1, B - 1);
+    const float head = nch > 1 ? a.headroom : 1.f;
+
+    int jst = 0;
+    uint32_t jph = 0;
+    int c0a = 0, c0b = 0;
+    for (int k = 0; k < my_lines; ++k) {
+        const int line = blockIdx.x + k * gridDim.x;
+        float cdk0 = 0.f, sdk0 = 0.f, adk0 = kMagic, cdk1 = 0.f, sdk1 = 0.f, adk1 = kMagic;
+        float ylo = kMagic, yhi = kMagic;
+        for (int c = 0; c < nch; ++c) {
+            const int n = min(kCh, P - c * kCh);
+            const int st = jst;
+            const int k2 = k * nch + c, buf = k2 & 1;
+            tc::mbar_wait(&full[st], jph);
+            if (tid == 0) TR(1, k, c);
+            if (++jst == NS) {
+                jst = 0;
+                jph ^= 1u;
+            }
+            if (c == 0) {
+                // ---- the line's centre and predicted range, from the chunk just landed
+                float4 mn = make_float4(3.402823466e38f, 3.402823466e38f, 3.402823466e38f, 3.402823466e38f);
+                float4 mx = make_float4(-3.402823466e38f, -3.402823466e38f, -3.402823466e38f, -3.402823466e38f);
+                if (quad_live) {
+                    const int p0 = warp * 8;
+                    const float* xp = ring + size_t(st) * kCh * B + p0 * B + 4 * lane;
+                    const int np = min(8, n - p0);
+                    for (int pp = 0; pp < np; ++pp) {
+                        const float4 x = *reinterpret_cast<const float4*>(xp + pp * B);
+                        mn.x = fmin_nan(mn.x, x.x); mn.y = fmin_nan(mn.y, x.y);
+                        mn.z = fmin_nan(mn.z, x.z); mn.w = fmin_nan(mn.w, x.w);
+                        mx.x = fmaxf(mx.x, x.x); mx.y = fmaxf(mx.y, x.y); mx.z = fmaxf(mx.z, x.z); mx.w = fmaxf(mx.w, x.w);
+                    }
+                    if (warp < 4) {  // centre: the first 32 pixels, per 8-pixel group (k_stats.cu's rule)
+                        double4 cs = make_double4(0.0, 0.0, 0.0, 0.0);
+                        for (int pp = 0; pp < np; ++pp) {
+                            const float4 x = *reinterpret_cast<const float4*>(xp + pp * B);
+                            cs.x += double(x.x); cs.y += double(x.y); cs.z += double(x.z); cs.w += double(x.w);
+                        }
+                        red_cs[warp][4 * lane] = cs.x; red_cs[warp][4 * lane + 1] = cs.y;
+                        red_cs[warp][4 * lane + 2] = cs.z; red_cs[warp][4 * lane + 3] = cs.w;
+                    }
+                    *reinterpret_cast<float4*>(&red_mn[warp][4 * lane]) = mn;
+                    *reinterpret_cast<float4*>(&red_mx[warp][4 * lane]) = mx;
+                }
+                bar_compute();
+                if (tid < 128) {
+                    const int d = tid;
+                    float cd = 0.f, sd = 0.f, sq = 0.f;
+                    const float ad = kMagic + (d == D ? 256.f : 0.f);  // ones row: q = 256
+                    if (d < D) {
+                        const int n0 = min(32, P);
+                        const double c0 = red_cs[0][d] + red_cs[1][d] + red_cs[2][d] + red_cs[3][d];
+                        cd = float(c0 / double(n0));
+                        float lo = red_mn[0][d], hi = red_mx[0][d];
+                        for (int w = 1; w < 8; ++w) {  // (groups past the line's end hold the neutral +-FLT_MAX)
+                            lo = fminf(lo, red_mn[w][d]);
+                            hi = fmaxf(hi, red_mx[w][d]);
+                        }
+                        const float m = head * fmaxf(hi - cd, cd - lo);
+                        sd = i8::v_scale(m);
+                        // a dim with no range in the first chunk: any later deviation must overflow
+                        sq = sd > 0.f ? sd : (nch > 1 ? 3.0e38f : 0.f);
+                        if (a.vmax) a.vmax[size_t(line) * D + d] = (m <= 3.402823466e38f) ? m : 0.f;
+                    }
+                    cen_s[d] = cd;
+                    scale_s[d] = sq;
+                    add_s[d] = ad;
+                    inv_s[d] = sd > 0.f ? 1.0 / double(sd) : 0.0;
+                }
+                bar_compute();
+                cdk0 = cen_s[dd0 & 127]; sdk0 = scale_s[dd0 & 127]; adk0 = add_s[dd0 & 127];
+                cdk1 = cen_s[dd1 & 127]; sdk1 = scale_s[dd1 & 127]; adk1 = add_s[dd1 & 127];
+                if (tid == 0) TR(6, k, c);
+            }
+            // ---- quantise the chunk into digit planes (stats_i8_kernel's arithmetic) and check the range
+            if (k2 >= 2) tc::mbar_wait(&pempty[buf], uint32_t((k2 - 2) >> 1) & 1u);
+            if (tid == 0) TR(2, k, c);
+            const float* sb = ring + size_t(st) * kCh * B + (pg2 * 16) * B;
+            unsigned char* op = ops + buf * kOps;
+            uint32_t w[2][3][4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                uint32_t u0[4], u1[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float* xp = sb + (jj * 4 + e) * B;
+                    float y0 = fmaf(xp[ld0] - cdk0, sdk0, adk0), y1 = fmaf(xp[ld1] - cdk1, sdk1, adk1);
+                    if (n != kCh && pg2 * 16 + jj * 4 + e >= n) y0 = y1 = kMagic;  // past the line's end
+                    ylo = fmin_nan(fmin_nan(ylo, y0), y1);
+                    yhi = fmaxf(fmaxf(yhi, y0), y1);
+                    u0[e] = __float_as_uint(y0) + (0x808080u - 0x4B400000u);
+                    u1[e] = __float_as_uint(y1) + (0x808080u - 0x4B400000u);
+                }
+                pack_digits(u0, w[0][0][jj], w[0][1][jj], w[0][2][jj]);
+                pack_digits(u1, w[1][0][jj], w[1][1][jj], w[1][2][jj]);
+                c0a = __dp4a(int(w[0][0][jj]), int(w[0][0][jj]), c0a);
+                c0b = __dp4a(int(w[1][0][jj]), int(w[1][0][jj]), c0b);
+            }
+            const uint32_t off0 = plane_off(dd0, pg2 * 16), off1 = plane_off(dd1, pg2 * 16);
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl) {
+                *reinterpret_cast<uint4*>(op + pl * tc::kSliceBytes + off0) = make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
+                *reinterpret_cast<uint4*>(op + pl * tc::kSliceBytes + off1) = make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
+            }
+            tc::fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&empty[st]);
+                mbar_arrive(&pfull[buf]);
+            }
+            if (tid == 0) TR(3, k, c);
+            if (c == nch - 1) {  // the line's class-0 diagonal partials (folded by c0_fold_kernel)
+                int* c0l = a.c0 + size_t(line) * 4 * D + pg2 * D;
+                if (dd0 < D) c0l[dd0] = c0a;
+                if (dd1 < D) c0l[dd1] = c0b;
+                c0a = c0b = 0;
+            }
+            if (a.vplanes) {
+                const int gp = c * kCh + pg2 * 16;
+                unsigned char* vt = a.vplanes + (size_t(line) * ntile_v + (gp >> 7)) * i8::kTileBytes;
+                const uint64_t stream_out = tc::policy_evict_first();
+                const int used = i8::vplane_used_dims(D);
+#pragma unroll
+                for (int pl = 0; pl < 3; ++pl) {
+                    if (dd0 < used)
+                        tc::st16_hint(vt + i8::vplane_off(pl, dd0, gp & 127),
+                                      make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]), stream_out);
+                    if (dd1 < used)
+                        tc::st16_hint(vt + i8::vplane_off(pl, dd1, gp & 127),
+                                      make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]), stream_out);
+                }
+            }
+        }
+        // ---- every rounded value inside the digit range?  (false for NaN / inf as well)
+        const bool bad_mine = !(ylo >= kYLo && yhi <= kYHi);
+        const unsigned bw = __ballot_sync(0xffffffffu, bad_mine);
+        if (lane == 0) bad_s[warp] = bw != 0;
+        // ---- epilogue (stats_i8_kernel's); a line out of range is listed for the redo pass instead
+        if (tid == 0) TR(7, k, 0);
+        tc::mbar_wait(&accfull, uint32_t(k) & 1u);
+        if (tid == 0) TR(4, k, 0);
+        tc::tc_fence_after();
+        for (int gi = g0; gi < g1; ++gi) {
+            uint32_t v[4][16];
+            tc::tmem_ld16x4(tmem + lane_base + uint32_t(gi * 16), 128u, v);
+            if (row < D) {
+                const double ia = inv_s[row];
+#pragma unroll
+                for (int ii = 0; ii < 16; ++ii) {
+                    const int e = gi * 16 + ii;
+                    const long long si_i = (static_cast<long long>(int(v[3][ii])) << 32) +
+                                           (static_cast<long long>(int(v[2][ii])) << 24) +
+                                           (static_cast<long long>(int(v[1][ii])) << 16) +
+                                           (static_cast<long long>(int(v[0][ii])) << 8);
+                    const double si = double(si_i);
+                    if (e <= row) S[tri(row, e)] = si * ia * inv_s[e];
+                    if (e == D) sum_s[row] = si * (1.0 / 256.0) * ia;
+                }
+            }
+        }
+        tc::tc_fence_before();
+        bar_compute();
+        if (tid == 0) TR(8, k, 0);
+        if (tid == 0) mbar_arrive(&accempty);  // TMEM free for the next line's MMAs
+        const bool bad = bad_s[0] | bad_s[1] | bad_s[2] | bad_s[3] | bad_s[4] | bad_s[5] | bad_s[6] | bad_s[7];
+        if (bad) {
+            if (tid == 0) a.redo[2 + atomicAdd(&a.redo[0], 1)] = line;
+        } else {
+            double* out = a.stats + size_t(line) * (g.SE + g.D);
+            for (int i = tid; i < D; i += kThreads) {
+                out[i] = double(cen_s[i]);
+                out[D + i] = sum_s[i];
+            }
+            const int ntri = D * (D + 1) / 2;
+            for (int i = tid; i < ntri; i += kThreads) out[2 * D + i] = S[i];
+        }
+        bar_compute();  // S / sum_s / cen_s / bad_s are rewritten for the next line
+        if (tid == 0) TR(5, k, 0);
+    }
+    if (warp == 0) tc::tmem_free<512>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// stats_i8_ws: the same statistics with the range pass on its own warps.  In stats_i8_kernel the
+// eight compute warps run the range pass of line k, the quantise pass of line k-1, its epilogue and
+// the range step one after the other; measured, that chain (not the loads) bounds the kernel
+// (DESIGN.md §6).  Here warps 8-11 stream pass 1 (range of line k, its own ring, HBM, evict_last)
+// and hand each line's centre / scale to the quantise warps through per-parity shared arrays
+// (sready / sfree mbarriers), so the range pass runs beside the quantise / MMA / epilogue chain of
+// warps 0-7.  The pass-2 producer re-reads a chunk from L2 only once the range warps have passed it
+// (a monotonic chunk count).  Arithmetic per line is the stats_i8_kernel's (bit-identical output).
+// Warps: 0-7 quantise + epilogue, 8-11 range, 12 pass-1 producer, 13 pass-2 producer, 14 MMA issuer.
+// ---------------------------------------------------------------------------
 constexpr int kWsThreads = 480;
 constexpr int kWsRing1 = 2;  // pass-1 stages (the range pass consumes fast); the rest go to pass 2
 
@@ -573,8 +905,6 @@ __global__ void __launch_bounds__(kWsThreads, 1) stats_i8_ws_kernel(StatsI8Args 
     if (warp == 14) {
         // ---------------- MMA issuer: 2 K-steps x 8 digit-plane pairs per chunk (as stats_i8_kernel)
         if (lane == 0) {
-            const uint32_t idesc = tc::idesc_s8_s32(128, a.N);
-            const int pr[8][3] = {{0, 1, 0}, {1, 0, 0}, {0, 2, 1}, {1, 1, 1}, {2, 0, 1}, {1, 2, 2}, {2, 1, 2}, {2, 2, 3}};
             for (int k = 0; k < my_lines; ++k) {
                 if (k >= 1) tc::mbar_wait(&accempty, uint32_t(k - 1) & 1u);
                 for (int c = 0; c < nch; ++c) {
@@ -583,15 +913,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) stats_i8_ws_kernel(StatsI8Args 
                     TR(20, k, c);
                     tc::tc_fence_after();
                     const uint32_t base = tc::smem_u32(ops + buf * kOps);
-#pragma unroll
-                    for (int s = 0; s < kCh / 32; ++s)
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const uint64_t ad = tc::smem_desc(base + pr[q][0] * kPlane + s * tc::kSliceBytes);
-                            const uint64_t bd = tc::smem_desc(base + pr[q][1] * kPlane + s * tc::kSliceBytes);
-                            const bool first = c == 0 && s == 0 && (q == 0 || q == 2 || q == 5 || q == 7);
-                            tc::mma_s8(tmem + uint32_t(pr[q][2]) * 128u, ad, bd, idesc, first ? 0u : 1u);
-                        }
+                    issue_chunk_mmas(tmem, base, a.N, c == 0);
                     tc::mma_commit(&pempty[buf]);
                     TR(21, k, c);
                 }
@@ -736,11 +1058,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) stats_i8_ws_kernel(StatsI8Args 
                 c0a = __dp4a(int(w[0][0][jj]), int(w[0][0][jj]), c0a);
                 c0b = __dp4a(int(w[1][0][jj]), int(w[1][0][jj]), c0b);
             }
-            const uint32_t off0 = tc::kmajor_off_s8(dd0, pg2 * 16), off1 = tc::kmajor_off_s8(dd1, pg2 * 16);
+            const uint32_t off0 = plane_off(dd0, pg2 * 16), off1 = plane_off(dd1, pg2 * 16);
 #pragma unroll
             for (int pl = 0; pl < 3; ++pl) {
-                *reinterpret_cast<uint4*>(op + pl * kPlane + off0) = make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
-                *reinterpret_cast<uint4*>(op + pl * kPlane + off1) = make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
+                *reinterpret_cast<uint4*>(op + pl * tc::kSliceBytes + off0) = make_uint4(w[0][pl][0], w[0][pl][1], w[0][pl][2], w[0][pl][3]);
+                *reinterpret_cast<uint4*>(op + pl * tc::kSliceBytes + off1) = make_uint4(w[1][pl][0], w[1][pl][1], w[1][pl][2], w[1][pl][3]);
             }
             tc::fence_proxy_async();
             __syncwarp();
@@ -821,8 +1143,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) stats_i8_ws_kernel(StatsI8Args 
 // S_aa += sum_p d0_a^2 / s_a^2 for every (line, dim): the class-0 diagonal the MMAs leave out, from the
 // quantiser's four pixel-group partials (exact int32 sums), scaled exactly as the epilogue scales S.
 __global__ void __launch_bounds__(256) c0_fold_kernel(int D, int SS, int n_lines, const int* __restrict__ c0,
-                                                      const float* __restrict__ vmax, double* __restrict__ stats) {
+                                                      const float* __restrict__ vmax, double* __restrict__ stats,
+                                                      int* redo) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 && redo) {  // the one-pass statistics' redo list: consumed by the launch before this one
+        redo[1] += redo[0];
+        redo[0] = 0;
+    }
     if (i >= n_lines * D) return;
     const int line = i / D, a = i - line * D;
     const float s = i8::v_scale(vmax[i]);
@@ -859,13 +1186,32 @@ bool stats_i8_eligible(const Geometry& g) {
 }
 
 void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in_stride, int n_lines_total,
-                     double* stats, float* vmax, unsigned char* vplanes, int* c0, cudaStream_t st, int ring1) {
+                     double* stats, float* vmax, unsigned char* vplanes, int* c0, cudaStream_t st, int ring1,
+                     int* redo, int headroom) {
     const int sms = sm_count();
     ensure_smem(stats_i8_kernel<0>, kSmemCap - kStaticSmem);
     ensure_smem(stats_i8_kernel<108>, kSmemCap - kStaticSmem);
     StatsI8Args a{g, x, n_per_stream, in_stride, n_lines_total, stats, vmax, vplanes, c0, (g.D + 1 + 15) / 16 * 16,
-                  i8_stages(g)};
+                  i8_stages(g), 0, redo, float(headroom)};
     const int grid = n_lines_total < sms ? n_lines_total : sms;
+    if (redo && headroom > 0) {
+        // one pass with the predicted range, then the exact two-pass kernel over the lines it listed
+        ensure_smem(stats_i8_op_kernel<0>, kSmemCap - kStaticSmem);
+        ensure_smem(stats_i8_op_kernel<108>, kSmemCap - kStaticSmem);
+        ensure_smem(stats_i8_kernel<0, true>, kSmemCap - kStaticSmem);
+        ensure_smem(stats_i8_kernel<108, true>, kSmemCap - kStaticSmem);
+        if (g.B == 108) {
+            stats_i8_op_kernel<108><<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
+            stats_i8_kernel<108, true><<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
+        } else {
+            stats_i8_op_kernel<0><<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
+            stats_i8_kernel<0, true><<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
+        }
+        const int items = n_lines_total * g.D;
+        c0_fold_kernel<<<(items + 255) / 256, 256, 0, st>>>(g.D, g.SE + g.D, n_lines_total, c0, vmax, stats, redo);
+        return;
+    }
+    a.redo = nullptr;
     // ring1 > 0: the range pass on its own warps (stats_i8_ws_kernel) with ring1 pass-1 stages, where
     // the ring holds at least ring1 + 2 (ERX_OPT_STATS_SPLIT); 0: the single-role kernel
     const int ws = (ring1 > 0 && a.stages >= ring1 + 2) ? ring1 : 0;
@@ -882,7 +1228,7 @@ void launch_stats_i8(const Geometry& g, const float* x, int n_per_stream, int in
     else
         stats_i8_kernel<0><<<grid, kThreads + 64, stats_i8_smem(g), st>>>(a);
     const int items = n_lines_total * g.D;
-    c0_fold_kernel<<<(items + 255) / 256, 256, 0, st>>>(g.D, g.SE + g.D, n_lines_total, c0, vmax, stats);
+    c0_fold_kernel<<<(items + 255) / 256, 256, 0, st>>>(g.D, g.SE + g.D, n_lines_total, c0, vmax, stats, nullptr);
 }
 
 }  // namespace erxk

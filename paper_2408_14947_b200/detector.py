@@ -272,6 +272,14 @@ class Engine:
         """0 auto, 32 or 64 (see ERX_OPT_FACTOR_PRECISION in include/erx_b200.h)."""
         self._check(self._lib.erx_set_option(self._h, L.OPT_FACTOR_PRECISION, bits))
 
+    def set_stats_onepass(self, headroom: int):
+        """Headroom of the one-pass statistics' predicted range, 0 for the two-pass kernels (ERX_OPT_STATS_ONEPASS)."""
+        self._check(self._lib.erx_set_option(self._h, L.OPT_STATS_ONEPASS, int(headroom)))
+
+    def stats_redone_lines(self) -> int:
+        """Lines the one-pass statistics handed to the exact two-pass kernel so far (ERX_OPT_STATS_REDONE)."""
+        return int(self._lib.erx_get_option(self._h, L.OPT_STATS_REDONE))
+
     def set_stats_split(self, ring1: int):
         """Pass-1 stages of the split statistics kernel, 0 for the single-role kernel (ERX_OPT_STATS_SPLIT)."""
         self._check(self._lib.erx_set_option(self._h, L.OPT_STATS_SPLIT, int(ring1)))

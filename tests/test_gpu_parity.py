@@ -672,6 +672,7 @@ def test_stats_split_bitwise(pkg, cid, S, P, B):
     outs = []
     for split in (0, 3):
         eng = pkg.Engine(pkg.ErxConfig(no_srp=True), B, S, T)
+        eng.set_stats_onepass(0)  # the two-pass kernels for every line
         eng.set_stats_split(split)
         raw = torch.empty((S, T, P), dtype=torch.float32, device="cuda")
         norm = torch.empty_like(raw)
@@ -684,3 +685,82 @@ def test_stats_split_bitwise(pkg, cid, S, P, B):
         eng.close()
     for a, b in zip(outs[0], outs[1]):
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def _run_windows(pkg, dev, S, T, P, B, onepass, n_win=2):
+    import torch
+
+    eng = pkg.Engine(pkg.ErxConfig(no_srp=True), B, S, T)
+    eng.set_stats_onepass(onepass)
+    raw = torch.empty((S, T, P), dtype=torch.float32, device="cuda")
+    norm = torch.empty_like(raw)
+    res = []
+    for w in range(n_win):
+        eng.run_device(dev[w].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr(), first_index=w * T)
+        eng.sync()
+        res.append((raw.cpu().numpy().copy(), norm.cpu().numpy().copy()))
+    redone = eng.stats_redone_lines()
+    eng.close()
+    return res, redone
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("S,P,B", [(8, 640, 108), (3, 200, 40)])
+def test_stats_onepass_redo_is_the_two_pass_result(pkg, S, P, B):
+    """ERX_OPT_STATS_ONEPASS: a line whose values leave the range predicted from its first 64 pixels is
+    redone by the two-pass kernel.  With an outlier far beyond the headroom in EVERY line (after the first
+    chunk), every line is redone, so the one-pass run must give the two-pass bits; with a small headroom
+    (2) on ordinary lines some are redone and some are not, and the scores stay within the gates' reach
+    of the two-pass ones."""
+    import torch
+
+    T = 16
+    host = np.stack([pkg.gen_lines(pkg.gen_spec(3, s), 0, 2 * T)[0][:, :P, :B] for s in range(S)]).copy()
+    spiked = host.copy()
+    spiked[:, :, 100, :] += 1000.0 * np.abs(host).max()  # pixel 100: second chunk
+    for data, all_redone in ((spiked, True), (host, False)):
+        dev = torch.from_numpy(np.ascontiguousarray(data.reshape(S, 2, T, P, B).transpose(1, 0, 2, 3, 4))).cuda()
+        two, r0 = _run_windows(pkg, dev, S, T, P, B, 0)
+        one, r1 = _run_windows(pkg, dev, S, T, P, B, 8 if all_redone else 2)
+        assert r0 == 0
+        if all_redone:
+            assert r1 == 2 * S * T, r1
+            for a, b in zip(two, one):
+                assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        else:
+            assert 0 < r1 < 2 * S * T, r1
+            for a, b in zip(two, one):
+                rel = np.abs(a[0] - b[0]) / np.abs(a[0])
+                assert rel.max() < 1e-4 and np.median(rel) < 1e-5, (rel.max(), np.median(rel))
+
+
+@pytest.mark.gpu
+def test_stats_onepass_single_chunk_is_exact(pkg):
+    """Lines of one chunk (P <= 64) get their exact range in the one-pass kernel: the two-pass bits."""
+    import torch
+
+    S, T, P, B = 4, 16, 64, 108
+    host = np.stack([pkg.gen_lines(pkg.gen_spec(3, s), 0, 2 * T)[0][:, :P, :B] for s in range(S)])
+    dev = torch.from_numpy(np.ascontiguousarray(host.reshape(S, 2, T, P, B).transpose(1, 0, 2, 3, 4))).cuda()
+    two, _ = _run_windows(pkg, dev, S, T, P, B, 0)
+    one, redone = _run_windows(pkg, dev, S, T, P, B, 8)
+    assert redone == 0
+    for a, b in zip(two, one):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.gpu
+def test_stats_onepass_constant_first_chunk(pkg, oracle):
+    """A band that is constant over the line's first 64 pixels and varies later has no predicted range:
+    the line must be redone (not silently quantised to zero in that band)."""
+    spec = pkg.gen_spec(3, 0)
+    lines = pkg.gen_lines(spec, 0, 24)[0][:, :320, :].copy()
+    lines[:, :64, 7] = 0.25
+    cfg = pkg.ErxConfig(no_srp=True)
+    eng = pkg.Engine(cfg, lines.shape[2], 1, 8)
+    eng.push(lines[None], 0)
+    eng.finish()
+    assert eng.stats_redone_lines() == lines.shape[0]
+    _, _, raw, norm = eng.pop()
+    raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), lines)
+    check_gates(oracle, raw[0], norm[0], raw_o, norm_o, label="const-first-chunk")

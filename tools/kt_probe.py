@@ -26,6 +26,8 @@ norm = torch.empty_like(raw)
 eng = pkg.Engine(pkg.ErxConfig(no_srp=mode == "full", alpha=config["alpha"]), B, S, T)
 if os.environ.get("ERX_FACTOR"):
     eng.set_factor_precision(int(os.environ["ERX_FACTOR"]))
+if os.environ.get("ERX_STATS_ONEPASS"):
+    eng.set_stats_onepass(int(os.environ["ERX_STATS_ONEPASS"]))
 if os.environ.get("ERX_DEVICE_GROUPS"):
     eng.set_device_groups(int(os.environ["ERX_DEVICE_GROUPS"]))
 if os.environ.get("ERX_FACTOR_THREADS"):
@@ -43,5 +45,5 @@ for k in range(K):
     eng.run_device(dev[k % n_win].data_ptr(), T, P, raw.data_ptr(), norm.data_ptr(), first_index=k * T)
 eng.sync()
 kt = eng.kernel_times()
-print(os.environ.get("ERX_B200_LIB", "default"), f"factor={eng.factor_precision()}", f"c{cid} {mode} T={T}: {ms:.4f} ms/step, {S * T / ms * 1e3 / 1e6:.3f} M lines/s |",
+print(os.environ.get("ERX_B200_LIB", "default"), f"factor={eng.factor_precision()}", f"redone={eng.stats_redone_lines()}", f"c{cid} {mode} T={T}: {ms:.4f} ms/step, {S * T / ms * 1e3 / 1e6:.3f} M lines/s |",
       " ".join(f"{k} {v[0] / max(v[1], 1):.4f}" for k, v in kt.items()))

@@ -23,6 +23,8 @@ raw = torch.empty((S, T, P), dtype=torch.float32, device="cuda")
 norm = torch.empty_like(raw)
 eng = pkg.Engine(pkg.ErxConfig(no_srp=True, alpha=config["alpha"]), B, S, T)
 eng.set_graphs(False)
+if os.environ.get("ERX_STATS_ONEPASS"):
+    eng.set_stats_onepass(int(os.environ["ERX_STATS_ONEPASS"]))
 lib = C.CDLL(_lib.LIB_PATH)
 lib.erx_x_trace.restype = C.c_int
 buf = (C.c_ulonglong * (2 * 32768))()
@@ -36,7 +38,7 @@ n = lib.erx_x_trace(buf, 32768)
 a = np.frombuffer(buf, dtype=np.uint64, count=2 * n).reshape(n, 2)
 a = a[np.argsort(a[:, 0])]
 t0 = int(a[0, 0])
-names = {0: "Q sready", 1: "Q full2", 2: "Q pempty", 3: "Q planes", 4: "Q accfull", 5: "Q epi-done",
+names = {6: "Q range", 7: "Q quant-done", 8: "Q tmem-read", 0: "Q sready", 1: "Q full2", 2: "Q pempty", 3: "Q planes", 4: "Q accfull", 5: "Q epi-done",
          10: "R full1", 11: "R sready", 20: "M pfull", 21: "M commit", 30: "P1 issue", 31: "P2 issue"}
 lines = [(int(t) - t0, int(v) >> 24, (int(v) >> 12) & 0xfff, int(v) & 0xfff) for t, v in a]
 kmax = max(l[2] for l in lines)
@@ -49,5 +51,5 @@ for kk in (kmax // 2, kmax // 2 + 1):
 # per-line durations
 starts = {}
 for t, i, k, c in lines:
-    if i == 0: starts[k] = t
+    if i == 0 or (i == 1 and c == 0): starts[k] = t
 print("line starts (Q sready):", [starts.get(k) for k in range(kmax + 1)])
