@@ -186,9 +186,11 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
  * pass on its own warps with this many of the ring's stages (stats_i8_ws_kernel, where the ring holds
  * two more); 0 runs the single-role kernel (stats_i8_kernel).  Bit-identical results. */
 #define ERX_OPT_STATS_SPLIT 8
-/* ERX_OPT_STATS_ONEPASS: 8 (default), 0, 2, 4, 8, 16 or 32.  The exact-integer statistics (16 < D <= 127)
- * read every line ONCE: the per-dim quantisation range is predicted as this factor times the range of
- * the line's first 64 pixels, every quantised value is checked against the digit range, and a line with
+/* ERX_OPT_STATS_ONEPASS: 0 (default), 2, 4, 8, 16 or 32.  Opt-in (measured: no faster than the two-pass
+ * kernels on configs[3], 0.258 vs 0.254 ms per 2048 lines, and the wider predicted range fails the
+ * radiance-scale ill-conditioned gates, so it is off by default).  With a non-zero headroom the
+ * exact-integer statistics (16 < D <= 127) read every line ONCE: the per-dim quantisation range is
+ * predicted as this factor times the range of the line's first 64 pixels, every quantised value is checked against the digit range, and a line with
  * any value outside (or a non-finite one) is redone by the two-pass kernel with its exact range
  * (stats_i8_op_kernel, then stats_i8_kernel over the listed lines).  0 runs the two-pass kernels for
  * every line (ERX_OPT_STATS_SPLIT picks which).  Lines of one chunk (<= 64 pixels) get their exact range

@@ -133,7 +133,7 @@ struct erx_engine {
     static constexpr int kDevGroups = 2;
     int dev_groups = 0;          // 0 auto, 1 or 2
     int stats_split = 3;         // ERX_OPT_STATS_SPLIT: pass-1 stages of the split statistics kernel (0: single role)
-    int stats_onepass = 8;       // ERX_OPT_STATS_ONEPASS: headroom of the one-pass statistics (0: the two-pass kernels)
+    int stats_onepass = 0;       // ERX_OPT_STATS_ONEPASS: headroom of the one-pass statistics (0: the two-pass kernels)
     int64_t redone_before = 0;   // redone lines counted by earlier (re-planned) lists
     cudaStream_t stream2 = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;

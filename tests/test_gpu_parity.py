@@ -758,6 +758,7 @@ def test_stats_onepass_constant_first_chunk(pkg, oracle):
     lines[:, :64, 7] = 0.25
     cfg = pkg.ErxConfig(no_srp=True)
     eng = pkg.Engine(cfg, lines.shape[2], 1, 8)
+    eng.set_stats_onepass(8)  # opt-in (the two-pass kernels are the default)
     eng.push(lines[None], 0)
     eng.finish()
     assert eng.stats_redone_lines() == lines.shape[0]
