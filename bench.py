@@ -55,14 +55,19 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+LINES_PER_GPU_WINDOW = 4096
+
+
 def workload(cid, mode, world, window=0):
     """The benchmark workload of BASELINE.json configs[cid] at `world` ranks: (config dict shared by both
-    arms, streams per rank, window T).  The window (lag per stream) defaults to ~2048 lines per GPU
-    (T = 32 at N = 1, 256 at N = 8) so each GPU's launches stay full as the fixed streams spread out."""
+    arms, streams per rank, window T).  The window (lag per stream) defaults to ~4096 lines per GPU
+    (T = 64 at N = 1, 512 at N = 8) so each GPU's launches stay full as the fixed streams spread out
+    (measured on configs[3] D = B at N = 1: T = 32 / 48 / 64 / 96 -> 3.45 / 3.56 / 3.65 / 3.72 M lines/s;
+    a window of >= 1024 lines runs as two stream groups of half the streams on two CUDA streams)."""
     cfgd = CONFIGS[cid]
     S_tot = cfgd["streams"]
     S = max(1, S_tot // world)
-    T = window if window else min(max(32, 2048 // S), cfgd["lines"] // 2)
+    T = window if window else min(max(32, LINES_PER_GPU_WINDOW // S), cfgd["lines"] // 2)
     no_srp = mode == "full"
     config = {"workload": f"configs[{cid}]", "streams": S_tot, "streams_per_gpu": S, "pixels": cfgd["pixels"],
               "bands": cfgd["bands"], "dims": cfgd["bands"] if no_srp else 5,
@@ -819,7 +824,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--mode", default="full", choices=["full", "srp"])
-    ap.add_argument("--window", type=int, default=0, help="lines per stream per window (0: ~2048 lines per GPU)")
+    ap.add_argument("--window", type=int, default=0, help="lines per stream per window (0: ~4096 lines per GPU)")
     ap.add_argument("--factor", type=int, default=0, choices=[0, 1, 32, 64],
                     help="factor kernel precision (ERX_OPT_FACTOR_PRECISION)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

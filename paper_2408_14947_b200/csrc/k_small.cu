@@ -17,6 +17,7 @@
 //
 // Stats slot contract as k_stats.cu: [c | s | S packed lower], fp64.
 #include <algorithm>
+#include <cstdlib>
 
 #include "erx_common.cuh"
 
@@ -199,6 +200,138 @@ __global__ void __launch_bounds__(kStatsSmallThreads, DM <= 8 ? 4 : (DM <= 10 ? 
             out[2 * D + (q - D)] = v;
         }
     }
+}
+
+// Identity projection, a WARP per line (D = B <= 12: configs[2]).  The CTA-per-line kernel above spends
+// its time outside the rank-1 updates on narrow lines (ncu, configs[2]: 247 registers -> 8 warps per SM,
+// 24 % of the stalls at its CTA barriers, and 40 % of its instructions in the 65-value block reduction
+// every 8 pixels per lane).  Here each warp streams a whole line through its own double-buffered
+// cp.async stage -- no CTA barrier anywhere, one butterfly reduction per line (32 pixels per lane at
+// P = 1024) -- and the warps of an SM hide one another's start-up latency.  Same per-pixel arithmetic:
+// centre = fp64 mean of the first min(32, P) pixels, v = fl32(z - c), exact fp64 products.
+// EX: D == DM (configs[2]'s 10 bands, d = 5): every `j < D` folds at compile time.
+template <int DM, bool EX>
+__global__ void __launch_bounds__(kStatsSmallThreads, 2) stats_small_wl_kernel(SmallArgs a, int n_lines) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int kW = kStatsSmallThreads / 32;
+    constexpr int DT = DM * (DM + 1) / 2;
+    const Geometry& g = a.g;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int line = blockIdx.x * kW + warp;
+    if (line >= n_lines) return;  // (no CTA barrier below)
+    const int D = EX ? DM : g.D, B = EX ? DM : g.B, P = g.P;  // (identity projection: B == D)
+    const int CH = a.sm.CH;
+    float* buf = reinterpret_cast<float*>(smem) + size_t(warp) * 2 * CH * B;  // [2][CH][B]
+    const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
+    float* vc = a.vcache + size_t(line) * D * P;
+    const int nck = (P + CH - 1) / CH;
+    auto issue = [&](int ci, int b) {
+        const int p0 = ci * CH, n = min(CH, P - p0);
+        const float* src = xl + size_t(p0) * B;
+        float* dst = buf + b * CH * B;
+        const int nfl = n * B;
+        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && (nfl & 3) == 0) {
+            for (int i = lane; i < nfl / 4; i += 32) cp_async16(dst + 4 * i, src + 4 * i);
+        } else {
+            for (int i = lane; i < nfl; i += 32) cp_async4(dst + i, src + i);
+        }
+        cp_async_commit();
+    };
+    issue(0, 0);
+    if (1 < nck) issue(1, 1);
+    if (1 < nck) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncwarp();
+    // centre: lane p < n0 holds pixel p of chunk 0 (CH >= 32 or CH >= P), fp64 butterfly sum
+    double cen[DM];
+    {
+        const int n0 = min(32, P);
+        const float* row = buf + min(lane, n0 - 1) * B;
+#pragma unroll
+        for (int j = 0; j < DM; ++j) {
+            double v = (lane < n0 && j < D) ? double(row[j]) : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            cen[j] = v / double(n0);
+        }
+    }
+    double s1[DM], s2[DT];
+#pragma unroll
+    for (int j = 0; j < DM; ++j) s1[j] = 0.0;
+#pragma unroll
+    for (int j = 0; j < DT; ++j) s2[j] = 0.0;
+    for (int ci = 0; ci < nck; ++ci) {
+        if (ci + 1 < nck) cp_async_wait<1>();
+        else cp_async_wait<0>();
+        __syncwarp();
+        const float* st = buf + (ci & 1) * CH * B;
+        const int p0 = ci * CH, n = min(CH, P - p0);
+        // software pipeline over the lane's pixels: the load -> fp64 subtract -> fp32 round -> cache
+        // store chain of pixel pp + 32 is issued before the rank-1 updates of pixel pp (ncu: half of
+        // the stall samples sat on that chain when each iteration ran it first)
+        // (straight-line: a warp-uniform `if (j < D)` around each dim's chain compiles to a branch per dim,
+        // which serialises the ten load -> convert -> subtract -> convert chains; loads are clamped to a
+        // real band instead and padded dims zeroed by a select)
+        auto prep = [&](int pp, float (&v)[DM]) {
+            const float* row = st + pp * B;
+            float xr[DM];
+#pragma unroll
+            for (int j = 0; j < DM; ++j) xr[j] = row[min(j, D - 1)];
+#pragma unroll
+            for (int j = 0; j < DM; ++j) v[j] = float(double(xr[j]) - cen[j]);
+            float* vp = vc + p0 + pp;
+#pragma unroll
+            for (int j = 0; j < DM; ++j) {
+                if (j < D) *vp = v[j];
+                else v[j] = 0.f;
+                vp += P;  // (one pointer add per dim instead of a 64-bit multiply)
+            }
+        };
+        float vn[DM];
+#pragma unroll
+        for (int j = 0; j < DM; ++j) vn[j] = 0.f;
+        if (lane < n) prep(lane, vn);
+        for (int pp = lane; pp < n; pp += 32) {
+            double vd[DM];
+#pragma unroll
+            for (int j = 0; j < DM; ++j) vd[j] = double(vn[j]);
+            if (pp + 32 < n) prep(pp + 32, vn);
+#pragma unroll
+            for (int i = 0; i < DM; ++i) {
+                s1[i] += vd[i];
+#pragma unroll
+                for (int j = 0; j <= i; ++j) s2[i * (i + 1) / 2 + j] = fma(vd[i], vd[j], s2[i * (i + 1) / 2 + j]);
+            }
+        }
+        __syncwarp();  // the stage is refilled next
+        if (ci + 2 < nck) issue(ci + 2, ci & 1);
+    }
+    // one butterfly per value (every lane ends with the line's total), staged through the warp's
+    // (now idle) buffer so the slot is written with coalesced stores
+    double* red = reinterpret_cast<double*>(buf);
+#pragma unroll
+    for (int i = 0; i < DM; ++i) {
+        double v = s1[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && i < D) {
+            red[i] = cen[i];
+            red[D + i] = v;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < DM; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+            double v = s2[i * (i + 1) / 2 + j];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0 && i < D) red[2 * D + i * (i + 1) / 2 + j] = v;
+        }
+    __syncwarp();
+    double* out = a.stats + size_t(line) * (g.SE + D);
+    const int NV = 2 * D + D * (D + 1) / 2;
+    for (int q = lane; q < NV; q += 32) out[q] = red[q];
 }
 
 // SRP variant (the reference default, d = 5): one CTA per line, all threads share each staged chunk;
@@ -454,9 +587,109 @@ __global__ void __launch_bounds__(kSmallThreads, 4) score_small_kernel(Geometry 
         norm[size_t(line) * g.P + p] = (sd < 1e-12) ? 0.f : float((double(dl[p]) - mean) / sd);
 }
 
+// score_small + normalize with a WARP per line (narrow lines): W (packed lower, <= 78 values) lives in
+// registers, the line's raw scores in the warp's own shared-memory strip; no CTA barrier.  The mean / std
+// sums are fp64 per lane then one butterfly (the CTA kernel sums per thread, per warp, then over warps:
+// a different, equally fixed order).
+constexpr int kScoreWlWarps = 4;
+template <int DM, bool EX>
+__global__ void __launch_bounds__(kScoreWlWarps * 32, 4) score_small_wl_kernel(Geometry g, const double* __restrict__ stats,
+                                                                           const double* __restrict__ prior,
+                                                                           const float* __restrict__ Wp,
+                                                                           const float* __restrict__ vcache,
+                                                                           float* __restrict__ raw, float* __restrict__ norm,
+                                                                           int* __restrict__ status, int* __restrict__ fixlist,
+                                                                           int n_lines) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int DT = DM * (DM + 1) / 2;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int line = blockIdx.x * kScoreWlWarps + warp;
+    if (line >= n_lines) return;
+    const int D = EX ? DM : g.D, P = g.P;
+    float* dl = reinterpret_cast<float*>(smem) + size_t(warp) * P;  // raw scores of the line [P]
+    const int nblk = g.nb * (g.nb + 1) / 2;
+    const float* W = Wp + size_t(line) * nblk * 64;
+    float Wr[DT], off[DM];
+#pragma unroll
+    for (int r = 0; r < DM; ++r) {
+#pragma unroll
+        for (int c = 0; c <= r; ++c) {
+            const int I = r / 8, J = c / 8;
+            const float w = __ldg(W + (I * (I + 1) / 2 + J) * 64 + (c % 8) * 8 + (r % 8));  // (the blocks cover Dp >= DM rows)
+            Wr[r * (r + 1) / 2 + c] = (r < D) ? w : 0.f;
+        }
+    }
+    {
+        // u = v - (mu_{t-1} - c_t): v is centred on this line's c_t
+        const double* st = stats + size_t(line) * (g.SE + D);
+        const double* pr = prior + size_t(line) * g.SE;
+#pragma unroll
+        for (int j = 0; j < DM; ++j) off[j] = (j < D) ? float(__ldg(pr + j) - __ldg(st + j)) : 0.f;
+    }
+    const float* vc = vcache + size_t(line) * D * P;
+    double ls = 0.0;
+    constexpr int kPX = DM <= 8 ? 4 : 2;  // pixels per lane per pass, all their loads in flight first
+    for (int p0 = lane; p0 < P; p0 += kPX * 32) {
+        float u[kPX][DM];
+#pragma unroll
+        for (int x = 0; x < kPX; ++x) {
+            const int p = min(p0 + x * 32, P - 1);
+            // (unconditional clamped loads: no branch per dim; W = 0 in the padded columns)
+            const float* vp = vc + p;
+#pragma unroll
+            for (int j = 0; j < DM; ++j) {
+                u[x][j] = __ldg(vp) - off[j];
+                if (j + 1 < D) vp += P;  // (clamped to the last real dim)
+            }
+        }
+#pragma unroll
+        for (int x = 0; x < kPX; ++x) {
+            const int p = p0 + x * 32;
+            float ssq = 0.f;
+#pragma unroll
+            for (int r = 0; r < DM; ++r) {
+                float m = 0.f;
+#pragma unroll
+                for (int c = 0; c <= r; ++c) m = fmaf(Wr[r * (r + 1) / 2 + c], u[x][c], m);
+                ssq = fmaf(m, m, ssq);  // (rows r >= D: W = 0, m = 0)
+            }
+            if (p < P) {
+                const float d = sqrtf(ssq);
+                dl[p] = d;
+                raw[size_t(line) * P + p] = d;
+                ls += double(d);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
+    const double mean = ls / double(P);
+    __syncwarp();
+    double lv = 0.0;
+    for (int p = lane; p < P; p += 32) {
+        const double dd = double(dl[p]) - mean;
+        lv += dd * dd;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lv += __shfl_xor_sync(0xffffffffu, lv, o);
+    const double sd = sqrt(lv / double(P));
+    if (lane == 0 && fixlist && flat_line(mean, sd) && status[line] != -2) list_for_fixup(fixlist, status, line);
+    for (int p = lane; p < P; p += 32)
+        norm[size_t(line) * P + p] = (sd < 1e-12) ? 0.f : float((double(dl[p]) - mean) / sd);
+}
+
 }  // namespace
 
 bool small_path(const Geometry& g) { return g.D <= 16; }
+
+constexpr int kSmallWlMinLines = 2048;
+static bool small_wl() {  // A/B switch of the warp-per-line kernels (default on)
+    static const bool on = [] {
+        const char* e = std::getenv("ERX_SMALL_WL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 SmallLaunch plan_small(const Geometry& g) {
     SmallLaunch sm{};
@@ -511,6 +744,30 @@ void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x
             stats_small_srp_kernel<16><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
         return;
     }
+    // narrow identity lines: a warp per line (stats_small_wl_kernel) while a chunk holds the centre's
+    // pixels; ERX_SMALL_WL=0 keeps the CTA-per-line kernels (A/B)
+    // (from ~2048 lines per launch: below, warps-per-line leave SMs idle -- configs[1] d = 5 at 256 lines:
+    // score 0.0106 -> 0.0166 ms)
+    if (small_wl() && n_lines_total >= kSmallWlMinLines && g.D <= 12 && (sm.CH >= 32 || sm.CH >= g.P)) {
+        constexpr int kW = kStatsSmallThreads / 32;
+        const int grid = (n_lines_total + kW - 1) / kW;
+        // ~10 KB stages (8 pixels per lane per chunk at 10 bands: the pipeline restarts once per chunk)
+        int chw = int(std::min<size_t>(256, size_t(10240) / (size_t(g.B) * 4))) / 32 * 32;
+        if (chw > sm.CH) a.sm.CH = chw;
+        const size_t smw = size_t(kW) * 2 * a.sm.CH * g.B * 4;
+#define ERX_STATS_WL(DMV, EXV)                                              \
+    do {                                                                    \
+        ensure_smem(stats_small_wl_kernel<DMV, EXV>, 200 * 1024);           \
+        stats_small_wl_kernel<DMV, EXV><<<grid, kStatsSmallThreads, smw, st>>>(a, n_lines_total); \
+    } while (0)
+        if (g.D == 5) ERX_STATS_WL(5, true);
+        else if (g.D == 8) ERX_STATS_WL(8, true);
+        else if (g.D < 8) ERX_STATS_WL(8, false);
+        else if (g.D == 10) ERX_STATS_WL(10, true);
+        else ERX_STATS_WL(12, false);
+#undef ERX_STATS_WL
+        return;
+    }
     if (g.D == 5)  // the reference default, d = 5
         stats_small_kernel<5><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
     else if (g.D <= 8)
@@ -532,6 +789,20 @@ void launch_score_small(const Geometry& g, const SmallLaunch& sm, const double* 
         ensure_smem(score_small_kernel<10>, 200 * 1024);
         ensure_smem(score_small_kernel<12>, 200 * 1024);
         ensure_smem(score_small_kernel<16>, 200 * 1024);
+    }
+    if (small_wl() && n_lines_total >= kSmallWlMinLines && g.D <= 12 && size_t(kScoreWlWarps) * g.P * 4 <= 48 * 1024) {
+        const int grid = (n_lines_total + kScoreWlWarps - 1) / kScoreWlWarps;
+        const size_t smw = size_t(kScoreWlWarps) * g.P * 4;
+#define ERX_SCORE_WL(DMV, EXV)                                                                                   \
+    score_small_wl_kernel<DMV, EXV><<<grid, kScoreWlWarps * 32, smw, st>>>(g, stats, prior, whiten, vcache, raw, \
+                                                                           norm, status, fixlist, n_lines_total)
+        if (g.D == 5) ERX_SCORE_WL(5, true);
+        else if (g.D == 8) ERX_SCORE_WL(8, true);
+        else if (g.D < 8) ERX_SCORE_WL(8, false);
+        else if (g.D == 10) ERX_SCORE_WL(10, true);
+        else ERX_SCORE_WL(12, false);
+#undef ERX_SCORE_WL
+        return;
     }
     if (g.D == 5)  // the reference default, d = 5
         score_small_kernel<5><<<n_lines_total, kSmallThreads, sm.smem_score, st>>>(g, stats, prior, whiten, vcache,
