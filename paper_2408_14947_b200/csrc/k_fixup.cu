@@ -50,6 +50,9 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(FixupArgs a) {
     double* mu = reinterpret_cast<double*>(smem);   // [Dp]
     double* dyn = mu + Dp;                          // factor / inverse / scoring scratch
     const int count = a.list[0];
+    // nothing listed (the usual window): no CTA touches the list, so there is nothing to reset either --
+    // skip the fence / atomic hand-shake below (the empty launch: 6.2 -> ~3 us)
+    if (count == 0) return;
     const int initialized = a.state.meta->initialized;
     const long long n_seen0 = a.state.meta->welford_n;
     const double Pd = double(g.P), invP = 1.0 / Pd, invP1 = 1.0 / (Pd - 1.0), om = 1.0 - a.alpha;

@@ -20,6 +20,7 @@
 #include <cstdlib>
 
 #include "erx_common.cuh"
+#include "tc_common.cuh"
 
 namespace erxk {
 namespace {
@@ -376,18 +377,30 @@ __global__ void __launch_bounds__(kStatsSmallThreads) stats_small_srp_kernel(Sma
     const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
     float* vc = a.vcache + size_t(line) * D * g.P;
     const int n0 = min(32, g.P);
-    const bool use_async = (B % 4) == 0;
+    // 16-byte rows: a chunk is ONE bulk copy (cp.async.bulk, mbarrier transaction count) issued by thread 0
+    // instead of ~40 cp.async per thread (ncu, configs[3] d = 5: 17 % of the kernel's instructions)
+    const bool use_bulk = (B % 4) == 0 && (reinterpret_cast<uintptr_t>(xl) & 15) == 0;
+    __shared__ __align__(8) uint64_t fullb[2];
+    if (tid == 0) {
+        tc::mbar_init(&fullb[0], 1);
+        tc::mbar_init(&fullb[1], 1);
+        tc::fence_barrier_init();
+    }
+    __syncthreads();
     const int nchunks = (g.P + sm.CH2 - 1) / sm.CH2;
     auto issue = [&](int c) {
         const int c0 = c * sm.CH2, n = min(sm.CH2, g.P - c0);
         float* dst = stage + (c & 1) * sm.CH2 * B;
         const float* src = xl + size_t(c0) * B;
-        if (use_async) {
-            for (int i = tid; i < n * B / 4; i += kStatsSmallThreads) cp_async16(dst + 4 * i, src + 4 * i);
+        if (use_bulk) {
+            if (tid == 0) {
+                tc::fence_proxy_async();  // the stage's earlier generic-proxy reads (ordered by the CTA barrier)
+                tc::mbar_expect_tx(&fullb[c & 1], uint32_t(n) * B * 4);
+                tc::bulk_g2s(dst, src, uint32_t(n) * B * 4, &fullb[c & 1]);
+            }
         } else {
             for (int i = tid; i < n * B; i += kStatsSmallThreads) dst[i] = __ldg(src + i);
         }
-        cp_async_commit();
     };
     issue(0);
     __syncthreads();
@@ -401,13 +414,9 @@ __global__ void __launch_bounds__(kStatsSmallThreads) stats_small_srp_kernel(Sma
     for (int j = 0; j < DT; ++j) s2[j] = 0.0;
 
     for (int c = 0; c < nchunks; ++c) {
-        if (c + 1 < nchunks) {
-            issue(c + 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
+        if (c + 1 < nchunks) issue(c + 1);
+        if (use_bulk) tc::mbar_wait(&fullb[c & 1], uint32_t(c >> 1) & 1u);
+        else __syncthreads();
         const int c0 = c * sm.CH2, n = min(sm.CH2, g.P - c0);
         const float* st = stage + (c & 1) * sm.CH2 * B;
         if (c == 0) {  // centre: fp64 mean of the first min(32, P) projected pixels, from the staged chunk
@@ -427,8 +436,10 @@ __global__ void __launch_bounds__(kStatsSmallThreads) stats_small_srp_kernel(Sma
         }
         // projection: one (dim, pixel) item per thread, consecutive threads on consecutive
         // pixels of one dim (coalesced cache writes, warp-uniform nnz loop bounds)
+        // (j = i / n by a float reciprocal: (i + 0.5) / n is at least 0.5 / n away from an integer)
+        const float rn = 1.f / float(n);
         for (int i = tid; i < n * D; i += kStatsSmallThreads) {
-            const int j = i / n, pp = i - j * n;
+            const int j = int((float(i) + 0.5f) * rn), pp = i - j * n;
             const float* row = st + pp * B;
             const double z = g.srp ? srp_dot(row, j) : double(row[j]);
             const float v = float(z - cen_s[j]);
