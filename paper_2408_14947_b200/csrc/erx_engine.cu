@@ -343,7 +343,7 @@ int configure(erx_engine* e, uint32_t P) {
     e->sl = erxk::plan_stats(g);
     e->sc = erxk::plan_score(g);
     e->small = erxk::small_path(g);
-    if (e->small) e->smp = erxk::plan_small(g);
+    if (e->small) e->smp = erxk::plan_small(g, size_t(e->S) * e->T);
     e->factor_prec = erxk::factor_precision(g, e->factor_req, int(e->S * e->T));
     // exact-integer tensor path: stats_i8 + factor writing int8 W planes + score_i8
     e->tensor = e->stats_tensor == 2 && erxk::stats_i8_eligible(g) && erxk::score_i8_eligible(g) &&

@@ -81,11 +81,12 @@ struct SmallLaunch {
     int CH2;            // pixels per shared stage (SRP variant)
     size_t smem_stats;
     size_t smem_score;
+    bool wl;            // warp-per-line kernels (engines with >= 2048 lines per window)
 };
 
 // small-D path (k_small.cu): D <= 16, one CTA per line, fused normalisation
 bool small_path(const Geometry& g);
-SmallLaunch plan_small(const Geometry& g);
+SmallLaunch plan_small(const Geometry& g, size_t capacity_lines);
 void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x, int n_per_stream, int in_stride,
                         int n_lines_total, double* stats, float* vcache, cudaStream_t st);
 void launch_score_small(const Geometry& g, const SmallLaunch& sm, const double* stats, const double* prior,

@@ -498,6 +498,150 @@ __global__ void __launch_bounds__(kStatsSmallThreads) stats_small_srp_kernel(Sma
     }
 }
 
+// SRP with a WARP per line (the reference default d = 5 on batched windows: configs[3]).  The CTA-per-line
+// kernel above is issue-bound (ncu: 39 % of its instructions in the per-item sparse dot products, three CTA
+// barriers per 44-pixel chunk, 58 % issue-active at 76 % of the HBM peak).  Here each warp streams its own
+// line in 32-pixel chunks -- one bulk copy per chunk into the warp's two stages, its own mbarriers, no CTA
+// barrier -- and a lane owns a pixel: the dims' sums run as DM independent fp64 chains over a k-major
+// padded table {band offset, sign} read by broadcast loads (padding: sign 0 on the dim's first band), then
+// v = fl32(z - c), the cache store and the exact fp64 rank-1 updates; one butterfly per line.
+// z sums at most srp_wmax fp32 values in fp64 (exact for any realistic exponent spread), the centre is the
+// CTA kernel's sequential fp64 mean of the first min(32, P) pixels.
+constexpr int kSrpWlWarps = 4;
+struct SrpEnt {
+    uint32_t off;  // band * 4 (byte offset inside a pixel row)
+    float w;       // +1, -1, or 0 (padding)
+};
+
+template <int DM, bool EX>
+__global__ void __launch_bounds__(kSrpWlWarps * 32, 2) stats_small_srp_wl_kernel(SmallArgs a, int n_lines) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t full[kSrpWlWarps][2];
+    constexpr int DT = DM * (DM + 1) / 2;
+    const Geometry& g = a.g;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int D = EX ? DM : g.D, B = g.B, P = g.P, WM = g.srp_wmax;
+    const size_t stage_fl = size_t(32) * B;
+    float* stage = reinterpret_cast<float*>(smem) + size_t(warp) * 2 * stage_fl;  // [2][32][B]
+    SrpEnt* ent = reinterpret_cast<SrpEnt*>(smem + size_t(kSrpWlWarps) * 2 * stage_fl * 4);  // [WM][DM]
+    for (int q = tid; q < WM * DM; q += kSrpWlWarps * 32) {
+        const int k = q / DM, j = q - k * DM;
+        SrpEnt e{0u, 0.f};
+        if (j < D) {
+            const int b0 = __ldg(g.srp_ptr + j), nz = __ldg(g.srp_ptr + j + 1) - b0;
+            if (nz > 0) {
+                e.off = uint32_t(__ldg(g.srp_band + b0 + (k < nz ? k : 0))) * 4u;
+                e.w = k < nz ? __ldg(g.srp_w + b0 + k) : 0.f;
+            }
+        }
+        ent[q] = e;
+    }
+    if (tid < kSrpWlWarps * 2) tc::mbar_init(&full[tid >> 1][tid & 1], 1);
+    tc::fence_barrier_init();
+    __syncthreads();
+    const int line = blockIdx.x * kSrpWlWarps + warp;
+    if (line >= n_lines) return;  // (no CTA barrier below)
+    const float* xl = line_ptr(a.x, line, a.n, a.in_stride, g);
+    float* vc = a.vcache + size_t(line) * D * P;
+    const int nck = (P + 31) / 32;
+    auto issue = [&](int c) {
+        if (lane == 0) {
+            const uint32_t bytes = uint32_t(min(32, P - c * 32)) * B * 4;
+            tc::fence_proxy_async();  // the stage's earlier generic-proxy reads (ordered by __syncwarp)
+            tc::mbar_expect_tx(&full[warp][c & 1], bytes);
+            tc::bulk_g2s(stage + (c & 1) * stage_fl, xl + size_t(c) * 32 * B, bytes, &full[warp][c & 1]);
+        }
+    };
+    issue(0);
+    if (nck > 1) issue(1);
+    const double scale = g.srp_scale;
+    // z of one staged pixel row: DM independent chains, every table entry one broadcast load
+    auto zrow = [&](const unsigned char* row, double (&z)[DM]) {
+#pragma unroll
+        for (int j = 0; j < DM; ++j) z[j] = 0.0;
+        for (int k = 0; k < WM; ++k) {
+            const SrpEnt* ek = ent + k * DM;
+#pragma unroll
+            for (int j = 0; j < DM; ++j) {
+                const SrpEnt e = ek[j];
+                z[j] += double(*reinterpret_cast<const float*>(row + e.off) * e.w);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < DM; ++j) z[j] *= scale;
+    };
+    double cen[DM];
+    double s1[DM], s2[DT];
+#pragma unroll
+    for (int j = 0; j < DM; ++j) s1[j] = 0.0;
+#pragma unroll
+    for (int j = 0; j < DT; ++j) s2[j] = 0.0;
+    for (int c = 0; c < nck; ++c) {
+        tc::mbar_wait(&full[warp][c & 1], uint32_t(c >> 1) & 1u);
+        const int n = min(32, P - c * 32);
+        const unsigned char* row =
+            reinterpret_cast<const unsigned char*>(stage + (c & 1) * stage_fl + size_t(min(lane, n - 1)) * B);
+        double z[DM];
+        zrow(row, z);
+        if (c == 0) {
+            // centre: the fp64 mean of the first n0 = min(32, P) projected pixels, summed in pixel order
+            // (the CTA kernel's order) by broadcast shuffles
+            const int n0 = n;
+#pragma unroll
+            for (int j = 0; j < DM; ++j) {
+                double sc = 0.0;
+                for (int pp = 0; pp < n0; ++pp) sc += __shfl_sync(0xffffffffu, z[j], pp);
+                cen[j] = sc / double(n0);
+            }
+        }
+        if (lane < n) {
+            double vd[DM];
+            float* vp = vc + c * 32 + lane;
+#pragma unroll
+            for (int j = 0; j < DM; ++j) {
+                const float v = float(z[j] - cen[j]);
+                if (j < D) *vp = v;
+                vp += P;
+                vd[j] = (j < D) ? double(v) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < DM; ++i) {
+                s1[i] += vd[i];
+#pragma unroll
+                for (int j = 0; j <= i; ++j) s2[i * (i + 1) / 2 + j] = fma(vd[i], vd[j], s2[i * (i + 1) / 2 + j]);
+            }
+        }
+        __syncwarp();  // the stage is refilled next
+        if (c + 2 < nck) issue(c + 2);
+    }
+    // one butterfly per value, staged through the warp's (idle) buffer for coalesced stores of the slot
+    __syncwarp();
+    double* red = reinterpret_cast<double*>(stage);
+#pragma unroll
+    for (int i = 0; i < DM; ++i) {
+        double v = s1[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && i < D) {
+            red[i] = cen[i];
+            red[D + i] = v;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < DM; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+            double v = s2[i * (i + 1) / 2 + j];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0 && i < D) red[2 * D + i * (i + 1) / 2 + j] = v;
+        }
+    __syncwarp();
+    double* out = a.stats + size_t(line) * (g.SE + D);
+    const int NV = 2 * D + D * (D + 1) / 2;
+    for (int q = lane; q < NV; q += 32) out[q] = red[q];
+}
+
 // score_small + normalize.  W: packed lower 8x8 blocks (column-major inside).
 template <int DM>
 __global__ void __launch_bounds__(kSmallThreads, 4) score_small_kernel(Geometry g, const double* __restrict__ stats,
@@ -702,8 +846,11 @@ static bool small_wl() {  // A/B switch of the warp-per-line kernels (default on
     return on;
 }
 
-SmallLaunch plan_small(const Geometry& g) {
+SmallLaunch plan_small(const Geometry& g, size_t capacity_lines) {
     SmallLaunch sm{};
+    // warp-per-line kernels for engines whose windows hold >= 2048 lines (decided once per engine, so every
+    // window of a run -- the ragged last one included -- takes the same kernels and arithmetic)
+    sm.wl = small_wl() && capacity_lines >= size_t(kSmallWlMinLines);
     // identity projection (B = D <= 16): per-warp stages of ~6 KB (4 warps x 2 stages = 48 KB, four
     // lines per SM); a lane owns one pixel of a chunk (a multiple of 32 pixels)
     int ch = int(std::min<size_t>(256, std::max<size_t>(4, size_t(6144) / (size_t(g.B) * 4))));
@@ -744,6 +891,24 @@ void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x
         ensure_smem(stats_small_kernel<16>, 200 * 1024);
     }
     SmallArgs a{g, sm, x, n_per_stream, in_stride, stats, vcache};
+    // SRP on batched windows: a warp per line while two CTAs of four warps (two 32-pixel stages each) fit
+    // an SM (B <= 109) and the padded table stays small
+    const size_t srp_wl_smem = size_t(kSrpWlWarps) * 2 * 32 * g.B * 4 + size_t(g.srp_wmax) * 16 * sizeof(SrpEnt);
+    if (g.srp && sm.wl && g.D <= 12 && (g.B % 4) == 0 &&
+        (reinterpret_cast<uintptr_t>(x) & 15) == 0 && srp_wl_smem <= 112 * 1024) {
+        const int grid = (n_lines_total + kSrpWlWarps - 1) / kSrpWlWarps;
+#define ERX_SRP_WL(DMV, EXV)                                                      \
+    do {                                                                          \
+        ensure_smem(stats_small_srp_wl_kernel<DMV, EXV>, 200 * 1024);             \
+        stats_small_srp_wl_kernel<DMV, EXV><<<grid, kSrpWlWarps * 32, srp_wl_smem, st>>>(a, n_lines_total); \
+    } while (0)
+        if (g.D == 5) ERX_SRP_WL(5, true);
+        else if (g.D == 8) ERX_SRP_WL(8, true);
+        else if (g.D < 8) ERX_SRP_WL(8, false);
+        else ERX_SRP_WL(12, false);
+#undef ERX_SRP_WL
+        return;
+    }
     if (g.srp) {
         if (g.D == 5 && g.B <= 128)  // the reference default (measured: DM = 8 is faster at B = 224)
             stats_small_srp_kernel<5><<<n_lines_total, kStatsSmallThreads, sm.smem_stats, st>>>(a);
@@ -759,7 +924,7 @@ void launch_stats_small(const Geometry& g, const SmallLaunch& sm, const float* x
     // pixels; ERX_SMALL_WL=0 keeps the CTA-per-line kernels (A/B)
     // (from ~2048 lines per launch: below, warps-per-line leave SMs idle -- configs[1] d = 5 at 256 lines:
     // score 0.0106 -> 0.0166 ms)
-    if (small_wl() && n_lines_total >= kSmallWlMinLines && g.D <= 12 && (sm.CH >= 32 || sm.CH >= g.P)) {
+    if (sm.wl && g.D <= 12 && (sm.CH >= 32 || sm.CH >= g.P)) {
         constexpr int kW = kStatsSmallThreads / 32;
         const int grid = (n_lines_total + kW - 1) / kW;
         // ~10 KB stages (8 pixels per lane per chunk at 10 bands: the pipeline restarts once per chunk)
@@ -801,7 +966,7 @@ void launch_score_small(const Geometry& g, const SmallLaunch& sm, const double* 
         ensure_smem(score_small_kernel<12>, 200 * 1024);
         ensure_smem(score_small_kernel<16>, 200 * 1024);
     }
-    if (small_wl() && n_lines_total >= kSmallWlMinLines && g.D <= 12 && size_t(kScoreWlWarps) * g.P * 4 <= 48 * 1024) {
+    if (sm.wl && g.D <= 12 && size_t(kScoreWlWarps) * g.P * 4 <= 48 * 1024) {
         const int grid = (n_lines_total + kScoreWlWarps - 1) / kScoreWlWarps;
         const size_t smw = size_t(kScoreWlWarps) * g.P * 4;
 #define ERX_SCORE_WL(DMV, EXV)                                                                                   \

@@ -115,6 +115,44 @@ def test_chunked_scan_matches_plain_scan(pkg, oracle, cid, no_srp):
     check_gates(oracle, ref[0], ref[1], raw_o, norm_o, label=f"c{cid} chunked scan")
 
 
+def test_warp_per_line_identity(pkg, oracle):
+    """Engines whose windows hold >= 2048 lines run the D <= 12 kernels with a warp per line
+    (k_small.cu: stats_small_wl / score_small_wl).  configs[2] (10 bands) in one 2048-line window plus
+    a ragged one: the oracle's gates, and bit-identical scores when the stream is cut differently."""
+    spec = pkg.gen_spec(2)
+    n = 2100
+    lines, _ = pkg.gen_lines(spec, 0, n)
+    cfg = pkg.ErxConfig(no_srp=True, alpha=0.1, buffer_len=20)
+    got = run_gpu(pkg, cfg, lines, 2048)
+    raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), lines)
+    check_gates(oracle, got[0], got[1], raw_o, norm_o, label="c2 warp-per-line")
+    eng = pkg.Engine(cfg, lines.shape[2], n_streams=1, window_lines=2048)
+    for t0, t1 in ((0, 700), (700, 2048), (2048, n)):  # partial device windows on the same engine
+        eng.push(lines[None, t0:t1], t0)
+    eng.finish()
+    _, _, raw, norm = eng.pop()
+    eng.close()
+    assert np.array_equal(raw[0], got[0]) and np.array_equal(norm[0], got[1])
+
+
+def test_warp_per_line_srp(pkg, oracle):
+    """The reference default d = 5 on a batched engine (64 streams x 32 lines = 2048 lines per window):
+    stats_small_srp_wl (a warp per line, bulk-copied 32-pixel chunks) and score_small_wl against the
+    oracle on three of the streams, over full and ragged windows."""
+    S, n, P = 64, 40, 200
+    lines = np.stack([pkg.gen_lines(pkg.gen_spec(3, s), 0, n)[0][:, :P, :] for s in range(S)])
+    cfg = pkg.ErxConfig(no_srp=False, alpha=0.1, buffer_len=10)
+    eng = pkg.Engine(cfg, lines.shape[3], n_streams=S, window_lines=32)
+    eng.push(lines, 0)
+    eng.finish()
+    idx, _, raw, norm = eng.pop()
+    eng.close()
+    assert idx.tolist() == list(range(n))
+    for s in (0, 31, 63):
+        raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), lines[s])
+        check_gates(oracle, raw[s], norm[s], raw_o, norm_o, label=f"d=5 warp-per-line stream {s}")
+
+
 def test_batched_streams_equal_single_streams(pkg):
     S, n = 3, 24
     lines = np.stack([pkg.gen_lines(pkg.gen_spec(3, s), 0, n)[0] for s in range(S)])
