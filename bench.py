@@ -114,7 +114,7 @@ class StubEngine:
         return (self.t[b] - self.t[a]) * 1e3
 
 
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02c_ncu_full_c3.txt")  # one group of 2048 lines per launch
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02e_ncu_full_c3.txt")  # one group of 4096 lines per launch (T = 64)
 NCU_NAMES = {"stats": ("stats_i8_ws_kernel", "stats_i8_kernel", "stats_kernel", "stats_small"),
              "score": ("score_i8_kernel", "score_kernel"), "factor": ("factor_blk_kernel",),
              "scan": ("scan_tile_kernel", "scan_kernel"), "normalize": ("normalize_kernel",)}
@@ -557,9 +557,10 @@ def secondary_measurements(pkg, args):
     except Exception as ex:
         out["single_stream_c2"] = {"error": repr(ex)}
     try:
+        t_srp = workload(3, "srp", 1)[2]  # the headline's window (~4096 lines per GPU)
         out["batched_srp"] = {"workload": "configs[3] with the reference default d = 5 SRP: 64 streams, "
-                                          "640 px x 108 bands, alpha=0.1", "window_lines": 32,
-                              **throughput(3, 32, ("srp",), streams=tuple(range(64)))}
+                                          "640 px x 108 bands, alpha=0.1", "window_lines": t_srp,
+                              **throughput(3, t_srp, ("srp",), streams=tuple(range(64)))}
     except Exception as ex:
         out["batched_srp"] = {"error": repr(ex)}
     try:

@@ -201,7 +201,9 @@ __global__ void __launch_bounds__(128) scan_tile_kernel(Geometry g, const double
 // per-element arithmetic and its order are exactly the kernel above's (EMA
 // mode), so the results are bit-identical.
 // ---------------------------------------------------------------------------
-template <int TC, int NTH, int kU>
+// E: state elements per CTA (32, or 8 where even 32-element CTAs leave most SMs idle: configs[2]'s 65
+// elements run as 9 CTAs whose loader warps finish a chunk under the recurrence of the previous one)
+template <int TC, int NTH, int kU, int E = 32>
 __global__ void __launch_bounds__(NTH) scan_chunk_kernel(Geometry g, const double* __restrict__ stats,
                                                          double* __restrict__ prior, StateRef sref, int n,
                                                          double alpha, float* __restrict__ kblk) {
@@ -209,16 +211,16 @@ __global__ void __launch_bounds__(NTH) scan_chunk_kernel(Geometry g, const doubl
     double* __restrict__ st_out = sref.out();
     const int initialized = sref.meta->initialized;
     extern __shared__ __align__(16) unsigned char smem[];
-    double* kh = reinterpret_cast<double*>(smem);  // [2][TC][32] finished line statistics
-    double* ps = kh + 2 * TC * 32;                 // [2][TC][32] pre-update background
-    __shared__ int o0_s[32], o1_s[32], o2_s[32], boff_s[32];
-    const int s = blockIdx.y, e0 = blockIdx.x * 32;
-    const int ne = min(32, g.SE - e0);
+    double* kh = reinterpret_cast<double*>(smem);  // [2][TC][E] finished line statistics
+    double* ps = kh + 2 * TC * E;                  // [2][TC][E] pre-update background
+    __shared__ int o0_s[E], o1_s[E], o2_s[E], boff_s[E];
+    const int s = blockIdx.y, e0 = blockIdx.x * E;
+    const int ne = min(E, g.SE - e0);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int D = g.D, SS = g.SE + g.D;
     const double P = double(g.P), invP = 1.0 / P, invP1 = 1.0 / (P - 1.0);
     const int nblk = g.nb * (g.nb + 1) / 2;
-    if (tid < 32) {
+    if (tid < E) {
         const int e = e0 + min(tid, ne - 1);
         int a = e, b = e;
         if (e >= D) unpack_tri(e - D, a, b);
@@ -240,12 +242,12 @@ __global__ void __launch_bounds__(NTH) scan_chunk_kernel(Geometry g, const doubl
             // recurrence over chunk it - 1
             const int c = it - 1;
             if (c >= 0 && c < nch) {
-                const double* kc = kh + (c & 1) * TC * 32;
-                double* pc = ps + (c & 1) * TC * 32;
+                const double* kc = kh + (c & 1) * TC * E;
+                double* pc = ps + (c & 1) * TC * E;
                 const int nt = min(TC, n - c * TC);
 #pragma unroll 8
                 for (int t = 0; t < nt; ++t) {
-                    const double cur = kc[t * 32 + lane];
+                    const double cur = kc[t * E + (lane & (E - 1))];
                     double pr;
                     if (!initialized && c == 0 && t == 0) {
                         pr = cur;
@@ -254,22 +256,22 @@ __global__ void __launch_bounds__(NTH) scan_chunk_kernel(Geometry g, const doubl
                         pr = state;
                         state = ema_step(state, cur, om, alpha);
                     }
-                    pc[t * 32 + lane] = pr;
+                    if (lane < E) pc[t * E + lane] = pr;
                 }
             }
         } else {
             const int q0 = tid - 32, nq = NTH - 32;
             // finish the line statistics of chunk it
             if (it < nch) {
-                double* kc = kh + (it & 1) * TC * 32;
+                double* kc = kh + (it & 1) * TC * E;
                 const int nt = min(TC, n - it * TC);
                 // batches of kU items per thread: all 3 kU loads in flight before any is used
-                for (int qb = q0; qb < nt * 32; qb += kU * nq) {
+                for (int qb = q0; qb < nt * E; qb += kU * nq) {
                     double x0[kU], x1[kU], x2[kU];
 #pragma unroll
                     for (int u = 0; u < kU; ++u) {
-                        const int q = min(qb + u * nq, nt * 32 - 1);
-                        const int t = q >> 5, j = q & 31;
+                        const int q = min(qb + u * nq, nt * E - 1);
+                        const int t = q / E, j = q & (E - 1);
                         const double* st = stats + (l0 + size_t(it) * TC + t) * SS;
                         x0[u] = __ldg(st + o0_s[j]);
                         x1[u] = __ldg(st + o1_s[j]);
@@ -278,17 +280,17 @@ __global__ void __launch_bounds__(NTH) scan_chunk_kernel(Geometry g, const doubl
 #pragma unroll
                     for (int u = 0; u < kU; ++u) {
                         const int q = qb + u * nq;
-                        if (q < nt * 32) kc[q] = finish_stat(e0 + (q & 31) < D, x0[u], x1[u], x2[u], invP, invP1);
+                        if (q < nt * E) kc[q] = finish_stat(e0 + (q & (E - 1)) < D, x0[u], x1[u], x2[u], invP, invP1);
                     }
                 }
             }
             // write back chunk it - 2
             const int c = it - 2;
             if (c >= 0) {
-                const double* pc = ps + (c & 1) * TC * 32;
+                const double* pc = ps + (c & 1) * TC * E;
                 const int nt = min(TC, n - c * TC);
-                for (int q = q0; q < nt * 32; q += nq) {
-                    const int t = q >> 5, j = q & 31;
+                for (int q = q0; q < nt * E; q += nq) {
+                    const int t = q / E, j = q & (E - 1);
                     if (j >= ne) continue;
                     const size_t l = l0 + size_t(c) * TC + t;
                     if (boff_s[j] >= 0)
@@ -325,7 +327,15 @@ void launch_scan(const Geometry& g, const double* stats, double* prior, StateRef
         // too few elements to hide the per-line load latency: chunked variant
         dim3 grid((g.SE + 31) / 32, n_streams);
         const int ctas = int(grid.x * grid.y);
-        if (ctas <= sm_count()) {
+        const int ctas8 = (g.SE + 7) / 8 * n_streams;
+        if (4 * ctas <= sm_count() && ctas8 <= sm_count() && n_per_stream >= 512) {
+            // a handful of elements (configs[2]: 65): 8 per CTA, so a CTA's loader warps finish a chunk
+            // under the recurrence of the previous one
+            dim3 grid8((g.SE + 7) / 8, n_streams);
+            const size_t sm = 2 * size_t(2) * 192 * 8 * sizeof(double);
+            ensure_smem(scan_chunk_kernel<192, 256, 7, 8>, sm);
+            scan_chunk_kernel<192, 256, 7, 8><<<grid8, 256, sm, st>>>(g, stats, prior, state, n_per_stream, alpha, kblk);
+        } else if (ctas <= sm_count()) {
             const size_t sm = 2 * size_t(2) * 192 * 32 * sizeof(double);
             ensure_smem(scan_chunk_kernel<192, 512, 13>, sm);  // 6144 items per chunk: one batch per thread
             scan_chunk_kernel<192, 512, 13><<<grid, 512, sm, st>>>(g, stats, prior, state, n_per_stream, alpha, kblk);

@@ -685,8 +685,14 @@ __global__ void __launch_bounds__(kSmallThreads, 4) score_small_kernel(Geometry 
 #pragma unroll
         for (int x = 0; x < kPX; ++x) {
             const int p = min(p0 + x * kSmallThreads, g.P - 1);
+            // (unconditional loads clamped to the last real dim: a warp-uniform `j < D` around each load
+            // compiles to a branch per dim; W = 0 in the padded columns)
+            const float* vp = vc + p;
 #pragma unroll
-            for (int j = 0; j < DM; ++j) u[x][j] = (j < D) ? __ldg(vc + size_t(j) * g.P + p) - off[j] : 0.f;
+            for (int j = 0; j < DM; ++j) {
+                u[x][j] = __ldg(vp) - off[j];
+                if (j + 1 < D) vp += g.P;
+            }
         }
 #pragma unroll
         for (int x = 0; x < kPX; ++x) {
