@@ -274,7 +274,8 @@ __device__ __forceinline__ void load_panel_t(float* __restrict__ Pt, int LDT, co
     }
 }
 
-__global__ void __launch_bounds__(256) factor_big_kernel(Geometry g, const double* __restrict__ prior, double eps0,
+template <int NT>
+__global__ void __launch_bounds__(NT) factor_big_kernel(Geometry g, const double* __restrict__ prior, double eps0,
                                                          float* __restrict__ work, float* __restrict__ whiten,
                                                          int* __restrict__ status, int* __restrict__ fixlist,
                                                          bool xk_smem) {
@@ -1363,9 +1364,23 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
             cudaLaunchKernelEx(&cfg, factor_cl_kernel<8>, g, prior, eps0, whiten, status, fixlist);
         }
     } else if (precision == 31) {
-        ensure_smem(factor_big_kernel, sm);
-        factor_big_kernel<<<n_lines_total, 256, sm, st>>>(g, prior, eps0, reinterpret_cast<float*>(work), whiten,
-                                                          status, fixlist, factor_big_xk(g));
+        // 512 threads per line (16 warps, 128 registers): the kernel waits on its L2 workspace (ncu at 256
+        // threads: 39 % long-scoreboard, 27 % barrier stalls, 8 warps per SM); measured at 448 bands,
+        // 256 / 384 / 512 / 768 threads: 1.41 / 1.20 / 1.11 / 1.78 ms per 128 lines.  ERX_FACTOR_BIG_THREADS=256
+        // keeps the round-2d launch (A/B).
+        static const int big_nt = [] {
+            const char* e = std::getenv("ERX_FACTOR_BIG_THREADS");
+            return e ? std::atoi(e) : 512;
+        }();
+        if (big_nt == 256) {
+            ensure_smem(factor_big_kernel<256>, sm);
+            factor_big_kernel<256><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, reinterpret_cast<float*>(work), whiten,
+                                                                   status, fixlist, factor_big_xk(g));
+        } else {
+            ensure_smem(factor_big_kernel<512>, sm);
+            factor_big_kernel<512><<<n_lines_total, 512, sm, st>>>(g, prior, eps0, reinterpret_cast<float*>(work), whiten,
+                                                                   status, fixlist, factor_big_xk(g));
+        }
     } else {
         ensure_smem(factor_global_kernel, sm);
         factor_global_kernel<<<n_lines_total, 256, sm, st>>>(g, prior, eps0, work, whiten, status, latch, meta,
