@@ -67,7 +67,10 @@ def workload(cid, mode, world, window=0):
     cfgd = CONFIGS[cid]
     S_tot = cfgd["streams"]
     S = max(1, S_tot // world)
-    T = window if window else min(max(32, LINES_PER_GPU_WINDOW // S), cfgd["lines"] // 2)
+    # (the d = 5 path's windows are cheap -- 0.22 ms per 4096 lines -- so its fixed per-window costs weigh
+    # more: 8192 lines per GPU, measured 18.3 -> 19.5 M lines/s on configs[3])
+    per_gpu = LINES_PER_GPU_WINDOW * (2 if mode == "srp" else 1)
+    T = window if window else min(max(32, per_gpu // S), cfgd["lines"] // 2)
     no_srp = mode == "full"
     config = {"workload": f"configs[{cid}]", "streams": S_tot, "streams_per_gpu": S, "pixels": cfgd["pixels"],
               "bands": cfgd["bands"], "dims": cfgd["bands"] if no_srp else 5,

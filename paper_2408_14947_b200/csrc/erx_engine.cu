@@ -1157,8 +1157,8 @@ int erx_set_option(erx_engine* e, int option, int64_t value) {
         return ERX_OK;
     }
     if (option == ERX_OPT_FACTOR_THREADS) {
-        if (value != 0 && value != 64 && value != 128 && value != 256)
-            return fail(e, ERX_ERR_CONFIG, "factor threads: 0, 64, 128 or 256");
+        if (value != 0 && value != 64 && value != 128 && value != 256 && value != 512)
+            return fail(e, ERX_ERR_CONFIG, "factor threads: 0, 64, 128, 256 or 512");
         e->factor_threads = int(value);
         return ERX_OK;
     }

@@ -1332,7 +1332,11 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
         else if (threads == 128)
             factor_blk_kernel<128, 7><<<n_lines_total, 128, sm, st>>>(g, prior, eps0, whiten, status, fixlist, stats,
                                                                    vmax, kblk);
-        else
+        else if (threads == 512) {
+            ensure_smem(factor_blk_kernel<512, 2>, sm);
+            factor_blk_kernel<512, 2><<<n_lines_total, 512, sm, st>>>(g, prior, eps0, whiten, status, fixlist, stats,
+                                                                   vmax, kblk);
+        } else
             factor_blk_kernel<256, 3><<<n_lines_total, 256, sm, st>>>(g, prior, eps0, whiten, status, fixlist, stats,
                                                                    vmax, kblk);
     } else if (precision == 64) {
