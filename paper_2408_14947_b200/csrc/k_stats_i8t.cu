@@ -346,7 +346,8 @@ __global__ void __launch_bounds__(256) range_kernel(Geometry g, const float* __r
     const float* xl = line_ptr(x, line, n, in_stride, g);
     const int nq = B / 4, tid = threadIdx.x;
     const int n0 = min(32, P);
-    for (int q0 = 0; q0 < nq; q0 += 64) {
+    // (one CTA per 64-quad block of the line: blockIdx.y; at 448 bands two CTAs per line double the loads in flight)
+    for (int q0 = 64 * blockIdx.y; q0 < nq; q0 += 64 * gridDim.y) {
         const int q = q0 + (tid & 63), pg = tid >> 6;
         float4 lo = make_float4(3.402823466e38f, 3.402823466e38f, 3.402823466e38f, 3.402823466e38f);
         float4 hi = make_float4(-3.402823466e38f, -3.402823466e38f, -3.402823466e38f, -3.402823466e38f);
@@ -434,7 +435,7 @@ int launch_stats_i8t(const Geometry& g, const float* x, int n_per_stream, int in
     const int ntile = (g.D + kTile - 1) / kTile;
     StatsI8TArgs a{g, n_per_stream, in_stride, n_streams * n_per_stream, ntile, ntile * (ntile + 1) / 2,
                    (g.P + kTile - 1) / kTile, stats, cen, vmax, vplanes};
-    range_kernel<<<a.n_lines, 256, 0, st>>>(g, x, n_per_stream, in_stride, cen, vmax);
+    range_kernel<<<dim3(a.n_lines, (g.B / 4 + 63) / 64), 256, 0, st>>>(g, x, n_per_stream, in_stride, cen, vmax);
     const int items = a.n_lines * a.npair;
     const int grid = items < sm_count() ? items : sm_count();
     ensure_smem(stats_i8t_kernel, kSmem);
