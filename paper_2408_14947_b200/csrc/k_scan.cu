@@ -9,10 +9,17 @@
 // here:  mu_hat = c + s/P,  K_hat = (S - s_a s_b / P) / (P - 1).
 #include "scan_rec.cuh"
 
+#ifndef SCAN_MINB
+#define SCAN_MINB 1
+#endif
+#ifndef SCAN_KB
+#define SCAN_KB 8
+#endif
+
 namespace erxk {
 namespace {
 
-__global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __restrict__ stats,
+__global__ void __launch_bounds__(128, SCAN_MINB) scan_kernel(Geometry g, const double* __restrict__ stats,
                                                    double* __restrict__ prior, StateRef sref, int n, double alpha,
                                                    int incremental, float* __restrict__ kblk) {
     const double* __restrict__ st_in = sref.in();
@@ -48,7 +55,7 @@ __global__ void __launch_bounds__(128) scan_kernel(Geometry g, const double* __r
         double state = in[e];
         // the line statistics do not depend on the recurrence: they are loaded a batch
         // ahead (double-buffered registers) so the sequential EMA never waits on memory
-        constexpr int kB = 8;
+        constexpr int kB = SCAN_KB;
         double cur[kB], nxt[kB];
         // branch-free loads (clamped line index, select after) so all 3 x kB loads issue back to back
         const bool is_mu = e < D;
