@@ -15,6 +15,10 @@
 #include <algorithm>
 #include <cstdlib>
 
+#ifndef FACTOR_MB128
+#define FACTOR_MB128 7  // resident 128-thread lines per SM the register budget allows (A/B: 5, 6)
+#endif
+
 #include "tc_common.cuh"
 
 #include "erx_common.cuh"
@@ -1313,7 +1317,7 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
     const size_t sm = factor_smem(g, precision);
     if (precision == 32) {
         ensure_smem(factor_blk_kernel<64, 7>, sm);
-        ensure_smem(factor_blk_kernel<128, 7>, sm);
+        ensure_smem(factor_blk_kernel<128, FACTOR_MB128>, sm);
         ensure_smem(factor_blk_kernel<256, 3>, sm);
         // 128 threads per line when the SMs hold >= 6 lines each (configs[3]: 7 per SM by shared
         // memory); with fewer resident lines (small windows, lag 0, or D > ~150 where a line's blocks
@@ -1330,7 +1334,7 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
             factor_blk_kernel<64, 7><<<n_lines_total, 64, sm, st>>>(g, prior, eps0, whiten, status, fixlist, stats,
                                                                  vmax, kblk);
         else if (threads == 128)
-            factor_blk_kernel<128, 7><<<n_lines_total, 128, sm, st>>>(g, prior, eps0, whiten, status, fixlist, stats,
+            factor_blk_kernel<128, FACTOR_MB128><<<n_lines_total, 128, sm, st>>>(g, prior, eps0, whiten, status, fixlist, stats,
                                                                    vmax, kblk);
         else if (threads == 512) {
             ensure_smem(factor_blk_kernel<512, 2>, sm);
