@@ -153,6 +153,30 @@ def test_warp_per_line_srp(pkg, oracle):
         check_gates(oracle, raw[s], norm[s], raw_o, norm_o, label=f"d=5 warp-per-line stream {s}")
 
 
+@pytest.mark.parametrize("bands,dims", [(3, 0), (8, 0), (9, 0), (12, 0), (40, 1), (40, 3), (40, 7), (40, 10), (16, 5)])
+def test_warp_per_line_shapes(pkg, oracle, bands, dims):
+    """The warp-per-line kernels' other template instances (D < DM, D = 8, 12; SRP with d != 5) and ragged
+    geometry (77 pixels: a 13-pixel last chunk; 40 lines in windows of 32: a ragged last window), on a
+    64-stream engine (2048 lines per window), two streams against the oracle.  dims = 0: identity."""
+    S, n, P = 64, 40, 77
+    rng = np.random.default_rng(1000 + 17 * bands + dims)
+    base = rng.uniform(0.05, 0.6, size=(S, 1, 1, bands))
+    load = rng.normal(0.0, 0.03, size=(S, bands, 3))
+    z = rng.normal(size=(S, n, P, 3))
+    lines = (base + np.einsum("snpk,sbk->snpb", z, load) + rng.normal(0.0, 0.01, size=(S, n, P, bands))
+             + np.linspace(0.0, 0.05, n)[None, :, None, None]).astype(np.float32)
+    cfg = pkg.ErxConfig(no_srp=dims == 0, dims=max(dims, 1), alpha=0.1, buffer_len=8, seed=3)
+    eng = pkg.Engine(cfg, bands, n_streams=S, window_lines=32)
+    eng.push(lines, 0)
+    eng.finish()
+    idx, _, raw, norm = eng.pop()
+    eng.close()
+    assert idx.tolist() == list(range(n))
+    for s in (0, 63):
+        raw_o, norm_o, _ = oracle.run_stream(ocfg(oracle, cfg), lines[s])
+        check_gates(oracle, raw[s], norm[s], raw_o, norm_o, label=f"wl B={bands} d={dims} stream {s}")
+
+
 def test_batched_streams_equal_single_streams(pkg):
     S, n = 3, 24
     lines = np.stack([pkg.gen_lines(pkg.gen_spec(3, s), 0, n)[0] for s in range(S)])
