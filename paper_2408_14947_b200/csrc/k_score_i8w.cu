@@ -70,20 +70,35 @@ __global__ void __launch_bounds__(kT) wplanes_w_kernel(Geometry g, const float* 
     auto stage = [&](int kt) {   // W[ti tile][kt tile] -> Wt (+ the kt tile's column scales)
         __syncthreads();
         // 16 x 16 blocks of 64 floats; block (bi, bj) valid when J <= I and the block exists (I < nb)
-        for (int q = tid; q < 16 * 16 * 16; q += kT) {
-            const int blk = q >> 4, part = q & 15;  // 16 float4 per block
-            const int bi = blk >> 4, bj = blk & 15;
-            const int I = ti * 16 + bi, J = kt * 16 + bj;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (J <= I && I < g.nb) v = __ldg(reinterpret_cast<const float4*>(W + size_t(tri(I, J)) * 64) + part);
-            // element e = c * 8 + r (column-major inside the block); part covers e = 4 part .. 4 part + 3
-            const float vv[4] = {v.x, v.y, v.z, v.w};
+        // batches of kLB loads per thread in flight before any is scattered (the kernel waits on L2: ncu
+        // 49 % long-scoreboard at one load per iteration); blocks that do not exist read block 0 and are
+        // zeroed by the (gi, gj) test
+        constexpr int kLB = 8;
+        for (int q0 = tid; q0 < 16 * 16 * 16; q0 += kLB * kT) {
+            float4 v[kLB];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int e = 4 * part + u, c = e >> 3, r = e & 7;
-                const int row = bi * 8 + r, col = bj * 8 + c;
-                const int gi = ti * kT + row, gj = kt * kT + col;
-                Wt[row * kWLd + col] = (gi < D && gj <= gi) ? vv[u] : 0.f;
+            for (int b = 0; b < kLB; ++b) {
+                const int q = q0 + b * kT;
+                const int blk = q >> 4, part = q & 15;  // 16 float4 per block
+                const int I = ti * 16 + (blk >> 4), J = kt * 16 + (blk & 15);
+                const bool ok = J <= I && I < g.nb;
+                v[b] = __ldg(reinterpret_cast<const float4*>(W + size_t(ok ? tri(I, J) : 0) * 64) + part);
+                if (!ok) v[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int b = 0; b < kLB; ++b) {
+                const int q = q0 + b * kT;
+                const int blk = q >> 4, part = q & 15;
+                const int bi = blk >> 4, bj = blk & 15;
+                // element e = c * 8 + r (column-major inside the block); part covers e = 4 part .. 4 part + 3
+                const float vv[4] = {v[b].x, v[b].y, v[b].z, v[b].w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = 4 * part + u, c = e >> 3, r = e & 7;
+                    const int row = bi * 8 + r, col = bj * 8 + c;
+                    const int gi = ti * kT + row, gj = kt * kT + col;
+                    Wt[row * kWLd + col] = (gi < D && gj <= gi) ? vv[u] : 0.f;
+                }
             }
         }
         for (int d = tid; d < kT; d += kT) {
