@@ -37,14 +37,25 @@ template <typename Get>
 __device__ __forceinline__ void write_wblocks(float* __restrict__ whiten, int line, const Geometry& g, Get get) {
     const int nblk = g.nb * (g.nb + 1) / 2;
     float* Wp = whiten + size_t(line) * nblk * 64;
-    for (int idx = threadIdx.x; idx < nblk * 64; idx += blockDim.x) {
-        const int bq = idx >> 6, e = idx & 63, c = e >> 3, r = e & 7;
-        int I = int((sqrtf(8.f * bq + 1.f) - 1.f) * 0.5f);
-        while (I * (I + 1) / 2 > bq) --I;
-        while ((I + 1) * (I + 2) / 2 <= bq) ++I;
-        const int J = bq - I * (I + 1) / 2;
-        const int i = I * kBlk + r, j = J * kBlk + c;
-        Wp[idx] = (i < g.D && j <= i) ? get(i, j) : 0.f;
+    constexpr int kLB = 4;  // values per thread fetched before the stores (get() may read an L2 workspace)
+    for (int i0 = threadIdx.x; i0 < nblk * 64; i0 += kLB * blockDim.x) {
+        float v[kLB];
+#pragma unroll
+        for (int b = 0; b < kLB; ++b) {
+            const int idx = min(i0 + b * int(blockDim.x), nblk * 64 - 1);
+            const int bq = idx >> 6, e = idx & 63, c = e >> 3, r = e & 7;
+            int I = int((sqrtf(8.f * bq + 1.f) - 1.f) * 0.5f);
+            while (I * (I + 1) / 2 > bq) --I;
+            while ((I + 1) * (I + 2) / 2 <= bq) ++I;
+            const int J = bq - I * (I + 1) / 2;
+            const int i = I * kBlk + r, j = J * kBlk + c;
+            v[b] = (i < g.D && j <= i) ? get(i, j) : 0.f;
+        }
+#pragma unroll
+        for (int b = 0; b < kLB; ++b) {
+            const int idx = i0 + b * int(blockDim.x);
+            if (idx < nblk * 64) Wp[idx] = v[b];
+        }
     }
 }
 
@@ -204,6 +215,18 @@ __device__ __forceinline__ void tri_inv32_warp(const float* __restrict__ Lkk, fl
     for (int r = 0; r < kBB; ++r) Di[r * kLD + lane] = col[r];
 }
 
+// Fire-and-forget fp32 adds at L2 (REDG.ADD.F32x4): the trailing updates of factor_big subtract their tile
+// from the L2 workspace without reading it first -- each element gets exactly one update per step, from one
+// thread, so the result is the plain fp32 subtraction's (denormals flush).  The read-modify-write form left
+// two loads in flight per thread and the kernel on the long scoreboard (ncu: 39 % of its stalls).  The
+// workspace is then always READ with ld.global.cg (L2): the L1 does not see the reductions.
+__device__ __forceinline__ void red_add4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+__device__ __forceinline__ void red_add1(float* p, float a) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(a) : "memory");
+}
+
 // C[rows r0.., cols 0..ncol) op= Pt^T Bk over l < 32 as 8x8 register tiles: Pt is [32][LDT]
 // (row l holds the 32-column factor block transposed), Bk is [32][ldb] (row l of the right-hand
 // block row).  A warp takes 8 row tiles x 4 column tiles: the B reads of a warp are one 128-byte
@@ -246,21 +269,16 @@ __device__ __forceinline__ void tile_update(const float* __restrict__ Pt, int LD
                 float* cr = C + size_t(ri) * ldc + Cc * 8;
 #pragma unroll
                 for (int jx = 0; jx < 8; ++jx)
-                    if (jx <= i) cr[jx] -= acc[i][jx];
+                    if (jx <= i) red_add1(cr + jx, -acc[i][jx]);
                 continue;
             }
-            float4 v0, v1;
             if (init) {
-                v0 = make_float4(-acc[i][0], -acc[i][1], -acc[i][2], -acc[i][3]);
-                v1 = make_float4(-acc[i][4], -acc[i][5], -acc[i][6], -acc[i][7]);
+                crow[0] = make_float4(-acc[i][0], -acc[i][1], -acc[i][2], -acc[i][3]);
+                crow[1] = make_float4(-acc[i][4], -acc[i][5], -acc[i][6], -acc[i][7]);
             } else {
-                v0 = crow[0];
-                v1 = crow[1];
-                v0.x -= acc[i][0], v0.y -= acc[i][1], v0.z -= acc[i][2], v0.w -= acc[i][3];
-                v1.x -= acc[i][4], v1.y -= acc[i][5], v1.z -= acc[i][6], v1.w -= acc[i][7];
+                red_add4(reinterpret_cast<float*>(crow), -acc[i][0], -acc[i][1], -acc[i][2], -acc[i][3]);
+                red_add4(reinterpret_cast<float*>(crow + 1), -acc[i][4], -acc[i][5], -acc[i][6], -acc[i][7]);
             }
-            crow[0] = v0;
-            crow[1] = v1;
         }
     }
 }
@@ -271,10 +289,23 @@ __device__ __forceinline__ void tile_update(const float* __restrict__ Pt, int LD
 __device__ __forceinline__ void load_panel_t(float* __restrict__ Pt, int LDT, const float* __restrict__ M, int ldm,
                                              int r0, int k0, int nr, int tid, int nt) {
     const int nr8 = (nr + 7) & ~7;
-    for (int idx = tid; idx < nr8 * kBB; idx += nt) {
-        const int q = idx >> 5, ln = idx & 31;
-        const int c = (q & 3) * 8 + (ln & 7), rr = (q >> 2) * 4 + (ln >> 3);
-        Pt[c * LDT + rr] = rr < nr ? M[size_t(r0 + rr) * ldm + k0 + c] : 0.f;
+    constexpr int kLB = 4;  // loads per thread in flight before the shared stores
+    for (int i0 = tid; i0 < nr8 * kBB; i0 += kLB * nt) {
+        float v[kLB];
+#pragma unroll
+        for (int b = 0; b < kLB; ++b) {
+            const int idx = i0 + b * nt;
+            const int q = idx >> 5, ln = idx & 31;
+            const int c = (q & 3) * 8 + (ln & 7), rr = (q >> 2) * 4 + (ln >> 3);
+            v[b] = (idx < nr8 * kBB && rr < nr) ? __ldcg(M + size_t(r0 + rr) * ldm + k0 + c) : 0.f;
+        }
+#pragma unroll
+        for (int b = 0; b < kLB; ++b) {
+            const int idx = i0 + b * nt;
+            const int q = idx >> 5, ln = idx & 31;
+            const int c = (q & 3) * 8 + (ln & 7), rr = (q >> 2) * 4 + (ln >> 3);
+            if (idx < nr8 * kBB) Pt[c * LDT + rr] = v[b];
+        }
     }
 }
 
@@ -335,7 +366,7 @@ __global__ void __launch_bounds__(NT) factor_big_kernel(Geometry g, const double
             const int kb = min(kBB, D - k0);
             for (int idx = tid; idx < kBB * kBB; idx += nt) {
                 const int r = idx >> 5, c = idx & 31;
-                Lkk[r * kLD + c] = r < kb ? (c <= r ? A[size_t(k0 + r) * Dp + k0 + c] : 0.f) : (r == c ? 1.f : 0.f);
+                Lkk[r * kLD + c] = r < kb ? (c <= r ? __ldcg(A + size_t(k0 + r) * Dp + k0 + c) : 0.f) : (r == c ? 1.f : 0.f);
             }
             if (tid == 0) s_fail = -1;
             __syncthreads();
@@ -394,7 +425,7 @@ __global__ void __launch_bounds__(NT) factor_big_kernel(Geometry g, const double
                 float av[kBB], x[kBB];
 #pragma unroll
                 for (int q = 0; q < kBB / 4; ++q) {
-                    const float4 v = arow[q];
+                    const float4 v = __ldcg(arow + q);
                     av[4 * q] = v.x, av[4 * q + 1] = v.y, av[4 * q + 2] = v.z, av[4 * q + 3] = v.w;
                 }
 #pragma unroll
@@ -433,10 +464,10 @@ __global__ void __launch_bounds__(NT) factor_big_kernel(Geometry g, const double
         __syncthreads();
         for (int idx = tid; idx < kBB * kBB; idx += nt) {
             const int r = idx >> 5, c = idx & 31;
-            Di[r * kLD + c] = (r < kb && c < kb) ? X[size_t(k0 + r) * Dp + k0 + c] : 0.f;
+            Di[r * kLD + c] = (r < kb && c < kb) ? __ldcg(X + size_t(k0 + r) * Dp + k0 + c) : 0.f;
         }
         for (int r = warp; r < kBB; r += nw)
-            for (int j = lane; j < k0; j += 32) Pt[r * LDT + j] = r < kb ? X[size_t(k0 + r) * Dp + j] : 0.f;
+            for (int j = lane; j < k0; j += 32) Pt[r * LDT + j] = r < kb ? __ldcg(X + size_t(k0 + r) * Dp + j) : 0.f;
         __syncthreads();
         float* xk = xk_smem ? Xk : X + size_t(k0) * Dp;
         const int ldx = xk_smem ? LDT : Dp;
@@ -471,7 +502,7 @@ __global__ void __launch_bounds__(NT) factor_big_kernel(Geometry g, const double
         }
     }
     __syncthreads();
-    write_wblocks(whiten, line, g, [&](int i, int j) { return X[size_t(i) * Dp + j]; });
+    write_wblocks(whiten, line, g, [&](int i, int j) { return __ldcg(X + size_t(i) * Dp + j); });
     if (tid == 0) status[line] = -1;
 }
 
