@@ -37,6 +37,18 @@ template <typename Get>
 __device__ __forceinline__ void write_wblocks(float* __restrict__ whiten, int line, const Geometry& g, Get get) {
     const int nblk = g.nb * (g.nb + 1) / 2;
     float* Wp = whiten + size_t(line) * nblk * 64;
+    if (nblk * 64 < 8 * int(blockDim.x)) {  // small matrices: one value per thread and pass
+        for (int idx = threadIdx.x; idx < nblk * 64; idx += blockDim.x) {
+            const int bq = idx >> 6, e = idx & 63, c = e >> 3, r = e & 7;
+            int I = int((sqrtf(8.f * bq + 1.f) - 1.f) * 0.5f);
+            while (I * (I + 1) / 2 > bq) --I;
+            while ((I + 1) * (I + 2) / 2 <= bq) ++I;
+            const int J = bq - I * (I + 1) / 2;
+            const int i = I * kBlk + r, j = J * kBlk + c;
+            Wp[idx] = (i < g.D && j <= i) ? get(i, j) : 0.f;
+        }
+        return;
+    }
     constexpr int kLB = 4;  // values per thread fetched before the stores (get() may read an L2 workspace)
     for (int i0 = threadIdx.x; i0 < nblk * 64; i0 += kLB * blockDim.x) {
         float v[kLB];
