@@ -47,7 +47,6 @@ __device__ __forceinline__ void slab_block(const Geometry& g, int s, int t, int&
 __device__ void score_slabs(const Geometry& g, const ScoreLaunch& sc, const float* vt, float* red, const float* Wl,
                             int s, int q) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int tid = threadIdx.x;
     const int nsteps = g.nb + 1;
     float* ring = reinterpret_cast<float*>(smem + sc.slab_off);  // [kSlabDepth][npairs][64]
     const bool active = s < sc.npairs;

@@ -515,7 +515,7 @@ struct SrpEnt {
 
 template <int DM, bool EX>
 __global__ void __launch_bounds__(kSrpWlWarps * 32, 2) stats_small_srp_wl_kernel(SmallArgs a, int n_lines) {
-    extern __shared__ __align__(128) unsigned char smem[];
+    extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(8) uint64_t full[kSrpWlWarps][2];
     constexpr int DT = DM * (DM + 1) / 2;
     const Geometry& g = a.g;

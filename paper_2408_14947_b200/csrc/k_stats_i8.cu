@@ -812,7 +812,6 @@ __global__ void __launch_bounds__(kThreads + 64, 1) stats_i8_op_kernel(StatsI8Ar
 // Warps: 0-7 quantise + epilogue, 8-11 range, 12 pass-1 producer, 13 pass-2 producer, 14 MMA issuer.
 // ---------------------------------------------------------------------------
 constexpr int kWsThreads = 480;
-constexpr int kWsRing1 = 2;  // pass-1 stages (the range pass consumes fast); the rest go to pass 2
 
 __device__ __forceinline__ void bar_range() { asm volatile("bar.sync 2, 128;" ::); }
 
