@@ -665,13 +665,17 @@ __device__ __forceinline__ int diag_factor8(float (&row)[kBlk], unsigned gmask, 
                                             float* dit, const float* dg) {
     int f = -1;
     float rd[kBlk];
+    // the block's conditioning bounds up front (a shared-memory load behind each column's dit store would sit
+    // on the pivot chain)
+    float dgr[kBlk];
+    ld8(dg + k0, dgr);
     // the columns of L go through dit (free until Di^T is written at the end): one 4-byte store per
     // lane and two 16-byte broadcast loads per column instead of a shuffle per entry; the pivot chain
     // itself stays in registers (lane j + 1 updates its own next pivot)
 #pragma unroll
     for (int j = 0; j < kBlk; ++j) {
         float d = __shfl_sync(gmask, row[j], j, kBlk);
-        if (!(d > 0.f) || d * kCondTau < dg[k0 + j]) {
+        if (!(d > 0.f) || d * kCondTau < dgr[j]) {
             if (f < 0) f = k0 + j;
             d = 1.f;
         }
