@@ -1011,6 +1011,52 @@ __global__ void __launch_bounds__(NT, MB) factor_blk_kernel(Geometry g, const do
 }
 
 // ---------------------------------------------------------------------------
+// D <= 8 (the reference default d = 5): the whole matrix is ONE 8x8 block, so diag_factor8 is the whole
+// factorisation.  factor_blk spends a 128-thread CTA, two CTA barriers and a block-grid walk per line on it
+// (configs[3] d = 5: 0.029 ms per 8192 lines, 0.009 ms of a 0.033-ms lag-0 line); here sixteen lines share a
+// CTA, eight lanes each, no CTA barrier.  Same arithmetic in the same order as factor_blk (bit-identical W).
+// ---------------------------------------------------------------------------
+constexpr int kTinyLines = 16;
+__global__ void __launch_bounds__(kTinyLines * 8) factor_tiny_kernel(Geometry g, double eps0, float* __restrict__ whiten,
+                                                                    int* __restrict__ status, int* __restrict__ fixlist,
+                                                                    const float* __restrict__ kblk, int n_lines) {
+    __shared__ __align__(16) float blk_s[kTinyLines][64], dit_s[kTinyLines][64], dg_s[kTinyLines][kBlk];
+    const int tid = threadIdx.x, grp = tid >> 3, gl = tid & 7, lane = tid & 31;
+    const unsigned gmask = 0xffu << (lane & 24);
+    const int line = blockIdx.x * kTinyLines + grp;
+    if (line >= n_lines) return;  // (whole 8-lane groups leave together; only group-wide syncs below)
+    const int D = g.D;
+    float row[kBlk];
+    ld8r(kblk + size_t(line) * 64, gl, row);  // the scan's fp32 block image (swizzled rows), row gl
+    const float fe = float(eps0);
+    float dgv = 1.f;
+#pragma unroll
+    for (int c = 0; c < kBlk; ++c) {
+        if (gl >= D) row[c] = (c == gl) ? 1.f : 0.f;  // padding dims: identity
+        else if (c > gl) row[c] = 0.f;
+        else if (c == gl) {
+            row[c] += fe;
+            dgv = row[c];
+        }
+    }
+    dg_s[grp][gl] = dgv;
+    __syncwarp(gmask);
+    const int f = diag_factor8(row, gmask, gl, 0, blk_s[grp], dit_s[grp], dg_s[grp]);
+    if (f >= 0) {  // the fp64 rescue (k_fixup.cu) redoes this line, escalation included
+        if (gl == 0) list_for_fixup(fixlist, status, line);
+        return;
+    }
+    __syncwarp(gmask);
+    // dit holds Di^T in plain rows: dit[c * 8 + r] = Di[r][c], the W block's own column-major layout
+    float w[kBlk];
+    ld8(dit_s[grp] + gl * kBlk, w);
+#pragma unroll
+    for (int r = 0; r < kBlk; ++r) w[r] = (r < D && gl <= r) ? w[r] : 0.f;
+    st8(whiten + size_t(line) * 64 + gl * kBlk, w);
+    if (gl == 0) status[line] = -1;
+}
+
+// ---------------------------------------------------------------------------
 // factor_cl (fp32, default for D > 233: configs[4]'s 448 bands): factor_blk's merged Cholesky +
 // inverse sweep over a THREAD-BLOCK CLUSTER of CL CTAs (one SM each), the packed lower 8x8 blocks
 // distributed block-row-cyclically (CTA c owns block rows I = c mod CL) so the whole factor lives in
@@ -1362,6 +1408,11 @@ void launch_factor(const Geometry& g, const double* prior, int n_lines_total, do
                    long long line_off, int precision, cudaStream_t st, int* fixlist, const double* stats,
                    const float* vmax, const float* kblk, int blk_threads) {
     const size_t sm = factor_smem(g, precision);
+    if (precision == 32 && g.nb == 1 && kblk && !vmax) {
+        factor_tiny_kernel<<<(n_lines_total + kTinyLines - 1) / kTinyLines, kTinyLines * 8, 0, st>>>(
+            g, eps0, whiten, status, fixlist, kblk, n_lines_total);
+        return;
+    }
     if (precision == 32) {
         ensure_smem(factor_blk_kernel<64, 7>, sm);
         ensure_smem(factor_blk_kernel<128, FACTOR_MB128>, sm);
