@@ -117,7 +117,7 @@ class StubEngine:
         return (self.t[b] - self.t[a]) * 1e3
 
 
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02i_ncu_full_c3.txt")  # one group of 4096 lines per launch (T = 64)
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02j_ncu_full_c3.txt")  # one group of 4096 lines per launch (T = 64)
 NCU_NAMES = {"stats": ("stats_i8_ws_kernel", "stats_i8_kernel", "stats_kernel", "stats_small"),
              "score": ("score_i8_kernel", "score_kernel"), "factor": ("factor_blk_kernel",),
              "scan": ("scan_tile_kernel", "scan_kernel"), "normalize": ("normalize_kernel",)}
