@@ -168,7 +168,7 @@ int erx_set_state(erx_engine* e, uint32_t stream, const double* mu, const double
 #define ERX_OPT_ASYNC_HOST 4
 /* ERX_OPT_FACTOR_THREADS: threads per line of the blocked fp32 shared-memory
  * factor (precision 32).  0 (default) picks 128 when every SM holds >= 6 lines
- * of a launch, else 256; 64, 128 or 256 force that CTA size (same results to
+ * of a launch, else 256; 64, 128, 256 or 512 force that CTA size (same results to
  * rounding; a tuning and test hook). */
 #define ERX_OPT_FACTOR_THREADS 5
 /* ERX_OPT_GRAPHS: 1 (default) erx_run_device captures a window's launches once
